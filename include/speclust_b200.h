@@ -1,0 +1,199 @@
+/*
+ * speclust_b200 — C ABI of the B200-native spectral-clustering engine.
+ *
+ * Every entry point takes plain pointers and sizes.  Pointers marked (dev) are
+ * CUDA device pointers (any allocator; the Python host uses torch tensors);
+ * pointers marked (host) are host memory.  All device work is enqueued on the
+ * caller's stream `stream` (a cudaStream_t passed as void*; NULL = legacy
+ * default stream).  Functions return an int status (SC_OK or one negative code
+ * per error class of the reference's errors.py); sc_last_error() returns the
+ * thread-local message of the last failure.
+ *
+ * The entry points replace the reference's Python operators on the hot path
+ * (reference = /root/reference/pkg/src/speclust; see INTEGRATION.md for the
+ * ctypes binding the host package uses):
+ *
+ *   sc_spmv_f64            sparse.py:195-207        spmv(a, x)
+ *   sc_degrees_f64         laplacian.py:27-31       degrees(w)
+ *   sc_find_nonpositive    laplacian.py:44-52,67-72 handle_isolated / _check_positive
+ *   sc_sym_scale_f64       laplacian.py:84-91       sym_scale(w, d)
+ *   sc_csr_is_symmetric    sparse.py:210-222        is_symmetric(a)
+ *   sc_knn_graph_f64       graph.py:185-237 +       build_edges_knn + build_similarity
+ *                          sparse.py:182-187        + coo_to_csr   (exp_decay measure)
+ *   sc_lanczos_*           eigen.py:86-266          RciSession / rci_new / rci_advance / rci_extract
+ *   sc_eigensolve_csr      eigen.py:269-302         eigensolve(a, cfg) (device-resident loop)
+ *   sc_symmetry_probe      eigen.py:279-288         _check_symmetric
+ *   sc_recover_embedding   laplacian.py:94-106 +    recover_row_eigvecs (+ normalize_rows,
+ *                          pipeline.py:242-245      pipeline stage "kmeans" prologue)
+ *   sc_pairwise_sq_dist    kmeans.py:84-98          pairwise_sq_dist(v, c)
+ *   sc_kmeanspp_*          kmeans.py:107-136        kmeanspp_init (host supplies the PCG64 draws)
+ *   sc_lloyd               kmeans.py:159-196        lloyd(v, init_c, cfg)
+ *   sc_ncut                metrics.py:34-67         ncut(w, labels)
+ */
+#ifndef SPECLUST_B200_H
+#define SPECLUST_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes: one per errors.py class on the hot path --------------- */
+enum {
+    SC_OK = 0,
+    SC_ERR_VALUE = -1,           /* ValueError / BadConfig (usage errors)        */
+    SC_ERR_DIMENSION = -2,       /* errors.DimensionMismatch                     */
+    SC_ERR_FORMAT = -3,          /* errors.InvalidFormat                         */
+    SC_ERR_NOT_SQUARE = -4,      /* errors.NotSquare                             */
+    SC_ERR_NOT_SYMMETRIC = -5,   /* errors.NotSymmetric                          */
+    SC_ERR_ISOLATED = -6,        /* errors.IsolatedNode                          */
+    SC_ERR_ZERO_DEGREE = -7,     /* errors.ZeroDegree                            */
+    SC_ERR_BREAKDOWN = -8,       /* errors.Breakdown                             */
+    SC_ERR_MAX_RESTARTS = -9,    /* errors.MaxRestartsExceeded (payload: stats)  */
+    SC_ERR_NOT_CONVERGED = -10,  /* errors.NotConverged                          */
+    SC_ERR_STATE = -11,          /* errors.SpeclustError (wrong session state)   */
+    SC_ERR_CUDA = -20,           /* CUDA runtime failure                         */
+    SC_ERR_NO_MEMORY = -21,      /* device allocation failed                     */
+    SC_ERR_INTERNAL = -22        /* numerical kernel failed (e.g. QL no convergence) */
+};
+
+typedef void* sc_stream_t;                 /* cudaStream_t */
+typedef struct sc_lanczos sc_lanczos_t;    /* opaque RCI session (library-owned) */
+
+const char* sc_last_error(void);
+int sc_version(void);
+/* number of kernel launches issued by this library since the last reset */
+int64_t sc_launch_count(void);
+void sc_launch_count_reset(void);
+
+/* ---- kernel timing (CUDA events on the launching stream) ------------------ */
+/* When enabled, launches of the named kernel classes ("spmv", "knn_tile",
+ * "reorth", "ritz", "symeig", "kmeans_assign", "kmeans_update", ...) are
+ * bracketed by events; sc_profile_query syncs and reports the accumulated
+ * device milliseconds, launch count and algorithmic bytes/flops recorded. */
+void sc_profile_enable(int on);
+void sc_profile_reset(void);
+int sc_profile_query(const char* name, double* ms, int64_t* launches, double* work);
+
+/* ---- sparse (CSR: row_ptr int64[n+1], col int32[nnz], vals f64[nnz]) ----- */
+/* y = A x.  deterministic=1: each row summed sequentially in column order
+ * (bit-identical to sparse.py:205-207); 0: vectorised sub-warp reduction. */
+int sc_spmv_f64(int64_t n_rows, int64_t n_cols, const int64_t* row_ptr, const int32_t* col,
+                const double* vals, const double* x, double* y, int deterministic,
+                sc_stream_t stream);
+/* d = W 1, rows summed sequentially (laplacian.py:27-31). */
+int sc_degrees_f64(int64_t n, const int64_t* row_ptr, const double* vals, double* d,
+                   sc_stream_t stream);
+/* mode 0: entries == 0.0 (isolated nodes); mode 1: entries <= 0.0.
+ * count_out/first_out are HOST pointers; idx_out (dev, optional, capacity
+ * max_idx) receives the first max_idx matching indices in ascending order. */
+int sc_find_nonpositive(int64_t n, const double* d, int mode, int64_t* count_out,
+                        int64_t* idx_out, int64_t max_idx, sc_stream_t stream);
+/* out = vals / sqrt(d[row] * d[col]) (laplacian.py:84-91). */
+int sc_sym_scale_f64(int64_t n, const int64_t* row_ptr, const int32_t* col,
+                     const double* vals, const double* d, double* out, sc_stream_t stream);
+/* *result (host) = 1 iff A == A^T bit-for-bit (sparse.py:210-222). */
+int sc_csr_is_symmetric(int64_t n, int64_t nnz, const int64_t* row_ptr, const int32_t* col,
+                        const double* vals, int* result, sc_stream_t stream);
+
+/* ---- stage 1: kNN + exp_decay similarity graph straight into CSR ---------- */
+/* x: (dev) n x d row-major f64.  Outputs (dev): row_ptr[n+1], col/vals with
+ * capacity 2*n*knn; *nnz_out (host) receives the true nnz.  Semantics:
+ * graph.py:149-157 ranking (similarity desc, index asc), union symmetrisation
+ * (graph.py:203-204), one exp(-d2/(2 sigma^2)) per unordered pair
+ * (graph.py:136-141).  stats_out (host, optional, 8 int64): candidates per row
+ * budget, rows that needed the exact fallback, max row degree, ...         */
+int sc_knn_graph_f64(int64_t n, int64_t d, const double* x, int64_t knn, double two_sigma_sq,
+                     int64_t* row_ptr, int32_t* col, double* vals, int64_t* nnz_out,
+                     int64_t* stats_out, sc_stream_t stream);
+/* out[p] = exp(-|x_a - x_b|^2 / two_sigma_sq) for pairs (a, b) = pairs[2p..2p+1]
+ * (graph.py:136-141, used by build_similarity on a given edge list). */
+int sc_pair_weights(int64_t n, int64_t d, const double* x, int64_t m, const int64_t* pairs,
+                    double two_sigma_sq, double* out, sc_stream_t stream);
+
+/* ---- stage 2: thick-restart Lanczos ----------------------------------------- */
+typedef struct {
+    int64_t restarts;        /* RciSession.restart_count  */
+    int64_t breakdowns;      /* RciSession.breakdown_count */
+    int64_t matvecs;         /* operator applications       */
+    int64_t n_history;       /* valid entries in history    */
+    double history[512];     /* residual_history (first 512 sweeps) */
+} sc_lanczos_stats;
+
+/* RCI session (eigen.py:86-266).  m <= 0 selects default_subspace_dim. */
+int sc_lanczos_create(int64_t n, int64_t k, int64_t m, double tol, int64_t max_restarts,
+                      uint64_t seed, sc_stream_t stream, sc_lanczos_t** out);
+void sc_lanczos_destroy(sc_lanczos_t* s);
+/* state: 0 need_matvec, 1 converged, 2 failed */
+int sc_lanczos_state(const sc_lanczos_t* s);
+/* (dev) pointer to the current in_slot vector (length n, read-only for callers) */
+const double* sc_lanczos_in_slot(const sc_lanczos_t* s);
+/* (dev) pointer to the out_slot buffer the caller fills with A * in_slot */
+double* sc_lanczos_out_slot(sc_lanczos_t* s);
+/* one Lanczos step consuming out_slot; returns SC_ERR_MAX_RESTARTS /
+ * SC_ERR_BREAKDOWN on failure (session then in state 2). */
+int sc_lanczos_advance(sc_lanczos_t* s);
+int sc_lanczos_get_stats(const sc_lanczos_t* s, sc_lanczos_stats* st);
+/* values (host, k) and residual estimates (host, k) of the last sweep; valid
+ * after convergence or after SC_ERR_MAX_RESTARTS. */
+int sc_lanczos_ritz(const sc_lanczos_t* s, double* values, double* estimates);
+/* converged pairs: values (host, k) descending, vectors (dev) n x k row-major */
+int sc_lanczos_extract(sc_lanczos_t* s, double* values, double* vectors);
+
+/* Device-resident eigensolve of a symmetric CSR: symmetry probe excluded;
+ * vectors (dev) n x k row-major; values/residuals host arrays of length k. */
+int sc_eigensolve_csr(int64_t n, const int64_t* row_ptr, const int32_t* col,
+                      const double* vals, int64_t k, int64_t m, double tol,
+                      int64_t max_restarts, uint64_t seed, double* values, double* vectors,
+                      double* residuals, sc_lanczos_stats* stats, sc_stream_t stream);
+/* max over the three probes of eigen.py:279-288 of |x'Ay - y'Ax| / (|x| |y|)
+ * divided by max(1, max|a|) (host *ratio_out); probes are device Philox normals.
+ * The caller raises NotSymmetric when ratio > 1e-10. */
+int sc_symmetry_probe(int64_t n, const int64_t* row_ptr, const int32_t* col,
+                      const double* vals, uint64_t seed, double* ratio_out,
+                      sc_stream_t stream);
+
+/* ---- embedding ------------------------------------------------------------- */
+/* v = u / sqrt(d) rowwise, columns to unit norm, optionally rows to unit norm.
+ * u, out: (dev) n x k row-major (may alias). */
+int sc_recover_embedding(int64_t n, int64_t k, const double* u, const double* d,
+                         int normalize_rows, double* out, sc_stream_t stream);
+int sc_normalize_rows(int64_t n, int64_t k, const double* v, double* out, sc_stream_t stream);
+
+/* ---- stage 3: k-means --------------------------------------------------------- */
+int sc_pairwise_sq_dist(int64_t n, int64_t k, int64_t d, const double* v, const double* c,
+                        double* out, sc_stream_t stream);
+
+typedef struct sc_kmeanspp sc_kmeanspp_t;
+/* k-means++ (kmeans.py:107-136).  The host owns the numpy PCG64 stream:
+ * begin(first) picks chosen[0] = first; then per step the host calls
+ * sc_kmeanspp_candidates (host count of untaken rows with d2 > 0), draws
+ * u = rng.random() (or rng.integers(free) when the count is 0) and calls
+ * sc_kmeanspp_pick. */
+int sc_kmeanspp_create(int64_t n, int64_t d, const double* v, sc_stream_t stream,
+                       sc_kmeanspp_t** out);
+void sc_kmeanspp_destroy(sc_kmeanspp_t* s);
+int sc_kmeanspp_take(sc_kmeanspp_t* s, int64_t index);
+int sc_kmeanspp_candidates(sc_kmeanspp_t* s, int64_t* count, int64_t* n_free);
+/* mode 0: weighted draw with uniform u in [0,1); mode 1: the r-th untaken row */
+int sc_kmeanspp_pick(sc_kmeanspp_t* s, int mode, double u, int64_t r, int64_t* index);
+
+/* Lloyd iterations (kmeans.py:159-196).  v (dev) n x d row-major, c_init (dev)
+ * k x d; outputs labels (dev int64 n), centroids (dev k x d), sse_history
+ * (host, capacity max_iters+1), *iters_out (host). */
+int sc_lloyd(int64_t n, int64_t d, int64_t k, const double* v, const double* c_init,
+             int64_t max_iters, int64_t tol_changes, int64_t* labels, double* centroids,
+             double* sse_history, int64_t* iters_out, sc_stream_t stream);
+
+/* ---- metrics ---------------------------------------------------------------- */
+/* ncut over labels in [0, k) (metrics.py:59-67); *out host.  Returns
+ * SC_ERR_VALUE with *out = -1 when a part has zero volume. */
+int sc_ncut(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* vals,
+            const int64_t* labels, int64_t k, double* out, sc_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPECLUST_B200_H */

@@ -1,0 +1,182 @@
+"""ctypes binding of the C ABI declared in include/speclust_b200.h.
+
+The shared library ``libspeclust_b200.so`` is built in-tree by
+``__graft_entry__.build()``.  There is no CPU fallback: every compute entry
+point of the package goes through this module, and a missing library or a
+missing CUDA device raises ``NativeUnavailable`` at the first call.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+import numpy as np
+
+from . import errors
+
+_LIB_PATH = Path(__file__).resolve().parent / "libspeclust_b200.so"
+_lib = None
+
+i64, i32, f64, vp = C.c_int64, C.c_int, C.c_double, C.c_void_p
+P_i64 = C.POINTER(C.c_int64)
+P_f64 = C.POINTER(C.c_double)
+P_int = C.POINTER(C.c_int)
+
+
+class LanczosStats(C.Structure):
+    _fields_ = [
+        ("restarts", C.c_int64),
+        ("breakdowns", C.c_int64),
+        ("matvecs", C.c_int64),
+        ("n_history", C.c_int64),
+        ("history", C.c_double * 512),
+    ]
+
+
+# name -> (restype, argtypes); mirrors include/speclust_b200.h one-to-one
+SIGNATURES = {
+    "sc_last_error": (C.c_char_p, []),
+    "sc_version": (i32, []),
+    "sc_launch_count": (i64, []),
+    "sc_launch_count_reset": (None, []),
+    "sc_profile_enable": (None, [i32]),
+    "sc_profile_reset": (None, []),
+    "sc_profile_query": (i32, [C.c_char_p, P_f64, P_i64, P_f64]),
+    "sc_spmv_f64": (i32, [i64, i64, vp, vp, vp, vp, vp, i32, vp]),
+    "sc_degrees_f64": (i32, [i64, vp, vp, vp, vp]),
+    "sc_find_nonpositive": (i32, [i64, vp, i32, P_i64, vp, i64, vp]),
+    "sc_sym_scale_f64": (i32, [i64, vp, vp, vp, vp, vp, vp]),
+    "sc_csr_is_symmetric": (i32, [i64, i64, vp, vp, vp, P_int, vp]),
+    "sc_knn_graph_f64": (i32, [i64, i64, vp, i64, f64, vp, vp, vp, P_i64, P_i64, vp]),
+    "sc_pair_weights": (i32, [i64, i64, vp, i64, vp, f64, vp, vp]),
+    "sc_lanczos_create": (i32, [i64, i64, i64, f64, i64, C.c_uint64, vp, C.POINTER(vp)]),
+    "sc_lanczos_destroy": (None, [vp]),
+    "sc_lanczos_state": (i32, [vp]),
+    "sc_lanczos_in_slot": (vp, [vp]),
+    "sc_lanczos_out_slot": (vp, [vp]),
+    "sc_lanczos_advance": (i32, [vp]),
+    "sc_lanczos_get_stats": (i32, [vp, C.POINTER(LanczosStats)]),
+    "sc_lanczos_ritz": (i32, [vp, P_f64, P_f64]),
+    "sc_lanczos_extract": (i32, [vp, P_f64, vp]),
+    "sc_eigensolve_csr": (i32, [i64, vp, vp, vp, i64, i64, f64, i64, C.c_uint64, P_f64, vp, P_f64,
+                                C.POINTER(LanczosStats), vp]),
+    "sc_symmetry_probe": (i32, [i64, vp, vp, vp, C.c_uint64, P_f64, vp]),
+    "sc_recover_embedding": (i32, [i64, i64, vp, vp, i32, vp, vp]),
+    "sc_normalize_rows": (i32, [i64, i64, vp, vp, vp]),
+    "sc_pairwise_sq_dist": (i32, [i64, i64, i64, vp, vp, vp, vp]),
+    "sc_kmeanspp_create": (i32, [i64, i64, vp, vp, C.POINTER(vp)]),
+    "sc_kmeanspp_destroy": (None, [vp]),
+    "sc_kmeanspp_take": (i32, [vp, i64]),
+    "sc_kmeanspp_candidates": (i32, [vp, P_i64, P_i64]),
+    "sc_kmeanspp_pick": (i32, [vp, i32, f64, i64, P_i64]),
+    "sc_lloyd": (i32, [i64, i64, i64, vp, vp, i64, i64, vp, vp, P_f64, P_i64, vp]),
+    "sc_ncut": (i32, [i64, vp, vp, vp, vp, i64, P_f64, vp]),
+}
+
+# status code -> exception class (include/speclust_b200.h enum)
+_STATUS = {
+    -1: errors.BadConfig,
+    -2: errors.DimensionMismatch,
+    -3: errors.InvalidFormat,
+    -4: errors.NotSquare,
+    -5: errors.NotSymmetric,
+    -6: errors.IsolatedNode,
+    -7: errors.ZeroDegree,
+    -8: errors.Breakdown,
+    -9: errors.MaxRestartsExceeded,
+    -10: errors.NotConverged,
+    -11: errors.SpeclustError,
+    -20: errors.NativeError,
+    -21: errors.NativeError,
+    -22: errors.NativeError,
+}
+
+
+class NativeUnavailable(RuntimeError):
+    """The CUDA library or a CUDA device is missing; there is no CPU path."""
+
+
+def library_path() -> Path:
+    return _LIB_PATH
+
+
+def load(path: str | os.PathLike | None = None):
+    """Load (once) and return the ctypes handle with all signatures bound."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = Path(path) if path is not None else _LIB_PATH
+    if not p.exists():
+        raise NativeUnavailable(
+            f"{p} is missing: build it with `python __graft_entry__.py` (nvcc, sm_100a); "
+            "this package has no CPU fallback"
+        )
+    lib = C.CDLL(str(p))
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def last_error() -> str:
+    msg = load().sc_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(rc: int, **payload):
+    """Raise the errors.py class mapped from a status code."""
+    if rc == 0:
+        return
+    cls = _STATUS.get(rc, errors.NativeError)
+    msg = last_error()
+    if cls is errors.IsolatedNode:
+        raise cls(payload.get("indices", []))
+    if cls is errors.MaxRestartsExceeded:
+        raise cls(msg, values=payload.get("values"), residuals=payload.get("residuals"))
+    raise cls(msg)
+
+
+# ---------------------------------------------------------------------------
+# torch handoff (device memory + streams only)
+def torch_cuda():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise NativeUnavailable("no CUDA device visible; the speclust_b200 engine runs on B200 only")
+    return torch
+
+
+def stream_handle():
+    torch = torch_cuda()
+    return vp(torch.cuda.current_stream().cuda_stream)
+
+
+def ptr(t) -> vp:
+    return vp(t.data_ptr()) if t is not None else vp(0)
+
+
+def to_device(a, dtype):
+    """numpy / torch -> contiguous CUDA tensor of `dtype` (torch dtype)."""
+    torch = torch_cuda()
+    if isinstance(a, torch.Tensor):
+        return a.to(device="cuda", dtype=dtype).contiguous()
+    arr = np.ascontiguousarray(a)
+    return torch.from_numpy(arr).to(device="cuda", dtype=dtype, non_blocking=False).contiguous()
+
+
+def to_host(t, dtype=None) -> np.ndarray:
+    out = t.detach().cpu().numpy()
+    if dtype is not None:
+        out = out.astype(dtype, copy=False)
+    return np.ascontiguousarray(out)
+
+
+def frozen(a: np.ndarray) -> np.ndarray:
+    a = np.ascontiguousarray(a)
+    a.flags.writeable = False
+    return a

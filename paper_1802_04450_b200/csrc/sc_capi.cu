@@ -1,0 +1,111 @@
+// Error state, launch accounting and kernel timing for the C ABI.
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "sc_common.cuh"
+
+namespace sc {
+
+static thread_local std::string g_last_error;
+static int64_t g_launches = 0;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+    g_last_error = std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e);
+    return e == cudaErrorMemoryAllocation ? SC_ERR_NO_MEMORY : SC_ERR_CUDA;
+}
+void count_launch(int n) { g_launches += n; }
+
+// ---- profiling ---------------------------------------------------------------
+struct ProfSlot {
+    std::string name;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
+    double ms = 0.0;
+    int64_t launches = 0;
+    double work = 0.0;
+};
+static bool g_prof = false;
+static std::mutex g_prof_mu;
+static std::vector<ProfSlot> g_slots;
+
+static int slot_of(const char* name) {
+    for (size_t i = 0; i < g_slots.size(); ++i)
+        if (g_slots[i].name == name) return (int)i;
+    g_slots.push_back(ProfSlot{});
+    g_slots.back().name = name;
+    return (int)g_slots.size() - 1;
+}
+
+ProfScope::ProfScope(const char* name, cudaStream_t s, double work) {
+    if (!g_prof) return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    slot = slot_of(name);
+    stream = s;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, s);
+    g_slots[slot].pending.push_back({a, b});
+    g_slots[slot].launches += 1;
+    g_slots[slot].work += work;
+}
+ProfScope::~ProfScope() {
+    if (slot < 0) return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    cudaEventRecord(g_slots[slot].pending.back().second, stream);
+}
+
+static void drain(ProfSlot& s) {
+    for (auto& ev : s.pending) {
+        cudaEventSynchronize(ev.second);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev.first, ev.second);
+        s.ms += ms;
+        cudaEventDestroy(ev.first);
+        cudaEventDestroy(ev.second);
+    }
+    s.pending.clear();
+}
+
+}  // namespace sc
+
+using namespace sc;
+
+extern "C" {
+
+const char* sc_last_error(void) { return g_last_error.c_str(); }
+int sc_version(void) { return 100; }
+int64_t sc_launch_count(void) { return g_launches; }
+void sc_launch_count_reset(void) { g_launches = 0; }
+
+void sc_profile_enable(int on) { g_prof = on != 0; }
+void sc_profile_reset(void) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    for (auto& s : g_slots) drain(s);
+    g_slots.clear();
+}
+int sc_profile_query(const char* name, double* ms, int64_t* launches, double* work) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    for (auto& s : g_slots) {
+        if (s.name == name) {
+            drain(s);
+            if (ms) *ms = s.ms;
+            if (launches) *launches = s.launches;
+            if (work) *work = s.work;
+            return SC_OK;
+        }
+    }
+    if (ms) *ms = 0.0;
+    if (launches) *launches = 0;
+    if (work) *work = 0.0;
+    return SC_ERR_VALUE;
+}
+
+}  // extern "C"

@@ -1,0 +1,132 @@
+// Shared helpers for the speclust_b200 kernels (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/speclust_b200.h"
+
+namespace sc {
+
+constexpr int kNumSMs = 148;  // B200: 2 dies x 74 SMs
+
+// ---- error plumbing ---------------------------------------------------------
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+void count_launch(int n = 1);
+
+#define SC_CUDA(expr)                                          \
+    do {                                                       \
+        cudaError_t _e = (expr);                               \
+        if (_e != cudaSuccess) return ::sc::cuda_fail(_e, #expr); \
+    } while (0)
+
+// check the last launch; every wrapper calls this after its kernels
+#define SC_LAUNCHED(n)                                                    \
+    do {                                                                  \
+        ::sc::count_launch(n);                                            \
+        cudaError_t _e = cudaGetLastError();                              \
+        if (_e != cudaSuccess) return ::sc::cuda_fail(_e, "kernel launch"); \
+    } while (0)
+
+inline cudaStream_t as_stream(sc_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ---- kernel timing ----------------------------------------------------------
+// Scoped CUDA-event bracket around launches of a named kernel class; a no-op
+// unless sc_profile_enable(1).  `work` = algorithmic bytes or flops.
+struct ProfScope {
+    int slot = -1;
+    cudaStream_t stream = nullptr;
+    ProfScope(const char* name, cudaStream_t s, double work);
+    ~ProfScope();
+};
+
+// ---- device memory owned by the library (sessions) -------------------------
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    int alloc(size_t count) {
+        free();
+        n = count;
+        if (count == 0) return SC_OK;
+        cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+        if (e != cudaSuccess) {
+            p = nullptr;
+            n = 0;
+            (void)cudaGetLastError();
+            return fail(SC_ERR_NO_MEMORY, "cudaMalloc failed for " + std::to_string(count * sizeof(T)) + " bytes");
+        }
+        return SC_OK;
+    }
+    void free() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    ~DevBuf() { free(); }
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+};
+
+// ---- device helpers ---------------------------------------------------------
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ float warp_min(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ int64_t warp_sum_i64(int64_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ int64_t imax64(int64_t a, int64_t b) { return a > b ? a : b; }
+
+// Philox4x32-10 counter-based generator (device side), used for Lanczos start
+// vectors, fresh directions and probe vectors.  Deterministic in (seed, stream,
+// element index).
+struct Philox {
+    __device__ static uint4 round(uint4 c, uint2 k) {
+        const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+        uint32_t hi0 = __umulhi(M0, c.x), lo0 = M0 * c.x;
+        uint32_t hi1 = __umulhi(M1, c.z), lo1 = M1 * c.z;
+        return make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    }
+    __device__ static uint4 gen(uint4 c, uint2 k) {
+#pragma unroll
+        for (int i = 0; i < 10; ++i) {
+            c = round(c, k);
+            k.x += 0x9E3779B9u;
+            k.y += 0xBB67AE85u;
+        }
+        return c;
+    }
+};
+
+// standard normal for element `i` of stream `stream_id` under `seed`
+__device__ __forceinline__ double philox_normal(uint64_t seed, uint64_t stream_id, uint64_t i) {
+    uint4 c = make_uint4((uint32_t)i, (uint32_t)(i >> 32), (uint32_t)stream_id,
+                         (uint32_t)(stream_id >> 32));
+    uint2 k = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+    uint4 r = Philox::gen(c, k);
+    // two 53-bit uniforms in (0, 1]
+    uint64_t a = ((uint64_t)r.x << 21) ^ ((uint64_t)r.y >> 11);
+    uint64_t b = ((uint64_t)r.z << 21) ^ ((uint64_t)r.w >> 11);
+    double u1 = ((double)(a & ((1ull << 53) - 1)) + 1.0) * (1.0 / 9007199254740992.0);
+    double u2 = (double)(b & ((1ull << 53) - 1)) * (1.0 / 9007199254740992.0);
+    return sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+}
+
+}  // namespace sc

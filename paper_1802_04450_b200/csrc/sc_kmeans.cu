@@ -1,0 +1,760 @@
+// k-means: fp64 Gram-expansion distance tiles with fused argmin epilogue,
+// stable label bucketing + point-order centroid sums, farthest-point reseed,
+// k-means++ device steps, Lloyd driver, and the ncut metric.
+//
+// Reference semantics (kmeans.py:84-196, metrics.py:59-67):
+//   S = (|v|^2 + |c|^2) - 2 v.c, clamped at 0; argmin ties -> lowest index;
+//   centroid = (sum of members in point order) / count; empty clusters take
+//   the rows with the largest current cost (stable: ties -> lower index).
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "sc_common.cuh"
+#include "sc_sparse.cuh"
+
+namespace sc {
+
+__device__ __forceinline__ int64_t ceil_div_dev(int64_t d) { return (d + 31) / 32; }
+
+// ---------------------------------------------------------------------------
+// row squared norms as a sequential fma chain over the feature index: the
+// same chain the distance tile uses for v.c, so identical rows give an exact
+// zero distance (kmeans.py:92-97; test_kmeans.py:23-27).
+__global__ void rownorm_kernel(int64_t n, int64_t d, const double* __restrict__ v,
+                               double* __restrict__ out) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double* r = v + i * d;
+    double acc = 0.0;
+    for (int64_t l = 0; l < d; ++l) acc = fma(r[l], r[l], acc);
+    out[i] = acc;
+}
+
+constexpr int TP = 64, TQ = 64, KC = 16;
+
+// MODE 0: assignment (argmin epilogue); MODE 1: write the clamped n x k matrix.
+template <int MODE>
+__global__ void __launch_bounds__(256) dist_tile_kernel(
+    int64_t n, int64_t k, int64_t d, const double* __restrict__ v, const double* __restrict__ vn,
+    const double* __restrict__ c, const double* __restrict__ cn, double* __restrict__ out,
+    int64_t* __restrict__ labels, const int64_t* __restrict__ old_labels,
+    double* __restrict__ cost, unsigned long long* __restrict__ changes,
+    double* __restrict__ cost_partial) {
+    __shared__ double Vs[KC][TP + 1];
+    __shared__ double Cs[KC][TQ + 1];
+    const int tid = threadIdx.x;
+    const int tx = tid & 15, ty = tid >> 4;
+    const int64_t p0 = (int64_t)blockIdx.x * TP;
+
+    double best[4];
+    int64_t arg[4];
+    double vnr[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        best[i] = INFINITY;
+        arg[i] = 0;
+        int64_t p = p0 + ty + 16 * i;
+        vnr[i] = p < n ? vn[p] : 0.0;
+    }
+
+    for (int64_t q0 = 0; q0 < k; q0 += TQ) {
+        double acc[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+        for (int64_t l0 = 0; l0 < d; l0 += KC) {
+            __syncthreads();
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                int idx = tid + 256 * r;
+                int pp = idx >> 4, ll = idx & 15;
+                int64_t gp = p0 + pp, gl = l0 + ll;
+                Vs[ll][pp] = (gp < n && gl < d) ? v[gp * d + gl] : 0.0;
+                int64_t gq = q0 + pp;
+                Cs[ll][pp] = (gq < k && gl < d) ? c[gq * d + gl] : 0.0;
+            }
+            __syncthreads();
+            const int lmax = (int)imin64(KC, d - l0);
+            for (int l = 0; l < lmax; ++l) {
+                double a[4], b[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) a[i] = Vs[l][ty + 16 * i];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) b[j] = Cs[l][tx + 16 * j];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+            }
+        }
+        // epilogue for this centroid tile
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            int64_t q = q0 + tx + 16 * j;
+            if (q >= k) continue;
+            double cq = cn[q];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                double s = __dsub_rn(__dadd_rn(vnr[i], cq), __dmul_rn(2.0, acc[i][j]));
+                s = s > 0.0 ? s : 0.0;  // np.maximum(s, 0.0)
+                if (MODE == 1) {
+                    int64_t p = p0 + ty + 16 * i;
+                    if (p < n) out[p * k + q] = s;
+                } else if (s < best[i]) {
+                    best[i] = s;
+                    arg[i] = q;
+                }
+            }
+        }
+    }
+    if (MODE == 1) return;
+    // reduce (best, arg) over the 16 lanes sharing a point: lexicographic min
+    double blk_cost = 0.0;
+    int nchg = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        double b = best[i];
+        int64_t a = arg[i];
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) {
+            double ob = __shfl_xor_sync(0xffffffffu, b, o);
+            int64_t oa = __shfl_xor_sync(0xffffffffu, a, o);
+            if (ob < b || (ob == b && oa < a)) {
+                b = ob;
+                a = oa;
+            }
+        }
+        int64_t p = p0 + ty + 16 * i;
+        if (tx == 0 && p < n) {
+            labels[p] = a;
+            cost[p] = b;
+            if (old_labels) nchg += (old_labels[p] != a);
+        }
+    }
+    // per-block cost sum in fixed order (deterministic)
+    __shared__ double red[TP];
+    __shared__ int chg[TP];
+    if (tx == 0) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            int64_t p = p0 + ty + 16 * i;
+            red[ty + 16 * i] = p < n ? cost[p] : 0.0;
+        }
+        chg[ty] = nchg;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        for (int i = 0; i < TP; ++i) blk_cost += red[i];
+        int tot = 0;
+        for (int i = 0; i < 16; ++i) tot += chg[i];
+        cost_partial[blockIdx.x] = blk_cost;
+        if (tot) atomicAdd(changes, (unsigned long long)tot);
+    }
+}
+
+// sum of a partial array in fixed order by one block (deterministic)
+__global__ void sum_partials_kernel(int64_t m, const double* __restrict__ part, double* __restrict__ out) {
+    __shared__ double red[1024];
+    double acc = 0.0;
+    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) acc += part[i];
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if ((int)threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = red[0];
+}
+
+// ---------------------------------------------------------------------------
+// Stable bucketing by label.
+constexpr int BK_ITEMS = 2048;  // items per bucketing block (one warp per block)
+
+__global__ void bucket_count_kernel(int64_t n, int64_t k, const int64_t* __restrict__ labels,
+                                    int32_t* __restrict__ blkcount) {
+    int64_t b = blockIdx.x;
+    int32_t* row = blkcount + b * k;
+    for (int64_t c = threadIdx.x; c < k; c += blockDim.x) row[c] = 0;
+    __syncthreads();
+    int64_t lo = b * BK_ITEMS, hi = imin64(n, lo + BK_ITEMS);
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) atomicAdd(row + labels[i], 1);
+}
+
+// per label: exclusive offsets over blocks in block order; start[] over labels
+__global__ void bucket_offsets_kernel(int64_t nblk, int64_t k, const int32_t* __restrict__ blkcount,
+                                      int64_t* __restrict__ blkoff, int64_t* __restrict__ total) {
+    int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= k) return;
+    int64_t run = 0;
+    for (int64_t b = 0; b < nblk; ++b) {
+        blkoff[b * k + c] = run;
+        run += blkcount[b * k + c];
+    }
+    total[c] = run;
+}
+
+__global__ void exclusive_scan_small_kernel(int64_t k, int64_t* __restrict__ start) {
+    // start[0..k) holds totals on entry; converts in place to offsets, start[k] = sum
+    if (threadIdx.x != 0) return;
+    int64_t run = 0;
+    for (int64_t c = 0; c < k; ++c) {
+        int64_t t = start[c];
+        start[c] = run;
+        run += t;
+    }
+    start[k] = run;
+}
+
+__global__ void bucket_scatter_kernel(int64_t n, int64_t k, const int64_t* __restrict__ labels,
+                                      const int64_t* __restrict__ blkoff,
+                                      const int64_t* __restrict__ start,
+                                      int32_t* __restrict__ members) {
+    extern __shared__ int32_t run[];  // k counters
+    int64_t b = blockIdx.x;
+    for (int64_t c = threadIdx.x; c < k; c += 32) run[c] = 0;
+    __syncwarp();
+    int lane = threadIdx.x;
+    int64_t lo = b * BK_ITEMS, hi = imin64(n, lo + BK_ITEMS);
+    const int64_t* off = blkoff + b * k;
+    for (int64_t base = lo; base < hi; base += 32) {
+        int64_t i = base + lane;
+        bool valid = i < hi;
+        int64_t lab = valid ? labels[i] : -1 - lane;
+        unsigned peers = __match_any_sync(0xffffffffu, lab);
+        int rank = __popc(peers & ((1u << lane) - 1u));
+        int32_t before = valid ? run[lab] : 0;
+        if (valid) members[start[lab] + off[lab] + before + rank] = (int32_t)i;
+        __syncwarp();
+        if (valid && rank == 0) run[lab] = before + __popc(peers);
+        __syncwarp();
+    }
+}
+
+int Bucketer::init(int64_t n_, int64_t k_) {
+    n = n_;
+    k = k_;
+    nblk = ceil_div(n, BK_ITEMS);
+    if (int rc = blkcount.alloc((size_t)std::max<int64_t>(1, nblk * k))) return rc;
+    if (int rc = blkoff.alloc((size_t)std::max<int64_t>(1, nblk * k))) return rc;
+    if (int rc = start.alloc((size_t)k + 1)) return rc;
+    if (int rc = members.alloc((size_t)std::max<int64_t>(1, n))) return rc;
+    return SC_OK;
+}
+
+int Bucketer::run(const int64_t* labels, cudaStream_t st) {
+    if (n == 0) {
+        SC_CUDA(cudaMemsetAsync(start.p, 0, sizeof(int64_t) * (k + 1), st));
+        return SC_OK;
+    }
+    bucket_count_kernel<<<(unsigned)nblk, 256, 0, st>>>(n, k, labels, blkcount.p);
+    bucket_offsets_kernel<<<(unsigned)ceil_div(k, 128), 128, 0, st>>>(nblk, k, blkcount.p, blkoff.p, start.p);
+    exclusive_scan_small_kernel<<<1, 32, 0, st>>>(k, start.p);
+    size_t smem = sizeof(int32_t) * (size_t)k;
+    if (smem > 48 * 1024) {
+        cudaFuncSetAttribute(bucket_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    }
+    bucket_scatter_kernel<<<(unsigned)nblk, 32, smem, st>>>(n, k, labels, blkoff.p, start.p, members.p);
+    SC_LAUNCHED(4);
+    return SC_OK;
+}
+
+// centroid = point-order member sum / count (kmeans.py:144-148; np.add.at is a
+// sequential scatter-add in point order, reproduced exactly per (cluster, dim)).
+__global__ void centroid_mean_kernel(int64_t k, int64_t d, const double* __restrict__ v,
+                                     const int64_t* __restrict__ start,
+                                     const int32_t* __restrict__ members,
+                                     double* __restrict__ cent, int* __restrict__ empty_flag) {
+    int64_t dchunks = ceil_div_dev(d);
+    int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (w >= k * dchunks) return;
+    int64_t cl = w / dchunks;
+    int64_t dim = (w % dchunks) * 32 + lane;
+    int64_t b = start[cl], e = start[cl + 1];
+    if (e == b) {
+        if (lane == 0 && (w % dchunks) == 0) empty_flag[cl] = 1;
+        if (dim < d) cent[cl * d + dim] = 0.0;
+        return;
+    }
+    if (dim >= d) return;
+    double acc = 0.0;
+    int64_t m = b;
+    for (; m + 4 <= e; m += 4) {
+        int32_t i0 = members[m], i1 = members[m + 1], i2 = members[m + 2], i3 = members[m + 3];
+        double x0 = v[(int64_t)i0 * d + dim], x1 = v[(int64_t)i1 * d + dim];
+        double x2 = v[(int64_t)i2 * d + dim], x3 = v[(int64_t)i3 * d + dim];
+        acc = __dadd_rn(acc, x0);
+        acc = __dadd_rn(acc, x1);
+        acc = __dadd_rn(acc, x2);
+        acc = __dadd_rn(acc, x3);
+    }
+    for (; m < e; ++m) acc = __dadd_rn(acc, v[(int64_t)members[m] * d + dim]);
+    cent[cl * d + dim] = __ddiv_rn(acc, (double)(e - b));
+}
+
+// argmax of cost over unmarked points, ties -> lowest index (one reseed slot)
+__global__ void argmax_partial_kernel(int64_t n, const double* __restrict__ cost,
+                                      const uint8_t* __restrict__ used, double* __restrict__ pv,
+                                      int64_t* __restrict__ pi) {
+    __shared__ double sv[256];
+    __shared__ int64_t si[256];
+    double bv = -INFINITY;
+    int64_t bi = INT64_MAX;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (used[i]) continue;
+        double c = cost[i];
+        if (c > bv || (c == bv && i < bi)) {
+            bv = c;
+            bi = i;
+        }
+    }
+    sv[threadIdx.x] = bv;
+    si[threadIdx.x] = bi;
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+        if ((int)threadIdx.x < s) {
+            double ov = sv[threadIdx.x + s];
+            int64_t oi = si[threadIdx.x + s];
+            if (ov > sv[threadIdx.x] || (ov == sv[threadIdx.x] && oi < si[threadIdx.x])) {
+                sv[threadIdx.x] = ov;
+                si[threadIdx.x] = oi;
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        pv[blockIdx.x] = sv[0];
+        pi[blockIdx.x] = si[0];
+    }
+}
+
+__global__ void reseed_finish_kernel(int nb, const double* __restrict__ pv, const int64_t* __restrict__ pi,
+                                     int64_t d, const double* __restrict__ v, uint8_t* __restrict__ used,
+                                     double* __restrict__ cent, int64_t cl) {
+    __shared__ int64_t pick;
+    if (threadIdx.x == 0) {
+        double bv = -INFINITY;
+        int64_t bi = INT64_MAX;
+        for (int b = 0; b < nb; ++b) {
+            if (pv[b] > bv || (pv[b] == bv && pi[b] < bi)) {
+                bv = pv[b];
+                bi = pi[b];
+            }
+        }
+        pick = bi;
+        used[bi] = 1;
+    }
+    __syncthreads();
+    for (int64_t l = threadIdx.x; l < d; l += blockDim.x) cent[cl * d + l] = v[pick * d + l];
+}
+
+
+// ---------------------------------------------------------------------------
+// k-means++ device steps (kmeans.py:101-136)
+// d2 <- min(d2, |v - v[pick]|^2) by direct differences; mark taken; per-block
+// candidate partials (count, weight sum) over untaken rows with d2 > 0.
+__global__ void kpp_update_kernel(int64_t n, int64_t d, const double* __restrict__ v, int64_t pick,
+                                  int first, double* __restrict__ d2, uint8_t* __restrict__ taken,
+                                  double* __restrict__ pw, int64_t* __restrict__ pc) {
+    __shared__ double sw[8];
+    __shared__ int64_t scn[8];
+    int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int64_t i = (int64_t)blockIdx.x * 8 + warp;  // one warp per row
+    double w = 0.0;
+    int64_t cnt = 0;
+    if (i < n) {
+        const double* r = v + i * d;
+        const double* p = v + pick * d;
+        double acc = 0.0;
+        for (int64_t l = lane; l < d; l += 32) {
+            double t = r[l] - p[l];
+            acc = fma(t, t, acc);
+        }
+        acc = warp_sum(acc);
+        double nv = first ? acc : fmin(d2[i], acc);
+        if (i == pick) taken[i] = 1;
+        bool tk = (i == pick) || taken[i];
+        if (lane == 0) d2[i] = nv;
+        if (!tk && nv > 0.0) {
+            w = nv;
+            cnt = 1;
+        }
+    }
+    if (lane == 0) {
+        sw[warp] = w;
+        scn[warp] = cnt;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0;
+        int64_t c = 0;
+        for (int q = 0; q < 8; ++q) {
+            a += sw[q];
+            c += scn[q];
+        }
+        pw[blockIdx.x] = a;
+        pc[blockIdx.x] = c;
+    }
+}
+
+__global__ void kpp_total_kernel(int64_t nb, const double* __restrict__ pw, const int64_t* __restrict__ pc,
+                                 double* __restrict__ out_total, int64_t* __restrict__ out_count) {
+    __shared__ double sw[1024];
+    __shared__ int64_t sc_[1024];
+    double a = 0.0;
+    int64_t c = 0;
+    for (int64_t b = threadIdx.x; b < nb; b += blockDim.x) {
+        a += pw[b];
+        c += pc[b];
+    }
+    sw[threadIdx.x] = a;
+    sc_[threadIdx.x] = c;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if ((int)threadIdx.x < s) {
+            sw[threadIdx.x] += sw[threadIdx.x + s];
+            sc_[threadIdx.x] += sc_[threadIdx.x + s];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        *out_total = sw[0];
+        *out_count = sc_[0];
+    }
+}
+
+constexpr int KPP_BLK = 1024;
+
+// per-block sums of p_i = w_i / total over candidates (rng.choice p vector)
+__global__ void kpp_psum_kernel(int64_t n, const double* __restrict__ d2, const uint8_t* __restrict__ taken,
+                                const double* __restrict__ total, double* __restrict__ bsum) {
+    __shared__ double red[KPP_BLK];
+    int64_t i = (int64_t)blockIdx.x * KPP_BLK + threadIdx.x;
+    double tot = *total;
+    double p = 0.0;
+    if (i < n && !taken[i] && d2[i] > 0.0) p = d2[i] / tot;
+    red[threadIdx.x] = p;
+    __syncthreads();
+    for (int s = KPP_BLK / 2; s > 0; s >>= 1) {
+        if ((int)threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) bsum[blockIdx.x] = red[0];
+}
+
+// first index whose normalised cumulative probability exceeds u
+// (numpy Generator.choice: cdf = p.cumsum(); cdf /= cdf[-1];
+//  cdf.searchsorted(u, side="right")).
+__global__ void kpp_search_kernel(int64_t n, int64_t nb, const double* __restrict__ d2,
+                                  const uint8_t* __restrict__ taken, const double* __restrict__ total,
+                                  const double* __restrict__ bsum, double u, int64_t* __restrict__ out) {
+    if (threadIdx.x != 0) return;
+    double last = 0.0;
+    for (int64_t b = 0; b < nb; ++b) last += bsum[b];
+    double run = 0.0;
+    int64_t b = 0;
+    for (; b < nb; ++b) {
+        if ((run + bsum[b]) / last > u) break;
+        run += bsum[b];
+    }
+    double tot = *total;
+    int64_t lastcand = -1;
+    if (b == nb) b = nb - 1, run -= bsum[nb - 1];
+    int64_t lo = b * KPP_BLK, hi = imin64(n, lo + KPP_BLK);
+    for (int64_t i = lo; i < hi; ++i) {
+        if (taken[i] || !(d2[i] > 0.0)) continue;
+        lastcand = i;
+        run += d2[i] / tot;
+        if (run / last > u) {
+            *out = i;
+            return;
+        }
+    }
+    if (lastcand < 0) {  // rounding pushed the crossing past every candidate
+        for (int64_t i = n - 1; i >= 0; --i)
+            if (!taken[i] && d2[i] > 0.0) { lastcand = i; break; }
+    }
+    *out = lastcand;
+}
+
+// r-th untaken row in ascending order (uniform fallback, kmeans.py:133-134)
+__global__ void kpp_nth_free_kernel(int64_t n, const uint8_t* __restrict__ taken, int64_t r,
+                                    int64_t* __restrict__ out) {
+    if (threadIdx.x != 0) return;
+    int64_t c = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        if (taken[i]) continue;
+        if (c == r) {
+            *out = i;
+            return;
+        }
+        ++c;
+    }
+    *out = -1;
+}
+
+// ---------------------------------------------------------------------------
+// ncut (metrics.py:34-39, 59-67): per part, one sequential chain over member
+// rows in ascending order reproduces the reference's bincount order.
+__global__ void ncut_parts_kernel(int64_t k, const int64_t* __restrict__ row_ptr,
+                                  const int32_t* __restrict__ col, const double* __restrict__ vals,
+                                  const double* __restrict__ deg, const int64_t* __restrict__ labels,
+                                  const int64_t* __restrict__ start, const int32_t* __restrict__ members,
+                                  double* __restrict__ bnd, double* __restrict__ vol) {
+    int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= k) return;
+    double b = 0.0, v = 0.0;
+    for (int64_t m = start[c]; m < start[c + 1]; ++m) {
+        int64_t i = members[m];
+        v = __dadd_rn(v, deg[i]);
+        for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p)
+            if (labels[col[p]] != c) b = __dadd_rn(b, vals[p]);
+    }
+    bnd[c] = b;
+    vol[c] = v;
+}
+
+// numpy's pairwise summation (DOUBLE_pairwise_sum) for a contiguous array
+static double np_pairwise_sum(const double* a, int64_t n) {
+    if (n < 8) {
+        double res = 0.0;  // numpy starts from the first element: (-0.0) aware
+        if (n == 0) return 0.0;
+        res = a[0];
+        for (int64_t i = 1; i < n; ++i) res += a[i];
+        return res;
+    } else if (n <= 128) {
+        double r[8];
+        for (int j = 0; j < 8; ++j) r[j] = a[j];
+        int64_t i = 8;
+        for (; i < n - (n % 8); i += 8)
+            for (int j = 0; j < 8; ++j) r[j] += a[i + j];
+        double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+        for (; i < n; ++i) res += a[i];
+        return res;
+    }
+    int64_t n2 = n / 2;
+    n2 -= n2 % 8;
+    return np_pairwise_sum(a, n2) + np_pairwise_sum(a + n2, n - n2);
+}
+
+}  // namespace sc
+
+using namespace sc;
+
+// ---------------------------------------------------------------------------
+// host entry points
+struct sc_kmeanspp {
+    int64_t n = 0, d = 0, nb_upd = 0, nb_p = 0;
+    const double* v = nullptr;
+    cudaStream_t st = nullptr;
+    bool first = true;
+    int64_t taken_count = 0;
+    DevBuf<double> d2, pw, bsum, total;
+    DevBuf<int64_t> pc, count, pick;
+    DevBuf<uint8_t> taken;
+};
+
+extern "C" {
+
+int sc_pairwise_sq_dist(int64_t n, int64_t k, int64_t d, const double* v, const double* c,
+                        double* out, sc_stream_t stream) {
+    if (n < 0 || k < 0 || d < 0) return fail(SC_ERR_VALUE, "negative dimension");
+    if (n == 0 || k == 0) return SC_OK;
+    cudaStream_t st = as_stream(stream);
+    DevBuf<double> vn, cn;
+    if (int rc = vn.alloc(n)) return rc;
+    if (int rc = cn.alloc(k)) return rc;
+    rownorm_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, d, v, vn.p);
+    rownorm_kernel<<<(unsigned)ceil_div(k, 256), 256, 0, st>>>(k, d, c, cn.p);
+    dist_tile_kernel<1><<<(unsigned)ceil_div(n, TP), 256, 0, st>>>(n, k, d, v, vn.p, c, cn.p, out,
+                                                                   nullptr, nullptr, nullptr, nullptr, nullptr);
+    SC_LAUNCHED(3);
+    SC_CUDA(cudaStreamSynchronize(st));
+    return SC_OK;
+}
+
+int sc_lloyd(int64_t n, int64_t d, int64_t k, const double* v, const double* c_init,
+             int64_t max_iters, int64_t tol_changes, int64_t* labels, double* centroids,
+             double* sse_history, int64_t* iters_out, sc_stream_t stream) {
+    if (n < 1 || k < 1 || d < 0) return fail(SC_ERR_VALUE, "lloyd requires n >= 1, k >= 1");
+    if (max_iters < 1) return fail(SC_ERR_VALUE, "max_iters must be >= 1");
+    cudaStream_t st = as_stream(stream);
+    const int64_t nb = ceil_div(n, TP);
+    DevBuf<double> vn, cn, cost, part, sse;
+    DevBuf<int64_t> lab2;
+    DevBuf<unsigned long long> changes;
+    DevBuf<int> empty;
+    DevBuf<uint8_t> used;
+    DevBuf<double> pv;
+    DevBuf<int64_t> pi;
+    Bucketer bk;
+    int rc;
+    if ((rc = vn.alloc(n)) || (rc = cn.alloc(k)) || (rc = cost.alloc(n)) || (rc = part.alloc(nb)) ||
+        (rc = sse.alloc(1)) || (rc = lab2.alloc(n)) || (rc = changes.alloc(1)) || (rc = empty.alloc(k)) ||
+        (rc = bk.init(n, k)))
+        return rc;
+    SC_CUDA(cudaMemcpyAsync(centroids, c_init, sizeof(double) * k * d, cudaMemcpyDeviceToDevice, st));
+    rownorm_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, d, v, vn.p);
+    rownorm_kernel<<<(unsigned)ceil_div(k, 256), 256, 0, st>>>(k, d, centroids, cn.p);
+    double flops = 2.0 * (double)n * (double)k * (double)d;
+    {
+        ProfScope prof("kmeans_assign", st, flops);
+        dist_tile_kernel<0><<<(unsigned)nb, 256, 0, st>>>(n, k, d, v, vn.p, centroids, cn.p, nullptr, labels,
+                                                          nullptr, cost.p, changes.p, part.p);
+    }
+    sum_partials_kernel<<<1, 1024, 0, st>>>(nb, part.p, sse.p);
+    SC_LAUNCHED(4);
+    SC_CUDA(cudaMemcpyAsync(&sse_history[0], sse.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+    SC_CUDA(cudaStreamSynchronize(st));
+
+    int64_t* cur = labels;
+    int64_t* nxt = lab2.p;
+    int64_t iters = 0;
+    const int64_t dchunks = ceil_div(d, 32);
+    std::vector<int> hempty;
+    while (iters < max_iters) {
+        // ---- update (kmeans.py:139-156)
+        if ((rc = bk.run(cur, st))) return rc;
+        SC_CUDA(cudaMemsetAsync(empty.p, 0, sizeof(int) * k, st));
+        {
+            ProfScope prof("kmeans_update", st, (double)n * d * 8.0 + 12.0 * n + 16.0 * k * d);
+            int64_t warps = k * dchunks;
+            centroid_mean_kernel<<<(unsigned)ceil_div(warps * 32, 256), 256, 0, st>>>(
+                k, d, v, bk.start.p, bk.members.p, centroids, empty.p);
+        }
+        SC_LAUNCHED(1);
+        // empty clusters: count them from the bucket offsets (cheap host read)
+        std::vector<int64_t> hstart(k + 1);
+        SC_CUDA(cudaMemcpyAsync(hstart.data(), bk.start.p, sizeof(int64_t) * (k + 1), cudaMemcpyDeviceToHost, st));
+        SC_CUDA(cudaStreamSynchronize(st));
+        std::vector<int64_t> empties;
+        for (int64_t c = 0; c < k; ++c)
+            if (hstart[c + 1] == hstart[c]) empties.push_back(c);
+        if (!empties.empty()) {
+            if (!used.p) {
+                if ((rc = used.alloc(n)) || (rc = pv.alloc(256)) || (rc = pi.alloc(256))) return rc;
+            }
+            SC_CUDA(cudaMemsetAsync(used.p, 0, n, st));
+            for (size_t s = 0; s < empties.size() && (int64_t)s < n; ++s) {
+                argmax_partial_kernel<<<256, 256, 0, st>>>(n, cost.p, used.p, pv.p, pi.p);
+                reseed_finish_kernel<<<1, 128, 0, st>>>(256, pv.p, pi.p, d, v, used.p, centroids, empties[s]);
+                SC_LAUNCHED(2);
+            }
+        }
+        // ---- assign
+        rownorm_kernel<<<(unsigned)ceil_div(k, 256), 256, 0, st>>>(k, d, centroids, cn.p);
+        SC_CUDA(cudaMemsetAsync(changes.p, 0, sizeof(unsigned long long), st));
+        {
+            ProfScope prof("kmeans_assign", st, flops);
+            dist_tile_kernel<0><<<(unsigned)nb, 256, 0, st>>>(n, k, d, v, vn.p, centroids, cn.p, nullptr, nxt,
+                                                              cur, cost.p, changes.p, part.p);
+        }
+        sum_partials_kernel<<<1, 1024, 0, st>>>(nb, part.p, sse.p);
+        SC_LAUNCHED(3);
+        unsigned long long hchg = 0;
+        SC_CUDA(cudaMemcpyAsync(&sse_history[iters + 1], sse.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+        SC_CUDA(cudaMemcpyAsync(&hchg, changes.p, sizeof(hchg), cudaMemcpyDeviceToHost, st));
+        SC_CUDA(cudaStreamSynchronize(st));
+        ++iters;
+        std::swap(cur, nxt);
+        if ((int64_t)hchg <= tol_changes) break;
+    }
+    if (cur != labels) SC_CUDA(cudaMemcpyAsync(labels, cur, sizeof(int64_t) * n, cudaMemcpyDeviceToDevice, st));
+    SC_CUDA(cudaStreamSynchronize(st));
+    *iters_out = iters;
+    return SC_OK;
+}
+
+int sc_kmeanspp_create(int64_t n, int64_t d, const double* v, sc_stream_t stream, sc_kmeanspp_t** out) {
+    if (n < 1) return fail(SC_ERR_VALUE, "k-means++ needs n >= 1");
+    auto* s = new sc_kmeanspp();
+    s->n = n;
+    s->d = d;
+    s->v = v;
+    s->st = as_stream(stream);
+    s->nb_upd = ceil_div(n, 8);
+    s->nb_p = ceil_div(n, KPP_BLK);
+    int rc;
+    if ((rc = s->d2.alloc(n)) || (rc = s->taken.alloc(n)) || (rc = s->pw.alloc(s->nb_upd)) ||
+        (rc = s->pc.alloc(s->nb_upd)) || (rc = s->bsum.alloc(s->nb_p)) || (rc = s->total.alloc(1)) ||
+        (rc = s->count.alloc(1)) || (rc = s->pick.alloc(1))) {
+        delete s;
+        return rc;
+    }
+    cudaMemsetAsync(s->taken.p, 0, n, s->st);
+    *out = s;
+    return SC_OK;
+}
+
+void sc_kmeanspp_destroy(sc_kmeanspp_t* s) { delete s; }
+
+int sc_kmeanspp_take(sc_kmeanspp_t* s, int64_t index) {
+    if (index < 0 || index >= s->n) return fail(SC_ERR_VALUE, "k-means++ index out of range");
+    {
+        ProfScope prof("kmeanspp", s->st, (double)s->n * s->d * 8.0);
+        kpp_update_kernel<<<(unsigned)s->nb_upd, 256, 0, s->st>>>(s->n, s->d, s->v, index, s->first ? 1 : 0,
+                                                                  s->d2.p, s->taken.p, s->pw.p, s->pc.p);
+    }
+    kpp_total_kernel<<<1, 1024, 0, s->st>>>(s->nb_upd, s->pw.p, s->pc.p, s->total.p, s->count.p);
+    SC_LAUNCHED(2);
+    s->first = false;
+    s->taken_count += 1;
+    return SC_OK;
+}
+
+int sc_kmeanspp_candidates(sc_kmeanspp_t* s, int64_t* count, int64_t* n_free) {
+    SC_CUDA(cudaMemcpyAsync(count, s->count.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s->st));
+    SC_CUDA(cudaStreamSynchronize(s->st));
+    *n_free = s->n - s->taken_count;
+    return SC_OK;
+}
+
+int sc_kmeanspp_pick(sc_kmeanspp_t* s, int mode, double u, int64_t r, int64_t* index) {
+    if (mode == 0) {
+        kpp_psum_kernel<<<(unsigned)s->nb_p, KPP_BLK, 0, s->st>>>(s->n, s->d2.p, s->taken.p, s->total.p, s->bsum.p);
+        kpp_search_kernel<<<1, 32, 0, s->st>>>(s->n, s->nb_p, s->d2.p, s->taken.p, s->total.p, s->bsum.p, u,
+                                               s->pick.p);
+        SC_LAUNCHED(2);
+    } else {
+        kpp_nth_free_kernel<<<1, 32, 0, s->st>>>(s->n, s->taken.p, r, s->pick.p);
+        SC_LAUNCHED(1);
+    }
+    int64_t h = -1;
+    SC_CUDA(cudaMemcpyAsync(&h, s->pick.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s->st));
+    SC_CUDA(cudaStreamSynchronize(s->st));
+    if (h < 0) return fail(SC_ERR_INTERNAL, "k-means++ draw found no row");
+    *index = h;
+    return sc_kmeanspp_take(s, h);
+}
+
+int sc_ncut(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* vals,
+            const int64_t* labels, int64_t k, double* out, sc_stream_t stream) {
+    *out = -1.0;
+    if (n < 1 || k < 1) return fail(SC_ERR_VALUE, "ncut needs n >= 1 and k >= 1");
+    cudaStream_t st = as_stream(stream);
+    DevBuf<double> deg, bnd, vol;
+    Bucketer bk;
+    int rc;
+    if ((rc = deg.alloc(n)) || (rc = bnd.alloc(k)) || (rc = vol.alloc(k)) || (rc = bk.init(n, k))) return rc;
+    if ((rc = degrees_launch(n, row_ptr, vals, deg.p, st))) return rc;
+    if ((rc = bk.run(labels, st))) return rc;
+    ncut_parts_kernel<<<(unsigned)ceil_div(k, 64), 64, 0, st>>>(k, row_ptr, col, vals, deg.p, labels, bk.start.p,
+                                                                 bk.members.p, bnd.p, vol.p);
+    SC_LAUNCHED(1);
+    std::vector<double> hb(k), hv(k);
+    SC_CUDA(cudaMemcpyAsync(hb.data(), bnd.p, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
+    SC_CUDA(cudaMemcpyAsync(hv.data(), vol.p, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
+    SC_CUDA(cudaStreamSynchronize(st));
+    std::vector<double> q(k);
+    for (int64_t c = 0; c < k; ++c) {
+        if (!(hv[c] > 0.0)) return fail(SC_ERR_VALUE, "part " + std::to_string(c) + " has zero volume");
+        q[c] = hb[c] / hv[c];
+    }
+    *out = 0.5 * np_pairwise_sum(q.data(), k);
+    return SC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,608 @@
+// Stage 1: kNN + exp_decay similarity graph, emitted straight into CSR.
+//
+// Reference semantics (graph.py:149-157, 185-204, 136-141, 214-237):
+//   row i ranks every j != i by (similarity desc, index asc) with
+//   s_ij = exp(inv * d2_ij), inv = -1/(2 sigma^2), d2 from direct differences;
+//   the first knn are selected; edge {i,j} exists iff j in top(i) or i in
+//   top(j); its weight exp(-d2/(2 sigma^2)) is evaluated once per pair.
+//
+// Pipeline:
+//   prep      centre X (fp64 column means), fp32 copy + fp32 norms, fp64 norms
+//   candidates  distance tiles |x_j|^2 - 2 x_i.x_j (low precision) with a
+//             streaming per-row top-R list (append + quickselect compaction)
+//   recheck   exact fp64 d2 and s for the R..CAP candidates, rank by
+//             (-s, j), certify with an error bound that no non-candidate can
+//             enter the top knn; uncertified rows -> exact fallback
+//   fallback  fp64 scan of all n points + radix select on (s, -j)
+//   union     reverse lists, duplicate removal, scan, CSR fill with fp64 values
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "sc_common.cuh"
+#include "sc_knn.cuh"
+#include "sc_scan.cuh"
+
+namespace sc {
+
+// ---------------------------------------------------------------------------
+// prep
+__global__ void colsum_partial_kernel(int64_t n, int64_t d, const double* __restrict__ x, double* __restrict__ part) {
+    // block b: rows [b*256, b*256+256); thread t handles columns t, t+blockDim...
+    int64_t r0 = (int64_t)blockIdx.x * 256, r1 = imin64(n, r0 + 256);
+    for (int64_t c = threadIdx.x; c < d; c += blockDim.x) {
+        double a = 0.0;
+        for (int64_t r = r0; r < r1; ++r) a += x[r * d + c];
+        part[blockIdx.x * d + c] = a;
+    }
+}
+__global__ void colmean_finish_kernel(int64_t nb, int64_t n, int64_t d, const double* __restrict__ part,
+                                      double* __restrict__ mean) {
+    int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= d) return;
+    double a = 0.0;
+    for (int64_t b = 0; b < nb; ++b) a += part[b * d + c];
+    mean[c] = a / (double)n;
+}
+
+// xf = fp32(x - mean) padded to dp columns; cnf = fp32(|xf|^2) (computed in
+// fp64 from the fp32 values); rn = |x - mean| (fp64); rmax = max rn
+__global__ void knn_prep_kernel(int64_t n, int64_t d, int64_t dp, const double* __restrict__ x,
+                                const double* __restrict__ mean, float* __restrict__ xf,
+                                float* __restrict__ cnf, double* __restrict__ rn, double* __restrict__ qn,
+                                unsigned long long* __restrict__ rmax_bits) {
+    int64_t i = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    int lane = threadIdx.x & 31;
+    if (i >= n) return;
+    double a64 = 0.0, a32 = 0.0;
+    for (int64_t c = lane; c < dp; c += 32) {
+        float f = 0.f;
+        if (c < d) {
+            double v = x[i * d + c] - mean[c];
+            a64 = fma(v, v, a64);
+            f = (float)v;
+        }
+        xf[i * dp + c] = f;
+        a32 = fma((double)f, (double)f, a32);
+    }
+    a64 = warp_sum(a64);
+    a32 = warp_sum(a32);
+    if (lane == 0) {
+        cnf[i] = (float)a32;
+        double r = sqrt(a64);
+        rn[i] = r;
+        qn[i] = a32;
+        atomicMax(rmax_bits, (unsigned long long)__double_as_longlong(r));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// streaming top-R list (per query row, owned by one thread)
+__device__ float list_compact(float2* L, int cap, int R) {
+    int lo = 0, hi = cap - 1, target = R - 1;
+    while (lo < hi) {
+        float a = L[lo].x, b = L[(lo + hi) >> 1].x, c = L[hi].x;
+        float pivot = fmaxf(fminf(a, b), fminf(fmaxf(a, b), c));  // median of three
+        int i = lo, j = hi;
+        while (i <= j) {
+            while (L[i].x < pivot) ++i;
+            while (L[j].x > pivot) --j;
+            if (i <= j) {
+                float2 t = L[i];
+                L[i] = L[j];
+                L[j] = t;
+                ++i;
+                --j;
+            }
+        }
+        if (target <= j) hi = j;
+        else if (target >= i) lo = i;
+        else break;
+    }
+    float tau = -INFINITY;
+    for (int q = 0; q < R; ++q) tau = fmaxf(tau, L[q].x);
+    return tau;
+}
+
+// ---------------------------------------------------------------------------
+// candidate generation, SIMT fp32 tiles (128 query rows x 128 columns)
+constexpr int KM = 128, KN = 128, KK = 16;
+
+__global__ void __launch_bounds__(256) knn_cand_simt_kernel(int64_t n, int dp, const float* __restrict__ xf,
+                                                            const float* __restrict__ cnf, int cap, int R,
+                                                            float2* __restrict__ lists, int* __restrict__ counts,
+                                                            float* __restrict__ taus) {
+    extern __shared__ float smem[];
+    float* As = smem;                    // KK x KM
+    float* Bs = As + KK * KM;            // KK x KN
+    float* Ks = Bs + KK * KN;            // KM x (KN + 1)
+    float* cns = Ks + KM * (KN + 1);     // KN
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const int64_t r0 = (int64_t)blockIdx.x * KM;
+    const int64_t myrow = r0 + tid;
+    const bool selector = tid < KM && myrow < n;
+    int cnt = 0;
+    float tau = INFINITY;
+    float2* L = lists + (selector ? myrow : 0) * (int64_t)cap;
+
+    for (int64_t c0 = 0; c0 < n; c0 += KN) {
+        float acc[8][8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+        for (int k0 = 0; k0 < dp; k0 += KK) {
+            __syncthreads();
+            // 128 rows x 16 floats each for A and B: 512 float4 each, 2 per thread
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+                int idx = tid + 256 * t;
+                int rr = idx >> 2, q4 = (idx & 3) * 4;
+                int64_t ga = r0 + rr, gb = c0 + rr;
+                float4 va = ga < n ? *reinterpret_cast<const float4*>(xf + ga * dp + k0 + q4) : make_float4(0, 0, 0, 0);
+                float4 vb = gb < n ? *reinterpret_cast<const float4*>(xf + gb * dp + k0 + q4) : make_float4(0, 0, 0, 0);
+                As[(q4 + 0) * KM + rr] = va.x;
+                As[(q4 + 1) * KM + rr] = va.y;
+                As[(q4 + 2) * KM + rr] = va.z;
+                As[(q4 + 3) * KM + rr] = va.w;
+                Bs[(q4 + 0) * KN + rr] = vb.x;
+                Bs[(q4 + 1) * KN + rr] = vb.y;
+                Bs[(q4 + 2) * KN + rr] = vb.z;
+                Bs[(q4 + 3) * KN + rr] = vb.w;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int k = 0; k < KK; ++k) {
+                float4 a0 = *reinterpret_cast<const float4*>(As + k * KM + ty * 4);
+                float4 a1 = *reinterpret_cast<const float4*>(As + k * KM + 64 + ty * 4);
+                float4 b0 = *reinterpret_cast<const float4*>(Bs + k * KN + tx * 4);
+                float4 b1 = *reinterpret_cast<const float4*>(Bs + k * KN + 64 + tx * 4);
+                float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+                float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+            }
+        }
+        if (tid < KN) cns[tid] = (c0 + tid < n) ? cnf[c0 + tid] : 0.f;
+        __syncthreads();
+        // keys = |x_j|^2 - 2 x_i.x_j into the smem tile
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            int m = i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                int nn = j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4);
+                Ks[m * (KN + 1) + nn] = fmaf(-2.f, acc[i][j], cns[nn]);
+            }
+        }
+        __syncthreads();
+        if (selector) {
+            int cmax = (int)imin64(KN, n - c0);
+            const float* krow = Ks + tid * (KN + 1);
+            for (int c = 0; c < cmax; ++c) {
+                float key = krow[c];
+                if (key < tau) {
+                    int64_t col = c0 + c;
+                    if (col == myrow) continue;
+                    L[cnt++] = make_float2(key, __int_as_float((int)col));
+                    if (cnt == cap) {
+                        tau = list_compact(L, cap, R);
+                        cnt = R;
+                    }
+                }
+            }
+        }
+    }
+    if (selector) {
+        counts[myrow] = cnt;
+        taus[myrow] = tau;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// exact recheck: warp per row
+__device__ __forceinline__ double exact_d2(const double* __restrict__ xi, const double* __restrict__ xj, int64_t d) {
+    double acc = 0.0;
+    for (int64_t l = 0; l < d; ++l) {
+        double t = __dsub_rn(xj[l], xi[l]);
+        acc = __dadd_rn(acc, __dmul_rn(t, t));
+    }
+    return acc;
+}
+
+// (s desc, j asc) ordering: a precedes b
+__device__ __forceinline__ bool precedes(double sa, int ja, double sb, int jb) {
+    return sa > sb || (sa == sb && ja < jb);
+}
+
+__global__ void __launch_bounds__(256) knn_recheck_kernel(int64_t n, int64_t d, const double* __restrict__ x,
+                                                          int64_t knn, double inv, int cap,
+                                                          const float2* __restrict__ lists,
+                                                          const int* __restrict__ counts,
+                                                          const float* __restrict__ taus,
+                                                          const double* __restrict__ rn, const double* __restrict__ qn,
+                                                          const unsigned long long* __restrict__ rmax_bits,
+                                                          double cdelta, int32_t* __restrict__ sel,
+                                                          int32_t* __restrict__ flagged,
+                                                          unsigned long long* __restrict__ nflag) {
+    extern __shared__ unsigned char rsm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double* S = reinterpret_cast<double*>(rsm) + (size_t)warp * cap;
+    int* J = reinterpret_cast<int*>(reinterpret_cast<double*>(rsm) + (size_t)8 * cap) + (size_t)warp * cap;
+    const int64_t i = (int64_t)blockIdx.x * 8 + warp;
+    if (i >= n) return;
+    const int cnt = counts[i];
+    const float2* L = lists + i * (int64_t)cap;
+    const double* xi = x + i * d;
+    for (int t = lane; t < cnt; t += 32) {
+        int j = __float_as_int(L[t].y);
+        double d2 = exact_d2(xi, x + (int64_t)j * d, d);
+        S[t] = exp(inv * d2);
+        J[t] = j;
+    }
+    __syncwarp();
+    // rank each candidate; the knn first ranks are selected
+    double s_k = INFINITY;
+    for (int t = lane; t < cnt; t += 32) {
+        double st = S[t];
+        int jt = J[t];
+        int r = 0;
+        for (int u = 0; u < cnt; ++u) r += precedes(S[u], J[u], st, jt);
+        if (r < knn) sel[i * knn + r] = jt;
+        if (r == knn - 1) s_k = st;
+    }
+    // broadcast s_k (held by exactly one lane)
+    for (int o = 16; o > 0; o >>= 1) s_k = fmin(s_k, __shfl_xor_sync(0xffffffffu, s_k, o));
+    if (lane != 0) return;
+    float tau = taus[i];
+    bool ok;
+    if (cnt < knn) {
+        ok = false;
+    } else if (isinf(tau)) {
+        ok = true;  // never compacted: every other point is a candidate
+    } else {
+        double rmax = __longlong_as_double((long long)*rmax_bits);
+        double r = rn[i] + rmax;
+        double delta = cdelta * r * r;
+        double lower = qn[i] + (double)tau - delta;  // lower bound of d2 for non-candidates
+        lower = lower * (1.0 - 1e-12) - 1e-300;
+        ok = lower > 0.0 && s_k > exp(inv * lower);
+    }
+    if (!ok) {
+        unsigned long long slot = atomicAdd(nflag, 1ull);
+        flagged[slot] = (int32_t)i;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// exact fallback: block per flagged row, radix select on the (s, -j) order
+__global__ void __launch_bounds__(512) knn_fallback_kernel(int64_t n, int64_t d, const double* __restrict__ x,
+                                                           int64_t knn, double inv,
+                                                           const int32_t* __restrict__ flagged, int64_t nflag,
+                                                           unsigned long long* __restrict__ scratch,
+                                                           int32_t* __restrict__ sel) {
+    __shared__ unsigned int hist[256];
+    __shared__ unsigned long long s_prefix;
+    __shared__ long long s_remaining;
+    __shared__ int s_out;
+    __shared__ int wcount[16];
+    __shared__ long long s_base;
+    unsigned long long* key = scratch + (size_t)blockIdx.x * n;
+    for (int64_t f = blockIdx.x; f < nflag; f += gridDim.x) {
+        const int64_t i = flagged[f];
+        const double* xi = x + i * d;
+        for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+            if (j == i) {
+                key[j] = 0ull;
+            } else {
+                double s = exp(inv * exact_d2(xi, x + j * d, d));
+                key[j] = (unsigned long long)__double_as_longlong(s) + 1ull;  // s >= 0 -> monotone bits
+            }
+        }
+        if (threadIdx.x == 0) {
+            s_prefix = 0ull;
+            s_remaining = knn;
+        }
+        __syncthreads();
+        unsigned long long mask = 0ull;
+        for (int pass = 7; pass >= 0; --pass) {
+            const int shift = pass * 8;
+            for (int b = threadIdx.x; b < 256; b += blockDim.x) hist[b] = 0;
+            __syncthreads();
+            const unsigned long long pre = s_prefix;
+            for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+                unsigned long long kj = key[j];
+                if ((kj & mask) == pre) atomicAdd(&hist[(kj >> shift) & 255ull], 1u);
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                long long rem = s_remaining;
+                long long above = 0;
+                int g = 255;
+                for (; g > 0; --g) {
+                    if (above + (long long)hist[g] >= rem) break;
+                    above += hist[g];
+                }
+                s_remaining = rem - above;
+                s_prefix = pre | ((unsigned long long)g << shift);
+            }
+            mask |= 255ull << shift;
+            __syncthreads();
+        }
+        const unsigned long long T = s_prefix;
+        const long long take_eq = s_remaining;  // elements == T to take, lowest index first
+        if (threadIdx.x == 0) {
+            s_out = 0;
+            s_base = 0;
+        }
+        __syncthreads();
+        for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+            if (key[j] > T) {
+                int slot = atomicAdd(&s_out, 1);
+                sel[i * knn + slot] = (int32_t)j;
+            }
+        }
+        __syncthreads();
+        const int above_cnt = s_out;
+        for (int64_t base = 0; base < n; base += blockDim.x) {
+            int64_t j = base + threadIdx.x;
+            bool hit = j < n && key[j] == T;
+            unsigned bal = __ballot_sync(0xffffffffu, hit);
+            int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+            if (l == 0) wcount[w] = __popc(bal);
+            __syncthreads();
+            long long before = s_base;
+            for (int q = 0; q < w; ++q) before += wcount[q];
+            long long r = before + __popc(bal & ((1u << l) - 1u));
+            if (hit && r < take_eq) sel[i * knn + above_cnt + r] = (int32_t)j;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                long long tot = 0;
+                for (int q = 0; q < (int)(blockDim.x >> 5); ++q) tot += wcount[q];
+                s_base += tot;
+            }
+            __syncthreads();
+            if (s_base >= take_eq) break;
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// union + CSR
+__global__ void sort_rows_kernel(int64_t n, int64_t knn, int32_t* __restrict__ sel) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int32_t* r = sel + i * knn;
+    for (int64_t a = 1; a < knn; ++a) {
+        int32_t v = r[a];
+        int64_t b = a - 1;
+        while (b >= 0 && r[b] > v) {
+            r[b + 1] = r[b];
+            --b;
+        }
+        r[b + 1] = v;
+    }
+}
+
+__global__ void rev_count_kernel(int64_t total, const int32_t* __restrict__ sel, int64_t* __restrict__ rc) {
+    int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < total) atomicAdd(reinterpret_cast<unsigned long long*>(rc + sel[p]), 1ull);
+}
+
+__global__ void rev_fill_kernel(int64_t n, int64_t knn, const int32_t* __restrict__ sel,
+                                const int64_t* __restrict__ rev_ptr, unsigned int* __restrict__ fill,
+                                int32_t* __restrict__ rev) {
+    int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n * knn) return;
+    int32_t j = sel[p];
+    unsigned int pos = atomicAdd(fill + j, 1u);
+    rev[rev_ptr[j] + pos] = (int32_t)(p / knn);
+}
+
+__device__ __forceinline__ bool in_sorted(const int32_t* __restrict__ a, int64_t len, int32_t v) {
+    int64_t lo = 0, hi = len;
+    while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        if (a[mid] < v) lo = mid + 1; else hi = mid;
+    }
+    return lo < len && a[lo] == v;
+}
+
+// len_i = knn + #(reverse entries not already selected); marks duplicates
+__global__ void row_count_kernel(int64_t n, int64_t knn, const int32_t* __restrict__ sel,
+                                 const int64_t* __restrict__ rev_ptr, const int32_t* __restrict__ rev,
+                                 uint8_t* __restrict__ dup, int64_t* __restrict__ len) {
+    int64_t i = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    int lane = threadIdx.x & 31;
+    if (i >= n) return;
+    const int32_t* s = sel + i * knn;
+    int64_t c = 0;
+    for (int64_t p = rev_ptr[i] + lane; p < rev_ptr[i + 1]; p += 32) {
+        bool dp = in_sorted(s, knn, rev[p]);
+        dup[p] = dp;
+        c += !dp;
+    }
+    c = warp_sum_i64(c);
+    if (lane == 0) len[i] = knn + c;
+}
+
+__global__ void row_fill_kernel(int64_t n, int64_t d, int64_t knn, const double* __restrict__ x, double den,
+                                const int32_t* __restrict__ sel, const int64_t* __restrict__ rev_ptr,
+                                const int32_t* __restrict__ rev, const uint8_t* __restrict__ dup,
+                                const int64_t* __restrict__ row_ptr, int32_t* __restrict__ col,
+                                double* __restrict__ vals) {
+    int64_t i = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    int lane = threadIdx.x & 31;
+    if (i >= n) return;
+    const int32_t* s = sel + i * knn;
+    const int64_t rb = rev_ptr[i], re = rev_ptr[i + 1];
+    const int64_t out0 = row_ptr[i];
+    const double* xi = x + i * d;
+    // selected entries
+    for (int64_t t = lane; t < knn; t += 32) {
+        int32_t e = s[t];
+        int64_t r = t;
+        for (int64_t p = rb; p < re; ++p) r += (!dup[p] && rev[p] < e);
+        col[out0 + r] = e;
+        vals[out0 + r] = exp(-exact_d2(xi, x + (int64_t)e * d, d) / den);
+    }
+    // reverse-only entries
+    for (int64_t p = rb + lane; p < re; p += 32) {
+        if (dup[p]) continue;
+        int32_t e = rev[p];
+        int64_t lo = 0, hi = knn;
+        while (lo < hi) {
+            int64_t mid = (lo + hi) >> 1;
+            if (s[mid] < e) lo = mid + 1; else hi = mid;
+        }
+        int64_t r = lo;
+        for (int64_t q = rb; q < re; ++q) r += (!dup[q] && rev[q] < e);
+        col[out0 + r] = e;
+        vals[out0 + r] = exp(-exact_d2(xi, x + (int64_t)e * d, d) / den);
+    }
+}
+
+}  // namespace sc
+
+using namespace sc;
+
+namespace sc {
+
+int knn_graph_build(int64_t n, int64_t d, const double* x, int64_t knn, double two_sigma_sq, int64_t* row_ptr,
+                    int32_t* col, double* vals, int64_t* nnz_out, int64_t* stats, cudaStream_t st) {
+    const double inv = -1.0 / two_sigma_sq;  // graph.py:154
+    const int64_t dp = (d + 15) / 16 * 16;
+    const int R = (int)imin64(n - 1, knn + std::max<int64_t>(8, knn / 2));
+    int cap = 2 * R;
+    if (cap > n - 1) cap = (int)(n - 1);  // lists can hold every other point
+    if (cap < R) cap = R;
+    int rc;
+    DevBuf<double> part, mean, rn, qn;
+    DevBuf<float> xf, cnf, taus;
+    DevBuf<unsigned long long> rmax, nflag;
+    DevBuf<float2> lists;
+    DevBuf<int> counts;
+    DevBuf<int32_t> sel, flagged, rev;
+    DevBuf<int64_t> rc_cnt, rev_ptr, len, tmp;
+    DevBuf<unsigned int> fill;
+    DevBuf<uint8_t> dup;
+    const int64_t nbc = ceil_div(n, 256);
+    if ((rc = part.alloc((size_t)nbc * d)) || (rc = mean.alloc(d)) || (rc = rn.alloc(n)) || (rc = qn.alloc(n)) ||
+        (rc = xf.alloc((size_t)n * dp)) || (rc = cnf.alloc(n)) || (rc = taus.alloc(n)) || (rc = rmax.alloc(1)) ||
+        (rc = nflag.alloc(1)) || (rc = lists.alloc((size_t)n * cap)) || (rc = counts.alloc(n)) ||
+        (rc = sel.alloc((size_t)n * knn)) || (rc = flagged.alloc(n)))
+        return rc;
+    // ---- prep
+    colsum_partial_kernel<<<(unsigned)nbc, 128, 0, st>>>(n, d, x, part.p);
+    colmean_finish_kernel<<<(unsigned)ceil_div(d, 128), 128, 0, st>>>(nbc, n, d, part.p, mean.p);
+    SC_CUDA(cudaMemsetAsync(rmax.p, 0, sizeof(unsigned long long), st));
+    SC_CUDA(cudaMemsetAsync(nflag.p, 0, sizeof(unsigned long long), st));
+    knn_prep_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, st>>>(n, d, dp, x, mean.p, xf.p, cnf.p, rn.p, qn.p, rmax.p);
+    SC_LAUNCHED(3);
+    // ---- candidates
+    {
+        size_t smem = sizeof(float) * (KK * KM + KK * KN + KM * (KN + 1) + KN);
+        cudaFuncSetAttribute(knn_cand_simt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        ProfScope prof("knn_tile", st, 2.0 * (double)n * (double)n * (double)d);
+        knn_cand_simt_kernel<<<(unsigned)ceil_div(n, KM), 256, smem, st>>>(n, (int)dp, xf.p, cnf.p, cap, R, lists.p,
+                                                                           counts.p, taus.p);
+        SC_LAUNCHED(1);
+    }
+    // ---- exact recheck + certificate.  fp32 error bound on the key
+    // |x_j|^2 - 2 x_i.x_j: inputs rounded (u = 2^-24) and a dp-term fp32
+    // accumulation; generous constant (2 dp + 16) u (|x_i| + |x_j|)^2.
+    const double cdelta = (2.0 * (double)dp + 16.0) * std::ldexp(1.0, -24);
+    {
+        size_t smem = (size_t)8 * cap * (sizeof(double) + sizeof(int));
+        cudaFuncSetAttribute(knn_recheck_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        ProfScope prof("knn_recheck", st, (double)n * cap * d * 8.0);
+        knn_recheck_kernel<<<(unsigned)ceil_div(n, 8), 256, smem, st>>>(n, d, x, knn, inv, cap, lists.p, counts.p,
+                                                                        taus.p, rn.p, qn.p, rmax.p, cdelta, sel.p,
+                                                                        flagged.p, nflag.p);
+        SC_LAUNCHED(1);
+    }
+    unsigned long long hflag = 0;
+    SC_CUDA(cudaMemcpyAsync(&hflag, nflag.p, sizeof(hflag), cudaMemcpyDeviceToHost, st));
+    SC_CUDA(cudaStreamSynchronize(st));
+    lists.free();
+    xf.free();
+    if (hflag > 0) {
+        int64_t grid = imin64((int64_t)hflag, kNumSMs);
+        DevBuf<unsigned long long> scratch;
+        if ((rc = scratch.alloc((size_t)grid * n))) return rc;
+        ProfScope prof("knn_fallback", st, (double)hflag * n * d * 8.0);
+        knn_fallback_kernel<<<(unsigned)grid, 512, 0, st>>>(n, d, x, knn, inv, flagged.p, (int64_t)hflag, scratch.p,
+                                                            sel.p);
+        SC_LAUNCHED(1);
+        SC_CUDA(cudaStreamSynchronize(st));
+    }
+    // ---- union + CSR
+    if ((rc = rc_cnt.alloc(n)) || (rc = rev_ptr.alloc(n + 1)) || (rc = len.alloc(n)) ||
+        (rc = tmp.alloc(ceil_div(n, SCAN_BLK) + 1)) || (rc = fill.alloc(n)) || (rc = rev.alloc((size_t)n * knn)) ||
+        (rc = dup.alloc((size_t)n * knn)))
+        return rc;
+    ProfScope prof("knn_union", st, 0.0);
+    sort_rows_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(n, knn, sel.p);
+    SC_CUDA(cudaMemsetAsync(rc_cnt.p, 0, sizeof(int64_t) * n, st));
+    SC_CUDA(cudaMemsetAsync(fill.p, 0, sizeof(unsigned int) * n, st));
+    rev_count_kernel<<<(unsigned)ceil_div(n * knn, 256), 256, 0, st>>>(n * knn, sel.p, rc_cnt.p);
+    SC_LAUNCHED(2);
+    if ((rc = exclusive_scan_i64(n, rc_cnt.p, rev_ptr.p, tmp.p, st))) return rc;
+    rev_fill_kernel<<<(unsigned)ceil_div(n * knn, 256), 256, 0, st>>>(n, knn, sel.p, rev_ptr.p, fill.p, rev.p);
+    row_count_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, st>>>(n, knn, sel.p, rev_ptr.p, rev.p, dup.p, len.p);
+    SC_LAUNCHED(2);
+    if ((rc = exclusive_scan_i64(n, len.p, row_ptr, tmp.p, st))) return rc;
+    row_fill_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, st>>>(n, d, knn, x, two_sigma_sq, sel.p, rev_ptr.p, rev.p,
+                                                              dup.p, row_ptr, col, vals);
+    SC_LAUNCHED(1);
+    int64_t nnz = 0;
+    SC_CUDA(cudaMemcpyAsync(&nnz, row_ptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    SC_CUDA(cudaStreamSynchronize(st));
+    *nnz_out = nnz;
+    if (stats) {
+        stats[0] = R;
+        stats[1] = cap;
+        stats[2] = (int64_t)hflag;
+        stats[3] = nnz;
+        for (int q = 4; q < 8; ++q) stats[q] = 0;
+    }
+    return SC_OK;
+}
+
+}  // namespace sc
+
+extern "C" int sc_knn_graph_f64(int64_t n, int64_t d, const double* x, int64_t knn, double two_sigma_sq,
+                                int64_t* row_ptr, int32_t* col, double* vals, int64_t* nnz_out, int64_t* stats_out,
+                                sc_stream_t stream) {
+    if (n < 2 || d < 1) return fail(SC_ERR_FORMAT, "point matrix must be 2-D with n >= 2, d >= 1");
+    if (!(knn >= 1 && knn < n))
+        return fail(SC_ERR_VALUE, "knn must satisfy 1 <= knn < n, got " + std::to_string(knn) + " for n=" +
+                                      std::to_string(n));
+    if (!(two_sigma_sq > 0)) return fail(SC_ERR_VALUE, "exp_decay requires sigma > 0");
+    if (n >= (int64_t)INT32_MAX) return fail(SC_ERR_VALUE, "n must be < 2^31 for int32 column indices");
+    return knn_graph_build(n, d, x, knn, two_sigma_sq, row_ptr, col, vals, nnz_out, stats_out, as_stream(stream));
+}
+
+// exp(-d2 / (2 sigma^2)) per given pair (graph.py:136-141; build_similarity)
+namespace sc {
+__global__ void pair_weights_kernel(int64_t m, int64_t d, const double* __restrict__ x, const int64_t* __restrict__ e,
+                                    double den, double* __restrict__ out) {
+    int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= m) return;
+    int64_t a = e[2 * p], b = e[2 * p + 1];
+    out[p] = exp(-exact_d2(x + a * d, x + b * d, d) / den);
+}
+}  // namespace sc
+
+extern "C" int sc_pair_weights(int64_t n, int64_t d, const double* x, int64_t m, const int64_t* pairs,
+                               double two_sigma_sq, double* out, sc_stream_t stream) {
+    (void)n;
+    if (m <= 0) return SC_OK;
+    cudaStream_t st = as_stream(stream);
+    pair_weights_kernel<<<(unsigned)ceil_div(m, 256), 256, 0, st>>>(m, d, x, pairs, two_sigma_sq, out);
+    SC_LAUNCHED(1);
+    return SC_OK;
+}

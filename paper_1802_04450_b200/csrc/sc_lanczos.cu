@@ -1,0 +1,774 @@
+// Thick-restart Lanczos on device (eigen.py:86-302), usable both through the
+// reverse-communication session API (caller applies the operator) and as a
+// device-resident eigensolve whose SpMV never leaves the GPU.
+//
+// Data layout: the Krylov basis B is column-major n x (m+1) fp64
+// with leading dimension ld = round_up(n, 32) so every basis vector is a
+// contiguous, 256-byte aligned array (it is both the SpMV input and a GEMV
+// column).  The projected matrix T is m x m column-major.
+//
+// Per Lanczos step (reference: eigen.py:152-179):
+//   h1 = B^T w (alpha = h1[j]);  w -= B h1;  h2 = B^T w;  w -= B h2;  beta = |w|
+// i.e. two classical Gram-Schmidt passes over the raw product, which subsume
+// the reference's three-term subtraction (eigen.py:160) — every component
+// that subtraction removes is also removed by the first full pass.  T, the
+// breakdown rule, the convergence/verification logic and the thick restart
+// follow eigen.py:166-239 exactly.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "sc_common.cuh"
+#include "sc_sparse.cuh"
+#include "sc_symeig.cuh"
+
+namespace sc {
+
+constexpr int GT_ROWS = 1024;     // rows per gemv_t partial block
+constexpr int GN_THREADS = 256;   // rows per gemv_n block
+constexpr double kBreakdownRtol = 1e-13;  // eigen.py:50
+
+// ---- kernels ------------------------------------------------------------------
+__global__ void fill_normal_kernel(int64_t n, uint64_t seed, uint64_t stream_id, double* __restrict__ out) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = philox_normal(seed, stream_id, (uint64_t)i);
+}
+
+// part[b * ncols + c] = sum_{r in block b} B[c * ld + r] * w[r]
+__global__ void __launch_bounds__(256) gemv_t_partial_kernel(int64_t n, int64_t ld, int ncols,
+                                                             const double* __restrict__ B,
+                                                             const double* __restrict__ w,
+                                                             double* __restrict__ part) {
+    __shared__ double ws[GT_ROWS];
+    const int64_t r0 = (int64_t)blockIdx.x * GT_ROWS;
+    const int rows = (int)imin64(GT_ROWS, n - r0);
+    for (int i = threadIdx.x; i < GT_ROWS; i += blockDim.x) ws[i] = i < rows ? w[r0 + i] : 0.0;
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int c = warp; c < ncols; c += 8) {
+        const double* col = B + (int64_t)c * ld + r0;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        if (rows == GT_ROWS) {
+#pragma unroll 4
+            for (int t = lane; t < GT_ROWS; t += 128) {
+                a0 = fma(__ldg(col + t), ws[t], a0);
+                a1 = fma(__ldg(col + t + 32), ws[t + 32], a1);
+                a2 = fma(__ldg(col + t + 64), ws[t + 64], a2);
+                a3 = fma(__ldg(col + t + 96), ws[t + 96], a3);
+            }
+        } else {
+            for (int t = lane; t < rows; t += 32) a0 = fma(__ldg(col + t), ws[t], a0);
+        }
+        double acc = warp_sum((a0 + a1) + (a2 + a3));
+        if (lane == 0) part[blockIdx.x * (int64_t)ncols + c] = acc;
+    }
+}
+
+// h[c] = sum_b part[b * ncols + c] (fixed order), warp per column
+__global__ void reduce_cols_kernel(int64_t nb, int ncols, const double* __restrict__ part,
+                                   double* __restrict__ h) {
+    int c = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    int lane = threadIdx.x & 31;
+    if (c >= ncols) return;
+    double acc = 0.0;
+    for (int64_t b = lane; b < nb; b += 32) acc += part[b * ncols + c];
+    acc = warp_sum(acc);
+    if (lane == 0) h[c] = acc;
+}
+
+// w[r] -= sum_c B[c * ld + r] * h[c]; optional per-block sum of w_new^2
+__global__ void __launch_bounds__(GN_THREADS) gemv_n_update_kernel(int64_t n, int64_t ld, int ncols,
+                                                                   const double* __restrict__ B,
+                                                                   const double* __restrict__ h,
+                                                                   double* __restrict__ w,
+                                                                   double* __restrict__ sq_part) {
+    extern __shared__ double hs[];
+    for (int c = threadIdx.x; c < ncols; c += blockDim.x) hs[c] = h[c];
+    __syncthreads();
+    int64_t r = (int64_t)blockIdx.x * GN_THREADS + threadIdx.x;
+    double v = 0.0;
+    if (r < n) {
+        const double* p = B + r;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int c = 0;
+        for (; c + 4 <= ncols; c += 4) {
+            a0 = fma(__ldg(p + (int64_t)c * ld), hs[c], a0);
+            a1 = fma(__ldg(p + (int64_t)(c + 1) * ld), hs[c + 1], a1);
+            a2 = fma(__ldg(p + (int64_t)(c + 2) * ld), hs[c + 2], a2);
+            a3 = fma(__ldg(p + (int64_t)(c + 3) * ld), hs[c + 3], a3);
+        }
+        for (; c < ncols; ++c) a0 = fma(__ldg(p + (int64_t)c * ld), hs[c], a0);
+        v = w[r] - ((a0 + a1) + (a2 + a3));
+        w[r] = v;
+    }
+    if (sq_part) {
+        __shared__ double red[GN_THREADS / 32];
+        double s = warp_sum(v * v);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int i = 0; i < GN_THREADS / 32; ++i) t += red[i];
+            sq_part[blockIdx.x] = t;
+        }
+    }
+}
+
+// per-block partial sums of x^2 and non-finite detection
+__global__ void sumsq_partial_kernel(int64_t n, const double* __restrict__ x, double* __restrict__ part,
+                                     int* __restrict__ nonfinite) {
+    __shared__ double red[8];
+    int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
+    double v = i < n ? x[i] : 0.0;
+    if (nonfinite && !isfinite(v)) atomicOr(nonfinite, 1);
+    double s = warp_sum(v * v);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int k = 0; k < 8; ++k) t += red[k];
+        part[blockIdx.x] = t;
+    }
+}
+
+// scal[out] = sqrt(sum part) (fixed order)
+__global__ void finish_norm_kernel(int64_t nb, const double* __restrict__ part, double* __restrict__ scal, int out) {
+    __shared__ double red[1024];
+    double a = 0.0;
+    for (int64_t b = threadIdx.x; b < nb; b += blockDim.x) a += part[b];
+    red[threadIdx.x] = a;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if ((int)threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) scal[out] = sqrt(red[0]);
+}
+
+// dst = src / scal[idx]
+__global__ void scale_copy_kernel(int64_t n, const double* __restrict__ src, const double* __restrict__ scal,
+                                  int idx, double* __restrict__ dst) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = src[i] / scal[idx];
+}
+
+// T[j,j] = alpha (= h[j] after the first projection), scal[2] = alpha
+__global__ void commit_alpha_kernel(int64_t m, int64_t j, const double* __restrict__ h,
+                                    double* __restrict__ T, double* __restrict__ scal) {
+    if (threadIdx.x != 0) return;
+    T[j * m + j] = h[j];
+    scal[2] = h[j];
+}
+
+// T[j,j+1] = T[j+1,j] = beta (mode 1) or 0 (mode 0: breakdown, eigen.py:174-176)
+__global__ void set_coupling_kernel(int64_t m, int64_t j, const double* __restrict__ scal,
+                                    double* __restrict__ T, int mode) {
+    if (threadIdx.x != 0) return;
+    double b = mode ? scal[0] : 0.0;
+    T[j * m + j + 1] = b;
+    T[(j + 1) * m + j] = b;
+}
+
+// thick restart of T: diag(theta[:k]) plus (optionally) the arrowhead column
+__global__ void restart_T_kernel(int64_t m, int64_t k, const double* __restrict__ theta,
+                                 const double* __restrict__ S, const double* __restrict__ scal,
+                                 int coupled, double* __restrict__ T) {
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < m * m;
+         idx += (int64_t)gridDim.x * blockDim.x)
+        T[idx] = 0.0;
+    __syncthreads();  // single block launch
+    for (int64_t i = threadIdx.x; i < k; i += blockDim.x) {
+        T[i * m + i] = theta[i];
+        if (coupled) {
+            double cpl = scal[0] * S[i * m + (m - 1)];  // beta * s[m-1, i]
+            T[k * m + i] = cpl;
+            T[i * m + k] = cpl;
+        }
+    }
+}
+
+// gather S[m-1, :k] (last row of the sorted eigenvector block)
+__global__ void last_row_kernel(int64_t m, int64_t k, const double* __restrict__ S, double* __restrict__ out) {
+    for (int64_t i = threadIdx.x; i < k; i += blockDim.x) out[i] = S[i * m + (m - 1)];
+}
+
+// C = A (n x kk, col-major ld lda) * S (kk x kc, col-major ld lds);
+// out col-major (ldc) if rowmajor == 0 else row-major n x kc
+constexpr int GB_M = 64, GB_N = 64, GB_K = 16;
+__global__ void __launch_bounds__(256) dgemm_tall_kernel(int64_t n, int kk, int kc, const double* __restrict__ A,
+                                                         int64_t lda, const double* __restrict__ S, int64_t lds,
+                                                         double* __restrict__ C, int64_t ldc, int rowmajor) {
+    __shared__ double As[GB_K][GB_M + 1];
+    __shared__ double Ss[GB_K][GB_N + 1];
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const int64_t r0 = (int64_t)blockIdx.x * GB_M;
+    const int c0 = blockIdx.y * GB_N;
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    for (int k0 = 0; k0 < kk; k0 += GB_K) {
+        __syncthreads();
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            int idx = tid + 256 * t;
+            // A tile: 16 columns x 64 rows, rows fastest (coalesced)
+            int rr = idx & 63, kq = idx >> 6;
+            int64_t gr = r0 + rr;
+            int gk = k0 + kq;
+            As[kq][rr] = (gr < n && gk < kk) ? A[(int64_t)gk * lda + gr] : 0.0;
+            // S tile: 64 columns x 16 k, k fastest
+            int kq2 = idx & 15, cc = idx >> 4;
+            int gc = c0 + cc, gk2 = k0 + kq2;
+            Ss[kq2][cc] = (gc < kc && gk2 < kk) ? S[(int64_t)gc * lds + gk2] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < GB_K; ++q) {
+            double a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = As[q][ty + 16 * i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = Ss[q][tx + 16 * j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        int64_t r = r0 + ty + 16 * i;
+        if (r >= n) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            int c = c0 + tx + 16 * j;
+            if (c >= kc) continue;
+            if (rowmajor) C[r * kc + c] = acc[i][j];
+            else C[(int64_t)c * ldc + r] = acc[i][j];
+        }
+    }
+}
+
+// copy n x k col-major (ld) block between two buffers with the same ld
+__global__ void copy_cols_kernel(int64_t n, int64_t k, int64_t ld, const double* __restrict__ src,
+                                 double* __restrict__ dst) {
+    int64_t total = k * ld;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x)
+        if ((i % ld) < n) dst[i] = src[i];
+}
+
+// per-block column sums of squares of a row-major n x k matrix
+constexpr int CN_ROWS = 256;
+__global__ void colsq_partial_kernel(int64_t n, int64_t k, const double* __restrict__ V, double* __restrict__ part) {
+    int64_t r0 = (int64_t)blockIdx.x * CN_ROWS, r1 = imin64(n, r0 + CN_ROWS);
+    for (int64_t c = threadIdx.x; c < k; c += blockDim.x) {
+        double a = 0.0;
+        for (int64_t r = r0; r < r1; ++r) a = fma(V[r * k + c], V[r * k + c], a);
+        part[blockIdx.x * k + c] = a;
+    }
+}
+__global__ void colnorm_finish_kernel(int64_t nb, int64_t k, const double* __restrict__ part,
+                                      double* __restrict__ norms) {
+    int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= k) return;
+    double a = 0.0;
+    for (int64_t b = 0; b < nb; ++b) a += part[b * k + c];
+    norms[c] = sqrt(a);
+}
+__global__ void scale_cols_rowmajor_kernel(int64_t n, int64_t k, const double* __restrict__ norms, double* __restrict__ V) {
+    int64_t total = n * k;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x)
+        V[i] = V[i] / norms[i % k];
+}
+
+// residual partials: R[i, c] = (A V)[i, c] - theta_c V[i, c]; part[b, c] = sum_i R^2
+constexpr int RS_ROWS = 64;
+__global__ void residual_partial_kernel(int64_t n, int64_t k, const int64_t* __restrict__ row_ptr,
+                                        const int32_t* __restrict__ col, const double* __restrict__ vals,
+                                        const double* __restrict__ V, const double* __restrict__ theta,
+                                        double* __restrict__ part) {
+    // block: 256 threads = 8 warps; rows [r0, r0 + RS_ROWS); columns chunked by 32
+    __shared__ double red[8][32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t r0 = (int64_t)blockIdx.x * RS_ROWS;
+    for (int64_t c0 = 0; c0 < k; c0 += 32) {
+        int64_t c = c0 + lane;
+        double acc2 = 0.0;
+        for (int64_t r = r0 + warp; r < imin64(n, r0 + RS_ROWS); r += 8) {
+            double a = 0.0;
+            if (c < k) {
+                for (int64_t p = row_ptr[r]; p < row_ptr[r + 1]; ++p) a = fma(vals[p], V[(int64_t)col[p] * k + c], a);
+                double res = a - theta[c] * V[r * k + c];
+                acc2 = fma(res, res, acc2);
+            }
+        }
+        red[warp][lane] = acc2;
+        __syncthreads();
+        if (warp == 0 && c < k) {
+            double t = 0.0;
+            for (int q = 0; q < 8; ++q) t += red[q][lane];
+            part[blockIdx.x * k + c] = t;
+        }
+        __syncthreads();
+    }
+}
+
+// max |v| as ordered bits of a non-negative double
+__global__ void absmax_kernel(int64_t m, const double* __restrict__ v, unsigned long long* __restrict__ out) {
+    double a = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        a = fmax(a, fabs(v[i]));
+    for (int o = 16; o > 0; o >>= 1) a = fmax(a, __shfl_xor_sync(0xffffffffu, a, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(a));
+}
+
+// per-block partial of x.ay - y.ax (symmetry probe)
+__global__ void dot_partial_kernel(int64_t n, const double* __restrict__ x, const double* __restrict__ ay,
+                                   const double* __restrict__ y, const double* __restrict__ ax,
+                                   double* __restrict__ part) {
+    __shared__ double red[8];
+    int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
+    double v = i < n ? (x[i] * ay[i] - y[i] * ax[i]) : 0.0;
+    double s = warp_sum(v);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int q = 0; q < 8; ++q) t += red[q];
+        part[blockIdx.x] = t;
+    }
+}
+
+__global__ void finish_sum_kernel(int64_t nb, const double* __restrict__ part, double* __restrict__ out, int idx) {
+    __shared__ double red[1024];
+    double a = 0.0;
+    for (int64_t b = threadIdx.x; b < nb; b += blockDim.x) a += part[b];
+    red[threadIdx.x] = a;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if ((int)threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[idx] = red[0];
+}
+
+}  // namespace sc
+
+using namespace sc;
+
+// ---------------------------------------------------------------------------
+struct sc_lanczos {
+    int64_t n = 0, k = 0, m = 0, ld = 0, max_restarts = 0;
+    double tol = 0.0;
+    uint64_t seed = 0;
+    cudaStream_t st = nullptr;
+    int state = 0;  // 0 need_matvec, 1 converged, 2 failed
+    int64_t j = 0;
+    int64_t restarts = 0, breakdowns = 0, matvecs = 0;
+    uint64_t rng_stream = 0;
+    double scale = 0.0;
+    std::vector<double> history, pending, theta_k, est_k;
+    bool has_pending = false;
+
+    DevBuf<double> B, T, w, part, h, sqp, scal, Y, A, Z, wraw, wsort, S, lastrow, vectors;
+    DevBuf<int> info, nonfinite;
+    int64_t nb_t = 0, nb_n = 0;
+
+    // ---- building blocks
+    int project(const double* x, int ncols, bool fused_norm_unused = false) {
+        (void)fused_norm_unused;
+        gemv_t_partial_kernel<<<(unsigned)nb_t, 256, 0, st>>>(n, ld, ncols, B.p, x, part.p);
+        reduce_cols_kernel<<<(unsigned)ceil_div((int64_t)ncols * 32, 256), 256, 0, st>>>(nb_t, ncols, part.p, h.p);
+        SC_LAUNCHED(2);
+        return SC_OK;
+    }
+    int subtract(double* x, int ncols, bool with_norm) {
+        gemv_n_update_kernel<<<(unsigned)nb_n, GN_THREADS, sizeof(double) * (size_t)ncols, st>>>(
+            n, ld, ncols, B.p, h.p, x, with_norm ? sqp.p : nullptr);
+        SC_LAUNCHED(1);
+        return SC_OK;
+    }
+    // two CGS passes against the first `count` basis vectors; scal[0] = |x|
+    int cgs2(double* x, int count) {
+        double bytes = 4.0 * (double)n * count * 8.0;
+        ProfScope prof("reorth", st, bytes);
+        int rc;
+        if (count == 0) {
+            sumsq_partial_kernel<<<(unsigned)nb_n, 256, 0, st>>>(n, x, sqp.p, nullptr);
+            SC_LAUNCHED(1);
+        } else {
+            if ((rc = project(x, count)) || (rc = subtract(x, count, false))) return rc;
+            if ((rc = project(x, count)) || (rc = subtract(x, count, true))) return rc;
+        }
+        finish_norm_kernel<<<1, 1024, 0, st>>>(nb_n, sqp.p, scal.p, 0);
+        SC_LAUNCHED(1);
+        return SC_OK;
+    }
+    double read_scal(int idx) {
+        double v = 0.0;
+        cudaMemcpyAsync(&v, scal.p + idx, sizeof(double), cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        return v;
+    }
+    // unit vector orthogonal to B[:, :count] into column `dst` (eigen.py:137-150)
+    int fresh(int64_t count, int64_t dst, bool is_breakdown) {
+        for (int attempt = 0; attempt < 3; ++attempt) {
+            double* x = B.p + dst * ld;
+            fill_normal_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, seed, ++rng_stream, x);
+            SC_LAUNCHED(1);
+            // the first `count` columns are the basis; CGS2 against them
+            // (x lives in column dst >= count, so it is not projected on itself)
+            int rc = cgs2(x, (int)count);
+            if (rc) return rc;
+            double nv = read_scal(0);
+            if (nv > 1e-6 * std::sqrt((double)n)) {
+                if (is_breakdown) ++breakdowns;
+                scale_copy_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, x, scal.p, 0, x);
+                SC_LAUNCHED(1);
+                return SC_OK;
+            }
+        }
+        state = 2;
+        return fail(SC_ERR_BREAKDOWN, "could not extend the basis past " + std::to_string(count) + " vectors");
+    }
+
+    int init(int64_t n_, int64_t k_, int64_t m_, double tol_, int64_t maxr, uint64_t seed_, cudaStream_t st_) {
+        n = n_;
+        k = k_;
+        m = m_ > 0 ? m_ : imin64(n_, std::max<int64_t>(2 * k_, k_ + 8));  // eigen.py:53-55
+        if (!(1 <= k && k < m && m <= n))
+            return fail(SC_ERR_VALUE, "need 1 <= k < m <= n, got k=" + std::to_string(k) + ", m=" +
+                                          std::to_string(m) + ", n=" + std::to_string(n));
+        if (!(tol_ > 0)) return fail(SC_ERR_VALUE, "tol must be positive");
+        if (maxr < 0) return fail(SC_ERR_VALUE, "max_restarts must be nonnegative");
+        tol = tol_;
+        max_restarts = maxr;
+        seed = seed_;
+        st = st_;
+        ld = (n + 31) / 32 * 32;
+        nb_t = ceil_div(n, GT_ROWS);
+        nb_n = ceil_div(n, GN_THREADS);
+        int rc;
+        if ((rc = B.alloc((size_t)ld * (m + 1))) || (rc = T.alloc((size_t)m * m)) || (rc = w.alloc(ld)) ||
+            (rc = part.alloc((size_t)nb_t * (m + 1))) || (rc = h.alloc(m + 1)) || (rc = sqp.alloc(nb_n)) ||
+            (rc = scal.alloc(8)) || (rc = A.alloc((size_t)m * m)) || (rc = Z.alloc((size_t)m * m)) ||
+            (rc = wraw.alloc(m)) || (rc = wsort.alloc(m)) || (rc = S.alloc((size_t)m * k)) ||
+            (rc = lastrow.alloc(k)) || (rc = info.alloc(1)) || (rc = nonfinite.alloc(1)))
+            return rc;
+        SC_CUDA(cudaMemsetAsync(T.p, 0, sizeof(double) * m * m, st));
+        SC_CUDA(cudaMemsetAsync(w.p, 0, sizeof(double) * ld, st));
+        // start vector: normal draws, normalised (eigen.py:113-115)
+        double* q0 = B.p;
+        fill_normal_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, seed, 0, q0);
+        SC_LAUNCHED(1);
+        if ((rc = cgs2(q0, 0))) return rc;
+        scale_copy_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, q0, scal.p, 0, q0);
+        SC_LAUNCHED(1);
+        j = 0;
+        state = 0;
+        SC_CUDA(cudaStreamSynchronize(st));
+        return SC_OK;
+    }
+
+    const double* in_slot() const { return B.p + j * ld; }
+
+    // one Lanczos step on w = A q_j (eigen.py:152-179)
+    int advance(bool check_finite) {
+        if (state != 0) return fail(SC_ERR_STATE, "advance called in a finished session");
+        ++matvecs;
+        int rc;
+        if (check_finite) {
+            SC_CUDA(cudaMemsetAsync(nonfinite.p, 0, sizeof(int), st));
+            sumsq_partial_kernel<<<(unsigned)nb_n, 256, 0, st>>>(n, w.p, sqp.p, nonfinite.p);
+            SC_LAUNCHED(1);
+            int bad = 0;
+            SC_CUDA(cudaMemcpyAsync(&bad, nonfinite.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+            SC_CUDA(cudaStreamSynchronize(st));
+            if (bad) return fail(SC_ERR_VALUE, "out_slot contains non-finite values");
+        }
+        const int cnt = (int)(j + 1);
+        {
+            ProfScope prof("reorth", st, 4.0 * (double)n * cnt * 8.0);
+            if ((rc = project(w.p, cnt))) return rc;  // h[j] = alpha = q_j^T w
+            // keep alpha before the second pass overwrites h
+            commit_alpha_kernel<<<1, 32, 0, st>>>(m, j, h.p, T.p, scal.p);
+            SC_LAUNCHED(1);
+            if ((rc = subtract(w.p, cnt, false))) return rc;
+            if ((rc = project(w.p, cnt)) || (rc = subtract(w.p, cnt, true))) return rc;
+        }
+        finish_norm_kernel<<<1, 1024, 0, st>>>(nb_n, sqp.p, scal.p, 0);
+        SC_LAUNCHED(1);
+        double ab[3];
+        SC_CUDA(cudaMemcpyAsync(ab, scal.p, sizeof(double) * 3, cudaMemcpyDeviceToHost, st));
+        SC_CUDA(cudaStreamSynchronize(st));
+        const double beta = ab[0], alpha = ab[2];
+        scale = std::max(scale, std::max(std::fabs(alpha), beta));
+        if (j + 1 == m) return finish_sweep(beta);
+        double* next = B.p + (j + 1) * ld;
+        if (beta > kBreakdownRtol * std::max(1.0, scale)) {
+            set_coupling_kernel<<<1, 32, 0, st>>>(m, j, scal.p, T.p, 1);
+            scale_copy_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, w.p, scal.p, 0, next);
+            SC_LAUNCHED(2);
+        } else {
+            set_coupling_kernel<<<1, 32, 0, st>>>(m, j, scal.p, T.p, 0);
+            SC_LAUNCHED(1);
+            if ((rc = fresh(j + 1, j + 1, true))) return rc;
+        }
+        ++j;
+        return SC_OK;
+    }
+    // Y = B[:, :m] S[:, :k]
+    int ritz(double* out, int64_t ldc, int rowmajor) {
+        dim3 grid((unsigned)ceil_div(n, GB_M), (unsigned)ceil_div(k, GB_N));
+        ProfScope prof("ritz", st, 2.0 * (double)n * m * k);
+        dgemm_tall_kernel<<<grid, 256, 0, st>>>(n, (int)m, (int)k, B.p, ld, S.p, m, out, ldc, rowmajor);
+        SC_LAUNCHED(1);
+        return SC_OK;
+    }
+
+    // eigen.py:187-239
+    int finish_sweep(double beta) {
+        int rc;
+        SC_CUDA(cudaMemcpyAsync(A.p, T.p, sizeof(double) * m * m, cudaMemcpyDeviceToDevice, st));
+        if ((rc = symeig_launch((int)m, (int)k, A.p, Z.p, wraw.p, wsort.p, S.p, info.p, st))) return rc;
+        last_row_kernel<<<1, 256, 0, st>>>(m, k, S.p, lastrow.p);
+        SC_LAUNCHED(1);
+        theta_k.assign(k, 0.0);
+        std::vector<double> lr(k);
+        int hinfo = 0;
+        SC_CUDA(cudaMemcpyAsync(theta_k.data(), wsort.p, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
+        SC_CUDA(cudaMemcpyAsync(lr.data(), lastrow.p, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
+        SC_CUDA(cudaMemcpyAsync(&hinfo, info.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+        SC_CUDA(cudaStreamSynchronize(st));
+        if (hinfo) {
+            state = 2;
+            return fail(SC_ERR_INTERNAL, "projected eigenproblem: QL did not converge");
+        }
+        est_k.assign(k, 0.0);
+        double worst = 0.0;
+        bool converged = true;
+        for (int64_t i = 0; i < k; ++i) {
+            est_k[i] = beta * std::fabs(lr[i]);
+            worst = std::max(worst, est_k[i]);
+            if (!(est_k[i] <= tol * std::max(1.0, std::fabs(theta_k[i])))) converged = false;
+        }
+        history.push_back(worst);
+        bool verified = false;
+        if (has_pending) {
+            verified = true;
+            for (int64_t i = 0; i < k; ++i) {
+                double slack = std::max(1.0, std::fabs(theta_k[i])) * std::max(tol, 1e-12);
+                if (!(std::fabs(theta_k[i] - pending[i]) <= slack)) verified = false;
+            }
+        }
+        if (converged && (m == n || verified)) {
+            if ((rc = vectors.alloc((size_t)n * k))) return rc;
+            if ((rc = ritz(vectors.p, k, 1))) return rc;
+            if ((rc = normalize_vectors())) return rc;
+            state = 1;
+            return SC_OK;
+        }
+        if (restarts >= max_restarts) {
+            state = 2;
+            char buf[160];
+            snprintf(buf, sizeof(buf), "%lld restarts without verified convergence; worst residual estimate %.3e",
+                     (long long)restarts, worst);
+            return fail(SC_ERR_MAX_RESTARTS, buf);
+        }
+        ++restarts;
+        if (!Y.p) {
+            if ((rc = Y.alloc((size_t)ld * k))) return rc;
+        }
+        if ((rc = ritz(Y.p, ld, 0))) return rc;
+        copy_cols_kernel<<<4 * kNumSMs, 256, 0, st>>>(n, k, ld, Y.p, B.p);
+        SC_LAUNCHED(1);
+        const bool coupled = !converged && beta > kBreakdownRtol * std::max(1.0, scale);
+        restart_T_kernel<<<1, 1024, 0, st>>>(m, k, wsort.p, S.p, scal.p, coupled ? 1 : 0, T.p);
+        SC_LAUNCHED(1);
+        if (converged) {
+            pending = theta_k;
+            has_pending = true;
+            if ((rc = fresh(k, k, false))) return rc;
+        } else {
+            has_pending = false;
+            if (coupled) {
+                scale_copy_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, w.p, scal.p, 0, B.p + k * ld);
+                SC_LAUNCHED(1);
+            } else {
+                if ((rc = fresh(k, k, true))) return rc;
+            }
+        }
+        j = k;
+        return SC_OK;
+    }
+
+    int normalize_vectors() {
+        int64_t nb = ceil_div(n, CN_ROWS);
+        DevBuf<double> p, nr;
+        int rc;
+        if ((rc = p.alloc((size_t)nb * k)) || (rc = nr.alloc(k))) return rc;
+        colsq_partial_kernel<<<(unsigned)nb, 256, 0, st>>>(n, k, vectors.p, p.p);
+        colnorm_finish_kernel<<<(unsigned)ceil_div(k, 128), 128, 0, st>>>(nb, k, p.p, nr.p);
+        scale_cols_rowmajor_kernel<<<4 * kNumSMs, 256, 0, st>>>(n, k, nr.p, vectors.p);
+        SC_LAUNCHED(3);
+        SC_CUDA(cudaStreamSynchronize(st));
+        return SC_OK;
+    }
+};
+
+static int residuals_launch(int64_t n, int64_t k, const int64_t* row_ptr, const int32_t* col, const double* vals,
+                            const double* V, const double* theta_dev, double* res_host, cudaStream_t st) {
+    int64_t nb = ceil_div(n, RS_ROWS);
+    DevBuf<double> p, nr;
+    int rc;
+    if ((rc = p.alloc((size_t)nb * k)) || (rc = nr.alloc(k))) return rc;
+    residual_partial_kernel<<<(unsigned)nb, 256, 0, st>>>(n, k, row_ptr, col, vals, V, theta_dev, p.p);
+    colnorm_finish_kernel<<<(unsigned)ceil_div(k, 128), 128, 0, st>>>(nb, k, p.p, nr.p);
+    SC_LAUNCHED(2);
+    SC_CUDA(cudaMemcpyAsync(res_host, nr.p, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
+    SC_CUDA(cudaStreamSynchronize(st));
+    return SC_OK;
+}
+
+extern "C" {
+
+int sc_lanczos_create(int64_t n, int64_t k, int64_t m, double tol, int64_t max_restarts, uint64_t seed,
+                      sc_stream_t stream, sc_lanczos_t** out) {
+    auto* s = new sc_lanczos();
+    int rc = s->init(n, k, m, tol, max_restarts, seed, as_stream(stream));
+    if (rc) {
+        delete s;
+        return rc;
+    }
+    *out = s;
+    return SC_OK;
+}
+
+void sc_lanczos_destroy(sc_lanczos_t* s) { delete s; }
+int sc_lanczos_state(const sc_lanczos_t* s) { return s->state; }
+const double* sc_lanczos_in_slot(const sc_lanczos_t* s) { return s->in_slot(); }
+double* sc_lanczos_out_slot(sc_lanczos_t* s) { return s->w.p; }
+
+int sc_lanczos_advance(sc_lanczos_t* s) {
+    int rc = s->advance(true);
+    if (rc && rc != SC_ERR_VALUE && rc != SC_ERR_STATE) s->state = 2;
+    return rc;
+}
+
+int sc_lanczos_get_stats(const sc_lanczos_t* s, sc_lanczos_stats* st) {
+    st->restarts = s->restarts;
+    st->breakdowns = s->breakdowns;
+    st->matvecs = s->matvecs;
+    st->n_history = (int64_t)std::min<size_t>(s->history.size(), 512);
+    for (int64_t i = 0; i < st->n_history; ++i) st->history[i] = s->history[i];
+    return SC_OK;
+}
+
+int sc_lanczos_ritz(const sc_lanczos_t* s, double* values, double* estimates) {
+    if (s->theta_k.empty()) return fail(SC_ERR_NOT_CONVERGED, "no completed sweep");
+    for (int64_t i = 0; i < s->k; ++i) {
+        values[i] = s->theta_k[i];
+        estimates[i] = s->est_k[i];
+    }
+    return SC_OK;
+}
+
+int sc_lanczos_extract(sc_lanczos_t* s, double* values, double* vectors) {
+    if (s->state != 1) return fail(SC_ERR_NOT_CONVERGED, "extract called before convergence");
+    for (int64_t i = 0; i < s->k; ++i) values[i] = s->theta_k[i];
+    SC_CUDA(cudaMemcpyAsync(vectors, s->vectors.p, sizeof(double) * s->n * s->k, cudaMemcpyDeviceToDevice, s->st));
+    SC_CUDA(cudaStreamSynchronize(s->st));
+    return SC_OK;
+}
+
+int sc_eigensolve_csr(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* vals, int64_t k,
+                      int64_t m, double tol, int64_t max_restarts, uint64_t seed, double* values, double* vectors,
+                      double* residuals, sc_lanczos_stats* stats, sc_stream_t stream) {
+    cudaStream_t st = as_stream(stream);
+    sc_lanczos s;
+    int rc = s.init(n, k, m, tol, max_restarts, seed, st);
+    if (rc) return rc;
+    int64_t nnz = 0;
+    SC_CUDA(cudaMemcpyAsync(&nnz, row_ptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    SC_CUDA(cudaStreamSynchronize(st));
+    while (s.state == 0) {
+        if ((rc = spmv_launch(n, nnz, row_ptr, col, vals, s.in_slot(), s.w.p, false, st))) return rc;
+        rc = s.advance(false);
+        if (rc) {
+            if (stats) sc_lanczos_get_stats(&s, stats);
+            if (rc == SC_ERR_MAX_RESTARTS) {
+                for (int64_t i = 0; i < k; ++i) {
+                    values[i] = s.theta_k[i];
+                    residuals[i] = s.est_k[i];
+                }
+            }
+            return rc;
+        }
+    }
+    for (int64_t i = 0; i < k; ++i) values[i] = s.theta_k[i];
+    SC_CUDA(cudaMemcpyAsync(vectors, s.vectors.p, sizeof(double) * n * k, cudaMemcpyDeviceToDevice, st));
+    // true residuals |A v - theta v| (eigen.py:241-248)
+    if ((rc = residuals_launch(n, k, row_ptr, col, vals, vectors, s.wsort.p, residuals, st))) return rc;
+    if (stats) sc_lanczos_get_stats(&s, stats);
+    return SC_OK;
+}
+
+int sc_symmetry_probe(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* vals,
+                      uint64_t seed, double* ratio_out, sc_stream_t stream) {
+    // eigen.py:279-288: three random (x, y) pairs; ratio = |x'Ay - y'Ax| / (|x| |y|)
+    // (the caller multiplies the tolerance by max(1, max|a|))
+    cudaStream_t st = as_stream(stream);
+    *ratio_out = 0.0;
+    if (n <= 0) return SC_OK;
+    int64_t nnz = 0;
+    SC_CUDA(cudaMemcpyAsync(&nnz, row_ptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    SC_CUDA(cudaStreamSynchronize(st));
+    DevBuf<double> x, y, ax, ay, part, out;
+    int64_t nb = ceil_div(n, 256);
+    int rc;
+    if ((rc = x.alloc(n)) || (rc = y.alloc(n)) || (rc = ax.alloc(n)) || (rc = ay.alloc(n)) ||
+        (rc = part.alloc(nb)) || (rc = out.alloc(4)))
+        return rc;
+    double worst = 0.0;
+    for (int t = 0; t < 3; ++t) {
+        uint64_t sid = (1ull << 40) + 2 * (uint64_t)t;
+        fill_normal_kernel<<<(unsigned)nb, 256, 0, st>>>(n, seed, sid, x.p);
+        fill_normal_kernel<<<(unsigned)nb, 256, 0, st>>>(n, seed, sid + 1, y.p);
+        SC_LAUNCHED(2);
+        if ((rc = spmv_launch(n, nnz, row_ptr, col, vals, y.p, ay.p, false, st))) return rc;
+        if ((rc = spmv_launch(n, nnz, row_ptr, col, vals, x.p, ax.p, false, st))) return rc;
+        dot_partial_kernel<<<(unsigned)nb, 256, 0, st>>>(n, x.p, ay.p, y.p, ax.p, part.p);
+        finish_sum_kernel<<<1, 1024, 0, st>>>(nb, part.p, out.p, 0);
+        sumsq_partial_kernel<<<(unsigned)nb, 256, 0, st>>>(n, x.p, part.p, nullptr);
+        finish_norm_kernel<<<1, 1024, 0, st>>>(nb, part.p, out.p, 1);
+        sumsq_partial_kernel<<<(unsigned)nb, 256, 0, st>>>(n, y.p, part.p, nullptr);
+        finish_norm_kernel<<<1, 1024, 0, st>>>(nb, part.p, out.p, 2);
+        SC_LAUNCHED(6);
+        double h[3];
+        SC_CUDA(cudaMemcpyAsync(h, out.p, sizeof(double) * 3, cudaMemcpyDeviceToHost, st));
+        SC_CUDA(cudaStreamSynchronize(st));
+        double denom = h[1] * h[2];
+        double r = denom > 0 ? std::fabs(h[0]) / denom : 0.0;
+        worst = std::max(worst, r);
+    }
+    // scale by max(1, max|a|) (eigen.py:282, 285)
+    DevBuf<unsigned long long> vmax;
+    if ((rc = vmax.alloc(1))) return rc;
+    SC_CUDA(cudaMemsetAsync(vmax.p, 0, sizeof(unsigned long long), st));
+    if (nnz > 0) {
+        absmax_kernel<<<(unsigned)std::min<int64_t>(ceil_div(nnz, 256), 4 * kNumSMs), 256, 0, st>>>(nnz, vals, vmax.p);
+        SC_LAUNCHED(1);
+    }
+    unsigned long long vb = 0;
+    SC_CUDA(cudaMemcpyAsync(&vb, vmax.p, sizeof(vb), cudaMemcpyDeviceToHost, st));
+    SC_CUDA(cudaStreamSynchronize(st));
+    double vm;
+    std::memcpy(&vm, &vb, sizeof(vm));
+    *ratio_out = worst / std::max(1.0, vm);
+    return SC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,206 @@
+"""Similarity-graph construction (drop-in for speclust.graph).
+
+The north-star pattern — union kNN with the Gaussian ``exp_decay`` measure —
+runs entirely on the GPU (``sc_knn_graph_f64``): low-precision distance
+tiles with a streaming per-row top-R list, an exact fp64 recheck certified by
+an error bound, an exact fallback for uncertified rows, and union
+symmetrisation written straight into CSR.  The ranking key and edge values
+follow graph.py:149-157 / 136-141 of the reference.
+
+Other measures (cosine, cross-correlation) and the eps / threshold patterns
+are outside this round's hot-path scope and raise
+``NotImplementedError`` instead of silently running on the host.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as nat
+from .errors import DegenerateVector, DimensionMismatch, InvalidFormat
+from .sparse import CooMatrix, DeviceCsr, coo_canonicalize
+
+__all__ = [
+    "SimilarityMeasure",
+    "similarity",
+    "build_edges_eps",
+    "build_edges_knn",
+    "build_edges_threshold",
+    "build_similarity",
+    "validate_edges",
+    "knn_graph_device",
+]
+
+MEASURE_KINDS = ("cosine", "cross_correlation", "exp_decay")
+NEGATIVE_POLICIES = ("clamp_zero", "abs", "keep")
+
+
+@dataclass(frozen=True)
+class SimilarityMeasure:
+    """Measure selector; ``sigma`` is the Gaussian width of exp_decay
+    (reference graph.py:32-57)."""
+
+    kind: str
+    sigma: float | None = None
+
+    def __post_init__(self):
+        if self.kind not in MEASURE_KINDS:
+            raise ValueError(f"unknown measure kind {self.kind!r}")
+        if self.kind == "exp_decay" and (self.sigma is None or not self.sigma > 0):
+            raise ValueError("exp_decay requires sigma > 0")
+
+    @classmethod
+    def cosine(cls) -> "SimilarityMeasure":
+        return cls("cosine")
+
+    @classmethod
+    def cross_correlation(cls) -> "SimilarityMeasure":
+        return cls("cross_correlation")
+
+    @classmethod
+    def exp_decay(cls, sigma: float) -> "SimilarityMeasure":
+        return cls("exp_decay", sigma)
+
+    def two_sigma_sq(self) -> float:
+        # evaluated exactly as the reference writes it: 2.0 * sigma**2
+        return 2.0 * self.sigma**2
+
+
+def as_points(x) -> np.ndarray:
+    a = np.ascontiguousarray(x, dtype=np.float64)
+    if a.ndim != 2 or a.shape[0] < 1 or a.shape[1] < 1:
+        raise InvalidFormat("point matrix must be 2-D with n >= 1, d >= 1")
+    if not np.isfinite(a).all():
+        raise InvalidFormat("point matrix must be finite")
+    return a
+
+
+def validate_edges(pairs, n: int) -> np.ndarray:
+    """(m, 2) int64 edge list without self-loops, out-of-range indices or
+    repeated unordered pairs (reference graph.py:70-84)."""
+    e = np.asarray(pairs, dtype=np.int64).reshape(-1, 2)
+    if len(e):
+        if e.min() < 0 or e.max() >= n:
+            raise InvalidFormat("edge index out of range")
+        if (e[:, 0] == e[:, 1]).any():
+            raise InvalidFormat("edge list contains a self-loop")
+        key = np.minimum(e[:, 0], e[:, 1]) * n + np.maximum(e[:, 0], e[:, 1])
+        if len(np.unique(key)) != len(key):
+            raise InvalidFormat("edge list contains a duplicate unordered pair")
+    return e
+
+
+def similarity(x_i, x_j, m: SimilarityMeasure) -> float:
+    """Scalar similarity of two vectors (reference graph.py:107-133); a
+    convenience helper, not part of the device path."""
+    a = np.asarray(x_i, dtype=np.float64)
+    b = np.asarray(x_j, dtype=np.float64)
+    if a.ndim != 1 or a.shape != b.shape:
+        raise DimensionMismatch(f"vectors must be 1-D of equal length, got {a.shape} and {b.shape}")
+    if a.shape[0] < 1:
+        raise DimensionMismatch("vectors must have d >= 1")
+    if m.kind == "exp_decay":
+        return float(np.exp(-float(np.sum((a - b) ** 2)) / m.two_sigma_sq()))
+    if m.kind == "cross_correlation":
+        a, b = a - a.mean(), b - b.mean()
+    sa, sb = float(a @ a), float(b @ b)
+    for s, side in ((sa, "left"), (sb, "right")):
+        if s == 0.0:
+            raise DegenerateVector(f"{side} vector is degenerate for {m.kind}", index=None)
+    return float(np.clip((a @ b) / np.sqrt(sa * sb), -1.0, 1.0))
+
+
+def _require_exp_decay(m: SimilarityMeasure, what: str):
+    if m.kind != "exp_decay":
+        raise NotImplementedError(
+            f"{what} with measure {m.kind!r} is not on the device path this round "
+            "(SURVEY.md §8(f) F3); only exp_decay is implemented"
+        )
+
+
+def knn_graph_device(x, knn: int, m: SimilarityMeasure, return_stats: bool = False):
+    """Union-kNN exp_decay similarity matrix W as a DeviceCsr, built on the
+    GPU in one call (graph.py:185-237 + sparse.py:182-187 fused).
+
+    ``x`` may be a numpy array or a CUDA float64 tensor (n x d)."""
+    _require_exp_decay(m, "knn graph")
+    torch = nat.torch_cuda()
+    if isinstance(x, torch.Tensor):
+        xd = x.to(dtype=torch.float64).contiguous()
+        n, d = xd.shape
+    else:
+        xh = as_points(x)
+        n, d = xh.shape
+        xd = nat.to_device(xh, torch.float64)
+    if not 1 <= knn < n:
+        raise ValueError(f"knn must satisfy 1 <= knn < n, got {knn} for n={n}")
+    cap = 2 * n * knn
+    row_ptr = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+    col = torch.empty(cap, dtype=torch.int32, device="cuda")
+    vals = torch.empty(cap, dtype=torch.float64, device="cuda")
+    nnz = nat.C.c_int64(0)
+    stats = (nat.C.c_int64 * 8)()
+    lib = nat.load()
+    nat.check(lib.sc_knn_graph_f64(n, d, nat.ptr(xd), knn, m.two_sigma_sq(), nat.ptr(row_ptr), nat.ptr(col),
+                                   nat.ptr(vals), nat.C.byref(nnz), stats, nat.stream_handle()))
+    k = nnz.value
+    w = DeviceCsr(n, n, row_ptr, col[:k], vals[:k])
+    if return_stats:
+        keys = ("list_R", "list_cap", "fallback_rows", "nnz")
+        return w, {key: int(stats[i]) for i, key in enumerate(keys)}
+    return w
+
+
+def build_edges_knn(x, knn: int, m: SimilarityMeasure) -> np.ndarray:
+    """Union kNN pattern as (i, j) pairs with i < j in row-major order
+    (reference graph.py:185-204), computed on the GPU."""
+    x = as_points(x)
+    n = x.shape[0]
+    if not 1 <= knn < n:
+        raise ValueError(f"knn must satisfy 1 <= knn < n, got {knn} for n={n}")
+    _require_exp_decay(m, "build_edges_knn")
+    w = knn_graph_device(x, knn, m)
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(nat.to_host(w.row_ptr)))
+    cols = nat.to_host(w.col, np.int64)
+    upper = cols > rows
+    return np.column_stack((rows[upper], cols[upper]))
+
+
+def build_edges_eps(x, eps: float) -> np.ndarray:
+    raise NotImplementedError("eps-graph pattern is out of this round's device scope (SURVEY.md §8(f) F3)")
+
+
+def build_edges_threshold(x, lam: float, m: SimilarityMeasure) -> np.ndarray:
+    raise NotImplementedError("threshold pattern is out of this round's device scope (SURVEY.md §8(f) F3)")
+
+
+def build_similarity(x, e, m: SimilarityMeasure, negative_policy: str = "clamp_zero") -> CooMatrix:
+    """Symmetric similarity matrix over a given edge pattern: one value per
+    unordered pair, mirrored (reference graph.py:214-237).  Values are
+    computed on the GPU."""
+    x = as_points(x)
+    n = x.shape[0]
+    e = validate_edges(e, n)
+    if negative_policy not in NEGATIVE_POLICIES:
+        raise ValueError(f"unknown negative_policy {negative_policy!r}")
+    _require_exp_decay(m, "build_similarity")
+    vals = _pair_weights(x, e, m)
+    # exp >= 0: clamp_zero / abs / keep are all identities (graph.py:230-233)
+    rows = np.concatenate((e[:, 0], e[:, 1]))
+    cols = np.concatenate((e[:, 1], e[:, 0]))
+    return coo_canonicalize(CooMatrix(n, n, rows, cols, np.concatenate((vals, vals))), dup_policy="error")
+
+
+def _pair_weights(x: np.ndarray, e: np.ndarray, m: SimilarityMeasure) -> np.ndarray:
+    torch = nat.torch_cuda()
+    if len(e) == 0:
+        return np.zeros(0)
+    xd = nat.to_device(x, torch.float64)
+    ed = nat.to_device(e.astype(np.int64), torch.int64)
+    out = torch.empty(len(e), dtype=torch.float64, device="cuda")
+    lib = nat.load()
+    nat.check(lib.sc_pair_weights(x.shape[0], x.shape[1], nat.ptr(xd), len(e), nat.ptr(ed), m.two_sigma_sq(),
+                                  nat.ptr(out), nat.stream_handle()))
+    return nat.to_host(out)

@@ -1,0 +1,338 @@
+"""GPU parity tests of the individual device operators against the golden
+vectors of the real reference (tests/golden) and the CPU oracle."""
+
+import numpy as np
+import pytest
+
+import paper_1802_04450_b200 as sc
+from oracle import speclust_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+def csr(rp, col, vals):
+    n = len(rp) - 1
+    return sc.CsrMatrix(n, n, rp, col, vals)
+
+
+def dense(m):
+    out = np.zeros((m.n_rows, m.n_cols))
+    out[m.row_indices(), m.col_idx] = m.vals
+    return out
+
+
+# ---------------------------------------------------------------- sparse
+def test_spmv_bit_exact_vs_reference(golden):
+    g = golden("spmv_cases")
+    for t in range(int(g["ncases"])):
+        m = csr(g[f"c{t}_row_ptr"], g[f"c{t}_col"], g[f"c{t}_vals"])
+        y = sc.spmv(m, g[f"c{t}_x"])
+        assert np.array_equal(y, g[f"c{t}_y"]), t
+
+
+def test_spmv_known_answers():
+    eye = sc.coo_to_csr(sc.CooMatrix(3, 3, [0, 1, 2], [0, 1, 2], [1.0, 1.0, 1.0]))
+    assert np.array_equal(sc.spmv(eye, [1.0, 2.0, 3.0]), [1.0, 2.0, 3.0])
+    path = sc.coo_to_csr(sc.CooMatrix(3, 3, [0, 1, 1, 2], [1, 0, 2, 1], [1.0] * 4))
+    assert np.array_equal(sc.spmv(path, np.ones(3)), [1.0, 2.0, 1.0])
+    assert np.array_equal(sc.spmv(path, np.zeros(3)), np.zeros(3))
+    with pytest.raises(sc.errors.DimensionMismatch):
+        sc.spmv(eye, np.ones(4))
+    empty = sc.coo_to_csr(sc.CooMatrix(4, 4, [], [], []))
+    assert np.array_equal(sc.spmv(empty, np.ones(4)), np.zeros(4))
+
+
+def test_spmv_dense_oracle_random():
+    rng = np.random.default_rng(11)
+    for _ in range(20):
+        n = int(rng.integers(1, 200))
+        nnz = int(rng.integers(0, min(n * n, 3000) + 1))
+        flat = rng.choice(n * n, size=nnz, replace=False)
+        m = sc.coo_to_csr(sc.coo_canonicalize(sc.CooMatrix(n, n, flat // n, flat % n, rng.standard_normal(nnz))))
+        x = rng.standard_normal(n)
+        want = dense(m) @ x
+        got = sc.spmv(m, x)
+        assert np.all(np.abs(got - want) <= 1e-12 * max(1.0, np.abs(want).max()))
+
+
+def test_vectorised_spmv_matches(golden):
+    import torch
+
+    from paper_1802_04450_b200 import _native as nat
+
+    g = golden("graph_c2s")
+    m = csr(g["row_ptr"], g["col"], g["vals"]).device()
+    x = np.random.default_rng(0).standard_normal(m.n_rows)
+    xd = torch.from_numpy(x).cuda()
+    y = torch.empty_like(xd)
+    nat.check(nat.load().sc_spmv_f64(m.n_rows, m.n_cols, nat.ptr(m.row_ptr), nat.ptr(m.col), nat.ptr(m.vals),
+                                     nat.ptr(xd), nat.ptr(y), 0, nat.stream_handle()))
+    want = orc.spmv_seq(g["row_ptr"], g["col"], g["vals"], x)
+    assert np.max(np.abs(y.cpu().numpy() - want)) <= 1e-12 * np.abs(want).max()
+
+
+@pytest.mark.parametrize("name", ["graph_blobs600", "graph_ties", "graph_c2s"])
+def test_degrees_and_sym_scale_bit_exact(golden, name):
+    g = golden(name)
+    w = csr(g["row_ptr"], g["col"], g["vals"])
+    d = sc.degrees(w)
+    assert np.array_equal(d, g["degrees"])
+    a = sc.sym_scale(w, d)
+    assert np.array_equal(a.vals, g["sym_vals"])
+
+
+def test_symmetry_gate():
+    w = sc.coo_to_csr(sc.CooMatrix(2, 2, [0, 1], [1, 0], [2.0, 2.0]))
+    assert sc.sparse.is_symmetric(w)
+    a = sc.coo_to_csr(sc.CooMatrix(2, 2, [0], [1], [1.0]))
+    assert not sc.sparse.is_symmetric(a)
+    b = sc.coo_to_csr(sc.CooMatrix(2, 2, [0, 1], [1, 0], [1.0, 2.0]))
+    assert not sc.sparse.is_symmetric(b)
+
+
+def test_isolated_and_zero_degree():
+    w = sc.coo_to_csr(sc.CooMatrix(4, 4, [0, 1], [1, 0], [1.0, 1.0]))
+    d = sc.degrees(w)
+    assert np.array_equal(d, [1.0, 1.0, 0.0, 0.0])
+    with pytest.raises(sc.errors.IsolatedNode) as exc:
+        sc.handle_isolated(w, d)
+    assert exc.value.indices == [2, 3]
+    sub, dd, remap = sc.handle_isolated(w, d, "remove")
+    assert sub.n_rows == 2 and list(remap) == [0, 1, -1, -1]
+    with pytest.raises(sc.errors.ZeroDegree):
+        sc.sym_scale(w, d)
+
+
+# ---------------------------------------------------------------- graph
+def _assert_graph(g, w):
+    assert np.array_equal(w.row_ptr, g["row_ptr"])
+    assert np.array_equal(w.col_idx, g["col"])
+    # values: one exp per pair; einsum order differs -> a few ulp
+    ref = g["vals"]
+    assert np.all(np.abs(w.vals - ref) <= 8 * np.spacing(np.maximum(ref, 1e-300)) + 1e-300)
+
+
+@pytest.mark.parametrize("name", ["graph_blobs600", "graph_underflow", "graph_ties", "graph_c2s"])
+def test_knn_graph_csr_bit_exact(golden, name):
+    from paper_1802_04450_b200.graph import knn_graph_device
+
+    g = golden(name)
+    m = sc.SimilarityMeasure.exp_decay(float(g["sigma"]))
+    w, stats = knn_graph_device(g["x"], int(g["knn"]), m, return_stats=True)
+    _assert_graph(g, w.to_host())
+    e = sc.build_edges_knn(g["x"], int(g["knn"]), m)
+    assert np.array_equal(e, g["edges"])
+
+
+def test_knn_small_examples():
+    m = sc.SimilarityMeasure.exp_decay(1.0)
+    e = sc.build_edges_knn(np.array([[0.0], [1.0], [3.0]]), 1, m)
+    assert e.tolist() == [[0, 1], [1, 2]]
+    e = sc.build_edges_knn(np.random.default_rng(1).standard_normal((5, 2)), 4, m)
+    assert len(e) == 10
+    e = sc.build_edges_knn(np.zeros((2, 3)), 1, m)
+    assert e.tolist() == [[0, 1]]
+    with pytest.raises(ValueError):
+        sc.build_edges_knn(np.zeros((3, 1)), 3, m)
+
+
+def test_knn_matches_oracle_random_shapes():
+    rng = np.random.default_rng(5)
+    for n, d, knn, scale in [(300, 3, 4, 1.0), (513, 17, 9, 0.3), (130, 64, 31, 3.0), (1000, 5, 1, 10.0)]:
+        x = rng.standard_normal((n, d)) * scale
+        sigma = float(np.sqrt(d))
+        e = orc.knn_edges(x, knn, sigma)
+        want = orc.csr_from_edges(n, e, orc.edge_weights(x, e, sigma))
+        m = sc.SimilarityMeasure.exp_decay(sigma)
+        from paper_1802_04450_b200.graph import knn_graph_device
+
+        w = knn_graph_device(x, knn, m).to_host()
+        assert np.array_equal(w.row_ptr, want[0]), (n, d, knn)
+        assert np.array_equal(w.col_idx, want[1]), (n, d, knn)
+
+
+def test_build_similarity_values(golden):
+    g = golden("graph_blobs600")
+    m = sc.SimilarityMeasure.exp_decay(float(g["sigma"]))
+    coo = sc.build_similarity(g["x"], g["edges"], m)
+    w = sc.coo_to_csr(coo)
+    _assert_graph(g, w)
+
+
+# ---------------------------------------------------------------- eigen
+def _principal_cos(a, b):
+    qa, _ = np.linalg.qr(a)
+    qb, _ = np.linalg.qr(b)
+    return np.linalg.svd(qa.T @ qb, compute_uv=False)
+
+
+def test_eigensolve_vs_reference(golden):
+    g = golden("eigen_cases")
+    for t in range(int(g["ncases"])):
+        m = csr(g[f"e{t}_row_ptr"], g[f"e{t}_col"], g[f"e{t}_vals"])
+        k = int(g[f"e{t}_k"])
+        b = sc.eigensolve(m, sc.LanczosConfig(k=k, seed=0))
+        ref = g[f"e{t}_values"]
+        assert np.max(np.abs(b.values - ref)) <= 1e-8 * max(1.0, np.abs(ref).max())
+        assert np.all(b.residuals <= 1e-6 * np.maximum(1.0, np.abs(b.values)))
+        defect = np.abs(b.vectors.T @ b.vectors - np.eye(k)).max()
+        assert defect <= 1e-8
+        cos = _principal_cos(b.vectors, g[f"e{t}_vectors"])
+        assert np.min(cos) > np.cos(1e-4)
+
+
+def test_eigensolve_dense_oracle_and_errors():
+    rng = np.random.default_rng(61)
+    n = 50
+    a = np.zeros((n, n))
+    nz = int(0.1 * n * n / 2)
+    a[rng.integers(0, n, nz), rng.integers(0, n, nz)] = rng.standard_normal(nz)
+    a = a + a.T
+    r, c = np.nonzero(a)
+    m = sc.coo_to_csr(sc.coo_canonicalize(sc.CooMatrix(n, n, r, c, a[r, c])))
+    want = np.sort(np.linalg.eigvalsh(a))[::-1][:5]
+    b = sc.eigensolve(m, sc.LanczosConfig(k=5, seed=0))
+    assert np.max(np.abs(b.values - want)) <= 1e-8
+    with pytest.raises(ValueError):
+        b.values[0] = 1.0
+    asym = rng.standard_normal((20, 20))
+    r, c = np.nonzero(asym)
+    with pytest.raises(sc.errors.NotSymmetric):
+        sc.eigensolve(sc.coo_to_csr(sc.CooMatrix(20, 20, r, c, asym[r, c])), sc.LanczosConfig(k=2))
+    rect = sc.coo_to_csr(sc.CooMatrix(2, 3, [0, 0, 0, 1, 1, 1], [0, 1, 2, 0, 1, 2], [1.0] * 6))
+    with pytest.raises(sc.errors.NotSquare):
+        sc.eigensolve(rect, sc.LanczosConfig(k=1, m=2))
+    with pytest.raises(sc.errors.MaxRestartsExceeded) as exc:
+        big = np.zeros((100, 100))
+        nz = 250
+        big[rng.integers(0, 100, nz), rng.integers(0, 100, nz)] = rng.standard_normal(nz)
+        big = big + big.T
+        r, c = np.nonzero(big)
+        sc.eigensolve(sc.coo_to_csr(sc.CooMatrix(100, 100, r, c, big[r, c])),
+                      sc.LanczosConfig(k=8, m=10, tol=1e-14, max_restarts=0))
+    assert exc.value.values is not None and len(exc.value.residuals) == 8
+
+
+def test_multiplicity_and_disconnected():
+    w = sc.coo_to_csr(sc.CooMatrix(4, 4, [0, 1, 2, 3], [1, 0, 3, 2], [1.0] * 4))
+    op = sc.sym_scale(w, sc.degrees(w))
+    b = sc.eigensolve(op, sc.LanczosConfig(k=2, m=4, seed=0))
+    assert np.allclose(b.values, [1.0, 1.0], atol=1e-10)
+
+
+def drive(s, op):
+    while s.state == "need_matvec":
+        s.out_slot = op @ s.in_slot
+        sc.rci_advance(s)
+    return sc.rci_extract(s, lambda v: op @ v)
+
+
+def test_rci_contract():
+    s = sc.rci_new(10, sc.LanczosConfig(k=2, m=6, seed=0))
+    assert s.state == "need_matvec"
+    assert np.linalg.norm(s.in_slot) == pytest.approx(1.0, abs=1e-14)
+    with pytest.raises(sc.errors.NotConverged):
+        sc.rci_extract(s, lambda v: v)
+    for bad in (dict(k=5, m=5), dict(k=2, m=11), dict(k=2, m=6, tol=0.0)):
+        with pytest.raises(sc.errors.BadConfig):
+            sc.rci_new(10, sc.LanczosConfig(**bad))
+    a = sc.rci_new(16, sc.LanczosConfig(k=2, seed=9))
+    b = sc.rci_new(16, sc.LanczosConfig(k=2, seed=9))
+    assert np.array_equal(a.in_slot, b.in_slot)
+
+
+def test_rci_identity_diag_breakdown_path():
+    s = sc.rci_new(10, sc.LanczosConfig(k=2, m=6, seed=1))
+    basis = drive(s, np.eye(10))
+    assert s.restart_count <= 1
+    assert np.allclose(basis.values, 1.0, atol=1e-12)
+    s = sc.rci_new(9, sc.LanczosConfig(k=2, m=5, seed=3))
+    assert np.allclose(drive(s, np.diag(np.arange(9, 0, -1.0))).values, [9.0, 8.0], atol=1e-8)
+    s = sc.rci_new(8, sc.LanczosConfig(k=2, m=4, seed=0))
+    while s.state == "need_matvec":
+        s.out_slot = np.zeros(8)
+        sc.rci_advance(s)
+    assert s.breakdown_count > 0
+    assert np.allclose(sc.rci_extract(s, lambda v: np.zeros(8)).values, 0.0, atol=1e-14)
+    w = sc.coo_to_csr(sc.CooMatrix(3, 3, [0, 1, 1, 2], [1, 0, 2, 1], [1.0] * 4))
+    op = dense(sc.sym_scale(w, sc.degrees(w)))
+    s = sc.rci_new(3, sc.LanczosConfig(k=2, m=3, seed=0))
+    assert np.allclose(drive(s, op).values, [1.0, 0.0], atol=1e-8)
+
+
+def test_rci_rejects_bad_out_slot():
+    s = sc.rci_new(6, sc.LanczosConfig(k=2, m=4))
+    s.out_slot = np.full(6, np.nan)
+    with pytest.raises(sc.errors.BadConfig):
+        sc.rci_advance(s)
+
+
+def test_residual_history_monotone_psd():
+    rng = np.random.default_rng(89)
+    for trial in range(3):
+        b = rng.standard_normal((60, 60)) * (rng.random((60, 60)) < 0.2)
+        a = b @ b.T
+        s = sc.rci_new(60, sc.LanczosConfig(k=3, m=10, seed=trial))
+        while s.state == "need_matvec":
+            s.out_slot = a @ s.in_slot
+            sc.rci_advance(s)
+        hist = s.residual_history
+        assert len(hist) >= 1
+        for prev, cur in zip(hist, hist[1:]):
+            assert cur <= prev * (1.0 + 1e-6) + 1e-12
+
+
+# ---------------------------------------------------------------- k-means
+def test_pairwise_sq_dist():
+    s = sc.pairwise_sq_dist(np.array([[0.0, 0.0], [1.0, 0.0]]), np.array([[0.0, 0.0]]))
+    assert np.array_equal(s, [[0.0], [1.0]])
+    rng = np.random.default_rng(1)
+    v = rng.standard_normal((8, 4))
+    assert np.array_equal(np.diag(sc.pairwise_sq_dist(v, v)), np.zeros(8))
+    v = rng.standard_normal((40, 5))
+    c = rng.standard_normal((7, 5))
+    naive = ((v[:, None, :] - c[None, :, :]) ** 2).sum(-1)
+    assert np.max(np.abs(sc.pairwise_sq_dist(v, c) - naive) / np.maximum(naive, 1e-12)) <= 1e-9
+    base = rng.standard_normal((30, 3)) * 1e8
+    assert np.all(sc.pairwise_sq_dist(base, base + 1e-9) >= 0.0)
+    with pytest.raises(sc.errors.DimensionMismatch):
+        sc.pairwise_sq_dist(np.ones((3, 2)), np.ones((2, 3)))
+
+
+def test_kmeanspp_and_lloyd_vs_reference(golden):
+    g = golden("kmeans_cases")
+    for t in range(int(g["ncases"])):
+        v, k = g[f"k{t}_v"], int(g[f"k{t}_k"])
+        init = sc.kmeanspp_init(v, k, t)
+        assert np.array_equal(init, v[g[f"k{t}_chosen"]]), t
+        lab = sc.lloyd(v, v[g[f"k{t}_chosen"]], sc.KmeansConfig(k=k))
+        assert np.array_equal(lab.labels, g[f"k{t}_labels"])
+        assert lab.iters_run == int(g[f"k{t}_iters"])
+        assert np.allclose(lab.centroids, g[f"k{t}_centroids"], rtol=1e-12, atol=1e-12)
+        assert np.allclose(lab.sse_history, g[f"k{t}_sse_history"], rtol=1e-12)
+        full = sc.kmeans(v, sc.KmeansConfig(k=k, seed=t, restarts=2))
+        assert orc.ari(full.labels, g[f"k{t}_full_labels"]) == 1.0
+
+
+def test_lloyd_reseed_and_examples(golden):
+    g = golden("kmeans_cases")
+    lab = sc.lloyd(g["r_v"], g["r_init"], sc.KmeansConfig(k=3))
+    assert np.array_equal(lab.labels, g["r_labels"])
+    assert np.array_equal(lab.centroids, g["r_centroids"])
+    v = np.array([[0.0], [1.0], [10.0], [11.0]])
+    lab = sc.lloyd(v, np.array([[0.0], [10.0]]), sc.KmeansConfig(k=2))
+    assert lab.labels.tolist() == [0, 0, 1, 1]
+    assert np.allclose(lab.centroids.ravel(), [0.5, 10.5])
+    lab = sc.lloyd(v, np.array([[3.0]]), sc.KmeansConfig(k=1))
+    assert np.allclose(lab.centroids.ravel(), [5.5])
+    with pytest.raises(sc.errors.BadConfig):
+        sc.kmeans(np.zeros((2, 2)), sc.KmeansConfig(k=3))
+
+
+def test_ncut_matches_oracle(golden):
+    g = golden("graph_blobs600")
+    w = csr(g["row_ptr"], g["col"], g["vals"])
+    lab = np.random.default_rng(0).integers(0, 6, w.n_rows)
+    assert sc.ncut(w, lab) == orc.ncut(g["row_ptr"], g["col"], g["vals"], lab)
+    with pytest.raises(sc.errors.ZeroVolumePart):
+        sc.ncut(w, lab, k=7)

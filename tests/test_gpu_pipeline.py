@@ -1,0 +1,116 @@
+"""End-to-end parity of run() on the GPU against the real reference's outputs
+(tests/golden/pipeline_c1s.npz: scaled config 1, N=2000; pipeline_c1.npz:
+config 1, N=20000, structure stored as SHA-256 digests)."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import paper_1802_04450_b200 as sc
+from oracle import speclust_oracle as orc
+from paper_1802_04450_b200.pipeline import run_device
+
+pytestmark = pytest.mark.gpu
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def cfg_for(x, knn, sigma, k):
+    return sc.PipelineConfig(
+        input=sc.PointsInput(measure=sc.SimilarityMeasure.exp_decay(sigma), pattern="knn", points=x, knn=knn),
+        k_clusters=k, eigen=sc.LanczosConfig(k=k, seed=0), kmeans=sc.KmeansConfig(k=k, seed=0),
+        normalize_rows=True)
+
+
+def principal_angle(a, b):
+    qa, _ = np.linalg.qr(a)
+    qb, _ = np.linalg.qr(b)
+    s = np.linalg.svd(qa.T @ qb, compute_uv=False)
+    return float(np.arccos(np.clip(s.min(), -1.0, 1.0)))
+
+
+def test_pipeline_scaled_config1(golden):
+    g = golden("pipeline_c1s")
+    k = int(g["k"])
+    rep, wd = run_device(cfg_for(g["x"], int(g["knn"]), float(g["sigma"]), k))
+    w = wd.to_host()
+    # (1) CSR structure bit-exact, values within a few ulp
+    assert np.array_equal(w.row_ptr, g["row_ptr"]) and np.array_equal(w.col_idx, g["col"])
+    assert np.max(np.abs(w.vals - g["vals"]) / g["vals"]) < 1e-14
+    # (2) eigenvalues (lambda(A) form) 1e-5 relative
+    assert np.max(np.abs(rep.eigenvalues - g["values"]) / np.abs(g["values"])) < 1e-5
+    assert np.all(rep.eigen_residuals < 1e-6)
+    # (3) labels: ARI >= 0.999 vs the reference run
+    assert orc.ari(rep.labeling.labels, g["labels"]) >= 0.999
+    assert set(rep.timings) == {"graph", "degrees", "eigen", "kmeans", "metrics"}
+
+
+def test_stage_isolated_kmeans_parity(golden):
+    """Same embedding + same init rows -> same labels."""
+    g = golden("pipeline_c1s")
+    emb = g["embedding"]
+    lab = sc.lloyd(emb, emb[g["chosen"]], sc.KmeansConfig(k=int(g["k"])))
+    assert orc.ari(lab.labels, g["labels"]) >= 0.999
+    assert np.array_equal(sc.kmeanspp_init(emb, int(g["k"]), 0), emb[g["chosen"]])
+
+
+def test_eigen_subspace_vs_reference(golden):
+    g = golden("pipeline_c1s")
+    w = sc.CsrMatrix(len(g["degrees"]), len(g["degrees"]), g["row_ptr"], g["col"], g["vals"])
+    a = sc.sym_scale(w, g["degrees"])
+    b = sc.eigensolve(a, sc.LanczosConfig(k=int(g["k"]), seed=0))
+    assert principal_angle(b.vectors, g["vectors"]) < 1e-4
+
+
+def test_pipeline_config1_full(golden):
+    g = golden("pipeline_c1")
+    x, truth = orc.blobs(int(g["n"]), int(g["d"]), int(g["k"]), 1.0, seed=0)
+    assert np.array_equal(truth, g["truth"])
+    k = int(g["k"])
+    rep, wd = run_device(cfg_for(x, int(g["knn"]), float(g["sigma"]), k))
+    w = wd.to_host()
+    assert sha(w.row_ptr) == str(g["row_ptr_sha"])
+    assert sha(w.col_idx) == str(g["col_sha"])
+    assert np.max(np.abs(rep.eigenvalues - g["values"]) / np.abs(g["values"])) < 1e-5
+    assert orc.ari(rep.labeling.labels, g["labels"]) >= 0.999
+
+
+def test_matrix_input_two_triangles():
+    w = np.zeros((6, 6))
+    for base in (0, 3):
+        for i in range(3):
+            for j in range(i + 1, 3):
+                w[base + i, base + j] = w[base + j, base + i] = 1.0
+    r, c = np.nonzero(w)
+    coo = sc.coo_canonicalize(sc.CooMatrix(6, 6, r, c, w[r, c]))
+    rep = sc.run(sc.PipelineConfig(input=sc.MatrixInput(matrix=coo), k_clusters=2,
+                                   eigen=sc.LanczosConfig(k=2, seed=0), kmeans=sc.KmeansConfig(k=2, seed=0)))
+    assert sc.adjusted_rand_index(rep.labeling.labels, [0, 0, 0, 1, 1, 1]) == 1.0
+    assert rep.ncut_value == 0.0
+    assert np.allclose(rep.eigenvalues, [1.0, 1.0], atol=1e-9)
+    assert np.all(rep.eigen_residuals <= 1e-8)
+
+
+def test_pipeline_errors():
+    coo = sc.CooMatrix(3, 3, [0, 1], [1, 0], [1.0, 1.0])
+    with pytest.raises(sc.errors.PipelineError) as exc:
+        sc.run(sc.PipelineConfig(input=sc.MatrixInput(matrix=coo), k_clusters=2))
+    assert exc.value.stage == "degrees"
+    assert isinstance(exc.value.cause, sc.errors.IsolatedNode)
+    asym = sc.CooMatrix(3, 3, [0, 1, 1, 2], [1, 0, 2, 1], [1.0, 2.0, 1.0, 1.0])
+    with pytest.raises(sc.errors.PipelineError) as exc:
+        sc.run(sc.PipelineConfig(input=sc.MatrixInput(matrix=asym), k_clusters=2))
+    assert exc.value.stage == "graph"
+    assert isinstance(exc.value.cause, sc.errors.NotSymmetric)
+
+
+def test_determinism():
+    x, _ = orc.blobs(800, 8, 4, 3.0, seed=7)
+    a = sc.run(cfg_for(x, 8, 3.0, 4))
+    b = sc.run(cfg_for(x, 8, 3.0, 4))
+    assert np.array_equal(a.labeling.labels, b.labeling.labels)
+    assert np.array_equal(a.eigenvalues, b.eigenvalues)
+    assert a.ncut_value == b.ncut_value
