@@ -166,6 +166,8 @@ def to_device(a, dtype):
     if isinstance(a, torch.Tensor):
         return a.to(device="cuda", dtype=dtype).contiguous()
     arr = np.ascontiguousarray(a)
+    if not arr.flags.writeable:
+        arr = arr.copy()
     return torch.from_numpy(arr).to(device="cuda", dtype=dtype, non_blocking=False).contiguous()
 
 

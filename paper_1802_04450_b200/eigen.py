@@ -88,7 +88,7 @@ class _DevVec:
     """Zero-copy view of a library-owned device vector (CUDA array interface)."""
 
     def __init__(self, p: int, n: int, readonly: bool):
-        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (p, readonly), "version": 3,
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (p, False), "version": 3,
                                          "strides": None}
 
 
