@@ -15,12 +15,18 @@
 //             enter the top knn; uncertified rows -> exact fallback
 //   fallback  fp64 scan of all n points + radix select on (s, -j)
 //   union     reverse lists, duplicate removal, scan, CSR fill with fp64 values
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "sc_common.cuh"
 #include "sc_knn.cuh"
+#include "sc_list.cuh"
+#include "sc_knn_tc.cuh"
 #include "sc_scan.cuh"
 
 namespace sc {
@@ -77,35 +83,8 @@ __global__ void knn_prep_kernel(int64_t n, int64_t d, int64_t dp, const double* 
 }
 
 // ---------------------------------------------------------------------------
-// streaming top-R list (per query row, owned by one thread)
-__device__ float list_compact(float2* L, int cap, int R) {
-    int lo = 0, hi = cap - 1, target = R - 1;
-    while (lo < hi) {
-        float a = L[lo].x, b = L[(lo + hi) >> 1].x, c = L[hi].x;
-        float pivot = fmaxf(fminf(a, b), fminf(fmaxf(a, b), c));  // median of three
-        int i = lo, j = hi;
-        while (i <= j) {
-            while (L[i].x < pivot) ++i;
-            while (L[j].x > pivot) --j;
-            if (i <= j) {
-                float2 t = L[i];
-                L[i] = L[j];
-                L[j] = t;
-                ++i;
-                --j;
-            }
-        }
-        if (target <= j) hi = j;
-        else if (target >= i) lo = i;
-        else break;
-    }
-    float tau = -INFINITY;
-    for (int q = 0; q < R; ++q) tau = fmaxf(tau, L[q].x);
-    return tau;
-}
-
-// ---------------------------------------------------------------------------
-// candidate generation, SIMT fp32 tiles (128 query rows x 128 columns)
+// candidate generation, SIMT fp32 tiles (reference kernel for A/B checks of
+// the tcgen05 path; selected with SPECLUST_KNN_KERNEL=simt) (128 query rows x 128 columns)
 constexpr int KM = 128, KN = 128, KK = 16;
 
 __global__ void __launch_bounds__(256) knn_cand_simt_kernel(int64_t n, int dp, const float* __restrict__ xf,
@@ -471,17 +450,72 @@ using namespace sc;
 
 namespace sc {
 
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+template <int NKB, int STAGES>
+static int launch_tc(const CUtensorMap& map, int64_t n, int64_t ntiles, const float* cnk, float key_scale, int cap,
+                     int R, float2* lists, int* counts, float* taus, cudaStream_t st) {
+    const uint32_t smem = TcLayout<NKB, STAGES>::total;
+    SC_CUDA(cudaFuncSetAttribute(knn_cand_tc_kernel<NKB, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    knn_cand_tc_kernel<NKB, STAGES><<<(unsigned)ntiles, TC_THREADS, smem, st>>>(map, n, ntiles, cnk, key_scale, cap, R,
+                                                                                lists, counts, taus);
+    SC_LAUNCHED(1);
+    return SC_OK;
+}
+
+// tensor-core candidate lists: every query tile against every candidate tile
+int knn_candidates_tc(int64_t n, int64_t n_pad, int64_t dp64, const __half* xh, const float* cnk, float key_scale,
+                      int cap, int R, float2* lists, int* counts, float* taus, cudaStream_t st) {
+    auto encode = tensor_map_encoder();
+    if (!encode) return fail(SC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    CUtensorMap map;
+    cuuint64_t gdim[2] = {(cuuint64_t)dp64, (cuuint64_t)n_pad};
+    cuuint64_t gstride[1] = {(cuuint64_t)dp64 * sizeof(__half)};
+    cuuint32_t box[2] = {64, 128};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult cr = encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half*>(xh), gdim, gstride, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return fail(SC_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
+    const int64_t ntiles = n_pad / 128;
+    ProfScope prof("knn_tile", st, 2.0 * (double)n * (double)n * (double)dp64);
+    switch (dp64 / 64) {
+        case 1: return launch_tc<1, 4>(map, n, ntiles, cnk, key_scale, cap, R, lists, counts, taus, st);
+        case 2: return launch_tc<2, 3>(map, n, ntiles, cnk, key_scale, cap, R, lists, counts, taus, st);
+        case 3: return launch_tc<3, 2>(map, n, ntiles, cnk, key_scale, cap, R, lists, counts, taus, st);
+        default: return launch_tc<4, 2>(map, n, ntiles, cnk, key_scale, cap, R, lists, counts, taus, st);
+    }
+}
+
 int knn_graph_build(int64_t n, int64_t d, const double* x, int64_t knn, double two_sigma_sq, int64_t* row_ptr,
                     int32_t* col, double* vals, int64_t* nnz_out, int64_t* stats, cudaStream_t st) {
     const double inv = -1.0 / two_sigma_sq;  // graph.py:154
     const int64_t dp = (d + 15) / 16 * 16;
-    const int R = (int)imin64(n - 1, knn + std::max<int64_t>(8, knn / 2));
+    const char* kenv = std::getenv("SPECLUST_KNN_KERNEL");
+    const int64_t dp64 = (d + 63) / 64 * 64;
+    const bool use_tc = dp64 <= 256 && !(kenv && std::strcmp(kenv, "simt") == 0);
+    // list budget: R kept candidates per row, 2R append capacity.  The fp16
+    // tensor-core keys carry a larger error bound than fp32, so keep more.
+    const int64_t margin = use_tc ? std::max<int64_t>(12, knn / 2 + 8) : std::max<int64_t>(8, knn / 2);
+    const int R = (int)imin64(n - 1, knn + margin);
     int cap = 2 * R;
     if (cap > n - 1) cap = (int)(n - 1);  // lists can hold every other point
     if (cap < R) cap = R;
     int rc;
     DevBuf<double> part, mean, rn, qn;
     DevBuf<float> xf, cnf, taus;
+    DevBuf<__half> xh;
     DevBuf<unsigned long long> rmax, nflag;
     DevBuf<float2> lists;
     DevBuf<int> counts;
@@ -490,31 +524,56 @@ int knn_graph_build(int64_t n, int64_t d, const double* x, int64_t knn, double t
     DevBuf<unsigned int> fill;
     DevBuf<uint8_t> dup;
     const int64_t nbc = ceil_div(n, 256);
+    const int64_t n_pad = (n + 127) / 128 * 128;
     if ((rc = part.alloc((size_t)nbc * d)) || (rc = mean.alloc(d)) || (rc = rn.alloc(n)) || (rc = qn.alloc(n)) ||
-        (rc = xf.alloc((size_t)n * dp)) || (rc = cnf.alloc(n)) || (rc = taus.alloc(n)) || (rc = rmax.alloc(1)) ||
-        (rc = nflag.alloc(1)) || (rc = lists.alloc((size_t)n * cap)) || (rc = counts.alloc(n)) ||
-        (rc = sel.alloc((size_t)n * knn)) || (rc = flagged.alloc(n)))
+        (rc = taus.alloc(n)) || (rc = rmax.alloc(1)) || (rc = nflag.alloc(1)) ||
+        (rc = lists.alloc((size_t)n * cap)) || (rc = counts.alloc(n)) || (rc = sel.alloc((size_t)n * knn)) ||
+        (rc = flagged.alloc(n)))
         return rc;
-    // ---- prep
+    // ---- prep: fp64 column means (the key is translation invariant; centring
+    // shrinks |x| and with it the error bound)
     colsum_partial_kernel<<<(unsigned)nbc, 128, 0, st>>>(n, d, x, part.p);
     colmean_finish_kernel<<<(unsigned)ceil_div(d, 128), 128, 0, st>>>(nbc, n, d, part.p, mean.p);
     SC_CUDA(cudaMemsetAsync(rmax.p, 0, sizeof(unsigned long long), st));
     SC_CUDA(cudaMemsetAsync(nflag.p, 0, sizeof(unsigned long long), st));
-    knn_prep_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, st>>>(n, d, dp, x, mean.p, xf.p, cnf.p, rn.p, qn.p, rmax.p);
-    SC_LAUNCHED(3);
-    // ---- candidates
-    {
+    SC_LAUNCHED(2);
+    double cdelta;
+    if (use_tc) {
+        knn_rownorm_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, st>>>(n, d, x, mean.p, rn.p, rmax.p);
+        SC_LAUNCHED(1);
+        unsigned long long rb = 0;
+        SC_CUDA(cudaMemcpyAsync(&rb, rmax.p, sizeof(rb), cudaMemcpyDeviceToHost, st));
+        SC_CUDA(cudaStreamSynchronize(st));
+        double rm;
+        std::memcpy(&rm, &rb, sizeof(rm));
+        // power-of-two scale: every |element| <= 128, |row|^2 stays far from overflow
+        const double scale = rm > 0 ? std::ldexp(1.0, (int)std::floor(std::log2(128.0 / rm))) : 1.0;
+        if ((rc = xh.alloc((size_t)n_pad * dp64)) || (rc = cnf.alloc(n_pad))) return rc;
+        knn_prep_f16_kernel<<<(unsigned)ceil_div(n_pad, 8), 256, 0, st>>>(n, n_pad, d, dp64, x, mean.p, scale, xh.p,
+                                                                          cnf.p, qn.p);
+        SC_LAUNCHED(1);
+        if ((rc = knn_candidates_tc(n, n_pad, dp64, xh.p, cnf.p, (float)(-2.0 / (scale * scale)), cap, R, lists.p,
+                                    counts.p, taus.p, st)))
+            return rc;
+        // fp16 rounding of both operands (u = 2^-11) + fp32 accumulation of
+        // dp64 products + fp32 rounding of |x_j|^2 and of the key, relative to
+        // (|x_i| + |x_j|)^2; 10% slack on top.
+        cdelta = 1.1 * (2.0 * std::ldexp(1.0, -11) + (double)(dp64 + 8) * std::ldexp(1.0, -24));
+    } else {
+        if ((rc = xf.alloc((size_t)n * dp)) || (rc = cnf.alloc(n))) return rc;
+        knn_prep_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, st>>>(n, d, dp, x, mean.p, xf.p, cnf.p, rn.p, qn.p,
+                                                                  rmax.p);
+        SC_LAUNCHED(1);
         size_t smem = sizeof(float) * (KK * KM + KK * KN + KM * (KN + 1) + KN);
         cudaFuncSetAttribute(knn_cand_simt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         ProfScope prof("knn_tile", st, 2.0 * (double)n * (double)n * (double)d);
         knn_cand_simt_kernel<<<(unsigned)ceil_div(n, KM), 256, smem, st>>>(n, (int)dp, xf.p, cnf.p, cap, R, lists.p,
                                                                            counts.p, taus.p);
         SC_LAUNCHED(1);
+        // fp32 inputs (u = 2^-24) and a dp-term fp32 accumulation
+        cdelta = (2.0 * (double)dp + 16.0) * std::ldexp(1.0, -24);
     }
-    // ---- exact recheck + certificate.  fp32 error bound on the key
-    // |x_j|^2 - 2 x_i.x_j: inputs rounded (u = 2^-24) and a dp-term fp32
-    // accumulation; generous constant (2 dp + 16) u (|x_i| + |x_j|)^2.
-    const double cdelta = (2.0 * (double)dp + 16.0) * std::ldexp(1.0, -24);
+    // ---- exact recheck + certificate
     {
         size_t smem = (size_t)8 * cap * (sizeof(double) + sizeof(int));
         cudaFuncSetAttribute(knn_recheck_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -529,6 +588,7 @@ int knn_graph_build(int64_t n, int64_t d, const double* x, int64_t knn, double t
     SC_CUDA(cudaStreamSynchronize(st));
     lists.free();
     xf.free();
+    xh.free();
     if (hflag > 0) {
         int64_t grid = imin64((int64_t)hflag, kNumSMs);
         DevBuf<unsigned long long> scratch;

@@ -1,0 +1,234 @@
+// kNN candidate generation on the 5th-generation tensor cores.
+//
+// One CTA owns 128 query rows and streams every candidate tile of 128 rows:
+//   warp 0     TMA producer: query tile once, candidate tiles through a ring
+//   warp 1     TMEM allocation + single-thread tcgen05.mma issuer
+//              (M=128, N=128, K=16 per instruction, fp16 in / fp32 out)
+//   warps 2-5  epilogue: thread <-> query row (TMEM lane); tcgen05.ld of the
+//              accumulator, key = |x_j|^2 - 2 x_i.x_j, min-of-16 filter against
+//              the row's running threshold, rare appends to the row's list
+// Two TMEM accumulators (2 x 128 columns) let the MMA of tile t+1 overlap the
+// epilogue of tile t.  Operands are K-major fp16 in 128-byte swizzled rows,
+// staged by TMA (SWIZZLE_128B) and described to UMMA with matching
+// descriptors.  Included by sc_knn.cu (shares list_compact).
+#pragma once
+#include <cuda_fp16.h>
+
+#include "sc_tc.cuh"
+
+namespace sc {
+
+constexpr int TC_THREADS = 192;
+constexpr uint32_t TC_TILE_BYTES = 128 * 128;  // 128 rows x 64 fp16
+
+template <int NKB, int STAGES>
+struct TcLayout {
+    static constexpr uint32_t kA = NKB * TC_TILE_BYTES;
+    static constexpr uint32_t kB = NKB * TC_TILE_BYTES;
+    static constexpr uint32_t kBar = 8 * (2 * STAGES + 5) + 8;
+    static constexpr uint32_t total = 1024 + kA + STAGES * kB + kBar;
+};
+
+struct ListState {
+    int cnt;
+    float tau;
+};
+
+// append one passing candidate; compaction when the list is full (rare path)
+__device__ __noinline__ ListState tc_push(float2* L, ListState st, float key, int col, int cap, int R) {
+    L[st.cnt++] = make_float2(key, __int_as_float(col));
+    if (st.cnt == cap) {
+        st.tau = list_compact(L, cap, R);
+        st.cnt = R;
+    }
+    return st;
+}
+
+template <int NKB, int STAGES>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    knn_cand_tc_kernel(const __grid_constant__ CUtensorMap xmap, int64_t n, int64_t ntiles,
+                       const float* __restrict__ cnk, float key_scale, int cap, int R, float2* __restrict__ lists,
+                       int* __restrict__ counts, float* __restrict__ taus) {
+    using Lay = TcLayout<NKB, STAGES>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = base;
+    uint8_t* sB = base + Lay::kA;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * Lay::kB);
+    uint64_t* empty = full + STAGES;
+    uint64_t* afull = empty + STAGES;
+    uint64_t* tfull = afull + 1;   // [2]
+    uint64_t* tempty = tfull + 2;  // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t row0 = (int64_t)blockIdx.x * 128;
+
+    if (warp == 0 && lane == 0) tc::tma_prefetch(&xmap);
+    if (warp == 1) {
+        if (lane == 0) {
+            for (int s = 0; s < STAGES; ++s) {
+                tc::mbar_init(&full[s], 1);
+                tc::mbar_init(&empty[s], 1);
+            }
+            tc::mbar_init(afull, 1);
+            for (int b = 0; b < 2; ++b) {
+                tc::mbar_init(&tfull[b], 1);
+                tc::mbar_init(&tempty[b], 4);
+            }
+            tc::fence_mbar_init();
+        }
+        __syncwarp();
+        tc::tmem_alloc(tmem_slot, 256);
+    }
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            tc::mbar_expect_tx(afull, Lay::kA);
+            for (int kb = 0; kb < NKB; ++kb) tc::tma_load_2d(sA + kb * TC_TILE_BYTES, &xmap, afull, kb * 64, (int)row0);
+            for (int64_t t = 0; t < ntiles; ++t) {
+                const int s = (int)(t % STAGES);
+                const uint32_t ph = (uint32_t)((t / STAGES) & 1);
+                tc::mbar_wait(&empty[s], ph ^ 1);
+                tc::mbar_expect_tx(&full[s], Lay::kB);
+                for (int kb = 0; kb < NKB; ++kb)
+                    tc::tma_load_2d(sB + s * Lay::kB + kb * TC_TILE_BYTES, &xmap, &full[s], kb * 64, (int)(t * 128));
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = tc::idesc_f16_f32(128, 128);
+            tc::mbar_wait(afull, 0);
+            for (int64_t t = 0; t < ntiles; ++t) {
+                const int s = (int)(t % STAGES);
+                const uint32_t ph = (uint32_t)((t / STAGES) & 1);
+                const int buf = (int)(t & 1);
+                const uint32_t bph = (uint32_t)((t >> 1) & 1);
+                tc::mbar_wait(&tempty[buf], bph ^ 1);
+                tc::mbar_wait(&full[s], ph);
+                tc::fence_after();
+#pragma unroll
+                for (int kb = 0; kb < NKB; ++kb) {
+                    const uint64_t ad = tc::desc_k_sw128(sA + kb * TC_TILE_BYTES);
+                    const uint64_t bd = tc::desc_k_sw128(sB + s * Lay::kB + kb * TC_TILE_BYTES);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)  // 4 x K=16 per 64-element swizzle row (32 B steps)
+                        tc::umma_f16(tmem + buf * 128, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+                }
+                tc::umma_commit(&empty[s]);
+                tc::umma_commit(&tfull[buf]);
+            }
+        }
+    } else {
+        const int quad = warp & 3;
+        const int64_t row = row0 + quad * 32 + lane;
+        const bool valid = row < n;
+        float2* L = lists + (valid ? row : 0) * (int64_t)cap;
+        ListState st{0, INFINITY};
+        for (int64_t t = 0; t < ntiles; ++t) {
+            const int buf = (int)(t & 1);
+            const uint32_t bph = (uint32_t)((t >> 1) & 1);
+            tc::mbar_wait(&tfull[buf], bph);
+            tc::fence_after();
+            const int64_t col0 = t * 128;
+            const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * 128);
+#pragma unroll 1
+            for (int half = 0; half < 2; ++half) {
+                float v[64];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) tc::tmem_ld16(taddr + half * 64 + q * 16, v + q * 16);
+                tc::tmem_wait_ld();
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int c = half * 64 + q * 16;
+                    const float4* cp = reinterpret_cast<const float4*>(cnk + col0 + c);
+                    float keys[16];
+                    float m = INFINITY;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        float4 cn4 = __ldg(cp + u);
+                        keys[4 * u + 0] = fmaf(key_scale, v[q * 16 + 4 * u + 0], cn4.x);
+                        keys[4 * u + 1] = fmaf(key_scale, v[q * 16 + 4 * u + 1], cn4.y);
+                        keys[4 * u + 2] = fmaf(key_scale, v[q * 16 + 4 * u + 2], cn4.z);
+                        keys[4 * u + 3] = fmaf(key_scale, v[q * 16 + 4 * u + 3], cn4.w);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) m = fminf(m, keys[u]);
+                    if (valid && m < st.tau) {
+#pragma unroll
+                        for (int u = 0; u < 16; ++u) {
+                            const int64_t col = col0 + c + u;
+                            if (keys[u] < st.tau && col != row && col < n)
+                                st = tc_push(L, st, keys[u], (int)col, cap, R);
+                        }
+                    }
+                }
+            }
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&tempty[buf]);
+        }
+        if (valid) {
+            counts[row] = st.cnt;
+            taus[row] = st.tau;
+        }
+    }
+    __syncthreads();
+    if (warp == 1) {
+        tc::fence_after();
+        tc::tmem_dealloc(tmem, 256);
+    }
+}
+
+// fp16 operand prep: xh = fp16(scale * (x - mean)) padded to (n_pad x dp);
+// cnk = |xh|^2 / scale^2 (fp64 sum of the fp16 values, +inf on padding rows);
+// qn = same in fp64 for query rows.
+__global__ void knn_prep_f16_kernel(int64_t n, int64_t n_pad, int64_t d, int64_t dp, const double* __restrict__ x,
+                                    const double* __restrict__ mean, double scale, __half* __restrict__ xh,
+                                    float* __restrict__ cnk, double* __restrict__ qn) {
+    int64_t i = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    int lane = threadIdx.x & 31;
+    if (i >= n_pad) return;
+    double acc = 0.0;
+    for (int64_t c = lane; c < dp; c += 32) {
+        __half h = __float2half_rn(0.f);
+        if (i < n && c < d) h = __double2half((x[i * d + c] - mean[c]) * scale);
+        xh[i * dp + c] = h;
+        double hv = (double)__half2float(h);
+        acc = fma(hv, hv, acc);
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) {
+        double inv_s2 = 1.0 / (scale * scale);
+        if (i < n) {
+            cnk[i] = (float)(acc * inv_s2);
+            qn[i] = acc * inv_s2;
+        } else {
+            cnk[i] = INFINITY;
+        }
+    }
+}
+
+// fp64 centred row norms and their maximum (pass 1 of the prep)
+__global__ void knn_rownorm_kernel(int64_t n, int64_t d, const double* __restrict__ x, const double* __restrict__ mean,
+                                   double* __restrict__ rn, unsigned long long* __restrict__ rmax_bits) {
+    int64_t i = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    int lane = threadIdx.x & 31;
+    if (i >= n) return;
+    double a = 0.0;
+    for (int64_t c = lane; c < d; c += 32) {
+        double v = x[i * d + c] - mean[c];
+        a = fma(v, v, a);
+    }
+    a = warp_sum(a);
+    if (lane == 0) {
+        double r = sqrt(a);
+        rn[i] = r;
+        atomicMax(rmax_bits, (unsigned long long)__double_as_longlong(r));
+    }
+}
+
+}  // namespace sc
