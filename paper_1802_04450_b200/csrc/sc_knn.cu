@@ -462,14 +462,14 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     return fn;
 }
 
-template <int NKB, int STAGES>
+template <int NKB, int STAGES, bool LSMEM>
 static int launch_tc(const CUtensorMap& map, int64_t n, int64_t ntiles, const float* cnk, float key_scale, int cap,
                      int R, float2* lists, int* counts, float* taus, cudaStream_t st) {
-    const uint32_t smem = TcLayout<NKB, STAGES>::total;
-    SC_CUDA(cudaFuncSetAttribute(knn_cand_tc_kernel<NKB, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    const uint32_t smem = TcLayout<NKB, STAGES, LSMEM>::total;
+    SC_CUDA(cudaFuncSetAttribute(knn_cand_tc_kernel<NKB, STAGES, LSMEM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
-    knn_cand_tc_kernel<NKB, STAGES><<<(unsigned)ntiles, TC_THREADS, smem, st>>>(map, n, ntiles, cnk, key_scale, cap, R,
-                                                                                lists, counts, taus);
+    knn_cand_tc_kernel<NKB, STAGES, LSMEM><<<(unsigned)ntiles, TC_THREADS, smem, st>>>(map, n, ntiles, cnk, key_scale,
+                                                                                       cap, R, lists, counts, taus);
     SC_LAUNCHED(1);
     return SC_OK;
 }
@@ -491,10 +491,10 @@ int knn_candidates_tc(int64_t n, int64_t n_pad, int64_t dp64, const __half* xh, 
     const int64_t ntiles = n_pad / 128;
     ProfScope prof("knn_tile", st, 2.0 * (double)n * (double)n * (double)dp64);
     switch (dp64 / 64) {
-        case 1: return launch_tc<1, 4>(map, n, ntiles, cnk, key_scale, cap, R, lists, counts, taus, st);
-        case 2: return launch_tc<2, 3>(map, n, ntiles, cnk, key_scale, cap, R, lists, counts, taus, st);
-        case 3: return launch_tc<3, 2>(map, n, ntiles, cnk, key_scale, cap, R, lists, counts, taus, st);
-        default: return launch_tc<4, 2>(map, n, ntiles, cnk, key_scale, cap, R, lists, counts, taus, st);
+        case 1: return launch_tc<1, 4, true>(map, n, ntiles, cnk, key_scale, cap, R, lists, counts, taus, st);
+        case 2: return launch_tc<2, 3, false>(map, n, ntiles, cnk, key_scale, cap, R, lists, counts, taus, st);
+        case 3: return launch_tc<3, 2, false>(map, n, ntiles, cnk, key_scale, cap, R, lists, counts, taus, st);
+        default: return launch_tc<4, 2, false>(map, n, ntiles, cnk, key_scale, cap, R, lists, counts, taus, st);
     }
 }
 
@@ -504,12 +504,15 @@ int knn_graph_build(int64_t n, int64_t d, const double* x, int64_t knn, double t
     const int64_t dp = (d + 15) / 16 * 16;
     const char* kenv = std::getenv("SPECLUST_KNN_KERNEL");
     const int64_t dp64 = (d + 63) / 64 * 64;
-    const bool use_tc = dp64 <= 256 && !(kenv && std::strcmp(kenv, "simt") == 0);
+    const int64_t tc_margin = std::max<int64_t>(12, knn / 2 + 8);
+    // the tensor-core path sorts lists of <= TC_LIST_P slots and needs R + 16 <= cap
+    const bool use_tc = dp64 <= 256 && knn + tc_margin + 16 <= TC_LIST_P && n > 2 * (knn + tc_margin) + 1 &&
+                        !(kenv && std::strcmp(kenv, "simt") == 0);
     // list budget: R kept candidates per row, 2R append capacity.  The fp16
     // tensor-core keys carry a larger error bound than fp32, so keep more.
-    const int64_t margin = use_tc ? std::max<int64_t>(12, knn / 2 + 8) : std::max<int64_t>(8, knn / 2);
+    const int64_t margin = use_tc ? tc_margin : std::max<int64_t>(8, knn / 2);
     const int R = (int)imin64(n - 1, knn + margin);
-    int cap = 2 * R;
+    int cap = use_tc ? (int)std::min<int64_t>(2 * R, TC_LIST_P) : 2 * R;
     if (cap > n - 1) cap = (int)(n - 1);  // lists can hold every other point
     if (cap < R) cap = R;
     int rc;

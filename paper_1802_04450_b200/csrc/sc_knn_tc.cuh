@@ -10,7 +10,14 @@
 // Two TMEM accumulators (2 x 128 columns) let the MMA of tile t+1 overlap the
 // epilogue of tile t.  Operands are K-major fp16 in 128-byte swizzled rows,
 // staged by TMA (SWIZZLE_128B) and described to UMMA with matching
-// descriptors.  Included by sc_knn.cu (shares list_compact).
+// descriptors.
+//
+// Candidate lists: each row appends (key, column) pairs with key < tau into
+// a list of `cap` slots; a list that could overflow is compacted by the
+// whole warp (bitonic sort of the row's list in shared memory, keep the R
+// smallest, tau = R-th key), so compaction never serialises 32 divergent
+// lanes.  For d <= 64 the lists live in shared memory for the whole scan;
+// wider rows keep them in global memory and sort through a per-warp scratch.
 #pragma once
 #include <cuda_fp16.h>
 
@@ -20,41 +27,55 @@ namespace sc {
 
 constexpr int TC_THREADS = 192;
 constexpr uint32_t TC_TILE_BYTES = 128 * 128;  // 128 rows x 64 fp16
+constexpr int TC_LIST_P = 128;                 // sort width (power of two >= cap)
 
-template <int NKB, int STAGES>
+template <int NKB, int STAGES, bool LSMEM>
 struct TcLayout {
     static constexpr uint32_t kA = NKB * TC_TILE_BYTES;
     static constexpr uint32_t kB = NKB * TC_TILE_BYTES;
+    // lists: 128 rows x P slots (smem-resident) or 4 warps x P scratch
+    static constexpr uint32_t kL = (LSMEM ? 128 : 4) * TC_LIST_P * 8;
     static constexpr uint32_t kBar = 8 * (2 * STAGES + 5) + 8;
-    static constexpr uint32_t total = 1024 + kA + STAGES * kB + kBar;
+    static constexpr uint32_t total = 1024 + kA + STAGES * kB + kL + kBar;
 };
 
-struct ListState {
-    int cnt;
-    float tau;
-};
-
-// append one passing candidate; compaction when the list is full (rare path)
-__device__ __noinline__ ListState tc_push(float2* L, ListState st, float key, int col, int cap, int R) {
-    L[st.cnt++] = make_float2(key, __int_as_float(col));
-    if (st.cnt == cap) {
-        st.tau = list_compact(L, cap, R);
-        st.cnt = R;
+// warp-cooperative: sort S[0..P) ascending by key (entries >= cnt are +inf)
+__device__ __forceinline__ void warp_bitonic_sort(float2* S, int lane) {
+#pragma unroll 1
+    for (int k = 2; k <= TC_LIST_P; k <<= 1) {
+#pragma unroll 1
+        for (int j = k >> 1; j > 0; j >>= 1) {
+#pragma unroll
+            for (int t = 0; t < TC_LIST_P / 64; ++t) {
+                // pair index p in [0, P/2): element i = ((p & ~(j-1)) << 1) | (p & (j-1)), partner i + j
+                int p = lane + 32 * t;
+                int i = ((p & ~(j - 1)) << 1) | (p & (j - 1));
+                int q = i + j;
+                float2 a = S[i], b = S[q];
+                bool up = (i & k) == 0;
+                bool swap = up ? (a.x > b.x) : (a.x < b.x);
+                if (swap) {
+                    S[i] = b;
+                    S[q] = a;
+                }
+            }
+            __syncwarp();
+        }
     }
-    return st;
 }
 
-template <int NKB, int STAGES>
+template <int NKB, int STAGES, bool LSMEM>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     knn_cand_tc_kernel(const __grid_constant__ CUtensorMap xmap, int64_t n, int64_t ntiles,
                        const float* __restrict__ cnk, float key_scale, int cap, int R, float2* __restrict__ lists,
                        int* __restrict__ counts, float* __restrict__ taus) {
-    using Lay = TcLayout<NKB, STAGES>;
+    using Lay = TcLayout<NKB, STAGES, LSMEM>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = base;
     uint8_t* sB = base + Lay::kA;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * Lay::kB);
+    float2* sL = reinterpret_cast<float2*>(sB + STAGES * Lay::kB);
+    uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sL) + Lay::kL);
     uint64_t* empty = full + STAGES;
     uint64_t* afull = empty + STAGES;
     uint64_t* tfull = afull + 1;   // [2]
@@ -124,10 +145,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
     } else {
         const int quad = warp & 3;
-        const int64_t row = row0 + quad * 32 + lane;
+        const int lrow = quad * 32 + lane;
+        const int64_t row = row0 + lrow;
         const bool valid = row < n;
-        float2* L = lists + (valid ? row : 0) * (int64_t)cap;
-        ListState st{0, INFINITY};
+        // list of this row: smem-resident or global (with a per-warp smem scratch)
+        float2* L = LSMEM ? sL + (size_t)lrow * TC_LIST_P : lists + (valid ? row : 0) * (int64_t)cap;
+        float2* scratch = LSMEM ? nullptr : sL + (size_t)quad * TC_LIST_P;
+        int cnt = 0;
+        float tau = INFINITY;
         for (int64_t t = 0; t < ntiles; ++t) {
             const int buf = (int)(t & 1);
             const uint32_t bph = (uint32_t)((t >> 1) & 1);
@@ -157,12 +182,41 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     }
 #pragma unroll
                     for (int u = 0; u < 16; ++u) m = fminf(m, keys[u]);
-                    if (valid && m < st.tau) {
+                    const bool pass = valid && m < tau;
+                    // make room: warp-cooperative compaction of every list
+                    // that could overflow while taking this chunk
+                    unsigned want = __ballot_sync(0xffffffffu, pass && cnt > cap - 16);
+                    while (want) {
+                        __syncwarp();  // make lane src's appends visible
+                        const int src = __ffs(want) - 1;
+                        want &= want - 1;
+                        const int c_src = __shfl_sync(0xffffffffu, cnt, src);
+                        float2* Ls = LSMEM ? sL + (size_t)(quad * 32 + src) * TC_LIST_P : scratch;
+                        const float2* Lg = lists + (row0 + quad * 32 + src) * (int64_t)cap;
+                        for (int e = lane; e < TC_LIST_P; e += 32) {
+                            float2 val = make_float2(INFINITY, __int_as_float(-1));
+                            if (e < c_src) val = LSMEM ? Ls[e] : Lg[e];
+                            Ls[e] = val;
+                        }
+                        __syncwarp();
+                        warp_bitonic_sort(Ls, lane);
+                        if (!LSMEM) {
+                            float2* Lw = lists + (row0 + quad * 32 + src) * (int64_t)cap;
+                            for (int e = lane; e < R; e += 32) Lw[e] = Ls[e];
+                        }
+                        const float new_tau = Ls[R - 1].x;
+                        __syncwarp();
+                        if (lane == src) {
+                            cnt = R;
+                            tau = new_tau;
+                        }
+                    }
+                    if (pass) {
 #pragma unroll
                         for (int u = 0; u < 16; ++u) {
                             const int64_t col = col0 + c + u;
-                            if (keys[u] < st.tau && col != row && col < n)
-                                st = tc_push(L, st, keys[u], (int)col, cap, R);
+                            if (keys[u] < tau && col != row && col < n)
+                                L[cnt++] = make_float2(keys[u], __int_as_float((int)col));
                         }
                     }
                 }
@@ -172,8 +226,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             if (lane == 0) tc::mbar_arrive(&tempty[buf]);
         }
         if (valid) {
-            counts[row] = st.cnt;
-            taus[row] = st.tau;
+            if (LSMEM) {
+                float2* Lg = lists + row * (int64_t)cap;
+                for (int e = 0; e < cnt; ++e) Lg[e] = L[e];
+            }
+            counts[row] = cnt;
+            taus[row] = tau;
         }
     }
     __syncthreads();
