@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -468,9 +469,30 @@ static int launch_tc(const CUtensorMap& map, int64_t n, int64_t ntiles, const fl
     const uint32_t smem = TcLayout<NKB, STAGES, LSMEM>::total;
     SC_CUDA(cudaFuncSetAttribute(knn_cand_tc_kernel<NKB, STAGES, LSMEM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
+    DevBuf<long long> dbg;
+    const bool want_dbg = std::getenv("SPECLUST_KNN_DEBUG") != nullptr;
+    if (want_dbg) {
+        if (int rc = dbg.alloc((size_t)ntiles * 16)) return rc;
+        SC_CUDA(cudaMemsetAsync(dbg.p, 0, sizeof(long long) * ntiles * 16, st));
+    }
     knn_cand_tc_kernel<NKB, STAGES, LSMEM><<<(unsigned)ntiles, TC_THREADS, smem, st>>>(map, n, ntiles, cnk, key_scale,
-                                                                                       cap, R, lists, counts, taus);
+                                                                                       cap, R, lists, counts, taus,
+                                                                                       dbg.p);
     SC_LAUNCHED(1);
+    if (want_dbg) {
+        std::vector<long long> h((size_t)ntiles * 16);
+        SC_CUDA(cudaMemcpyAsync(h.data(), dbg.p, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, st));
+        SC_CUDA(cudaStreamSynchronize(st));
+        double acc[12] = {0};
+        for (int64_t b = 0; b < ntiles; ++b)
+            for (int q = 0; q < 12; ++q) acc[q] += (double)h[b * 16 + q];
+        const char* names[12] = {"tma.wait_empty", "-", "-", "tma.total", "mma.wait_tempty", "mma.wait_full",
+                                 "mma.latency64", "mma.total", "epi.wait_tfull", "epi.ldtm", "epi.work", "epi.fast"};
+        for (int q = 0; q < 12; ++q)
+            if (names[q][0] != '-')
+                fprintf(stderr, "[knn_tc dbg] %-16s %.1f cycles/tile\n", names[q],
+                        q == 6 ? acc[q] / ntiles / 64 : acc[q] / ntiles / ntiles);
+    }
     return SC_OK;
 }
 
@@ -491,7 +513,7 @@ int knn_candidates_tc(int64_t n, int64_t n_pad, int64_t dp64, const __half* xh, 
     const int64_t ntiles = n_pad / 128;
     ProfScope prof("knn_tile", st, 2.0 * (double)n * (double)n * (double)dp64);
     switch (dp64 / 64) {
-        case 1: return launch_tc<1, 4, true>(map, n, ntiles, cnk, key_scale, cap, R, lists, counts, taus, st);
+        case 1: return launch_tc<1, 4, false>(map, n, ntiles, cnk, key_scale, cap, R, lists, counts, taus, st);
         case 2: return launch_tc<2, 3, false>(map, n, ntiles, cnk, key_scale, cap, R, lists, counts, taus, st);
         case 3: return launch_tc<3, 2, false>(map, n, ntiles, cnk, key_scale, cap, R, lists, counts, taus, st);
         default: return launch_tc<4, 2, false>(map, n, ntiles, cnk, key_scale, cap, R, lists, counts, taus, st);
@@ -504,7 +526,9 @@ int knn_graph_build(int64_t n, int64_t d, const double* x, int64_t knn, double t
     const int64_t dp = (d + 15) / 16 * 16;
     const char* kenv = std::getenv("SPECLUST_KNN_KERNEL");
     const int64_t dp64 = (d + 63) / 64 * 64;
-    const int64_t tc_margin = std::max<int64_t>(12, knn / 2 + 8);
+    // candidate margin beyond knn for the fp16 keys (tuning knob for experiments)
+    const char* menv = std::getenv("SPECLUST_KNN_MARGIN");
+    const int64_t tc_margin = menv ? std::max<int64_t>(1, std::atoll(menv)) : std::max<int64_t>(12, knn / 2 + 8);
     // the tensor-core path sorts lists of <= TC_LIST_P slots and needs R + 16 <= cap
     const bool use_tc = dp64 <= 256 && knn + tc_margin + 16 <= TC_LIST_P && n > 2 * (knn + tc_margin) + 1 &&
                         !(kenv && std::strcmp(kenv, "simt") == 0);
@@ -512,9 +536,15 @@ int knn_graph_build(int64_t n, int64_t d, const double* x, int64_t knn, double t
     // tensor-core keys carry a larger error bound than fp32, so keep more.
     const int64_t margin = use_tc ? tc_margin : std::max<int64_t>(8, knn / 2);
     const int R = (int)imin64(n - 1, knn + margin);
-    int cap = use_tc ? (int)std::min<int64_t>(2 * R, TC_LIST_P) : 2 * R;
-    if (cap > n - 1) cap = (int)(n - 1);  // lists can hold every other point
-    if (cap < R) cap = R;
+    int cap;
+    if (use_tc) {
+        // a compaction leaves R entries and must leave room for one 16-column chunk
+        cap = (int)std::min<int64_t>(std::max<int64_t>(2 * R, R + 16), TC_LIST_P);
+    } else {
+        cap = 2 * R;
+        if (cap > n - 1) cap = (int)(n - 1);  // lists can hold every other point
+        if (cap < R) cap = R;
+    }
     int rc;
     DevBuf<double> part, mean, rn, qn;
     DevBuf<float> xf, cnf, taus;

@@ -35,8 +35,9 @@ struct TcLayout {
     static constexpr uint32_t kB = NKB * TC_TILE_BYTES;
     // lists: 128 rows x P slots (smem-resident) or 4 warps x P scratch
     static constexpr uint32_t kL = (LSMEM ? 128 : 4) * TC_LIST_P * 8;
+    static constexpr uint32_t kCn = 2 * 128 * 4;  // column norms of the two in-flight tiles
     static constexpr uint32_t kBar = 8 * (2 * STAGES + 5) + 8;
-    static constexpr uint32_t total = 1024 + kA + STAGES * kB + kL + kBar;
+    static constexpr uint32_t total = 1024 + kA + STAGES * kB + kL + kCn + kBar;
 };
 
 // warp-cooperative: sort S[0..P) ascending by key (entries >= cnt are +inf)
@@ -65,17 +66,19 @@ __device__ __forceinline__ void warp_bitonic_sort(float2* S, int lane) {
 }
 
 template <int NKB, int STAGES, bool LSMEM>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+__global__ void __launch_bounds__(TC_THREADS, LSMEM ? 1 : 2)
     knn_cand_tc_kernel(const __grid_constant__ CUtensorMap xmap, int64_t n, int64_t ntiles,
                        const float* __restrict__ cnk, float key_scale, int cap, int R, float2* __restrict__ lists,
-                       int* __restrict__ counts, float* __restrict__ taus) {
+                       int* __restrict__ counts, float* __restrict__ taus, long long* __restrict__ dbg) {
     using Lay = TcLayout<NKB, STAGES, LSMEM>;
+    long long d_wait0 = 0, d_wait1 = 0, d_work = 0, d_fast = 0, d_t0 = clock64();
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = base;
     uint8_t* sB = base + Lay::kA;
     float2* sL = reinterpret_cast<float2*>(sB + STAGES * Lay::kB);
-    uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sL) + Lay::kL);
+    float* sCn = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(sL) + Lay::kL);  // [2][128]
+    uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sCn) + Lay::kCn);
     uint64_t* empty = full + STAGES;
     uint64_t* afull = empty + STAGES;
     uint64_t* tfull = afull + 1;   // [2]
@@ -94,7 +97,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             }
             tc::mbar_init(afull, 1);
             for (int b = 0; b < 2; ++b) {
-                tc::mbar_init(&tfull[b], 1);
+                // two arrivals per use: the column-norm bulk copy (expect_tx) and the MMA commit
+                tc::mbar_init(&tfull[b], 2);
                 tc::mbar_init(&tempty[b], 4);
             }
             tc::fence_mbar_init();
@@ -113,7 +117,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             for (int64_t t = 0; t < ntiles; ++t) {
                 const int s = (int)(t % STAGES);
                 const uint32_t ph = (uint32_t)((t / STAGES) & 1);
+                long long c0 = clock64();
                 tc::mbar_wait(&empty[s], ph ^ 1);
+                d_wait0 += clock64() - c0;
                 tc::mbar_expect_tx(&full[s], Lay::kB);
                 for (int kb = 0; kb < NKB; ++kb)
                     tc::tma_load_2d(sB + s * Lay::kB + kb * TC_TILE_BYTES, &xmap, &full[s], kb * 64, (int)(t * 128));
@@ -128,8 +134,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 const uint32_t ph = (uint32_t)((t / STAGES) & 1);
                 const int buf = (int)(t & 1);
                 const uint32_t bph = (uint32_t)((t >> 1) & 1);
+                long long c0 = clock64();
                 tc::mbar_wait(&tempty[buf], bph ^ 1);
+                long long c1 = clock64();
                 tc::mbar_wait(&full[s], ph);
+                long long c2 = clock64();
+                d_wait0 += c1 - c0;
+                d_wait1 += c2 - c1;
+                // the accumulator slot is free, so is its column-norm slot
+                tc::mbar_expect_tx(&tfull[buf], 128 * 4);
+                tc::bulk_g2s(sCn + buf * 128, cnk + t * 128, 128 * 4, &tfull[buf]);
                 tc::fence_after();
 #pragma unroll
                 for (int kb = 0; kb < NKB; ++kb) {
@@ -141,6 +155,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 }
                 tc::umma_commit(&empty[s]);
                 tc::umma_commit(&tfull[buf]);
+                if (dbg && t < 64) {  // debug: raw MMA completion latency (first tiles)
+                    long long c3 = clock64();
+                    tc::mbar_wait(&tfull[buf], bph);
+                    d_work += clock64() - c3;
+                }
             }
         }
     } else {
@@ -156,30 +175,42 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         for (int64_t t = 0; t < ntiles; ++t) {
             const int buf = (int)(t & 1);
             const uint32_t bph = (uint32_t)((t >> 1) & 1);
+            long long c0 = clock64();
             tc::mbar_wait(&tfull[buf], bph);
+            long long c1 = clock64();
+            d_wait0 += c1 - c0;
             tc::fence_after();
             const int64_t col0 = t * 128;
             const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * 128);
 #pragma unroll 1
             for (int half = 0; half < 2; ++half) {
                 float v[64];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) tc::tmem_ld16(taddr + half * 64 + q * 16, v + q * 16);
+                const long long h0 = clock64();
+                tc::tmem_ld64(taddr + half * 64, v);
                 tc::tmem_wait_ld();
+                const long long h1 = clock64();
+                d_wait1 += h1 - h0;
+                const float4* cp = reinterpret_cast<const float4*>(sCn + buf * 128 + half * 64);
+                float m0 = INFINITY, m1 = INFINITY;
+#pragma unroll
+                for (int u = 0; u < 16; ++u) {
+                    const float4 cn4 = cp[u];  // smem broadcast
+                    v[4 * u + 0] = fmaf(key_scale, v[4 * u + 0], cn4.x);
+                    v[4 * u + 1] = fmaf(key_scale, v[4 * u + 1], cn4.y);
+                    v[4 * u + 2] = fmaf(key_scale, v[4 * u + 2], cn4.z);
+                    v[4 * u + 3] = fmaf(key_scale, v[4 * u + 3], cn4.w);
+                    m0 = fminf(m0, fminf(v[4 * u + 0], v[4 * u + 1]));
+                    m1 = fminf(m1, fminf(v[4 * u + 2], v[4 * u + 3]));
+                }
+                // steady state: no row of the warp improves -> one vote per 64 columns
+                const bool any = __any_sync(0xffffffffu, valid && fminf(m0, m1) < tau);
+                d_fast += clock64() - h1;
+                if (!any) continue;
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const int c = half * 64 + q * 16;
-                    const float4* cp = reinterpret_cast<const float4*>(cnk + col0 + c);
-                    float keys[16];
+                    const float* keys = v + q * 16;
                     float m = INFINITY;
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        float4 cn4 = __ldg(cp + u);
-                        keys[4 * u + 0] = fmaf(key_scale, v[q * 16 + 4 * u + 0], cn4.x);
-                        keys[4 * u + 1] = fmaf(key_scale, v[q * 16 + 4 * u + 1], cn4.y);
-                        keys[4 * u + 2] = fmaf(key_scale, v[q * 16 + 4 * u + 2], cn4.z);
-                        keys[4 * u + 3] = fmaf(key_scale, v[q * 16 + 4 * u + 3], cn4.w);
-                    }
 #pragma unroll
                     for (int u = 0; u < 16; ++u) m = fminf(m, keys[u]);
                     const bool pass = valid && m < tau;
@@ -224,6 +255,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             tc::fence_before();
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&tempty[buf]);
+            d_work += clock64() - c1;
         }
         if (valid) {
             if (LSMEM) {
@@ -233,6 +265,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             counts[row] = cnt;
             taus[row] = tau;
         }
+    }
+    if (dbg && lane == 0 && warp < 3) {
+        long long* o = dbg + (size_t)blockIdx.x * 16 + warp * 4;
+        o[0] = d_wait0;
+        o[1] = d_wait1;
+        o[2] = d_work;
+        o[3] = warp == 2 ? d_fast : clock64() - d_t0;
     }
     __syncthreads();
     if (warp == 1) {
