@@ -540,6 +540,24 @@ static double np_pairwise_sum(const double* a, int64_t n) {
     return np_pairwise_sum(a, n2) + np_pairwise_sum(a + n2, n - n2);
 }
 
+// labels[i] = nearest of the k rows of c (fp64 distance tiles, ties -> lowest)
+int assign_nearest(int64_t n, int64_t d, const double* v, int64_t k, const double* c, int64_t* labels,
+                   cudaStream_t st) {
+    const int64_t nb = ceil_div(n, TP);
+    DevBuf<double> vn, cn, cost, part;
+    DevBuf<unsigned long long> changes;
+    int rc;
+    if ((rc = vn.alloc(n)) || (rc = cn.alloc(k)) || (rc = cost.alloc(n)) || (rc = part.alloc(nb)) ||
+        (rc = changes.alloc(1)))
+        return rc;
+    rownorm_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, d, v, vn.p);
+    rownorm_kernel<<<(unsigned)ceil_div(k, 256), 256, 0, st>>>(k, d, c, cn.p);
+    dist_tile_kernel<0><<<(unsigned)nb, 256, 0, st>>>(n, k, d, v, vn.p, c, cn.p, nullptr, labels, nullptr, cost.p,
+                                                      changes.p, part.p);
+    SC_LAUNCHED(3);
+    return SC_OK;
+}
+
 }  // namespace sc
 
 using namespace sc;

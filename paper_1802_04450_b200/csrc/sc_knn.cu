@@ -29,6 +29,7 @@
 #include "sc_list.cuh"
 #include "sc_knn_tc.cuh"
 #include "sc_scan.cuh"
+#include "sc_sparse.cuh"
 
 namespace sc {
 
@@ -50,6 +51,14 @@ __global__ void colmean_finish_kernel(int64_t nb, int64_t n, int64_t d, const do
     double a = 0.0;
     for (int64_t b = 0; b < nb; ++b) a += part[b * d + c];
     mean[c] = a / (double)n;
+}
+
+// pivots for the scan order: rows floor(c * n / C), c < C
+__global__ void gather_strided_rows_kernel(int64_t n, int64_t d, int64_t C, const double* __restrict__ x,
+                                           double* __restrict__ out) {
+    const int64_t c = blockIdx.x;
+    const int64_t r = c * n / C;
+    for (int64_t l = threadIdx.x; l < d; l += blockDim.x) out[c * d + l] = x[r * d + l];
 }
 
 // xf = fp32(x - mean) padded to dp columns; cnf = fp32(|xf|^2) (computed in
@@ -204,20 +213,25 @@ __global__ void __launch_bounds__(256) knn_recheck_kernel(int64_t n, int64_t d, 
                                                           const float* __restrict__ taus,
                                                           const double* __restrict__ rn, const double* __restrict__ qn,
                                                           const unsigned long long* __restrict__ rmax_bits,
-                                                          double cdelta, int32_t* __restrict__ sel,
+                                                          double cdelta, const int32_t* __restrict__ perm,
+                                                          int32_t* __restrict__ sel,
                                                           int32_t* __restrict__ flagged,
                                                           unsigned long long* __restrict__ nflag) {
+    // lists/counts/taus are in scan order (position ip holds point perm[ip]);
+    // everything else, including the (-s, j) tie-break, uses original indices
     extern __shared__ unsigned char rsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double* S = reinterpret_cast<double*>(rsm) + (size_t)warp * cap;
     int* J = reinterpret_cast<int*>(reinterpret_cast<double*>(rsm) + (size_t)8 * cap) + (size_t)warp * cap;
-    const int64_t i = (int64_t)blockIdx.x * 8 + warp;
-    if (i >= n) return;
-    const int cnt = counts[i];
-    const float2* L = lists + i * (int64_t)cap;
+    const int64_t ip = (int64_t)blockIdx.x * 8 + warp;
+    if (ip >= n) return;
+    const int64_t i = perm ? (int64_t)perm[ip] : ip;
+    const int cnt = counts[ip];
+    const float2* L = lists + ip * (int64_t)cap;
     const double* xi = x + i * d;
     for (int t = lane; t < cnt; t += 32) {
         int j = __float_as_int(L[t].y);
+        if (perm) j = perm[j];
         double d2 = exact_d2(xi, x + (int64_t)j * d, d);
         S[t] = exp(inv * d2);
         J[t] = j;
@@ -236,7 +250,7 @@ __global__ void __launch_bounds__(256) knn_recheck_kernel(int64_t n, int64_t d, 
     // broadcast s_k (held by exactly one lane)
     for (int o = 16; o > 0; o >>= 1) s_k = fmin(s_k, __shfl_xor_sync(0xffffffffu, s_k, o));
     if (lane != 0) return;
-    float tau = taus[i];
+    float tau = taus[ip];
     bool ok;
     if (cnt < knn) {
         ok = false;
@@ -571,6 +585,10 @@ int knn_graph_build(int64_t n, int64_t d, const double* x, int64_t knn, double t
     SC_CUDA(cudaMemsetAsync(nflag.p, 0, sizeof(unsigned long long), st));
     SC_LAUNCHED(2);
     double cdelta;
+    const int32_t* perm = nullptr;  // scan order -> original index (nullptr: identity)
+    DevBuf<double> piv;
+    DevBuf<int64_t> plab;
+    Bucketer bk;
     if (use_tc) {
         knn_rownorm_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, st>>>(n, d, x, mean.p, rn.p, rmax.p);
         SC_LAUNCHED(1);
@@ -581,9 +599,20 @@ int knn_graph_build(int64_t n, int64_t d, const double* x, int64_t knn, double t
         std::memcpy(&rm, &rb, sizeof(rm));
         // power-of-two scale: every |element| <= 128, |row|^2 stays far from overflow
         const double scale = rm > 0 ? std::ldexp(1.0, (int)std::floor(std::log2(128.0 / rm))) : 1.0;
+        // locality order for the scan: points bucketed (stably) by their nearest
+        // of C strided pivots, so a query tile's neighbours sit in nearby
+        // candidate tiles and its threshold tightens within the first tiles
+        if (n >= 4096 && !std::getenv("SPECLUST_KNN_NOSORT")) {
+            const int64_t C = std::min<int64_t>(1024, std::max<int64_t>(8, n / 1024));
+            if ((rc = piv.alloc((size_t)C * d)) || (rc = plab.alloc(n)) || (rc = bk.init(n, C))) return rc;
+            gather_strided_rows_kernel<<<(unsigned)C, 128, 0, st>>>(n, d, C, x, piv.p);
+            SC_LAUNCHED(1);
+            if ((rc = assign_nearest(n, d, x, C, piv.p, plab.p, st)) || (rc = bk.run(plab.p, st))) return rc;
+            perm = bk.members.p;
+        }
         if ((rc = xh.alloc((size_t)n_pad * dp64)) || (rc = cnf.alloc(n_pad))) return rc;
-        knn_prep_f16_kernel<<<(unsigned)ceil_div(n_pad, 8), 256, 0, st>>>(n, n_pad, d, dp64, x, mean.p, scale, xh.p,
-                                                                          cnf.p, qn.p);
+        knn_prep_f16_kernel<<<(unsigned)ceil_div(n_pad, 8), 256, 0, st>>>(n, n_pad, d, dp64, x, mean.p, scale, perm,
+                                                                          xh.p, cnf.p, qn.p);
         SC_LAUNCHED(1);
         if ((rc = knn_candidates_tc(n, n_pad, dp64, xh.p, cnf.p, (float)(-2.0 / (scale * scale)), cap, R, lists.p,
                                     counts.p, taus.p, st)))
@@ -612,8 +641,8 @@ int knn_graph_build(int64_t n, int64_t d, const double* x, int64_t knn, double t
         cudaFuncSetAttribute(knn_recheck_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         ProfScope prof("knn_recheck", st, (double)n * cap * d * 8.0);
         knn_recheck_kernel<<<(unsigned)ceil_div(n, 8), 256, smem, st>>>(n, d, x, knn, inv, cap, lists.p, counts.p,
-                                                                        taus.p, rn.p, qn.p, rmax.p, cdelta, sel.p,
-                                                                        flagged.p, nflag.p);
+                                                                        taus.p, rn.p, qn.p, rmax.p, cdelta, perm,
+                                                                        sel.p, flagged.p, nflag.p);
         SC_LAUNCHED(1);
     }
     unsigned long long hflag = 0;

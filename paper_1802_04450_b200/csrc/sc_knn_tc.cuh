@@ -122,7 +122,8 @@ __global__ void __launch_bounds__(TC_THREADS, LSMEM ? 1 : 2)
                 d_wait0 += clock64() - c0;
                 tc::mbar_expect_tx(&full[s], Lay::kB);
                 for (int kb = 0; kb < NKB; ++kb)
-                    tc::tma_load_2d(sB + s * Lay::kB + kb * TC_TILE_BYTES, &xmap, &full[s], kb * 64, (int)(t * 128));
+                    tc::tma_load_2d(sB + s * Lay::kB + kb * TC_TILE_BYTES, &xmap, &full[s], kb * 64,
+                                    (int)(((blockIdx.x + t) % ntiles) * 128));
             }
         }
     } else if (warp == 1) {
@@ -143,7 +144,7 @@ __global__ void __launch_bounds__(TC_THREADS, LSMEM ? 1 : 2)
                 d_wait1 += c2 - c1;
                 // the accumulator slot is free, so is its column-norm slot
                 tc::mbar_expect_tx(&tfull[buf], 128 * 4);
-                tc::bulk_g2s(sCn + buf * 128, cnk + t * 128, 128 * 4, &tfull[buf]);
+                tc::bulk_g2s(sCn + buf * 128, cnk + ((blockIdx.x + t) % ntiles) * 128, 128 * 4, &tfull[buf]);
                 tc::fence_after();
 #pragma unroll
                 for (int kb = 0; kb < NKB; ++kb) {
@@ -180,7 +181,8 @@ __global__ void __launch_bounds__(TC_THREADS, LSMEM ? 1 : 2)
             long long c1 = clock64();
             d_wait0 += c1 - c0;
             tc::fence_after();
-            const int64_t col0 = t * 128;
+            // scan order: the query tile's own (locality-sorted) neighbourhood first
+            const int64_t col0 = ((blockIdx.x + t) % ntiles) * 128;
             const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * 128);
 #pragma unroll 1
             for (int half = 0; half < 2; ++half) {
@@ -283,16 +285,19 @@ __global__ void __launch_bounds__(TC_THREADS, LSMEM ? 1 : 2)
 // fp16 operand prep: xh = fp16(scale * (x - mean)) padded to (n_pad x dp);
 // cnk = |xh|^2 / scale^2 (fp64 sum of the fp16 values, +inf on padding rows);
 // qn = same in fp64 for query rows.
+// Rows are written in scan order: position i holds original point perm[i]
+// (perm == nullptr: identity); qn is indexed by the original point.
 __global__ void knn_prep_f16_kernel(int64_t n, int64_t n_pad, int64_t d, int64_t dp, const double* __restrict__ x,
-                                    const double* __restrict__ mean, double scale, __half* __restrict__ xh,
-                                    float* __restrict__ cnk, double* __restrict__ qn) {
+                                    const double* __restrict__ mean, double scale, const int32_t* __restrict__ perm,
+                                    __half* __restrict__ xh, float* __restrict__ cnk, double* __restrict__ qn) {
     int64_t i = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     int lane = threadIdx.x & 31;
     if (i >= n_pad) return;
+    const int64_t src = (i < n && perm) ? (int64_t)perm[i] : i;
     double acc = 0.0;
     for (int64_t c = lane; c < dp; c += 32) {
         __half h = __float2half_rn(0.f);
-        if (i < n && c < d) h = __double2half((x[i * d + c] - mean[c]) * scale);
+        if (i < n && c < d) h = __double2half((x[src * d + c] - mean[c]) * scale);
         xh[i * dp + c] = h;
         double hv = (double)__half2float(h);
         acc = fma(hv, hv, acc);
@@ -302,7 +307,7 @@ __global__ void knn_prep_f16_kernel(int64_t n, int64_t n_pad, int64_t d, int64_t
         double inv_s2 = 1.0 / (scale * scale);
         if (i < n) {
             cnk[i] = (float)(acc * inv_s2);
-            qn[i] = acc * inv_s2;
+            qn[src] = acc * inv_s2;
         } else {
             cnk[i] = INFINITY;
         }

@@ -23,4 +23,9 @@ struct Bucketer {
     int run(const int64_t* labels, cudaStream_t st);
 };
 
+// labels[i] = index of the nearest of the k rows of c (fp64 Gram-expansion
+// distance tiles; ties -> lowest index)
+int assign_nearest(int64_t n, int64_t d, const double* v, int64_t k, const double* c, int64_t* labels,
+                   cudaStream_t st);
+
 }  // namespace sc
