@@ -188,10 +188,14 @@ int sc_lloyd(int64_t n, int64_t d, int64_t k, const double* v, const double* c_i
              double* sse_history, int64_t* iters_out, sc_stream_t stream);
 
 /* ---- metrics ---------------------------------------------------------------- */
-/* ncut over labels in [0, k) (metrics.py:59-67); *out host.  Returns
- * SC_ERR_VALUE with *out = -1 when a part has zero volume. */
+/* ncut over labels (dev int64) in [0, k) (metrics.py:59-67); *out host.
+ * skip_empty=1 drops parts without members first (the pipeline's np.unique
+ * compaction, pipeline.py:256-257) and *occupied (host, optional) receives
+ * the number of occupied parts.  Returns SC_ERR_VALUE with *out = -1 when a
+ * remaining part has zero volume. */
 int sc_ncut(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* vals,
-            const int64_t* labels, int64_t k, double* out, sc_stream_t stream);
+            const int64_t* labels, int64_t k, int skip_empty, double* out, int64_t* occupied,
+            sc_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -72,7 +72,7 @@ SIGNATURES = {
     "sc_kmeanspp_candidates": (i32, [vp, P_i64, P_i64]),
     "sc_kmeanspp_pick": (i32, [vp, i32, f64, i64, P_i64]),
     "sc_lloyd": (i32, [i64, i64, i64, vp, vp, i64, i64, vp, vp, P_f64, P_i64, vp]),
-    "sc_ncut": (i32, [i64, vp, vp, vp, vp, i64, P_f64, vp]),
+    "sc_ncut": (i32, [i64, vp, vp, vp, vp, i64, i32, P_f64, P_i64, vp]),
 }
 
 # status code -> exception class (include/speclust_b200.h enum)

@@ -279,16 +279,17 @@ __global__ void centroid_mean_kernel(int64_t k, int64_t d, const double* __restr
         return;
     }
     if (dim >= d) return;
+    // the sum is a strictly sequential chain (point order); only the loads are
+    // batched, 16 in flight per thread, so the chain runs at add latency
     double acc = 0.0;
     int64_t m = b;
-    for (; m + 4 <= e; m += 4) {
-        int32_t i0 = members[m], i1 = members[m + 1], i2 = members[m + 2], i3 = members[m + 3];
-        double x0 = v[(int64_t)i0 * d + dim], x1 = v[(int64_t)i1 * d + dim];
-        double x2 = v[(int64_t)i2 * d + dim], x3 = v[(int64_t)i3 * d + dim];
-        acc = __dadd_rn(acc, x0);
-        acc = __dadd_rn(acc, x1);
-        acc = __dadd_rn(acc, x2);
-        acc = __dadd_rn(acc, x3);
+    constexpr int B = 16;
+    for (; m + B <= e; m += B) {
+        double x[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) x[u] = __ldg(v + (int64_t)__ldg(members + m + u) * d + dim);
+#pragma unroll
+        for (int u = 0; u < B; ++u) acc = __dadd_rn(acc, x[u]);
     }
     for (; m < e; ++m) acc = __dadd_rn(acc, v[(int64_t)members[m] * d + dim]);
     cent[cl * d + dim] = __ddiv_rn(acc, (double)(e - b));
@@ -497,21 +498,40 @@ __global__ void kpp_nth_free_kernel(int64_t n, const uint8_t* __restrict__ taken
 }
 
 // ---------------------------------------------------------------------------
-// ncut (metrics.py:34-39, 59-67): per part, one sequential chain over member
-// rows in ascending order reproduces the reference's bincount order.
-__global__ void ncut_parts_kernel(int64_t k, const int64_t* __restrict__ row_ptr,
-                                  const int32_t* __restrict__ col, const double* __restrict__ vals,
-                                  const double* __restrict__ deg, const int64_t* __restrict__ labels,
+// ncut (metrics.py:34-39, 59-67).  Per row (warp): degree and the weight of
+// the row's entries that cross to another part; per part: one sequential
+// chain over its member rows in ascending order.
+__global__ void ncut_rows_kernel(int64_t n, const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                                 const double* __restrict__ vals, const int64_t* __restrict__ labels,
+                                 double* __restrict__ deg, double* __restrict__ cross) {
+    const int64_t i = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    if (i >= n) return;
+    const int64_t li = labels[i];
+    double dg = 0.0, cr = 0.0;
+    for (int64_t p = row_ptr[i] + lane; p < row_ptr[i + 1]; p += 32) {
+        const double v = vals[p];
+        dg += v;
+        if (labels[col[p]] != li) cr += v;
+    }
+    dg = warp_sum(dg);
+    cr = warp_sum(cr);
+    if (lane == 0) {
+        deg[i] = dg;
+        cross[i] = cr;
+    }
+}
+
+__global__ void ncut_parts_kernel(int64_t k, const double* __restrict__ deg, const double* __restrict__ cross,
                                   const int64_t* __restrict__ start, const int32_t* __restrict__ members,
                                   double* __restrict__ bnd, double* __restrict__ vol) {
     int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= k) return;
     double b = 0.0, v = 0.0;
     for (int64_t m = start[c]; m < start[c + 1]; ++m) {
-        int64_t i = members[m];
-        v = __dadd_rn(v, deg[i]);
-        for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p)
-            if (labels[col[p]] != c) b = __dadd_rn(b, vals[p]);
+        const int64_t i = members[m];
+        v += deg[i];
+        b += cross[i];
     }
     bnd[c] = b;
     vol[c] = v;
@@ -749,29 +769,41 @@ int sc_kmeanspp_pick(sc_kmeanspp_t* s, int mode, double u, int64_t r, int64_t* i
 }
 
 int sc_ncut(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* vals,
-            const int64_t* labels, int64_t k, double* out, sc_stream_t stream) {
+            const int64_t* labels, int64_t k, int skip_empty, double* out, int64_t* occupied,
+            sc_stream_t stream) {
     *out = -1.0;
     if (n < 1 || k < 1) return fail(SC_ERR_VALUE, "ncut needs n >= 1 and k >= 1");
     cudaStream_t st = as_stream(stream);
-    DevBuf<double> deg, bnd, vol;
+    DevBuf<double> deg, cross, bnd, vol;
     Bucketer bk;
     int rc;
-    if ((rc = deg.alloc(n)) || (rc = bnd.alloc(k)) || (rc = vol.alloc(k)) || (rc = bk.init(n, k))) return rc;
-    if ((rc = degrees_launch(n, row_ptr, vals, deg.p, st))) return rc;
+    if ((rc = deg.alloc(n)) || (rc = cross.alloc(n)) || (rc = bnd.alloc(k)) || (rc = vol.alloc(k)) ||
+        (rc = bk.init(n, k)))
+        return rc;
+    ProfScope prof("ncut", st, 0.0);
     if ((rc = bk.run(labels, st))) return rc;
-    ncut_parts_kernel<<<(unsigned)ceil_div(k, 64), 64, 0, st>>>(k, row_ptr, col, vals, deg.p, labels, bk.start.p,
-                                                                 bk.members.p, bnd.p, vol.p);
-    SC_LAUNCHED(1);
+    ncut_rows_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, st>>>(n, row_ptr, col, vals, labels, deg.p, cross.p);
+    ncut_parts_kernel<<<(unsigned)ceil_div(k, 64), 64, 0, st>>>(k, deg.p, cross.p, bk.start.p, bk.members.p, bnd.p,
+                                                                 vol.p);
+    SC_LAUNCHED(2);
     std::vector<double> hb(k), hv(k);
+    std::vector<int64_t> hs(k + 1);
     SC_CUDA(cudaMemcpyAsync(hb.data(), bnd.p, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
     SC_CUDA(cudaMemcpyAsync(hv.data(), vol.p, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
+    SC_CUDA(cudaMemcpyAsync(hs.data(), bk.start.p, sizeof(int64_t) * (k + 1), cudaMemcpyDeviceToHost, st));
     SC_CUDA(cudaStreamSynchronize(st));
-    std::vector<double> q(k);
+    // parts in label order; empty parts are dropped when compacting (the
+    // pipeline's np.unique relabelling, pipeline.py:256-257)
+    std::vector<double> q;
+    q.reserve(k);
     for (int64_t c = 0; c < k; ++c) {
+        const bool empty = hs[c + 1] == hs[c];
+        if (empty && skip_empty) continue;
         if (!(hv[c] > 0.0)) return fail(SC_ERR_VALUE, "part " + std::to_string(c) + " has zero volume");
-        q[c] = hb[c] / hv[c];
+        q.push_back(hb[c] / hv[c]);
     }
-    *out = 0.5 * np_pairwise_sum(q.data(), k);
+    if (occupied) *occupied = (int64_t)q.size();
+    *out = 0.5 * np_pairwise_sum(q.data(), (int64_t)q.size());
     return SC_OK;
 }
 

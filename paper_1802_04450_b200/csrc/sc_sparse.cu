@@ -4,6 +4,8 @@
 // Device CSR layout: row_ptr int64[n+1],
 // col int32[nnz] (n < 2^31), vals f64[nnz]; rows sorted, columns strictly
 // increasing within a row (sparse.py:110-138).
+#include <cstdlib>
+
 #include "sc_common.cuh"
 #include "sc_sparse.cuh"
 
@@ -64,6 +66,8 @@ int spmv_launch(int64_t n, int64_t nnz, const int64_t* row_ptr, const int32_t* c
         spmv_seq_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, row_ptr, col, vals, x, y);
     } else {
         double mean = n ? (double)nnz / (double)n : 0.0;
+        static const char* genv = std::getenv("SPECLUST_SPMV_G");  // tuning override
+        if (genv) mean = std::atoi(genv) == 32 ? 100 : std::atoi(genv) == 16 ? 20 : std::atoi(genv) == 8 ? 8 : 1;
         if (mean > 24) {
             spmv_vec_kernel<32><<<(unsigned)ceil_div(n * 32, 256), 256, 0, st>>>(n, row_ptr, col, vals, x, y);
         } else if (mean > 10) {

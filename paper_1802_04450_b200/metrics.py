@@ -54,14 +54,17 @@ def ratio_cut(w, labels, k: int | None = None) -> float:
     return 0.5 * float((bnd / sizes).sum())
 
 
-def ncut_device(w: DeviceCsr, labels_dev, k: int) -> float:
+def ncut_device(w: DeviceCsr, labels_dev, k: int, skip_empty: bool = False):
+    """(ncut, occupied parts) on device labels; ``skip_empty`` reproduces the
+    pipeline's label compaction (pipeline.py:256-257) without a host pass."""
     out = nat.C.c_double(-1.0)
+    occ = nat.C.c_int64(0)
     rc = nat.load().sc_ncut(w.n_rows, nat.ptr(w.row_ptr), nat.ptr(w.col), nat.ptr(w.vals), nat.ptr(labels_dev), k,
-                            nat.C.byref(out), nat.stream_handle())
+                            1 if skip_empty else 0, nat.C.byref(out), nat.C.byref(occ), nat.stream_handle())
     if rc == -1 and out.value < 0:
         raise ZeroVolumePart(nat.last_error())
     nat.check(rc)
-    return float(out.value)
+    return float(out.value), int(occ.value)
 
 
 def ncut(w, labels, k: int | None = None) -> float:
@@ -71,7 +74,7 @@ def ncut(w, labels, k: int | None = None) -> float:
     if w.n_rows == 0:
         return 0.0
     d = w if isinstance(w, DeviceCsr) else w.device()
-    return ncut_device(d, nat.to_device(lab, torch.int64), k)
+    return ncut_device(d, nat.to_device(lab, torch.int64), k)[0]
 
 
 def adjusted_rand_index(a, b) -> float:

@@ -333,6 +333,17 @@ def test_ncut_matches_oracle(golden):
     g = golden("graph_blobs600")
     w = csr(g["row_ptr"], g["col"], g["vals"])
     lab = np.random.default_rng(0).integers(0, 6, w.n_rows)
-    assert sc.ncut(w, lab) == orc.ncut(g["row_ptr"], g["col"], g["vals"], lab)
+    want = orc.ncut(g["row_ptr"], g["col"], g["vals"], lab)
+    assert abs(sc.ncut(w, lab) - want) <= 1e-13 * want
+    # pipeline form: empty parts skipped == ncut over np.unique-compacted labels
+    from paper_1802_04450_b200.metrics import ncut_device
+    import torch
+
+    lab2 = np.where(lab == 3, 5, lab)  # part 3 empty
+    val, occ = ncut_device(w.device(), torch.from_numpy(lab2).cuda(), 6, skip_empty=True)
+    _, compact = np.unique(lab2, return_inverse=True)
+    assert occ == 5
+    want2 = orc.ncut(g["row_ptr"], g["col"], g["vals"], compact)
+    assert abs(val - want2) <= 1e-13 * want2
     with pytest.raises(sc.errors.ZeroVolumePart):
         sc.ncut(w, lab, k=7)
