@@ -128,7 +128,8 @@ def knn_graph_device(x, knn: int, m: SimilarityMeasure, return_stats: bool = Fal
     _require_exp_decay(m, "knn graph")
     torch = nat.torch_cuda()
     if isinstance(x, torch.Tensor):
-        xd = x.to(dtype=torch.float64).contiguous()
+        # CUDA tensors are used in place; host tensors (e.g. pinned) are copied
+        xd = x.to(device="cuda", dtype=torch.float64, non_blocking=True).contiguous()
         n, d = xd.shape
     else:
         xh = as_points(x)
