@@ -172,7 +172,9 @@ __global__ void __launch_bounds__(SE_THREADS, 1) symeig_kernel(int m, double* __
                 int cnt = 0;
                 for (i = mm - 1; i >= l; --i) {
                     double f = s * e[i], b = c * e[i];
-                    r = hypot(f, g);
+                    // |f|, |g| are O(|T|) here: plain sqrt instead of hypot's
+                    // rescaling, one reciprocal instead of two divisions
+                    r = sqrt(fma(f, f, g * g));
                     e[i + 1] = r;
                     if (r == 0.0) {
                         d[i + 1] -= p;
@@ -180,8 +182,9 @@ __global__ void __launch_bounds__(SE_THREADS, 1) symeig_kernel(int m, double* __
                         early = true;
                         break;
                     }
-                    s = f / r;
-                    c = g / r;
+                    const double ri = 1.0 / r;
+                    s = f * ri;
+                    c = g * ri;
                     g = d[i + 1] - p;
                     r = (d[i] - g) * s + 2.0 * c * b;
                     p = s * r;
