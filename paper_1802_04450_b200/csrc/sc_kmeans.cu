@@ -295,6 +295,61 @@ __global__ void centroid_mean_kernel(int64_t k, int64_t d, const double* __restr
     cent[cl * d + dim] = __ddiv_rn(acc, (double)(e - b));
 }
 
+// Segmented variant for large clusters: each cluster's member list (point
+// order) is cut into segments of CM_SEG members; level 1 sums a segment
+// sequentially (warp = segment x 32 features), level 2 adds the segment sums
+// of a cluster in segment order and divides by the count.  Deterministic;
+// identical to the point-order chain for clusters of <= CM_SEG members.
+constexpr int64_t CM_SEG = 512;
+__global__ void centroid_segsum_kernel(int64_t k, int64_t d, int64_t nseg, const double* __restrict__ v,
+                                       const int64_t* __restrict__ start, const int32_t* __restrict__ members,
+                                       const int64_t* __restrict__ seg_off, double* __restrict__ part) {
+    const int64_t dchunks = ceil_div_dev(d);
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= nseg * dchunks) return;
+    const int64_t s = w / dchunks;
+    const int64_t dim = (w % dchunks) * 32 + lane;
+    // cluster owning global segment s: last c with seg_off[c] <= s
+    int64_t lo = 0, hi = k;
+    while (hi - lo > 1) {
+        int64_t mid = (lo + hi) >> 1;
+        if (seg_off[mid] <= s) lo = mid; else hi = mid;
+    }
+    const int64_t cl = lo;
+    const int64_t b = start[cl] + (s - seg_off[cl]) * CM_SEG;
+    const int64_t e = imin64(start[cl + 1], b + CM_SEG);
+    if (dim >= d) return;
+    double acc = 0.0;
+    int64_t m = b;
+    constexpr int B = 16;
+    for (; m + B <= e; m += B) {
+        double x[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) x[u] = __ldg(v + (int64_t)__ldg(members + m + u) * d + dim);
+#pragma unroll
+        for (int u = 0; u < B; ++u) acc = __dadd_rn(acc, x[u]);
+    }
+    for (; m < e; ++m) acc = __dadd_rn(acc, v[(int64_t)members[m] * d + dim]);
+    part[s * d + dim] = acc;
+}
+
+__global__ void centroid_segmean_kernel(int64_t k, int64_t d, const int64_t* __restrict__ start,
+                                        const int64_t* __restrict__ seg_off, const double* __restrict__ part,
+                                        double* __restrict__ cent) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= k * d) return;
+    const int64_t cl = idx / d, dim = idx % d;
+    const int64_t cnt = start[cl + 1] - start[cl];
+    if (cnt == 0) {
+        cent[idx] = 0.0;
+        return;
+    }
+    double acc = 0.0;
+    for (int64_t s = seg_off[cl]; s < seg_off[cl + 1]; ++s) acc = __dadd_rn(acc, part[s * d + dim]);
+    cent[idx] = __ddiv_rn(acc, (double)cnt);
+}
+
 // argmax of cost over unmarked points, ties -> lowest index (one reseed slot)
 __global__ void argmax_partial_kernel(int64_t n, const double* __restrict__ cost,
                                       const uint8_t* __restrict__ used, double* __restrict__ pv,
@@ -652,22 +707,29 @@ int sc_lloyd(int64_t n, int64_t d, int64_t k, const double* v, const double* c_i
     int64_t* nxt = lab2.p;
     int64_t iters = 0;
     const int64_t dchunks = ceil_div(d, 32);
-    std::vector<int> hempty;
+    std::vector<int64_t> hseg(k + 1, 0);
+    DevBuf<int64_t> seg_off;
+    DevBuf<double> segpart;
+    if ((rc = seg_off.alloc(k + 1)) || (rc = segpart.alloc((size_t)(n / CM_SEG + k + 1) * d))) return rc;
     while (iters < max_iters) {
         // ---- update (kmeans.py:139-156)
         if ((rc = bk.run(cur, st))) return rc;
-        SC_CUDA(cudaMemsetAsync(empty.p, 0, sizeof(int) * k, st));
-        {
-            ProfScope prof("kmeans_update", st, (double)n * d * 8.0 + 12.0 * n + 16.0 * k * d);
-            int64_t warps = k * dchunks;
-            centroid_mean_kernel<<<(unsigned)ceil_div(warps * 32, 256), 256, 0, st>>>(
-                k, d, v, bk.start.p, bk.members.p, centroids, empty.p);
-        }
-        SC_LAUNCHED(1);
-        // empty clusters: count them from the bucket offsets (cheap host read)
+        // cluster sizes (host): segment plan + empty clusters
         std::vector<int64_t> hstart(k + 1);
         SC_CUDA(cudaMemcpyAsync(hstart.data(), bk.start.p, sizeof(int64_t) * (k + 1), cudaMemcpyDeviceToHost, st));
         SC_CUDA(cudaStreamSynchronize(st));
+        for (int64_t c = 0; c < k; ++c) hseg[c + 1] = hseg[c] + ceil_div(hstart[c + 1] - hstart[c], CM_SEG);
+        const int64_t nseg = hseg[k];
+        {
+            ProfScope prof("kmeans_update", st, (double)n * d * 8.0 + 12.0 * n + 16.0 * k * d);
+            SC_CUDA(cudaMemcpyAsync(seg_off.p, hseg.data(), sizeof(int64_t) * (k + 1), cudaMemcpyHostToDevice, st));
+            if (nseg > 0)
+                centroid_segsum_kernel<<<(unsigned)ceil_div(nseg * dchunks * 32, 256), 256, 0, st>>>(
+                    k, d, nseg, v, bk.start.p, bk.members.p, seg_off.p, segpart.p);
+            centroid_segmean_kernel<<<(unsigned)ceil_div(k * d, 256), 256, 0, st>>>(k, d, bk.start.p, seg_off.p,
+                                                                                    segpart.p, centroids);
+        }
+        SC_LAUNCHED(2);
         std::vector<int64_t> empties;
         for (int64_t c = 0; c < k; ++c)
             if (hstart[c + 1] == hstart[c]) empties.push_back(c);

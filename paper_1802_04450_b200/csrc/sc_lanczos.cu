@@ -115,60 +115,6 @@ __global__ void __launch_bounds__(GN_THREADS) gemv_n_update_kernel(int64_t n, in
     }
 }
 
-// Fused CGS middle pass: for each 32-row group, w1 = w - B h1 (written back
-// to w) and h2 += B[rows]^T w1 while the group's basis rows are still in L1.
-// Persistent grid; group g is owned by block g % gridDim.x, so the per-block
-// partials (and their fixed-order reduction) are deterministic.
-constexpr int FZ_ROWS = 32;
-__global__ void __launch_bounds__(256) reorth_fused_kernel(int64_t n, int64_t ld, int ncols,
-                                                           const double* __restrict__ B,
-                                                           const double* __restrict__ h1,
-                                                           double* __restrict__ w, double* __restrict__ part) {
-    extern __shared__ double fsm[];
-    double* hs = fsm;              // ncols: h1
-    double* acc = fsm + ncols;     // ncols: this block's h2 partial
-    __shared__ double red[8][FZ_ROWS];
-    __shared__ double wnew[FZ_ROWS];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int c = threadIdx.x; c < ncols; c += blockDim.x) {
-        hs[c] = h1[c];
-        acc[c] = 0.0;
-    }
-    __syncthreads();
-    const int64_t ngroups = (n + FZ_ROWS - 1) / FZ_ROWS;
-    for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
-        const int64_t r = g * FZ_ROWS + lane;
-        const bool ok = r < n;
-        // phase A: per-warp partial of (B h1)[r] over columns c = warp (mod 8)
-        double a0 = 0.0, a1 = 0.0;
-        int c = warp;
-        for (; c + 8 < ncols; c += 16) {
-            a0 = fma(ok ? __ldg(B + (int64_t)c * ld + r) : 0.0, hs[c], a0);
-            a1 = fma(ok ? __ldg(B + (int64_t)(c + 8) * ld + r) : 0.0, hs[c + 8], a1);
-        }
-        if (c < ncols) a0 = fma(ok ? __ldg(B + (int64_t)c * ld + r) : 0.0, hs[c], a0);
-        red[warp][lane] = a0 + a1;
-        __syncthreads();
-        if (warp == 0) {
-            double s = 0.0;
-#pragma unroll
-            for (int q = 0; q < 8; ++q) s += red[q][lane];
-            double v = ok ? w[r] - s : 0.0;
-            if (ok) w[r] = v;
-            wnew[lane] = v;
-        }
-        __syncthreads();
-        // phase B: column dots with the updated rows (L1-resident re-read)
-        const double wl = wnew[lane];
-        for (int c2 = warp; c2 < ncols; c2 += 8) {
-            double t = warp_sum((ok ? __ldg(B + (int64_t)c2 * ld + r) : 0.0) * wl);
-            if (lane == 0) acc[c2] += t;
-        }
-        __syncthreads();
-    }
-    for (int c = threadIdx.x; c < ncols; c += blockDim.x) part[(int64_t)blockIdx.x * ncols + c] = acc[c];
-}
-
 // per-block partial sums of x^2 and non-finite detection
 __global__ void sumsq_partial_kernel(int64_t n, const double* __restrict__ x, double* __restrict__ part,
                                      int* __restrict__ nonfinite) {
@@ -547,19 +493,14 @@ struct sc_lanczos {
         }
         const int cnt = (int)(j + 1);
         {
-            // three passes over the basis: h1 = B^T w; fused {w -= B h1; h2 = B^T w};
-            // w -= B h2 (+ |w|^2)
-            ProfScope prof("reorth", st, 3.0 * (double)n * cnt * 8.0);
+            // two CGS passes = four GEMV passes over the basis
+            ProfScope prof("reorth", st, 4.0 * (double)n * cnt * 8.0);
             if ((rc = project(w.p, cnt))) return rc;  // h[j] = alpha = q_j^T w
+            // keep alpha before the second pass overwrites h
             commit_alpha_kernel<<<1, 32, 0, st>>>(m, j, h.p, T.p, scal.p);
-            const int64_t ngroups = ceil_div(n, FZ_ROWS);
-            const int fz_grid = (int)std::min<int64_t>(fz_blocks, ngroups);
-            reorth_fused_kernel<<<fz_grid, 256, sizeof(double) * 2 * (size_t)cnt, st>>>(n, ld, cnt, B.p, h.p, w.p,
-                                                                                      part.p);
-            reduce_cols_kernel<<<(unsigned)ceil_div((int64_t)cnt * 32, 256), 256, 0, st>>>(fz_grid, cnt, part.p,
-                                                                                          h.p);
-            SC_LAUNCHED(3);
-            if ((rc = subtract(w.p, cnt, true))) return rc;
+            SC_LAUNCHED(1);
+            if ((rc = subtract(w.p, cnt, false))) return rc;
+            if ((rc = project(w.p, cnt)) || (rc = subtract(w.p, cnt, true))) return rc;
         }
         finish_norm_kernel<<<1, 1024, 0, st>>>(nb_n, sqp.p, scal.p, 0);
         SC_LAUNCHED(1);
