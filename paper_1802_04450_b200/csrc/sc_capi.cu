@@ -23,6 +23,25 @@ int cuda_fail(cudaError_t e, const char* what) {
 }
 void count_launch(int n) { g_launches += n; }
 
+cudaStream_t& tl_stream() {
+    static thread_local cudaStream_t s = nullptr;
+    return s;
+}
+
+void ensure_pool() {
+    static bool done = false;
+    if (done) return;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;  // keep freed blocks cached in the pool
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    (void)cudaGetLastError();
+    done = true;
+}
+
 // ---- profiling ---------------------------------------------------------------
 struct ProfSlot {
     std::string name;

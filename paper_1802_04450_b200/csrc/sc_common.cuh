@@ -44,26 +44,42 @@ struct ProfScope {
     ~ProfScope();
 };
 
-// ---- device memory owned by the library (sessions) -------------------------
+// ---- device memory owned by the library ---------------------------------------
+// Scratch comes from the stream-ordered pool (cudaMallocAsync on the stream
+// the calling entry point works on; the pool keeps freed memory, so repeated
+// calls never go back to the driver and never synchronise the device).
+// Entry points set the thread's working stream with StreamScope.
+cudaStream_t& tl_stream();
+void ensure_pool();
+struct StreamScope {
+    cudaStream_t prev;
+    explicit StreamScope(cudaStream_t s) : prev(tl_stream()) { tl_stream() = s; }
+    ~StreamScope() { tl_stream() = prev; }
+};
+
 template <typename T>
 struct DevBuf {
     T* p = nullptr;
     size_t n = 0;
+    cudaStream_t s = nullptr;
     int alloc(size_t count) {
         free();
         n = count;
         if (count == 0) return SC_OK;
-        cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+        ensure_pool();
+        s = tl_stream();
+        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), s);
         if (e != cudaSuccess) {
             p = nullptr;
             n = 0;
             (void)cudaGetLastError();
-            return fail(SC_ERR_NO_MEMORY, "cudaMalloc failed for " + std::to_string(count * sizeof(T)) + " bytes");
+            return fail(SC_ERR_NO_MEMORY, "device allocation failed for " + std::to_string(count * sizeof(T)) +
+                                              " bytes");
         }
         return SC_OK;
     }
     void free() {
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, s);
         p = nullptr;
         n = 0;
     }

@@ -65,6 +65,7 @@ int sc_recover_embedding(int64_t n, int64_t k, const double* u, const double* d,
     if (n < 0 || k < 0) return fail(SC_ERR_VALUE, "negative dimension");
     if (n == 0 || k == 0) return SC_OK;
     cudaStream_t st = as_stream(stream);
+    StreamScope stream_scope(st);
     int64_t nb = ceil_div(n, EMB_ROWS);
     DevBuf<double> part, norms;
     int rc;
@@ -81,6 +82,7 @@ int sc_recover_embedding(int64_t n, int64_t k, const double* u, const double* d,
 int sc_normalize_rows(int64_t n, int64_t k, const double* v, double* out, sc_stream_t stream) {
     if (n <= 0 || k <= 0) return SC_OK;
     cudaStream_t st = as_stream(stream);
+    StreamScope stream_scope(st);
     if (out != v) SC_CUDA(cudaMemcpyAsync(out, v, sizeof(double) * n * k, cudaMemcpyDeviceToDevice, st));
     emb_finish_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, st>>>(n, k, nullptr, 1, out);
     SC_LAUNCHED(1);

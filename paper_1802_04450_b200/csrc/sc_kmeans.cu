@@ -657,6 +657,7 @@ int sc_pairwise_sq_dist(int64_t n, int64_t k, int64_t d, const double* v, const 
     if (n < 0 || k < 0 || d < 0) return fail(SC_ERR_VALUE, "negative dimension");
     if (n == 0 || k == 0) return SC_OK;
     cudaStream_t st = as_stream(stream);
+    StreamScope stream_scope(st);
     DevBuf<double> vn, cn;
     if (int rc = vn.alloc(n)) return rc;
     if (int rc = cn.alloc(k)) return rc;
@@ -675,6 +676,7 @@ int sc_lloyd(int64_t n, int64_t d, int64_t k, const double* v, const double* c_i
     if (n < 1 || k < 1 || d < 0) return fail(SC_ERR_VALUE, "lloyd requires n >= 1, k >= 1");
     if (max_iters < 1) return fail(SC_ERR_VALUE, "max_iters must be >= 1");
     cudaStream_t st = as_stream(stream);
+    StreamScope stream_scope(st);
     const int64_t nb = ceil_div(n, TP);
     DevBuf<double> vn, cn, cost, part, sse;
     DevBuf<int64_t> lab2;
@@ -770,6 +772,7 @@ int sc_lloyd(int64_t n, int64_t d, int64_t k, const double* v, const double* c_i
 
 int sc_kmeanspp_create(int64_t n, int64_t d, const double* v, sc_stream_t stream, sc_kmeanspp_t** out) {
     if (n < 1) return fail(SC_ERR_VALUE, "k-means++ needs n >= 1");
+    StreamScope stream_scope(as_stream(stream));
     auto* s = new sc_kmeanspp();
     s->n = n;
     s->d = d;
@@ -836,6 +839,7 @@ int sc_ncut(int64_t n, const int64_t* row_ptr, const int32_t* col, const double*
     *out = -1.0;
     if (n < 1 || k < 1) return fail(SC_ERR_VALUE, "ncut needs n >= 1 and k >= 1");
     cudaStream_t st = as_stream(stream);
+    StreamScope stream_scope(st);
     DevBuf<double> deg, cross, bnd, vol;
     Bucketer bk;
     int rc;

@@ -705,6 +705,7 @@ extern "C" int sc_knn_graph_f64(int64_t n, int64_t d, const double* x, int64_t k
                                       std::to_string(n));
     if (!(two_sigma_sq > 0)) return fail(SC_ERR_VALUE, "exp_decay requires sigma > 0");
     if (n >= (int64_t)INT32_MAX) return fail(SC_ERR_VALUE, "n must be < 2^31 for int32 column indices");
+    StreamScope stream_scope(as_stream(stream));
     return knn_graph_build(n, d, x, knn, two_sigma_sq, row_ptr, col, vals, nnz_out, stats_out, as_stream(stream));
 }
 

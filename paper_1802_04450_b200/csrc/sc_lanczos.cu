@@ -640,6 +640,7 @@ extern "C" {
 
 int sc_lanczos_create(int64_t n, int64_t k, int64_t m, double tol, int64_t max_restarts, uint64_t seed,
                       sc_stream_t stream, sc_lanczos_t** out) {
+    StreamScope stream_scope(as_stream(stream));
     auto* s = new sc_lanczos();
     int rc = s->init(n, k, m, tol, max_restarts, seed, as_stream(stream));
     if (rc) {
@@ -656,6 +657,7 @@ const double* sc_lanczos_in_slot(const sc_lanczos_t* s) { return s->in_slot(); }
 double* sc_lanczos_out_slot(sc_lanczos_t* s) { return s->w.p; }
 
 int sc_lanczos_advance(sc_lanczos_t* s) {
+    StreamScope stream_scope(s->st);
     int rc = s->advance(true);
     if (rc && rc != SC_ERR_VALUE && rc != SC_ERR_STATE) s->state = 2;
     return rc;
@@ -691,6 +693,7 @@ int sc_eigensolve_csr(int64_t n, const int64_t* row_ptr, const int32_t* col, con
                       int64_t m, double tol, int64_t max_restarts, uint64_t seed, double* values, double* vectors,
                       double* residuals, sc_lanczos_stats* stats, sc_stream_t stream) {
     cudaStream_t st = as_stream(stream);
+    StreamScope stream_scope(st);
     sc_lanczos s;
     int rc = s.init(n, k, m, tol, max_restarts, seed, st);
     if (rc) return rc;
@@ -724,6 +727,7 @@ int sc_symmetry_probe(int64_t n, const int64_t* row_ptr, const int32_t* col, con
     // eigen.py:279-288: three random (x, y) pairs; ratio = |x'Ay - y'Ax| / (|x| |y|)
     // (the caller multiplies the tolerance by max(1, max|a|))
     cudaStream_t st = as_stream(stream);
+    StreamScope stream_scope(st);
     *ratio_out = 0.0;
     if (n <= 0) return SC_OK;
     int64_t nnz = 0;

@@ -182,6 +182,7 @@ int sc_spmv_f64(int64_t n_rows, int64_t n_cols, const int64_t* row_ptr, const in
                 sc_stream_t stream) {
     if (n_rows < 0 || n_cols < 0) return fail(SC_ERR_VALUE, "negative dimension");
     cudaStream_t st = as_stream(stream);
+    StreamScope stream_scope(st);
     int64_t nnz = 0;
     if (n_rows > 0) SC_CUDA(cudaMemcpyAsync(&nnz, row_ptr + n_rows, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     SC_CUDA(cudaStreamSynchronize(st));
@@ -197,6 +198,7 @@ int sc_degrees_f64(int64_t n, const int64_t* row_ptr, const double* vals, double
 int sc_find_nonpositive(int64_t n, const double* d, int mode, int64_t* count_out,
                         int64_t* idx_out, int64_t max_idx, sc_stream_t stream) {
     cudaStream_t st = as_stream(stream);
+    StreamScope stream_scope(st);
     *count_out = 0;
     if (n <= 0) return SC_OK;
     DevBuf<unsigned long long> cnt;
@@ -220,6 +222,7 @@ int sc_sym_scale_f64(int64_t n, const int64_t* row_ptr, const int32_t* col,
                      const double* vals, const double* d, double* out, sc_stream_t stream) {
     if (n <= 0) return SC_OK;
     cudaStream_t st = as_stream(stream);
+    StreamScope stream_scope(st);
     sym_scale_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, st>>>(n, row_ptr, col, vals, d, out);
     SC_LAUNCHED(1);
     return SC_OK;
@@ -231,6 +234,7 @@ int sc_csr_is_symmetric(int64_t n, int64_t nnz, const int64_t* row_ptr, const in
     *result = 1;
     if (n <= 0) return SC_OK;
     cudaStream_t st = as_stream(stream);
+    StreamScope stream_scope(st);
     DevBuf<int> bad;
     if (int rc = bad.alloc(1)) return rc;
     SC_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
