@@ -187,6 +187,57 @@ int sc_lloyd(int64_t n, int64_t d, int64_t k, const double* v, const double* c_i
              int64_t max_iters, int64_t tol_changes, int64_t* labels, double* centroids,
              double* sse_history, int64_t* iters_out, sc_stream_t stream);
 
+/* ---- per-shard building blocks (row-sharded Lanczos, point-sharded k-means;
+ *      driven by paper_1802_04450_b200/distributed.py over NCCL) -------------- */
+/* h = B^T w for the first ncols columns of a column-major shard (ld rows) */
+int sc_gemv_t_f64(int64_t n, int64_t ld, int64_t ncols, const double* B, const double* w, double* h,
+                  sc_stream_t stream);
+/* w -= B h; *sq_out (dev, optional) = |w|^2 of the updated shard */
+int sc_gemv_n_f64(int64_t n, int64_t ld, int64_t ncols, const double* B, const double* h, double* w,
+                  double* sq_out, sc_stream_t stream);
+/* dst = src / div */
+int sc_div_copy_f64(int64_t n, const double* src, double div, double* dst, sc_stream_t stream);
+/* out[i] = normal draw of global element offset + i (shard-independent) */
+int sc_fill_normal(int64_t n, int64_t offset, uint64_t seed, uint64_t stream_id, double* out,
+                   sc_stream_t stream);
+/* eigen-decomposition of the m x m projected matrix (eigen.py:189-192):
+ * theta (dev, m) stable descending, S (dev, m x kout column-major) */
+int sc_symeig_f64(int64_t m, int64_t kout, const double* T, double* theta, double* S, sc_stream_t stream);
+/* C = A (n x kk, col-major lda) * S (kk x kc, col-major lds); C col-major ldc or row-major */
+int sc_dgemm_tall(int64_t n, int64_t kk, int64_t kc, const double* A, int64_t lda, const double* S,
+                  int64_t lds, double* C, int64_t ldc, int rowmajor, sc_stream_t stream);
+/* local assignment: labels/cost, *changes vs old_labels (null -> 0), *sse (host) */
+int sc_kmeans_assign(int64_t n, int64_t d, int64_t k, const double* v, const double* c,
+                     const int64_t* old_labels, int64_t* labels, double* cost, int64_t* changes,
+                     double* sse, sc_stream_t stream);
+/* unnormalised per-cluster sums (point order) and counts of the local points */
+int sc_kmeans_local_sums(int64_t n, int64_t d, int64_t k, const double* v, const int64_t* labels,
+                         double* sums, int64_t* counts, sc_stream_t stream);
+int sc_centroid_divide(int64_t k, int64_t d, const double* sums, const int64_t* counts, double* cent,
+                       sc_stream_t stream);
+/* first e indices (host) of the stable descending order of cost (kmeans.py:151) */
+int sc_farthest(int64_t n, const double* cost, int64_t e, int64_t* idx_out, sc_stream_t stream);
+/* shard-aware k-means++: draw given by coordinates (row dev, d) and the local
+ * index (-1 when the row is on another shard) */
+int sc_kmeanspp_take_row(sc_kmeanspp_t* s, const double* row, int64_t local_index);
+int sc_kmeanspp_weight(sc_kmeanspp_t* s, double* wsum, int64_t* count, int64_t* n_free);
+int sc_kmeanspp_psum(sc_kmeanspp_t* s, double total_global, double* psum);
+int sc_kmeanspp_search(sc_kmeanspp_t* s, double target, int64_t* index);
+int sc_kmeanspp_nth_free(sc_kmeanspp_t* s, int64_t r, int64_t* index);
+/* sym_scale on rows row_offset .. row_offset+n_local-1 (global degree vector) */
+int sc_sym_scale_shard_f64(int64_t n_local, int64_t row_offset, const int64_t* row_ptr, const int32_t* col,
+                           const double* vals, const double* d_global, double* out, sc_stream_t stream);
+/* two-phase embedding of a row shard: scale + column sums of squares (dev k),
+ * then finish with the all-reduced column sums */
+int sc_embed_scale(int64_t n, int64_t k, const double* u, const double* d, double* out, double* colsq,
+                   sc_stream_t stream);
+int sc_embed_finish(int64_t n, int64_t k, const double* colsq, int normalize_rows, double* out,
+                    sc_stream_t stream);
+/* per-part boundary weight, volume and member count of a row shard (dev k each) */
+int sc_ncut_partials(int64_t n_local, int64_t row_offset, const int64_t* row_ptr, const int32_t* col,
+                     const double* vals, const int64_t* labels_global, int64_t k, double* bnd, double* vol,
+                     int64_t* counts, sc_stream_t stream);
+
 /* ---- metrics ---------------------------------------------------------------- */
 /* ncut over labels (dev int64) in [0, k) (metrics.py:59-67); *out host.
  * skip_empty=1 drops parts without members first (the pipeline's np.unique

@@ -73,6 +73,25 @@ SIGNATURES = {
     "sc_kmeanspp_pick": (i32, [vp, i32, f64, i64, P_i64]),
     "sc_lloyd": (i32, [i64, i64, i64, vp, vp, i64, i64, vp, vp, P_f64, P_i64, vp]),
     "sc_ncut": (i32, [i64, vp, vp, vp, vp, i64, i32, P_f64, P_i64, vp]),
+    "sc_gemv_t_f64": (i32, [i64, i64, i64, vp, vp, vp, vp]),
+    "sc_gemv_n_f64": (i32, [i64, i64, i64, vp, vp, vp, vp, vp]),
+    "sc_fill_normal": (i32, [i64, i64, C.c_uint64, C.c_uint64, vp, vp]),
+    "sc_div_copy_f64": (i32, [i64, vp, f64, vp, vp]),
+    "sc_symeig_f64": (i32, [i64, i64, vp, vp, vp, vp]),
+    "sc_dgemm_tall": (i32, [i64, i64, i64, vp, i64, vp, i64, vp, i64, i32, vp]),
+    "sc_kmeans_assign": (i32, [i64, i64, i64, vp, vp, vp, vp, vp, P_i64, P_f64, vp]),
+    "sc_kmeans_local_sums": (i32, [i64, i64, i64, vp, vp, vp, vp, vp]),
+    "sc_centroid_divide": (i32, [i64, i64, vp, vp, vp, vp]),
+    "sc_farthest": (i32, [i64, vp, i64, P_i64, vp]),
+    "sc_kmeanspp_take_row": (i32, [vp, vp, i64]),
+    "sc_kmeanspp_weight": (i32, [vp, P_f64, P_i64, P_i64]),
+    "sc_kmeanspp_psum": (i32, [vp, f64, P_f64]),
+    "sc_kmeanspp_search": (i32, [vp, f64, P_i64]),
+    "sc_kmeanspp_nth_free": (i32, [vp, i64, P_i64]),
+    "sc_sym_scale_shard_f64": (i32, [i64, i64, vp, vp, vp, vp, vp, vp]),
+    "sc_embed_scale": (i32, [i64, i64, vp, vp, vp, vp, vp]),
+    "sc_embed_finish": (i32, [i64, i64, vp, i32, vp, vp]),
+    "sc_ncut_partials": (i32, [i64, i64, vp, vp, vp, vp, i64, vp, vp, vp, vp]),
 }
 
 # status code -> exception class (include/speclust_b200.h enum)

@@ -34,6 +34,21 @@ __global__ void emb_colnorm_kernel(int64_t nb, int64_t k, const double* __restri
     norms[c] = nv == 0.0 ? 1.0 : nv;  // laplacian.py:105 norms[norms == 0] = 1
 }
 
+__global__ void emb_colsum_kernel(int64_t nb, int64_t k, const double* __restrict__ part, double* __restrict__ colsq) {
+    int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= k) return;
+    double acc = 0.0;
+    for (int64_t b = 0; b < nb; ++b) acc = __dadd_rn(acc, part[b * k + c]);
+    colsq[c] = acc;
+}
+
+__global__ void emb_norms_from_sq_kernel(int64_t k, const double* __restrict__ colsq, double* __restrict__ norms) {
+    int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= k) return;
+    double nv = __dsqrt_rn(colsq[c]);
+    norms[c] = nv == 0.0 ? 1.0 : nv;
+}
+
 // divide by column norms, then (optionally) each row by its 2-norm; warp per row
 __global__ void emb_finish_kernel(int64_t n, int64_t k, const double* __restrict__ norms,
                                   int normalize_rows, double* __restrict__ out) {
@@ -76,6 +91,39 @@ int sc_recover_embedding(int64_t n, int64_t k, const double* u, const double* d,
     emb_finish_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, st>>>(n, k, norms.p, normalize_rows, out);
     SC_LAUNCHED(3);
     SC_CUDA(cudaStreamSynchronize(st));
+    return SC_OK;
+}
+
+// Row-sharded embedding: phase 1 scales the local rows and returns their
+// column sums of squares (dev k; all-reduced by the caller), phase 2 divides
+// by the global column norms and optionally normalises rows.
+int sc_embed_scale(int64_t n, int64_t k, const double* u, const double* d, double* out, double* colsq,
+                   sc_stream_t stream) {
+    cudaStream_t st = as_stream(stream);
+    StreamScope stream_scope(st);
+    if (k <= 0) return SC_OK;
+    if (n <= 0) {
+        SC_CUDA(cudaMemsetAsync(colsq, 0, sizeof(double) * k, st));
+        return SC_OK;
+    }
+    int64_t nb = ceil_div(n, EMB_ROWS);
+    DevBuf<double> part;
+    if (int rc = part.alloc(nb * k)) return rc;
+    emb_scale_kernel<<<(unsigned)nb, 256, 0, st>>>(n, k, u, d, out, part.p);
+    emb_colsum_kernel<<<(unsigned)ceil_div(k, 128), 128, 0, st>>>(nb, k, part.p, colsq);
+    SC_LAUNCHED(2);
+    return SC_OK;
+}
+
+int sc_embed_finish(int64_t n, int64_t k, const double* colsq, int normalize_rows, double* out, sc_stream_t stream) {
+    cudaStream_t st = as_stream(stream);
+    StreamScope stream_scope(st);
+    if (n <= 0 || k <= 0) return SC_OK;
+    DevBuf<double> norms;
+    if (int rc = norms.alloc(k)) return rc;
+    emb_norms_from_sq_kernel<<<(unsigned)ceil_div(k, 128), 128, 0, st>>>(k, colsq, norms.p);
+    emb_finish_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, st>>>(n, k, norms.p, normalize_rows, out);
+    SC_LAUNCHED(2);
     return SC_OK;
 }
 

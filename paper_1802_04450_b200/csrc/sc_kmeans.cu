@@ -350,6 +350,27 @@ __global__ void centroid_segmean_kernel(int64_t k, int64_t d, const int64_t* __r
     cent[idx] = __ddiv_rn(acc, (double)cnt);
 }
 
+// unnormalised cluster totals + counts (shard partials for an all-reduce)
+__global__ void centroid_segtotal_kernel(int64_t k, int64_t d, const int64_t* __restrict__ start,
+                                         const int64_t* __restrict__ seg_off, const double* __restrict__ part,
+                                         double* __restrict__ sums, int64_t* __restrict__ counts) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= k * d) return;
+    const int64_t cl = idx / d, dim = idx % d;
+    double acc = 0.0;
+    for (int64_t s = seg_off[cl]; s < seg_off[cl + 1]; ++s) acc = __dadd_rn(acc, part[s * d + dim]);
+    sums[idx] = acc;
+    if (dim == 0) counts[cl] = start[cl + 1] - start[cl];
+}
+
+__global__ void centroid_divide_kernel(int64_t k, int64_t d, const double* __restrict__ sums,
+                                       const int64_t* __restrict__ counts, double* __restrict__ cent) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= k * d) return;
+    const int64_t c = counts[idx / d];
+    cent[idx] = c > 0 ? __ddiv_rn(sums[idx], (double)c) : 0.0;
+}
+
 // argmax of cost over unmarked points, ties -> lowest index (one reseed slot)
 __global__ void argmax_partial_kernel(int64_t n, const double* __restrict__ cost,
                                       const uint8_t* __restrict__ used, double* __restrict__ pv,
@@ -412,8 +433,10 @@ __global__ void reseed_finish_kernel(int nb, const double* __restrict__ pv, cons
 // k-means++ device steps (kmeans.py:101-136)
 // d2 <- min(d2, |v - v[pick]|^2) by direct differences; mark taken; per-block
 // candidate partials (count, weight sum) over untaken rows with d2 > 0.
-__global__ void kpp_update_kernel(int64_t n, int64_t d, const double* __restrict__ v, int64_t pick,
-                                  int first, double* __restrict__ d2, uint8_t* __restrict__ taken,
+// `prow` = coordinates of the drawn row; `pick` = its local index (or -1 when
+// the row lives on another shard)
+__global__ void kpp_update_kernel(int64_t n, int64_t d, const double* __restrict__ v, const double* __restrict__ prow,
+                                  int64_t pick, int first, double* __restrict__ d2, uint8_t* __restrict__ taken,
                                   double* __restrict__ pw, int64_t* __restrict__ pc) {
     __shared__ double sw[8];
     __shared__ int64_t scn[8];
@@ -423,7 +446,7 @@ __global__ void kpp_update_kernel(int64_t n, int64_t d, const double* __restrict
     int64_t cnt = 0;
     if (i < n) {
         const double* r = v + i * d;
-        const double* p = v + pick * d;
+        const double* p = prow;
         double acc = 0.0;
         for (int64_t l = lane; l < d; l += 32) {
             double t = r[l] - p[l];
@@ -537,6 +560,57 @@ __global__ void kpp_search_kernel(int64_t n, int64_t nb, const double* __restric
 }
 
 // r-th untaken row in ascending order (uniform fallback, kmeans.py:133-134)
+// first candidate whose cumulative p (= w / *total) exceeds `target`; -1 if none
+__global__ void kpp_search_target_kernel(int64_t n, int64_t nb, const double* __restrict__ d2,
+                                         const uint8_t* __restrict__ taken, const double* __restrict__ total,
+                                         const double* __restrict__ bsum, double target, int64_t* __restrict__ out) {
+    if (threadIdx.x != 0) return;
+    double run = 0.0;
+    int64_t b = 0;
+    for (; b < nb; ++b) {
+        if (run + bsum[b] > target) break;
+        run += bsum[b];
+    }
+    *out = -1;
+    if (b == nb) {  // target at/above this shard's total: its last candidate
+        for (int64_t i = n - 1; i >= 0; --i)
+            if (!taken[i] && d2[i] > 0.0) {
+                *out = i;
+                return;
+            }
+        return;
+    }
+    const double tot = *total;
+    const int64_t lo = b * KPP_BLK, hi = imin64(n, lo + KPP_BLK);
+    int64_t last = -1;
+    for (int64_t i = lo; i < hi; ++i) {
+        if (taken[i] || !(d2[i] > 0.0)) continue;
+        last = i;
+        run += d2[i] / tot;
+        if (run > target) {
+            *out = i;
+            return;
+        }
+    }
+    *out = last;  // rounding: the block sum said the crossing is here
+}
+
+// one step of the stable descending order: mark and record the argmax
+__global__ void argmax_finish_kernel(int nb, const double* __restrict__ pv, const int64_t* __restrict__ pi,
+                                     uint8_t* __restrict__ used, int64_t* __restrict__ out) {
+    if (threadIdx.x != 0) return;
+    double bv = -INFINITY;
+    int64_t bi = INT64_MAX;
+    for (int b = 0; b < nb; ++b) {
+        if (pv[b] > bv || (pv[b] == bv && pi[b] < bi)) {
+            bv = pv[b];
+            bi = pi[b];
+        }
+    }
+    used[bi] = 1;
+    *out = bi;
+}
+
 __global__ void kpp_nth_free_kernel(int64_t n, const uint8_t* __restrict__ taken, int64_t r,
                                     int64_t* __restrict__ out) {
     if (threadIdx.x != 0) return;
@@ -558,11 +632,11 @@ __global__ void kpp_nth_free_kernel(int64_t n, const uint8_t* __restrict__ taken
 // chain over its member rows in ascending order.
 __global__ void ncut_rows_kernel(int64_t n, const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
                                  const double* __restrict__ vals, const int64_t* __restrict__ labels,
-                                 double* __restrict__ deg, double* __restrict__ cross) {
+                                 double* __restrict__ deg, double* __restrict__ cross, int64_t row_offset = 0) {
     const int64_t i = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
     if (i >= n) return;
-    const int64_t li = labels[i];
+    const int64_t li = labels[row_offset + i];
     double dg = 0.0, cr = 0.0;
     for (int64_t p = row_ptr[i] + lane; p < row_ptr[i + 1]; p += 32) {
         const double v = vals[p];
@@ -575,6 +649,11 @@ __global__ void ncut_rows_kernel(int64_t n, const int64_t* __restrict__ row_ptr,
         deg[i] = dg;
         cross[i] = cr;
     }
+}
+
+__global__ void bucket_sizes_kernel(int64_t k, const int64_t* __restrict__ start, int64_t* __restrict__ counts) {
+    int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c < k) counts[c] = start[c + 1] - start[c];
 }
 
 __global__ void ncut_parts_kernel(int64_t k, const double* __restrict__ deg, const double* __restrict__ cross,
@@ -798,8 +877,9 @@ int sc_kmeanspp_take(sc_kmeanspp_t* s, int64_t index) {
     if (index < 0 || index >= s->n) return fail(SC_ERR_VALUE, "k-means++ index out of range");
     {
         ProfScope prof("kmeanspp", s->st, (double)s->n * s->d * 8.0);
-        kpp_update_kernel<<<(unsigned)s->nb_upd, 256, 0, s->st>>>(s->n, s->d, s->v, index, s->first ? 1 : 0,
-                                                                  s->d2.p, s->taken.p, s->pw.p, s->pc.p);
+        kpp_update_kernel<<<(unsigned)s->nb_upd, 256, 0, s->st>>>(s->n, s->d, s->v, s->v + index * s->d, index,
+                                                                  s->first ? 1 : 0, s->d2.p, s->taken.p, s->pw.p,
+                                                                  s->pc.p);
     }
     kpp_total_kernel<<<1, 1024, 0, s->st>>>(s->nb_upd, s->pw.p, s->pc.p, s->total.p, s->count.p);
     SC_LAUNCHED(2);
@@ -831,6 +911,191 @@ int sc_kmeanspp_pick(sc_kmeanspp_t* s, int mode, double u, int64_t r, int64_t* i
     if (h < 0) return fail(SC_ERR_INTERNAL, "k-means++ draw found no row");
     *index = h;
     return sc_kmeanspp_take(s, h);
+}
+
+// ---- shard-aware k-means++ steps (point shards, global draw order = rank order)
+int sc_kmeanspp_take_row(sc_kmeanspp_t* s, const double* row, int64_t local_index) {
+    {
+        ProfScope prof("kmeanspp", s->st, (double)s->n * s->d * 8.0);
+        kpp_update_kernel<<<(unsigned)s->nb_upd, 256, 0, s->st>>>(s->n, s->d, s->v, row, local_index,
+                                                                  s->first ? 1 : 0, s->d2.p, s->taken.p, s->pw.p,
+                                                                  s->pc.p);
+    }
+    kpp_total_kernel<<<1, 1024, 0, s->st>>>(s->nb_upd, s->pw.p, s->pc.p, s->total.p, s->count.p);
+    SC_LAUNCHED(2);
+    s->first = false;
+    if (local_index >= 0) s->taken_count += 1;
+    return SC_OK;
+}
+
+// local candidate weight sum (sum of d2 over untaken rows with d2 > 0), count, untaken rows
+int sc_kmeanspp_weight(sc_kmeanspp_t* s, double* wsum, int64_t* count, int64_t* n_free) {
+    SC_CUDA(cudaMemcpyAsync(wsum, s->total.p, sizeof(double), cudaMemcpyDeviceToHost, s->st));
+    SC_CUDA(cudaMemcpyAsync(count, s->count.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s->st));
+    SC_CUDA(cudaStreamSynchronize(s->st));
+    *n_free = s->n - s->taken_count;
+    return SC_OK;
+}
+
+// local sum of p = w / total_global over candidates (host *psum)
+int sc_kmeanspp_psum(sc_kmeanspp_t* s, double total_global, double* psum) {
+    SC_CUDA(cudaMemcpyAsync(s->total.p, &total_global, sizeof(double), cudaMemcpyHostToDevice, s->st));
+    kpp_psum_kernel<<<(unsigned)s->nb_p, KPP_BLK, 0, s->st>>>(s->n, s->d2.p, s->taken.p, s->total.p, s->bsum.p);
+    DevBuf<double> out;
+    if (int rc = out.alloc(1)) return rc;
+    sum_partials_kernel<<<1, 1024, 0, s->st>>>(s->nb_p, s->bsum.p, out.p);
+    SC_LAUNCHED(2);
+    SC_CUDA(cudaMemcpyAsync(psum, out.p, sizeof(double), cudaMemcpyDeviceToHost, s->st));
+    SC_CUDA(cudaStreamSynchronize(s->st));
+    return SC_OK;
+}
+
+// first local candidate whose cumulative p exceeds `target` (after sc_kmeanspp_psum);
+// *index = -1 when the crossing is not on this shard
+int sc_kmeanspp_search(sc_kmeanspp_t* s, double target, int64_t* index) {
+    kpp_search_target_kernel<<<1, 32, 0, s->st>>>(s->n, s->nb_p, s->d2.p, s->taken.p, s->total.p, s->bsum.p, target,
+                                                  s->pick.p);
+    SC_LAUNCHED(1);
+    SC_CUDA(cudaMemcpyAsync(index, s->pick.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s->st));
+    SC_CUDA(cudaStreamSynchronize(s->st));
+    return SC_OK;
+}
+
+int sc_kmeanspp_nth_free(sc_kmeanspp_t* s, int64_t r, int64_t* index) {
+    kpp_nth_free_kernel<<<1, 32, 0, s->st>>>(s->n, s->taken.p, r, s->pick.p);
+    SC_LAUNCHED(1);
+    SC_CUDA(cudaMemcpyAsync(index, s->pick.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s->st));
+    SC_CUDA(cudaStreamSynchronize(s->st));
+    return SC_OK;
+}
+
+// ---- per-shard building blocks of point-sharded Lloyd -------------------------------
+// labels/cost for the local points; *changes (host) vs old_labels (or -1 when
+// old_labels is null), *sse (host) = local sum of costs
+int sc_kmeans_assign(int64_t n, int64_t d, int64_t k, const double* v, const double* c, const int64_t* old_labels,
+                     int64_t* labels, double* cost, int64_t* changes, double* sse, sc_stream_t stream) {
+    cudaStream_t st = as_stream(stream);
+    StreamScope stream_scope(st);
+    *changes = 0;
+    *sse = 0.0;
+    if (n <= 0) return SC_OK;
+    const int64_t nb = ceil_div(n, TP);
+    DevBuf<double> vn, cn, part, out;
+    DevBuf<unsigned long long> chg;
+    int rc;
+    if ((rc = vn.alloc(n)) || (rc = cn.alloc(k)) || (rc = part.alloc(nb)) || (rc = out.alloc(1)) ||
+        (rc = chg.alloc(1)))
+        return rc;
+    SC_CUDA(cudaMemsetAsync(chg.p, 0, sizeof(unsigned long long), st));
+    rownorm_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, d, v, vn.p);
+    rownorm_kernel<<<(unsigned)ceil_div(k, 256), 256, 0, st>>>(k, d, c, cn.p);
+    {
+        ProfScope prof("kmeans_assign", st, 2.0 * (double)n * k * d);
+        dist_tile_kernel<0><<<(unsigned)nb, 256, 0, st>>>(n, k, d, v, vn.p, c, cn.p, nullptr, labels, old_labels,
+                                                          cost, chg.p, part.p);
+    }
+    sum_partials_kernel<<<1, 1024, 0, st>>>(nb, part.p, out.p);
+    SC_LAUNCHED(4);
+    unsigned long long hc = 0;
+    SC_CUDA(cudaMemcpyAsync(&hc, chg.p, sizeof(hc), cudaMemcpyDeviceToHost, st));
+    SC_CUDA(cudaMemcpyAsync(sse, out.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+    SC_CUDA(cudaStreamSynchronize(st));
+    *changes = (int64_t)hc;
+    return SC_OK;
+}
+
+// unnormalised per-cluster sums of the local points (point order, segmented)
+// and counts (dev int64)
+int sc_kmeans_local_sums(int64_t n, int64_t d, int64_t k, const double* v, const int64_t* labels, double* sums,
+                         int64_t* counts, sc_stream_t stream) {
+    cudaStream_t st = as_stream(stream);
+    StreamScope stream_scope(st);
+    if (n <= 0) {
+        SC_CUDA(cudaMemsetAsync(sums, 0, sizeof(double) * k * d, st));
+        SC_CUDA(cudaMemsetAsync(counts, 0, sizeof(int64_t) * k, st));
+        return SC_OK;
+    }
+    Bucketer bk;
+    DevBuf<int64_t> seg_off;
+    DevBuf<double> segpart;
+    int rc;
+    if ((rc = bk.init(n, k)) || (rc = seg_off.alloc(k + 1)) ||
+        (rc = segpart.alloc((size_t)(n / CM_SEG + k + 1) * d)))
+        return rc;
+    if ((rc = bk.run(labels, st))) return rc;
+    std::vector<int64_t> hstart(k + 1), hseg(k + 1, 0);
+    SC_CUDA(cudaMemcpyAsync(hstart.data(), bk.start.p, sizeof(int64_t) * (k + 1), cudaMemcpyDeviceToHost, st));
+    SC_CUDA(cudaStreamSynchronize(st));
+    for (int64_t c = 0; c < k; ++c) hseg[c + 1] = hseg[c] + ceil_div(hstart[c + 1] - hstart[c], CM_SEG);
+    const int64_t nseg = hseg[k];
+    SC_CUDA(cudaMemcpyAsync(seg_off.p, hseg.data(), sizeof(int64_t) * (k + 1), cudaMemcpyHostToDevice, st));
+    const int64_t dchunks = ceil_div(d, 32);
+    if (nseg > 0)
+        centroid_segsum_kernel<<<(unsigned)ceil_div(nseg * dchunks * 32, 256), 256, 0, st>>>(
+            k, d, nseg, v, bk.start.p, bk.members.p, seg_off.p, segpart.p);
+    centroid_segtotal_kernel<<<(unsigned)ceil_div(k * d, 256), 256, 0, st>>>(k, d, bk.start.p, seg_off.p, segpart.p,
+                                                                            sums, counts);
+    SC_LAUNCHED(2);
+    SC_CUDA(cudaStreamSynchronize(st));
+    return SC_OK;
+}
+
+// cent = sums / counts (0 for empty clusters)
+int sc_centroid_divide(int64_t k, int64_t d, const double* sums, const int64_t* counts, double* cent,
+                       sc_stream_t stream) {
+    cudaStream_t st = as_stream(stream);
+    if (k * d <= 0) return SC_OK;
+    centroid_divide_kernel<<<(unsigned)ceil_div(k * d, 256), 256, 0, st>>>(k, d, sums, counts, cent);
+    SC_LAUNCHED(1);
+    return SC_OK;
+}
+
+// first e indices of the stable descending order of cost (kmeans.py:151)
+int sc_farthest(int64_t n, const double* cost, int64_t e, int64_t* idx_out, sc_stream_t stream) {
+    cudaStream_t st = as_stream(stream);
+    StreamScope stream_scope(st);
+    DevBuf<uint8_t> used;
+    DevBuf<double> pv;
+    DevBuf<int64_t> pi, pick;
+    int rc;
+    if ((rc = used.alloc(n)) || (rc = pv.alloc(256)) || (rc = pi.alloc(256)) || (rc = pick.alloc(e > 0 ? e : 1)))
+        return rc;
+    SC_CUDA(cudaMemsetAsync(used.p, 0, n, st));
+    for (int64_t s = 0; s < e && s < n; ++s) {
+        argmax_partial_kernel<<<256, 256, 0, st>>>(n, cost, used.p, pv.p, pi.p);
+        argmax_finish_kernel<<<1, 32, 0, st>>>(256, pv.p, pi.p, used.p, pick.p + s);
+        SC_LAUNCHED(2);
+    }
+    SC_CUDA(cudaMemcpyAsync(idx_out, pick.p, sizeof(int64_t) * e, cudaMemcpyDeviceToHost, st));
+    SC_CUDA(cudaStreamSynchronize(st));
+    return SC_OK;
+}
+
+// row-sharded ncut partials: rows row_offset.. of W, labels of ALL points;
+// per part boundary weight / volume of the local rows and member counts (dev)
+int sc_ncut_partials(int64_t n_local, int64_t row_offset, const int64_t* row_ptr, const int32_t* col,
+                     const double* vals, const int64_t* labels_global, int64_t k, double* bnd, double* vol,
+                     int64_t* counts, sc_stream_t stream) {
+    cudaStream_t st = as_stream(stream);
+    StreamScope stream_scope(st);
+    if (k < 1) return fail(SC_ERR_VALUE, "ncut needs k >= 1");
+    if (n_local <= 0) {
+        SC_CUDA(cudaMemsetAsync(bnd, 0, sizeof(double) * k, st));
+        SC_CUDA(cudaMemsetAsync(vol, 0, sizeof(double) * k, st));
+        SC_CUDA(cudaMemsetAsync(counts, 0, sizeof(int64_t) * k, st));
+        return SC_OK;
+    }
+    DevBuf<double> deg, cross;
+    Bucketer bk;
+    int rc;
+    if ((rc = deg.alloc(n_local)) || (rc = cross.alloc(n_local)) || (rc = bk.init(n_local, k))) return rc;
+    if ((rc = bk.run(labels_global + row_offset, st))) return rc;
+    ncut_rows_kernel<<<(unsigned)ceil_div(n_local, 8), 256, 0, st>>>(n_local, row_ptr, col, vals, labels_global,
+                                                                     deg.p, cross.p, row_offset);
+    ncut_parts_kernel<<<(unsigned)ceil_div(k, 64), 64, 0, st>>>(k, deg.p, cross.p, bk.start.p, bk.members.p, bnd, vol);
+    bucket_sizes_kernel<<<(unsigned)ceil_div(k, 256), 256, 0, st>>>(k, bk.start.p, counts);
+    SC_LAUNCHED(3);
+    return SC_OK;
 }
 
 int sc_ncut(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* vals,

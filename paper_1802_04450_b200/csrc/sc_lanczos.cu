@@ -35,6 +35,13 @@ __global__ void fill_normal_kernel(int64_t n, uint64_t seed, uint64_t stream_id,
     if (i < n) out[i] = philox_normal(seed, stream_id, (uint64_t)i);
 }
 
+// element i of a shard starting at global row `offset` (shard-independent draws)
+__global__ void fill_normal_offset_kernel(int64_t n, int64_t offset, uint64_t seed, uint64_t stream_id,
+                                          double* __restrict__ out) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = philox_normal(seed, stream_id, (uint64_t)(offset + i));
+}
+
 // part[b * ncols + c] = sum_{r in block b} B[c * ld + r] * w[r]
 __global__ void __launch_bounds__(256) gemv_t_partial_kernel(int64_t n, int64_t ld, int ncols,
                                                              const double* __restrict__ B,
@@ -144,6 +151,11 @@ __global__ void finish_norm_kernel(int64_t nb, const double* __restrict__ part, 
         __syncthreads();
     }
     if (threadIdx.x == 0) scal[out] = sqrt(red[0]);
+}
+
+__global__ void div_copy_kernel(int64_t n, const double* __restrict__ src, double div, double* __restrict__ dst) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = src[i] / div;
 }
 
 // dst = src / scal[idx]
@@ -775,6 +787,101 @@ int sc_symmetry_probe(int64_t n, const int64_t* row_ptr, const int32_t* col, con
     double vm;
     std::memcpy(&vm, &vb, sizeof(vm));
     *ratio_out = worst / std::max(1.0, vm);
+    return SC_OK;
+}
+
+// ---- per-shard building blocks of the row-sharded eigensolver -------------------
+int sc_gemv_t_f64(int64_t n, int64_t ld, int64_t ncols, const double* B, const double* w, double* h,
+                  sc_stream_t stream) {
+    cudaStream_t st = as_stream(stream);
+    StreamScope stream_scope(st);
+    if (ncols <= 0) return SC_OK;
+    if (n <= 0) {
+        SC_CUDA(cudaMemsetAsync(h, 0, sizeof(double) * ncols, st));
+        return SC_OK;
+    }
+    const int64_t nb = ceil_div(n, GT_ROWS);
+    DevBuf<double> part;
+    if (int rc = part.alloc((size_t)nb * ncols)) return rc;
+    gemv_t_partial_kernel<<<(unsigned)nb, 256, 0, st>>>(n, ld, (int)ncols, B, w, part.p);
+    reduce_cols_kernel<<<(unsigned)ceil_div(ncols * 32, 256), 256, 0, st>>>(nb, (int)ncols, part.p, h);
+    SC_LAUNCHED(2);
+    return SC_OK;
+}
+
+int sc_gemv_n_f64(int64_t n, int64_t ld, int64_t ncols, const double* B, const double* h, double* w, double* sq_out,
+                  sc_stream_t stream) {
+    cudaStream_t st = as_stream(stream);
+    StreamScope stream_scope(st);
+    if (n <= 0) {
+        if (sq_out) SC_CUDA(cudaMemsetAsync(sq_out, 0, sizeof(double), st));
+        return SC_OK;
+    }
+    const int64_t nb = ceil_div(n, GN_THREADS);
+    DevBuf<double> sq, scal;
+    if (sq_out) {
+        if (int rc = sq.alloc(nb)) return rc;
+    }
+    if (ncols > 0) {
+        gemv_n_update_kernel<<<(unsigned)nb, GN_THREADS, sizeof(double) * (size_t)ncols, st>>>(
+            n, ld, (int)ncols, B, h, w, sq_out ? sq.p : nullptr);
+        SC_LAUNCHED(1);
+    } else if (sq_out) {
+        sumsq_partial_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, w, sq.p, nullptr);
+        SC_LAUNCHED(1);
+    }
+    if (sq_out) {
+        const int64_t parts = ncols > 0 ? nb : ceil_div(n, 256);
+        finish_sum_kernel<<<1, 1024, 0, st>>>(parts, sq.p, sq_out, 0);
+        SC_LAUNCHED(1);
+    }
+    return SC_OK;
+}
+
+// dst = src / div (IEEE division, as `w / beta` in eigen.py:172)
+int sc_div_copy_f64(int64_t n, const double* src, double div, double* dst, sc_stream_t stream) {
+    cudaStream_t st = as_stream(stream);
+    if (n <= 0) return SC_OK;
+    div_copy_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, src, div, dst);
+    SC_LAUNCHED(1);
+    return SC_OK;
+}
+
+int sc_fill_normal(int64_t n, int64_t offset, uint64_t seed, uint64_t stream_id, double* out, sc_stream_t stream) {
+    cudaStream_t st = as_stream(stream);
+    if (n <= 0) return SC_OK;
+    fill_normal_offset_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, offset, seed, stream_id, out);
+    SC_LAUNCHED(1);
+    return SC_OK;
+}
+
+int sc_symeig_f64(int64_t m, int64_t kout, const double* T, double* theta, double* S, sc_stream_t stream) {
+    cudaStream_t st = as_stream(stream);
+    StreamScope stream_scope(st);
+    if (m < 1 || kout < 1 || kout > m) return fail(SC_ERR_VALUE, "symeig needs 1 <= kout <= m");
+    DevBuf<double> A, Z, wraw;
+    DevBuf<int> info;
+    int rc;
+    if ((rc = A.alloc((size_t)m * m)) || (rc = Z.alloc((size_t)m * m)) || (rc = wraw.alloc(m)) ||
+        (rc = info.alloc(1)))
+        return rc;
+    SC_CUDA(cudaMemcpyAsync(A.p, T, sizeof(double) * m * m, cudaMemcpyDeviceToDevice, st));
+    if ((rc = symeig_launch((int)m, (int)kout, A.p, Z.p, wraw.p, theta, S, info.p, st))) return rc;
+    int h = 0;
+    SC_CUDA(cudaMemcpyAsync(&h, info.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    SC_CUDA(cudaStreamSynchronize(st));
+    if (h) return fail(SC_ERR_INTERNAL, "projected eigenproblem: QL did not converge");
+    return SC_OK;
+}
+
+int sc_dgemm_tall(int64_t n, int64_t kk, int64_t kc, const double* A, int64_t lda, const double* S, int64_t lds,
+                  double* C, int64_t ldc, int rowmajor, sc_stream_t stream) {
+    cudaStream_t st = as_stream(stream);
+    if (n <= 0 || kc <= 0) return SC_OK;
+    dim3 grid((unsigned)ceil_div(n, GB_M), (unsigned)ceil_div(kc, GB_N));
+    ProfScope prof("ritz", st, 2.0 * (double)n * kk * kc);
+    dgemm_tall_kernel<<<grid, 256, 0, st>>>(n, (int)kk, (int)kc, A, lda, S, lds, C, ldc, rowmajor);
+    SC_LAUNCHED(1);
     return SC_OK;
 }
 

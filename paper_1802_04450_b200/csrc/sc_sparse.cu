@@ -102,12 +102,14 @@ int degrees_launch(int64_t n, const int64_t* row_ptr, const double* vals, double
 
 // a_ij = w_ij / sqrt(d_i * d_j)  (laplacian.py:89-91: one product, one sqrt,
 // one division, all IEEE round-to-nearest -> bit-identical to numpy).
+// (row_offset: the CSR holds rows row_offset .. row_offset+n-1 of the global
+// matrix; d is the global degree vector)
 __global__ void sym_scale_kernel(int64_t n, const int64_t* __restrict__ row_ptr,
                                  const int32_t* __restrict__ col, const double* __restrict__ vals,
-                                 const double* __restrict__ d, double* __restrict__ out) {
+                                 const double* __restrict__ d, double* __restrict__ out, int64_t row_offset = 0) {
     int64_t i = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     if (i >= n) return;
-    double di = d[i];
+    double di = d[row_offset + i];
     for (int64_t p = row_ptr[i] + (threadIdx.x & 31), e = row_ptr[i + 1]; p < e; p += 32) {
         double s = __dsqrt_rn(__dmul_rn(di, __ldg(d + col[p])));
         out[p] = __ddiv_rn(vals[p], s);
@@ -224,6 +226,16 @@ int sc_sym_scale_f64(int64_t n, const int64_t* row_ptr, const int32_t* col,
     cudaStream_t st = as_stream(stream);
     StreamScope stream_scope(st);
     sym_scale_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, st>>>(n, row_ptr, col, vals, d, out);
+    SC_LAUNCHED(1);
+    return SC_OK;
+}
+
+int sc_sym_scale_shard_f64(int64_t n_local, int64_t row_offset, const int64_t* row_ptr, const int32_t* col,
+                           const double* vals, const double* d_global, double* out, sc_stream_t stream) {
+    if (n_local <= 0) return SC_OK;
+    cudaStream_t st = as_stream(stream);
+    sym_scale_kernel<<<(unsigned)ceil_div(n_local, 8), 256, 0, st>>>(n_local, row_ptr, col, vals, d_global, out,
+                                                                     row_offset);
     SC_LAUNCHED(1);
     return SC_OK;
 }

@@ -1,0 +1,73 @@
+"""Worker bodies for the multi-process (gloo, CPU) tests of the sharded
+drivers; each returns a dict of numpy arrays saved by the test harness."""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+
+import paper_1802_04450_b200 as sc
+from oracle import speclust_oracle as orc
+from paper_1802_04450_b200.distributed import Comm, lanczos_sharded, row_bounds, run_sharded
+from tests.np_ops import HostCsr, NumpyOps
+
+
+def random_symmetric(n=240, density=0.04, seed=3):
+    rng = np.random.default_rng(seed)
+    a = np.zeros((n, n))
+    nz = int(density * n * n / 2)
+    a[rng.integers(0, n, nz), rng.integers(0, n, nz)] = rng.standard_normal(nz)
+    a = a + a.T
+    r, c = np.nonzero(a)
+    return a, sc.coo_to_csr(sc.coo_canonicalize(sc.CooMatrix(n, n, r, c, a[r, c])))
+
+
+def lanczos_worker(rank, world):
+    import torch
+
+    _, m = random_symmetric()
+    ops = NumpyOps()
+    comm = Comm("cpu")
+    n = m.n_rows
+    bounds = row_bounds(n, comm.world)
+    full = ops.from_host_csr(m)
+    loc = ops.slice_rows(full, bounds[comm.rank], bounds[comm.rank + 1])
+    vals, V, res, st = lanczos_sharded(ops, comm, loc, n, bounds, sc.LanczosConfig(k=6, seed=0))
+    Vf = comm.gather_rows(V, bounds)
+    return dict(values=vals, vectors=Vf.numpy(), residuals=res, restarts=st["restarts"], matvecs=st["matvecs"])
+
+
+def blobs_cfg():
+    x, truth = orc.blobs(360, 6, 4, 4.0, seed=11)
+    cfg = sc.PipelineConfig(
+        input=sc.PointsInput(measure=sc.SimilarityMeasure.exp_decay(float(np.sqrt(6.0))), pattern="knn", points=x,
+                             knn=8),
+        k_clusters=4, eigen=sc.LanczosConfig(k=4, seed=0), kmeans=sc.KmeansConfig(k=4, seed=0),
+        normalize_rows=True)
+    return x, truth, cfg
+
+
+def pipeline_worker(rank, world):
+    _, _, cfg = blobs_cfg()
+    rep = run_sharded(cfg, Comm("cpu"), NumpyOps())
+    return dict(labels=rep.labeling.labels, values=rep.eigenvalues, residuals=rep.eigen_residuals,
+                ncut=np.array(rep.ncut_value), sse=rep.labeling.sse_history, centroids=rep.labeling.centroids)
+
+
+WORKERS = {"lanczos": lanczos_worker, "pipeline": pipeline_worker}
+
+
+def spawn_entry(rank, world, port, name, out_dir):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    if world > 1:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        res = WORKERS[name](rank, world)
+        np.savez(os.path.join(out_dir, f"{name}_w{world}_r{rank}.npz"), **res)
+    finally:
+        if world > 1:
+            dist.destroy_process_group()

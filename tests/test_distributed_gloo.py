@@ -1,0 +1,76 @@
+"""Multi-process (gloo, CPU) coverage of the sharded drivers: row-sharded
+Lanczos and the sharded pipeline (row-sharded eigen + point-sharded
+k-means++/Lloyd + sharded ncut) at world sizes 1, 2 and 3 must agree with each
+other and with the CPU oracle.  Per-shard compute is the numpy ops of
+tests/np_ops.py; the collectives are the product code's (Comm)."""
+
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from oracle import speclust_oracle as orc
+from tests import dist_workers as dw
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def run_world(name, world, tmp_path):
+    if world == 1:
+        dw.spawn_entry(0, 1, 0, name, str(tmp_path))
+    else:
+        mp.spawn(dw.spawn_entry, args=(world, _port(), name, str(tmp_path)), nprocs=world, join=True)
+    out = []
+    for r in range(world):
+        with np.load(tmp_path / f"{name}_w{world}_r{r}.npz") as f:
+            out.append({k: f[k] for k in f.files})
+    return out
+
+
+def test_lanczos_sharded_matches_single_and_lapack(tmp_path):
+    a, _ = dw.random_symmetric()
+    want = np.sort(np.linalg.eigvalsh(a))[::-1][:6]
+    w1 = run_world("lanczos", 1, tmp_path)[0]
+    for world in (2, 3):
+        res = run_world("lanczos", world, tmp_path)
+        for r in res:  # every rank holds the same replicated result
+            assert np.array_equal(r["values"], res[0]["values"])
+        got = res[0]
+        assert np.max(np.abs(got["values"] - want)) <= 1e-8
+        assert np.max(np.abs(got["values"] - w1["values"])) <= 1e-10
+        assert int(got["restarts"]) == int(w1["restarts"])
+        assert np.all(got["residuals"] <= 1e-6)
+        v = got["vectors"]
+        assert np.abs(v.T @ v - np.eye(6)).max() <= 1e-8
+
+
+def test_pipeline_sharded_matches_oracle(tmp_path):
+    x, truth, _ = dw.blobs_cfg()
+    ref = orc.run_points(x, 8, float(np.sqrt(6.0)), 4)
+    w1 = run_world("pipeline", 1, tmp_path)[0]
+    w2 = run_world("pipeline", 2, tmp_path)
+    for r in w2:
+        assert np.array_equal(r["labels"], w2[0]["labels"])
+    got = w2[0]
+    assert np.max(np.abs(got["values"] - ref["values"]) / np.abs(ref["values"])) <= 1e-8
+    assert orc.ari(got["labels"], ref["labels"]) >= 0.999
+    assert orc.ari(got["labels"], w1["labels"]) == 1.0
+    assert abs(float(got["ncut"]) - ref["ncut"]) <= 1e-10 * max(1.0, ref["ncut"])
+    assert orc.ari(got["labels"], truth) >= 0.99
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_row_bounds_partition(world):
+    from paper_1802_04450_b200.distributed import row_bounds
+
+    b = row_bounds(10, world)
+    assert b[0] == 0 and b[-1] == 10 and all(b[i] <= b[i + 1] for i in range(world))
+    sizes = np.diff(b)
+    assert sizes.max() - sizes.min() <= 1
