@@ -108,6 +108,23 @@ int sc_csr_is_symmetric(int64_t n, int64_t nnz, const int64_t* row_ptr, const in
 int sc_knn_graph_f64(int64_t n, int64_t d, const double* x, int64_t knn, double two_sigma_sq,
                      int64_t* row_ptr, int32_t* col, double* vals, int64_t* nnz_out,
                      int64_t* stats_out, sc_stream_t stream);
+/* The same graph in two stages, for a build sharded over query rows
+ * (SURVEY.md §8(e)); sc_knn_graph_f64 == select(0, n) + union(0, n).
+ * select: the top-knn of the points at scan positions [p0, p1) (p0 a multiple
+ *   of 128) into sel ((p1-p0) x knn int32, each row ascending) and the scan
+ *   order perm (n int32: position -> point; identical for the same x on
+ *   every caller).  Concatenating every shard's sel gives the n x knn
+ *   selection in scan order.
+ * union: CSR rows [r0, r1) (row_ptr local, r1-r0+1 entries; global columns)
+ *   from the full selection; SC_ERR_VALUE with *nnz_out = the required size
+ *   when it exceeds cap. */
+int sc_knn_select_f64(int64_t n, int64_t d, const double* x, int64_t knn, double two_sigma_sq,
+                      int64_t p0, int64_t p1, int32_t* sel, int32_t* perm, int64_t* stats_out,
+                      sc_stream_t stream);
+int sc_knn_union_f64(int64_t n, int64_t d, const double* x, int64_t knn, double two_sigma_sq,
+                     const int32_t* sel, const int32_t* perm, int64_t r0, int64_t r1,
+                     int64_t* row_ptr, int32_t* col, double* vals, int64_t cap, int64_t* nnz_out,
+                     sc_stream_t stream);
 /* out[p] = exp(-|x_a - x_b|^2 / two_sigma_sq) for pairs (a, b) = pairs[2p..2p+1]
  * (graph.py:136-141, used by build_similarity on a given edge list). */
 int sc_pair_weights(int64_t n, int64_t d, const double* x, int64_t m, const int64_t* pairs,

@@ -145,4 +145,55 @@ __device__ __forceinline__ double philox_normal(uint64_t seed, uint64_t stream_i
     return sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
 }
 
+// ---------------------------------------------------------------------------
+// numpy's float64 sum-of-products order.  The reference computes squared
+// norms, distances and k-means cross terms with np.einsum over contiguous
+// rows (graph.py:92, kmeans.py:92-104), whose inner loop (this image's x86
+// numpy build) runs on two-lane vectors: each block of 8 elements is folded
+// last vector first (acc = p0 + (p1 + (p2 + (p3 + acc)))), the tail goes two
+// lanes at a time with zero fill, the result is lane0 + lane1, and nothing is
+// fused.  Reproducing it makes those values bit-identical to the reference
+// (identified against numpy for d = 1..129; checked by the golden tests).
+struct NpDot {
+    double a0 = 0.0, a1 = 0.0;
+    // products of elements c..c+7 of a full block (c % 8 == 0)
+    __device__ __forceinline__ void block(double p0, double p1, double p2, double p3, double p4, double p5, double p6,
+                                          double p7) {
+        a0 = __dadd_rn(p0, __dadd_rn(p2, __dadd_rn(p4, __dadd_rn(p6, a0))));
+        a1 = __dadd_rn(p1, __dadd_rn(p3, __dadd_rn(p5, __dadd_rn(p7, a1))));
+    }
+    __device__ __forceinline__ void pair(double pe, double po) {
+        a0 = __dadd_rn(pe, a0);
+        a1 = __dadd_rn(po, a1);
+    }
+    __device__ __forceinline__ void single(double pe) { a0 = __dadd_rn(pe, a0); }
+    __device__ __forceinline__ double result() const { return __dadd_rn(a0, a1); }
+};
+
+// sum over l of f(l) (a product, computed unfused) for l in [c, end), in the
+// order above; c % 8 == 0 and the span is either whole blocks or reaches d
+template <class F>
+__device__ __forceinline__ void np_dot_span(NpDot& s, int64_t c, int64_t end, F f) {
+    for (; c + 8 <= end; c += 8) s.block(f(c), f(c + 1), f(c + 2), f(c + 3), f(c + 4), f(c + 5), f(c + 6), f(c + 7));
+    for (; c + 2 <= end; c += 2) s.pair(f(c), f(c + 1));
+    if (c < end) s.single(f(c));
+}
+
+// |a - b|^2 (np.einsum("ij,ij->i", diff, diff) with diff = a - b)
+__device__ __forceinline__ double np_sqdist(const double* __restrict__ a, const double* __restrict__ b, int64_t d) {
+    NpDot s;
+    np_dot_span(s, 0, d, [&](int64_t l) {
+        const double t = __dsub_rn(a[l], b[l]);
+        return __dmul_rn(t, t);
+    });
+    return s.result();
+}
+
+// |a|^2 (np.einsum("ij,ij->i", v, v))
+__device__ __forceinline__ double np_sqnorm(const double* __restrict__ a, int64_t d) {
+    NpDot s;
+    np_dot_span(s, 0, d, [&](int64_t l) { return __dmul_rn(a[l], a[l]); });
+    return s.result();
+}
+
 }  // namespace sc

@@ -18,17 +18,14 @@ namespace sc {
 __device__ __forceinline__ int64_t ceil_div_dev(int64_t d) { return (d + 31) / 32; }
 
 // ---------------------------------------------------------------------------
-// row squared norms as a sequential fma chain over the feature index: the
-// same chain the distance tile uses for v.c, so identical rows give an exact
-// zero distance (kmeans.py:92-97; test_kmeans.py:23-27).
+// row squared norms in numpy's einsum order (kmeans.py:92-97): the same
+// order the distance tile uses for v.c, so the expansion is bit-identical to
+// the reference and identical rows give an exact zero (test_kmeans.py:23-27)
 __global__ void rownorm_kernel(int64_t n, int64_t d, const double* __restrict__ v,
                                double* __restrict__ out) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const double* r = v + i * d;
-    double acc = 0.0;
-    for (int64_t l = 0; l < d; ++l) acc = fma(r[l], r[l], acc);
-    out[i] = acc;
+    out[i] = np_sqnorm(v + i * d, d);
 }
 
 constexpr int TP = 64, TQ = 64, KC = 16;
@@ -59,11 +56,12 @@ __global__ void __launch_bounds__(256) dist_tile_kernel(
     }
 
     for (int64_t q0 = 0; q0 < k; q0 += TQ) {
-        double acc[4][4];
+        // v.c in numpy's einsum order (NpDot): even / odd lane accumulators
+        double acc[4][4], acc1[4][4];
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+            for (int j = 0; j < 4; ++j) acc[i][j] = acc1[i][j] = 0.0;
         for (int64_t l0 = 0; l0 < d; l0 += KC) {
             __syncthreads();
 #pragma unroll
@@ -77,7 +75,8 @@ __global__ void __launch_bounds__(256) dist_tile_kernel(
             }
             __syncthreads();
             const int lmax = (int)imin64(KC, d - l0);
-            for (int l = 0; l < lmax; ++l) {
+            // acc += p_l for element l (unfused), into the even or odd lane
+            auto step = [&](int l, bool odd) {
                 double a[4], b[4];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) a[i] = Vs[l][ty + 16 * i];
@@ -86,9 +85,29 @@ __global__ void __launch_bounds__(256) dist_tile_kernel(
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+                    for (int j = 0; j < 4; ++j) {
+                        double& r = odd ? acc1[i][j] : acc[i][j];
+                        r = __dadd_rn(__dmul_rn(a[i], b[j]), r);
+                    }
+            };
+            int l = 0;
+            for (; l + 8 <= lmax; l += 8) {  // whole block: p0 + (p2 + (p4 + (p6 + acc)))
+#pragma unroll
+                for (int t = 6; t >= 0; t -= 2) {
+                    step(l + t, false);
+                    step(l + t + 1, true);
+                }
             }
+            for (; l + 2 <= lmax; l += 2) {
+                step(l, false);
+                step(l + 1, true);
+            }
+            if (l < lmax) step(l, false);
         }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = __dadd_rn(acc[i][j], acc1[i][j]);
         // epilogue for this centroid tile
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -435,42 +454,67 @@ __global__ void reseed_finish_kernel(int nb, const double* __restrict__ pv, cons
 // candidate partials (count, weight sum) over untaken rows with d2 > 0.
 // `prow` = coordinates of the drawn row; `pick` = its local index (or -1 when
 // the row lives on another shard)
-__global__ void kpp_update_kernel(int64_t n, int64_t d, const double* __restrict__ v, const double* __restrict__ prow,
+constexpr int KPP_UPD_ROWS = 128, KPP_UPD_COLS = 32;
+
+__global__ void __launch_bounds__(KPP_UPD_ROWS) kpp_update_kernel(int64_t n, int64_t d, const double* __restrict__ v, const double* __restrict__ prow,
                                   int64_t pick, int first, double* __restrict__ d2, uint8_t* __restrict__ taken,
                                   double* __restrict__ pw, int64_t* __restrict__ pc) {
-    __shared__ double sw[8];
-    __shared__ int64_t scn[8];
-    int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    int64_t i = (int64_t)blockIdx.x * 8 + warp;  // one warp per row
+    // one thread per row; the block's KPP_UPD_ROWS rows are staged through
+    // shared memory in 32-column chunks (coalesced loads), and each thread
+    // folds its row in numpy's einsum order (_dist_to_one, kmeans.py:101-104)
+    __shared__ double tile[KPP_UPD_ROWS][KPP_UPD_COLS + 1];
+    __shared__ double sp[KPP_UPD_COLS];
+    __shared__ double sw[KPP_UPD_ROWS / 32];
+    __shared__ int64_t scn[KPP_UPD_ROWS / 32];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t r0 = (int64_t)blockIdx.x * KPP_UPD_ROWS;
+    const int64_t i = r0 + tid;
+    const int nrows = (int)imin64(KPP_UPD_ROWS, n - r0);
+    NpDot acc;
+    for (int64_t c0 = 0; c0 < d; c0 += KPP_UPD_COLS) {
+        const int nc = (int)imin64(KPP_UPD_COLS, d - c0);
+        __syncthreads();
+        for (int e = tid; e < nrows * KPP_UPD_COLS; e += KPP_UPD_ROWS) {
+            const int rr = e / KPP_UPD_COLS, cc = e % KPP_UPD_COLS;
+            if (cc < nc) tile[rr][cc] = v[(r0 + rr) * d + c0 + cc];
+        }
+        if (tid < nc) sp[tid] = prow[c0 + tid];
+        __syncthreads();
+        if (tid < nrows) {
+            const double* row = tile[tid];
+            np_dot_span(acc, 0, nc, [&](int64_t l) {
+                const double t = __dsub_rn(row[l], sp[l]);
+                return __dmul_rn(t, t);
+            });
+        }
+    }
     double w = 0.0;
     int64_t cnt = 0;
     if (i < n) {
-        const double* r = v + i * d;
-        const double* p = prow;
-        double acc = 0.0;
-        for (int64_t l = lane; l < d; l += 32) {
-            double t = r[l] - p[l];
-            acc = fma(t, t, acc);
-        }
-        acc = warp_sum(acc);
-        double nv = first ? acc : fmin(d2[i], acc);
+        const double dist = acc.result();
+        const double nv = first ? dist : fmin(d2[i], dist);
         if (i == pick) taken[i] = 1;
-        bool tk = (i == pick) || taken[i];
-        if (lane == 0) d2[i] = nv;
+        const bool tk = (i == pick) || taken[i];
+        d2[i] = nv;
         if (!tk && nv > 0.0) {
             w = nv;
             cnt = 1;
         }
+    }
+    // fixed-order block partials (deterministic)
+    for (int o = 16; o > 0; o >>= 1) {
+        w += __shfl_down_sync(0xffffffffu, w, o);
+        cnt += __shfl_down_sync(0xffffffffu, cnt, o);
     }
     if (lane == 0) {
         sw[warp] = w;
         scn[warp] = cnt;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (tid == 0) {
         double a = 0.0;
         int64_t c = 0;
-        for (int q = 0; q < 8; ++q) {
+        for (int q = 0; q < KPP_UPD_ROWS / 32; ++q) {
             a += sw[q];
             c += scn[q];
         }
@@ -857,7 +901,7 @@ int sc_kmeanspp_create(int64_t n, int64_t d, const double* v, sc_stream_t stream
     s->d = d;
     s->v = v;
     s->st = as_stream(stream);
-    s->nb_upd = ceil_div(n, 8);
+    s->nb_upd = ceil_div(n, KPP_UPD_ROWS);
     s->nb_p = ceil_div(n, KPP_BLK);
     int rc;
     if ((rc = s->d2.alloc(n)) || (rc = s->taken.alloc(n)) || (rc = s->pw.alloc(s->nb_upd)) ||
@@ -877,7 +921,7 @@ int sc_kmeanspp_take(sc_kmeanspp_t* s, int64_t index) {
     if (index < 0 || index >= s->n) return fail(SC_ERR_VALUE, "k-means++ index out of range");
     {
         ProfScope prof("kmeanspp", s->st, (double)s->n * s->d * 8.0);
-        kpp_update_kernel<<<(unsigned)s->nb_upd, 256, 0, s->st>>>(s->n, s->d, s->v, s->v + index * s->d, index,
+        kpp_update_kernel<<<(unsigned)s->nb_upd, KPP_UPD_ROWS, 0, s->st>>>(s->n, s->d, s->v, s->v + index * s->d, index,
                                                                   s->first ? 1 : 0, s->d2.p, s->taken.p, s->pw.p,
                                                                   s->pc.p);
     }
@@ -917,7 +961,7 @@ int sc_kmeanspp_pick(sc_kmeanspp_t* s, int mode, double u, int64_t r, int64_t* i
 int sc_kmeanspp_take_row(sc_kmeanspp_t* s, const double* row, int64_t local_index) {
     {
         ProfScope prof("kmeanspp", s->st, (double)s->n * s->d * 8.0);
-        kpp_update_kernel<<<(unsigned)s->nb_upd, 256, 0, s->st>>>(s->n, s->d, s->v, row, local_index,
+        kpp_update_kernel<<<(unsigned)s->nb_upd, KPP_UPD_ROWS, 0, s->st>>>(s->n, s->d, s->v, row, local_index,
                                                                   s->first ? 1 : 0, s->d2.p, s->taken.p, s->pw.p,
                                                                   s->pc.p);
     }

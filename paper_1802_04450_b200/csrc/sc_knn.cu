@@ -97,7 +97,8 @@ __global__ void knn_prep_kernel(int64_t n, int64_t d, int64_t dp, const double* 
 // the tcgen05 path; selected with SPECLUST_KNN_KERNEL=simt) (128 query rows x 128 columns)
 constexpr int KM = 128, KN = 128, KK = 16;
 
-__global__ void __launch_bounds__(256) knn_cand_simt_kernel(int64_t n, int dp, const float* __restrict__ xf,
+__global__ void __launch_bounds__(256) knn_cand_simt_kernel(int64_t n, int64_t qtile0, int dp,
+                                                            const float* __restrict__ xf,
                                                             const float* __restrict__ cnf, int cap, int R,
                                                             float2* __restrict__ lists, int* __restrict__ counts,
                                                             float* __restrict__ taus) {
@@ -107,12 +108,13 @@ __global__ void __launch_bounds__(256) knn_cand_simt_kernel(int64_t n, int dp, c
     float* Ks = Bs + KK * KN;            // KM x (KN + 1)
     float* cns = Ks + KM * (KN + 1);     // KN
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-    const int64_t r0 = (int64_t)blockIdx.x * KM;
+    const int64_t r0 = (qtile0 + blockIdx.x) * KM;
     const int64_t myrow = r0 + tid;
+    const int64_t lrow = (int64_t)blockIdx.x * KM + tid;  // list slot
     const bool selector = tid < KM && myrow < n;
     int cnt = 0;
     float tau = INFINITY;
-    float2* L = lists + (selector ? myrow : 0) * (int64_t)cap;
+    float2* L = lists + (selector ? lrow : 0) * (int64_t)cap;
 
     for (int64_t c0 = 0; c0 < n; c0 += KN) {
         float acc[8][8];
@@ -185,20 +187,18 @@ __global__ void __launch_bounds__(256) knn_cand_simt_kernel(int64_t n, int dp, c
         }
     }
     if (selector) {
-        counts[myrow] = cnt;
-        taus[myrow] = tau;
+        counts[lrow] = cnt;
+        taus[lrow] = tau;
     }
 }
 
 // ---------------------------------------------------------------------------
 // exact recheck: warp per row
+// |x_j - x_i|^2 in the summation order of the reference's
+// np.einsum("ij,ij->i", diff, diff) (graph.py:92, 156; 136-141), so ranking
+// keys and edge values are bit-identical (NpDot, sc_common.cuh)
 __device__ __forceinline__ double exact_d2(const double* __restrict__ xi, const double* __restrict__ xj, int64_t d) {
-    double acc = 0.0;
-    for (int64_t l = 0; l < d; ++l) {
-        double t = __dsub_rn(xj[l], xi[l]);
-        acc = __dadd_rn(acc, __dmul_rn(t, t));
-    }
-    return acc;
+    return np_sqdist(xj, xi, d);
 }
 
 // (s desc, j asc) ordering: a precedes b
@@ -206,7 +206,8 @@ __device__ __forceinline__ bool precedes(double sa, int ja, double sb, int jb) {
     return sa > sb || (sa == sb && ja < jb);
 }
 
-__global__ void __launch_bounds__(256) knn_recheck_kernel(int64_t n, int64_t d, const double* __restrict__ x,
+__global__ void __launch_bounds__(256) knn_recheck_kernel(int64_t n, int64_t p0, int64_t p1, int64_t d,
+                                                          const double* __restrict__ x,
                                                           int64_t knn, double inv, int cap,
                                                           const float2* __restrict__ lists,
                                                           const int* __restrict__ counts,
@@ -217,17 +218,19 @@ __global__ void __launch_bounds__(256) knn_recheck_kernel(int64_t n, int64_t d, 
                                                           int32_t* __restrict__ sel,
                                                           int32_t* __restrict__ flagged,
                                                           unsigned long long* __restrict__ nflag) {
-    // lists/counts/taus are in scan order (position ip holds point perm[ip]);
-    // everything else, including the (-s, j) tie-break, uses original indices
+    // lists/counts/taus/sel are in scan order relative to p0 (position ip
+    // holds point perm[ip]); distances, norms and the (-s, j) tie-break use
+    // original indices; flagged rows are recorded by scan position
     extern __shared__ unsigned char rsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double* S = reinterpret_cast<double*>(rsm) + (size_t)warp * cap;
     int* J = reinterpret_cast<int*>(reinterpret_cast<double*>(rsm) + (size_t)8 * cap) + (size_t)warp * cap;
-    const int64_t ip = (int64_t)blockIdx.x * 8 + warp;
-    if (ip >= n) return;
+    const int64_t lp = (int64_t)blockIdx.x * 8 + warp;
+    const int64_t ip = p0 + lp;
+    if (ip >= p1) return;
     const int64_t i = perm ? (int64_t)perm[ip] : ip;
-    const int cnt = counts[ip];
-    const float2* L = lists + ip * (int64_t)cap;
+    const int cnt = counts[lp];
+    const float2* L = lists + lp * (int64_t)cap;
     const double* xi = x + i * d;
     for (int t = lane; t < cnt; t += 32) {
         int j = __float_as_int(L[t].y);
@@ -244,13 +247,13 @@ __global__ void __launch_bounds__(256) knn_recheck_kernel(int64_t n, int64_t d, 
         int jt = J[t];
         int r = 0;
         for (int u = 0; u < cnt; ++u) r += precedes(S[u], J[u], st, jt);
-        if (r < knn) sel[i * knn + r] = jt;
+        if (r < knn) sel[lp * knn + r] = jt;
         if (r == knn - 1) s_k = st;
     }
     // broadcast s_k (held by exactly one lane)
     for (int o = 16; o > 0; o >>= 1) s_k = fmin(s_k, __shfl_xor_sync(0xffffffffu, s_k, o));
     if (lane != 0) return;
-    float tau = taus[ip];
+    float tau = taus[lp];
     bool ok;
     if (cnt < knn) {
         ok = false;
@@ -266,14 +269,15 @@ __global__ void __launch_bounds__(256) knn_recheck_kernel(int64_t n, int64_t d, 
     }
     if (!ok) {
         unsigned long long slot = atomicAdd(nflag, 1ull);
-        flagged[slot] = (int32_t)i;
+        flagged[slot] = (int32_t)ip;
     }
 }
 
 // ---------------------------------------------------------------------------
 // exact fallback: block per flagged row, radix select on the (s, -j) order
-__global__ void __launch_bounds__(512) knn_fallback_kernel(int64_t n, int64_t d, const double* __restrict__ x,
-                                                           int64_t knn, double inv,
+__global__ void __launch_bounds__(512) knn_fallback_kernel(int64_t n, int64_t p0, int64_t d,
+                                                           const double* __restrict__ x, int64_t knn, double inv,
+                                                           const int32_t* __restrict__ perm,
                                                            const int32_t* __restrict__ flagged, int64_t nflag,
                                                            unsigned long long* __restrict__ scratch,
                                                            int32_t* __restrict__ sel) {
@@ -285,7 +289,9 @@ __global__ void __launch_bounds__(512) knn_fallback_kernel(int64_t n, int64_t d,
     __shared__ long long s_base;
     unsigned long long* key = scratch + (size_t)blockIdx.x * n;
     for (int64_t f = blockIdx.x; f < nflag; f += gridDim.x) {
-        const int64_t i = flagged[f];
+        const int64_t ip = flagged[f];
+        const int64_t i = perm ? (int64_t)perm[ip] : ip;
+        int32_t* srow = sel + (ip - p0) * knn;
         const double* xi = x + i * d;
         for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
             if (j == i) {
@@ -335,7 +341,7 @@ __global__ void __launch_bounds__(512) knn_fallback_kernel(int64_t n, int64_t d,
         for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
             if (key[j] > T) {
                 int slot = atomicAdd(&s_out, 1);
-                sel[i * knn + slot] = (int32_t)j;
+                srow[slot] = (int32_t)j;
             }
         }
         __syncthreads();
@@ -350,7 +356,7 @@ __global__ void __launch_bounds__(512) knn_fallback_kernel(int64_t n, int64_t d,
             long long before = s_base;
             for (int q = 0; q < w; ++q) before += wcount[q];
             long long r = before + __popc(bal & ((1u << l) - 1u));
-            if (hit && r < take_eq) sel[i * knn + above_cnt + r] = (int32_t)j;
+            if (hit && r < take_eq) srow[above_cnt + r] = (int32_t)j;
             __syncthreads();
             if (threadIdx.x == 0) {
                 long long tot = 0;
@@ -381,19 +387,32 @@ __global__ void sort_rows_kernel(int64_t n, int64_t knn, int32_t* __restrict__ s
     }
 }
 
-__global__ void rev_count_kernel(int64_t total, const int32_t* __restrict__ sel, int64_t* __restrict__ rc) {
-    int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p < total) atomicAdd(reinterpret_cast<unsigned long long*>(rc + sel[p]), 1ull);
+// The union works on the selections of ALL points (sel: n x knn in scan
+// order, row q = point perm[q]) and emits the CSR rows [r0, r1) only, so
+// each shard of a multi-GPU build produces its own row block.
+__global__ void pos_of_kernel(int64_t n, const int32_t* __restrict__ perm, int32_t* __restrict__ pos) {
+    int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q < n) pos[perm ? perm[q] : q] = (int32_t)q;
 }
 
-__global__ void rev_fill_kernel(int64_t n, int64_t knn, const int32_t* __restrict__ sel,
-                                const int64_t* __restrict__ rev_ptr, unsigned int* __restrict__ fill,
-                                int32_t* __restrict__ rev) {
+__global__ void rev_count_kernel(int64_t total, int64_t r0, int64_t r1, const int32_t* __restrict__ sel,
+                                 int64_t* __restrict__ rc) {
+    int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= total) return;
+    const int64_t j = sel[p];
+    if (j >= r0 && j < r1) atomicAdd(reinterpret_cast<unsigned long long*>(rc + (j - r0)), 1ull);
+}
+
+__global__ void rev_fill_kernel(int64_t n, int64_t knn, int64_t r0, int64_t r1, const int32_t* __restrict__ sel,
+                                const int32_t* __restrict__ perm, const int64_t* __restrict__ rev_ptr,
+                                unsigned int* __restrict__ fill, int32_t* __restrict__ rev) {
     int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n * knn) return;
-    int32_t j = sel[p];
-    unsigned int pos = atomicAdd(fill + j, 1u);
-    rev[rev_ptr[j] + pos] = (int32_t)(p / knn);
+    const int64_t j = sel[p];
+    if (j < r0 || j >= r1) return;
+    unsigned int slot = atomicAdd(fill + (j - r0), 1u);
+    const int64_t q = p / knn;
+    rev[rev_ptr[j - r0] + slot] = perm ? perm[q] : (int32_t)q;
 }
 
 __device__ __forceinline__ bool in_sorted(const int32_t* __restrict__ a, int64_t len, int32_t v) {
@@ -406,13 +425,14 @@ __device__ __forceinline__ bool in_sorted(const int32_t* __restrict__ a, int64_t
 }
 
 // len_i = knn + #(reverse entries not already selected); marks duplicates
-__global__ void row_count_kernel(int64_t n, int64_t knn, const int32_t* __restrict__ sel,
-                                 const int64_t* __restrict__ rev_ptr, const int32_t* __restrict__ rev,
-                                 uint8_t* __restrict__ dup, int64_t* __restrict__ len) {
-    int64_t i = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+__global__ void row_count_kernel(int64_t nl, int64_t r0, int64_t knn, const int32_t* __restrict__ sel,
+                                 const int32_t* __restrict__ pos, const int64_t* __restrict__ rev_ptr,
+                                 const int32_t* __restrict__ rev, uint8_t* __restrict__ dup,
+                                 int64_t* __restrict__ len) {
+    int64_t i = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;  // local row
     int lane = threadIdx.x & 31;
-    if (i >= n) return;
-    const int32_t* s = sel + i * knn;
+    if (i >= nl) return;
+    const int32_t* s = sel + (int64_t)pos[r0 + i] * knn;
     int64_t c = 0;
     for (int64_t p = rev_ptr[i] + lane; p < rev_ptr[i + 1]; p += 32) {
         bool dp = in_sorted(s, knn, rev[p]);
@@ -423,18 +443,18 @@ __global__ void row_count_kernel(int64_t n, int64_t knn, const int32_t* __restri
     if (lane == 0) len[i] = knn + c;
 }
 
-__global__ void row_fill_kernel(int64_t n, int64_t d, int64_t knn, const double* __restrict__ x, double den,
-                                const int32_t* __restrict__ sel, const int64_t* __restrict__ rev_ptr,
-                                const int32_t* __restrict__ rev, const uint8_t* __restrict__ dup,
-                                const int64_t* __restrict__ row_ptr, int32_t* __restrict__ col,
-                                double* __restrict__ vals) {
-    int64_t i = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+__global__ void row_fill_kernel(int64_t nl, int64_t r0, int64_t d, int64_t knn, const double* __restrict__ x,
+                                double den, const int32_t* __restrict__ sel, const int32_t* __restrict__ pos,
+                                const int64_t* __restrict__ rev_ptr, const int32_t* __restrict__ rev,
+                                const uint8_t* __restrict__ dup, const int64_t* __restrict__ row_ptr,
+                                int32_t* __restrict__ col, double* __restrict__ vals) {
+    int64_t i = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;  // local row
     int lane = threadIdx.x & 31;
-    if (i >= n) return;
-    const int32_t* s = sel + i * knn;
+    if (i >= nl) return;
+    const int32_t* s = sel + (int64_t)pos[r0 + i] * knn;
     const int64_t rb = rev_ptr[i], re = rev_ptr[i + 1];
     const int64_t out0 = row_ptr[i];
-    const double* xi = x + i * d;
+    const double* xi = x + (r0 + i) * d;
     // selected entries
     for (int64_t t = lane; t < knn; t += 32) {
         int32_t e = s[t];
@@ -478,41 +498,43 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 }
 
 template <int NKB, int STAGES, bool LSMEM>
-static int launch_tc(const CUtensorMap& map, int64_t n, int64_t ntiles, const float* cnk, float key_scale, int cap,
-                     int R, float2* lists, int* counts, float* taus, cudaStream_t st) {
+static int launch_tc(const CUtensorMap& map, int64_t n, int64_t ntiles, int64_t qtile0, int64_t nq, const float* cnk,
+                     float key_scale, int cap, int R, float2* lists, int* counts, float* taus, cudaStream_t st) {
     const uint32_t smem = TcLayout<NKB, STAGES, LSMEM>::total;
     SC_CUDA(cudaFuncSetAttribute(knn_cand_tc_kernel<NKB, STAGES, LSMEM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
     DevBuf<long long> dbg;
     const bool want_dbg = std::getenv("SPECLUST_KNN_DEBUG") != nullptr;
     if (want_dbg) {
-        if (int rc = dbg.alloc((size_t)ntiles * 16)) return rc;
-        SC_CUDA(cudaMemsetAsync(dbg.p, 0, sizeof(long long) * ntiles * 16, st));
+        if (int rc = dbg.alloc((size_t)nq * 16)) return rc;
+        SC_CUDA(cudaMemsetAsync(dbg.p, 0, sizeof(long long) * nq * 16, st));
     }
-    knn_cand_tc_kernel<NKB, STAGES, LSMEM><<<(unsigned)ntiles, TC_THREADS, smem, st>>>(map, n, ntiles, cnk, key_scale,
-                                                                                       cap, R, lists, counts, taus,
-                                                                                       dbg.p);
+    knn_cand_tc_kernel<NKB, STAGES, LSMEM><<<(unsigned)nq, TC_THREADS, smem, st>>>(map, n, ntiles, qtile0, cnk,
+                                                                                   key_scale, cap, R, lists, counts,
+                                                                                   taus, dbg.p);
     SC_LAUNCHED(1);
     if (want_dbg) {
-        std::vector<long long> h((size_t)ntiles * 16);
+        std::vector<long long> h((size_t)nq * 16);
         SC_CUDA(cudaMemcpyAsync(h.data(), dbg.p, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, st));
         SC_CUDA(cudaStreamSynchronize(st));
         double acc[12] = {0};
-        for (int64_t b = 0; b < ntiles; ++b)
+        for (int64_t b = 0; b < nq; ++b)
             for (int q = 0; q < 12; ++q) acc[q] += (double)h[b * 16 + q];
         const char* names[12] = {"tma.wait_empty", "-", "-", "tma.total", "mma.wait_tempty", "mma.wait_full",
                                  "mma.latency64", "mma.total", "epi.wait_tfull", "epi.ldtm", "epi.work", "epi.fast"};
         for (int q = 0; q < 12; ++q)
             if (names[q][0] != '-')
                 fprintf(stderr, "[knn_tc dbg] %-16s %.1f cycles/tile\n", names[q],
-                        q == 6 ? acc[q] / ntiles / 64 : acc[q] / ntiles / ntiles);
+                        q == 6 ? acc[q] / nq / 64 : acc[q] / nq / ntiles);
     }
     return SC_OK;
 }
 
-// tensor-core candidate lists: every query tile against every candidate tile
+// tensor-core candidate lists: query tiles [qtile0, qtile0 + nq) against every
+// candidate tile
 int knn_candidates_tc(int64_t n, int64_t n_pad, int64_t dp64, const __half* xh, const float* cnk, float key_scale,
-                      int cap, int R, float2* lists, int* counts, float* taus, cudaStream_t st) {
+                      int64_t qtile0, int64_t nq, int cap, int R, float2* lists, int* counts, float* taus,
+                      cudaStream_t st) {
     auto encode = tensor_map_encoder();
     if (!encode) return fail(SC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     CUtensorMap map;
@@ -525,17 +547,25 @@ int knn_candidates_tc(int64_t n, int64_t n_pad, int64_t dp64, const __half* xh, 
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (cr != CUDA_SUCCESS) return fail(SC_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
     const int64_t ntiles = n_pad / 128;
-    ProfScope prof("knn_tile", st, 2.0 * (double)n * (double)n * (double)dp64);
+    ProfScope prof("knn_tile", st, 2.0 * (double)imin64(n, nq * 128) * (double)n * (double)dp64);
     switch (dp64 / 64) {
-        case 1: return launch_tc<1, 4, false>(map, n, ntiles, cnk, key_scale, cap, R, lists, counts, taus, st);
-        case 2: return launch_tc<2, 3, false>(map, n, ntiles, cnk, key_scale, cap, R, lists, counts, taus, st);
-        case 3: return launch_tc<3, 2, false>(map, n, ntiles, cnk, key_scale, cap, R, lists, counts, taus, st);
-        default: return launch_tc<4, 2, false>(map, n, ntiles, cnk, key_scale, cap, R, lists, counts, taus, st);
+        case 1: return launch_tc<1, 4, false>(map, n, ntiles, qtile0, nq, cnk, key_scale, cap, R, lists, counts, taus, st);
+        case 2: return launch_tc<2, 3, false>(map, n, ntiles, qtile0, nq, cnk, key_scale, cap, R, lists, counts, taus, st);
+        case 3: return launch_tc<3, 2, false>(map, n, ntiles, qtile0, nq, cnk, key_scale, cap, R, lists, counts, taus, st);
+        default: return launch_tc<4, 2, false>(map, n, ntiles, qtile0, nq, cnk, key_scale, cap, R, lists, counts, taus, st);
     }
 }
 
-int knn_graph_build(int64_t n, int64_t d, const double* x, int64_t knn, double two_sigma_sq, int64_t* row_ptr,
-                    int32_t* col, double* vals, int64_t* nnz_out, int64_t* stats, cudaStream_t st) {
+__global__ void iota_kernel(int64_t n, int32_t* __restrict__ out) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = (int32_t)i;
+}
+
+// Selection stage: the top-knn of every point at scan positions [p0, p1),
+// written to sel ((p1 - p0) x knn, each row ascending), plus the scan order
+// perm (n entries; identical on every caller for the same x).
+int knn_select(int64_t n, int64_t d, const double* x, int64_t knn, double two_sigma_sq, int64_t p0, int64_t p1,
+               int32_t* sel, int32_t* perm_out, int64_t* stats, cudaStream_t st) {
     const double inv = -1.0 / two_sigma_sq;  // graph.py:154
     const int64_t dp = (d + 15) / 16 * 16;
     const char* kenv = std::getenv("SPECLUST_KNN_KERNEL");
@@ -559,6 +589,9 @@ int knn_graph_build(int64_t n, int64_t d, const double* x, int64_t knn, double t
         if (cap > n - 1) cap = (int)(n - 1);  // lists can hold every other point
         if (cap < R) cap = R;
     }
+    const int64_t np = p1 - p0;  // positions of this call
+    const int64_t qtile0 = p0 / 128, qtile1 = ceil_div(p1, 128), nq = qtile1 - qtile0;
+    const int64_t nslots = nq * 128;  // list slots (whole query tiles)
     int rc;
     DevBuf<double> part, mean, rn, qn;
     DevBuf<float> xf, cnf, taus;
@@ -566,16 +599,12 @@ int knn_graph_build(int64_t n, int64_t d, const double* x, int64_t knn, double t
     DevBuf<unsigned long long> rmax, nflag;
     DevBuf<float2> lists;
     DevBuf<int> counts;
-    DevBuf<int32_t> sel, flagged, rev;
-    DevBuf<int64_t> rc_cnt, rev_ptr, len, tmp;
-    DevBuf<unsigned int> fill;
-    DevBuf<uint8_t> dup;
+    DevBuf<int32_t> flagged;
     const int64_t nbc = ceil_div(n, 256);
     const int64_t n_pad = (n + 127) / 128 * 128;
     if ((rc = part.alloc((size_t)nbc * d)) || (rc = mean.alloc(d)) || (rc = rn.alloc(n)) || (rc = qn.alloc(n)) ||
-        (rc = taus.alloc(n)) || (rc = rmax.alloc(1)) || (rc = nflag.alloc(1)) ||
-        (rc = lists.alloc((size_t)n * cap)) || (rc = counts.alloc(n)) || (rc = sel.alloc((size_t)n * knn)) ||
-        (rc = flagged.alloc(n)))
+        (rc = taus.alloc(nslots)) || (rc = rmax.alloc(1)) || (rc = nflag.alloc(1)) ||
+        (rc = lists.alloc((size_t)nslots * cap)) || (rc = counts.alloc(nslots)) || (rc = flagged.alloc(np)))
         return rc;
     // ---- prep: fp64 column means (the key is translation invariant; centring
     // shrinks |x| and with it the error bound)
@@ -614,8 +643,8 @@ int knn_graph_build(int64_t n, int64_t d, const double* x, int64_t knn, double t
         knn_prep_f16_kernel<<<(unsigned)ceil_div(n_pad, 8), 256, 0, st>>>(n, n_pad, d, dp64, x, mean.p, scale, perm,
                                                                           xh.p, cnf.p, qn.p);
         SC_LAUNCHED(1);
-        if ((rc = knn_candidates_tc(n, n_pad, dp64, xh.p, cnf.p, (float)(-2.0 / (scale * scale)), cap, R, lists.p,
-                                    counts.p, taus.p, st)))
+        if ((rc = knn_candidates_tc(n, n_pad, dp64, xh.p, cnf.p, (float)(-2.0 / (scale * scale)), qtile0, nq, cap, R,
+                                    lists.p, counts.p, taus.p, st)))
             return rc;
         // fp16 rounding of both operands (u = 2^-11) + fp32 accumulation of
         // dp64 products + fp32 rounding of |x_j|^2 and of the key, relative to
@@ -628,21 +657,23 @@ int knn_graph_build(int64_t n, int64_t d, const double* x, int64_t knn, double t
         SC_LAUNCHED(1);
         size_t smem = sizeof(float) * (KK * KM + KK * KN + KM * (KN + 1) + KN);
         cudaFuncSetAttribute(knn_cand_simt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        ProfScope prof("knn_tile", st, 2.0 * (double)n * (double)n * (double)d);
-        knn_cand_simt_kernel<<<(unsigned)ceil_div(n, KM), 256, smem, st>>>(n, (int)dp, xf.p, cnf.p, cap, R, lists.p,
-                                                                           counts.p, taus.p);
+        ProfScope prof("knn_tile", st, 2.0 * (double)np * (double)n * (double)d);
+        knn_cand_simt_kernel<<<(unsigned)nq, 256, smem, st>>>(n, qtile0, (int)dp, xf.p, cnf.p, cap, R, lists.p,
+                                                              counts.p, taus.p);
         SC_LAUNCHED(1);
         // fp32 inputs (u = 2^-24) and a dp-term fp32 accumulation
         cdelta = (2.0 * (double)dp + 16.0) * std::ldexp(1.0, -24);
     }
+    // list slots start at tile qtile0; the recheck addresses them from p0
+    const int64_t slot0 = p0 - qtile0 * 128;
     // ---- exact recheck + certificate
     {
         size_t smem = (size_t)8 * cap * (sizeof(double) + sizeof(int));
         cudaFuncSetAttribute(knn_recheck_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        ProfScope prof("knn_recheck", st, (double)n * cap * d * 8.0);
-        knn_recheck_kernel<<<(unsigned)ceil_div(n, 8), 256, smem, st>>>(n, d, x, knn, inv, cap, lists.p, counts.p,
-                                                                        taus.p, rn.p, qn.p, rmax.p, cdelta, perm,
-                                                                        sel.p, flagged.p, nflag.p);
+        ProfScope prof("knn_recheck", st, (double)np * cap * d * 8.0);
+        knn_recheck_kernel<<<(unsigned)ceil_div(np, 8), 256, smem, st>>>(
+            n, p0, p1, d, x, knn, inv, cap, lists.p + slot0 * cap, counts.p + slot0, taus.p + slot0, rn.p, qn.p,
+            rmax.p, cdelta, perm, sel, flagged.p, nflag.p);
         SC_LAUNCHED(1);
     }
     unsigned long long hflag = 0;
@@ -656,57 +687,138 @@ int knn_graph_build(int64_t n, int64_t d, const double* x, int64_t knn, double t
         DevBuf<unsigned long long> scratch;
         if ((rc = scratch.alloc((size_t)grid * n))) return rc;
         ProfScope prof("knn_fallback", st, (double)hflag * n * d * 8.0);
-        knn_fallback_kernel<<<(unsigned)grid, 512, 0, st>>>(n, d, x, knn, inv, flagged.p, (int64_t)hflag, scratch.p,
-                                                            sel.p);
+        knn_fallback_kernel<<<(unsigned)grid, 512, 0, st>>>(n, p0, d, x, knn, inv, perm, flagged.p, (int64_t)hflag,
+                                                            scratch.p, sel);
         SC_LAUNCHED(1);
-        SC_CUDA(cudaStreamSynchronize(st));
     }
-    // ---- union + CSR
-    if ((rc = rc_cnt.alloc(n)) || (rc = rev_ptr.alloc(n + 1)) || (rc = len.alloc(n)) ||
-        (rc = tmp.alloc(ceil_div(n, SCAN_BLK) + 1)) || (rc = fill.alloc(n)) || (rc = rev.alloc((size_t)n * knn)) ||
-        (rc = dup.alloc((size_t)n * knn)))
-        return rc;
-    ProfScope prof("knn_union", st, 0.0);
-    sort_rows_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(n, knn, sel.p);
-    SC_CUDA(cudaMemsetAsync(rc_cnt.p, 0, sizeof(int64_t) * n, st));
-    SC_CUDA(cudaMemsetAsync(fill.p, 0, sizeof(unsigned int) * n, st));
-    rev_count_kernel<<<(unsigned)ceil_div(n * knn, 256), 256, 0, st>>>(n * knn, sel.p, rc_cnt.p);
-    SC_LAUNCHED(2);
-    if ((rc = exclusive_scan_i64(n, rc_cnt.p, rev_ptr.p, tmp.p, st))) return rc;
-    rev_fill_kernel<<<(unsigned)ceil_div(n * knn, 256), 256, 0, st>>>(n, knn, sel.p, rev_ptr.p, fill.p, rev.p);
-    row_count_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, st>>>(n, knn, sel.p, rev_ptr.p, rev.p, dup.p, len.p);
-    SC_LAUNCHED(2);
-    if ((rc = exclusive_scan_i64(n, len.p, row_ptr, tmp.p, st))) return rc;
-    row_fill_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, st>>>(n, d, knn, x, two_sigma_sq, sel.p, rev_ptr.p, rev.p,
-                                                              dup.p, row_ptr, col, vals);
-    SC_LAUNCHED(1);
-    int64_t nnz = 0;
-    SC_CUDA(cudaMemcpyAsync(&nnz, row_ptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    SC_CUDA(cudaStreamSynchronize(st));
-    *nnz_out = nnz;
+    {
+        ProfScope prof("knn_union", st, 0.0);
+        sort_rows_kernel<<<(unsigned)ceil_div(np, 128), 128, 0, st>>>(np, knn, sel);
+        if (perm)
+            SC_CUDA(cudaMemcpyAsync(perm_out, perm, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, st));
+        else
+            iota_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, perm_out);
+        SC_LAUNCHED(2);
+    }
+    // the pooled scratch above is released on st; callers see sel/perm ordered on st
     if (stats) {
         stats[0] = R;
         stats[1] = cap;
         stats[2] = (int64_t)hflag;
-        stats[3] = nnz;
-        for (int q = 4; q < 8; ++q) stats[q] = 0;
+        for (int q = 3; q < 8; ++q) stats[q] = 0;
     }
+    return SC_OK;
+}
+
+// Union stage: CSR rows [r0, r1) (local row_ptr, global columns) of the
+// symmetrised kNN graph from the selections of all n points.
+int knn_union(int64_t n, int64_t d, const double* x, int64_t knn, double two_sigma_sq, const int32_t* sel,
+              const int32_t* perm, int64_t r0, int64_t r1, int64_t* row_ptr, int32_t* col, double* vals, int64_t cap,
+              int64_t* nnz_out, cudaStream_t st) {
+    const int64_t nl = r1 - r0;
+    int rc;
+    DevBuf<int32_t> pos, rev;
+    DevBuf<int64_t> rc_cnt, rev_ptr, len, tmp;
+    DevBuf<unsigned int> fill;
+    DevBuf<uint8_t> dup;
+    if ((rc = pos.alloc(n)) || (rc = rc_cnt.alloc(nl)) || (rc = rev_ptr.alloc(nl + 1)) || (rc = len.alloc(nl)) ||
+        (rc = tmp.alloc(ceil_div(std::max<int64_t>(n, nl), SCAN_BLK) + 1)) || (rc = fill.alloc(nl)))
+        return rc;
+    ProfScope prof("knn_union", st, 0.0);
+    pos_of_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, perm, pos.p);
+    SC_CUDA(cudaMemsetAsync(rc_cnt.p, 0, sizeof(int64_t) * nl, st));
+    SC_CUDA(cudaMemsetAsync(fill.p, 0, sizeof(unsigned int) * nl, st));
+    rev_count_kernel<<<(unsigned)ceil_div(n * knn, 256), 256, 0, st>>>(n * knn, r0, r1, sel, rc_cnt.p);
+    SC_LAUNCHED(2);
+    if ((rc = exclusive_scan_i64(nl, rc_cnt.p, rev_ptr.p, tmp.p, st))) return rc;
+    int64_t nrev = 0;
+    SC_CUDA(cudaMemcpyAsync(&nrev, rev_ptr.p + nl, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    SC_CUDA(cudaStreamSynchronize(st));
+    if ((rc = rev.alloc(std::max<int64_t>(nrev, 1))) || (rc = dup.alloc(std::max<int64_t>(nrev, 1)))) return rc;
+    rev_fill_kernel<<<(unsigned)ceil_div(n * knn, 256), 256, 0, st>>>(n, knn, r0, r1, sel, perm, rev_ptr.p, fill.p,
+                                                                      rev.p);
+    row_count_kernel<<<(unsigned)ceil_div(nl, 8), 256, 0, st>>>(nl, r0, knn, sel, pos.p, rev_ptr.p, rev.p, dup.p,
+                                                                len.p);
+    SC_LAUNCHED(2);
+    if ((rc = exclusive_scan_i64(nl, len.p, row_ptr, tmp.p, st))) return rc;
+    int64_t nnz = 0;
+    SC_CUDA(cudaMemcpyAsync(&nnz, row_ptr + nl, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    SC_CUDA(cudaStreamSynchronize(st));
+    *nnz_out = nnz;
+    if (nnz > cap)
+        return fail(SC_ERR_VALUE, "knn union: " + std::to_string(nnz) + " entries exceed the output capacity " +
+                                      std::to_string(cap));
+    row_fill_kernel<<<(unsigned)ceil_div(nl, 8), 256, 0, st>>>(nl, r0, d, knn, x, two_sigma_sq, sel, pos.p, rev_ptr.p,
+                                                               rev.p, dup.p, row_ptr, col, vals);
+    SC_LAUNCHED(1);
+    return SC_OK;
+}
+
+int knn_graph_build(int64_t n, int64_t d, const double* x, int64_t knn, double two_sigma_sq, int64_t* row_ptr,
+                    int32_t* col, double* vals, int64_t* nnz_out, int64_t* stats, cudaStream_t st) {
+    DevBuf<int32_t> sel, perm;
+    int rc;
+    if ((rc = sel.alloc((size_t)n * knn)) || (rc = perm.alloc(n))) return rc;
+    if ((rc = knn_select(n, d, x, knn, two_sigma_sq, 0, n, sel.p, perm.p, stats, st))) return rc;
+    if ((rc = knn_union(n, d, x, knn, two_sigma_sq, sel.p, perm.p, 0, n, row_ptr, col, vals, 2 * n * knn, nnz_out,
+                        st)))
+        return rc;
+    if (stats) stats[3] = *nnz_out;
     return SC_OK;
 }
 
 }  // namespace sc
 
-extern "C" int sc_knn_graph_f64(int64_t n, int64_t d, const double* x, int64_t knn, double two_sigma_sq,
-                                int64_t* row_ptr, int32_t* col, double* vals, int64_t* nnz_out, int64_t* stats_out,
-                                sc_stream_t stream) {
+static int check_knn_args(int64_t n, int64_t d, int64_t knn, double two_sigma_sq) {
     if (n < 2 || d < 1) return fail(SC_ERR_FORMAT, "point matrix must be 2-D with n >= 2, d >= 1");
     if (!(knn >= 1 && knn < n))
         return fail(SC_ERR_VALUE, "knn must satisfy 1 <= knn < n, got " + std::to_string(knn) + " for n=" +
                                       std::to_string(n));
     if (!(two_sigma_sq > 0)) return fail(SC_ERR_VALUE, "exp_decay requires sigma > 0");
     if (n >= (int64_t)INT32_MAX) return fail(SC_ERR_VALUE, "n must be < 2^31 for int32 column indices");
+    return SC_OK;
+}
+
+extern "C" int sc_knn_graph_f64(int64_t n, int64_t d, const double* x, int64_t knn, double two_sigma_sq,
+                                int64_t* row_ptr, int32_t* col, double* vals, int64_t* nnz_out, int64_t* stats_out,
+                                sc_stream_t stream) {
+    if (int rc = check_knn_args(n, d, knn, two_sigma_sq)) return rc;
     StreamScope stream_scope(as_stream(stream));
     return knn_graph_build(n, d, x, knn, two_sigma_sq, row_ptr, col, vals, nnz_out, stats_out, as_stream(stream));
+}
+
+extern "C" int sc_knn_select_f64(int64_t n, int64_t d, const double* x, int64_t knn, double two_sigma_sq, int64_t p0,
+                                 int64_t p1, int32_t* sel, int32_t* perm, int64_t* stats_out, sc_stream_t stream) {
+    if (int rc = check_knn_args(n, d, knn, two_sigma_sq)) return rc;
+    if (!(0 <= p0 && p0 <= p1 && p1 <= n) || p0 % 128 != 0)
+        return fail(SC_ERR_VALUE, "scan range [p0, p1) must lie in [0, n] with p0 a multiple of 128");
+    StreamScope stream_scope(as_stream(stream));
+    if (p0 == p1) {  // empty shard: still provide the scan order
+        int64_t tmp[8];
+        DevBuf<int32_t> s1;
+        if (int rc = s1.alloc((size_t)128 * knn)) return rc;
+        const int64_t q0 = std::min<int64_t>(p0, n - 1) / 128 * 128;
+        return knn_select(n, d, x, knn, two_sigma_sq, q0, q0 + 1, s1.p, perm, stats_out ? stats_out : tmp,
+                          as_stream(stream));
+    }
+    return knn_select(n, d, x, knn, two_sigma_sq, p0, p1, sel, perm, stats_out, as_stream(stream));
+}
+
+extern "C" int sc_knn_union_f64(int64_t n, int64_t d, const double* x, int64_t knn, double two_sigma_sq,
+                                const int32_t* sel, const int32_t* perm, int64_t r0, int64_t r1, int64_t* row_ptr,
+                                int32_t* col, double* vals, int64_t cap, int64_t* nnz_out, sc_stream_t stream) {
+    if (int rc = check_knn_args(n, d, knn, two_sigma_sq)) return rc;
+    if (!(0 <= r0 && r0 <= r1 && r1 <= n)) return fail(SC_ERR_VALUE, "row range [r0, r1) must lie in [0, n]");
+    StreamScope stream_scope(as_stream(stream));
+    if (r0 == r1) {
+        *nnz_out = 0;
+        const int64_t z = 0;
+        SC_CUDA(cudaMemcpyAsync(row_ptr, &z, sizeof(z), cudaMemcpyHostToDevice, as_stream(stream)));
+        SC_CUDA(cudaStreamSynchronize(as_stream(stream)));
+        return SC_OK;
+    }
+    return knn_union(n, d, x, knn, two_sigma_sq, sel, perm, r0, r1, row_ptr, col, vals, cap, nnz_out,
+                     as_stream(stream));
 }
 
 // exp(-d2 / (2 sigma^2)) per given pair (graph.py:136-141; build_similarity)

@@ -67,7 +67,7 @@ __device__ __forceinline__ void warp_bitonic_sort(float2* S, int lane) {
 
 template <int NKB, int STAGES, bool LSMEM>
 __global__ void __launch_bounds__(TC_THREADS, LSMEM ? 1 : 2)
-    knn_cand_tc_kernel(const __grid_constant__ CUtensorMap xmap, int64_t n, int64_t ntiles,
+    knn_cand_tc_kernel(const __grid_constant__ CUtensorMap xmap, int64_t n, int64_t ntiles, int64_t qtile0,
                        const float* __restrict__ cnk, float key_scale, int cap, int R, float2* __restrict__ lists,
                        int* __restrict__ counts, float* __restrict__ taus, long long* __restrict__ dbg) {
     using Lay = TcLayout<NKB, STAGES, LSMEM>;
@@ -86,7 +86,11 @@ __global__ void __launch_bounds__(TC_THREADS, LSMEM ? 1 : 2)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t row0 = (int64_t)blockIdx.x * 128;
+    // query tile qt (scan positions row0..row0+127); lists/counts/taus are
+    // indexed by position relative to the first query tile of the launch
+    const int64_t qt = qtile0 + blockIdx.x;
+    const int64_t row0 = qt * 128;
+    const int64_t lrow0 = (int64_t)blockIdx.x * 128;
 
     if (warp == 0 && lane == 0) tc::tma_prefetch(&xmap);
     if (warp == 1) {
@@ -123,7 +127,7 @@ __global__ void __launch_bounds__(TC_THREADS, LSMEM ? 1 : 2)
                 tc::mbar_expect_tx(&full[s], Lay::kB);
                 for (int kb = 0; kb < NKB; ++kb)
                     tc::tma_load_2d(sB + s * Lay::kB + kb * TC_TILE_BYTES, &xmap, &full[s], kb * 64,
-                                    (int)(((blockIdx.x + t) % ntiles) * 128));
+                                    (int)(((qt + t) % ntiles) * 128));
             }
         }
     } else if (warp == 1) {
@@ -144,7 +148,7 @@ __global__ void __launch_bounds__(TC_THREADS, LSMEM ? 1 : 2)
                 d_wait1 += c2 - c1;
                 // the accumulator slot is free, so is its column-norm slot
                 tc::mbar_expect_tx(&tfull[buf], 128 * 4);
-                tc::bulk_g2s(sCn + buf * 128, cnk + ((blockIdx.x + t) % ntiles) * 128, 128 * 4, &tfull[buf]);
+                tc::bulk_g2s(sCn + buf * 128, cnk + ((qt + t) % ntiles) * 128, 128 * 4, &tfull[buf]);
                 tc::fence_after();
 #pragma unroll
                 for (int kb = 0; kb < NKB; ++kb) {
@@ -169,7 +173,7 @@ __global__ void __launch_bounds__(TC_THREADS, LSMEM ? 1 : 2)
         const int64_t row = row0 + lrow;
         const bool valid = row < n;
         // list of this row: smem-resident or global (with a per-warp smem scratch)
-        float2* L = LSMEM ? sL + (size_t)lrow * TC_LIST_P : lists + (valid ? row : 0) * (int64_t)cap;
+        float2* L = LSMEM ? sL + (size_t)lrow * TC_LIST_P : lists + (valid ? lrow0 + lrow : 0) * (int64_t)cap;
         float2* scratch = LSMEM ? nullptr : sL + (size_t)quad * TC_LIST_P;
         int cnt = 0;
         float tau = INFINITY;
@@ -182,7 +186,7 @@ __global__ void __launch_bounds__(TC_THREADS, LSMEM ? 1 : 2)
             d_wait0 += c1 - c0;
             tc::fence_after();
             // scan order: the query tile's own (locality-sorted) neighbourhood first
-            const int64_t col0 = ((blockIdx.x + t) % ntiles) * 128;
+            const int64_t col0 = ((qt + t) % ntiles) * 128;
             const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * 128);
 #pragma unroll 1
             for (int half = 0; half < 2; ++half) {
@@ -225,7 +229,7 @@ __global__ void __launch_bounds__(TC_THREADS, LSMEM ? 1 : 2)
                         want &= want - 1;
                         const int c_src = __shfl_sync(0xffffffffu, cnt, src);
                         float2* Ls = LSMEM ? sL + (size_t)(quad * 32 + src) * TC_LIST_P : scratch;
-                        const float2* Lg = lists + (row0 + quad * 32 + src) * (int64_t)cap;
+                        const float2* Lg = lists + (lrow0 + quad * 32 + src) * (int64_t)cap;
                         for (int e = lane; e < TC_LIST_P; e += 32) {
                             float2 val = make_float2(INFINITY, __int_as_float(-1));
                             if (e < c_src) val = LSMEM ? Ls[e] : Lg[e];
@@ -234,7 +238,7 @@ __global__ void __launch_bounds__(TC_THREADS, LSMEM ? 1 : 2)
                         __syncwarp();
                         warp_bitonic_sort(Ls, lane);
                         if (!LSMEM) {
-                            float2* Lw = lists + (row0 + quad * 32 + src) * (int64_t)cap;
+                            float2* Lw = lists + (lrow0 + quad * 32 + src) * (int64_t)cap;
                             for (int e = lane; e < R; e += 32) Lw[e] = Ls[e];
                         }
                         const float new_tau = Ls[R - 1].x;
@@ -261,11 +265,11 @@ __global__ void __launch_bounds__(TC_THREADS, LSMEM ? 1 : 2)
         }
         if (valid) {
             if (LSMEM) {
-                float2* Lg = lists + row * (int64_t)cap;
+                float2* Lg = lists + (lrow0 + lrow) * (int64_t)cap;
                 for (int e = 0; e < cnt; ++e) Lg[e] = L[e];
             }
-            counts[row] = cnt;
-            taus[row] = tau;
+            counts[lrow0 + lrow] = cnt;
+            taus[lrow0 + lrow] = tau;
         }
     }
     if (dbg && lane == 0 && warp < 3) {

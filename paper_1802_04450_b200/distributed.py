@@ -17,9 +17,10 @@ collectives.  The path shards the way SURVEY.md §8(e) prescribes:
   k-means++ keeps the reference's numpy stream on every rank (identical
   draws, no RNG traffic); the D^2 sample is located by an all-gather of the
   per-shard weight sums (kmeans.py:119-132).
-* graph: round 1 builds the full kNN graph on every rank and keeps its row
-  block (query-row sharding of the tensor-core kNN tiles plus an all-to-all
-  of reverse edges is the next step).
+* graph: query tiles (in the locality scan order) are split over ranks; each
+  rank scans its tiles against all points (X is replicated), one all-gather
+  of the n x knn int32 selection carries the reverse edges, and each rank
+  writes its own CSR row block (graph.py:185-237).
 
 The drivers are written against two small interfaces — ``Comm`` (the
 collectives) and an *ops* object (per-shard compute).  ``CudaOps`` calls the
@@ -128,6 +129,21 @@ class CudaOps:
         from .graph import knn_graph_device
 
         return knn_graph_device(x, knn, measure)
+
+    def points(self, x):
+        from .graph import _points_device
+
+        return _points_device(x)
+
+    def knn_select(self, x, knn, measure, p0, p1):
+        from .graph import knn_select_device
+
+        return knn_select_device(x, knn, measure, p0, p1)
+
+    def knn_union(self, x, knn, measure, sel, perm, r0, r1):
+        from .graph import knn_union_device
+
+        return knn_union_device(x, knn, measure, sel, perm, r0, r1)
 
     def slice_rows(self, w: DeviceCsr, r0: int, r1: int) -> DeviceCsr:
         rp = w.row_ptr[r0 : r1 + 1]
@@ -290,6 +306,31 @@ class _CudaKpp:
         i = nat.C.c_int64(-1)
         nat.check(self.ops.lib.sc_kmeanspp_nth_free(self.h, int(r), nat.C.byref(i)))
         return int(i.value)
+
+
+# ---------------------------------------------------------------------------
+# query-sharded kNN graph (graph.py:185-237)
+def scan_bounds(n: int, world: int) -> list[int]:
+    """Scan-position shards in whole 128-point query tiles."""
+    tiles = -(-n // 128)
+    return [min(n, b * 128) for b in row_bounds(tiles, world)]
+
+
+def knn_graph_sharded(ops, comm: Comm, x, knn: int, measure):
+    """Row block [bounds[rank], bounds[rank+1]) of the union-kNN graph.
+
+    Each rank selects the top-knn of its query tiles (the tensor-core scan
+    against all points), one all-gather assembles the n x knn selection (the
+    exchange that carries the reverse edges), and each rank emits its own CSR
+    rows from it.  Returns (local CSR, row bounds)."""
+    xd = ops.points(x)
+    n = int(xd.shape[0])
+    pb = scan_bounds(n, comm.world)
+    sel_loc, perm = ops.knn_select(xd, knn, measure, pb[comm.rank], pb[comm.rank + 1])
+    sel = comm.gather_rows(sel_loc.contiguous(), pb)
+    bounds = row_bounds(n, comm.world)
+    w_loc = ops.knn_union(xd, knn, measure, sel, perm, bounds[comm.rank], bounds[comm.rank + 1])
+    return w_loc, bounds
 
 
 # ---------------------------------------------------------------------------
@@ -556,20 +597,23 @@ def run_sharded(cfg, comm: Comm, ops=None):
     src = cfg.input
     if isinstance(src, PointsInput) and src.pattern == "knn":
         pts = src.points if isinstance(src.points, torch.Tensor) else as_points(src.points)
-        w = ops.knn_graph(pts, src.knn, src.measure)
+        if src.measure.kind != "exp_decay":
+            raise NotImplementedError("the sharded kNN graph supports the exp_decay measure")
+        w_loc, bounds = knn_graph_sharded(ops, comm, pts, src.knn, src.measure)
+        n = bounds[-1]
     elif isinstance(src, MatrixInput) and src.matrix is not None:
         from .sparse import CsrMatrix, coo_canonicalize, coo_to_csr
 
         m = src.matrix
         host = m if isinstance(m, CsrMatrix) else coo_to_csr(coo_canonicalize(m))
         w = ops.from_host_csr(host) if hasattr(ops, "from_host_csr") else host.device()
+        n = w.n_rows
+        bounds = row_bounds(n, comm.world)
+        w_loc = ops.slice_rows(w, bounds[comm.rank], bounds[comm.rank + 1])
+        del w
     else:
         raise NotImplementedError("sharded run supports PointsInput(pattern='knn') and in-memory MatrixInput")
-    n = w.n_rows
-    bounds = row_bounds(n, comm.world)
     r0, r1 = bounds[comm.rank], bounds[comm.rank + 1]
-    w_loc = ops.slice_rows(w, r0, r1)
-    del w
     sync()
     timings["graph"] = time.perf_counter() - t
 

@@ -154,6 +154,56 @@ def knn_graph_device(x, knn: int, m: SimilarityMeasure, return_stats: bool = Fal
     return w
 
 
+def _points_device(x):
+    torch = nat.torch_cuda()
+    if isinstance(x, torch.Tensor):
+        return x.to(device="cuda", dtype=torch.float64, non_blocking=True).contiguous()
+    return nat.to_device(as_points(x), torch.float64)
+
+
+def knn_select_device(x, knn: int, m: SimilarityMeasure, p0: int, p1: int):
+    """Selection stage of the kNN graph for the points at scan positions
+    [p0, p1) (sc_knn_select_f64): returns (sel (p1-p0, knn) int32 CUDA,
+    perm (n,) int32 CUDA scan order)."""
+    _require_exp_decay(m, "knn graph")
+    torch = nat.torch_cuda()
+    xd = _points_device(x)
+    n, d = xd.shape
+    if not 1 <= knn < n:
+        raise ValueError(f"knn must satisfy 1 <= knn < n, got {knn} for n={n}")
+    sel = torch.empty((max(p1 - p0, 1), knn), dtype=torch.int32, device="cuda")
+    perm = torch.empty(n, dtype=torch.int32, device="cuda")
+    nat.check(nat.load().sc_knn_select_f64(n, d, nat.ptr(xd), knn, m.two_sigma_sq(), p0, p1, nat.ptr(sel),
+                                           nat.ptr(perm), None, nat.stream_handle()))
+    return sel[: p1 - p0], perm
+
+
+def knn_union_device(x, knn: int, m: SimilarityMeasure, sel, perm, r0: int, r1: int) -> DeviceCsr:
+    """Union stage: CSR rows [r0, r1) of W (global columns) from the full
+    scan-order selection (sc_knn_union_f64)."""
+    torch = nat.torch_cuda()
+    xd = _points_device(x)
+    n, d = xd.shape
+    nl = r1 - r0
+    row_ptr = torch.empty(nl + 1, dtype=torch.int64, device="cuda")
+    nnz = nat.C.c_int64(0)
+    lib = nat.load()
+    cap = 2 * nl * knn + 1024
+    for _ in range(2):  # a shard whose reverse edges exceed 2*knn per row retries at the exact size
+        col = torch.empty(cap, dtype=torch.int32, device="cuda")
+        vals = torch.empty(cap, dtype=torch.float64, device="cuda")
+        rc = lib.sc_knn_union_f64(n, d, nat.ptr(xd), knn, m.two_sigma_sq(), nat.ptr(sel), nat.ptr(perm), r0, r1,
+                                  nat.ptr(row_ptr), nat.ptr(col), nat.ptr(vals), cap, nat.C.byref(nnz),
+                                  nat.stream_handle())
+        if rc == 0:
+            k = nnz.value
+            return DeviceCsr(nl, n, row_ptr, col[:k], vals[:k])
+        if nnz.value <= cap:
+            nat.check(rc)
+        cap = nnz.value
+    nat.check(rc)
+
+
 def build_edges_knn(x, knn: int, m: SimilarityMeasure) -> np.ndarray:
     """Union kNN pattern as (i, j) pairs with i < j in row-major order
     (reference graph.py:185-204), computed on the GPU."""

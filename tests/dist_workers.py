@@ -55,7 +55,24 @@ def pipeline_worker(rank, world):
                 ncut=np.array(rep.ncut_value), sse=rep.labeling.sse_history, centroids=rep.labeling.centroids)
 
 
-WORKERS = {"lanczos": lanczos_worker, "pipeline": pipeline_worker}
+def graph_worker(rank, world):
+    from paper_1802_04450_b200.distributed import knn_graph_sharded
+
+    x, _, cfg = blobs_cfg()
+    comm = Comm("cpu")
+    w, bounds = knn_graph_sharded(NumpyOps(), comm, x, 8, cfg.input.measure)
+    nnz = comm.gather_scalars([w.nnz])[:, 0].astype(np.int64)
+    rp = comm.gather_rows(w.row_ptr[1:], bounds)
+    offs = np.concatenate(([0], np.cumsum(nnz)))
+    rb = np.asarray(bounds)
+    row_ptr = np.concatenate(([0], rp.numpy() + np.repeat(offs[:-1], np.diff(rb))))
+    nb = [int(v) for v in offs]
+    col = comm.gather_rows(w.col, nb).numpy()
+    vals = comm.gather_rows(w.vals, nb).numpy()
+    return dict(row_ptr=row_ptr, col=col, vals=vals)
+
+
+WORKERS = {"lanczos": lanczos_worker, "pipeline": pipeline_worker, "graph": graph_worker}
 
 
 def spawn_entry(rank, world, port, name, out_dir):

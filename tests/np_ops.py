@@ -51,6 +51,35 @@ class NumpyOps:
         rp, col, vals = orc.csr_from_edges(x.shape[0], e, orc.edge_weights(x, e, measure.sigma))
         return HostCsr(x.shape[0], x.shape[0], _t(rp, torch.int64), _t(col, torch.int64), _t(vals))
 
+    def points(self, x):
+        return np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+
+    def knn_select(self, x, knn, measure, p0, p1):
+        # identity scan order; rows ascending like the device selection
+        inv = -1.0 / measure.two_sigma_sq()
+        sel = np.array([np.sort(orc.knn_select_row(x, i, knn, inv)) for i in range(p0, p1)],
+                       dtype=np.int64).reshape(p1 - p0, knn)
+        return _t(sel, torch.int32), _t(np.arange(x.shape[0]), torch.int32)
+
+    def knn_union(self, x, knn, measure, sel, perm, r0, r1):
+        sel, perm = sel.numpy().astype(np.int64), perm.numpy().astype(np.int64)
+        n = x.shape[0]
+        owner = np.repeat(perm, knn)  # point of each selection entry
+        tgt = sel.ravel()
+        # forward entries of local rows + reverse entries pointing into them
+        fwd = (owner >= r0) & (owner < r1)
+        rev = (tgt >= r0) & (tgt < r1)
+        rows = np.concatenate((owner[fwd], tgt[rev]))
+        cols = np.concatenate((tgt[fwd], owner[rev]))
+        key = np.unique(rows * n + cols)
+        rows, cols = key // n, key % n
+        rp = np.zeros(r1 - r0 + 1, dtype=np.int64)
+        np.add.at(rp, rows - r0 + 1, 1)
+        lo, hi = np.minimum(rows, cols), np.maximum(rows, cols)  # once per unordered pair, i < j
+        diff = x[lo] - x[hi]
+        vals = np.exp(-np.einsum("ij,ij->i", diff, diff) / measure.two_sigma_sq())
+        return HostCsr(r1 - r0, n, _t(np.cumsum(rp), torch.int64), _t(cols, torch.int64), _t(vals))
+
     def from_host_csr(self, m):
         return HostCsr(m.n_rows, m.n_cols, _t(m.row_ptr, torch.int64), _t(m.col_idx, torch.int64), _t(m.vals))
 

@@ -55,15 +55,29 @@ def test_pipeline_sharded_matches_oracle(tmp_path):
     x, truth, _ = dw.blobs_cfg()
     ref = orc.run_points(x, 8, float(np.sqrt(6.0)), 4)
     w1 = run_world("pipeline", 1, tmp_path)[0]
-    w2 = run_world("pipeline", 2, tmp_path)
-    for r in w2:
-        assert np.array_equal(r["labels"], w2[0]["labels"])
-    got = w2[0]
-    assert np.max(np.abs(got["values"] - ref["values"]) / np.abs(ref["values"])) <= 1e-8
-    assert orc.ari(got["labels"], ref["labels"]) >= 0.999
-    assert orc.ari(got["labels"], w1["labels"]) == 1.0
-    assert abs(float(got["ncut"]) - ref["ncut"]) <= 1e-10 * max(1.0, ref["ncut"])
-    assert orc.ari(got["labels"], truth) >= 0.99
+    for world in (2, 3):
+        res = run_world("pipeline", world, tmp_path)
+        for r in res:
+            assert np.array_equal(r["labels"], res[0]["labels"])
+        got = res[0]
+        assert np.max(np.abs(got["values"] - ref["values"]) / np.abs(ref["values"])) <= 1e-8
+        assert orc.ari(got["labels"], ref["labels"]) >= 0.999
+        assert orc.ari(got["labels"], w1["labels"]) == 1.0
+        assert abs(float(got["ncut"]) - ref["ncut"]) <= 1e-10 * max(1.0, ref["ncut"])
+        assert orc.ari(got["labels"], truth) >= 0.99
+
+
+def test_knn_graph_sharded_rows_match_oracle(tmp_path):
+    """Query-tile sharded selection + all-gather + per-rank union reassembles
+    the reference CSR bit for bit (graph.py:185-237)."""
+    x, _, _ = dw.blobs_cfg()
+    e = orc.knn_edges(x, 8, float(np.sqrt(6.0)))
+    rp, col, vals = orc.csr_from_edges(x.shape[0], e, orc.edge_weights(x, e, float(np.sqrt(6.0))))
+    for world in (2, 3):
+        got = run_world("graph", world, tmp_path)[0]
+        assert np.array_equal(got["row_ptr"], rp)
+        assert np.array_equal(got["col"], col)
+        assert np.array_equal(got["vals"], vals)
 
 
 @pytest.mark.parametrize("world", [1, 2, 3])

@@ -183,3 +183,73 @@ def test_run_sharded_world1_cuda_matches_oracle(ops):
     assert np.max(np.abs(rep.eigenvalues - ref["values"]) / np.abs(ref["values"])) <= 1e-8
     assert orc.ari(rep.labeling.labels, ref["labels"]) >= 0.999
     assert abs(rep.ncut_value - ref["ncut"]) <= 1e-10 * max(1.0, ref["ncut"])
+
+
+def _assemble(parts):
+    rp = [np.zeros(1, dtype=np.int64)]
+    off = 0
+    for w in parts:
+        r = w.row_ptr.cpu().numpy()
+        rp.append(r[1:] + off)
+        off += int(r[-1])
+    col = np.concatenate([w.col.cpu().numpy() for w in parts]).astype(np.int64)
+    vals = np.concatenate([w.vals.cpu().numpy() for w in parts])
+    return np.concatenate(rp), col, vals
+
+
+@pytest.mark.parametrize("n,d,knn,world", [(900, 5, 7, 2), (5000, 32, 16, 3), (20000, 64, 32, 5), (300, 4, 3, 4)])
+def test_knn_select_union_shards_reassemble(ops, n, d, knn, world):
+    """Query-tile shards of the selection + per-rank unions == the one-call
+    graph, bit for bit, and == the oracle (graph.py:185-237)."""
+    from paper_1802_04450_b200.distributed import row_bounds, scan_bounds
+    from paper_1802_04450_b200.graph import knn_graph_device
+
+    import paper_1802_04450_b200 as sc
+
+    x, _ = orc.blobs(n, d, 6, 3.0, seed=n)
+    m = sc.SimilarityMeasure.exp_decay(1.7)
+    xd = cu(x)
+    pb = scan_bounds(n, world)
+    sels, perms = [], []
+    for r in range(world):
+        s, p = ops.knn_select(xd, knn, m, pb[r], pb[r + 1])
+        sels.append(s)
+        perms.append(p)
+    for p in perms[1:]:
+        assert torch.equal(p, perms[0])  # the scan order is replicated
+    sel = torch.cat(sels)
+    rb = row_bounds(n, world)
+    parts = [ops.knn_union(xd, knn, m, sel, perms[0], rb[r], rb[r + 1]) for r in range(world)]
+    rp, col, vals = _assemble(parts)
+    full = knn_graph_device(x, knn, m)
+    assert np.array_equal(rp, full.row_ptr.cpu().numpy())
+    assert np.array_equal(col, full.col.cpu().numpy())
+    assert np.array_equal(vals, full.vals.cpu().numpy())
+    if n <= 5000:
+        e = orc.knn_edges(x, knn, 1.7)
+        orp, ocol, ovals = orc.csr_from_edges(n, e, orc.edge_weights(x, e, 1.7))
+        assert np.array_equal(rp, orp) and np.array_equal(col, ocol)
+        assert np.all(np.abs(vals - ovals) <= 2 * np.spacing(ovals))  # exp: CUDA vs numpy
+
+
+def test_knn_union_capacity_error_reports_size(ops):
+    import paper_1802_04450_b200 as sc
+    from paper_1802_04450_b200 import _native as nat
+    from paper_1802_04450_b200.errors import BadConfig
+
+    x, _ = orc.blobs(500, 4, 3, 3.0, seed=1)
+    m = sc.SimilarityMeasure.exp_decay(1.0)
+    xd = cu(x)
+    sel, perm = ops.knn_select(xd, 5, m, 0, 500)
+    rp = torch.empty(501, dtype=torch.int64, device="cuda")
+    col = torch.empty(4, dtype=torch.int32, device="cuda")
+    vals = torch.empty(4, dtype=torch.float64, device="cuda")
+    nnz = nat.C.c_int64(0)
+    rc = nat.load().sc_knn_union_f64(500, 4, nat.ptr(xd), 5, m.two_sigma_sq(), nat.ptr(sel), nat.ptr(perm), 0, 500,
+                                     nat.ptr(rp), nat.ptr(col), nat.ptr(vals), 4, nat.C.byref(nnz),
+                                     nat.stream_handle())
+    assert rc != 0 and nnz.value > 4
+    with pytest.raises(BadConfig):
+        nat.check(rc)
+    w = ops.knn_union(xd, 5, m, sel, perm, 0, 500)
+    assert w.nnz == nnz.value
