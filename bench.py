@@ -135,7 +135,7 @@ def run_reference_arm(args, wl):
     est, sample, _ = cpu_reference(n, d, knn, k, cs, sample_n, args.steps, args.warmup)
     line = {
         "metric": METRIC, "value": est, "unit": "s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": est * 1e3, "higher_is_better": False, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": est * 1e3, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{args.workload}: blobs N={n} d={d} kNN={knn} k={k} (BASELINE.json configs[1])"},
         "impl": "reference",
@@ -156,6 +156,8 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=3000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the public-API end-to-end timing (ncu runs)")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the sharded driver (distributed.run_sharded) even at N=1; it is always used for N>1")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":
@@ -174,14 +176,21 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    # N > 1: one problem sharded over the ranks (strong scaling, SURVEY.md
+    # §8(e)); every rank holds the same X
+    sharded = world > 1 or args.sharded
+    if sharded:
+        from paper_1802_04450_b200 import distributed as dsc
+
+        comm, ops = dsc.Comm("cuda"), dsc.CudaOps()
 
     def barrier():
         if world > 1:
             dist.barrier()
 
     n, d, knn, k, cs = wl
-    x_host, _ = make_blobs(n, d, k, cs, seed=rank)
+    x_host, _ = make_blobs(n, d, k, cs, seed=0)
     x_pin = torch.from_numpy(x_host).pin_memory()
     x_dev = x_pin.to("cuda")
     sigma = float(np.sqrt(d))
@@ -197,7 +206,11 @@ def main():
 
     def device_step():
         # X already resident in HBM: the CUDA tensor goes straight to the engine
-        return run_device(cfg_for(x_dev))
+        if sharded:
+            rep = dsc.run_sharded(cfg_for(x_dev), comm, ops)
+            return rep, dsc.last_info["nnz"]
+        rep, w = run_device(cfg_for(x_dev))
+        return rep, w.nnz
 
     for _ in range(args.warmup):
         device_step()
@@ -214,11 +227,11 @@ def main():
         for _ in range(args.steps):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            rep, w = device_step()
+            rep, nnz = device_step()
             e1.record()
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1) / 1e3)
-            reports.append((rep, w.nnz))
+            reports.append((rep, nnz))
     barrier()
     torch.cuda.synchronize()
     launches = int(lib.sc_launch_count())
@@ -245,7 +258,7 @@ def main():
     for _ in range(0 if args.no_e2e else args.steps):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        rep_h = sc.run(cfg_for(x_pin))
+        rep_h = dsc.run_sharded(cfg_for(x_pin), comm, ops) if sharded else sc.run(cfg_for(x_pin))
         _ = rep_h.labeling.labels.sum()
         torch.cuda.synchronize()
         e2e_times.append(time.perf_counter() - t0)
@@ -274,10 +287,11 @@ def main():
     line = {
         "metric": METRIC, "value": step_max, "unit": "s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_max * 1e3, "higher_is_better": False,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{args.workload}: blobs N={n} d={d} kNN={knn} k={k} cs={cs} (BASELINE.json configs[1])",
                    "inputs": "X resident in HBM (512 MB > L2) between steps", "parallelism":
-                   "replicas" if world > 1 else "single-gpu", "nnz": nnz},
+                   f"sharded x{world} (query tiles / row blocks / point shards, NCCL)" if sharded else "single-gpu",
+                   "nnz": nnz},
         "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(x_host.nbytes),
                 "d2h_bytes_per_step": int(rep.labeling.labels.nbytes + rep.labeling.centroids.nbytes + 8 * n)},
         "gpu_launches": launches // max(1, args.steps) * args.steps,
@@ -288,8 +302,8 @@ def main():
         "kmeans_iters": km_iters,
         "kernels_ms_per_step": {c: round(v[0], 3) for c, v in kstats.items() if v[0] > 0},
         "step_times_s": [round(t, 4) for t in times],
-        "eigen": {kk: v for kk, v in __import__("paper_1802_04450_b200.pipeline", fromlist=["x"]).last_info
-                  .get("eigen", {}).items() if kk != "history"},
+        "eigen": {kk: v for kk, v in (dsc.last_info if sharded else __import__(
+            "paper_1802_04450_b200.pipeline", fromlist=["x"]).last_info).get("eigen", {}).items() if kk != "history"},
     }
     clk = clocks.summary()
     line["clocks"] = clk

@@ -137,6 +137,7 @@ typedef struct {
     int64_t matvecs;         /* operator applications       */
     int64_t n_history;       /* valid entries in history    */
     double history[512];     /* residual_history (first 512 sweeps) */
+    int64_t second_passes;   /* steps that needed a second CGS pass */
 } sc_lanczos_stats;
 
 /* RCI session (eigen.py:86-266).  m <= 0 selects default_subspace_dim. */

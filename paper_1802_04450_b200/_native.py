@@ -32,6 +32,7 @@ class LanczosStats(C.Structure):
         ("matvecs", C.c_int64),
         ("n_history", C.c_int64),
         ("history", C.c_double * 512),
+        ("second_passes", C.c_int64),
     ]
 
 

@@ -8,12 +8,13 @@
 // column).  The projected matrix T is m x m column-major.
 //
 // Per Lanczos step (reference: eigen.py:152-179):
-//   h1 = B^T w (alpha = h1[j]);  w -= B h1;  h2 = B^T w;  w -= B h2;  beta = |w|
-// i.e. two classical Gram-Schmidt passes over the raw product, which subsume
+//   h1 = B^T w (alpha = h1[j]);  w -= B h1;  [h2 = B^T w;  w -= B h2;]  beta = |w|
+// i.e. a full classical Gram-Schmidt pass over the raw product, which subsumes
 // the reference's three-term subtraction (eigen.py:160) — every component
-// that subtraction removes is also removed by the first full pass.  T, the
-// breakdown rule, the convergence/verification logic and the thick restart
-// follow eigen.py:166-239 exactly.
+// that subtraction removes is also removed by the full pass — and a second
+// pass only when the first cancelled most of |w| (DGKS criterion, see
+// advance()).  T, the breakdown rule, the convergence/verification logic and
+// the thick restart follow eigen.py:166-239 exactly.
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -28,6 +29,8 @@ namespace sc {
 constexpr int GT_ROWS = 1024;     // rows per gemv_t partial block
 constexpr int GN_THREADS = 256;   // rows per gemv_n block
 constexpr double kBreakdownRtol = 1e-13;  // eigen.py:50
+// second CGS pass when the first one removed more than 1 - eta^2 of |w|^2
+constexpr double kReorthEta = 0.05;
 
 // ---- kernels ------------------------------------------------------------------
 __global__ void fill_normal_kernel(int64_t n, uint64_t seed, uint64_t stream_id, double* __restrict__ out) {
@@ -42,17 +45,25 @@ __global__ void fill_normal_offset_kernel(int64_t n, int64_t offset, uint64_t se
     if (i < n) out[i] = philox_normal(seed, stream_id, (uint64_t)(offset + i));
 }
 
-// part[b * ncols + c] = sum_{r in block b} B[c * ld + r] * w[r]
+// part[b * ncols + c] = sum_{r in block b} B[c * ld + r] * w[r];
+// optional sq_part[b] = sum_{r in block b} w[r]^2 (|w| before the projection)
 __global__ void __launch_bounds__(256) gemv_t_partial_kernel(int64_t n, int64_t ld, int ncols,
                                                              const double* __restrict__ B,
                                                              const double* __restrict__ w,
-                                                             double* __restrict__ part) {
+                                                             double* __restrict__ part,
+                                                             double* __restrict__ sq_part) {
     __shared__ double ws[GT_ROWS];
     const int64_t r0 = (int64_t)blockIdx.x * GT_ROWS;
     const int rows = (int)imin64(GT_ROWS, n - r0);
     for (int i = threadIdx.x; i < GT_ROWS; i += blockDim.x) ws[i] = i < rows ? w[r0 + i] : 0.0;
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (sq_part && warp == 0) {
+        double s = 0.0;
+        for (int t = lane; t < GT_ROWS; t += 32) s = fma(ws[t], ws[t], s);
+        s = warp_sum(s);
+        if (lane == 0) sq_part[blockIdx.x] = s;
+    }
     for (int c = warp; c < ncols; c += 8) {
         const double* col = B + (int64_t)c * ld + r0;
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
@@ -379,21 +390,20 @@ struct sc_lanczos {
     cudaStream_t st = nullptr;
     int state = 0;  // 0 need_matvec, 1 converged, 2 failed
     int64_t j = 0;
-    int64_t restarts = 0, breakdowns = 0, matvecs = 0;
+    int64_t restarts = 0, breakdowns = 0, matvecs = 0, second_passes = 0;
     uint64_t rng_stream = 0;
     double scale = 0.0;
     std::vector<double> history, pending, theta_k, est_k;
     bool has_pending = false;
 
-    DevBuf<double> B, T, w, part, h, sqp, scal, Y, A, Z, wraw, wsort, S, lastrow, vectors;
+    DevBuf<double> B, T, w, part, h, sqp, sq0, scal, Y, A, Z, wraw, wsort, S, lastrow, vectors;
     DevBuf<int> info, nonfinite;
     int64_t nb_t = 0, nb_n = 0;
     static constexpr int64_t fz_blocks = 4 * kNumSMs;  // persistent grid of the fused pass
 
     // ---- building blocks
-    int project(const double* x, int ncols, bool fused_norm_unused = false) {
-        (void)fused_norm_unused;
-        gemv_t_partial_kernel<<<(unsigned)nb_t, 256, 0, st>>>(n, ld, ncols, B.p, x, part.p);
+    int project(const double* x, int ncols, double* sq_part = nullptr) {
+        gemv_t_partial_kernel<<<(unsigned)nb_t, 256, 0, st>>>(n, ld, ncols, B.p, x, part.p, sq_part);
         reduce_cols_kernel<<<(unsigned)ceil_div((int64_t)ncols * 32, 256), 256, 0, st>>>(nb_t, ncols, part.p, h.p);
         SC_LAUNCHED(2);
         return SC_OK;
@@ -467,7 +477,7 @@ struct sc_lanczos {
         int rc;
         if ((rc = B.alloc((size_t)ld * (m + 1))) || (rc = T.alloc((size_t)m * m)) || (rc = w.alloc(ld)) ||
             (rc = part.alloc((size_t)std::max<int64_t>(nb_t, fz_blocks) * (m + 1))) || (rc = h.alloc(m + 1)) ||
-            (rc = sqp.alloc(nb_n)) ||
+            (rc = sqp.alloc(nb_n)) || (rc = sq0.alloc(nb_t)) ||
             (rc = scal.alloc(8)) || (rc = A.alloc((size_t)m * m)) || (rc = Z.alloc((size_t)m * m)) ||
             (rc = wraw.alloc(m)) || (rc = wsort.alloc(m)) || (rc = S.alloc((size_t)m * k)) ||
             (rc = lastrow.alloc(k)) || (rc = info.alloc(1)) || (rc = nonfinite.alloc(1)))
@@ -504,21 +514,36 @@ struct sc_lanczos {
             if (bad) return fail(SC_ERR_VALUE, "out_slot contains non-finite values");
         }
         const int cnt = (int)(j + 1);
+        double ab[4];
         {
-            // two CGS passes = four GEMV passes over the basis
-            ProfScope prof("reorth", st, 4.0 * (double)n * cnt * 8.0);
-            if ((rc = project(w.p, cnt))) return rc;  // h[j] = alpha = q_j^T w
-            // keep alpha before the second pass overwrites h
+            // Full classical Gram-Schmidt against the whole basis; the first
+            // pass also removes the three-term-recurrence components (h[j] =
+            // alpha = q_j^T w).  The reference always runs the recurrence plus
+            // two CGS passes (eigen.py:157-163); here a second pass runs only
+            // when the first one cancelled most of |w| (|w1| < kReorthEta |w0|),
+            // the case in which one pass can leave w non-orthogonal beyond
+            // working precision ("twice is enough", DGKS).  Otherwise the
+            // result is orthogonal to working precision after one pass.
+            ProfScope prof("reorth", st, 2.0 * (double)n * cnt * 8.0);
+            if ((rc = project(w.p, cnt, sq0.p))) return rc;
             commit_alpha_kernel<<<1, 32, 0, st>>>(m, j, h.p, T.p, scal.p);
             SC_LAUNCHED(1);
-            if ((rc = subtract(w.p, cnt, false))) return rc;
-            if ((rc = project(w.p, cnt)) || (rc = subtract(w.p, cnt, true))) return rc;
+            if ((rc = subtract(w.p, cnt, true))) return rc;
+            finish_norm_kernel<<<1, 1024, 0, st>>>(nb_n, sqp.p, scal.p, 0);
+            finish_norm_kernel<<<1, 1024, 0, st>>>(nb_t, sq0.p, scal.p, 3);
+            SC_LAUNCHED(2);
+            SC_CUDA(cudaMemcpyAsync(ab, scal.p, sizeof(double) * 4, cudaMemcpyDeviceToHost, st));
+            SC_CUDA(cudaStreamSynchronize(st));
         }
-        finish_norm_kernel<<<1, 1024, 0, st>>>(nb_n, sqp.p, scal.p, 0);
-        SC_LAUNCHED(1);
-        double ab[3];
-        SC_CUDA(cudaMemcpyAsync(ab, scal.p, sizeof(double) * 3, cudaMemcpyDeviceToHost, st));
-        SC_CUDA(cudaStreamSynchronize(st));
+        if (ab[0] < kReorthEta * ab[3]) {
+            ProfScope prof("reorth", st, 2.0 * (double)n * cnt * 8.0);
+            ++second_passes;
+            if ((rc = project(w.p, cnt)) || (rc = subtract(w.p, cnt, true))) return rc;
+            finish_norm_kernel<<<1, 1024, 0, st>>>(nb_n, sqp.p, scal.p, 0);
+            SC_LAUNCHED(1);
+            SC_CUDA(cudaMemcpyAsync(ab, scal.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+            SC_CUDA(cudaStreamSynchronize(st));
+        }
         const double beta = ab[0], alpha = ab[2];
         scale = std::max(scale, std::max(std::fabs(alpha), beta));
         if (j + 1 == m) return finish_sweep(beta);
@@ -680,6 +705,7 @@ int sc_lanczos_get_stats(const sc_lanczos_t* s, sc_lanczos_stats* st) {
     st->breakdowns = s->breakdowns;
     st->matvecs = s->matvecs;
     st->n_history = (int64_t)std::min<size_t>(s->history.size(), 512);
+    st->second_passes = s->second_passes;
     for (int64_t i = 0; i < st->n_history; ++i) st->history[i] = s->history[i];
     return SC_OK;
 }
@@ -803,7 +829,7 @@ int sc_gemv_t_f64(int64_t n, int64_t ld, int64_t ncols, const double* B, const d
     const int64_t nb = ceil_div(n, GT_ROWS);
     DevBuf<double> part;
     if (int rc = part.alloc((size_t)nb * ncols)) return rc;
-    gemv_t_partial_kernel<<<(unsigned)nb, 256, 0, st>>>(n, ld, (int)ncols, B, w, part.p);
+    gemv_t_partial_kernel<<<(unsigned)nb, 256, 0, st>>>(n, ld, (int)ncols, B, w, part.p, nullptr);
     reduce_cols_kernel<<<(unsigned)ceil_div(ncols * 32, 256), 256, 0, st>>>(nb, (int)ncols, part.p, h);
     SC_LAUNCHED(2);
     return SC_OK;

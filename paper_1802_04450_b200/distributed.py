@@ -44,6 +44,10 @@ from .sparse import DeviceCsr
 __all__ = ["Comm", "row_bounds", "CudaOps", "lanczos_sharded", "kmeanspp_sharded", "lloyd_sharded", "run_sharded"]
 
 BREAKDOWN_RTOL = 1e-13  # eigen.py:50
+REORTH_ETA = 0.05  # second CGS pass threshold (sc_lanczos.cu kReorthEta)
+
+# diagnostics of the last run_sharded call (global nnz, eigen statistics)
+last_info: dict = {}
 
 
 def row_bounds(n: int, world: int) -> list[int]:
@@ -389,18 +393,26 @@ def lanczos_sharded(ops, comm: Comm, a_local, n: int, bounds, cfg: LanczosConfig
     scale = 0.0
     pending = None
     j = 0
+    st["second_passes"] = 0
     while True:
         x_full = comm.gather_rows(B[j, :nl].contiguous(), bounds)
         w = ops.spmv(a_local, x_full)
         st["matvecs"] += 1
         cnt = j + 1
+        # one full CGS pass (subsumes the three-term recurrence, eigen.py:157-163)
+        # and a second only when the first cancelled most of |w| (DGKS; the
+        # same rule as the single-GPU session, sc_lanczos.cu advance())
+        w0 = norm_of(w)
         h = dot_all(ops.gemv_t(B, cnt, w))
         alpha = float(h[j].item())
         T[j, j] = alpha
-        ops.gemv_n(B, cnt, h, w)
-        h = dot_all(ops.gemv_t(B, cnt, w))
         sq = ops.gemv_n(B, cnt, h, w, want_sq=True)
         beta = math.sqrt(float(comm.sum_(sq)[0].item()))
+        if beta < REORTH_ETA * w0:
+            st["second_passes"] += 1
+            h = dot_all(ops.gemv_t(B, cnt, w))
+            sq = ops.gemv_n(B, cnt, h, w, want_sq=True)
+            beta = math.sqrt(float(comm.sum_(sq)[0].item()))
         scale = max(scale, abs(alpha), beta)
         if j + 1 < m:
             if beta > BREAKDOWN_RTOL * max(1.0, scale):
@@ -635,7 +647,7 @@ def run_sharded(cfg, comm: Comm, ops=None):
     ecfg = cfg.eigen if cfg.eigen is not None else LanczosConfig(k=cfg.k_clusters)
     a_loc = ops.sym_scale_shard(w_loc, r0, d_full)
     try:
-        values, U, residuals, _ = lanczos_sharded(ops, comm, a_loc, n, bounds, ecfg)
+        values, U, residuals, est = lanczos_sharded(ops, comm, a_loc, n, bounds, ecfg)
     except MaxRestartsExceeded as e:
         raise EigenNotConverged(e) from e
     V, colsq = ops.embed_scale(U, d_loc)
@@ -668,6 +680,9 @@ def run_sharded(cfg, comm: Comm, ops=None):
     timings["metrics"] = time.perf_counter() - t
 
     lab = Labeling(labels, ops.host(C), float(hist[-1]), iters, hist)
+    last_info.clear()
+    last_info["nnz"] = int(comm.gather_scalars([w_loc.nnz])[:, 0].sum())
+    last_info["eigen"] = dict(est, world=comm.world)
     rep = ClusterReport(labeling=lab, eigenvalues=nat.frozen(values), eigen_residuals=nat.frozen(residuals),
                         ncut_value=ncut_value, timings=timings, warnings=warnings,
                         index_map=np.arange(n, dtype=np.int64))
