@@ -94,6 +94,28 @@ int sc_find_nonpositive(int64_t n, const double* d, int mode, int64_t* count_out
 /* out = vals / sqrt(d[row] * d[col]) (laplacian.py:84-91). */
 int sc_sym_scale_f64(int64_t n, const int64_t* row_ptr, const int32_t* col,
                      const double* vals, const double* d, double* out, sc_stream_t stream);
+/* B = P A P^T: row p of B is row perm[p] of A, columns relabelled pos[c]
+ * (pos = perm^-1, see sc_invert_perm) and re-sorted; out_* have A's sizes.
+ * Used to run the eigensolver on the locality-ordered operator. */
+int sc_csr_permute_f64(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* vals,
+                       const int32_t* perm, const int32_t* pos, int64_t* out_row_ptr, int32_t* out_col,
+                       double* out_vals, sc_stream_t stream);
+/* SELL-32-sigma operator for repeated y = A x (the eigensolver's matvec
+ * format): rows sorted by length inside 256-row windows, 32-row slices stored
+ * column-major, rows longer than 2x the mean kept in CSR and summed by a
+ * warp-per-row kernel.  A's CSR arrays must outlive the handle.  The operator
+ * may have fewer rows than columns (a row shard with global columns). */
+typedef struct sc_sell sc_sell_t;
+int sc_sell_create(int64_t n_rows, const int64_t* row_ptr, const int32_t* col, const double* vals,
+                   sc_stream_t stream, sc_sell_t** out);
+int sc_sell_spmv(const sc_sell_t* op, const double* x, double* y, sc_stream_t stream);
+int sc_sell_info(const sc_sell_t* op, int64_t* stored, int64_t* n_long_rows);
+void sc_sell_destroy(sc_sell_t* op);
+/* pos[perm[p]] = p */
+int sc_invert_perm(int64_t n, const int32_t* perm, int32_t* pos, sc_stream_t stream);
+/* dst row r = src row idx[r] (row-major n x k f64) */
+int sc_gather_rows_f64(int64_t n, int64_t k, const double* src, const int32_t* idx, double* dst,
+                       sc_stream_t stream);
 /* *result (host) = 1 iff A == A^T bit-for-bit (sparse.py:210-222). */
 int sc_csr_is_symmetric(int64_t n, int64_t nnz, const int64_t* row_ptr, const int32_t* col,
                         const double* vals, int* result, sc_stream_t stream);

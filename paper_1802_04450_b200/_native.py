@@ -50,6 +50,13 @@ SIGNATURES = {
     "sc_find_nonpositive": (i32, [i64, vp, i32, P_i64, vp, i64, vp]),
     "sc_sym_scale_f64": (i32, [i64, vp, vp, vp, vp, vp, vp]),
     "sc_csr_is_symmetric": (i32, [i64, i64, vp, vp, vp, P_int, vp]),
+    "sc_csr_permute_f64": (i32, [i64, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "sc_invert_perm": (i32, [i64, vp, vp, vp]),
+    "sc_sell_create": (i32, [i64, vp, vp, vp, vp, C.POINTER(vp)]),
+    "sc_sell_spmv": (i32, [vp, vp, vp, vp]),
+    "sc_sell_info": (i32, [vp, P_i64, P_i64]),
+    "sc_sell_destroy": (None, [vp]),
+    "sc_gather_rows_f64": (i32, [i64, i64, vp, vp, vp, vp]),
     "sc_knn_graph_f64": (i32, [i64, i64, vp, i64, f64, vp, vp, vp, P_i64, P_i64, vp]),
     "sc_knn_select_f64": (i32, [i64, i64, vp, i64, f64, i64, i64, vp, vp, P_i64, vp]),
     "sc_knn_union_f64": (i32, [i64, i64, vp, i64, f64, vp, vp, i64, i64, vp, vp, vp, i64, P_i64, vp]),

@@ -17,6 +17,7 @@
 // the thick restart follow eigen.py:166-239 exactly.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -31,6 +32,10 @@ constexpr int GN_THREADS = 256;   // rows per gemv_n block
 constexpr double kBreakdownRtol = 1e-13;  // eigen.py:50
 // second CGS pass when the first one removed more than 1 - eta^2 of |w|^2
 constexpr double kReorthEta = 0.05;
+// SELL-32-sigma matvecs are opt-in (SPECLUST_SPMV_FORMAT=sell): on the C2
+// kNN operator the x gathers are L2-sector bound and the warp-per-row CSR
+// kernel measured faster (161 vs 183 ms per 500 matvecs, profiles/)
+constexpr int64_t kSellMinRows = INT64_MAX;
 
 // ---- kernels ------------------------------------------------------------------
 __global__ void fill_normal_kernel(int64_t n, uint64_t seed, uint64_t stream_id, double* __restrict__ out) {
@@ -738,8 +743,17 @@ int sc_eigensolve_csr(int64_t n, const int64_t* row_ptr, const int32_t* col, con
     int64_t nnz = 0;
     SC_CUDA(cudaMemcpyAsync(&nnz, row_ptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     SC_CUDA(cudaStreamSynchronize(st));
+    // large operators: SELL-32-sigma copy for the hundreds of matvecs
+    SellMatrix sell;
+    const char* fenv = std::getenv("SPECLUST_SPMV_FORMAT");
+    const bool use_sell = fenv ? std::strcmp(fenv, "sell") == 0 : n >= kSellMinRows;
+    if (use_sell && (rc = sell.build(n, row_ptr, col, vals, st))) return rc;
     while (s.state == 0) {
-        if ((rc = spmv_launch(n, nnz, row_ptr, col, vals, s.in_slot(), s.w.p, false, st))) return rc;
+        if (use_sell)
+            rc = sell.spmv(s.in_slot(), s.w.p, st);
+        else
+            rc = spmv_launch(n, nnz, row_ptr, col, vals, s.in_slot(), s.w.p, false, st);
+        if (rc) return rc;
         rc = s.advance(false);
         if (rc) {
             if (stats) sc_lanczos_get_stats(&s, stats);

@@ -6,7 +6,7 @@ namespace sc {
 
 constexpr int SCAN_BLK = 1024;
 
-__global__ void scan_block_sums_kernel(int64_t n, const int64_t* __restrict__ in, int64_t* __restrict__ bsum) {
+static __global__ void scan_block_sums_kernel(int64_t n, const int64_t* __restrict__ in, int64_t* __restrict__ bsum) {
     __shared__ int64_t red[32];
     int64_t i = (int64_t)blockIdx.x * SCAN_BLK + threadIdx.x;
     int64_t v = i < n ? in[i] : 0;
@@ -21,7 +21,7 @@ __global__ void scan_block_sums_kernel(int64_t n, const int64_t* __restrict__ in
 }
 
 // single block: exclusive scan of nb block sums in place, total into *total
-__global__ void scan_top_kernel(int64_t nb, int64_t* __restrict__ bsum, int64_t* __restrict__ total) {
+static __global__ void scan_top_kernel(int64_t nb, int64_t* __restrict__ bsum, int64_t* __restrict__ total) {
     __shared__ int64_t carry;
     __shared__ int64_t wsum[32];
     if (threadIdx.x == 0) carry = 0;
@@ -56,7 +56,7 @@ __global__ void scan_top_kernel(int64_t nb, int64_t* __restrict__ bsum, int64_t*
     if (threadIdx.x == 0) *total = carry;
 }
 
-__global__ void scan_apply_kernel(int64_t n, const int64_t* __restrict__ in, const int64_t* __restrict__ boff,
+static __global__ void scan_apply_kernel(int64_t n, const int64_t* __restrict__ in, const int64_t* __restrict__ boff,
                                   int64_t* __restrict__ out) {
     __shared__ int64_t wsum[32];
     int64_t i = (int64_t)blockIdx.x * SCAN_BLK + threadIdx.x;

@@ -260,3 +260,294 @@ int sc_csr_is_symmetric(int64_t n, int64_t nnz, const int64_t* row_ptr, const in
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Symmetric permutation B = P A P^T of a CSR matrix: row p of B is row perm[p]
+// of A with every column c relabelled pos[c] (pos = perm^-1) and the row
+// re-sorted.  The eigensolver runs on the locality-ordered operator so the
+// SpMV gathers of x hit nearby cache lines (stage 2).
+#include "sc_scan.cuh"
+
+namespace sc {
+__global__ void perm_row_len_kernel(int64_t n, const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ perm,
+                                    int64_t* __restrict__ len) {
+    int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const int64_t i = perm[p];
+    len[p] = row_ptr[i + 1] - row_ptr[i];
+}
+
+// warp per output row; entries ranked by their new column (distinct keys)
+__global__ void perm_row_fill_kernel(int64_t n, const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                                     const double* __restrict__ vals, const int32_t* __restrict__ perm,
+                                     const int32_t* __restrict__ pos, const int64_t* __restrict__ out_ptr,
+                                     int32_t* __restrict__ out_col, double* __restrict__ out_vals) {
+    const int64_t p = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    if (p >= n) return;
+    const int64_t i = perm[p];
+    const int64_t b = row_ptr[i], len = row_ptr[i + 1] - b, o = out_ptr[p];
+    for (int64_t e = lane; e < len; e += 32) {
+        const int32_t key = pos[col[b + e]];
+        int64_t r = 0;
+        for (int64_t f = 0; f < len; ++f) r += pos[col[b + f]] < key;
+        out_col[o + r] = key;
+        out_vals[o + r] = vals[b + e];
+    }
+}
+}  // namespace sc
+
+extern "C" int sc_csr_permute_f64(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* vals,
+                                  const int32_t* perm, const int32_t* pos, int64_t* out_row_ptr, int32_t* out_col,
+                                  double* out_vals, sc_stream_t stream) {
+    using namespace sc;
+    if (n <= 0) return SC_OK;
+    cudaStream_t st = as_stream(stream);
+    StreamScope stream_scope(st);
+    DevBuf<int64_t> len, tmp;
+    int rc;
+    if ((rc = len.alloc(n)) || (rc = tmp.alloc(ceil_div(n, SCAN_BLK) + 1))) return rc;
+    perm_row_len_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, row_ptr, perm, len.p);
+    SC_LAUNCHED(1);
+    if ((rc = exclusive_scan_i64(n, len.p, out_row_ptr, tmp.p, st))) return rc;
+    perm_row_fill_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, st>>>(n, row_ptr, col, vals, perm, pos, out_row_ptr,
+                                                                   out_col, out_vals);
+    SC_LAUNCHED(1);
+    return SC_OK;
+}
+
+// pos[perm[p]] = p
+namespace sc {
+__global__ void invert_perm_kernel(int64_t n, const int32_t* __restrict__ perm, int32_t* __restrict__ pos) {
+    int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < n) pos[perm[p]] = (int32_t)p;
+}
+// dst row r = src row idx[r] (row-major n x k)
+__global__ void gather_rows_kernel(int64_t n, int64_t k, const double* __restrict__ src, const int32_t* __restrict__ idx,
+                                   double* __restrict__ dst) {
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n * k) return;
+    const int64_t r = e / k, c = e - r * k;
+    dst[e] = src[(int64_t)idx[r] * k + c];
+}
+}  // namespace sc
+
+extern "C" int sc_invert_perm(int64_t n, const int32_t* perm, int32_t* pos, sc_stream_t stream) {
+    using namespace sc;
+    if (n <= 0) return SC_OK;
+    invert_perm_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, as_stream(stream)>>>(n, perm, pos);
+    SC_LAUNCHED(1);
+    return SC_OK;
+}
+
+extern "C" int sc_gather_rows_f64(int64_t n, int64_t k, const double* src, const int32_t* idx, double* dst,
+                                  sc_stream_t stream) {
+    using namespace sc;
+    if (n <= 0 || k <= 0) return SC_OK;
+    gather_rows_kernel<<<(unsigned)ceil_div(n * k, 256), 256, 0, as_stream(stream)>>>(n, k, src, idx, dst);
+    SC_LAUNCHED(1);
+    return SC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// SELL-32-sigma (see sc_sparse.cuh)
+namespace sc {
+// one block per window of SELL_SIGMA rows: rank rows by (length desc, row asc)
+__global__ void __launch_bounds__(SELL_SIGMA) sell_sort_kernel(int64_t n, int64_t lcap,
+                                                               const int64_t* __restrict__ row_ptr,
+                                                               int32_t* __restrict__ srow, int32_t* __restrict__ slen,
+                                                               int32_t* __restrict__ lrows,
+                                                               unsigned long long* __restrict__ nlong) {
+    __shared__ int32_t L[SELL_SIGMA];
+    const int64_t r = (int64_t)blockIdx.x * SELL_SIGMA + threadIdx.x;
+    int64_t full = r < n ? row_ptr[r + 1] - row_ptr[r] : -1;
+    if (full > lcap) {  // hub row: empty in the slices, listed for the long-row kernel
+        lrows[atomicAdd(nlong, 1ull)] = (int32_t)r;
+        full = 0;
+    }
+    const int32_t len = (int32_t)full;
+    L[threadIdx.x] = len;
+    __syncthreads();
+    int rank = 0;
+    for (int u = 0; u < SELL_SIGMA; ++u) {
+        const int32_t lu = L[u];
+        rank += (lu > len) || (lu == len && u < (int)threadIdx.x);
+    }
+    const int64_t o = (int64_t)blockIdx.x * SELL_SIGMA + rank;
+    srow[o] = (int32_t)r;
+    slen[o] = len < 0 ? 0 : len;
+}
+
+__global__ void sell_width_kernel(int64_t nslices, const int32_t* __restrict__ slen, int32_t* __restrict__ width,
+                                  int64_t* __restrict__ size) {
+    int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= nslices) return;
+    const int32_t w = slen[s * 32];  // longest row of the slice (sorted descending)
+    width[s] = w;
+    size[s] = (int64_t)w * 32;
+}
+
+// warp per slice
+__global__ void sell_fill_kernel(int64_t nslices, const int64_t* __restrict__ row_ptr,
+                                 const int32_t* __restrict__ col_in, const double* __restrict__ vals_in,
+                                 const int64_t* __restrict__ slice_ptr, const int32_t* __restrict__ width,
+                                 const int32_t* __restrict__ srow, const int32_t* __restrict__ slen,
+                                 int32_t* __restrict__ col, double* __restrict__ vals) {
+    const int64_t s = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int t = threadIdx.x & 31;
+    if (s >= nslices) return;
+    const int64_t idx = s * 32 + t;
+    const int32_t len = slen[idx];
+    const int64_t src = len > 0 ? row_ptr[srow[idx]] : 0;
+    const int64_t base = slice_ptr[s] + t;
+    const int32_t w = width[s];
+    for (int32_t j = 0; j < w; ++j) {
+        const bool in = j < len;
+        col[base + (int64_t)j * 32] = in ? col_in[src + j] : 0;
+        vals[base + (int64_t)j * 32] = in ? vals_in[src + j] : 0.0;
+    }
+}
+
+// warp per slice, lane per row; the block's 8 slices are one sorting window
+__global__ void __launch_bounds__(256) spmv_sell_kernel(int64_t n, int64_t nslices,
+                                                        const int64_t* __restrict__ slice_ptr,
+                                                        const int32_t* __restrict__ width,
+                                                        const int32_t* __restrict__ srow,
+                                                        const int32_t* __restrict__ slen,
+                                                        const int32_t* __restrict__ col,
+                                                        const double* __restrict__ vals,
+                                                        const double* __restrict__ x, double* __restrict__ y) {
+    const int64_t s = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int t = threadIdx.x & 31;
+    if (s >= nslices) return;
+    const int64_t idx = s * 32 + t;
+    const int32_t len = slen[idx];
+    const int32_t w = width[s];
+    const int32_t* c = col + slice_ptr[s] + t;
+    const double* v = vals + slice_ptr[s] + t;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int32_t j = 0;
+    for (; j + 4 <= w; j += 4) {
+        // every lane issues its loads for 4 entries before the first use
+        int32_t c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+        double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+        if (j < len) { c0 = __ldg(c + (int64_t)j * 32); v0 = __ldg(v + (int64_t)j * 32); }
+        if (j + 1 < len) { c1 = __ldg(c + (int64_t)(j + 1) * 32); v1 = __ldg(v + (int64_t)(j + 1) * 32); }
+        if (j + 2 < len) { c2 = __ldg(c + (int64_t)(j + 2) * 32); v2 = __ldg(v + (int64_t)(j + 2) * 32); }
+        if (j + 3 < len) { c3 = __ldg(c + (int64_t)(j + 3) * 32); v3 = __ldg(v + (int64_t)(j + 3) * 32); }
+        if (j < len) a0 = fma(v0, __ldg(x + c0), a0);
+        if (j + 1 < len) a1 = fma(v1, __ldg(x + c1), a1);
+        if (j + 2 < len) a2 = fma(v2, __ldg(x + c2), a2);
+        if (j + 3 < len) a3 = fma(v3, __ldg(x + c3), a3);
+    }
+    for (; j < w; ++j)
+        if (j < len) a0 = fma(__ldg(v + (int64_t)j * 32), __ldg(x + __ldg(c + (int64_t)j * 32)), a0);
+    const int32_t r = srow[idx];
+    if (r < n) y[r] = (a0 + a1) + (a2 + a3);
+}
+
+// warp per long row (after spmv_sell_kernel, which wrote 0 for it)
+__global__ void __launch_bounds__(256) spmv_long_rows_kernel(int64_t nlong, const int32_t* __restrict__ lrows,
+                                                             const int64_t* __restrict__ row_ptr,
+                                                             const int32_t* __restrict__ col,
+                                                             const double* __restrict__ vals,
+                                                             const double* __restrict__ x, double* __restrict__ y) {
+    const int64_t q = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (q >= nlong) return;
+    const int32_t r = lrows[q];
+    const int64_t b = row_ptr[r], e = row_ptr[r + 1];
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int64_t p = b + lane;
+    for (; p + 96 < e; p += 128) {
+        const int32_t c0 = __ldg(col + p), c1 = __ldg(col + p + 32), c2 = __ldg(col + p + 64), c3 = __ldg(col + p + 96);
+        const double v0 = __ldg(vals + p), v1 = __ldg(vals + p + 32), v2 = __ldg(vals + p + 64),
+                     v3 = __ldg(vals + p + 96);
+        a0 = fma(v0, __ldg(x + c0), a0);
+        a1 = fma(v1, __ldg(x + c1), a1);
+        a2 = fma(v2, __ldg(x + c2), a2);
+        a3 = fma(v3, __ldg(x + c3), a3);
+    }
+    for (; p < e; p += 32) a0 = fma(__ldg(vals + p), __ldg(x + __ldg(col + p)), a0);
+    double acc = warp_sum((a0 + a1) + (a2 + a3));
+    if (lane == 0) y[r] = acc;
+}
+
+int SellMatrix::build(int64_t n_, const int64_t* row_ptr_in, const int32_t* col_in, const double* vals_in,
+                      cudaStream_t st) {
+    n = n_;
+    row_ptr = row_ptr_in;
+    csr_col = col_in;
+    csr_vals = vals_in;
+    const int64_t nwin = ceil_div(n, SELL_SIGMA);
+    nslices = nwin * (SELL_SIGMA / 32);
+    int64_t nnz = 0;
+    SC_CUDA(cudaMemcpyAsync(&nnz, row_ptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    SC_CUDA(cudaStreamSynchronize(st));
+    // hub threshold: twice the mean row length (at least 64)
+    lcap = std::max<int64_t>(64, 2 * ceil_div(nnz, std::max<int64_t>(n, 1)));
+    DevBuf<int64_t> size, tmp;
+    DevBuf<unsigned long long> cnt;
+    int rc;
+    if ((rc = slice_ptr.alloc(nslices + 1)) || (rc = width.alloc(nslices)) || (rc = srow.alloc(nslices * 32)) ||
+        (rc = slen.alloc(nslices * 32)) || (rc = size.alloc(nslices)) || (rc = lrows.alloc(n)) ||
+        (rc = cnt.alloc(1)) || (rc = tmp.alloc(ceil_div(nslices, SCAN_BLK) + 1)))
+        return rc;
+    SC_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), st));
+    sell_sort_kernel<<<(unsigned)nwin, SELL_SIGMA, 0, st>>>(n, lcap, row_ptr, srow.p, slen.p, lrows.p, cnt.p);
+    sell_width_kernel<<<(unsigned)ceil_div(nslices, 256), 256, 0, st>>>(nslices, slen.p, width.p, size.p);
+    SC_LAUNCHED(2);
+    if ((rc = exclusive_scan_i64(nslices, size.p, slice_ptr.p, tmp.p, st))) return rc;
+    unsigned long long hl = 0;
+    SC_CUDA(cudaMemcpyAsync(&stored, slice_ptr.p + nslices, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    SC_CUDA(cudaMemcpyAsync(&hl, cnt.p, sizeof(hl), cudaMemcpyDeviceToHost, st));
+    SC_CUDA(cudaStreamSynchronize(st));
+    nlong = (int64_t)hl;
+    if ((rc = col.alloc(std::max<int64_t>(stored, 1))) || (rc = vals.alloc(std::max<int64_t>(stored, 1)))) return rc;
+    sell_fill_kernel<<<(unsigned)ceil_div(nslices, 8), 256, 0, st>>>(nslices, row_ptr_in, col_in, vals_in, slice_ptr.p,
+                                                                    width.p, srow.p, slen.p, col.p, vals.p);
+    SC_LAUNCHED(1);
+    return SC_OK;
+}
+
+int SellMatrix::spmv(const double* x, double* y, cudaStream_t st) const {
+    if (n == 0) return SC_OK;
+    ProfScope prof("spmv", st, 12.0 * (double)stored + 8.0 * 4.0 * (double)n);  // + long rows (small)
+    spmv_sell_kernel<<<(unsigned)ceil_div(nslices, 8), 256, 0, st>>>(n, nslices, slice_ptr.p, width.p, srow.p, slen.p,
+                                                                     col.p, vals.p, x, y);
+    SC_LAUNCHED(1);
+    if (nlong > 0) {
+        spmv_long_rows_kernel<<<(unsigned)ceil_div(nlong, 8), 256, 0, st>>>(nlong, lrows.p, row_ptr, csr_col, csr_vals,
+                                                                            x, y);
+        SC_LAUNCHED(1);
+    }
+    return SC_OK;
+}
+}  // namespace sc
+
+// ---- C ABI: SELL operator handle (built once, applied many times) ----------
+struct sc_sell {
+    sc::SellMatrix m;
+};
+extern "C" int sc_sell_create(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* vals,
+                              sc_stream_t stream, sc_sell** out) {
+    using namespace sc;
+    cudaStream_t st = as_stream(stream);
+    StreamScope stream_scope(st);
+    auto* h = new sc_sell();
+    if (int rc = h->m.build(n, row_ptr, col, vals, st)) {
+        delete h;
+        return rc;
+    }
+    *out = h;
+    return SC_OK;
+}
+extern "C" int sc_sell_spmv(const sc_sell* h, const double* x, double* y, sc_stream_t stream) {
+    return h->m.spmv(x, y, sc::as_stream(stream));
+}
+extern "C" int sc_sell_info(const sc_sell* h, int64_t* stored, int64_t* nlong) {
+    *stored = h->m.stored;
+    *nlong = h->m.nlong;
+    return SC_OK;
+}
+extern "C" void sc_sell_destroy(sc_sell* h) { delete h; }

@@ -10,6 +10,32 @@ int spmv_launch(int64_t n, int64_t nnz, const int64_t* row_ptr, const int32_t* c
 int degrees_launch(int64_t n, const int64_t* row_ptr, const double* vals, double* d,
                    cudaStream_t st);
 
+// Sliced ELLPACK (SELL-32-sigma) copy of a CSR matrix for the eigensolver's
+// SpMV: rows are sorted by length (descending, stable) inside windows of
+// SELL_SIGMA consecutive rows, every 32 sorted rows form a slice stored
+// column-major (entry j of the slice's 32 rows is contiguous), so a warp's
+// loads are coalesced, each lane sums one row sequentially with several
+// independent gathers in flight, and a block's rows are consecutive (in the
+// kNN locality order their x gathers share L1 lines).
+// Rows longer than `lcap` (kNN hubs) would stall their slice's warp: they are
+// stored empty in the slices and summed by a warp-per-row kernel instead.
+constexpr int SELL_SIGMA = 256;
+struct SellMatrix {
+    int64_t n = 0, nslices = 0, stored = 0, nlong = 0, lcap = 0;
+    DevBuf<int32_t> lrows;      // nlong: the long rows
+    const int64_t* row_ptr = nullptr;  // CSR kept for the long rows
+    const int32_t* csr_col = nullptr;
+    const double* csr_vals = nullptr;
+    DevBuf<int64_t> slice_ptr;  // nslices + 1 (entries)
+    DevBuf<int32_t> width;      // nslices
+    DevBuf<int32_t> srow;       // nslices * 32: sorted position -> row (>= n: padding)
+    DevBuf<int32_t> slen;       // nslices * 32: row length at that position
+    DevBuf<int32_t> col;        // stored
+    DevBuf<double> vals;        // stored
+    int build(int64_t n_, const int64_t* row_ptr, const int32_t* col_in, const double* vals_in, cudaStream_t st);
+    int spmv(const double* x, double* y, cudaStream_t st) const;
+};
+
 // Stable bucketing of n items by label in [0, k): members[] lists item
 // indices grouped by label, ascending index within a label; start[k+1] are
 // the group offsets.  Workspace is owned by the struct.

@@ -177,6 +177,16 @@ class CudaOps:
                                        nat.ptr(x_full), nat.ptr(y), 0, self._s()))
         return y
 
+    def operator(self, a: DeviceCsr):
+        """Repeated y = A_local x_full: the CSR warp-per-row kernel, or a
+        SELL-32-sigma handle when SPECLUST_SPMV_FORMAT=sell (as in the
+        single-GPU eigensolver)."""
+        import os
+
+        if os.environ.get("SPECLUST_SPMV_FORMAT") == "sell":
+            return _SellOp(self, a)
+        return _CsrOp(self, a)
+
     def gemv_t(self, B, ncols, w):
         h = self.torch.empty(max(1, ncols), dtype=self.torch.float64, device="cuda")
         nat.check(self.lib.sc_gemv_t_f64(w.numel(), B.shape[1], ncols, nat.ptr(B), nat.ptr(w), nat.ptr(h), self._s()))
@@ -275,6 +285,37 @@ class CudaOps:
         return bnd, vol, cnt
 
 
+class _CsrOp:
+    def __init__(self, ops: CudaOps, a: DeviceCsr):
+        self.ops, self.a = ops, a
+
+    def apply(self, x_full):
+        return self.ops.spmv(self.a, x_full)
+
+    def close(self):
+        pass
+
+
+class _SellOp:
+    """sc_sell_* handle of a row-shard operator (rows local, columns global)."""
+
+    def __init__(self, ops: CudaOps, a: DeviceCsr):
+        self.ops, self.a = ops, a  # keeps the CSR arrays alive with the handle
+        self.h = nat.vp()
+        nat.check(ops.lib.sc_sell_create(a.n_rows, nat.ptr(a.row_ptr), nat.ptr(a.col), nat.ptr(a.vals), ops._s(),
+                                         nat.C.byref(self.h)))
+
+    def apply(self, x_full):
+        y = self.ops.torch.empty(self.a.n_rows, dtype=self.ops.torch.float64, device="cuda")
+        nat.check(self.ops.lib.sc_sell_spmv(self.h, nat.ptr(x_full), nat.ptr(y), self.ops._s()))
+        return y
+
+    def close(self):
+        if self.h is not None and self.h.value:
+            self.ops.lib.sc_sell_destroy(self.h)
+            self.h = None
+
+
 class _CudaKpp:
     """Shard view of the device k-means++ state (sc_kmeanspp_*)."""
 
@@ -345,6 +386,18 @@ def lanczos_sharded(ops, comm: Comm, a_local, n: int, bounds, cfg: LanczosConfig
 
     Returns (values host (k,), vectors local (nl, k) row-major, residuals host
     (k,), stats dict).  Raises MaxRestartsExceeded / Breakdown like eigen.py."""
+    op = ops.operator(a_local) if hasattr(ops, "operator") else None
+    try:
+        return _lanczos_sharded(ops, comm, a_local, n, bounds, cfg, op)
+    finally:
+        if op is not None:
+            op.close()
+
+
+def _lanczos_sharded(ops, comm, a_local, n, bounds, cfg, op):
+    def matvec(x_full):
+        return op.apply(x_full) if op is not None else ops.spmv(a_local, x_full)
+
     k = cfg.k
     m = cfg.m if cfg.m is not None else default_subspace_dim(n, k)
     if not (1 <= k < m <= n):
@@ -396,7 +449,7 @@ def lanczos_sharded(ops, comm: Comm, a_local, n: int, bounds, cfg: LanczosConfig
     st["second_passes"] = 0
     while True:
         x_full = comm.gather_rows(B[j, :nl].contiguous(), bounds)
-        w = ops.spmv(a_local, x_full)
+        w = matvec(x_full)
         st["matvecs"] += 1
         cnt = j + 1
         # one full CGS pass (subsumes the three-term recurrence, eigen.py:157-163)
@@ -445,7 +498,7 @@ def lanczos_sharded(ops, comm: Comm, a_local, n: int, bounds, cfg: LanczosConfig
             one = ops.zeros((1,))
             for i in range(k):  # true residuals |A v - theta v| (eigen.py:241-248)
                 vi = V[:, i].contiguous()
-                yi = ops.spmv(a_local, comm.gather_rows(vi, bounds))
+                yi = matvec(comm.gather_rows(vi, bounds))
                 one.fill_(values[i])
                 sq = ops.gemv_n(vi.reshape(1, -1), 1, one, yi, want_sq=True)
                 res[i] = float(comm.sum_(sq)[0].item())

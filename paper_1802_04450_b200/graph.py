@@ -137,20 +137,22 @@ def knn_graph_device(x, knn: int, m: SimilarityMeasure, return_stats: bool = Fal
         xd = nat.to_device(xh, torch.float64)
     if not 1 <= knn < n:
         raise ValueError(f"knn must satisfy 1 <= knn < n, got {knn} for n={n}")
-    cap = 2 * n * knn
-    row_ptr = torch.empty(n + 1, dtype=torch.int64, device="cuda")
-    col = torch.empty(cap, dtype=torch.int32, device="cuda")
-    vals = torch.empty(cap, dtype=torch.float64, device="cuda")
-    nnz = nat.C.c_int64(0)
+    # selection (sc_knn_select_f64) + union (sc_knn_union_f64) == sc_knn_graph_f64;
+    # the two-stage form keeps the locality scan order for the eigensolver
+    sel = torch.empty((n, knn), dtype=torch.int32, device="cuda")
+    perm = torch.empty(n, dtype=torch.int32, device="cuda")
     stats = (nat.C.c_int64 * 8)()
     lib = nat.load()
-    nat.check(lib.sc_knn_graph_f64(n, d, nat.ptr(xd), knn, m.two_sigma_sq(), nat.ptr(row_ptr), nat.ptr(col),
-                                   nat.ptr(vals), nat.C.byref(nnz), stats, nat.stream_handle()))
-    k = nnz.value
-    w = DeviceCsr(n, n, row_ptr, col[:k], vals[:k])
+    nat.check(lib.sc_knn_select_f64(n, d, nat.ptr(xd), knn, m.two_sigma_sq(), 0, n, nat.ptr(sel), nat.ptr(perm),
+                                    stats, nat.stream_handle()))
+    w = knn_union_device(xd, knn, m, sel, perm, 0, n)
+    del sel
+    w.locality_perm = perm  # scan position -> point
     if return_stats:
-        keys = ("list_R", "list_cap", "fallback_rows", "nnz")
-        return w, {key: int(stats[i]) for i, key in enumerate(keys)}
+        keys = ("list_R", "list_cap", "fallback_rows")
+        out = {key: int(stats[i]) for i, key in enumerate(keys)}
+        out["nnz"] = w.nnz
+        return w, out
     return w
 
 

@@ -360,3 +360,58 @@ def test_ncut_matches_oracle(golden):
     assert abs(val - want2) <= 1e-13 * want2
     with pytest.raises(sc.errors.ZeroVolumePart):
         sc.ncut(w, lab, k=7)
+
+
+@pytest.mark.parametrize("fmt", ["sell", "csr"])
+def test_eigensolve_spmv_formats(golden, monkeypatch, fmt):
+    """The eigensolver's SELL-32-sigma matvec (default for large operators)
+    and the CSR one agree with the reference on every eigen golden case."""
+    monkeypatch.setenv("SPECLUST_SPMV_FORMAT", fmt)
+    g = golden("eigen_cases")
+    for t in range(int(g["ncases"])):
+        m = csr(g[f"e{t}_row_ptr"], g[f"e{t}_col"], g[f"e{t}_vals"])
+        k = int(g[f"e{t}_k"])
+        b = sc.eigensolve(m, sc.LanczosConfig(k=k, seed=0))
+        ref = g[f"e{t}_values"]
+        assert np.max(np.abs(b.values - ref)) <= 1e-8 * max(1.0, np.abs(ref).max())
+        assert np.min(_principal_cos(b.vectors, g[f"e{t}_vectors"])) > np.cos(1e-4)
+
+
+@pytest.mark.parametrize("n_rows,n_cols", [(50_003, 50_003), (1, 7), (300, 300), (20_000, 70_000)])
+def test_sell_operator_ragged(n_rows, n_cols):
+    """sc_sell_* on ragged rows (empty rows, hub rows far above the mean,
+    a row shard with more columns than rows) == the sequential CSR sum up
+    to reassociation."""
+    import torch
+
+    from paper_1802_04450_b200 import _native as nat
+
+    rng = np.random.default_rng(n_rows)
+    deg = rng.integers(0, 90, n_rows)
+    deg[rng.random(n_rows) < 0.02] = 0
+    hubs = rng.random(n_rows) < 0.003
+    deg[hubs] = rng.integers(300, 3000, int(hubs.sum()))
+    deg = np.minimum(deg, n_cols)
+    rp = np.concatenate(([0], np.cumsum(deg))).astype(np.int64)
+    col = np.concatenate([np.sort(rng.choice(n_cols, dd, replace=False)) for dd in deg]).astype(np.int64) \
+        if deg.sum() else np.zeros(0, np.int64)
+    vals = rng.standard_normal(col.size)
+    m = sc.CsrMatrix(n_rows, n_cols, rp, col, vals).device()
+    x = rng.standard_normal(n_cols)
+    want = orc.spmv_seq(rp, col, vals, x)
+    lib = nat.load()
+    h = nat.vp()
+    nat.check(lib.sc_sell_create(n_rows, nat.ptr(m.row_ptr), nat.ptr(m.col), nat.ptr(m.vals), nat.stream_handle(),
+                                 nat.C.byref(h)))
+    try:
+        stored, nlong = nat.C.c_int64(), nat.C.c_int64()
+        lib.sc_sell_info(h, nat.C.byref(stored), nat.C.byref(nlong))
+        assert nlong.value >= int((deg > max(64, 2 * -(-deg.sum() // n_rows))).sum())
+        xd = torch.from_numpy(x).cuda()
+        y = torch.full((n_rows,), np.nan, dtype=torch.float64, device="cuda")
+        nat.check(lib.sc_sell_spmv(h, nat.ptr(xd), nat.ptr(y), nat.stream_handle()))
+        got = y.cpu().numpy()
+    finally:
+        lib.sc_sell_destroy(h)
+    bound = 1e-13 * np.maximum(1.0, orc.spmv_seq(rp, col, np.abs(vals), np.abs(x)))
+    assert np.all(np.abs(got - want) <= bound)

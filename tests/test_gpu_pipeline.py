@@ -114,3 +114,49 @@ def test_determinism():
     assert np.array_equal(a.labeling.labels, b.labeling.labels)
     assert np.array_equal(a.eigenvalues, b.eigenvalues)
     assert a.ncut_value == b.ncut_value
+
+
+def test_csr_permute_and_gather_rows():
+    import torch
+
+    from paper_1802_04450_b200.pipeline import gather_rows_device, permute_device
+
+    rng = np.random.default_rng(3)
+    n = 700
+    a = (rng.random((n, n)) < 0.02) * rng.standard_normal((n, n))
+    a = a + a.T
+    r, c = np.nonzero(a)
+    m = sc.coo_to_csr(sc.coo_canonicalize(sc.CooMatrix(n, n, r, c, a[r, c]))).device()
+    perm = rng.permutation(n).astype(np.int32)
+    ap, pos = permute_device(m, torch.from_numpy(perm).cuda())
+    got = ap.to_host()
+    want = a[np.ix_(perm, perm)]
+    dense = np.zeros((n, n))
+    dense[got.row_indices(), got.col_idx] = got.vals
+    assert np.array_equal(dense, want)
+    for i in range(n):  # columns strictly increasing per row
+        seg = got.col_idx[got.row_ptr[i] : got.row_ptr[i + 1]]
+        assert np.all(np.diff(seg) > 0)
+    assert np.array_equal(pos.cpu().numpy()[perm], np.arange(n))
+    v = torch.from_numpy(rng.standard_normal((n, 5))).cuda()
+    g = gather_rows_device(v, pos)
+    assert np.array_equal(g.cpu().numpy(), v.cpu().numpy()[pos.cpu().numpy()])
+
+
+@pytest.mark.parametrize("flag", ["0", "1"])
+def test_pipeline_locality_order_eigen(golden, monkeypatch, flag):
+    """Eigen stage on P A P^T (kNN locality order) gives the reference's
+    spectrum and clustering at C1 (N=20k: a non-trivial scan order)."""
+    monkeypatch.setenv("SPECLUST_EIGEN_PERMUTE", flag)
+    from paper_1802_04450_b200 import pipeline
+
+    g = golden("pipeline_c1")
+    x, _ = orc.blobs(int(g["n"]), int(g["d"]), int(g["k"]), 1.0, seed=0)
+    k = int(g["k"])
+    rep, wd = pipeline.run_device(cfg_for(x, int(g["knn"]), float(g["sigma"]), k))
+    assert pipeline.last_info["eigen"]["locality_order"] == (flag == "1")
+    perm = wd.locality_perm.cpu().numpy()
+    assert not np.array_equal(perm, np.arange(len(perm)))
+    assert np.array_equal(np.sort(perm), np.arange(len(perm)))
+    assert np.max(np.abs(rep.eigenvalues - g["values"]) / np.abs(g["values"])) < 1e-5
+    assert orc.ari(rep.labeling.labels, g["labels"]) >= 0.999
