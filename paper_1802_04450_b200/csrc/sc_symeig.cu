@@ -1,7 +1,15 @@
 // Dense symmetric eigensolver for the Lanczos projected matrix (m x m),
-// entirely on device: Householder tridiagonalisation, explicit Q, implicit
-// QL with Wilkinson-type shifts (rotation chains computed by one thread and
-// applied to the rows of Q by the whole CTA), then a stable descending sort.
+// entirely on device:
+//   1. Householder tridiagonalisation (one CTA, matrix in global/L2);
+//   2. eigenvectors by row blocks: each of C CTAs owns RB rows of Z in shared
+//      memory, forms its rows of Q = H_0 ... H_{m-3} (row-local: z <- z H_k),
+//      then runs the implicit QL iteration with Wilkinson-type shifts on its
+//      own copy of (d, e) — every CTA computes the identical rotation chains,
+//      so no inter-CTA traffic — and applies each chain to its rows;
+//   3. a stable descending sort.
+// The row-block split keeps the rotation sweeps in shared memory (the
+// serial carry of a QL chain through global memory was the cost of the
+// single-CTA version: 13 ms per m=200 solve).
 //
 // Replaces np.linalg.eigh(proj) + argsort(-theta, kind="stable") in
 // eigen.py:189-192 (the reference's LAPACK dsyevd call on the host).
@@ -11,6 +19,7 @@
 namespace sc {
 
 constexpr int SE_THREADS = 1024;
+constexpr int SE_SMEM_MAX = 200 * 1024;
 
 __device__ __forceinline__ double block_sum(double v, double* red) {
     v = warp_sum(v);
@@ -28,23 +37,18 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
     return red[32];
 }
 
-// a: m x m column-major symmetric (destroyed); z: m x m output eigenvectors
-// (column j <-> eigenvalue w[j], unsorted); info: 0 ok, >0 QL failure.
-__global__ void __launch_bounds__(SE_THREADS, 1) symeig_kernel(int m, double* __restrict__ a,
-                                                                double* __restrict__ z,
-                                                                double* __restrict__ w, int* info) {
+// a: m x m column-major symmetric.  On exit reflector k (unit v, H = I - 2vv^T
+// acting on rows k+1..) is in a[k*m + k+1 ..] (all zero: no reflection), the
+// diagonal d_i in a[i*m + i] and the off-diagonal e_i in a[(i+1)*m + i].
+__global__ void __launch_bounds__(SE_THREADS, 1) symeig_tridiag_kernel(int m, double* __restrict__ a) {
     extern __shared__ double sm[];
-    double* d = sm;            // m
-    double* e = d + m;         // m
-    double* v = e + m;         // m (Householder vector / rotation cos)
-    double* q = v + m;         // m (p, q vectors / rotation sin)
-    double* red = q + m;       // 40
+    double* v = sm;      // m
+    double* q = v + m;   // m
+    double* red = q + m; // 40
     __shared__ double s_alpha, s_beta;
-    __shared__ int s_lo, s_hi, s_state;
     const int tid = threadIdx.x, nt = blockDim.x;
     const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
 
-    // ---- 1. tridiagonalisation; reflector k stored in a[k+1.., k]
     for (int k = 0; k + 2 < m; ++k) {
         const int len = m - k - 1;  // rows k+1 .. m-1
         double* col = a + (size_t)k * m;
@@ -67,7 +71,7 @@ __global__ void __launch_bounds__(SE_THREADS, 1) symeig_kernel(int m, double* __
         }
         __syncthreads();
         const double beta = s_beta;
-        e[k] = s_alpha;  // every thread writes the same value
+        if (tid == 0) a[(size_t)(k + 1) * m + k] = s_alpha;  // e_k (row k, column k+1)
         if (beta == 0.0) {
             for (int i = k + 1 + tid; i < m; i += nt) col[i] = 0.0;
             __syncthreads();
@@ -101,46 +105,69 @@ __global__ void __launch_bounds__(SE_THREADS, 1) symeig_kernel(int m, double* __
         }
         __syncthreads();
     }
-    for (int i = tid; i < m; i += nt) d[i] = a[(size_t)i * m + i];
-    if (tid == 0) {
-        if (m >= 2) e[m - 2] = a[(size_t)(m - 2) * m + (m - 1)];
-        e[m - 1] = 0.0;
+    if (m >= 2 && tid == 0) a[(size_t)(m - 1) * m + (m - 2)] = a[(size_t)(m - 2) * m + (m - 1)];
+}
+
+// CTA b: rows [b*rb, b*rb + rb) of the eigenvector matrix Z = Q * (QL rotations)
+__global__ void __launch_bounds__(256) symeig_ql_kernel(int m, int rb, const double* __restrict__ a,
+                                                        double* __restrict__ z, double* __restrict__ w,
+                                                        int* __restrict__ info) {
+    extern __shared__ double sm[];
+    double* zb = sm;                       // m x rb: zb[i * rb + rr] = Z[r0 + rr][i]
+    double* d = zb + (size_t)m * rb;       // m
+    double* e = d + m;                     // m
+    double* cs = e + m;                    // m
+    double* sn = cs + m;                   // m
+    double* v = sn + m;                    // m
+    __shared__ int s_lo, s_hi, s_state, s_zero;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int r0 = blockIdx.x * rb;
+    const int rows = min(rb, m - r0);
+
+    for (int i = tid; i < m; i += nt) {
+        d[i] = a[(size_t)i * m + i];
+        e[i] = i + 1 < m ? a[(size_t)(i + 1) * m + i] : 0.0;
+    }
+    for (int idx = tid; idx < m * rb; idx += nt) {
+        const int i = idx / rb, rr = idx - i * rb;
+        zb[idx] = (r0 + rr == i) ? 1.0 : 0.0;
     }
     __syncthreads();
 
-    // ---- 2. Q = H_0 H_1 ... H_{m-3}, accumulated backwards into z
-    for (int idx = tid; idx < m * m; idx += nt) z[idx] = (idx % (m + 1) == 0) ? 1.0 : 0.0;
-    __syncthreads();
-    for (int k = m - 3; k >= 0; --k) {
+    // ---- Q rows: z <- z H_k for k = 0 .. m-3 (Q = H_0 H_1 ... H_{m-3})
+    for (int k = 0; k + 2 < m; ++k) {
         const int len = m - k - 1;
         const double* vk = a + (size_t)k * m + (k + 1);
-        bool zero = true;
-        for (int i = 0; i < len && zero; ++i) zero = vk[i] == 0.0;  // uniform branch
-        if (zero) continue;
-        for (int i = tid; i < len; i += nt) v[i] = vk[i];
+        if (tid == 0) s_zero = 1;
         __syncthreads();
-        // w_j = v^T Q[k+1:, j] for columns j >= k+1  (warp per column)
-        for (int j = warp; j < len; j += nw) {
-            const double* cj = z + (size_t)(k + 1 + j) * m + (k + 1);
-            double acc = 0.0;
-            for (int i = lane; i < len; i += 32) acc = fma(v[i], cj[i], acc);
-            acc = warp_sum(acc);
-            if (lane == 0) q[j] = acc;
+        for (int i = tid; i < len; i += nt) {
+            const double x = vk[i];
+            v[i] = x;
+            if (x != 0.0) s_zero = 0;
         }
         __syncthreads();
-        for (int idx = tid; idx < len * len; idx += nt) {
-            int cJ = idx / len, r = idx - cJ * len;
-            z[(size_t)(k + 1 + cJ) * m + (k + 1 + r)] -= 2.0 * v[r] * q[cJ];
+        const int zero = s_zero;
+        __syncthreads();  // everyone has read s_zero before thread 0 resets it
+        if (zero) continue;  // uniform
+        // warp-cooperative per row: 8 lanes per row, rows strided over the CTA
+        const int g = tid >> 3, sub = tid & 7, ng = nt >> 3;
+        for (int rr = g; rr < rb; rr += ng) {
+            double dot = 0.0;
+            if (rr < rows)
+                for (int i = sub; i < len; i += 8) dot = fma(zb[(size_t)(k + 1 + i) * rb + rr], v[i], dot);
+            dot += __shfl_xor_sync(0xffffffffu, dot, 1);
+            dot += __shfl_xor_sync(0xffffffffu, dot, 2);
+            dot += __shfl_xor_sync(0xffffffffu, dot, 4);
+            if (rr < rows)
+                for (int i = sub; i < len; i += 8) zb[(size_t)(k + 1 + i) * rb + rr] -= 2.0 * dot * v[i];
         }
         __syncthreads();
     }
 
-    // ---- 3. implicit QL on (d, e); rotations applied to the rows of z
-    double* cs = v;
-    double* sn = q;
+    // ---- implicit QL on (d, e): thread 0 forms each rotation chain, the rows apply it
     if (tid == 0) {
         s_state = 0;
-        *info = 0;
+        if (blockIdx.x == 0) *info = 0;
     }
     __syncthreads();
     int l = 0, iter = 0;  // only meaningful in thread 0
@@ -159,7 +186,7 @@ __global__ void __launch_bounds__(SE_THREADS, 1) symeig_kernel(int m, double* __
                     continue;
                 }
                 if (++iter > 60) {
-                    *info = l + 1;
+                    if (blockIdx.x == 0) *info = l + 1;
                     l = m;
                     break;
                 }
@@ -170,29 +197,40 @@ __global__ void __launch_bounds__(SE_THREADS, 1) symeig_kernel(int m, double* __
                 int i;
                 bool early = false;
                 int cnt = 0;
+                // The chain is serial, so its latency is the QL cost: d[i],
+                // e[i] are prefetched into registers one rotation ahead (in
+                // program order a shared-memory load would otherwise wait
+                // behind the previous rotation's stores), and one rsqrt
+                // (1 ulp) replaces sqrt + reciprocal; c, s stay orthonormal
+                // to ~1 ulp.  |f|, |g| are O(|T|): no hypot rescaling.
+                double ei = e[mm - 1], di = d[mm - 1], di1 = d[mm];
                 for (i = mm - 1; i >= l; --i) {
-                    double f = s * e[i], b = c * e[i];
-                    // |f|, |g| are O(|T|) here: plain sqrt instead of hypot's
-                    // rescaling, one reciprocal instead of two divisions
-                    r = sqrt(fma(f, f, g * g));
-                    e[i + 1] = r;
-                    if (r == 0.0) {
-                        d[i + 1] -= p;
+                    const double e_nx = i > l ? e[i - 1] : 0.0;
+                    const double d_nx = i > l ? d[i - 1] : 0.0;
+                    const double f = s * ei, b = c * ei;
+                    const double r2 = fma(f, f, g * g);
+                    if (r2 == 0.0) {
+                        e[i + 1] = 0.0;
+                        d[i + 1] = di1 - p;
                         e[mm] = 0.0;
                         early = true;
                         break;
                     }
-                    const double ri = 1.0 / r;
+                    const double ri = rsqrt(r2);
+                    e[i + 1] = r2 * ri;
                     s = f * ri;
                     c = g * ri;
-                    g = d[i + 1] - p;
-                    r = (d[i] - g) * s + 2.0 * c * b;
+                    g = di1 - p;
+                    r = (di - g) * s + 2.0 * c * b;
                     p = s * r;
                     d[i + 1] = g + p;
                     g = c * r - b;
                     cs[cnt] = c;
                     sn[cnt] = s;
                     ++cnt;
+                    di1 = di;  // d[i] is untouched by this rotation
+                    di = d_nx;
+                    ei = e_nx;
                 }
                 if (!(early && i >= l)) {
                     d[l] -= p;
@@ -200,9 +238,9 @@ __global__ void __launch_bounds__(SE_THREADS, 1) symeig_kernel(int m, double* __
                     e[mm] = 0.0;
                 }
                 if (cnt > 0) {
-                    s_hi = mm - 1;          // first rotation acts on (mm-1, mm)
-                    s_lo = mm - cnt;        // last rotation acts on (mm-cnt, mm-cnt+1)
-                    break;                  // hand the chain to the CTA
+                    s_hi = mm - 1;    // first rotation acts on (mm-1, mm)
+                    s_lo = mm - cnt;  // last rotation acts on (mm-cnt, mm-cnt+1)
+                    break;            // hand the chain to the rows
                 }
             }
             if (l >= m && s_hi < 0) s_state = 1;
@@ -210,20 +248,25 @@ __global__ void __launch_bounds__(SE_THREADS, 1) symeig_kernel(int m, double* __
         __syncthreads();
         if (s_state) break;
         const int hi = s_hi, lo = s_lo;
-        for (int r = tid; r < m; r += nt) {
-            double carry = z[(size_t)(hi + 1) * m + r];  // z[r][i+1]
+        for (int rr = tid; rr < rows; rr += nt) {
+            double carry = zb[(size_t)(hi + 1) * rb + rr];
             int t = 0;
             for (int i = hi; i >= lo; --i, ++t) {
-                double c = cs[t], s = sn[t];
-                double zi = z[(size_t)i * m + r];
-                z[(size_t)(i + 1) * m + r] = s * zi + c * carry;
+                const double c = cs[t], s = sn[t];
+                const double zi = zb[(size_t)i * rb + rr];
+                zb[(size_t)(i + 1) * rb + rr] = s * zi + c * carry;
                 carry = c * zi - s * carry;
             }
-            z[(size_t)lo * m + r] = carry;
+            zb[(size_t)lo * rb + rr] = carry;
         }
         __syncthreads();
     }
-    for (int i = tid; i < m; i += nt) w[i] = d[i];
+    for (int idx = tid; idx < m * rows; idx += nt) {
+        const int i = idx / rows, rr = idx - i * rows;
+        z[(size_t)i * m + r0 + rr] = zb[(size_t)i * rb + rr];
+    }
+    if (blockIdx.x == 0)
+        for (int i = tid; i < m; i += nt) w[i] = d[i];
 }
 
 // stable descending order: rank_i = #{j : w_j > w_i or (w_j == w_i and j < i)}
@@ -253,20 +296,26 @@ __global__ void symeig_sort_kernel(int m, int kout, const double* __restrict__ w
 
 int symeig_launch(int m, int kout, double* a, double* z, double* w_raw, double* w_sorted,
                   double* z_sorted, int* info, cudaStream_t st) {
-    size_t smem = sizeof(double) * (4 * (size_t)m + 40);
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(symeig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(symeig_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(symeig_tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SE_SMEM_MAX);
+        cudaFuncSetAttribute(symeig_ql_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SE_SMEM_MAX);
+        cudaFuncSetAttribute(symeig_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SE_SMEM_MAX);
         attr_set = true;
     }
-    if (smem > 200 * 1024) return fail(SC_ERR_VALUE, "projected matrix too large for the device eigensolver");
+    // rows per CTA: as many as fit (at most 64) next to the 5 m-vectors
+    int rb = 64;
+    while (rb > 1 && sizeof(double) * ((size_t)m * rb + 5 * (size_t)m) > (size_t)SE_SMEM_MAX) rb >>= 1;
+    const size_t ql_smem = sizeof(double) * ((size_t)m * rb + 5 * (size_t)m);
+    if (ql_smem > (size_t)SE_SMEM_MAX) return fail(SC_ERR_VALUE, "projected matrix too large for the device eigensolver");
+    const int nblk = (m + rb - 1) / rb;
     {
         ProfScope prof("symeig", st, 0.0);
-        symeig_kernel<<<1, SE_THREADS, smem, st>>>(m, a, z, w_raw, info);
+        symeig_tridiag_kernel<<<1, SE_THREADS, sizeof(double) * (2 * (size_t)m + 40), st>>>(m, a);
+        symeig_ql_kernel<<<nblk, 256, ql_smem, st>>>(m, rb, a, z, w_raw, info);
         symeig_sort_kernel<<<1, 1024, sizeof(int) * (size_t)m, st>>>(m, kout, w_raw, z, w_sorted, z_sorted);
     }
-    SC_LAUNCHED(2);
+    SC_LAUNCHED(3);
     return SC_OK;
 }
 
