@@ -242,7 +242,7 @@ def main():
         lib.sc_profile_query(name.encode(), nat.C.byref(ms), nat.C.byref(cnt), nat.C.byref(work))
         return ms.value / max(1, args.steps), cnt.value / max(1, args.steps), work.value / max(1, args.steps)
 
-    kernel_classes = ["knn_tile", "knn_recheck", "knn_fallback", "knn_union", "spmv", "reorth", "ritz", "symeig",
+    kernel_classes = ["knn_order", "knn_tile", "knn_recheck", "knn_fallback", "knn_union", "spmv", "reorth", "ritz", "symeig",
                       "embed", "kmeanspp", "kmeans_assign", "kmeans_update", "ncut"]
     kstats = {c: prof(c) for c in kernel_classes}
     # per step: max over ranks; reported value: median over the timed steps

@@ -111,6 +111,17 @@ int sc_sell_create(int64_t n_rows, const int64_t* row_ptr, const int32_t* col, c
 int sc_sell_spmv(const sc_sell_t* op, const double* x, double* y, sc_stream_t stream);
 int sc_sell_info(const sc_sell_t* op, int64_t* stored, int64_t* n_long_rows);
 void sc_sell_destroy(sc_sell_t* op);
+/* Bulk-staged SpMV plan for repeated y = A x (the eigensolver's matvec;
+ * replaces eigen.py:269-276 `_fast_apply` / sparse.py:195-207 `spmv` inside
+ * the solve): ~2048-nonzero chunks of whole rows are streamed by one
+ * persistent CTA per SM through a cp.async.bulk shared-memory ring while the
+ * CTA's consumer warps gather x and reduce rows.  A's CSR arrays must outlive
+ * the handle; n_rows may be a row shard (columns global). */
+typedef struct sc_spmv_plan sc_spmv_plan_t;
+int sc_spmv_plan_create(int64_t n_rows, const int64_t* row_ptr, const int32_t* col, const double* vals,
+                        sc_stream_t stream, sc_spmv_plan_t** out);
+int sc_spmv_plan_apply(const sc_spmv_plan_t* plan, const double* x, double* y, sc_stream_t stream);
+void sc_spmv_plan_destroy(sc_spmv_plan_t* plan);
 /* pos[perm[p]] = p */
 int sc_invert_perm(int64_t n, const int32_t* perm, int32_t* pos, sc_stream_t stream);
 /* dst row r = src row idx[r] (row-major n x k f64) */

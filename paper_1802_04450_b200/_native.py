@@ -56,6 +56,9 @@ SIGNATURES = {
     "sc_sell_spmv": (i32, [vp, vp, vp, vp]),
     "sc_sell_info": (i32, [vp, P_i64, P_i64]),
     "sc_sell_destroy": (None, [vp]),
+    "sc_spmv_plan_create": (i32, [i64, vp, vp, vp, vp, C.POINTER(vp)]),
+    "sc_spmv_plan_apply": (i32, [vp, vp, vp, vp]),
+    "sc_spmv_plan_destroy": (None, [vp]),
     "sc_gather_rows_f64": (i32, [i64, i64, vp, vp, vp, vp]),
     "sc_knn_graph_f64": (i32, [i64, i64, vp, i64, f64, vp, vp, vp, P_i64, P_i64, vp]),
     "sc_knn_select_f64": (i32, [i64, i64, vp, i64, f64, i64, i64, vp, vp, P_i64, vp]),

@@ -53,6 +53,9 @@ struct ProfSlot {
 static bool g_prof = false;
 static std::mutex g_prof_mu;
 static std::vector<ProfSlot> g_slots;
+static thread_local int g_prof_mute = 0;
+ProfMute::ProfMute() { ++g_prof_mute; }
+ProfMute::~ProfMute() { --g_prof_mute; }
 
 static int slot_of(const char* name) {
     for (size_t i = 0; i < g_slots.size(); ++i)
@@ -63,7 +66,7 @@ static int slot_of(const char* name) {
 }
 
 ProfScope::ProfScope(const char* name, cudaStream_t s, double work) {
-    if (!g_prof) return;
+    if (!g_prof || g_prof_mute) return;
     std::lock_guard<std::mutex> lk(g_prof_mu);
     slot = slot_of(name);
     stream = s;

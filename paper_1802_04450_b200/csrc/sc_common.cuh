@@ -43,6 +43,12 @@ struct ProfScope {
     ProfScope(const char* name, cudaStream_t s, double work);
     ~ProfScope();
 };
+// ProfScopes opened on this thread while a ProfMute lives are not recorded
+// (an internal helper run accounted under its caller's kernel class)
+struct ProfMute {
+    ProfMute();
+    ~ProfMute();
+};
 
 // ---- device memory owned by the library ---------------------------------------
 // Scratch comes from the stream-ordered pool (cudaMallocAsync on the stream

@@ -61,6 +61,48 @@ __global__ void gather_strided_rows_kernel(int64_t n, int64_t d, int64_t C, cons
     for (int64_t l = threadIdx.x; l < d; l += blockDim.x) out[c * d + l] = x[r * d + l];
 }
 
+// squared distances between the C pivots (fp32 is plenty for ordering them)
+__global__ void pivot_dist_kernel(int64_t C, int64_t d, const double* __restrict__ piv, float* __restrict__ D) {
+    const int64_t a = blockIdx.y, b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= C) return;
+    double s = 0.0;
+    for (int64_t l = 0; l < d; ++l) {
+        const double t = piv[a * d + l] - piv[b * d + l];
+        s = fma(t, t, s);
+    }
+    D[a * C + b] = (float)s;
+}
+
+__global__ void gather_pivots_kernel(int64_t C, int64_t d, const double* __restrict__ src,
+                                     const int32_t* __restrict__ order, double* __restrict__ dst) {
+    const int64_t c = blockIdx.x;
+    for (int64_t l = threadIdx.x; l < d; l += blockDim.x) dst[c * d + l] = src[(int64_t)order[c] * d + l];
+}
+
+// Greedy nearest-neighbour tour over the pivots (start at pivot 0, always
+// step to the closest unvisited one; ties -> lower index).  Pivots of one
+// dense region are mutual near neighbours, so the tour visits them in a run
+// and their buckets become one contiguous range of the scan order.
+static void pivot_tour(int64_t C, const std::vector<float>& D, std::vector<int32_t>& order) {
+    std::vector<char> used((size_t)C, 0);
+    order.assign(1, 0);
+    used[0] = 1;
+    int64_t cur = 0;
+    for (int64_t t = 1; t < C; ++t) {
+        float best = INFINITY;
+        int64_t bi = -1;
+        const float* row = D.data() + cur * C;
+        for (int64_t b = 0; b < C; ++b)
+            if (!used[(size_t)b] && (bi < 0 || row[b] < best)) {
+                best = row[b];
+                bi = b;
+            }
+        used[(size_t)bi] = 1;
+        order.push_back((int32_t)bi);
+        cur = bi;
+    }
+}
+
 // xf = fp32(x - mean) padded to dp columns; cnf = fp32(|xf|^2) (computed in
 // fp64 from the fp32 values); rn = |x - mean| (fp64); rmax = max rn
 __global__ void knn_prep_kernel(int64_t n, int64_t d, int64_t dp, const double* __restrict__ x,
@@ -634,8 +676,52 @@ int knn_select(int64_t n, int64_t d, const double* x, int64_t knn, double two_si
         if (n >= 4096 && !std::getenv("SPECLUST_KNN_NOSORT")) {
             const int64_t C = std::min<int64_t>(1024, std::max<int64_t>(8, n / 1024));
             if ((rc = piv.alloc((size_t)C * d)) || (rc = plab.alloc(n)) || (rc = bk.init(n, C))) return rc;
+            ProfScope prof_order("knn_order", st, 0.0);
             gather_strided_rows_kernel<<<(unsigned)C, 128, 0, st>>>(n, d, C, x, piv.p);
             SC_LAUNCHED(1);
+            if (!std::getenv("SPECLUST_KNN_NOREFINE")) {
+                // a few Lloyd steps of the pivots on a strided subsample: raw
+                // strided pivots in high dimension split a dense region among
+                // the pivots of other regions (nearest-pivot distances are all
+                // alike); refined pivots sit inside the regions
+                const int64_t ns = std::min<int64_t>(n, 32 * C);
+                DevBuf<double> sub, cent;
+                DevBuf<int64_t> slab;
+                if ((rc = sub.alloc((size_t)ns * d)) || (rc = cent.alloc((size_t)C * d)) || (rc = slab.alloc(ns)))
+                    return rc;
+                gather_strided_rows_kernel<<<(unsigned)ns, 128, 0, st>>>(n, d, ns, x, sub.p);
+                SC_LAUNCHED(1);
+                std::vector<double> hist(8);
+                int64_t its = 0;
+                ProfMute mute;
+                if ((rc = sc_lloyd(ns, d, C, sub.p, piv.p, 4, 0, slab.p, cent.p, hist.data(), &its,
+                                   reinterpret_cast<sc_stream_t>(st))))
+                    return rc;
+                SC_CUDA(cudaMemcpyAsync(piv.p, cent.p, sizeof(double) * C * d, cudaMemcpyDeviceToDevice, st));
+            }
+            if (!std::getenv("SPECLUST_KNN_NOTOUR")) {
+                // renumber the pivots along a nearest-neighbour tour: bucket
+                // b's points then sit next to those of the pivots closest to
+                // b, so a dense region is one index range (kNN scan order and
+                // the eigensolver's SpMV locality)
+                DevBuf<float> pd;
+                DevBuf<double> piv2;
+                DevBuf<int32_t> ord;
+                if ((rc = pd.alloc((size_t)C * C)) || (rc = piv2.alloc((size_t)C * d)) || (rc = ord.alloc(C)))
+                    return rc;
+                pivot_dist_kernel<<<dim3((unsigned)ceil_div(C, 128), (unsigned)C), 128, 0, st>>>(C, d, piv.p, pd.p);
+                SC_LAUNCHED(1);
+                std::vector<float> hd((size_t)C * C);
+                SC_CUDA(cudaMemcpyAsync(hd.data(), pd.p, sizeof(float) * C * C, cudaMemcpyDeviceToHost, st));
+                SC_CUDA(cudaStreamSynchronize(st));
+                std::vector<int32_t> order;
+                pivot_tour(C, hd, order);
+                SC_CUDA(cudaMemcpyAsync(ord.p, order.data(), sizeof(int32_t) * C, cudaMemcpyHostToDevice, st));
+                gather_pivots_kernel<<<(unsigned)C, 128, 0, st>>>(C, d, piv.p, ord.p, piv2.p);
+                SC_CUDA(cudaMemcpyAsync(piv.p, piv2.p, sizeof(double) * C * d, cudaMemcpyDeviceToDevice, st));
+                SC_CUDA(cudaStreamSynchronize(st));  // `order` leaves scope
+                SC_LAUNCHED(1);
+            }
             if ((rc = assign_nearest(n, d, x, C, piv.p, plab.p, st)) || (rc = bk.run(plab.p, st))) return rc;
             perm = bk.members.p;
         }

@@ -5,6 +5,7 @@
 // col int32[nnz] (n < 2^31), vals f64[nnz]; rows sorted, columns strictly
 // increasing within a row (sparse.py:110-138).
 #include <cstdlib>
+#include <cstring>
 
 #include "sc_common.cuh"
 #include "sc_sparse.cuh"
@@ -56,14 +57,357 @@ __global__ void __launch_bounds__(256) spmv_vec_kernel(int64_t n, const int64_t*
     if (lane == 0) y[row] = acc;
 }
 
+// Cache-policy loads for the SpMV: the col/vals/row_ptr streams are read once
+// and must not evict the x entries the rows gather (L1::no_allocate), while x
+// is kept (L1::evict_last) so a row block's neighbourhood stays in L1.
+__device__ __forceinline__ int32_t ld_stream(const int32_t* p) {
+    int32_t v;
+    asm("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ int64_t ld_stream(const int64_t* p) {
+    int64_t v;
+    asm("ld.global.nc.L1::no_allocate.b64 %0, [%1];" : "=l"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double ld_stream(const double* p) {
+    double v;
+    asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double ld_keep(const double* p) {
+    double v;
+    asm("ld.global.nc.L1::evict_last.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+
+// Locality SpMV.  The rows are cut into kNumSMs contiguous ranges; block b
+// works on range b % kNumSMs, which for a grid of exactly one resident wave
+// (kNumSMs x SPMV_LOCAL_BPS blocks) is the SM the block scheduler puts it on.
+// All warps of that SM walk their range together, G lanes per row and 32/G
+// rows per warp, so once the operator is in locality order (a row's columns
+// lie in a window of nearby rows, pipeline.py / sc_knn.cu pivot chain) the
+// x gathers are served by the SM's L1 (no shared memory: the whole unified
+// carve-out is L1) instead of one random L2 sector per nonzero.  Correctness
+// does not depend on the block -> SM placement, only the hit rate does.
+template <int G>
+__global__ void __launch_bounds__(256) spmv_local_kernel(int64_t n, const int64_t* __restrict__ row_ptr,
+                                                         const int32_t* __restrict__ col,
+                                                         const double* __restrict__ vals,
+                                                         const double* __restrict__ x, double* __restrict__ y) {
+    constexpr int RPW = 32 / G;
+    const int grp = blockIdx.x % kNumSMs, sub = blockIdx.x / kNumSMs;
+    const int64_t r0 = n * grp / kNumSMs, r1 = n * (grp + 1) / kNumSMs;
+    const int lane = threadIdx.x & 31, sl = lane % G;
+    const int wpb = blockDim.x >> 5;
+    const int64_t stride = (int64_t)(gridDim.x / kNumSMs) * wpb * RPW;
+    for (int64_t base = r0 + ((int64_t)sub * wpb + (threadIdx.x >> 5)) * RPW; base < r1; base += stride) {
+        const int64_t row = base + lane / G;
+        const bool valid = row < r1;
+        int64_t p = 0, e = 0;
+        if (valid) {
+            p = ld_stream(row_ptr + row) + sl;
+            e = ld_stream(row_ptr + row + 1);
+        }
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        for (; p + 3 * G < e; p += 4 * G) {
+            const int32_t c0 = ld_stream(col + p), c1 = ld_stream(col + p + G), c2 = ld_stream(col + p + 2 * G),
+                          c3 = ld_stream(col + p + 3 * G);
+            const double v0 = ld_stream(vals + p), v1 = ld_stream(vals + p + G), v2 = ld_stream(vals + p + 2 * G),
+                         v3 = ld_stream(vals + p + 3 * G);
+            a0 = fma(v0, ld_keep(x + c0), a0);
+            a1 = fma(v1, ld_keep(x + c1), a1);
+            a2 = fma(v2, ld_keep(x + c2), a2);
+            a3 = fma(v3, ld_keep(x + c3), a3);
+        }
+        if (p + G < e) {
+            const int32_t c0 = ld_stream(col + p), c1 = ld_stream(col + p + G);
+            const double v0 = ld_stream(vals + p), v1 = ld_stream(vals + p + G);
+            a0 = fma(v0, ld_keep(x + c0), a0);
+            a1 = fma(v1, ld_keep(x + c1), a1);
+            p += 2 * G;
+        }
+        if (p < e) a2 = fma(ld_stream(vals + p), ld_keep(x + ld_stream(col + p)), a2);
+        double acc = (a0 + a1) + (a2 + a3);
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, G);
+        if (valid && sl == 0) y[row] = acc;
+    }
+}
+
+// Batched warp-per-row SpMV: a warp owns R consecutive rows and issues the
+// first two 32-wide strips of all R rows (2R col + 2R val loads per lane, then
+// 2R independent x gathers) before consuming any of them, so each warp keeps
+// ~R times the bytes in flight of a one-row warp.  (The one-row kernel is
+// long-scoreboard bound at ~2.2 TB/s: row_ptr -> col/vals -> x is a chain of
+// three dependent round trips per ~55 nonzeros.)  Longer rows finish in a
+// strip loop; lane sums go through one shuffle tree per row.
+template <int R>
+__global__ void __launch_bounds__(256) spmv_batch_kernel(int64_t n, const int64_t* __restrict__ row_ptr,
+                                                         const int32_t* __restrict__ col,
+                                                         const double* __restrict__ vals,
+                                                         const double* __restrict__ x, double* __restrict__ y) {
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t row0 = warp * R;
+    if (row0 >= n) return;
+    const int64_t nr = imin64(R, n - row0);
+    const int64_t rp = lane <= nr ? __ldg(row_ptr + row0 + lane) : 0;
+    int64_t b[R], e[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        b[r] = __shfl_sync(0xffffffffu, rp, r);
+        e[r] = r < nr ? __shfl_sync(0xffffffffu, rp, r + 1) : b[r];
+    }
+    int32_t c[R][2];
+    double v[R][2];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int64_t p = b[r] + lane + 32 * u;
+            const bool ok = p < e[r];
+            c[r][u] = ok ? __ldg(col + p) : -1;
+            v[r][u] = ok ? __ldg(vals + p) : 0.0;
+        }
+    double acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        double a = 0.0;
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+            if (c[r][u] >= 0) a = fma(v[r][u], __ldg(x + c[r][u]), a);
+        for (int64_t p = b[r] + lane + 64; p < e[r]; p += 32) a = fma(__ldg(vals + p), __ldg(x + __ldg(col + p)), a);
+        acc[r] = a;
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const double s = warp_sum(acc[r]);
+        if (lane == r && r < nr) y[row0 + r] = s;
+    }
+}
+
+// Software-pipelined warp-per-row SpMV over per-SM row ranges (as in
+// spmv_local_kernel).  While a warp's x gathers for row t are in flight it
+// already holds the first two 32-wide col/val strips of row t+1 and the
+// row_ptr pair of row t+2, so the HBM stream (col, vals, row_ptr) never
+// waits behind the gathers.  Rows longer than 64 finish in a strip loop.
+__global__ void __launch_bounds__(256) spmv_pipe_kernel(int64_t n, const int64_t* __restrict__ row_ptr,
+                                                        const int32_t* __restrict__ col,
+                                                        const double* __restrict__ vals,
+                                                        const double* __restrict__ x, double* __restrict__ y) {
+    const int grp = blockIdx.x % kNumSMs, sub = blockIdx.x / kNumSMs;
+    const int64_t r0 = n * grp / kNumSMs, r1 = n * (grp + 1) / kNumSMs;
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)(gridDim.x / kNumSMs) * (blockDim.x >> 5);
+    int64_t row = r0 + (int64_t)sub * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (row >= r1) return;
+    auto bounds = [&](int64_t r, int64_t& b, int64_t& e) {
+        if (r < r1) {
+            const int64_t v = __ldg(row_ptr + r + (lane & 1));
+            b = __shfl_sync(0xffffffffu, v, 0);
+            e = __shfl_sync(0xffffffffu, v, 1);
+        } else {
+            b = e = 0;
+        }
+    };
+    auto strips = [&](int64_t b, int64_t e, int32_t& c0, int32_t& c1, double& v0, double& v1) {
+        const int64_t p = b + lane;
+        c0 = p < e ? __ldg(col + p) : -1;
+        v0 = p < e ? __ldg(vals + p) : 0.0;
+        c1 = p + 32 < e ? __ldg(col + p + 32) : -1;
+        v1 = p + 32 < e ? __ldg(vals + p + 32) : 0.0;
+    };
+    int64_t b, e, nb, ne;
+    bounds(row, b, e);
+    bounds(row + stride, nb, ne);
+    int32_t c0, c1;
+    double v0, v1;
+    strips(b, e, c0, c1, v0, v1);
+    for (; row < r1; row += stride) {
+        // prefetch: strips of the next row, bounds of the one after
+        int32_t d0, d1;
+        double w0, w1;
+        strips(nb, ne, d0, d1, w0, w1);
+        int64_t nnb, nne;
+        bounds(row + 2 * stride, nnb, nne);
+        double acc = 0.0, acc2 = 0.0;
+        if (c0 >= 0) acc = v0 * __ldg(x + c0);
+        if (c1 >= 0) acc2 = v1 * __ldg(x + c1);
+        for (int64_t p = b + 64 + lane; p < e; p += 32) acc = fma(__ldg(vals + p), __ldg(x + __ldg(col + p)), acc);
+        const double s = warp_sum(acc + acc2);
+        if (lane == 0) y[row] = s;
+        b = nb;
+        e = ne;
+        nb = nnb;
+        ne = nne;
+        c0 = d0;
+        c1 = d1;
+        v0 = w0;
+        v1 = w1;
+    }
+}
+
+// SM-affine SpMV: the rows are cut into one contiguous range per SM id
+// (%nsmid ranges); a warp first drains the range of the SM it runs on
+// (atomic per-range cursor, SPMV_GRAB rows per grab) and then steals from the
+// other ranges, so every row is done exactly once whatever the block
+// placement, and in locality order an SM's gathers stay inside its range's
+// x neighbourhood (its L1).  cursors: nsmid ints, zero at launch.
+constexpr int SPMV_GRAB_ITERS = 16;
+constexpr int SPMV_MAX_RANGES = kNumSMs;
+__device__ __forceinline__ uint32_t sm_id() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t sm_count() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%nsmid;" : "=r"(r));
+    return r;
+}
+template <int G>
+__global__ void __launch_bounds__(256) spmv_affine_kernel(int64_t n, int nranges, const int64_t* __restrict__ row_ptr,
+                                                          const int32_t* __restrict__ col,
+                                                          const double* __restrict__ vals,
+                                                          const double* __restrict__ x, double* __restrict__ y,
+                                                          int* __restrict__ cursors) {
+    constexpr int RPW = 32 / G;
+    constexpr int GRAB = RPW * SPMV_GRAB_ITERS;
+    const int lane = threadIdx.x & 31, sl = lane % G;
+    const int home = (int)(sm_id() % (uint32_t)nranges);
+    for (int t = 0; t < nranges; ++t) {
+        const int rg = (home + t) % nranges;
+        const int64_t r0 = n * rg / nranges, r1 = n * (rg + 1) / nranges;
+        const int len = (int)(r1 - r0);
+        while (true) {
+            int start = 0;
+            if (lane == 0) start = *((volatile int*)cursors + rg) >= len ? len : atomicAdd(cursors + rg, GRAB);
+            start = __shfl_sync(0xffffffffu, start, 0);
+            if (start >= len) break;
+            const int64_t end = imin64(r1, r0 + start + GRAB);
+            for (int64_t base = r0 + start; base < end; base += RPW) {
+                const int64_t row = base + lane / G;
+                const bool valid = row < end;
+                int64_t p = 0, e = 0;
+                if (valid) {
+                    p = ld_stream(row_ptr + row) + sl;
+                    e = ld_stream(row_ptr + row + 1);
+                }
+                double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+                for (; p + 3 * G < e; p += 4 * G) {
+                    const int32_t c0 = ld_stream(col + p), c1 = ld_stream(col + p + G),
+                                  c2 = ld_stream(col + p + 2 * G), c3 = ld_stream(col + p + 3 * G);
+                    const double v0 = ld_stream(vals + p), v1 = ld_stream(vals + p + G),
+                                 v2 = ld_stream(vals + p + 2 * G), v3 = ld_stream(vals + p + 3 * G);
+                    a0 = fma(v0, ld_keep(x + c0), a0);
+                    a1 = fma(v1, ld_keep(x + c1), a1);
+                    a2 = fma(v2, ld_keep(x + c2), a2);
+                    a3 = fma(v3, ld_keep(x + c3), a3);
+                }
+                if (p + G < e) {
+                    const int32_t c0 = ld_stream(col + p), c1 = ld_stream(col + p + G);
+                    const double v0 = ld_stream(vals + p), v1 = ld_stream(vals + p + G);
+                    a0 = fma(v0, ld_keep(x + c0), a0);
+                    a1 = fma(v1, ld_keep(x + c1), a1);
+                    p += 2 * G;
+                }
+                if (p < e) a2 = fma(ld_stream(vals + p), ld_keep(x + ld_stream(col + p)), a2);
+                double acc = (a0 + a1) + (a2 + a3);
+#pragma unroll
+                for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, G);
+                if (valid && sl == 0) y[row] = acc;
+            }
+        }
+    }
+}
+
+template <int G>
+static int spmv_affine_launch(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* vals,
+                              const double* x, double* y, int* cursors, cudaStream_t st) {
+    static int bps = 0, nsm = 0;
+    if (!bps) {
+        cudaFuncSetAttribute(spmv_affine_kernel<G>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, spmv_affine_kernel<G>, 256, 0);
+        if (bps < 1) bps = 1;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    }
+    SC_CUDA(cudaMemsetAsync(cursors, 0, sizeof(int) * SPMV_MAX_RANGES, st));
+    spmv_affine_kernel<G><<<nsm * bps, 256, 0, st>>>(n, SPMV_MAX_RANGES, row_ptr, col, vals, x, y, cursors);
+    return SC_OK;
+}
+
+template <int G>
+static void spmv_local_launch(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* vals,
+                              const double* x, double* y, cudaStream_t st) {
+    static int bps = 0;
+    if (!bps) {  // all of the unified L1/shared array as L1; one resident wave
+        cudaFuncSetAttribute(spmv_local_kernel<G>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, spmv_local_kernel<G>, 256, 0);
+        if (bps < 1) bps = 1;
+    }
+    spmv_local_kernel<G><<<kNumSMs * bps, 256, 0, st>>>(n, row_ptr, col, vals, x, y);
+}
+
+// SpMV kernel choice.  Default: the per-SM-range warp kernel ("local").
+// SPECLUST_SPMV_KERNEL overrides it (tuning and tests): "vec" (one row per
+// warp, flat grid), "affine" (SM-id ranges with stealing), "pipe"
+// (software-pipelined), "batch2"/"batch4"/"batch8" (R rows per warp),
+// "bulk" (SpmvPlan only: cp.async.bulk staged chunks).
+int spmv_kind() {
+    const char* kenv = std::getenv("SPECLUST_SPMV_KERNEL");
+    if (!kenv) return 6;
+    if (!std::strcmp(kenv, "vec")) return 0;
+    if (!std::strcmp(kenv, "affine")) return 1;
+    if (!std::strcmp(kenv, "batch2")) return 2;
+    if (!std::strcmp(kenv, "batch4")) return 4;
+    if (!std::strcmp(kenv, "pipe")) return 5;
+    if (!std::strcmp(kenv, "batch8")) return 8;
+    if (!std::strcmp(kenv, "bulk")) return 9;
+    return 6;
+}
+
 int spmv_launch(int64_t n, int64_t nnz, const int64_t* row_ptr, const int32_t* col,
                 const double* vals, const double* x, double* y, bool deterministic,
                 cudaStream_t st) {
     if (n == 0) return SC_OK;
     double bytes = (double)nnz * 12.0 + (double)(n + 1) * 8.0 + 2.0 * (double)n * 8.0;
     ProfScope prof(deterministic ? "spmv_seq" : "spmv", st, bytes);
+    const int kind = spmv_kind();
+    const double mean_len = (double)nnz / (double)n;
     if (deterministic) {
         spmv_seq_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, row_ptr, col, vals, x, y);
+    } else if (kind == 5 && mean_len > 24 && n >= 4096) {
+        static int bps = 0;
+        if (!bps) {  // one resident wave: blocks per SM from the occupancy calculator
+            cudaFuncSetAttribute(spmv_pipe_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, spmv_pipe_kernel, 256, 0);
+            if (bps < 1) bps = 1;
+        }
+        spmv_pipe_kernel<<<kNumSMs * bps, 256, 0, st>>>(n, row_ptr, col, vals, x, y);
+    } else if ((kind == 2 || kind == 4 || kind == 8 || kind == 9) && mean_len > 24) {
+        if (kind == 2)
+            spmv_batch_kernel<2><<<(unsigned)ceil_div(ceil_div(n, 2) * 32, 256), 256, 0, st>>>(n, row_ptr, col, vals, x, y);
+        else if (kind == 8)
+            spmv_batch_kernel<8><<<(unsigned)ceil_div(ceil_div(n, 8) * 32, 256), 256, 0, st>>>(n, row_ptr, col, vals, x, y);
+        else
+            spmv_batch_kernel<4><<<(unsigned)ceil_div(ceil_div(n, 4) * 32, 256), 256, 0, st>>>(n, row_ptr, col, vals, x, y);
+    } else if (kind == 6 && n >= 4096) {
+        if (mean_len > 24)
+            spmv_local_launch<16>(n, row_ptr, col, vals, x, y, st);
+        else
+            spmv_local_launch<8>(n, row_ptr, col, vals, x, y, st);
+    } else if (kind == 1 && n >= 4096) {
+        DevBuf<int> cur;
+        int rc;
+        if ((rc = cur.alloc(SPMV_MAX_RANGES))) return rc;
+        if (mean_len > 24)
+            rc = spmv_affine_launch<16>(n, row_ptr, col, vals, x, y, cur.p, st);
+        else
+            rc = spmv_affine_launch<8>(n, row_ptr, col, vals, x, y, cur.p, st);
+        if (rc) return rc;
     } else {
         double mean = n ? (double)nnz / (double)n : 0.0;
         static const char* genv = std::getenv("SPECLUST_SPMV_G");  // tuning override
@@ -551,3 +895,206 @@ extern "C" int sc_sell_info(const sc_sell* h, int64_t* stored, int64_t* nlong) {
     return SC_OK;
 }
 extern "C" void sc_sell_destroy(sc_sell* h) { delete h; }
+
+// ---------------------------------------------------------------------------
+// Bulk-staged SpMV (see SpmvPlan in sc_sparse.cuh).
+#include "sc_tc.cuh"
+
+namespace sc {
+
+// chunk c = the rows whose first nonzero index lies in [c*CH, (c+1)*CH)
+__device__ __forceinline__ int64_t first_row_at_or_after(const int64_t* __restrict__ row_ptr, int64_t n, int64_t p) {
+    int64_t lo = 0, hi = n + 1;  // first r in [0, n] with row_ptr[r] >= p (n if none)
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (row_ptr[mid] < p) lo = mid + 1; else hi = mid;
+    }
+    return lo > n ? n : lo;
+}
+
+__global__ void spmv_plan_kernel(int64_t n, int64_t nnz, int64_t nch, const int64_t* __restrict__ row_ptr,
+                                 SpmvChunk* __restrict__ chunks) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nch) return;
+    const int64_t ra = first_row_at_or_after(row_ptr, n, c * SPMV_CH);
+    const int64_t rb = c + 1 == nch ? n : first_row_at_or_after(row_ptr, n, (c + 1) * SPMV_CH);
+    SpmvChunk ch;
+    ch.row_begin = ra;
+    ch.row_end = rb;
+    ch.p_begin = row_ptr[ra];
+    ch.p_end = row_ptr[rb];
+    // staged iff it fits the stage and the 16-byte-rounded bulk reads stay
+    // inside the arrays (only the matrix tail can fail the latter)
+    const int64_t pa = ch.p_begin & ~3ll, pv = ch.p_begin & ~1ll, rr = ra & ~1ll;
+    const int64_t ncol = (ch.p_end - pa + 3) & ~3ll, nval = (ch.p_end - pv + 1) & ~1ll,
+                  nrp = (rb + 1 - rr + 1) & ~1ll;
+    ch.staged = ch.p_end - ch.p_begin <= SPMV_CAP && rb - ra <= SPMV_RCAP && pa + ncol <= nnz && pv + nval <= nnz &&
+                rr + nrp <= n + 1;
+    chunks[c] = ch;
+}
+
+struct SpmvStage {
+    int32_t col[SPMV_CAP + 4];
+    double vals[SPMV_CAP + 2];
+    int64_t rp[SPMV_RCAP + 2];
+};
+
+// one CTA per SM: warp 0 streams chunk after chunk of (col, vals, row_ptr)
+// into a SPMV_STAGES-deep shared-memory ring with cp.async.bulk (completion on
+// the stage's mbarrier); warps 1.. consume the staged chunk G lanes per row,
+// gather x (L1 / L2) and write y, then release the stage.  The CTA's chunks
+// are one contiguous range, so in locality order its x window stays in L1.
+template <int G>
+__global__ void __launch_bounds__(SPMV_THREADS, 1) spmv_bulk_kernel(int64_t n, int64_t nch,
+                                                                    const SpmvChunk* __restrict__ chunks,
+                                                                    const int64_t* __restrict__ row_ptr,
+                                                                    const int32_t* __restrict__ col,
+                                                                    const double* __restrict__ vals,
+                                                                    const double* __restrict__ x,
+                                                                    double* __restrict__ y) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    SpmvStage* stages = reinterpret_cast<SpmvStage*>(smem_raw);
+    __shared__ uint64_t full[SPMV_STAGES], empty[SPMV_STAGES];
+    __shared__ SpmvChunk hdr[SPMV_STAGES];
+    constexpr int NCW = SPMV_THREADS / 32 - 1;  // consumer warps
+    constexpr int RPW = 32 / G;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t c0 = nch * blockIdx.x / gridDim.x, c1 = nch * (blockIdx.x + 1) / gridDim.x;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < SPMV_STAGES; ++s) {
+            tc::mbar_init(&full[s], 1);
+            tc::mbar_init(&empty[s], NCW);
+        }
+        tc::fence_mbar_init();
+    }
+    __syncthreads();
+    if (warp == 0) {
+        if (lane != 0) return;
+        for (int64_t c = c0; c < c1; ++c) {
+            const int64_t i = c - c0;
+            const int s = (int)(i % SPMV_STAGES);
+            tc::mbar_wait(&empty[s], (uint32_t)(((i / SPMV_STAGES) & 1) ^ 1));
+            const SpmvChunk ch = chunks[c];
+            hdr[s] = ch;
+            if (ch.staged && ch.p_end > ch.p_begin) {
+                const int64_t pa = ch.p_begin & ~3ll, pv = ch.p_begin & ~1ll, rr = ch.row_begin & ~1ll;
+                const uint32_t bc = (uint32_t)(((ch.p_end - pa + 3) & ~3ll) * 4);
+                const uint32_t bv = (uint32_t)(((ch.p_end - pv + 1) & ~1ll) * 8);
+                const uint32_t br = (uint32_t)(((ch.row_end + 1 - rr + 1) & ~1ll) * 8);
+                tc::mbar_expect_tx(&full[s], bc + bv + br);
+                tc::bulk_g2s(stages[s].col, col + pa, bc, &full[s]);
+                tc::bulk_g2s(stages[s].vals, vals + pv, bv, &full[s]);
+                tc::bulk_g2s(stages[s].rp, row_ptr + rr, br, &full[s]);
+            } else {
+                tc::mbar_arrive(&full[s]);  // direct chunk: consumers read global memory
+            }
+        }
+        return;
+    }
+    const int cw = warp - 1, sl = lane % G;
+    for (int64_t c = c0; c < c1; ++c) {
+        const int64_t i = c - c0;
+        const int s = (int)(i % SPMV_STAGES);
+        tc::mbar_wait(&full[s], (uint32_t)((i / SPMV_STAGES) & 1));
+        const SpmvChunk ch = hdr[s];
+        const SpmvStage& st = stages[s];
+        const bool staged = ch.staged != 0;
+        const int64_t pa = ch.p_begin & ~3ll, pv = ch.p_begin & ~1ll, rr = ch.row_begin & ~1ll;
+        for (int64_t base = ch.row_begin + (int64_t)cw * RPW; base < ch.row_end; base += (int64_t)NCW * RPW) {
+            const int64_t row = base + lane / G;
+            const bool valid = row < ch.row_end;
+            int64_t p = 0, e = 0;
+            if (valid) {
+                if (staged) {
+                    p = st.rp[row - rr];
+                    e = st.rp[row + 1 - rr];
+                } else {
+                    p = row_ptr[row];
+                    e = row_ptr[row + 1];
+                }
+            }
+            p += sl;
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+            if (staged) {
+                for (; p + 3 * G < e; p += 4 * G) {
+                    const int32_t q0 = st.col[p - pa], q1 = st.col[p + G - pa], q2 = st.col[p + 2 * G - pa],
+                                  q3 = st.col[p + 3 * G - pa];
+                    a0 = fma(st.vals[p - pv], __ldg(x + q0), a0);
+                    a1 = fma(st.vals[p + G - pv], __ldg(x + q1), a1);
+                    a2 = fma(st.vals[p + 2 * G - pv], __ldg(x + q2), a2);
+                    a3 = fma(st.vals[p + 3 * G - pv], __ldg(x + q3), a3);
+                }
+                for (; p < e; p += G) a0 = fma(st.vals[p - pv], __ldg(x + st.col[p - pa]), a0);
+            } else {
+                for (; p < e; p += G) a0 = fma(__ldg(vals + p), __ldg(x + __ldg(col + p)), a0);
+            }
+            double acc = (a0 + a1) + (a2 + a3);
+#pragma unroll
+            for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, G);
+            if (valid && sl == 0) y[row] = acc;
+        }
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&empty[s]);
+    }
+}
+
+int SpmvPlan::build(int64_t n_, const int64_t* row_ptr_, const int32_t* col_, const double* vals_, cudaStream_t st) {
+    n = n_;
+    row_ptr = row_ptr_;
+    col = col_;
+    vals = vals_;
+    nnz = 0;
+    if (n > 0) {
+        SC_CUDA(cudaMemcpyAsync(&nnz, row_ptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        SC_CUDA(cudaStreamSynchronize(st));
+    }
+    nch = std::max<int64_t>(1, ceil_div(nnz, SPMV_CH));
+    int rc;
+    if ((rc = chunks.alloc(nch))) return rc;
+    if (n > 0) {
+        spmv_plan_kernel<<<(unsigned)ceil_div(nch, 256), 256, 0, st>>>(n, nnz, nch, row_ptr, chunks.p);
+        SC_LAUNCHED(1);
+    }
+    return SC_OK;
+}
+
+int SpmvPlan::apply(const double* x, double* y, cudaStream_t st) const {
+    if (n == 0) return SC_OK;
+    const double mean = (double)nnz / (double)n;
+    if (spmv_kind() != 9 || mean <= 8) return spmv_launch(n, nnz, row_ptr, col, vals, x, y, false, st);
+    ProfScope prof("spmv", st, (double)nnz * 12.0 + (double)(n + 1) * 8.0 + 2.0 * (double)n * 8.0);
+    const size_t smem = sizeof(SpmvStage) * SPMV_STAGES;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(spmv_bulk_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    const int64_t grid = std::min<int64_t>(kNumSMs, nch);
+    spmv_bulk_kernel<8><<<(unsigned)grid, SPMV_THREADS, smem, st>>>(n, nch, chunks.p, row_ptr, col, vals, x, y);
+    SC_LAUNCHED(1);
+    return SC_OK;
+}
+
+}  // namespace sc
+
+// ---- C ABI: SpMV plan handle (built once per operator, applied per matvec) --
+struct sc_spmv_plan {
+    sc::SpmvPlan p;
+};
+extern "C" int sc_spmv_plan_create(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* vals,
+                                   sc_stream_t stream, sc_spmv_plan** out) {
+    using namespace sc;
+    cudaStream_t st = as_stream(stream);
+    StreamScope stream_scope(st);
+    auto* h = new sc_spmv_plan();
+    if (int rc = h->p.build(n, row_ptr, col, vals, st)) {
+        delete h;
+        return rc;
+    }
+    *out = h;
+    return SC_OK;
+}
+extern "C" int sc_spmv_plan_apply(const sc_spmv_plan* h, const double* x, double* y, sc_stream_t stream) {
+    return h->p.apply(x, y, sc::as_stream(stream));
+}
+extern "C" void sc_spmv_plan_destroy(sc_spmv_plan* h) { delete h; }

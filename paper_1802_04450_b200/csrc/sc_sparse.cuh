@@ -10,6 +10,28 @@ int spmv_launch(int64_t n, int64_t nnz, const int64_t* row_ptr, const int32_t* c
 int degrees_launch(int64_t n, const int64_t* row_ptr, const double* vals, double* d,
                    cudaStream_t st);
 
+// Bulk-staged SpMV plan for an operator applied many times (the Lanczos
+// matvecs): the nonzeros are cut into chunks of ~SPMV_CH (whole rows; a chunk
+// holds the rows whose first nonzero falls in its window), one persistent CTA
+// per SM streams its contiguous run of chunks through a shared-memory ring
+// with cp.async.bulk while consumer warps gather x and reduce rows.  Chunks
+// that do not fit a stage (hub rows) are read straight from global memory.
+constexpr int64_t SPMV_CH = 2048;
+constexpr int SPMV_CAP = 3072, SPMV_RCAP = 192, SPMV_STAGES = 3, SPMV_THREADS = 512;
+struct SpmvChunk {
+    int64_t row_begin, row_end, p_begin, p_end;
+    int64_t staged;
+};
+struct SpmvPlan {
+    int64_t n = 0, nnz = 0, nch = 0;
+    const int64_t* row_ptr = nullptr;
+    const int32_t* col = nullptr;
+    const double* vals = nullptr;
+    DevBuf<SpmvChunk> chunks;
+    int build(int64_t n_, const int64_t* row_ptr, const int32_t* col, const double* vals, cudaStream_t st);
+    int apply(const double* x, double* y, cudaStream_t st) const;
+};
+
 // Sliced ELLPACK (SELL-32-sigma) copy of a CSR matrix for the eigensolver's
 // SpMV: rows are sorted by length (descending, stable) inside windows of
 // SELL_SIGMA consecutive rows, every 32 sorted rows form a slice stored

@@ -415,3 +415,51 @@ def test_sell_operator_ragged(n_rows, n_cols):
         lib.sc_sell_destroy(h)
     bound = 1e-13 * np.maximum(1.0, orc.spmv_seq(rp, col, np.abs(vals), np.abs(x)))
     assert np.all(np.abs(got - want) <= bound)
+
+
+def _ragged_csr(n_rows, n_cols, seed):
+    rng = np.random.default_rng(seed)
+    deg = rng.integers(0, 90, n_rows)
+    deg[rng.random(n_rows) < 0.02] = 0
+    hubs = rng.random(n_rows) < 0.003
+    deg[hubs] = rng.integers(300, 5000, int(hubs.sum()))
+    deg = np.minimum(deg, n_cols)
+    rp = np.concatenate(([0], np.cumsum(deg))).astype(np.int64)
+    col = np.concatenate([np.sort(rng.choice(n_cols, dd, replace=False)) for dd in deg]).astype(np.int64) \
+        if deg.sum() else np.zeros(0, np.int64)
+    vals = rng.standard_normal(col.size)
+    return rp, col, vals, rng.standard_normal(n_cols)
+
+
+@pytest.mark.parametrize("kernel", ["local", "vec", "affine", "pipe", "batch2", "batch4", "batch8", "bulk"])
+@pytest.mark.parametrize("n_rows,n_cols", [(60_001, 60_001), (5000, 5000), (1, 7), (20_000, 70_000)])
+def test_spmv_kernels_and_plan_ragged(monkeypatch, kernel, n_rows, n_cols):
+    """Every SpMV kernel variant, through sc_spmv_f64 and through an
+    sc_spmv_plan (bulk-staged chunks, hub rows read directly, a ragged tail
+    chunk), equals the sequential CSR sum up to reassociation, on rows from
+    empty to 5000 nonzeros and on a row shard with more columns than rows."""
+    import torch
+
+    from paper_1802_04450_b200 import _native as nat
+
+    monkeypatch.setenv("SPECLUST_SPMV_KERNEL", kernel)
+    rp, col, vals, x = _ragged_csr(n_rows, n_cols, n_rows + len(kernel))
+    m = sc.CsrMatrix(n_rows, n_cols, rp, col, vals).device()
+    want = orc.spmv_seq(rp, col, vals, x)
+    bound = 1e-13 * np.maximum(1.0, orc.spmv_seq(rp, col, np.abs(vals), np.abs(x)))
+    lib = nat.load()
+    xd = torch.from_numpy(x).cuda()
+    y = torch.full((n_rows,), np.nan, dtype=torch.float64, device="cuda")
+    nat.check(lib.sc_spmv_f64(n_rows, n_cols, nat.ptr(m.row_ptr), nat.ptr(m.col), nat.ptr(m.vals), nat.ptr(xd),
+                              nat.ptr(y), 0, nat.stream_handle()))
+    assert np.all(np.abs(y.cpu().numpy() - want) <= bound)
+    h = nat.vp()
+    nat.check(lib.sc_spmv_plan_create(n_rows, nat.ptr(m.row_ptr), nat.ptr(m.col), nat.ptr(m.vals),
+                                      nat.stream_handle(), nat.C.byref(h)))
+    try:
+        for _ in range(2):  # the plan is reusable
+            y.fill_(np.nan)
+            nat.check(lib.sc_spmv_plan_apply(h, nat.ptr(xd), nat.ptr(y), nat.stream_handle()))
+            assert np.all(np.abs(y.cpu().numpy() - want) <= bound)
+    finally:
+        lib.sc_spmv_plan_destroy(h)
