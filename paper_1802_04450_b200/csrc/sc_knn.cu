@@ -27,6 +27,7 @@
 #include "sc_common.cuh"
 #include "sc_knn.cuh"
 #include "sc_list.cuh"
+#include "sc_knn_tc2.cuh"
 #include "sc_knn_tc.cuh"
 #include "sc_scan.cuh"
 #include "sc_sparse.cuh"
@@ -559,9 +560,12 @@ static int launch_tc(const CUtensorMap& map, int64_t n, int64_t ntiles, int64_t 
         std::vector<long long> h((size_t)nq * 16);
         SC_CUDA(cudaMemcpyAsync(h.data(), dbg.p, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, st));
         SC_CUDA(cudaStreamSynchronize(st));
-        double acc[12] = {0};
+        double acc[16] = {0};
         for (int64_t b = 0; b < nq; ++b)
-            for (int q = 0; q < 12; ++q) acc[q] += (double)h[b * 16 + q];
+            for (int q = 0; q < 16; ++q) acc[q] += (double)h[b * 16 + q];
+        fprintf(stderr, "[knn_tc dbg] warp2 per tile: fired halves %.4f, quarters %.4f, appends/row %.2f (total), "
+                        "compactions/row %.2f (total)\n",
+                acc[12] / nq / ntiles, acc[15] / nq / ntiles, acc[13] / nq / 32, acc[14] / nq / 32);
         const char* names[12] = {"tma.wait_empty", "-", "-", "tma.total", "mma.wait_tempty", "mma.wait_full",
                                  "mma.latency64", "mma.total", "epi.wait_tfull", "epi.ldtm", "epi.work", "epi.fast"};
         for (int q = 0; q < 12; ++q)
@@ -570,6 +574,43 @@ static int launch_tc(const CUtensorMap& map, int64_t n, int64_t ntiles, int64_t 
                         q == 6 ? acc[q] / nq / 64 : acc[q] / nq / ntiles);
     }
     return SC_OK;
+}
+
+template <int NKB, int STAGES, int WMODE>
+static int launch_tc2_w(const CUtensorMap& map, int64_t n, int64_t ntiles, int64_t qtile0, int64_t nq, const float* cnk,
+                        float key_scale, int cap, int R, float2* lists, int* counts, float* taus, cudaStream_t st) {
+    // at least 114 KB so that exactly one CTA (holding all 512 TMEM columns) fits an SM
+    const uint32_t smem = std::max<uint32_t>(Tc2Layout<NKB, STAGES>::total, 116u * 1024u);
+    SC_CUDA(cudaFuncSetAttribute(knn_cand_tc2_kernel<NKB, STAGES, WMODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    const int64_t grid = ceil_div(nq, 2);
+    knn_cand_tc2_kernel<NKB, STAGES, WMODE><<<(unsigned)grid, TC2_THREADS, smem, st>>>(
+        map, n, ntiles, qtile0, nq, cnk, key_scale, cap, R, lists, counts, taus);
+    SC_LAUNCHED(1);
+    return SC_OK;
+}
+// WMODE bit 0: producer / MMA waits with a suspend hint; bit 1: epilogue waits
+// with it; bits 2-4 are profiling switches (skip epilogue / MMA / list path:
+// SPECLUST_KNN_WAIT=7, 11, 15, 19, 27 with SPECLUST_KNN_TILE_ONLY=1, results
+// invalid) used to separate the MMA, epilogue and list-maintenance costs
+template <int NKB, int STAGES>
+static int launch_tc2(const CUtensorMap& map, int64_t n, int64_t ntiles, int64_t qtile0, int64_t nq, const float* cnk,
+                      float key_scale, int cap, int R, float2* lists, int* counts, float* taus, cudaStream_t st) {
+    const char* wenv = std::getenv("SPECLUST_KNN_WAIT");
+    const int w = wenv ? std::atoi(wenv) : 3;
+#define SC_TC2(W) \
+    case W: return launch_tc2_w<NKB, STAGES, W>(map, n, ntiles, qtile0, nq, cnk, key_scale, cap, R, lists, counts, taus, st)
+    switch (w) {
+        SC_TC2(0);
+        SC_TC2(7);
+        SC_TC2(11);
+        SC_TC2(15);
+        SC_TC2(19);
+        SC_TC2(27);
+        default: return launch_tc2_w<NKB, STAGES, 3>(map, n, ntiles, qtile0, nq, cnk, key_scale, cap, R, lists, counts,
+                                                     taus, st);
+    }
+#undef SC_TC2
 }
 
 // tensor-core candidate lists: query tiles [qtile0, qtile0 + nq) against every
@@ -590,6 +631,13 @@ int knn_candidates_tc(int64_t n, int64_t n_pad, int64_t dp64, const __half* xh, 
     if (cr != CUDA_SUCCESS) return fail(SC_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
     const int64_t ntiles = n_pad / 128;
     ProfScope prof("knn_tile", st, 2.0 * (double)imin64(n, nq * 128) * (double)n * (double)dp64);
+    // query-pair kernel for d <= 128 (SPECLUST_KNN_TC=1 selects the one-tile kernel)
+    const char* tenv = std::getenv("SPECLUST_KNN_TC");
+    if (!(tenv && std::strcmp(tenv, "1") == 0) && dp64 <= 128) {
+        if (dp64 == 64)
+            return launch_tc2<1, 6>(map, n, ntiles, qtile0, nq, cnk, key_scale, cap, R, lists, counts, taus, st);
+        return launch_tc2<2, 3>(map, n, ntiles, qtile0, nq, cnk, key_scale, cap, R, lists, counts, taus, st);
+    }
     switch (dp64 / 64) {
         case 1: return launch_tc<1, 4, false>(map, n, ntiles, qtile0, nq, cnk, key_scale, cap, R, lists, counts, taus, st);
         case 2: return launch_tc<2, 3, false>(map, n, ntiles, qtile0, nq, cnk, key_scale, cap, R, lists, counts, taus, st);
@@ -732,6 +780,8 @@ int knn_select(int64_t n, int64_t d, const double* x, int64_t knn, double two_si
         if ((rc = knn_candidates_tc(n, n_pad, dp64, xh.p, cnf.p, (float)(-2.0 / (scale * scale)), qtile0, nq, cap, R,
                                     lists.p, counts.p, taus.p, st)))
             return rc;
+        if (std::getenv("SPECLUST_KNN_TILE_ONLY"))  // profiling: stop after the candidate kernel
+            return fail(SC_ERR_VALUE, "SPECLUST_KNN_TILE_ONLY set");
         // fp16 rounding of both operands (u = 2^-11) + fp32 accumulation of
         // dp64 products + fp32 rounding of |x_j|^2 and of the key, relative to
         // (|x_i| + |x_j|)^2; 10% slack on top.

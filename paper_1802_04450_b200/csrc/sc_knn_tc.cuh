@@ -72,6 +72,7 @@ __global__ void __launch_bounds__(TC_THREADS, LSMEM ? 1 : 2)
                        int* __restrict__ counts, float* __restrict__ taus, long long* __restrict__ dbg) {
     using Lay = TcLayout<NKB, STAGES, LSMEM>;
     long long d_wait0 = 0, d_wait1 = 0, d_work = 0, d_fast = 0, d_t0 = clock64();
+    long long n_fire = 0, n_app = 0, n_comp = 0, n_quart = 0;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = base;
@@ -212,6 +213,7 @@ __global__ void __launch_bounds__(TC_THREADS, LSMEM ? 1 : 2)
                 const bool any = __any_sync(0xffffffffu, valid && fminf(m0, m1) < tau);
                 d_fast += clock64() - h1;
                 if (!any) continue;
+                ++n_fire;
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const int c = half * 64 + q * 16;
@@ -223,6 +225,8 @@ __global__ void __launch_bounds__(TC_THREADS, LSMEM ? 1 : 2)
                     // make room: warp-cooperative compaction of every list
                     // that could overflow while taking this chunk
                     unsigned want = __ballot_sync(0xffffffffu, pass && cnt > cap - 16);
+                    n_quart += __any_sync(0xffffffffu, pass);
+                    n_comp += __popc(want);
                     while (want) {
                         __syncwarp();  // make lane src's appends visible
                         const int src = __ffs(want) - 1;
@@ -252,8 +256,10 @@ __global__ void __launch_bounds__(TC_THREADS, LSMEM ? 1 : 2)
 #pragma unroll
                         for (int u = 0; u < 16; ++u) {
                             const int64_t col = col0 + c + u;
-                            if (keys[u] < tau && col != row && col < n)
+                            if (keys[u] < tau && col != row && col < n) {
                                 L[cnt++] = make_float2(keys[u], __int_as_float((int)col));
+                                ++n_app;
+                            }
                         }
                     }
                 }
@@ -278,6 +284,16 @@ __global__ void __launch_bounds__(TC_THREADS, LSMEM ? 1 : 2)
         o[1] = d_wait1;
         o[2] = d_work;
         o[3] = warp == 2 ? d_fast : clock64() - d_t0;
+    }
+    if (dbg && warp == 2) {
+        const long long a = warp_sum_i64(n_app);
+        if (lane == 0) {
+            long long* o = dbg + (size_t)blockIdx.x * 16;
+            o[12] = n_fire;
+            o[13] = a;
+            o[14] = n_comp;
+            o[15] = n_quart;
+        }
     }
     __syncthreads();
     if (warp == 1) {

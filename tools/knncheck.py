@@ -1,5 +1,5 @@
 import sys, numpy as np, torch
-sys.path.insert(0, '.')
+sys.path.insert(0, __import__('os').path.dirname(__import__('os').path.dirname(__import__('os').path.abspath(__file__))))
 import paper_1802_04450_b200 as sc
 from paper_1802_04450_b200.graph import knn_graph_device
 from oracle import speclust_oracle as orc
