@@ -576,19 +576,24 @@ static int launch_tc(const CUtensorMap& map, int64_t n, int64_t ntiles, int64_t 
     return SC_OK;
 }
 
-template <int NKB, int STAGES, int WMODE>
+static uint32_t tc2_heap_bytes(int R) { return 16 + 256u * (uint32_t)R * 8u + 8u * 32u * 16u * 4u; }
+
+template <int NKB, int STAGES, int WMODE, bool HEAP>
 static int launch_tc2_w(const CUtensorMap& map, int64_t n, int64_t ntiles, int64_t qtile0, int64_t nq, const float* cnk,
                         float key_scale, int cap, int R, float2* lists, int* counts, float* taus, cudaStream_t st) {
-    // at least 114 KB so that exactly one CTA (holding all 512 TMEM columns) fits an SM
-    const uint32_t smem = std::max<uint32_t>(Tc2Layout<NKB, STAGES>::total, 116u * 1024u);
-    SC_CUDA(cudaFuncSetAttribute(knn_cand_tc2_kernel<NKB, STAGES, WMODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
     const int64_t grid = ceil_div(nq, 2);
-    knn_cand_tc2_kernel<NKB, STAGES, WMODE><<<(unsigned)grid, TC2_THREADS, smem, st>>>(
+    // heap variant: + per-row heaps; list variant: at least 114 KB so that
+    // exactly one CTA (holding all 512 TMEM columns) fits an SM
+    const uint32_t smem = HEAP ? Tc2Layout<NKB, STAGES>::total + tc2_heap_bytes(R)
+                               : std::max<uint32_t>(Tc2Layout<NKB, STAGES>::total, 116u * 1024u);
+    SC_CUDA(cudaFuncSetAttribute(knn_cand_tc2_kernel<NKB, STAGES, WMODE, HEAP>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    knn_cand_tc2_kernel<NKB, STAGES, WMODE, HEAP><<<(unsigned)grid, TC2_THREADS, smem, st>>>(
         map, n, ntiles, qtile0, nq, cnk, key_scale, cap, R, lists, counts, taus);
     SC_LAUNCHED(1);
     return SC_OK;
 }
+
 // WMODE bit 0: producer / MMA waits with a suspend hint; bit 1: epilogue waits
 // with it; bits 2-4 are profiling switches (skip epilogue / MMA / list path:
 // SPECLUST_KNN_WAIT=7, 11, 15, 19, 27 with SPECLUST_KNN_TILE_ONLY=1, results
@@ -598,8 +603,24 @@ static int launch_tc2(const CUtensorMap& map, int64_t n, int64_t ntiles, int64_t
                       float key_scale, int cap, int R, float2* lists, int* counts, float* taus, cudaStream_t st) {
     const char* wenv = std::getenv("SPECLUST_KNN_WAIT");
     const int w = wenv ? std::atoi(wenv) : 3;
+    // opt-in (SPECLUST_KNN_HEAP=1): candidate lists as shared-memory max-heaps
+    // (d <= 64: the 256 x R heaps fit beside a 3- or 2-deep operand ring).
+    // Measured at C2 it is slower than the global lists with warp compaction
+    // (319 vs 271 ms: each replacement is a chain of ~6 dependent shared loads
+    // on the inserting lane while its warp waits), so it is off by default.
+    const char* henv = std::getenv("SPECLUST_KNN_HEAP");
+    const bool heap_ok = NKB == 1 && henv && std::strcmp(henv, "1") == 0;
+    constexpr uint32_t kMax = 227u * 1024u;
+    if (heap_ok && w == 3) {
+        if (Tc2Layout<NKB, 3>::total + tc2_heap_bytes(R) <= kMax)
+            return launch_tc2_w<NKB, 3, 3, true>(map, n, ntiles, qtile0, nq, cnk, key_scale, cap, R, lists, counts,
+                                                 taus, st);
+        if (Tc2Layout<NKB, 2>::total + tc2_heap_bytes(R) <= kMax)
+            return launch_tc2_w<NKB, 2, 3, true>(map, n, ntiles, qtile0, nq, cnk, key_scale, cap, R, lists, counts,
+                                                 taus, st);
+    }
 #define SC_TC2(W) \
-    case W: return launch_tc2_w<NKB, STAGES, W>(map, n, ntiles, qtile0, nq, cnk, key_scale, cap, R, lists, counts, taus, st)
+    case W: return launch_tc2_w<NKB, STAGES, W, false>(map, n, ntiles, qtile0, nq, cnk, key_scale, cap, R, lists, counts, taus, st)
     switch (w) {
         SC_TC2(0);
         SC_TC2(7);
@@ -607,8 +628,8 @@ static int launch_tc2(const CUtensorMap& map, int64_t n, int64_t ntiles, int64_t
         SC_TC2(15);
         SC_TC2(19);
         SC_TC2(27);
-        default: return launch_tc2_w<NKB, STAGES, 3>(map, n, ntiles, qtile0, nq, cnk, key_scale, cap, R, lists, counts,
-                                                     taus, st);
+        default: return launch_tc2_w<NKB, STAGES, 3, false>(map, n, ntiles, qtile0, nq, cnk, key_scale, cap, R, lists,
+                                                            counts, taus, st);
     }
 #undef SC_TC2
 }

@@ -112,7 +112,7 @@ __device__ __forceinline__ int64_t scan_tile(int64_t qt0, int64_t t, int64_t nti
 }
 __device__ __forceinline__ float fmin3(float a, float b, float c) { return fminf(a, fminf(b, c)); }
 
-template <int NKB, int STAGES, int WMODE>
+template <int NKB, int STAGES, int WMODE, bool HEAP>
 __global__ void __launch_bounds__(TC2_THREADS, 1)
     knn_cand_tc2_kernel(const __grid_constant__ CUtensorMap xmap, int64_t n, int64_t ntiles, int64_t qtile0,
                         int64_t nq, const float* __restrict__ cnk, float key_scale, int cap, int R,
@@ -132,6 +132,10 @@ __global__ void __launch_bounds__(TC2_THREADS, 1)
     uint64_t* cfull = tempty + 2;                // [TC2_CN_RING]
     uint64_t* cempty = cfull + TC2_CN_RING;      // [TC2_CN_RING]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cempty + TC2_CN_RING);
+    // HEAP: per-row max-heaps of the R best candidates (256 x R float2) and a
+    // 16-key staging slot per epilogue thread, after the barriers
+    float2* sH = reinterpret_cast<float2*>(reinterpret_cast<uintptr_t>(tmem_slot + 4 + 15) & ~uintptr_t(15));
+    float* sStage = reinterpret_cast<float*>(sH + (HEAP ? 256 * R : 0));
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // query tiles qt0, qt0 + 1 (scan positions); list slots relative to qtile0
@@ -220,8 +224,38 @@ __global__ void __launch_bounds__(TC2_THREADS, 1)
         const int64_t slot = lq0 * 128 + lrow;  // list slot of this row
         float2* L = lists + (valid ? slot : 0) * (int64_t)cap;
         float2* scratch = sL + (size_t)(warp - 2) * TC_LIST_P;
+        float2* H = sH + (size_t)lrow * R;
+        float* stage = sStage + ((size_t)(warp - 2) * 32 + lane) * 16;
         int cnt = 0;
         float tau = INFINITY;
+        // max-heap on the key: sift `e` down from slot i
+        auto sift_down = [&](int i, float2 e) {
+            while (true) {
+                const int l = 2 * i + 1;
+                if (l >= R) break;
+                int c = l;
+                if (l + 1 < R && H[l + 1].x > H[l].x) c = l + 1;
+                const float2 hc = H[c];
+                if (hc.x <= e.x) break;
+                H[i] = hc;
+                i = c;
+            }
+            H[i] = e;
+        };
+        // keep the R smallest keys: fill, heapify once full, then replace the max
+        auto heap_push = [&](float k, int64_t col) {
+            const float2 e = make_float2(k, __int_as_float((int)col));
+            if (cnt < R) {
+                H[cnt++] = e;
+                if (cnt == R) {
+                    for (int i = R / 2 - 1; i >= 0; --i) sift_down(i, H[i]);
+                    tau = H[0].x;
+                }
+            } else {
+                sift_down(0, e);
+                tau = H[0].x;
+            }
+        };
         const float2 ks = make_float2(key_scale, key_scale);
         for (int64_t t = 0; t < ntiles; ++t) {
             const int buf = (int)(t & 1);
@@ -304,8 +338,35 @@ __global__ void __launch_bounds__(TC2_THREADS, 1)
                     }
                 }
             };
-            if (!(WMODE & 16) && __any_sync(0xffffffffu, valid && h0 < tau)) slow(v, qm, col0);
-            if (!(WMODE & 16) && __any_sync(0xffffffffu, valid && h1 < tau)) slow(v + 64, qm + 4, col0 + 64);
+            // heap variant: every row owns its heap, so lanes proceed
+            // independently; the passing 16-key quarter is staged in shared
+            // memory and walked by a rolled loop (small code, no register
+            // indexing)
+            auto slow_heap = [&](const float* keys64, const float* qm4, int64_t cbase) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (!(valid && qm4[q] < tau)) continue;
+                    float4* st4 = reinterpret_cast<float4*>(stage);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        st4[u] = make_float4(keys64[16 * q + 4 * u], keys64[16 * q + 4 * u + 1],
+                                             keys64[16 * q + 4 * u + 2], keys64[16 * q + 4 * u + 3]);
+                    const int64_t cb = cbase + q * 16;
+#pragma unroll 1
+                    for (int u = 0; u < 16; ++u) {
+                        const float k = stage[u];
+                        const int64_t col = cb + u;
+                        if (k < tau && col != row && col < n) heap_push(k, col);
+                    }
+                }
+            };
+            if (HEAP) {
+                if (!(WMODE & 16) && __any_sync(0xffffffffu, valid && h0 < tau)) slow_heap(v, qm, col0);
+                if (!(WMODE & 16) && __any_sync(0xffffffffu, valid && h1 < tau)) slow_heap(v + 64, qm + 4, col0 + 64);
+            } else {
+                if (!(WMODE & 16) && __any_sync(0xffffffffu, valid && h0 < tau)) slow(v, qm, col0);
+                if (!(WMODE & 16) && __any_sync(0xffffffffu, valid && h1 < tau)) slow(v + 64, qm + 4, col0 + 64);
+            }
             tc::fence_before();
             __syncwarp();
             if (lane == 0) {
@@ -314,6 +375,8 @@ __global__ void __launch_bounds__(TC2_THREADS, 1)
             }
         }
         if (valid) {
+            if (HEAP)
+                for (int e = 0; e < cnt; ++e) L[e] = H[e];
             counts[slot] = cnt;
             taus[slot] = tau;
         }
