@@ -463,3 +463,37 @@ def test_spmv_kernels_and_plan_ragged(monkeypatch, kernel, n_rows, n_cols):
             assert np.all(np.abs(y.cpu().numpy() - want) <= bound)
     finally:
         lib.sc_spmv_plan_destroy(h)
+
+
+_VARIANT_CASES = []
+
+
+def _variant_cases():
+    """Blobs cases + their oracle CSR, computed once for all variants."""
+    if not _VARIANT_CASES:
+        rng = np.random.default_rng(17)
+        for n, d, knn in [(6000, 32, 16), (5000, 64, 32), (4500, 100, 10)]:
+            centers = rng.normal(0.0, 0.7, (12, d))
+            x = centers[rng.integers(0, 12, n)] + rng.standard_normal((n, d))
+            sigma = float(np.sqrt(d))
+            e = orc.knn_edges(x, knn, sigma)
+            _VARIANT_CASES.append((x, knn, sigma, orc.csr_from_edges(n, e, orc.edge_weights(x, e, sigma))))
+    return _VARIANT_CASES
+
+
+@pytest.mark.parametrize("variant", [{}, {"SPECLUST_KNN_TC": "1"}, {"SPECLUST_KNN_HEAP": "1"},
+                                     {"SPECLUST_KNN_KERNEL": "simt"}, {"SPECLUST_KNN_NOTOUR": "1"}])
+def test_knn_kernel_variants_match_oracle(monkeypatch, variant):
+    """Every candidate-kernel variant (query-pair tcgen05 kernel with global
+    lists or shared heaps, the one-tile tcgen05 kernel, the SIMT kernel, the
+    untoured pivot order) yields the reference CSR bit-for-bit on blobs large
+    enough for the locality order (n >= 4096), for d = 32, 64 and 100."""
+    from paper_1802_04450_b200.graph import knn_graph_device
+
+    for k_, v_ in variant.items():
+        monkeypatch.setenv(k_, v_)
+    for x, knn, sigma, want in _variant_cases():
+        w = knn_graph_device(x, knn, sc.SimilarityMeasure.exp_decay(sigma)).to_host()
+        assert np.array_equal(w.row_ptr, want[0]), (x.shape, knn)
+        assert np.array_equal(w.col_idx, want[1]), (x.shape, knn)
+        assert_ulp(w.vals, want[2], 2)
