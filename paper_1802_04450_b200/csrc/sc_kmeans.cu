@@ -8,6 +8,9 @@
 //   the rows with the largest current cost (stable: ties -> lower index).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "sc_common.cuh"
@@ -758,6 +761,226 @@ int assign_nearest(int64_t n, int64_t d, const double* v, int64_t k, const doubl
 
 }  // namespace sc
 
+// ---------------------------------------------------------------------------
+// Tensor-core assignment with certified argmin (sc_assign_tc.cuh)
+#include "sc_assign_tc.cuh"
+#include "sc_tma.cuh"
+
+namespace sc {
+
+__global__ void as_absmax_kernel(int64_t m, const double* __restrict__ x, unsigned long long* __restrict__ out) {
+    double a = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        a = fmax(a, fabs(x[i]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a = fmax(a, __shfl_xor_sync(0xffffffffu, a, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(a));
+}
+
+// rows x dp fp16 copy of s * x (zero padding), warp per row
+__global__ void as_prep_rows_kernel(int64_t rows, int64_t rows_pad, int64_t d, int64_t dp, const double* __restrict__ x,
+                                    double s, __half* __restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    if (i >= rows_pad) return;
+    for (int64_t l = lane; l < dp; l += 32)
+        out[i * dp + l] = __double2half(i < rows && l < d ? s * x[i * d + l] : 0.0);
+}
+
+// centroid norms for the keys (fp32, +inf on padding) and max |c|^2
+__global__ void as_cent_norms_kernel(int64_t k, int64_t k_pad, const double* __restrict__ cn, float* __restrict__ cnk,
+                                     unsigned long long* __restrict__ cnmax) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= k_pad) return;
+    cnk[c] = c < k ? (float)cn[c] : INFINITY;
+    if (c < k) atomicMax(cnmax, (unsigned long long)__double_as_longlong(cn[c]));
+}
+
+// exact S(v_i, c) in the reference's order (kmeans.py:92-98), clamped at 0
+__device__ __forceinline__ double exact_s(const double* __restrict__ vi, double vni, const double* __restrict__ cc,
+                                          double cnc, int64_t d) {
+    NpDot s;
+    np_dot_span(s, 0, d, [&](int64_t l) { return __dmul_rn(vi[l], cc[l]); });
+    const double r = __dsub_rn(__dadd_rn(vni, cnc), __dmul_rn(2.0, s.result()));
+    return r > 0.0 ? r : 0.0;
+}
+
+// certified rows: label = best, exact cost; others are listed for the rescan.
+// delta_i bounds |approx key - exact key| for row i (fp16 operands, fp32
+// accumulation of dp products, fp32 norms and FMA, fp16 subnormals):
+//   delta_i = 1.25 * ( 2 (2^-10 + (dp+1) 2^-24) |v_i| cmax
+//                      + 2^-24 (2 cnmax + 2 |v_i| cmax)
+//                      + 2^-24 sqrt(dp) (|v_i| + cmax) / s )
+__global__ void as_finalize_kernel(int64_t n, int64_t d, int64_t dp, double s, const double* __restrict__ v,
+                                   const double* __restrict__ vn, const double* __restrict__ c,
+                                   const double* __restrict__ cn, const unsigned long long* __restrict__ cnmax_bits,
+                                   const int32_t* __restrict__ best_idx, const float2* __restrict__ best_keys,
+                                   const int64_t* __restrict__ old_labels, int64_t* __restrict__ labels,
+                                   double* __restrict__ cost, int32_t* __restrict__ flagged,
+                                   unsigned long long* __restrict__ nflag, unsigned long long* __restrict__ changes) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int chg = 0;
+    if (i < n) {
+        const double cnmax = __longlong_as_double((long long)*cnmax_bits);
+        const double cmax = sqrt(cnmax);
+        const double va = sqrt(vn[i]);
+        const double delta = 1.25 * (2.0 * (0x1p-10 + (double)(dp + 1) * 0x1p-24) * va * cmax +
+                                     0x1p-24 * (2.0 * cnmax + 2.0 * va * cmax) +
+                                     0x1p-24 * sqrt((double)dp) * (va + cmax) / s);
+        const float2 bk = best_keys[i];
+        const int32_t b = best_idx[i];
+        if (b >= 0 && (double)bk.y - (double)bk.x > 2.0 * delta) {
+            labels[i] = b;
+            cost[i] = exact_s(v + i * d, vn[i], c + (int64_t)b * d, cn[b], d);
+            if (old_labels) chg = old_labels[i] != b;
+        } else {
+            flagged[atomicAdd(nflag, 1ull)] = (int32_t)i;
+        }
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, chg);
+    if ((threadIdx.x & 31) == 0 && bal) atomicAdd(changes, (unsigned long long)__popc(bal));
+}
+
+// flagged rows: exact scan over all centroids (warp per row, lowest index on ties)
+__global__ void as_rescan_kernel(int64_t d, int64_t k, const double* __restrict__ v, const double* __restrict__ vn,
+                                 const double* __restrict__ c, const double* __restrict__ cn,
+                                 const int32_t* __restrict__ flagged, const unsigned long long* __restrict__ nflag,
+                                 const int64_t* __restrict__ old_labels, int64_t* __restrict__ labels,
+                                 double* __restrict__ cost, unsigned long long* __restrict__ changes) {
+    const int64_t nf = (int64_t)*nflag;
+    const int lane = threadIdx.x & 31;
+    for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nf;
+         w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t i = flagged[w];
+        double best = INFINITY;
+        int64_t arg = 0;
+        for (int64_t q = lane; q < k; q += 32) {
+            const double sv = exact_s(v + i * d, vn[i], c + q * d, cn[q], d);
+            if (sv < best) {
+                best = sv;
+                arg = q;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const int64_t oa = __shfl_xor_sync(0xffffffffu, arg, o);
+            if (ob < best || (ob == best && oa < arg)) {
+                best = ob;
+                arg = oa;
+            }
+        }
+        if (lane == 0) {
+            labels[i] = arg;
+            cost[i] = best;
+            if (old_labels && old_labels[i] != arg) atomicAdd(changes, 1ull);
+        }
+    }
+}
+
+// part[b] = cost[64 b] + ... + cost[64 b + 63], sequential (the same fixed
+// order as dist_tile_kernel's per-block sum, so the SSE is path-independent)
+__global__ void cost_block_sum_kernel(int64_t n, const double* __restrict__ cost, double* __restrict__ part) {
+    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b * TP >= n) return;
+    double acc = 0.0;
+    for (int64_t i = b * TP; i < imin64(n, (b + 1) * TP); ++i) acc += cost[i];
+    part[b] = acc;
+}
+
+template <int NKB, int STAGES, int QT>
+static int launch_assign_tc(const CUtensorMap& vmap, const CUtensorMap& cmap, int64_t n, int64_t nptiles,
+                            int64_t nctiles, const float* cnk, float key_scale, int32_t* best_idx, float2* best_keys,
+                            cudaStream_t st) {
+    const uint32_t smem = AsLayout<NKB, STAGES, QT>::total;
+    SC_CUDA(cudaFuncSetAttribute(assign_tc_kernel<NKB, STAGES, QT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    assign_tc_kernel<NKB, STAGES, QT><<<(unsigned)ceil_div(nptiles, QT), 64 + QT * 128, smem, st>>>(
+        vmap, cmap, n, nptiles, nctiles, cnk, key_scale, best_idx, best_keys);
+    SC_LAUNCHED(1);
+    return SC_OK;
+}
+
+// Per-lloyd-call state of the tensor-core assignment (V converted once).
+struct AssignTc {
+    int64_t n = 0, d = 0, dp = 0, n_pad = 0;
+    double s = 1.0;
+    bool active = false;
+    DevBuf<__half> vh;
+    CUtensorMap vmap;
+    DevBuf<int32_t> bidx, flagged;
+    DevBuf<float2> bkeys;
+    DevBuf<unsigned long long> scal;  // [0] nflag, [1] cnmax bits, [2] absmax bits
+    // eligible: d <= 256, enough rows to pay for the conversion; SPECLUST_ASSIGN=fp64 disables
+    int init(int64_t n_, int64_t d_, int64_t k, const double* v, cudaStream_t st) {
+        n = n_;
+        d = d_;
+        dp = (d + 63) / 64 * 64;
+        const char* env = std::getenv("SPECLUST_ASSIGN");
+        active = !(env && std::strcmp(env, "fp64") == 0) && d >= 1 && dp <= 256 && n >= 4096 && k >= 8;
+        if (!active) return SC_OK;
+        n_pad = (n + 127) / 128 * 128;
+        int rc;
+        if ((rc = vh.alloc((size_t)n_pad * dp)) || (rc = bidx.alloc(n)) || (rc = bkeys.alloc(n)) ||
+            (rc = flagged.alloc(n)) || (rc = scal.alloc(3)))
+            return rc;
+        SC_CUDA(cudaMemsetAsync(scal.p, 0, sizeof(unsigned long long) * 3, st));
+        as_absmax_kernel<<<kNumSMs * 4, 256, 0, st>>>(n * d, v, scal.p + 2);
+        SC_LAUNCHED(1);
+        unsigned long long hb = 0;
+        SC_CUDA(cudaMemcpyAsync(&hb, scal.p + 2, sizeof(hb), cudaMemcpyDeviceToHost, st));
+        SC_CUDA(cudaStreamSynchronize(st));
+        double amax;
+        std::memcpy(&amax, &hb, sizeof(amax));
+        // power-of-two scale: |s x| <= 128 for every element of V (centroids
+        // are means / copies of rows, so the same bound holds for them)
+        s = amax > 0 ? std::ldexp(1.0, (int)std::floor(std::log2(128.0 / amax))) : 1.0;
+        as_prep_rows_kernel<<<(unsigned)ceil_div(n_pad, 8), 256, 0, st>>>(n, n_pad, d, dp, v, s, vh.p);
+        SC_LAUNCHED(1);
+        return make_f16_tile_map(&vmap, vh.p, n_pad, dp);
+    }
+    // labels / cost / change count of one assignment step
+    int assign(int64_t k, const double* v, const double* vn, const double* c, const double* cn,
+               const int64_t* old_labels, int64_t* labels, double* cost, unsigned long long* changes,
+               cudaStream_t st) {
+        const int64_t k_pad = (k + 127) / 128 * 128;
+        DevBuf<__half> ch;
+        DevBuf<float> cnk;
+        int rc;
+        if ((rc = ch.alloc((size_t)k_pad * dp)) || (rc = cnk.alloc(k_pad))) return rc;
+        SC_CUDA(cudaMemsetAsync(scal.p, 0, sizeof(unsigned long long) * 2, st));
+        as_prep_rows_kernel<<<(unsigned)ceil_div(k_pad, 8), 256, 0, st>>>(k, k_pad, d, dp, c, s, ch.p);
+        as_cent_norms_kernel<<<(unsigned)ceil_div(k_pad, 256), 256, 0, st>>>(k, k_pad, cn, cnk.p, scal.p + 1);
+        SC_LAUNCHED(2);
+        CUtensorMap cmap;
+        if ((rc = make_f16_tile_map(&cmap, ch.p, k_pad, dp))) return rc;
+        const int64_t nptiles = n_pad / 128, nctiles = k_pad / 128;
+        const float key_scale = (float)(-2.0 / (s * s));
+        switch (dp / 64) {
+            case 1: rc = launch_assign_tc<1, 4, 2>(vmap, cmap, n, nptiles, nctiles, cnk.p, key_scale, bidx.p, bkeys.p, st); break;
+            case 2: rc = launch_assign_tc<2, 3, 2>(vmap, cmap, n, nptiles, nctiles, cnk.p, key_scale, bidx.p, bkeys.p, st); break;
+            case 3: rc = launch_assign_tc<3, 2, 2>(vmap, cmap, n, nptiles, nctiles, cnk.p, key_scale, bidx.p, bkeys.p, st); break;
+            default: rc = launch_assign_tc<4, 2, 1>(vmap, cmap, n, nptiles, nctiles, cnk.p, key_scale, bidx.p, bkeys.p, st); break;
+        }
+        if (rc) return rc;
+        as_finalize_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, d, dp, s, v, vn, c, cn, scal.p + 1, bidx.p,
+                                                                        bkeys.p, old_labels, labels, cost, flagged.p,
+                                                                        scal.p, changes);
+        as_rescan_kernel<<<kNumSMs * 4, 256, 0, st>>>(d, k, v, vn, c, cn, flagged.p, scal.p, old_labels, labels, cost,
+                                                      changes);
+        SC_LAUNCHED(2);
+        return SC_OK;
+    }
+    int64_t flagged_count(cudaStream_t st) {
+        unsigned long long h = 0;
+        cudaMemcpyAsync(&h, scal.p, sizeof(h), cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        return (int64_t)h;
+    }
+};
+
+}  // namespace sc
+
 using namespace sc;
 
 // ---------------------------------------------------------------------------
@@ -818,13 +1041,29 @@ int sc_lloyd(int64_t n, int64_t d, int64_t k, const double* v, const double* c_i
     rownorm_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, d, v, vn.p);
     rownorm_kernel<<<(unsigned)ceil_div(k, 256), 256, 0, st>>>(k, d, centroids, cn.p);
     double flops = 2.0 * (double)n * (double)k * (double)d;
-    {
+    // tensor-core assignment with certified argmin when eligible (d <= 256)
+    AssignTc atc;
+    if ((rc = atc.init(n, d, k, v, st))) return rc;
+    auto assign_step = [&](const int64_t* old_lab, int64_t* out_lab) -> int {
         ProfScope prof("kmeans_assign", st, flops);
-        dist_tile_kernel<0><<<(unsigned)nb, 256, 0, st>>>(n, k, d, v, vn.p, centroids, cn.p, nullptr, labels,
-                                                          nullptr, cost.p, changes.p, part.p);
-    }
+        if (atc.active) {
+            int r = atc.assign(k, v, vn.p, centroids, cn.p, old_lab, out_lab, cost.p, changes.p, st);
+            if (r) return r;
+            if (std::getenv("SPECLUST_ASSIGN_DEBUG"))
+                fprintf(stderr, "[assign_tc] n=%lld k=%lld d=%lld rescanned rows %lld\n", (long long)n, (long long)k,
+                        (long long)d, (long long)atc.flagged_count(st));
+            cost_block_sum_kernel<<<(unsigned)ceil_div(nb, 256), 256, 0, st>>>(n, cost.p, part.p);
+        } else {
+            dist_tile_kernel<0><<<(unsigned)nb, 256, 0, st>>>(n, k, d, v, vn.p, centroids, cn.p, nullptr, out_lab,
+                                                              old_lab, cost.p, changes.p, part.p);
+        }
+        SC_LAUNCHED(1);
+        return SC_OK;
+    };
+    SC_LAUNCHED(2);
+    if ((rc = assign_step(nullptr, labels))) return rc;
     sum_partials_kernel<<<1, 1024, 0, st>>>(nb, part.p, sse.p);
-    SC_LAUNCHED(4);
+    SC_LAUNCHED(1);
     SC_CUDA(cudaMemcpyAsync(&sse_history[0], sse.p, sizeof(double), cudaMemcpyDeviceToHost, st));
     SC_CUDA(cudaStreamSynchronize(st));
 
@@ -872,13 +1111,9 @@ int sc_lloyd(int64_t n, int64_t d, int64_t k, const double* v, const double* c_i
         // ---- assign
         rownorm_kernel<<<(unsigned)ceil_div(k, 256), 256, 0, st>>>(k, d, centroids, cn.p);
         SC_CUDA(cudaMemsetAsync(changes.p, 0, sizeof(unsigned long long), st));
-        {
-            ProfScope prof("kmeans_assign", st, flops);
-            dist_tile_kernel<0><<<(unsigned)nb, 256, 0, st>>>(n, k, d, v, vn.p, centroids, cn.p, nullptr, nxt,
-                                                              cur, cost.p, changes.p, part.p);
-        }
+        if ((rc = assign_step(cur, nxt))) return rc;
         sum_partials_kernel<<<1, 1024, 0, st>>>(nb, part.p, sse.p);
-        SC_LAUNCHED(3);
+        SC_LAUNCHED(2);
         unsigned long long hchg = 0;
         SC_CUDA(cudaMemcpyAsync(&sse_history[iters + 1], sse.p, sizeof(double), cudaMemcpyDeviceToHost, st));
         SC_CUDA(cudaMemcpyAsync(&hchg, changes.p, sizeof(hchg), cudaMemcpyDeviceToHost, st));
@@ -1183,3 +1418,4 @@ int sc_ncut(int64_t n, const int64_t* row_ptr, const int32_t* col, const double*
 }
 
 }  // extern "C"
+

@@ -28,6 +28,7 @@
 #include "sc_knn.cuh"
 #include "sc_list.cuh"
 #include "sc_knn_tc2.cuh"
+#include "sc_tma.cuh"
 #include "sc_knn_tc.cuh"
 #include "sc_scan.cuh"
 #include "sc_sparse.cuh"
@@ -528,7 +529,7 @@ using namespace sc;
 
 namespace sc {
 
-static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     if (!fn) {
         void* p = nullptr;
@@ -538,6 +539,22 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
             fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
     }
     return fn;
+}
+
+// 2-D map over a rows x dp fp16 row-major matrix: 64 x 128 boxes, 128-byte
+// swizzle (the K-major UMMA operand layout of sc_tc.cuh)
+int make_f16_tile_map(CUtensorMap* map, const __half* base, int64_t rows, int64_t dp) {
+    auto encode = tensor_map_encoder();
+    if (!encode) return fail(SC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t gdim[2] = {(cuuint64_t)dp, (cuuint64_t)rows};
+    cuuint64_t gstride[1] = {(cuuint64_t)dp * sizeof(__half)};
+    cuuint32_t box[2] = {64, 128};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult cr = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half*>(base), gdim, gstride, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return fail(SC_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)cr));
+    return SC_OK;
 }
 
 template <int NKB, int STAGES, bool LSMEM>

@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(TC_THREADS, LSMEM ? 1 : 2)
 // qn = same in fp64 for query rows.
 // Rows are written in scan order: position i holds original point perm[i]
 // (perm == nullptr: identity); qn is indexed by the original point.
-__global__ void knn_prep_f16_kernel(int64_t n, int64_t n_pad, int64_t d, int64_t dp, const double* __restrict__ x,
+static __global__ void knn_prep_f16_kernel(int64_t n, int64_t n_pad, int64_t d, int64_t dp, const double* __restrict__ x,
                                     const double* __restrict__ mean, double scale, const int32_t* __restrict__ perm,
                                     __half* __restrict__ xh, float* __restrict__ cnk, double* __restrict__ qn) {
     int64_t i = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
@@ -335,7 +335,7 @@ __global__ void knn_prep_f16_kernel(int64_t n, int64_t n_pad, int64_t d, int64_t
 }
 
 // fp64 centred row norms and their maximum (pass 1 of the prep)
-__global__ void knn_rownorm_kernel(int64_t n, int64_t d, const double* __restrict__ x, const double* __restrict__ mean,
+static __global__ void knn_rownorm_kernel(int64_t n, int64_t d, const double* __restrict__ x, const double* __restrict__ mean,
                                    double* __restrict__ rn, unsigned long long* __restrict__ rmax_bits) {
     int64_t i = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     int lane = threadIdx.x & 31;

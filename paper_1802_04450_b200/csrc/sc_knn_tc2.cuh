@@ -89,7 +89,7 @@ __device__ __forceinline__ float4 lds_f4(uint32_t addr) {
 }
 // keep the R smallest of a row's c_src list entries (global) via a warp
 // bitonic sort in `scratch`; returns the new threshold (R-th key)
-__device__ __noinline__ float tc2_compact(float2* Lg, float2* scratch, int c_src, int R, int lane) {
+static __device__ __noinline__ float tc2_compact(float2* Lg, float2* scratch, int c_src, int R, int lane) {
     __syncwarp();  // the owner lane's appends are visible to the warp
     for (int e = lane; e < TC_LIST_P; e += 32)
         scratch[e] = e < c_src ? Lg[e] : make_float2(INFINITY, __int_as_float(-1));

@@ -497,3 +497,39 @@ def test_knn_kernel_variants_match_oracle(monkeypatch, variant):
         assert np.array_equal(w.row_ptr, want[0]), (x.shape, knn)
         assert np.array_equal(w.col_idx, want[1]), (x.shape, knn)
         assert_ulp(w.vals, want[2], 2)
+
+
+def _lloyd_cases():
+    rng = np.random.default_rng(23)
+    out = []
+    for n, d, k, kind in [(20_000, 100, 100, "unit"), (9_000, 16, 10, "unit"), (12_000, 200, 300, "unit"),
+                          (8_192, 64, 50, "raw"), (6_000, 33, 40, "dup")]:
+        centers = rng.normal(0.0, 1.0, (k, d))
+        v = centers[rng.integers(0, k, n)] + 0.3 * rng.standard_normal((n, d))
+        if kind == "unit":
+            v /= np.linalg.norm(v, axis=1, keepdims=True)
+        elif kind == "raw":
+            v *= 1e3  # large magnitudes: exercises the operand scaling
+        else:
+            v[n // 2:] = v[: n - n // 2]  # exact duplicate rows -> exact ties / zero costs
+        init = v[rng.choice(n, k, replace=False)].copy()
+        out.append((v, init, k))
+    return out
+
+
+def test_lloyd_tensor_core_assignment_bit_identical(monkeypatch):
+    """The tcgen05 assignment with certified argmin (d <= 256, n >= 4096)
+    yields bit-identical labels, centroids, SSE history and iteration counts
+    to the fp64 Gram-expansion path (itself bit-exact with the reference), on
+    unit-norm embeddings, raw large-magnitude data and data with exact
+    duplicate rows."""
+    for v, init, k in _lloyd_cases():
+        cfg = sc.KmeansConfig(k=k, max_iters=40)
+        monkeypatch.setenv("SPECLUST_ASSIGN", "fp64")
+        ref = sc.lloyd(v, init, cfg)
+        monkeypatch.delenv("SPECLUST_ASSIGN")
+        got = sc.lloyd(v, init, cfg)
+        assert got.iters_run == ref.iters_run, v.shape
+        assert np.array_equal(got.labels, ref.labels), v.shape
+        assert np.array_equal(got.centroids, ref.centroids), v.shape
+        assert np.array_equal(got.sse_history, ref.sse_history), v.shape
