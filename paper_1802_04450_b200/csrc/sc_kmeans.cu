@@ -742,22 +742,6 @@ static double np_pairwise_sum(const double* a, int64_t n) {
 }
 
 // labels[i] = nearest of the k rows of c (fp64 distance tiles, ties -> lowest)
-int assign_nearest(int64_t n, int64_t d, const double* v, int64_t k, const double* c, int64_t* labels,
-                   cudaStream_t st) {
-    const int64_t nb = ceil_div(n, TP);
-    DevBuf<double> vn, cn, cost, part;
-    DevBuf<unsigned long long> changes;
-    int rc;
-    if ((rc = vn.alloc(n)) || (rc = cn.alloc(k)) || (rc = cost.alloc(n)) || (rc = part.alloc(nb)) ||
-        (rc = changes.alloc(1)))
-        return rc;
-    rownorm_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, d, v, vn.p);
-    rownorm_kernel<<<(unsigned)ceil_div(k, 256), 256, 0, st>>>(k, d, c, cn.p);
-    dist_tile_kernel<0><<<(unsigned)nb, 256, 0, st>>>(n, k, d, v, vn.p, c, cn.p, nullptr, labels, nullptr, cost.p,
-                                                      changes.p, part.p);
-    SC_LAUNCHED(3);
-    return SC_OK;
-}
 
 }  // namespace sc
 
@@ -839,6 +823,11 @@ __global__ void as_finalize_kernel(int64_t n, int64_t d, int64_t dp, double s, c
     }
     const unsigned bal = __ballot_sync(0xffffffffu, chg);
     if ((threadIdx.x & 31) == 0 && bal) atomicAdd(changes, (unsigned long long)__popc(bal));
+}
+
+__global__ void as_take_best_kernel(int64_t n, const int32_t* __restrict__ best_idx, int64_t* __restrict__ labels) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) labels[i] = best_idx[i] < 0 ? 0 : best_idx[i];
 }
 
 // flagged rows: exact scan over all centroids (warp per row, lowest index on ties)
@@ -940,9 +929,11 @@ struct AssignTc {
         return make_f16_tile_map(&vmap, vh.p, n_pad, dp);
     }
     // labels / cost / change count of one assignment step
+    // certify = false: labels are the approximate argmin (no exact costs, no
+    // rescan) -- for callers that only need a heuristic grouping
     int assign(int64_t k, const double* v, const double* vn, const double* c, const double* cn,
                const int64_t* old_labels, int64_t* labels, double* cost, unsigned long long* changes,
-               cudaStream_t st) {
+               cudaStream_t st, bool certify = true) {
         const int64_t k_pad = (k + 127) / 128 * 128;
         DevBuf<__half> ch;
         DevBuf<float> cnk;
@@ -963,6 +954,11 @@ struct AssignTc {
             default: rc = launch_assign_tc<4, 2, 1>(vmap, cmap, n, nptiles, nctiles, cnk.p, key_scale, bidx.p, bkeys.p, st); break;
         }
         if (rc) return rc;
+        if (!certify) {
+            as_take_best_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, bidx.p, labels);
+            SC_LAUNCHED(1);
+            return SC_OK;
+        }
         as_finalize_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, d, dp, s, v, vn, c, cn, scal.p + 1, bidx.p,
                                                                         bkeys.p, old_labels, labels, cost, flagged.p,
                                                                         scal.p, changes);
@@ -978,6 +974,35 @@ struct AssignTc {
         return (int64_t)h;
     }
 };
+
+}  // namespace sc
+
+namespace sc {
+// labels[i] = index of the nearest of the k rows of c: exact fp64 Gram
+// expansion, or (eligible shapes) the tensor-core argmin without the exact
+// certificate -- used only for the kNN scan-order grouping, where any
+// near-nearest pivot serves
+int assign_nearest(int64_t n, int64_t d, const double* v, int64_t k, const double* c, int64_t* labels,
+                   cudaStream_t st) {
+    const int64_t nb = ceil_div(n, TP);
+    DevBuf<double> vn, cn, cost, part;
+    DevBuf<unsigned long long> changes;
+    int rc;
+    if ((rc = vn.alloc(n)) || (rc = cn.alloc(k)) || (rc = cost.alloc(n)) || (rc = part.alloc(nb)) ||
+        (rc = changes.alloc(1)))
+        return rc;
+    SC_CUDA(cudaMemsetAsync(changes.p, 0, sizeof(unsigned long long), st));
+    rownorm_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, d, v, vn.p);
+    rownorm_kernel<<<(unsigned)ceil_div(k, 256), 256, 0, st>>>(k, d, c, cn.p);
+    SC_LAUNCHED(2);
+    AssignTc atc;
+    if ((rc = atc.init(n, d, k, v, st))) return rc;
+    if (atc.active) return atc.assign(k, v, vn.p, c, cn.p, nullptr, labels, cost.p, changes.p, st, false);
+    dist_tile_kernel<0><<<(unsigned)nb, 256, 0, st>>>(n, k, d, v, vn.p, c, cn.p, nullptr, labels, nullptr, cost.p,
+                                                      changes.p, part.p);
+    SC_LAUNCHED(1);
+    return SC_OK;
+}
 
 }  // namespace sc
 
