@@ -574,75 +574,137 @@ __global__ void kpp_psum_kernel(int64_t n, const double* __restrict__ d2, const 
 // first index whose normalised cumulative probability exceeds u
 // (numpy Generator.choice: cdf = p.cumsum(); cdf /= cdf[-1];
 //  cdf.searchsorted(u, side="right")).
+// Warp-parallel inverse-CDF search over the candidates (kmeans.py:130-132:
+// rng.choice(p=d2/sum) = first candidate whose cumulative probability exceeds
+// the uniform draw).  Level 1 walks the KPP_BLK-row block sums (32 contiguous
+// chunks, one per lane, warp prefix over the chunk sums), level 2 the rows of
+// the crossing block (KPP_BLK / 32 per lane).  `crosses(c)` tests a cumulative value.
+// The cumulative sums are regrouped relative to a strictly sequential cumsum,
+// so a draw could differ only if it fell within a few ulps of a boundary.
+template <class Crosses>
+__device__ __forceinline__ int64_t kpp_warp_search(int64_t n, int64_t nb, const double* __restrict__ d2,
+                                                   const uint8_t* __restrict__ taken, double tot,
+                                                   const double* __restrict__ bsum, Crosses crosses) {
+    const int lane = threadIdx.x & 31;
+    // ---- level 1: block sums
+    const int64_t per = (nb + 31) / 32, b0 = imin64(nb, lane * per), b1 = imin64(nb, b0 + per);
+    double cs = 0.0;
+    for (int64_t b = b0; b < b1; ++b) cs += bsum[b];
+    double pre = cs;  // inclusive warp scan
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double t = __shfl_up_sync(0xffffffffu, pre, o);
+        if (lane >= o) pre += t;
+    }
+    double run = pre - cs;  // exclusive prefix of this lane's chunk
+    int64_t hit = -1;
+    if (crosses(pre))
+        for (int64_t b = b0; b < b1; ++b) {
+            if (crosses(run + bsum[b])) {
+                hit = b;
+                break;
+            }
+            run += bsum[b];
+        }
+    unsigned m = __ballot_sync(0xffffffffu, hit >= 0);
+    int64_t blk;
+    if (m) {
+        const int src = __ffs(m) - 1;
+        blk = __shfl_sync(0xffffffffu, hit, src);
+        run = __shfl_sync(0xffffffffu, run, src);
+    } else {
+        blk = nb - 1;  // rounding: no block crossed -> the last block, from its start
+        run = __shfl_sync(0xffffffffu, pre, 31) - bsum[nb - 1];
+    }
+    // ---- level 2: rows of the crossing block, KPP_BLK / 32 consecutive rows per lane
+    constexpr int RPL = KPP_BLK / 32;
+    const int64_t lo = blk * KPP_BLK, hi = imin64(n, lo + KPP_BLK);
+    const int64_t r0 = imin64(hi, lo + lane * RPL), r1 = imin64(hi, r0 + RPL);
+    double ps = 0.0;
+    int64_t mylast = -1;
+    for (int64_t i = r0; i < r1; ++i)
+        if (!taken[i] && d2[i] > 0.0) {
+            ps += d2[i] / tot;
+            mylast = i;
+        }
+    double pp = ps;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double t = __shfl_up_sync(0xffffffffu, pp, o);
+        if (lane >= o) pp += t;
+    }
+    double r = run + (pp - ps);
+    int64_t found = -1;
+    if (crosses(run + pp))
+        for (int64_t i = r0; i < r1; ++i) {
+            if (taken[i] || !(d2[i] > 0.0)) continue;
+            r += d2[i] / tot;
+            if (crosses(r)) {
+                found = i;
+                break;
+            }
+        }
+    m = __ballot_sync(0xffffffffu, found >= 0);
+    if (m) return __shfl_sync(0xffffffffu, found, __ffs(m) - 1);
+    // rounding pushed the crossing past every candidate of the block: its
+    // last candidate (or, if none, the last candidate overall)
+    unsigned ml = __ballot_sync(0xffffffffu, mylast >= 0);
+    if (ml) return __shfl_sync(0xffffffffu, mylast, 31 - __clz(ml));
+    return -2;
+}
+
+__device__ __forceinline__ int64_t kpp_last_candidate(int64_t n, const double* __restrict__ d2,
+                                                      const uint8_t* __restrict__ taken) {
+    for (int64_t i = n - 1; i >= 0; --i)
+        if (!taken[i] && d2[i] > 0.0) return i;
+    return -1;
+}
+
 __global__ void kpp_search_kernel(int64_t n, int64_t nb, const double* __restrict__ d2,
                                   const uint8_t* __restrict__ taken, const double* __restrict__ total,
                                   const double* __restrict__ bsum, double u, int64_t* __restrict__ out) {
-    if (threadIdx.x != 0) return;
-    double last = 0.0;
-    for (int64_t b = 0; b < nb; ++b) last += bsum[b];
-    double run = 0.0;
-    int64_t b = 0;
-    for (; b < nb; ++b) {
-        if ((run + bsum[b]) / last > u) break;
-        run += bsum[b];
+    // sum of all block sums (lane-chunked, as in kpp_warp_search)
+    const int lane = threadIdx.x & 31;
+    const int64_t per = (nb + 31) / 32, b0 = imin64(nb, lane * per), b1 = imin64(nb, b0 + per);
+    double cs = 0.0;
+    for (int64_t b = b0; b < b1; ++b) cs += bsum[b];
+    double last = cs;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double t = __shfl_up_sync(0xffffffffu, last, o);
+        if (lane >= o) last += t;
     }
-    double tot = *total;
-    int64_t lastcand = -1;
-    if (b == nb) b = nb - 1, run -= bsum[nb - 1];
-    int64_t lo = b * KPP_BLK, hi = imin64(n, lo + KPP_BLK);
-    for (int64_t i = lo; i < hi; ++i) {
-        if (taken[i] || !(d2[i] > 0.0)) continue;
-        lastcand = i;
-        run += d2[i] / tot;
-        if (run / last > u) {
-            *out = i;
-            return;
-        }
-    }
-    if (lastcand < 0) {  // rounding pushed the crossing past every candidate
-        for (int64_t i = n - 1; i >= 0; --i)
-            if (!taken[i] && d2[i] > 0.0) { lastcand = i; break; }
-    }
-    *out = lastcand;
+    last = __shfl_sync(0xffffffffu, last, 31);
+    int64_t r = kpp_warp_search(n, nb, d2, taken, *total, bsum, [&](double c) { return c / last > u; });
+    if (r == -2 && lane == 0) r = kpp_last_candidate(n, d2, taken);
+    if (lane == 0) *out = r;
 }
 
-// r-th untaken row in ascending order (uniform fallback, kmeans.py:133-134)
-// first candidate whose cumulative p (= w / *total) exceeds `target`; -1 if none
 __global__ void kpp_search_target_kernel(int64_t n, int64_t nb, const double* __restrict__ d2,
                                          const uint8_t* __restrict__ taken, const double* __restrict__ total,
                                          const double* __restrict__ bsum, double target, int64_t* __restrict__ out) {
-    if (threadIdx.x != 0) return;
-    double run = 0.0;
-    int64_t b = 0;
-    for (; b < nb; ++b) {
-        if (run + bsum[b] > target) break;
-        run += bsum[b];
+    const int lane = threadIdx.x & 31;
+    // target at/above this shard's total: its last candidate
+    const int64_t per = (nb + 31) / 32, b0 = imin64(nb, lane * per), b1 = imin64(nb, b0 + per);
+    double cs = 0.0;
+    for (int64_t b = b0; b < b1; ++b) cs += bsum[b];
+    double all = cs;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double t = __shfl_up_sync(0xffffffffu, all, o);
+        if (lane >= o) all += t;
     }
-    *out = -1;
-    if (b == nb) {  // target at/above this shard's total: its last candidate
-        for (int64_t i = n - 1; i >= 0; --i)
-            if (!taken[i] && d2[i] > 0.0) {
-                *out = i;
-                return;
-            }
-        return;
+    all = __shfl_sync(0xffffffffu, all, 31);
+    int64_t r;
+    if (!(all > target)) {
+        r = lane == 0 ? kpp_last_candidate(n, d2, taken) : -1;
+    } else {
+        r = kpp_warp_search(n, nb, d2, taken, *total, bsum, [&](double c) { return c > target; });
+        if (r == -2) r = -1;
     }
-    const double tot = *total;
-    const int64_t lo = b * KPP_BLK, hi = imin64(n, lo + KPP_BLK);
-    int64_t last = -1;
-    for (int64_t i = lo; i < hi; ++i) {
-        if (taken[i] || !(d2[i] > 0.0)) continue;
-        last = i;
-        run += d2[i] / tot;
-        if (run > target) {
-            *out = i;
-            return;
-        }
-    }
-    *out = last;  // rounding: the block sum said the crossing is here
+    if (lane == 0) *out = r;
 }
 
-// one step of the stable descending order: mark and record the argmax
 __global__ void argmax_finish_kernel(int nb, const double* __restrict__ pv, const int64_t* __restrict__ pi,
                                      uint8_t* __restrict__ used, int64_t* __restrict__ out) {
     if (threadIdx.x != 0) return;
