@@ -491,10 +491,14 @@ __global__ void row_fill_kernel(int64_t nl, int64_t r0, int64_t d, int64_t knn, 
                                 double den, const int32_t* __restrict__ sel, const int32_t* __restrict__ pos,
                                 const int64_t* __restrict__ rev_ptr, const int32_t* __restrict__ rev,
                                 const uint8_t* __restrict__ dup, const int64_t* __restrict__ row_ptr,
-                                int32_t* __restrict__ col, double* __restrict__ vals) {
-    int64_t i = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;  // local row
+                                int32_t* __restrict__ col, double* __restrict__ vals,
+                                const int32_t* __restrict__ order) {
+    // local row; with `order` (whole graph only) the rows are visited in the
+    // kNN locality order so the x rows of their neighbours are L2-resident
+    int64_t i = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     int lane = threadIdx.x & 31;
     if (i >= nl) return;
+    if (order) i = order[i];
     const int32_t* s = sel + (int64_t)pos[r0 + i] * knn;
     const int64_t rb = rev_ptr[i], re = rev_ptr[i + 1];
     const int64_t out0 = row_ptr[i];
@@ -923,7 +927,8 @@ int knn_union(int64_t n, int64_t d, const double* x, int64_t knn, double two_sig
         return fail(SC_ERR_VALUE, "knn union: " + std::to_string(nnz) + " entries exceed the output capacity " +
                                       std::to_string(cap));
     row_fill_kernel<<<(unsigned)ceil_div(nl, 8), 256, 0, st>>>(nl, r0, d, knn, x, two_sigma_sq, sel, pos.p, rev_ptr.p,
-                                                               rev.p, dup.p, row_ptr, col, vals);
+                                                               rev.p, dup.p, row_ptr, col, vals,
+                                                               (r0 == 0 && nl == n) ? perm : nullptr);
     SC_LAUNCHED(1);
     return SC_OK;
 }

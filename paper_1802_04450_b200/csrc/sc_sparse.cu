@@ -621,7 +621,12 @@ __global__ void perm_row_len_kernel(int64_t n, const int64_t* __restrict__ row_p
     len[p] = row_ptr[i + 1] - row_ptr[i];
 }
 
-// warp per output row; entries ranked by their new column (distinct keys)
+// warp per output row: rows of <= 64 entries are sorted by their new column
+// with a register bitonic network (2 keys per lane, key = new column << 32 |
+// source slot, all keys distinct); longer rows rank every entry by counting
+__device__ __forceinline__ int64_t cas64(int64_t v, int64_t o, bool keep_min) {
+    return keep_min ? (v < o ? v : o) : (v > o ? v : o);
+}
 __global__ void perm_row_fill_kernel(int64_t n, const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
                                      const double* __restrict__ vals, const int32_t* __restrict__ perm,
                                      const int32_t* __restrict__ pos, const int64_t* __restrict__ out_ptr,
@@ -631,6 +636,37 @@ __global__ void perm_row_fill_kernel(int64_t n, const int64_t* __restrict__ row_
     if (p >= n) return;
     const int64_t i = perm[p];
     const int64_t b = row_ptr[i], len = row_ptr[i + 1] - b, o = out_ptr[p];
+    if (len <= 64) {
+        int64_t v0 = lane < len ? ((int64_t)pos[col[b + lane]] << 32) | lane : INT64_MAX;
+        int64_t v1 = lane + 32 < len ? ((int64_t)pos[col[b + lane + 32]] << 32) | (lane + 32) : INT64_MAX;
+#pragma unroll
+        for (int k = 2; k <= 64; k <<= 1) {
+#pragma unroll
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                if (j == 32) {  // partners are the two keys of this lane
+                    const bool up = (lane & k) == 0;  // k == 64: always ascending
+                    const int64_t lo = v0 < v1 ? v0 : v1, hi = v0 < v1 ? v1 : v0;
+                    v0 = up ? lo : hi;
+                    v1 = up ? hi : lo;
+                } else {
+                    const int64_t o0 = __shfl_xor_sync(0xffffffffu, v0, j);
+                    const int64_t o1 = __shfl_xor_sync(0xffffffffu, v1, j);
+                    const bool lower = (lane & j) == 0;
+                    v0 = cas64(v0, o0, lower == ((lane & k) == 0));
+                    v1 = cas64(v1, o1, lower == (((lane + 32) & k) == 0));
+                }
+            }
+        }
+        if (lane < len) {
+            out_col[o + lane] = (int32_t)(v0 >> 32);
+            out_vals[o + lane] = vals[b + (int32_t)(v0 & 0xffffffff)];
+        }
+        if (lane + 32 < len) {
+            out_col[o + lane + 32] = (int32_t)(v1 >> 32);
+            out_vals[o + lane + 32] = vals[b + (int32_t)(v1 & 0xffffffff)];
+        }
+        return;
+    }
     for (int64_t e = lane; e < len; e += 32) {
         const int32_t key = pos[col[b + e]];
         int64_t r = 0;

@@ -124,8 +124,12 @@ def test_csr_permute_and_gather_rows():
     rng = np.random.default_rng(3)
     n = 700
     a = (rng.random((n, n)) < 0.02) * rng.standard_normal((n, n))
+    # rows of every length class of the kernel: <= 32, 33..64, > 64 entries
+    a[:40] += (rng.random((40, n)) < np.linspace(0.03, 0.2, 40)[:, None]) * rng.standard_normal((40, n))
     a = a + a.T
     r, c = np.nonzero(a)
+    lens = np.bincount(r, minlength=n)
+    assert lens.max() > 64 and np.any((lens > 32) & (lens <= 64)) and np.any(lens <= 32)
     m = sc.coo_to_csr(sc.coo_canonicalize(sc.CooMatrix(n, n, r, c, a[r, c]))).device()
     perm = rng.permutation(n).astype(np.int32)
     ap, pos = permute_device(m, torch.from_numpy(perm).cuda())
