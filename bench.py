@@ -153,7 +153,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
-    ap.add_argument("--ref-sample", type=int, default=3000)
+    ap.add_argument("--ref-sample", type=int, default=8000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the public-API end-to-end timing (ncu runs)")
     ap.add_argument("--sharded", action="store_true",
@@ -280,6 +280,13 @@ def main():
         roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm"], "unit": "GB/s",
                 "frac": achieved / pk["hbm"], "traffic": None, "kernel": dom, "peak_src": pk["src"],
                 "ms_per_step": dms}
+    # DRAM traffic of the dominant kernel from the committed ncu capture
+    tr = ROOT / "profiles" / "roofline_traffic.json"
+    if tr.exists():
+        ent = json.loads(tr.read_text()).get(dom)
+        if ent:
+            roof["traffic"] = ent["bytes"]
+            roof["traffic_src"] = ent["capture"]
     spmv_ms, spmv_n, spmv_bytes = kstats["spmv"]
     spmv_gbs = spmv_bytes / (spmv_ms / 1e3) / 1e9 if spmv_ms > 0 else None
     km_iters = rep.labeling.iters_run
