@@ -609,9 +609,23 @@ static int launch_tc2_w(const CUtensorMap& map, int64_t n, int64_t ntiles, int64
                                : std::max<uint32_t>(Tc2Layout<NKB, STAGES>::total, 116u * 1024u);
     SC_CUDA(cudaFuncSetAttribute(knn_cand_tc2_kernel<NKB, STAGES, WMODE, HEAP>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    DevBuf<long long> dbg;
+    if (WMODE & 64) {
+        if (int rc = dbg.alloc(8)) return rc;
+        SC_CUDA(cudaMemsetAsync(dbg.p, 0, 8 * sizeof(long long), st));
+    }
     knn_cand_tc2_kernel<NKB, STAGES, WMODE, HEAP><<<(unsigned)grid, TC2_THREADS, smem, st>>>(
-        map, n, ntiles, qtile0, nq, cnk, key_scale, cap, R, lists, counts, taus);
+        map, n, ntiles, qtile0, nq, cnk, key_scale, cap, R, lists, counts, taus, dbg.p);
     SC_LAUNCHED(1);
+    if (WMODE & 64) {
+        long long h[8];
+        SC_CUDA(cudaMemcpyAsync(h, dbg.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+        SC_CUDA(cudaStreamSynchronize(st));
+        const double warps = (double)grid * 8;
+        fprintf(stderr, "[knn_tc2 list path] per warp: cycles t<16 %.3g, 16<=t<128 %.3g, t>=128 %.3g; "
+                        "fired halves %.0f / %.0f / %.0f\n",
+                h[0] / warps, h[1] / warps, h[2] / warps, h[3] / warps, h[4] / warps, h[5] / warps);
+    }
     return SC_OK;
 }
 
@@ -624,6 +638,7 @@ static int launch_tc2(const CUtensorMap& map, int64_t n, int64_t ntiles, int64_t
                       float key_scale, int cap, int R, float2* lists, int* counts, float* taus, cudaStream_t st) {
     const char* wenv = std::getenv("SPECLUST_KNN_WAIT");
     const int w = wenv ? std::atoi(wenv) : 3;
+    if (std::getenv("SPECLUST_KNN_NOLIST")) cap = -cap;  // profiling only: results invalid
     // opt-in (SPECLUST_KNN_HEAP=1): candidate lists as shared-memory max-heaps
     // (d <= 64: the 256 x R heaps fit beside a 3- or 2-deep operand ring).
     // Measured at C2 it is slower than the global lists with warp compaction
@@ -649,6 +664,7 @@ static int launch_tc2(const CUtensorMap& map, int64_t n, int64_t ntiles, int64_t
         SC_TC2(15);
         SC_TC2(19);
         SC_TC2(27);
+        SC_TC2(67);
         default: return launch_tc2_w<NKB, STAGES, 3, false>(map, n, ntiles, qtile0, nq, cnk, key_scale, cap, R, lists,
                                                             counts, taus, st);
     }
@@ -715,7 +731,10 @@ int knn_select(int64_t n, int64_t d, const double* x, int64_t knn, double two_si
     int cap;
     if (use_tc) {
         // a compaction leaves R entries and must leave room for one 16-column chunk
-        cap = (int)std::min<int64_t>(std::max<int64_t>(2 * R, R + 16), TC_LIST_P);
+        // capacity 2R + 16 (<= the sort width): each warp compaction frees
+        // R + 16 slots (C2: 128 -> -9 ms of list maintenance vs 2R); tuning knob
+        const char* cenv = std::getenv("SPECLUST_KNN_CAP");
+        cap = (int)std::min<int64_t>(std::max<int64_t>(cenv ? std::atoll(cenv) : 2 * R + 16, R + 16), TC_LIST_P);
     } else {
         cap = 2 * R;
         if (cap > n - 1) cap = (int)(n - 1);  // lists can hold every other point

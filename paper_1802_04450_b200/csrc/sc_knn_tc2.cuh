@@ -116,7 +116,8 @@ template <int NKB, int STAGES, int WMODE, bool HEAP>
 __global__ void __launch_bounds__(TC2_THREADS, 1)
     knn_cand_tc2_kernel(const __grid_constant__ CUtensorMap xmap, int64_t n, int64_t ntiles, int64_t qtile0,
                         int64_t nq, const float* __restrict__ cnk, float key_scale, int cap, int R,
-                        float2* __restrict__ lists, int* __restrict__ counts, float* __restrict__ taus) {
+                        float2* __restrict__ lists, int* __restrict__ counts, float* __restrict__ taus,
+                        long long* __restrict__ dbg = nullptr) {
     using Lay = Tc2Layout<NKB, STAGES>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -137,6 +138,9 @@ __global__ void __launch_bounds__(TC2_THREADS, 1)
     float2* sH = reinterpret_cast<float2*>(reinterpret_cast<uintptr_t>(tmem_slot + 4 + 15) & ~uintptr_t(15));
     float* sStage = reinterpret_cast<float*>(sH + (HEAP ? 256 * R : 0));
 
+    // profiling: a negative cap keeps the list code compiled but never runs it
+    const bool capneg = cap < 0;
+    if (capneg) cap = -cap;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // query tiles qt0, qt0 + 1 (scan positions); list slots relative to qtile0
     const int64_t lq0 = (int64_t)blockIdx.x * 2;
@@ -228,6 +232,7 @@ __global__ void __launch_bounds__(TC2_THREADS, 1)
         float* stage = sStage + ((size_t)(warp - 2) * 32 + lane) * 16;
         int cnt = 0;
         float tau = INFINITY;
+        long long dbg_c[3] = {0, 0, 0}, dbg_f[3] = {0, 0, 0};
         // max-heap on the key: sift `e` down from slot i
         auto sift_down = [&](int i, float2 e) {
             while (true) {
@@ -360,18 +365,38 @@ __global__ void __launch_bounds__(TC2_THREADS, 1)
                     }
                 }
             };
-            if (HEAP) {
+            if (capneg) {
+            } else if (HEAP) {
                 if (!(WMODE & 16) && __any_sync(0xffffffffu, valid && h0 < tau)) slow_heap(v, qm, col0);
                 if (!(WMODE & 16) && __any_sync(0xffffffffu, valid && h1 < tau)) slow_heap(v + 64, qm + 4, col0 + 64);
             } else {
-                if (!(WMODE & 16) && __any_sync(0xffffffffu, valid && h0 < tau)) slow(v, qm, col0);
-                if (!(WMODE & 16) && __any_sync(0xffffffffu, valid && h1 < tau)) slow(v + 64, qm + 4, col0 + 64);
+                const long long z0 = (WMODE & 64) ? clock64() : 0;
+                int fired = 0;
+                if (!(WMODE & 16) && __any_sync(0xffffffffu, valid && h0 < tau)) {
+                    slow(v, qm, col0);
+                    ++fired;
+                }
+                if (!(WMODE & 16) && __any_sync(0xffffffffu, valid && h1 < tau)) {
+                    slow(v + 64, qm + 4, col0 + 64);
+                    ++fired;
+                }
+                if (WMODE & 64) {
+                    const int bin = t < 16 ? 0 : t < 128 ? 1 : 2;
+                    dbg_c[bin] += clock64() - z0;
+                    dbg_f[bin] += fired;
+                }
             }
             tc::fence_before();
             __syncwarp();
             if (lane == 0) {
                 tc::mbar_arrive(&tempty[buf]);
                 tc::mbar_arrive(&cempty[cslot]);
+            }
+        }
+        if ((WMODE & 64) && lane == 0 && dbg) {
+            for (int b = 0; b < 3; ++b) {
+                atomicAdd(reinterpret_cast<unsigned long long*>(dbg + b), (unsigned long long)dbg_c[b]);
+                atomicAdd(reinterpret_cast<unsigned long long*>(dbg + 3 + b), (unsigned long long)dbg_f[b]);
             }
         }
         if (valid) {
