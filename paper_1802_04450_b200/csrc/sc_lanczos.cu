@@ -52,37 +52,37 @@ __global__ void fill_normal_offset_kernel(int64_t n, int64_t offset, uint64_t se
 
 // part[b * ncols + c] = sum_{r in block b} B[c * ld + r] * w[r];
 // optional sq_part[b] = sum_{r in block b} w[r]^2 (|w| before the projection)
-__global__ void __launch_bounds__(256) gemv_t_partial_kernel(int64_t n, int64_t ld, int ncols,
+__global__ void __launch_bounds__(256) gemv_t_partial_kernel(int64_t n, int64_t ld, int ncols, int rpb,
                                                              const double* __restrict__ B,
                                                              const double* __restrict__ w,
                                                              double* __restrict__ part,
                                                              double* __restrict__ sq_part) {
+    // rpb rows per block (<= GT_ROWS); the grid is sized to one balanced wave
+    // of kNumSMs x 8 blocks when n allows (Lanczos::init)
     __shared__ double ws[GT_ROWS];
-    const int64_t r0 = (int64_t)blockIdx.x * GT_ROWS;
-    const int rows = (int)imin64(GT_ROWS, n - r0);
-    for (int i = threadIdx.x; i < GT_ROWS; i += blockDim.x) ws[i] = i < rows ? w[r0 + i] : 0.0;
+    const int64_t r0 = (int64_t)blockIdx.x * rpb;
+    const int rows = (int)imin64(rpb, n - r0);
+    for (int i = threadIdx.x; i < rows; i += blockDim.x) ws[i] = w[r0 + i];
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (sq_part && warp == 0) {
         double s = 0.0;
-        for (int t = lane; t < GT_ROWS; t += 32) s = fma(ws[t], ws[t], s);
+        for (int t = lane; t < rows; t += 32) s = fma(ws[t], ws[t], s);
         s = warp_sum(s);
         if (lane == 0) sq_part[blockIdx.x] = s;
     }
     for (int c = warp; c < ncols; c += 8) {
         const double* col = B + (int64_t)c * ld + r0;
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-        if (rows == GT_ROWS) {
-#pragma unroll 4
-            for (int t = lane; t < GT_ROWS; t += 128) {
-                a0 = fma(__ldg(col + t), ws[t], a0);
-                a1 = fma(__ldg(col + t + 32), ws[t + 32], a1);
-                a2 = fma(__ldg(col + t + 64), ws[t + 64], a2);
-                a3 = fma(__ldg(col + t + 96), ws[t + 96], a3);
-            }
-        } else {
-            for (int t = lane; t < rows; t += 32) a0 = fma(__ldg(col + t), ws[t], a0);
+        int t = lane;
+#pragma unroll 2
+        for (; t + 96 < rows; t += 128) {
+            a0 = fma(__ldg(col + t), ws[t], a0);
+            a1 = fma(__ldg(col + t + 32), ws[t + 32], a1);
+            a2 = fma(__ldg(col + t + 64), ws[t + 64], a2);
+            a3 = fma(__ldg(col + t + 96), ws[t + 96], a3);
         }
+        for (; t < rows; t += 32) a0 = fma(__ldg(col + t), ws[t], a0);
         double acc = warp_sum((a0 + a1) + (a2 + a3));
         if (lane == 0) part[blockIdx.x * (int64_t)ncols + c] = acc;
     }
@@ -404,11 +404,12 @@ struct sc_lanczos {
     DevBuf<double> B, T, w, part, h, sqp, sq0, scal, Y, A, Z, wraw, wsort, S, lastrow, vectors;
     DevBuf<int> info, nonfinite;
     int64_t nb_t = 0, nb_n = 0;
+    int rpb_t = GT_ROWS;  // rows per gemv_t block
     static constexpr int64_t fz_blocks = 4 * kNumSMs;  // persistent grid of the fused pass
 
     // ---- building blocks
     int project(const double* x, int ncols, double* sq_part = nullptr) {
-        gemv_t_partial_kernel<<<(unsigned)nb_t, 256, 0, st>>>(n, ld, ncols, B.p, x, part.p, sq_part);
+        gemv_t_partial_kernel<<<(unsigned)nb_t, 256, 0, st>>>(n, ld, ncols, rpb_t, B.p, x, part.p, sq_part);
         reduce_cols_kernel<<<(unsigned)ceil_div((int64_t)ncols * 32, 256), 256, 0, st>>>(nb_t, ncols, part.p, h.p);
         SC_LAUNCHED(2);
         return SC_OK;
@@ -477,7 +478,9 @@ struct sc_lanczos {
         seed = seed_;
         st = st_;
         ld = (n + 31) / 32 * 32;
-        nb_t = ceil_div(n, GT_ROWS);
+        // one balanced wave (kNumSMs x 8 blocks) while the rows fit, 32-row granules
+        rpb_t = (int)std::min<int64_t>(GT_ROWS, std::max<int64_t>(32, ceil_div(ceil_div(n, kNumSMs * 8), 32) * 32));
+        nb_t = ceil_div(n, rpb_t);
         nb_n = ceil_div(n, GN_THREADS);
         int rc;
         if ((rc = B.alloc((size_t)ld * (m + 1))) || (rc = T.alloc((size_t)m * m)) || (rc = w.alloc(ld)) ||
@@ -843,7 +846,7 @@ int sc_gemv_t_f64(int64_t n, int64_t ld, int64_t ncols, const double* B, const d
     const int64_t nb = ceil_div(n, GT_ROWS);
     DevBuf<double> part;
     if (int rc = part.alloc((size_t)nb * ncols)) return rc;
-    gemv_t_partial_kernel<<<(unsigned)nb, 256, 0, st>>>(n, ld, (int)ncols, B, w, part.p, nullptr);
+    gemv_t_partial_kernel<<<(unsigned)nb, 256, 0, st>>>(n, ld, (int)ncols, GT_ROWS, B, w, part.p, nullptr);
     reduce_cols_kernel<<<(unsigned)ceil_div(ncols * 32, 256), 256, 0, st>>>(nb, (int)ncols, part.p, h);
     SC_LAUNCHED(2);
     return SC_OK;
