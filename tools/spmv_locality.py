@@ -46,3 +46,15 @@ for _ in range(5):
     nat.check(lib.sc_spmv_f64(n, n, nat.ptr(a.row_ptr), nat.ptr(a.col), nat.ptr(a.vals), nat.ptr(xv), nat.ptr(yv), 0,
                               nat.stream_handle()))
 torch.cuda.synchronize()
+# windowed-SpMV hit fraction (spmv_window_kernel geometry: 148 row ranges,
+# window of 26624 x entries centred on the range)
+G, WIN = 148, 26624
+hits = 0
+for b in range(G):
+    r0, r1 = n * b // G, n * (b + 1) // G
+    half = max(0, (WIN - (r1 - r0)) // 2)
+    wb = max(0, r0 - half)
+    we = min(n, min(wb + WIN, r1 + half))
+    c = col[rp[r0]:rp[r1]]
+    hits += np.count_nonzero((c >= wb) & (c < we))
+print(f"  window hit fraction {hits / col.size:.3f}")
