@@ -929,6 +929,30 @@ __global__ void as_rescan_kernel(int64_t d, int64_t k, const double* __restrict_
     }
 }
 
+// compact copy of the flagged rows (and their norms / old labels)
+__global__ void as_gather_kernel(int64_t nf, int64_t d, const int32_t* __restrict__ flagged,
+                                 const double* __restrict__ v, const double* __restrict__ vn,
+                                 const int64_t* __restrict__ old_labels, double* __restrict__ vf,
+                                 double* __restrict__ vnf, int64_t* __restrict__ oldf) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= nf * d) return;
+    const int64_t r = e / d, l = e - r * d;
+    const int64_t i = flagged[r];
+    vf[e] = v[i * d + l];
+    if (l == 0) {
+        vnf[r] = vn[i];
+        if (old_labels) oldf[r] = old_labels[i];
+    }
+}
+__global__ void as_scatter_kernel(int64_t nf, const int32_t* __restrict__ flagged, const int64_t* __restrict__ labf,
+                                  const double* __restrict__ costf, int64_t* __restrict__ labels,
+                                  double* __restrict__ cost) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= nf) return;
+    labels[flagged[r]] = labf[r];
+    cost[flagged[r]] = costf[r];
+}
+
 // part[b] = cost[64 b] + ... + cost[64 b + 63], sequential (the same fixed
 // order as dist_tile_kernel's per-block sum, so the SSE is path-independent)
 __global__ void cost_block_sum_kernel(int64_t n, const double* __restrict__ cost, double* __restrict__ part) {
@@ -1024,9 +1048,30 @@ struct AssignTc {
         as_finalize_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, d, dp, s, v, vn, c, cn, scal.p + 1, bidx.p,
                                                                         bkeys.p, old_labels, labels, cost, flagged.p,
                                                                         scal.p, changes);
-        as_rescan_kernel<<<kNumSMs * 4, 256, 0, st>>>(d, k, v, vn, c, cn, flagged.p, scal.p, old_labels, labels, cost,
-                                                      changes);
-        SC_LAUNCHED(2);
+        SC_LAUNCHED(1);
+        // uncertified rows: exact re-scan.  Few rows or few centroids: a warp
+        // per row; otherwise the rows are gathered and run through the tiled
+        // fp64 assignment kernel (the same arithmetic as the fp64 path)
+        const int64_t nf = flagged_count(st);
+        if (nf == 0) return SC_OK;
+        if (nf * k < (int64_t)1 << 24) {
+            as_rescan_kernel<<<kNumSMs * 4, 256, 0, st>>>(d, k, v, vn, c, cn, flagged.p, scal.p, old_labels, labels,
+                                                          cost, changes);
+            SC_LAUNCHED(1);
+            return SC_OK;
+        }
+        DevBuf<double> vf, vnf, costf, partf;
+        DevBuf<int64_t> labf, oldf;
+        if ((rc = vf.alloc((size_t)nf * d)) || (rc = vnf.alloc(nf)) || (rc = costf.alloc(nf)) ||
+            (rc = partf.alloc(ceil_div(nf, TP))) || (rc = labf.alloc(nf)) || (rc = oldf.alloc(nf)))
+            return rc;
+        as_gather_kernel<<<(unsigned)ceil_div(nf * d, 256), 256, 0, st>>>(nf, d, flagged.p, v, vn, old_labels, vf.p,
+                                                                          vnf.p, oldf.p);
+        dist_tile_kernel<0><<<(unsigned)ceil_div(nf, TP), 256, 0, st>>>(nf, k, d, vf.p, vnf.p, c, cn, nullptr, labf.p,
+                                                                        old_labels ? oldf.p : nullptr, costf.p,
+                                                                        changes, partf.p);
+        as_scatter_kernel<<<(unsigned)ceil_div(nf, 256), 256, 0, st>>>(nf, flagged.p, labf.p, costf.p, labels, cost);
+        SC_LAUNCHED(3);
         return SC_OK;
     }
     int64_t flagged_count(cudaStream_t st) {
