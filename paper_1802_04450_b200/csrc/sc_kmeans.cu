@@ -1400,13 +1400,23 @@ int sc_kmeans_assign(int64_t n, int64_t d, int64_t k, const double* v, const dou
     SC_CUDA(cudaMemsetAsync(chg.p, 0, sizeof(unsigned long long), st));
     rownorm_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, d, v, vn.p);
     rownorm_kernel<<<(unsigned)ceil_div(k, 256), 256, 0, st>>>(k, d, c, cn.p);
+    SC_LAUNCHED(2);
     {
         ProfScope prof("kmeans_assign", st, 2.0 * (double)n * k * d);
-        dist_tile_kernel<0><<<(unsigned)nb, 256, 0, st>>>(n, k, d, v, vn.p, c, cn.p, nullptr, labels, old_labels,
-                                                          cost, chg.p, part.p);
+        // tensor-core certified argmin when eligible (the shard's rows are
+        // converted to fp16 per call: one extra pass over v)
+        AssignTc atc;
+        if ((rc = atc.init(n, d, k, v, st))) return rc;
+        if (atc.active) {
+            if ((rc = atc.assign(k, v, vn.p, c, cn.p, old_labels, labels, cost, chg.p, st))) return rc;
+            cost_block_sum_kernel<<<(unsigned)ceil_div(nb, 256), 256, 0, st>>>(n, cost, part.p);
+        } else {
+            dist_tile_kernel<0><<<(unsigned)nb, 256, 0, st>>>(n, k, d, v, vn.p, c, cn.p, nullptr, labels, old_labels,
+                                                              cost, chg.p, part.p);
+        }
     }
     sum_partials_kernel<<<1, 1024, 0, st>>>(nb, part.p, out.p);
-    SC_LAUNCHED(4);
+    SC_LAUNCHED(2);
     unsigned long long hc = 0;
     SC_CUDA(cudaMemcpyAsync(&hc, chg.p, sizeof(hc), cudaMemcpyDeviceToHost, st));
     SC_CUDA(cudaMemcpyAsync(sse, out.p, sizeof(double), cudaMemcpyDeviceToHost, st));

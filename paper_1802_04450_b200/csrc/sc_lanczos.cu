@@ -843,10 +843,12 @@ int sc_gemv_t_f64(int64_t n, int64_t ld, int64_t ncols, const double* B, const d
         SC_CUDA(cudaMemsetAsync(h, 0, sizeof(double) * ncols, st));
         return SC_OK;
     }
-    const int64_t nb = ceil_div(n, GT_ROWS);
+    const int rpb = (int)std::min<int64_t>(GT_ROWS, std::max<int64_t>(32, ceil_div(ceil_div(n, kNumSMs * 8), 32) * 32));
+    const int64_t nb = ceil_div(n, rpb);
     DevBuf<double> part;
     if (int rc = part.alloc((size_t)nb * ncols)) return rc;
-    gemv_t_partial_kernel<<<(unsigned)nb, 256, 0, st>>>(n, ld, (int)ncols, GT_ROWS, B, w, part.p, nullptr);
+    ProfScope prof("reorth", st, (double)n * ncols * 8.0);
+    gemv_t_partial_kernel<<<(unsigned)nb, 256, 0, st>>>(n, ld, (int)ncols, rpb, B, w, part.p, nullptr);
     reduce_cols_kernel<<<(unsigned)ceil_div(ncols * 32, 256), 256, 0, st>>>(nb, (int)ncols, part.p, h);
     SC_LAUNCHED(2);
     return SC_OK;
@@ -865,6 +867,7 @@ int sc_gemv_n_f64(int64_t n, int64_t ld, int64_t ncols, const double* B, const d
     if (sq_out) {
         if (int rc = sq.alloc(nb)) return rc;
     }
+    ProfScope prof("reorth", st, (double)n * ncols * 8.0);
     if (ncols > 0) {
         gemv_n_update_kernel<<<(unsigned)nb, GN_THREADS, sizeof(double) * (size_t)ncols, st>>>(
             n, ld, (int)ncols, B, h, w, sq_out ? sq.p : nullptr);

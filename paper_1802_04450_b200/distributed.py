@@ -286,14 +286,24 @@ class CudaOps:
 
 
 class _CsrOp:
+    """sc_spmv_plan_* handle of a row-shard operator (rows local, columns
+    global): built once, applied per Lanczos step without host syncs."""
+
     def __init__(self, ops: CudaOps, a: DeviceCsr):
-        self.ops, self.a = ops, a
+        self.ops, self.a = ops, a  # keeps the CSR arrays alive with the handle
+        self.h = nat.vp()
+        nat.check(ops.lib.sc_spmv_plan_create(a.n_rows, nat.ptr(a.row_ptr), nat.ptr(a.col), nat.ptr(a.vals),
+                                              ops._s(), nat.C.byref(self.h)))
 
     def apply(self, x_full):
-        return self.ops.spmv(self.a, x_full)
+        y = self.ops.torch.empty(self.a.n_rows, dtype=self.ops.torch.float64, device="cuda")
+        nat.check(self.ops.lib.sc_spmv_plan_apply(self.h, nat.ptr(x_full), nat.ptr(y), self.ops._s()))
+        return y
 
     def close(self):
-        pass
+        if self.h:
+            self.ops.lib.sc_spmv_plan_destroy(self.h)
+            self.h = nat.vp()
 
 
 class _SellOp:
