@@ -29,6 +29,11 @@
  *   sc_kmeanspp_*          kmeans.py:107-136        kmeanspp_init (host supplies the PCG64 draws)
  *   sc_lloyd               kmeans.py:159-196        lloyd(v, init_c, cfg)
  *   sc_ncut                metrics.py:34-67         ncut(w, labels)
+ *   sc_partition_cuts      metrics.py:42-56         cut(w, labels), ratio_cut(w, labels)
+ *   sc_csr_remove_isolated laplacian.py:34-64       handle_isolated(w, d, "remove")
+ *   sc_row_scale_f64       laplacian.py:75-81       row_scale(w, d)
+ *   sc_edge_similarity_f64 graph.py:136-147,214-237 build_similarity (cosine, cross_correlation)
+ *   sc_pattern_edges_f64   graph.py:160-176,206-211 build_edges_eps, build_edges_threshold
  */
 #ifndef SPECLUST_B200_H
 #define SPECLUST_B200_H
@@ -111,12 +116,14 @@ int sc_sell_create(int64_t n_rows, const int64_t* row_ptr, const int32_t* col, c
 int sc_sell_spmv(const sc_sell_t* op, const double* x, double* y, sc_stream_t stream);
 int sc_sell_info(const sc_sell_t* op, int64_t* stored, int64_t* n_long_rows);
 void sc_sell_destroy(sc_sell_t* op);
-/* Bulk-staged SpMV plan for repeated y = A x (the eigensolver's matvec;
- * replaces eigen.py:269-276 `_fast_apply` / sparse.py:195-207 `spmv` inside
- * the solve): ~2048-nonzero chunks of whole rows are streamed by one
- * persistent CTA per SM through a cp.async.bulk shared-memory ring while the
- * CTA's consumer warps gather x and reduce rows.  A's CSR arrays must outlive
- * the handle; n_rows may be a row shard (columns global). */
+/* SpMV plan for repeated y = A x (the eigensolver's matvec; replaces
+ * eigen.py:269-276 `_fast_apply` / sparse.py:195-207 `spmv` inside the
+ * solve): built once (nnz read once, chunk table), applied without host
+ * syncs.  Default kernel: one contiguous row range per SM, 16 lanes per row
+ * (best measured on the C2 operator); SPECLUST_SPMV_KERNEL=bulk selects the
+ * cp.async.bulk-staged chunk pipeline (one persistent CTA per SM streams
+ * ~2048-nonzero chunks of whole rows through a shared-memory ring).  A's CSR
+ * arrays must outlive the handle; n_rows may be a row shard (columns global). */
 typedef struct sc_spmv_plan sc_spmv_plan_t;
 int sc_spmv_plan_create(int64_t n_rows, const int64_t* row_ptr, const int32_t* col, const double* vals,
                         sc_stream_t stream, sc_spmv_plan_t** out);
@@ -298,6 +305,37 @@ int sc_ncut_partials(int64_t n_local, int64_t row_offset, const int64_t* row_ptr
 int sc_ncut(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* vals,
             const int64_t* labels, int64_t k, int skip_empty, double* out, int64_t* occupied,
             sc_stream_t stream);
+/* cut and ratio_cut (metrics.py:42-56: cut(w, labels), ratio_cut(w, labels)):
+ * *cut_out = 1/2 of the crossing weight, *ratio_out = 1/2 sum_c bnd_c/|c|;
+ * *empty_part (host) = first empty part (ratio_cut raises EmptyPart) or -1. */
+int sc_partition_cuts(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* vals,
+                      const int64_t* labels, int64_t k, double* cut_out, double* ratio_out, int64_t* empty_part,
+                      sc_stream_t stream);
+/* handle_isolated(w, d, "remove") (laplacian.py:34-64): induced submatrix on
+ * the nodes with d != 0.  remap (dev, n): new index or -1; outputs are
+ * caller-allocated with the input sizes (row_ptr n+1, col/vals nnz, d n);
+ * *n_new / *nnz_new (host) receive the reduced sizes. */
+int sc_csr_remove_isolated(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* vals,
+                           const double* d, int64_t* remap, int64_t* out_row_ptr, int32_t* out_col,
+                           double* out_vals, double* out_d, int64_t* n_new, int64_t* nnz_new, sc_stream_t stream);
+/* cosine / cross-correlation similarity of each (i, j) pair of `pairs`
+ * (m x 2 int64, dev) (graph.py:136-147 + the negative policy, graph.py:229-
+ * 236): kind 1 cosine, 2 cross_correlation; negative_policy 0 clamp_zero,
+ * 1 abs, 2 keep.  A zero-norm (cosine) / constant (cross_correlation)
+ * endpoint returns SC_ERR_VALUE with *degenerate (host) = its index
+ * (DegenerateVector). */
+int sc_edge_similarity_f64(int64_t n, int64_t d, const double* x, int64_t m, const int64_t* pairs, int kind,
+                           int negative_policy, double* out, int64_t* degenerate, sc_stream_t stream);
+/* eps / threshold patterns (graph.py:160-176, 206-211): (i < j) pairs in
+ * row-major order.  mode 0 eps (a = eps), 1 threshold exp_decay (a = lambda,
+ * b = sigma), 2 threshold cosine, 3 threshold cross_correlation (a = lambda).
+ * Call with pairs == NULL for the count (*m_out, host), then with a
+ * caller-allocated m x 2 int64 (dev) buffer. */
+int sc_pattern_edges_f64(int64_t n, int64_t d, const double* x, int mode, double a, double b, int64_t* pairs,
+                         int64_t* m_out, int64_t* degenerate, sc_stream_t stream);
+/* row_scale(w, d) (laplacian.py:75-81): out = vals / d[row], IEEE division. */
+int sc_row_scale_f64(int64_t n, const int64_t* row_ptr, const double* vals, const double* d, double* out,
+                     sc_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -127,6 +127,52 @@ def edge_weights(x, e: np.ndarray, sigma: float) -> np.ndarray:
     return np.maximum(np.exp(-d2 / (2.0 * sigma**2)), 0.0)
 
 
+def edge_similarity(x, e: np.ndarray, kind: str, negative_policy: str = "clamp_zero") -> np.ndarray:
+    """graph.py:136-147 + 229-236 for the cosine / cross_correlation
+    measures: one value per (i < j) edge, then the negative policy.  Raises
+    ValueError(index) for a degenerate (zero-norm / constant) involved point."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    e = np.asarray(e, dtype=np.int64).reshape(-1, 2)
+    xc = x - x.mean(axis=1, keepdims=True) if kind == "cross_correlation" else x
+    sq = np.einsum("ij,ij->i", xc, xc)
+    bad = np.flatnonzero(sq == 0.0)
+    bad = bad[np.isin(bad, np.unique(e))]
+    if len(bad):
+        raise ValueError(int(bad[0]))
+    ei, ej = e[:, 0], e[:, 1]
+    v = np.clip(np.einsum("ij,ij->i", xc[ei], xc[ej]) / np.sqrt(sq[ei] * sq[ej]), -1.0, 1.0)
+    if negative_policy == "clamp_zero":
+        v = np.maximum(v, 0.0)
+    elif negative_policy == "abs":
+        v = np.abs(v)
+    return v
+
+
+def eps_edges(x, eps: float) -> np.ndarray:
+    """graph.py:160-176: pairs (i < j) with d2 <= eps^2, row-major."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    eps2 = eps * eps
+    out = []
+    for i in range(x.shape[0] - 1):
+        d2 = np.einsum("ij,ij->i", x[i + 1:] - x[i], x[i + 1:] - x[i])
+        hits = np.flatnonzero(d2 <= eps2) + i + 1
+        out.append(np.column_stack((np.full(len(hits), i, dtype=np.int64), hits)))
+    return np.concatenate(out) if out else np.empty((0, 2), dtype=np.int64)
+
+
+def threshold_edges_exp(x, lam: float, sigma: float) -> np.ndarray:
+    """graph.py:206-211 with the exp_decay measure (graph.py:149-157):
+    pairs (i < j) with exp(inv * d2) > lam."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    inv = -1.0 / (2.0 * sigma**2)
+    out = []
+    for i in range(x.shape[0] - 1):
+        s = np.exp(inv * np.einsum("ij,ij->i", x - x[i], x - x[i]))
+        hits = np.flatnonzero(s[i + 1:] > lam) + i + 1
+        out.append(np.column_stack((np.full(len(hits), i, dtype=np.int64), hits)))
+    return np.concatenate(out) if out else np.empty((0, 2), dtype=np.int64)
+
+
 def csr_from_edges(n: int, e: np.ndarray, w: np.ndarray):
     """Mirror each pair and sort by (row, col) (graph.py:232-237,
     sparse.py:145-170), then compress rows (sparse.py:182-187)."""
@@ -164,6 +210,26 @@ def sym_scale_vals(row_ptr, col, vals, d) -> np.ndarray:
     if np.any(d <= 0.0):
         raise ValueError("non-positive degree")
     return vals / np.sqrt(d[_row_ids(row_ptr)] * d[col])
+
+
+def row_scale_vals(row_ptr, vals, d) -> np.ndarray:
+    """laplacian.py:75-81: vals / d[row]."""
+    return vals / d[_row_ids(row_ptr)]
+
+
+def remove_isolated(row_ptr, col, vals, d):
+    """laplacian.py:53-64 (policy 'remove'): induced submatrix on d != 0,
+    returns (row_ptr, col, vals, d_kept, remap)."""
+    n = len(row_ptr) - 1
+    keep = d != 0.0
+    remap = np.full(n, -1, dtype=np.int64)
+    remap[keep] = np.arange(int(keep.sum()), dtype=np.int64)
+    rows = _row_ids(row_ptr)
+    mask = keep[rows] & keep[col]
+    n_new = int(keep.sum())
+    counts = np.bincount(remap[rows[mask]], minlength=n_new)
+    rp = np.concatenate(([0], np.cumsum(counts, dtype=np.int64)))
+    return rp, remap[col[mask]], vals[mask], d[keep], remap
 
 
 def recover_embedding(u: np.ndarray, d: np.ndarray) -> np.ndarray:
@@ -412,6 +478,26 @@ def ncut(row_ptr, col, vals, labels) -> float:
     if np.any(vol <= 0.0):
         raise ValueError("zero-volume part")
     return 0.5 * float((bnd / vol).sum())
+
+
+def cut(row_ptr, col, vals, labels) -> float:
+    """metrics.py:42-48: half the weight of the crossing entries."""
+    lab = np.asarray(labels, dtype=np.int64)
+    crossing = lab[_row_ids(row_ptr)] != lab[col]
+    return 0.5 * float(vals[crossing].sum())
+
+
+def ratio_cut(row_ptr, col, vals, labels, k: int) -> float:
+    """metrics.py:51-56: half the sum of boundary weight / part size
+    (ValueError for an empty part, EmptyPart in the package)."""
+    lab = np.asarray(labels, dtype=np.int64)
+    sizes = np.bincount(lab, minlength=k)
+    if np.any(sizes == 0):
+        raise ValueError("empty part")
+    rows = _row_ids(row_ptr)
+    crossing = lab[rows] != lab[col]
+    bnd = np.bincount(lab[rows[crossing]], weights=vals[crossing], minlength=k)
+    return 0.5 * float((bnd / sizes).sum())
 
 
 def ari(a, b) -> float:

@@ -86,6 +86,11 @@ SIGNATURES = {
     "sc_kmeanspp_pick": (i32, [vp, i32, f64, i64, P_i64]),
     "sc_lloyd": (i32, [i64, i64, i64, vp, vp, i64, i64, vp, vp, P_f64, P_i64, vp]),
     "sc_ncut": (i32, [i64, vp, vp, vp, vp, i64, i32, P_f64, P_i64, vp]),
+    "sc_partition_cuts": (i32, [i64, vp, vp, vp, vp, i64, P_f64, P_f64, P_i64, vp]),
+    "sc_csr_remove_isolated": (i32, [i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, P_i64, P_i64, vp]),
+    "sc_row_scale_f64": (i32, [i64, vp, vp, vp, vp, vp]),
+    "sc_edge_similarity_f64": (i32, [i64, i64, vp, i64, vp, i32, i32, vp, P_i64, vp]),
+    "sc_pattern_edges_f64": (i32, [i64, i64, vp, i32, f64, f64, vp, P_i64, P_i64, vp]),
     "sc_gemv_t_f64": (i32, [i64, i64, i64, vp, vp, vp, vp]),
     "sc_gemv_n_f64": (i32, [i64, i64, i64, vp, vp, vp, vp, vp]),
     "sc_fill_normal": (i32, [i64, i64, C.c_uint64, C.c_uint64, vp, vp]),

@@ -1559,5 +1559,52 @@ int sc_ncut(int64_t n, const int64_t* row_ptr, const int32_t* col, const double*
     return SC_OK;
 }
 
+// cut and ratio_cut (metrics.py:34-56): per-row crossing weights, per-part
+// boundary sums in member order, sizes from the label buckets.
+// cut = 1/2 sum_i cross_i; ratio_cut = 1/2 sum_c bnd_c / size_c (numpy's
+// pairwise order over parts).  *empty_part = first empty part (ratio_cut's
+// EmptyPart) or -1.
+int sc_partition_cuts(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* vals,
+                      const int64_t* labels, int64_t k, double* cut_out, double* ratio_out, int64_t* empty_part,
+                      sc_stream_t stream) {
+    if (n < 1 || k < 1) return fail(SC_ERR_VALUE, "cut metrics need n >= 1 and k >= 1");
+    cudaStream_t st = as_stream(stream);
+    StreamScope stream_scope(st);
+    DevBuf<double> deg, cross, bnd, vol, tot;
+    Bucketer bk;
+    int rc;
+    if ((rc = deg.alloc(n)) || (rc = cross.alloc(n)) || (rc = bnd.alloc(k)) || (rc = vol.alloc(k)) ||
+        (rc = tot.alloc(1)) || (rc = bk.init(n, k)))
+        return rc;
+    if ((rc = bk.run(labels, st))) return rc;
+    ncut_rows_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, st>>>(n, row_ptr, col, vals, labels, deg.p, cross.p);
+    ncut_parts_kernel<<<(unsigned)ceil_div(k, 64), 64, 0, st>>>(k, deg.p, cross.p, bk.start.p, bk.members.p, bnd.p,
+                                                                 vol.p);
+    sum_partials_kernel<<<1, 1024, 0, st>>>(n, cross.p, tot.p);
+    SC_LAUNCHED(3);
+    std::vector<double> hb(k);
+    std::vector<int64_t> hs(k + 1);
+    double htot = 0.0;
+    SC_CUDA(cudaMemcpyAsync(hb.data(), bnd.p, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
+    SC_CUDA(cudaMemcpyAsync(hs.data(), bk.start.p, sizeof(int64_t) * (k + 1), cudaMemcpyDeviceToHost, st));
+    SC_CUDA(cudaMemcpyAsync(&htot, tot.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+    SC_CUDA(cudaStreamSynchronize(st));
+    *cut_out = 0.5 * htot;
+    *empty_part = -1;
+    std::vector<double> q(k);
+    for (int64_t c = 0; c < k; ++c) {
+        const int64_t size = hs[c + 1] - hs[c];
+        if (size == 0) {
+            if (*empty_part < 0) *empty_part = c;
+            q[c] = 0.0;
+        } else {
+            q[c] = hb[c] / (double)size;
+        }
+    }
+    *ratio_out = *empty_part >= 0 ? -1.0 : 0.5 * np_pairwise_sum(q.data(), k);
+    return SC_OK;
+}
+
 }  // extern "C"
+
 

@@ -1134,3 +1134,114 @@ extern "C" int sc_spmv_plan_apply(const sc_spmv_plan* h, const double* x, double
     return h->p.apply(x, y, sc::as_stream(stream));
 }
 extern "C" void sc_spmv_plan_destroy(sc_spmv_plan* h) { delete h; }
+
+// ---------------------------------------------------------------------------
+// Input cleaning and row scaling (laplacian.py:34-81)
+namespace sc {
+__global__ void keep_flags_kernel(int64_t n, const double* __restrict__ d, int64_t* __restrict__ flag) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) flag[i] = d[i] != 0.0;
+}
+// remap[i] = new index of node i (exclusive scan of keep flags) or -1
+__global__ void remap_kernel(int64_t n, const double* __restrict__ d, const int64_t* __restrict__ scan,
+                             int64_t* __restrict__ remap, double* __restrict__ d_out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (d[i] != 0.0) {
+        remap[i] = scan[i];
+        d_out[scan[i]] = d[i];
+    } else {
+        remap[i] = -1;
+    }
+}
+// kept entries per kept row (warp per row)
+__global__ void induced_count_kernel(int64_t n, const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                                     const int64_t* __restrict__ remap, int64_t* __restrict__ len) {
+    const int64_t i = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    if (i >= n || remap[i] < 0) return;
+    int64_t c = 0;
+    for (int64_t p = row_ptr[i] + lane; p < row_ptr[i + 1]; p += 32) c += remap[col[p]] >= 0;
+    c = warp_sum_i64(c);
+    if (lane == 0) len[remap[i]] = c;
+}
+// entries of kept rows with kept columns, order preserved (warp ballot scan)
+__global__ void induced_fill_kernel(int64_t n, const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                                    const double* __restrict__ vals, const int64_t* __restrict__ remap,
+                                    const int64_t* __restrict__ out_ptr, int32_t* __restrict__ out_col,
+                                    double* __restrict__ out_vals) {
+    const int64_t i = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    if (i >= n || remap[i] < 0) return;
+    int64_t o = out_ptr[remap[i]];
+    for (int64_t p0 = row_ptr[i]; p0 < row_ptr[i + 1]; p0 += 32) {
+        const int64_t p = p0 + lane;
+        const int64_t rc = p < row_ptr[i + 1] ? remap[col[p]] : -1;
+        const unsigned m = __ballot_sync(0xffffffffu, rc >= 0);
+        if (rc >= 0) {
+            const int64_t q = o + __popc(m & ((1u << lane) - 1u));
+            out_col[q] = (int32_t)rc;
+            out_vals[q] = vals[p];
+        }
+        o += __popc(m);
+    }
+}
+__global__ void row_scale_kernel(int64_t n, const int64_t* __restrict__ row_ptr, const double* __restrict__ vals,
+                                 const double* __restrict__ d, double* __restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    if (i >= n) return;
+    const double di = d[i];
+    for (int64_t p = row_ptr[i] + (threadIdx.x & 31); p < row_ptr[i + 1]; p += 32) out[p] = __ddiv_rn(vals[p], di);
+}
+}  // namespace sc
+
+// Induced submatrix on the nonzero-degree nodes (handle_isolated 'remove'):
+// outputs are caller-allocated with the input sizes (n + 1, nnz, n); the new
+// sizes come back in *n_new / *nnz_new.
+extern "C" int sc_csr_remove_isolated(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* vals,
+                                      const double* d, int64_t* remap, int64_t* out_row_ptr, int32_t* out_col,
+                                      double* out_vals, double* out_d, int64_t* n_new, int64_t* nnz_new,
+                                      sc_stream_t stream) {
+    using namespace sc;
+    cudaStream_t st = as_stream(stream);
+    StreamScope stream_scope(st);
+    *n_new = 0;
+    *nnz_new = 0;
+    if (n <= 0) return SC_OK;
+    DevBuf<int64_t> flag, scan, len, tmp;
+    int rc;
+    if ((rc = flag.alloc(n)) || (rc = scan.alloc(n + 1)) || (rc = len.alloc(n)) ||
+        (rc = tmp.alloc(ceil_div(n, SCAN_BLK) + 1)))
+        return rc;
+    keep_flags_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, d, flag.p);
+    SC_LAUNCHED(1);
+    if ((rc = exclusive_scan_i64(n, flag.p, scan.p, tmp.p, st))) return rc;
+    SC_CUDA(cudaMemcpyAsync(n_new, scan.p + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    remap_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, d, scan.p, remap, out_d);
+    induced_count_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, st>>>(n, row_ptr, col, remap, len.p);
+    SC_LAUNCHED(2);
+    SC_CUDA(cudaStreamSynchronize(st));
+    if (*n_new == 0) {
+        SC_CUDA(cudaMemsetAsync(out_row_ptr, 0, sizeof(int64_t), st));
+        SC_CUDA(cudaStreamSynchronize(st));
+        return SC_OK;
+    }
+    if ((rc = exclusive_scan_i64(*n_new, len.p, out_row_ptr, tmp.p, st))) return rc;
+    induced_fill_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, st>>>(n, row_ptr, col, vals, remap, out_row_ptr, out_col,
+                                                                  out_vals);
+    SC_LAUNCHED(1);
+    SC_CUDA(cudaMemcpyAsync(nnz_new, out_row_ptr + *n_new, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    SC_CUDA(cudaStreamSynchronize(st));
+    return SC_OK;
+}
+
+// out[p] = vals[p] / d[row(p)] (row_scale, laplacian.py:75-81; IEEE division,
+// bit-identical to the reference)
+extern "C" int sc_row_scale_f64(int64_t n, const int64_t* row_ptr, const double* vals, const double* d, double* out,
+                                sc_stream_t stream) {
+    using namespace sc;
+    if (n <= 0) return SC_OK;
+    row_scale_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, as_stream(stream)>>>(n, row_ptr, vals, d, out);
+    SC_LAUNCHED(1);
+    return SC_OK;
+}

@@ -7,9 +7,10 @@ an error bound, an exact fallback for uncertified rows, and union
 symmetrisation written straight into CSR.  The ranking key and edge values
 follow graph.py:149-157 / 136-141 of the reference.
 
-Other measures (cosine, cross-correlation) and the eps / threshold patterns
-are outside this round's hot-path scope and raise
-``NotImplementedError`` instead of silently running on the host.
+The other measures (cosine, cross-correlation) over a given edge list and the
+eps / threshold patterns run on the GPU as well
+(sc_patterns.cu); the kNN pattern with cosine / cross-correlation is not
+implemented and raises ``NotImplementedError`` (no host fallback).
 """
 
 from __future__ import annotations
@@ -221,32 +222,65 @@ def build_edges_knn(x, knn: int, m: SimilarityMeasure) -> np.ndarray:
     return np.column_stack((rows[upper], cols[upper]))
 
 
+def _pattern_edges(x: np.ndarray, mode: int, a: float, b: float) -> np.ndarray:
+    """(i < j) pairs of the eps / threshold patterns, computed on the GPU
+    (sc_pattern_edges_f64: count, then fill)."""
+    torch = nat.torch_cuda()
+    n, d = x.shape
+    xd = nat.to_device(x, torch.float64)
+    lib = nat.load()
+    m, deg = nat.C.c_int64(), nat.C.c_int64()
+    rc = lib.sc_pattern_edges_f64(n, d, nat.ptr(xd), mode, a, b, None, nat.C.byref(m), nat.C.byref(deg),
+                                  nat.stream_handle())
+    if rc != 0 and deg.value >= 0:
+        raise DegenerateVector(nat.last_error(), index=int(deg.value))
+    nat.check(rc)
+    if m.value == 0:
+        return np.empty((0, 2), dtype=np.int64)
+    out = torch.empty((m.value, 2), dtype=torch.int64, device="cuda")
+    nat.check(lib.sc_pattern_edges_f64(n, d, nat.ptr(xd), mode, a, b, nat.ptr(out), nat.C.byref(m),
+                                       nat.C.byref(deg), nat.stream_handle()))
+    return nat.to_host(out)
+
+
 def build_edges_eps(x, eps: float) -> np.ndarray:
-    raise NotImplementedError("eps-graph pattern is out of this round's device scope (SURVEY.md §8(f) F3)")
+    """Pairs (i, j), i < j, with Euclidean distance at most ``eps``
+    (reference graph.py:160-176); d2 in numpy's einsum order on the GPU."""
+    x = as_points(x)
+    if not eps > 0:
+        raise ValueError("eps must be positive")
+    return _pattern_edges(x, 0, float(eps), 0.0)
 
 
 def build_edges_threshold(x, lam: float, m: SimilarityMeasure) -> np.ndarray:
-    raise NotImplementedError("threshold pattern is out of this round's device scope (SURVEY.md §8(f) F3)")
+    """Pairs (i, j), i < j, whose similarity strictly exceeds ``lam``
+    (reference graph.py:206-211), on the GPU.  exp_decay: the reference's
+    exp(inv * d2) with d2 in the einsum order; cosine / cross_correlation:
+    dot / sqrt(sq_i sq_j) with the dot in the einsum order (the reference
+    forms these with a BLAS GEMM, so pairs within rounding of lam may differ)."""
+    x = as_points(x)
+    if m.kind == "exp_decay":
+        return _pattern_edges(x, 1, float(lam), float(m.sigma))
+    return _pattern_edges(x, 2 if m.kind == "cosine" else 3, float(lam), 0.0)
 
 
 def build_similarity(x, e, m: SimilarityMeasure, negative_policy: str = "clamp_zero") -> CooMatrix:
     """Symmetric similarity matrix over a given edge pattern: one value per
     unordered pair, mirrored (reference graph.py:214-237).  Values are
-    computed on the GPU."""
+    computed on the GPU for every measure."""
     x = as_points(x)
     n = x.shape[0]
     e = validate_edges(e, n)
     if negative_policy not in NEGATIVE_POLICIES:
         raise ValueError(f"unknown negative_policy {negative_policy!r}")
-    _require_exp_decay(m, "build_similarity")
-    vals = _pair_weights(x, e, m)
-    # exp >= 0: clamp_zero / abs / keep are all identities (graph.py:230-233)
+    vals = _pair_weights(x, e, m, negative_policy)
     rows = np.concatenate((e[:, 0], e[:, 1]))
     cols = np.concatenate((e[:, 1], e[:, 0]))
     return coo_canonicalize(CooMatrix(n, n, rows, cols, np.concatenate((vals, vals))), dup_policy="error")
 
 
-def _pair_weights(x: np.ndarray, e: np.ndarray, m: SimilarityMeasure) -> np.ndarray:
+def _pair_weights(x: np.ndarray, e: np.ndarray, m: SimilarityMeasure,
+                  negative_policy: str = "clamp_zero") -> np.ndarray:
     torch = nat.torch_cuda()
     if len(e) == 0:
         return np.zeros(0)
@@ -254,6 +288,18 @@ def _pair_weights(x: np.ndarray, e: np.ndarray, m: SimilarityMeasure) -> np.ndar
     ed = nat.to_device(e.astype(np.int64), torch.int64)
     out = torch.empty(len(e), dtype=torch.float64, device="cuda")
     lib = nat.load()
-    nat.check(lib.sc_pair_weights(x.shape[0], x.shape[1], nat.ptr(xd), len(e), nat.ptr(ed), m.two_sigma_sq(),
-                                  nat.ptr(out), nat.stream_handle()))
+    if m.kind == "exp_decay":
+        # exp >= 0: clamp_zero / abs / keep are all identities (graph.py:230-233)
+        nat.check(lib.sc_pair_weights(x.shape[0], x.shape[1], nat.ptr(xd), len(e), nat.ptr(ed), m.two_sigma_sq(),
+                                      nat.ptr(out), nat.stream_handle()))
+        return nat.to_host(out)
+    deg = nat.C.c_int64()
+    rc = lib.sc_edge_similarity_f64(x.shape[0], x.shape[1], nat.ptr(xd), len(e), nat.ptr(ed),
+                                    1 if m.kind == "cosine" else 2, NEGATIVE_POLICIES.index(negative_policy),
+                                    nat.ptr(out), nat.C.byref(deg), nat.stream_handle())
+    if rc != 0 and deg.value >= 0:
+        what = "constant" if m.kind == "cross_correlation" else "zero"
+        raise DegenerateVector(f"{what} vector at point index {deg.value} is invalid for {m.kind}",
+                               index=int(deg.value))
+    nat.check(rc)
     return nat.to_host(out)

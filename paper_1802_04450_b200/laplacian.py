@@ -66,21 +66,23 @@ def handle_isolated(w, d, policy: str = "error"):
     _, idx = nonpositive_device(dd, 0, count)
     if policy == "error":
         raise IsolatedNode(idx)
-    # 'remove' (input cleaning): induced submatrix
-    host = w.to_host() if isinstance(w, DeviceCsr) else w
-    dh = nat.to_host(dd)
-    keep = dh != 0.0
-    remap = np.full(n, -1, dtype=np.int64)
-    remap[keep] = np.arange(int(keep.sum()), dtype=np.int64)
-    rows = host.row_indices()
-    m = keep[rows] & keep[host.col_idx]
-    n_new = int(keep.sum())
-    row_ptr = np.zeros(n_new + 1, dtype=np.int64)
-    np.cumsum(np.bincount(remap[rows[m]], minlength=n_new), out=row_ptr[1:])
-    sub = CsrMatrix(n_new, n_new, row_ptr, remap[host.col_idx[m]], host.vals[m])
+    # 'remove' (input cleaning): induced submatrix on device
+    dw = _dev(w)
+    remap = torch.empty(n, dtype=torch.int64, device="cuda")
+    rp = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+    col = torch.empty_like(dw.col)
+    vals = torch.empty_like(dw.vals)
+    d_out = torch.empty(n, dtype=torch.float64, device="cuda")
+    n_new, nnz_new = nat.C.c_int64(), nat.C.c_int64()
+    nat.check(nat.load().sc_csr_remove_isolated(n, nat.ptr(dw.row_ptr), nat.ptr(dw.col), nat.ptr(dw.vals),
+                                                nat.ptr(dd), nat.ptr(remap), nat.ptr(rp), nat.ptr(col),
+                                                nat.ptr(vals), nat.ptr(d_out), nat.C.byref(n_new),
+                                                nat.C.byref(nnz_new), nat.stream_handle()))
+    m, z = n_new.value, nnz_new.value
+    sub = DeviceCsr(m, m, rp[: m + 1], col[:z], vals[:z])
     if isinstance(w, DeviceCsr):
-        return sub.device(), dd[torch.from_numpy(keep).to("cuda")], remap
-    return sub, dh[keep], remap
+        return sub, d_out[:m], nat.to_host(remap)
+    return sub.to_host(), nat.to_host(d_out[:m]), nat.to_host(remap)
 
 
 def _positive(d):
@@ -108,13 +110,21 @@ def sym_scale(w, d):
     return CsrMatrix(w.n_rows, w.n_cols, w.row_ptr, w.col_idx, nat.to_host(out))
 
 
-def row_scale(w: CsrMatrix, d) -> CsrMatrix:
-    """Row-stochastic D^-1 W (reference laplacian.py:75-81); test helper
-    only, outside the hot path — kept for API completeness."""
-    dh = nat.to_host(_positive(d))
-    if len(dh) != w.n_rows:
-        raise DimensionMismatch(f"degree vector length {len(dh)} does not match n_rows {w.n_rows}")
-    return CsrMatrix(w.n_rows, w.n_cols, w.row_ptr, w.col_idx, w.vals / dh[w.row_indices()])
+def row_scale(w, d) -> CsrMatrix:
+    """Row-stochastic D^-1 W (reference laplacian.py:75-81) on device:
+    out = vals / d[row] with IEEE division (bit-identical)."""
+    torch = nat.torch_cuda()
+    dd = _positive(d)
+    if int(dd.numel()) != w.n_rows:
+        raise DimensionMismatch(f"degree vector length {int(dd.numel())} does not match n_rows {w.n_rows}")
+    dw = _dev(w)
+    out = torch.empty_like(dw.vals)
+    nat.check(nat.load().sc_row_scale_f64(dw.n_rows, nat.ptr(dw.row_ptr), nat.ptr(dw.vals), nat.ptr(dd),
+                                          nat.ptr(out), nat.stream_handle()))
+    res = dw.with_vals(out)
+    if isinstance(w, DeviceCsr):
+        return res
+    return CsrMatrix(w.n_rows, w.n_cols, w.row_ptr, w.col_idx, nat.to_host(out))
 
 
 def recover_embedding_device(u, d, normalize_rows: bool):

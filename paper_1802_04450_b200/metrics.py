@@ -35,23 +35,31 @@ def _host(w) -> CsrMatrix:
     return w.to_host() if isinstance(w, DeviceCsr) else w
 
 
+def _cuts_device(w, labels, k):
+    """(cut, ratio_cut, first empty part or -1) on device (sc_partition_cuts)."""
+    torch = nat.torch_cuda()
+    n = w.n_rows
+    lab, k = _labels(labels, n, k)
+    d = w if isinstance(w, DeviceCsr) else w.device()
+    c, r, e = nat.C.c_double(), nat.C.c_double(), nat.C.c_int64()
+    nat.check(nat.load().sc_partition_cuts(n, nat.ptr(d.row_ptr), nat.ptr(d.col), nat.ptr(d.vals),
+                                           nat.ptr(nat.to_device(lab, torch.int64)), k, nat.C.byref(c),
+                                           nat.C.byref(r), nat.C.byref(e), nat.stream_handle()))
+    return c.value, r.value, e.value
+
+
 def cut(w, labels, k: int | None = None) -> float:
-    w = _host(w)
-    lab, k = _labels(labels, w.n_rows, k)
-    crossing = lab[w.row_indices()] != lab[w.col_idx]
-    return 0.5 * float(w.vals[crossing].sum())
+    """Half the weight of the edges between different parts (metrics.py:42-48)."""
+    return _cuts_device(w, labels, k)[0]
 
 
 def ratio_cut(w, labels, k: int | None = None) -> float:
-    w = _host(w)
-    lab, k = _labels(labels, w.n_rows, k)
-    sizes = np.bincount(lab, minlength=k)
-    if (sizes == 0).any():
-        raise EmptyPart(f"empty part {int(np.argmax(sizes == 0))}")
-    rows = w.row_indices()
-    crossing = lab[rows] != lab[w.col_idx]
-    bnd = np.bincount(lab[rows[crossing]], weights=w.vals[crossing], minlength=k)
-    return 0.5 * float((bnd / sizes).sum())
+    """Half the sum over parts of boundary weight / part size
+    (metrics.py:51-56); EmptyPart if a part of range(k) is empty."""
+    c, r, empty = _cuts_device(w, labels, k)
+    if empty >= 0:
+        raise EmptyPart(f"empty part {empty}")
+    return r
 
 
 def ncut_device(w: DeviceCsr, labels_dev, k: int, skip_empty: bool = False):

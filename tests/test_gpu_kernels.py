@@ -533,3 +533,60 @@ def test_lloyd_tensor_core_assignment_bit_identical(monkeypatch):
         assert np.array_equal(got.labels, ref.labels), v.shape
         assert np.array_equal(got.centroids, ref.centroids), v.shape
         assert np.array_equal(got.sse_history, ref.sse_history), v.shape
+
+
+# ---------------------------------------------------------------- §8(f) rows
+def test_f4_metrics_and_cleaning_vs_reference(golden):
+    """cut / ratio_cut / ncut, row_scale and handle_isolated('remove') on the
+    device against the real reference's outputs (tests/golden/f_rows.npz)."""
+    f = golden("f_rows")
+    g = golden("graph_blobs600")
+    w = csr(g["row_ptr"], g["col"], g["vals"])
+    lab = f["m_labels"]
+    assert abs(sc.cut(w, lab) - f["m_cut"]) <= 1e-13 * f["m_cut"]
+    assert abs(sc.ratio_cut(w, lab) - f["m_ratio"]) <= 1e-13 * f["m_ratio"]
+    assert abs(sc.ncut(w, lab) - f["m_ncut"]) <= 1e-13 * f["m_ncut"]
+    with pytest.raises(sc.errors.EmptyPart):
+        sc.ratio_cut(w, np.where(lab == 2, 1, lab), k=6)
+    d = sc.degrees(w)
+    assert np.array_equal(sc.row_scale(w, d).vals, f["rs_vals"])  # IEEE division: bit-exact
+    wi = csr(f["iso_row_ptr"], f["iso_col"], f["iso_vals"])
+    sub, dsub, remap = sc.handle_isolated(wi, sc.degrees(wi), "remove")
+    assert np.array_equal(sub.row_ptr, f["iso_sub_row_ptr"]) and np.array_equal(sub.col_idx, f["iso_sub_col"])
+    assert np.array_equal(sub.vals, f["iso_sub_vals"]) and np.array_equal(dsub, f["iso_sub_d"])
+    assert np.array_equal(remap, f["iso_remap"])
+
+
+def test_f3_measures_and_patterns_vs_reference(golden):
+    """cosine / cross-correlation edge similarities (all negative policies),
+    the eps pattern and the exp_decay threshold pattern on the device against
+    the real reference (bit-exact); degenerate points raise DegenerateVector."""
+    f = golden("f_rows")
+    g = golden("graph_blobs600")
+    for kind in ("cosine", "cross_correlation"):
+        for pol in ("clamp_zero", "abs", "keep"):
+            coo = sc.build_similarity(g["x"], g["edges"], sc.SimilarityMeasure(kind), negative_policy=pol)
+            assert np.array_equal(coo.rows, f[f"sim_{kind}_{pol}_rows"])
+            assert np.array_equal(coo.cols, f[f"sim_{kind}_{pol}_cols"])
+            assert np.array_equal(coo.vals, f[f"sim_{kind}_{pol}_vals"]), (kind, pol)
+    coo = sc.build_similarity(f["sgn_x"], f["sgn_edges"], sc.SimilarityMeasure.cosine(), negative_policy="keep")
+    assert np.array_equal(coo.vals, f["sgn_vals"])
+    assert np.array_equal(sc.build_edges_eps(f["eps_x"], float(f["eps_eps"])), f["eps_edges"])
+    assert np.array_equal(sc.build_edges_eps(f["epsd_x"], float(f["epsd_eps"])), f["epsd_edges"])
+    e = sc.build_edges_threshold(f["thr_x"], float(f["thr_lam"]), sc.SimilarityMeasure.exp_decay(float(f["thr_sigma"])))
+    assert np.array_equal(e, f["thr_edges"])
+    x = np.random.default_rng(3).standard_normal((50, 4))
+    x[7] = 0.0
+    with pytest.raises(sc.errors.DegenerateVector) as exc:
+        sc.build_similarity(x, [[7, 9], [1, 2]], sc.SimilarityMeasure.cosine())
+    assert exc.value.index == 7
+    x[11] = 3.0  # constant row: degenerate for cross_correlation only
+    sc.build_similarity(x, [[11, 9]], sc.SimilarityMeasure.cosine())
+    with pytest.raises(sc.errors.DegenerateVector):
+        sc.build_similarity(x, [[11, 9]], sc.SimilarityMeasure.cross_correlation())
+    # cosine threshold vs the oracle's cosine values (einsum-order dots)
+    xs = f["sgn_x"]
+    e = sc.build_edges_threshold(xs, 0.5, sc.SimilarityMeasure.cosine())
+    allp = np.array([[i, j] for i in range(len(xs)) for j in range(i + 1, len(xs))])
+    v = orc.edge_similarity(xs, allp, "cosine", "keep")
+    assert np.array_equal(e, allp[v > 0.5])

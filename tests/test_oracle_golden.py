@@ -84,3 +84,40 @@ def test_ari_hand_values():
     assert orc.ari([0, 0, 1, 1], [1, 1, 0, 0]) == 1.0
     assert orc.ari([], []) == 1.0
     assert orc.ari([0, 0, 1, 1], [0, 1, 0, 1]) < 0.0
+
+
+def test_f_rows_oracle_bit_exact(golden):
+    """Oracle restatements of the §8(f) rows (F3 patterns / measures, F4
+    metrics and input cleaning) against the real reference (make_golden_f.py)."""
+    f = golden("f_rows")
+    g = golden("graph_blobs600")
+    rp, col, vals = g["row_ptr"], g["col"], g["vals"]
+    lab = f["m_labels"]
+    assert orc.cut(rp, col, vals, lab) == f["m_cut"]
+    assert orc.ratio_cut(rp, col, vals, lab, 6) == f["m_ratio"]
+    assert orc.ncut(rp, col, vals, lab) == f["m_ncut"]
+    d = orc.degrees(rp, col, vals)
+    assert np.array_equal(orc.row_scale_vals(rp, vals, d), f["rs_vals"])
+    irp, icol, ivals = f["iso_row_ptr"], f["iso_col"], f["iso_vals"]
+    srp, scol, svals, sd, remap = orc.remove_isolated(irp, icol, ivals, orc.degrees(irp, icol, ivals))
+    assert np.array_equal(srp, f["iso_sub_row_ptr"]) and np.array_equal(scol, f["iso_sub_col"])
+    assert np.array_equal(svals, f["iso_sub_vals"]) and np.array_equal(sd, f["iso_sub_d"])
+    assert np.array_equal(remap, f["iso_remap"])
+    e = g["edges"]
+    for kind in ("cosine", "cross_correlation"):
+        for pol in ("clamp_zero", "abs", "keep"):
+            v = orc.edge_similarity(g["x"], e, kind, pol)
+            want = f[f"sim_{kind}_{pol}_vals"]
+            # the reference emits the mirrored COO in canonical (row, col) order
+            rows = np.concatenate((e[:, 0], e[:, 1]))
+            cols = np.concatenate((e[:, 1], e[:, 0]))
+            order = np.lexsort((cols, rows))
+            assert np.array_equal(np.concatenate((v, v))[order], want)
+    v = orc.edge_similarity(f["sgn_x"], f["sgn_edges"], "cosine", "keep")
+    es = f["sgn_edges"]
+    order = np.lexsort((np.concatenate((es[:, 1], es[:, 0])), np.concatenate((es[:, 0], es[:, 1]))))
+    assert np.array_equal(np.concatenate((v, v))[order], f["sgn_vals"])
+    assert np.array_equal(orc.eps_edges(f["eps_x"], float(f["eps_eps"])), f["eps_edges"])
+    assert np.array_equal(orc.eps_edges(f["epsd_x"], float(f["epsd_eps"])), f["epsd_edges"])
+    assert np.array_equal(orc.threshold_edges_exp(f["thr_x"], float(f["thr_lam"]), float(f["thr_sigma"])),
+                          f["thr_edges"])
