@@ -60,6 +60,19 @@ def main():
     # ---- F3: threshold pattern (exp_decay)
     out.update(thr_x=xe, thr_sigma=2.0, thr_lam=0.3,
                thr_edges=sp.build_edges_threshold(xe, 0.3, sp.SimilarityMeasure.exp_decay(2.0)))
+    # ---- F3 through the pipeline: eps + exp_decay and threshold + cosine
+    xp, truth = blobs(400, 6, 4, 4.0, seed=5)
+    cfg = sp.PipelineConfig(
+        input=sp.PointsInput(measure=sp.SimilarityMeasure.exp_decay(2.0), pattern="eps", points=xp, eps=4.0),
+        k_clusters=4, eigen=sp.LanczosConfig(k=4, seed=0), kmeans=sp.KmeansConfig(k=4, seed=0), normalize_rows=True)
+    rep = sp.run(cfg)
+    out.update(pe_x=xp, pe_truth=truth, pe_labels=rep.labeling.labels, pe_values=rep.eigenvalues, pe_ncut=rep.ncut_value)
+    cfg = sp.PipelineConfig(
+        input=sp.PointsInput(measure=sp.SimilarityMeasure.cosine(), pattern="threshold", points=xp + 10.0,
+                             threshold=0.99),
+        k_clusters=4, eigen=sp.LanczosConfig(k=4, seed=0), kmeans=sp.KmeansConfig(k=4, seed=0), normalize_rows=True)
+    rep = sp.run(cfg)
+    out.update(pt_labels=rep.labeling.labels, pt_values=rep.eigenvalues)
     np.savez_compressed(HERE / "f_rows.npz", **out)
     print("f_rows.npz written", {k: v.shape for k, v in out.items() if hasattr(v, "shape")})
 

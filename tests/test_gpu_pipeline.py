@@ -164,3 +164,25 @@ def test_pipeline_locality_order_eigen(golden, monkeypatch, flag):
     assert np.array_equal(np.sort(perm), np.arange(len(perm)))
     assert np.max(np.abs(rep.eigenvalues - g["values"]) / np.abs(g["values"])) < 1e-5
     assert orc.ari(rep.labeling.labels, g["labels"]) >= 0.999
+
+
+def test_pipeline_eps_and_threshold_patterns_vs_reference(golden):
+    """run() with the eps pattern (exp_decay) and the threshold pattern
+    (cosine) -- graph built on the device -- against the real reference's
+    run() on the same inputs (tests/golden/f_rows.npz)."""
+    f = golden("f_rows")
+    x = f["pe_x"]
+    cfg = sc.PipelineConfig(
+        input=sc.PointsInput(measure=sc.SimilarityMeasure.exp_decay(2.0), pattern="eps", points=x, eps=4.0),
+        k_clusters=4, eigen=sc.LanczosConfig(k=4, seed=0), kmeans=sc.KmeansConfig(k=4, seed=0), normalize_rows=True)
+    rep = sc.run(cfg)
+    assert np.max(np.abs(rep.eigenvalues - f["pe_values"])) <= 1e-8
+    assert orc.ari(rep.labeling.labels, f["pe_labels"]) >= 0.999
+    assert abs(rep.ncut_value - float(f["pe_ncut"])) <= 1e-9 * max(1.0, abs(float(f["pe_ncut"])))
+    cfg = sc.PipelineConfig(
+        input=sc.PointsInput(measure=sc.SimilarityMeasure.cosine(), pattern="threshold", points=x + 10.0,
+                             threshold=0.99),
+        k_clusters=4, eigen=sc.LanczosConfig(k=4, seed=0), kmeans=sc.KmeansConfig(k=4, seed=0), normalize_rows=True)
+    rep = sc.run(cfg)
+    assert np.max(np.abs(rep.eigenvalues - f["pt_values"])) <= 1e-8
+    assert orc.ari(rep.labeling.labels, f["pt_labels"]) >= 0.999
