@@ -326,6 +326,14 @@ int sc_csr_remove_isolated(int64_t n, const int64_t* row_ptr, const int32_t* col
  * (DegenerateVector). */
 int sc_edge_similarity_f64(int64_t n, int64_t d, const double* x, int64_t m, const int64_t* pairs, int kind,
                            int negative_policy, double* out, int64_t* degenerate, sc_stream_t stream);
+/* union-kNN similarity graph for any measure (graph.py:149-163, 185-237):
+ * kind 0 exp_decay (sigma), 1 cosine, 2 cross_correlation; negative_policy
+ * 0 clamp_zero, 1 abs, 2 keep.  Outputs as sc_knn_graph_f64 (capacity
+ * 2 n knn).  A degenerate point returns SC_ERR_VALUE with *degenerate (host)
+ * = its index (DegenerateVector). */
+int sc_knn_graph_measure_f64(int64_t n, int64_t d, const double* x, int64_t knn, int kind, double sigma,
+                             int negative_policy, int64_t* row_ptr, int32_t* col, double* vals, int64_t* nnz_out,
+                             int64_t* stats_out, int64_t* degenerate, sc_stream_t stream);
 /* eps / threshold patterns (graph.py:160-176, 206-211): (i < j) pairs in
  * row-major order.  mode 0 eps (a = eps), 1 threshold exp_decay (a = lambda,
  * b = sigma), 2 threshold cosine, 3 threshold cross_correlation (a = lambda).

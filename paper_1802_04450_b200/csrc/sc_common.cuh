@@ -202,4 +202,30 @@ __device__ __forceinline__ double np_sqnorm(const double* __restrict__ a, int64_
     return s.result();
 }
 
+// numpy's pairwise summation of a contiguous float64 run (pairwise.c: blocks
+// of 8 accumulators up to 128 elements, halving above)
+inline __device__ double np_pairwise_sum_dev(const double* a, int64_t n) {
+    if (n < 8) {
+        double res = 0.0;  // numpy's short loop starts from +0.0
+        for (int64_t i = 0; i < n; ++i) res = __dadd_rn(res, a[i]);
+        return res;
+    }
+    if (n <= 128) {
+        double r[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = a[j];
+        int64_t i = 8;
+        for (; i < n - (n % 8); i += 8)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
+        double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                               __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+        for (; i < n; ++i) res = __dadd_rn(res, a[i]);
+        return res;
+    }
+    int64_t n2 = n / 2;
+    n2 -= n2 % 8;
+    return __dadd_rn(np_pairwise_sum_dev(a, n2), np_pairwise_sum_dev(a + n2, n - n2));
+}
+
 }  // namespace sc

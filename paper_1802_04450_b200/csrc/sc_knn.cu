@@ -245,6 +245,33 @@ __device__ __forceinline__ double exact_d2(const double* __restrict__ xi, const 
     return np_sqdist(xj, xi, d);
 }
 
+// Measure of the kNN ranking / edge values.  kind 0: exp_decay (the ranking
+// value is exp(inv * d2) over x, graph.py:149-157); kind 1: cosine or
+// cross-correlation: clip(dot(xc_i, xc_j) / sqrt(sq_i sq_j), -1, 1) with xc
+// the (centred) rows and sq their squared norms (graph.py:143-147, 158-163),
+// while the candidate search runs on the row-normalised xc (|a - b|^2 =
+// 2 - 2 cos for unit rows).  policy: negative policy of the edge values
+// (0 clamp_zero, 1 abs, 2 keep).
+struct KnnMeasure {
+    int kind = 0;
+    const double* xc = nullptr;
+    const double* sq = nullptr;
+    int policy = 0;
+};
+__device__ __forceinline__ double knn_corr(const KnnMeasure& ms, int64_t d, int64_t i, int64_t j) {
+    const double* a = ms.xc + i * d;
+    const double* b = ms.xc + j * d;
+    NpDot acc;
+    np_dot_span(acc, 0, d, [&](int64_t l) { return __dmul_rn(a[l], b[l]); });
+    const double v = __ddiv_rn(acc.result(), __dsqrt_rn(__dmul_rn(ms.sq[i], ms.sq[j])));
+    return v < -1.0 ? -1.0 : (v > 1.0 ? 1.0 : v);
+}
+// order-preserving 64-bit key of a double (any sign), 0 reserved
+__device__ __forceinline__ unsigned long long ordered_key(double s) {
+    const unsigned long long u = (unsigned long long)__double_as_longlong(s);
+    return (u >> 63) ? ~u : (u | (1ull << 63));
+}
+
 // (s desc, j asc) ordering: a precedes b
 __device__ __forceinline__ bool precedes(double sa, int ja, double sb, int jb) {
     return sa > sb || (sa == sb && ja < jb);
@@ -261,7 +288,7 @@ __global__ void __launch_bounds__(256) knn_recheck_kernel(int64_t n, int64_t p0,
                                                           double cdelta, const int32_t* __restrict__ perm,
                                                           int32_t* __restrict__ sel,
                                                           int32_t* __restrict__ flagged,
-                                                          unsigned long long* __restrict__ nflag) {
+                                                          unsigned long long* __restrict__ nflag, KnnMeasure ms) {
     // lists/counts/taus/sel are in scan order relative to p0 (position ip
     // holds point perm[ip]); distances, norms and the (-s, j) tie-break use
     // original indices; flagged rows are recorded by scan position
@@ -279,8 +306,7 @@ __global__ void __launch_bounds__(256) knn_recheck_kernel(int64_t n, int64_t p0,
     for (int t = lane; t < cnt; t += 32) {
         int j = __float_as_int(L[t].y);
         if (perm) j = perm[j];
-        double d2 = exact_d2(xi, x + (int64_t)j * d, d);
-        S[t] = exp(inv * d2);
+        S[t] = ms.kind == 0 ? exp(inv * exact_d2(xi, x + (int64_t)j * d, d)) : knn_corr(ms, d, i, j);
         J[t] = j;
     }
     __syncwarp();
@@ -309,7 +335,8 @@ __global__ void __launch_bounds__(256) knn_recheck_kernel(int64_t n, int64_t p0,
         double delta = cdelta * r * r;
         double lower = qn[i] + (double)tau - delta;  // lower bound of d2 for non-candidates
         lower = lower * (1.0 - 1e-12) - 1e-300;
-        ok = lower > 0.0 && s_k > exp(inv * lower);
+        // cosine: unit rows, so a non-candidate has cos <= 1 - lower / 2
+        ok = ms.kind == 0 ? (lower > 0.0 && s_k > exp(inv * lower)) : s_k > 1.0 - 0.5 * lower + 1e-12;
     }
     if (!ok) {
         unsigned long long slot = atomicAdd(nflag, 1ull);
@@ -324,7 +351,7 @@ __global__ void __launch_bounds__(512) knn_fallback_kernel(int64_t n, int64_t p0
                                                            const int32_t* __restrict__ perm,
                                                            const int32_t* __restrict__ flagged, int64_t nflag,
                                                            unsigned long long* __restrict__ scratch,
-                                                           int32_t* __restrict__ sel) {
+                                                           int32_t* __restrict__ sel, KnnMeasure ms) {
     __shared__ unsigned int hist[256];
     __shared__ unsigned long long s_prefix;
     __shared__ long long s_remaining;
@@ -341,8 +368,12 @@ __global__ void __launch_bounds__(512) knn_fallback_kernel(int64_t n, int64_t p0
             if (j == i) {
                 key[j] = 0ull;
             } else {
-                double s = exp(inv * exact_d2(xi, x + j * d, d));
-                key[j] = (unsigned long long)__double_as_longlong(s) + 1ull;  // s >= 0 -> monotone bits
+                if (ms.kind == 0) {
+                    double s = exp(inv * exact_d2(xi, x + j * d, d));
+                    key[j] = (unsigned long long)__double_as_longlong(s) + 1ull;  // s >= 0 -> monotone bits
+                } else {
+                    key[j] = ordered_key(knn_corr(ms, d, i, j));
+                }
             }
         }
         if (threadIdx.x == 0) {
@@ -487,12 +518,21 @@ __global__ void row_count_kernel(int64_t nl, int64_t r0, int64_t knn, const int3
     if (lane == 0) len[i] = knn + c;
 }
 
+// edge value of the pair (i, e): exp_decay exp((-d2) / (2 sigma^2)) or the
+// correlation under the negative policy (graph.py:136-147, 229-236)
+__device__ __forceinline__ double edge_value(const KnnMeasure& ms, const double* __restrict__ x, int64_t d,
+                                             double den, int64_t i, int64_t e) {
+    if (ms.kind == 0) return exp(-exact_d2(x + i * d, x + e * d, d) / den);
+    const double v = knn_corr(ms, d, i, e);
+    return ms.policy == 0 ? (v > 0.0 ? v : 0.0) : (ms.policy == 1 ? fabs(v) : v);
+}
+
 __global__ void row_fill_kernel(int64_t nl, int64_t r0, int64_t d, int64_t knn, const double* __restrict__ x,
                                 double den, const int32_t* __restrict__ sel, const int32_t* __restrict__ pos,
                                 const int64_t* __restrict__ rev_ptr, const int32_t* __restrict__ rev,
                                 const uint8_t* __restrict__ dup, const int64_t* __restrict__ row_ptr,
                                 int32_t* __restrict__ col, double* __restrict__ vals,
-                                const int32_t* __restrict__ order) {
+                                const int32_t* __restrict__ order, KnnMeasure ms) {
     // local row; with `order` (whole graph only) the rows are visited in the
     // kNN locality order so the x rows of their neighbours are L2-resident
     int64_t i = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
@@ -509,7 +549,7 @@ __global__ void row_fill_kernel(int64_t nl, int64_t r0, int64_t d, int64_t knn, 
         int64_t r = t;
         for (int64_t p = rb; p < re; ++p) r += (!dup[p] && rev[p] < e);
         col[out0 + r] = e;
-        vals[out0 + r] = exp(-exact_d2(xi, x + (int64_t)e * d, d) / den);
+        vals[out0 + r] = edge_value(ms, x, d, den, r0 + i, e);
     }
     // reverse-only entries
     for (int64_t p = rb + lane; p < re; p += 32) {
@@ -523,7 +563,7 @@ __global__ void row_fill_kernel(int64_t nl, int64_t r0, int64_t d, int64_t knn, 
         int64_t r = lo;
         for (int64_t q = rb; q < re; ++q) r += (!dup[q] && rev[q] < e);
         col[out0 + r] = e;
-        vals[out0 + r] = exp(-exact_d2(xi, x + (int64_t)e * d, d) / den);
+        vals[out0 + r] = edge_value(ms, x, d, den, r0 + i, e);
     }
 }
 
@@ -713,7 +753,7 @@ __global__ void iota_kernel(int64_t n, int32_t* __restrict__ out) {
 // written to sel ((p1 - p0) x knn, each row ascending), plus the scan order
 // perm (n entries; identical on every caller for the same x).
 int knn_select(int64_t n, int64_t d, const double* x, int64_t knn, double two_sigma_sq, int64_t p0, int64_t p1,
-               int32_t* sel, int32_t* perm_out, int64_t* stats, cudaStream_t st) {
+               int32_t* sel, int32_t* perm_out, int64_t* stats, cudaStream_t st, KnnMeasure ms = KnnMeasure()) {
     const double inv = -1.0 / two_sigma_sq;  // graph.py:154
     const int64_t dp = (d + 15) / 16 * 16;
     const char* kenv = std::getenv("SPECLUST_KNN_KERNEL");
@@ -870,7 +910,7 @@ int knn_select(int64_t n, int64_t d, const double* x, int64_t knn, double two_si
         ProfScope prof("knn_recheck", st, (double)np * cap * d * 8.0);
         knn_recheck_kernel<<<(unsigned)ceil_div(np, 8), 256, smem, st>>>(
             n, p0, p1, d, x, knn, inv, cap, lists.p + slot0 * cap, counts.p + slot0, taus.p + slot0, rn.p, qn.p,
-            rmax.p, cdelta, perm, sel, flagged.p, nflag.p);
+            rmax.p, cdelta, perm, sel, flagged.p, nflag.p, ms);
         SC_LAUNCHED(1);
     }
     unsigned long long hflag = 0;
@@ -885,7 +925,7 @@ int knn_select(int64_t n, int64_t d, const double* x, int64_t knn, double two_si
         if ((rc = scratch.alloc((size_t)grid * n))) return rc;
         ProfScope prof("knn_fallback", st, (double)hflag * n * d * 8.0);
         knn_fallback_kernel<<<(unsigned)grid, 512, 0, st>>>(n, p0, d, x, knn, inv, perm, flagged.p, (int64_t)hflag,
-                                                            scratch.p, sel);
+                                                            scratch.p, sel, ms);
         SC_LAUNCHED(1);
     }
     {
@@ -911,7 +951,7 @@ int knn_select(int64_t n, int64_t d, const double* x, int64_t knn, double two_si
 // symmetrised kNN graph from the selections of all n points.
 int knn_union(int64_t n, int64_t d, const double* x, int64_t knn, double two_sigma_sq, const int32_t* sel,
               const int32_t* perm, int64_t r0, int64_t r1, int64_t* row_ptr, int32_t* col, double* vals, int64_t cap,
-              int64_t* nnz_out, cudaStream_t st) {
+              int64_t* nnz_out, cudaStream_t st, KnnMeasure ms = KnnMeasure()) {
     const int64_t nl = r1 - r0;
     int rc;
     DevBuf<int32_t> pos, rev;
@@ -947,7 +987,7 @@ int knn_union(int64_t n, int64_t d, const double* x, int64_t knn, double two_sig
                                       std::to_string(cap));
     row_fill_kernel<<<(unsigned)ceil_div(nl, 8), 256, 0, st>>>(nl, r0, d, knn, x, two_sigma_sq, sel, pos.p, rev_ptr.p,
                                                                rev.p, dup.p, row_ptr, col, vals,
-                                                               (r0 == 0 && nl == n) ? perm : nullptr);
+                                                               (r0 == 0 && nl == n) ? perm : nullptr, ms);
     SC_LAUNCHED(1);
     return SC_OK;
 }
@@ -1037,5 +1077,74 @@ extern "C" int sc_pair_weights(int64_t n, int64_t d, const double* x, int64_t m,
     cudaStream_t st = as_stream(stream);
     pair_weights_kernel<<<(unsigned)ceil_div(m, 256), 256, 0, st>>>(m, d, x, pairs, two_sigma_sq, out);
     SC_LAUNCHED(1);
+    return SC_OK;
+}
+
+// ---- kNN graph with the cosine / cross-correlation measures ------------------
+namespace sc {
+// xc = x - mean(x, axis=1) (centre) or x, sq = einsum(xc, xc), xn = xc / sqrt(sq)
+__global__ void corr_prep_kernel(int64_t n, int64_t d, const double* __restrict__ x, int centre,
+                                 double* __restrict__ xc, double* __restrict__ sq, double* __restrict__ xn,
+                                 unsigned long long* __restrict__ first_bad) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double* xi = x + i * d;
+    double* oi = xc + i * d;
+    const double mu = centre ? __ddiv_rn(__dadd_rn(0.0, np_pairwise_sum_dev(xi, d)), (double)d) : 0.0;
+    for (int64_t l = 0; l < d; ++l) oi[l] = centre ? __dsub_rn(xi[l], mu) : xi[l];
+    const double q = np_sqnorm(oi, d);
+    sq[i] = q;
+    if (q == 0.0) atomicMin(first_bad, (unsigned long long)i);
+    const double r = q > 0.0 ? 1.0 / sqrt(q) : 0.0;
+    for (int64_t l = 0; l < d; ++l) xn[i * d + l] = oi[l] * r;
+}
+}  // namespace sc
+
+// Union-kNN similarity graph for any measure (graph.py:149-163, 185-237):
+// kind 0 exp_decay (sigma), 1 cosine, 2 cross_correlation; negative_policy
+// 0 clamp_zero, 1 abs, 2 keep.  The candidate search runs on the
+// row-normalised (centred) points; ranking, the certificate and the edge
+// values use the reference's formula.  A degenerate point returns
+// SC_ERR_VALUE with *degenerate (host) = its index.
+extern "C" int sc_knn_graph_measure_f64(int64_t n, int64_t d, const double* x, int64_t knn, int kind, double sigma,
+                                        int negative_policy, int64_t* row_ptr, int32_t* col, double* vals,
+                                        int64_t* nnz_out, int64_t* stats_out, int64_t* degenerate,
+                                        sc_stream_t stream) {
+    *degenerate = -1;
+    if (kind == 0) return sc_knn_graph_f64(n, d, x, knn, 2.0 * (sigma * sigma), row_ptr, col, vals, nnz_out,
+                                           stats_out, stream);
+    if (kind != 1 && kind != 2) return fail(SC_ERR_VALUE, "measure kind must be 0, 1 or 2");
+    if (int rc = check_knn_args(n, d, knn, 1.0)) return rc;
+    cudaStream_t st = as_stream(stream);
+    StreamScope stream_scope(st);
+    DevBuf<double> xc, sq, xn;
+    DevBuf<unsigned long long> bad;
+    DevBuf<int32_t> sel, perm;
+    int rc;
+    if ((rc = xc.alloc((size_t)n * d)) || (rc = sq.alloc(n)) || (rc = xn.alloc((size_t)n * d)) || (rc = bad.alloc(1)) ||
+        (rc = sel.alloc((size_t)n * knn)) || (rc = perm.alloc(n)))
+        return rc;
+    SC_CUDA(cudaMemsetAsync(bad.p, 0xff, sizeof(unsigned long long), st));
+    corr_prep_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(n, d, x, kind == 2, xc.p, sq.p, xn.p, bad.p);
+    SC_LAUNCHED(1);
+    unsigned long long hb = 0;
+    SC_CUDA(cudaMemcpyAsync(&hb, bad.p, sizeof(hb), cudaMemcpyDeviceToHost, st));
+    SC_CUDA(cudaStreamSynchronize(st));
+    if (hb != ~0ull) {  // graph.py:158-163: every point is checked
+        *degenerate = (int64_t)hb;
+        return fail(SC_ERR_VALUE, "degenerate vector at point index " + std::to_string(hb));
+    }
+    KnnMeasure ms;
+    ms.kind = 1;
+    ms.xc = xc.p;
+    ms.sq = sq.p;
+    ms.policy = negative_policy;
+    int64_t tmp[8];
+    int64_t* stats = stats_out ? stats_out : tmp;
+    if ((rc = knn_select(n, d, xn.p, knn, 1.0, 0, n, sel.p, perm.p, stats, st, ms))) return rc;
+    if ((rc = knn_union(n, d, xn.p, knn, 1.0, sel.p, perm.p, 0, n, row_ptr, col, vals, 2 * n * knn, nnz_out, st,
+                        ms)))
+        return rc;
+    stats[3] = *nnz_out;
     return SC_OK;
 }

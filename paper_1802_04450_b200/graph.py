@@ -116,17 +116,51 @@ def similarity(x_i, x_j, m: SimilarityMeasure) -> float:
 def _require_exp_decay(m: SimilarityMeasure, what: str):
     if m.kind != "exp_decay":
         raise NotImplementedError(
-            f"{what} with measure {m.kind!r} is not on the device path this round "
-            "(SURVEY.md §8(f) F3); only exp_decay is implemented"
+            f"{what} with measure {m.kind!r}: the sharded kNN stages support exp_decay only "
+            "(single-GPU knn_graph_device handles every measure)"
         )
 
 
-def knn_graph_device(x, knn: int, m: SimilarityMeasure, return_stats: bool = False):
-    """Union-kNN exp_decay similarity matrix W as a DeviceCsr, built on the
-    GPU in one call (graph.py:185-237 + sparse.py:182-187 fused).
+def _knn_graph_corr(xd, knn: int, m: SimilarityMeasure, negative_policy: str, return_stats: bool):
+    """kNN graph with the cosine / cross-correlation measure
+    (sc_knn_graph_measure_f64): ranking by the reference's similarity,
+    values under the negative policy."""
+    torch = nat.torch_cuda()
+    n, d = xd.shape
+    cap = 2 * n * knn
+    rp = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+    col = torch.empty(cap, dtype=torch.int32, device="cuda")
+    vals = torch.empty(cap, dtype=torch.float64, device="cuda")
+    nnz, deg = nat.C.c_int64(), nat.C.c_int64()
+    stats = (nat.C.c_int64 * 8)()
+    rc = nat.load().sc_knn_graph_measure_f64(n, d, nat.ptr(xd), knn, 1 if m.kind == "cosine" else 2, 1.0,
+                                             NEGATIVE_POLICIES.index(negative_policy), nat.ptr(rp), nat.ptr(col),
+                                             nat.ptr(vals), nat.C.byref(nnz), stats, nat.C.byref(deg),
+                                             nat.stream_handle())
+    if rc != 0 and deg.value >= 0:
+        what = "constant" if m.kind == "cross_correlation" else "zero"
+        raise DegenerateVector(f"{what} vector at point index {deg.value} is invalid for {m.kind}",
+                               index=int(deg.value))
+    nat.check(rc)
+    w = DeviceCsr(n, n, rp, col[: nnz.value].clone(), vals[: nnz.value].clone())
+    if return_stats:
+        keys = ("list_R", "list_cap", "fallback_rows")
+        out = {key: int(stats[i]) for i, key in enumerate(keys)}
+        out["nnz"] = w.nnz
+        return w, out
+    return w
+
+
+def knn_graph_device(x, knn: int, m: SimilarityMeasure, return_stats: bool = False,
+                     negative_policy: str = "clamp_zero"):
+    """Union-kNN similarity matrix W as a DeviceCsr, built on the GPU in one
+    call (graph.py:185-237 + sparse.py:182-187 fused).  exp_decay keeps the
+    kNN locality scan order on W (``locality_perm``) for the eigensolver;
+    cosine / cross_correlation go through sc_knn_graph_measure_f64.
 
     ``x`` may be a numpy array or a CUDA float64 tensor (n x d)."""
-    _require_exp_decay(m, "knn graph")
+    if negative_policy not in NEGATIVE_POLICIES:
+        raise ValueError(f"unknown negative_policy {negative_policy!r}")
     torch = nat.torch_cuda()
     if isinstance(x, torch.Tensor):
         # CUDA tensors are used in place; host tensors (e.g. pinned) are copied
@@ -138,6 +172,8 @@ def knn_graph_device(x, knn: int, m: SimilarityMeasure, return_stats: bool = Fal
         xd = nat.to_device(xh, torch.float64)
     if not 1 <= knn < n:
         raise ValueError(f"knn must satisfy 1 <= knn < n, got {knn} for n={n}")
+    if m.kind != "exp_decay":
+        return _knn_graph_corr(xd, knn, m, negative_policy, return_stats)
     # selection (sc_knn_select_f64) + union (sc_knn_union_f64) == sc_knn_graph_f64;
     # the two-stage form keeps the locality scan order for the eigensolver
     sel = torch.empty((n, knn), dtype=torch.int32, device="cuda")
@@ -214,8 +250,7 @@ def build_edges_knn(x, knn: int, m: SimilarityMeasure) -> np.ndarray:
     n = x.shape[0]
     if not 1 <= knn < n:
         raise ValueError(f"knn must satisfy 1 <= knn < n, got {knn} for n={n}")
-    _require_exp_decay(m, "build_edges_knn")
-    w = knn_graph_device(x, knn, m)
+    w = knn_graph_device(x, knn, m, negative_policy="keep")
     rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(nat.to_host(w.row_ptr)))
     cols = nat.to_host(w.col, np.int64)
     upper = cols > rows

@@ -73,6 +73,17 @@ def main():
         k_clusters=4, eigen=sp.LanczosConfig(k=4, seed=0), kmeans=sp.KmeansConfig(k=4, seed=0), normalize_rows=True)
     rep = sp.run(cfg)
     out.update(pt_labels=rep.labeling.labels, pt_values=rep.eigenvalues)
+    # ---- F3: kNN pattern with cosine / cross-correlation (n < and >= 4096)
+    for tag, (nn, dd, kk, seed) in {"kc1": (600, 8, 10, 21), "kc2": (5000, 16, 12, 22)}.items():
+        xk = np.random.default_rng(seed).standard_normal((nn, dd)) + 0.5
+        out[f"{tag}_x"] = xk
+        out[f"{tag}_knn"] = kk
+        for kind in ("cosine", "cross_correlation"):
+            meas = sp.SimilarityMeasure(kind)
+            ek = sp.build_edges_knn(xk, kk, meas)
+            coo = sp.build_similarity(xk, ek, meas, negative_policy="keep")
+            out[f"{tag}_{kind}_edges"] = ek
+            out[f"{tag}_{kind}_vals"] = coo.vals
     np.savez_compressed(HERE / "f_rows.npz", **out)
     print("f_rows.npz written", {k: v.shape for k, v in out.items() if hasattr(v, "shape")})
 

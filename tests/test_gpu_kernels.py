@@ -590,3 +590,24 @@ def test_f3_measures_and_patterns_vs_reference(golden):
     allp = np.array([[i, j] for i in range(len(xs)) for j in range(i + 1, len(xs))])
     v = orc.edge_similarity(xs, allp, "cosine", "keep")
     assert np.array_equal(e, allp[v > 0.5])
+
+
+@pytest.mark.parametrize("tag", ["kc1", "kc2"])
+@pytest.mark.parametrize("kind", ["cosine", "cross_correlation"])
+def test_knn_cosine_cross_correlation_vs_reference(golden, tag, kind):
+    """kNN pattern with the cosine / cross-correlation measures on the device
+    (tensor-core candidates on the row-normalised points, exact ranking by the
+    reference's similarity, certificate in cosine space) == the real
+    reference's build_edges_knn + build_similarity; kc2 (n = 5000) takes the
+    locality-ordered tcgen05 path."""
+    f = golden("f_rows")
+    x, knn = f[f"{tag}_x"], int(f[f"{tag}_knn"])
+    m = sc.SimilarityMeasure(kind)
+    e = sc.build_edges_knn(x, knn, m)
+    assert np.array_equal(e, f[f"{tag}_{kind}_edges"])
+    from paper_1802_04450_b200.graph import knn_graph_device
+
+    w = knn_graph_device(x, knn, m, negative_policy="keep").to_host()
+    coo = sc.build_similarity(x, e, m, negative_policy="keep")
+    assert np.array_equal(w.vals, coo.vals) and np.array_equal(w.vals, f[f"{tag}_{kind}_vals"])
+    assert sc.sparse.is_symmetric(w)
