@@ -34,6 +34,7 @@
  *   sc_row_scale_f64       laplacian.py:75-81       row_scale(w, d)
  *   sc_edge_similarity_f64 graph.py:136-147,214-237 build_similarity (cosine, cross_correlation)
  *   sc_pattern_edges_f64   graph.py:160-176,206-211 build_edges_eps, build_edges_threshold
+ *   sc_sbm_csr             sbm.py:68-108            sbm_generate (device, distributional parity)
  */
 #ifndef SPECLUST_B200_H
 #define SPECLUST_B200_H
@@ -334,6 +335,14 @@ int sc_edge_similarity_f64(int64_t n, int64_t d, const double* x, int64_t m, con
 int sc_knn_graph_measure_f64(int64_t n, int64_t d, const double* x, int64_t knn, int kind, double sigma,
                              int negative_policy, int64_t* row_ptr, int32_t* col, double* vals, int64_t* nnz_out,
                              int64_t* stats_out, int64_t* degenerate, sc_stream_t stream);
+/* Planted-partition SBM straight into CSR (sbm.py:68-108):
+ * offsets (dev int64, nblocks+1) = block boundaries; p_in / p_out edge
+ * probabilities; deterministic per seed (Philox, geometric skipping per row).
+ * Call with col == NULL for *nnz_out (host), then with caller-allocated
+ * row_ptr (n+1) / col / vals (nnz) (dev): symmetric, unit weights, no
+ * self-loops, columns ascending. */
+int sc_sbm_csr(int64_t n, const int64_t* offsets, int64_t nblocks, double p_in, double p_out, uint64_t seed,
+               int64_t* row_ptr, int32_t* col, double* vals, int64_t* nnz_out, sc_stream_t stream);
 /* eps / threshold patterns (graph.py:160-176, 206-211): (i < j) pairs in
  * row-major order.  mode 0 eps (a = eps), 1 threshold exp_decay (a = lambda,
  * b = sigma), 2 threshold cosine, 3 threshold cross_correlation (a = lambda).

@@ -91,6 +91,7 @@ SIGNATURES = {
     "sc_row_scale_f64": (i32, [i64, vp, vp, vp, vp, vp]),
     "sc_edge_similarity_f64": (i32, [i64, i64, vp, i64, vp, i32, i32, vp, P_i64, vp]),
     "sc_knn_graph_measure_f64": (i32, [i64, i64, vp, i64, i32, f64, i32, vp, vp, vp, P_i64, vp, P_i64, vp]),
+    "sc_sbm_csr": (i32, [i64, vp, i64, f64, f64, C.c_uint64, vp, vp, vp, P_i64, vp]),
     "sc_pattern_edges_f64": (i32, [i64, i64, vp, i32, f64, f64, vp, P_i64, P_i64, vp]),
     "sc_gemv_t_f64": (i32, [i64, i64, i64, vp, vp, vp, vp]),
     "sc_gemv_n_f64": (i32, [i64, i64, i64, vp, vp, vp, vp, vp]),

@@ -611,3 +611,50 @@ def test_knn_cosine_cross_correlation_vs_reference(golden, tag, kind):
     coo = sc.build_similarity(x, e, m, negative_policy="keep")
     assert np.array_equal(w.vals, coo.vals) and np.array_equal(w.vals, f[f"{tag}_{kind}_vals"])
     assert sc.sparse.is_symmetric(w)
+
+
+def test_sbm_generator_statistics():
+    """Device planted-partition SBM (sc_sbm_csr): canonical symmetric unit
+    CSR without self-loops; intra / inter edge counts within 5 sigma of the
+    binomial means of the reference's model (sbm.py:68-108); deterministic
+    per seed, different across seeds; p = 0 / p = 1 edge cases."""
+    cfg = sc.SbmConfig(block_sizes=(700, 500, 800, 650), p_in=0.05, p_out=0.002, seed=3)
+    adj, lab = sc.sbm_generate(cfg)
+    n = sum(cfg.block_sizes)
+    assert adj.n_rows == n and np.array_equal(lab, np.repeat(np.arange(4), cfg.block_sizes))
+    assert np.all(adj.vals == 1.0) and not np.any(adj.rows == adj.cols)
+    order = np.lexsort((adj.cols, adj.rows))
+    assert np.array_equal(order, np.arange(adj.nnz))  # canonical
+    key = set(zip(adj.rows.tolist(), adj.cols.tolist()))
+    assert all((c, r) in key for r, c in key)  # symmetric
+    intra = int(np.sum(lab[adj.rows] == lab[adj.cols])) // 2
+    inter = adj.nnz // 2 - intra
+    sizes = np.array(cfg.block_sizes)
+    n_in = int(np.sum(sizes * (sizes - 1) // 2))
+    n_out = n * (n - 1) // 2 - n_in
+    for got, pairs, p in ((intra, n_in, cfg.p_in), (inter, n_out, cfg.p_out)):
+        mu, sd = pairs * p, np.sqrt(pairs * p * (1 - p))
+        assert abs(got - mu) <= 5 * sd, (got, mu, sd)
+    adj2, _ = sc.sbm_generate(cfg)
+    assert np.array_equal(adj2.rows, adj.rows) and np.array_equal(adj2.cols, adj.cols)
+    adj3, _ = sc.sbm_generate(sc.SbmConfig(block_sizes=cfg.block_sizes, p_in=0.05, p_out=0.002, seed=4))
+    assert not (adj3.nnz == adj.nnz and np.array_equal(adj3.cols, adj.cols))
+    full, _ = sc.sbm_generate(sc.SbmConfig(block_sizes=(5, 4), p_in=1.0, p_out=0.0))
+    assert full.nnz == 5 * 4 + 4 * 3
+    empty, _ = sc.sbm_generate(sc.SbmConfig(block_sizes=(5, 4), p_in=0.0, p_out=0.0))
+    assert empty.nnz == 0
+
+
+def test_sbm_pipeline_and_binary_input(tmp_path):
+    """A device-generated SBM clustered through MatrixInput from a binary CSR
+    container (F2 path): recovers the planted blocks (ARI >= 0.95, the
+    reference's own SBM acceptance bar, test_pipeline.py)."""
+    from paper_1802_04450_b200 import io
+    from paper_1802_04450_b200.sbm import sbm_generate_device
+
+    w, lab = sbm_generate_device(sc.SbmConfig(block_sizes=(400,) * 10, p_in=0.08, p_out=0.002, seed=1))
+    io.save_csr_binary(tmp_path / "g.scb", w)
+    rep = sc.run(sc.PipelineConfig(input=sc.MatrixInput(path=str(tmp_path / "g.scb")), k_clusters=10,
+                                   eigen=sc.LanczosConfig(k=10, seed=0), kmeans=sc.KmeansConfig(k=10, seed=0),
+                                   normalize_rows=True))
+    assert sc.adjusted_rand_index(rep.labeling.labels, lab.cpu().numpy()) >= 0.95

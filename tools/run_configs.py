@@ -3,7 +3,11 @@ timings, not bench lines):
   c3s: blobs N=120k, d=128, kNN=32, k=1000 (C3's large-k Lanczos, m=2000)
   c5s: k-means stress, 1M x 256 embedding, k=10,000, 20 Lloyd iterations
        from random_points init (C5's shape at 1/10 of the rows)
-python tools/run_configs.py [c3s] [c5s]"""
+  c4g: C4's SBM graph at full size (16M nodes, 500 blocks, ~512M edges):
+       device generation only
+  c4s: C4 at 1/8 of the nodes (62 blocks x 32,000, same intra / inter
+       degrees), MatrixInput -> eigensolve (k=62) -> k-means
+python tools/run_configs.py [c3s] [c5s] [c4g] [c4s]"""
 import os
 import sys
 import time
@@ -29,7 +33,7 @@ def prof(lib, names):
 
 
 lib = nat.load()
-which = sys.argv[1:] or ["c3s", "c5s"]
+which = sys.argv[1:] or ["c3s", "c5s", "c4g", "c4s"]
 if "c3s" in which:
     n, d, knn, k = 120_000, 128, 32, 1000
     x, y = make_blobs(n, d, k, 1.0)
@@ -70,3 +74,30 @@ if "c5s" in which:
     t = time.perf_counter() - t0
     print(f"c5s: {t:.2f} s for {it} Lloyd iterations ({t / max(it, 1) * 1e3:.1f} ms/it) sse {hist[0]:.4e} -> "
           f"{hist[-1]:.4e} kernels {prof(lib, ['kmeans_assign', 'kmeans_update'])}", flush=True)
+if "c4g" in which:
+    from paper_1802_04450_b200.sbm import SbmConfig, sbm_generate_device
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    w, lab = sbm_generate_device(SbmConfig(block_sizes=(32_000,) * 500, p_in=1.6e-3, p_out=8.0e-7, seed=0))
+    torch.cuda.synchronize()
+    print(f"c4g: n={w.n_rows} nnz={w.nnz} ({w.nnz // 2} edges) generated in {time.perf_counter() - t0:.2f} s",
+          flush=True)
+    del w, lab
+    torch.cuda.empty_cache()
+if "c4s" in which:
+    from paper_1802_04450_b200.sbm import SbmConfig, sbm_generate_device
+    w, lab = sbm_generate_device(SbmConfig(block_sizes=(32_000,) * 62, p_in=1.6e-3, p_out=6.4e-6, seed=0))
+    k = 62
+    cfg = sc.PipelineConfig(input=sc.MatrixInput(matrix=w.to_host()), k_clusters=k,
+                            eigen=sc.LanczosConfig(k=k, seed=0), kmeans=sc.KmeansConfig(k=k, seed=0),
+                            normalize_rows=True)
+    lib.sc_profile_reset()
+    lib.sc_profile_enable(1)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    rep, _ = run_device(cfg)
+    torch.cuda.synchronize()
+    t = time.perf_counter() - t0
+    print(f"c4s: n={w.n_rows} nnz={w.nnz} {t:.2f} s stages {rep.timings} eigen {last_info.get('eigen')} "
+          f"ARI vs blocks {sc.adjusted_rand_index(rep.labeling.labels, lab.cpu().numpy()):.4f} "
+          f"kernels {prof(lib, ['spmv', 'reorth', 'symeig', 'ritz', 'kmeans_assign', 'kmeanspp'])}", flush=True)
