@@ -462,40 +462,40 @@ constexpr int KPP_UPD_ROWS = 128, KPP_UPD_COLS = 32;
 __global__ void __launch_bounds__(KPP_UPD_ROWS) kpp_update_kernel(int64_t n, int64_t d, const double* __restrict__ v, const double* __restrict__ prow,
                                   int64_t pick, int first, double* __restrict__ d2, uint8_t* __restrict__ taken,
                                   double* __restrict__ pw, int64_t* __restrict__ pc) {
-    // one thread per row; the block's KPP_UPD_ROWS rows are staged through
-    // shared memory in 32-column chunks (coalesced loads), and each thread
-    // folds its row in numpy's einsum order (_dist_to_one, kmeans.py:101-104)
-    __shared__ double tile[KPP_UPD_ROWS][KPP_UPD_COLS + 1];
-    __shared__ double sp[KPP_UPD_COLS];
+    // one thread per row, folding its row against the new centre in numpy's
+    // einsum order (_dist_to_one, kmeans.py:101-104).  Rows are read
+    // directly, 32 columns at a time; once the partial sum already reaches the
+    // row's current d2 the rest is skipped: rounded additions of nonnegative
+    // terms never decrease the sum, so the full distance could not lower d2
+    // and min(d2, dist) = d2 exactly (most rows, once the seeding has covered
+    // their region).
     __shared__ double sw[KPP_UPD_ROWS / 32];
     __shared__ int64_t scn[KPP_UPD_ROWS / 32];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int64_t r0 = (int64_t)blockIdx.x * KPP_UPD_ROWS;
-    const int64_t i = r0 + tid;
-    const int nrows = (int)imin64(KPP_UPD_ROWS, n - r0);
+    const int64_t i = (int64_t)blockIdx.x * KPP_UPD_ROWS + tid;
     NpDot acc;
-    for (int64_t c0 = 0; c0 < d; c0 += KPP_UPD_COLS) {
-        const int nc = (int)imin64(KPP_UPD_COLS, d - c0);
-        __syncthreads();
-        for (int e = tid; e < nrows * KPP_UPD_COLS; e += KPP_UPD_ROWS) {
-            const int rr = e / KPP_UPD_COLS, cc = e % KPP_UPD_COLS;
-            if (cc < nc) tile[rr][cc] = v[(r0 + rr) * d + c0 + cc];
-        }
-        if (tid < nc) sp[tid] = prow[c0 + tid];
-        __syncthreads();
-        if (tid < nrows) {
-            const double* row = tile[tid];
-            np_dot_span(acc, 0, nc, [&](int64_t l) {
-                const double t = __dsub_rn(row[l], sp[l]);
+    bool pruned = false;
+    double old = 0.0;
+    if (i < n) {
+        const double* row = v + i * d;
+        if (!first) old = d2[i];
+        for (int64_t c0 = 0; c0 < d; c0 += KPP_UPD_COLS) {
+            const int64_t c1 = imin64(d, c0 + KPP_UPD_COLS);
+            np_dot_span(acc, c0, c1, [&](int64_t l) {
+                const double t = __dsub_rn(__ldg(row + l), __ldg(prow + l));
                 return __dmul_rn(t, t);
             });
+            if (!first && c1 < d && acc.result() >= old) {
+                pruned = true;
+                break;
+            }
         }
     }
     double w = 0.0;
     int64_t cnt = 0;
     if (i < n) {
         const double dist = acc.result();
-        const double nv = first ? dist : fmin(d2[i], dist);
+        const double nv = first ? dist : (pruned ? old : fmin(old, dist));
         if (i == pick) taken[i] = 1;
         const bool tk = (i == pick) || taken[i];
         d2[i] = nv;
