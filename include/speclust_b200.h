@@ -166,6 +166,18 @@ int sc_knn_union_f64(int64_t n, int64_t d, const double* x, int64_t knn, double 
                      const int32_t* sel, const int32_t* perm, int64_t r0, int64_t r1,
                      int64_t* row_ptr, int32_t* col, double* vals, int64_t cap, int64_t* nnz_out,
                      sc_stream_t stream);
+/* The same two stages carrying the exact value of every selection slot
+ * (sel_vals, (p1-p0) x knn fp64, in sel's order: the einsum-order d2 of the
+ * pair): the union then fills the CSR values without recomputing a distance
+ * (a reverse entry takes the value of the other endpoint's slot, the same
+ * number).  Results are bit-identical to the plain forms. */
+int sc_knn_select_vals_f64(int64_t n, int64_t d, const double* x, int64_t knn, double two_sigma_sq,
+                           int64_t p0, int64_t p1, int32_t* sel, double* sel_vals, int32_t* perm,
+                           int64_t* stats_out, sc_stream_t stream);
+int sc_knn_union_vals_f64(int64_t n, int64_t d, const double* x, int64_t knn, double two_sigma_sq,
+                          const int32_t* sel, const double* sel_vals, const int32_t* perm, int64_t r0,
+                          int64_t r1, int64_t* row_ptr, int32_t* col, double* vals, int64_t cap,
+                          int64_t* nnz_out, sc_stream_t stream);
 /* out[p] = exp(-|x_a - x_b|^2 / two_sigma_sq) for pairs (a, b) = pairs[2p..2p+1]
  * (graph.py:136-141, used by build_similarity on a given edge list). */
 int sc_pair_weights(int64_t n, int64_t d, const double* x, int64_t m, const int64_t* pairs,

@@ -63,6 +63,8 @@ SIGNATURES = {
     "sc_knn_graph_f64": (i32, [i64, i64, vp, i64, f64, vp, vp, vp, P_i64, P_i64, vp]),
     "sc_knn_select_f64": (i32, [i64, i64, vp, i64, f64, i64, i64, vp, vp, P_i64, vp]),
     "sc_knn_union_f64": (i32, [i64, i64, vp, i64, f64, vp, vp, i64, i64, vp, vp, vp, i64, P_i64, vp]),
+    "sc_knn_select_vals_f64": (i32, [i64, i64, vp, i64, f64, i64, i64, vp, vp, vp, P_i64, vp]),
+    "sc_knn_union_vals_f64": (i32, [i64, i64, vp, i64, f64, vp, vp, vp, i64, i64, vp, vp, vp, i64, P_i64, vp]),
     "sc_pair_weights": (i32, [i64, i64, vp, i64, vp, f64, vp, vp]),
     "sc_lanczos_create": (i32, [i64, i64, i64, f64, i64, C.c_uint64, vp, C.POINTER(vp)]),
     "sc_lanczos_destroy": (None, [vp]),

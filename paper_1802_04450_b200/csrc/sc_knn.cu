@@ -75,6 +75,15 @@ __global__ void pivot_dist_kernel(int64_t C, int64_t d, const double* __restrict
     D[a * C + b] = (float)s;
 }
 
+// out row r = x row idx[r] (n x d)
+__global__ void gather_rows_i32_kernel(int64_t n, int64_t d, const double* __restrict__ x,
+                                       const int32_t* __restrict__ idx, double* __restrict__ out) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n * d) return;
+    const int64_t r = e / d;
+    out[e] = x[(int64_t)idx[r] * d + (e - r * d)];
+}
+
 __global__ void gather_pivots_kernel(int64_t C, int64_t d, const double* __restrict__ src,
                                      const int32_t* __restrict__ order, double* __restrict__ dst) {
     const int64_t c = blockIdx.x;
@@ -266,6 +275,59 @@ __device__ __forceinline__ double knn_corr(const KnnMeasure& ms, int64_t d, int6
     const double v = __ddiv_rn(acc.result(), __dsqrt_rn(__dmul_rn(ms.sq[i], ms.sq[j])));
     return v < -1.0 ? -1.0 : (v > 1.0 ? 1.0 : v);
 }
+// clip(dot / sqrt(sq_i sq_j), -1, 1) of a dot product in the einsum order
+__device__ __forceinline__ double knn_corr_of(const KnnMeasure& ms, double dot, int64_t i, int64_t j) {
+    const double v = __ddiv_rn(dot, __dsqrt_rn(__dmul_rn(ms.sq[i], ms.sq[j])));
+    return v < -1.0 ? -1.0 : (v > 1.0 ? 1.0 : v);
+}
+
+// Warp-cooperative einsum-order reductions of up to 32 rows (lane t owns the
+// row rt, nullptr = none) against the warp-uniform row ri.  The rows are
+// staged through shared memory (stage: 32 x 33 doubles per warp) 32 columns
+// at a time with coalesced loads; a lane-per-row loop would spend one L1
+// wavefront per lane per element.  DIFF: |rt - ri|^2 (np_sqdist(rt, ri));
+// else dot(ri, rt).  Bit-identical to the per-lane forms.  The row pointers
+// are exchanged through shared memory (after the 32 x 33 tile) rather than
+// shuffles, which would need a converged warp the compiler cannot prove.
+constexpr int kStageLd = 33;
+constexpr int kStageWarp = 32 * kStageLd + 32;  // doubles per warp
+template <bool DIFF>
+__device__ __forceinline__ double warp_rows_np(const double* __restrict__ ri, const double* rt, int64_t d,
+                                               double* __restrict__ stage) {
+    const int lane = threadIdx.x & 31;
+    const double** rows = reinterpret_cast<const double**>(stage + 32 * kStageLd);
+    __syncwarp();
+    rows[lane] = rt;
+    NpDot acc;
+    for (int64_t c0 = 0; c0 < d; c0 += 32) {
+        const int w = (int)(d - c0 < 32 ? d - c0 : 32);
+        __syncwarp();
+#pragma unroll
+        for (int r0 = 0; r0 < 32; r0 += 8) {
+            double v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const double* pr = rows[r0 + q];
+                v[q] = (pr && lane < w) ? __ldg(pr + c0 + lane) : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) stage[(r0 + q) * kStageLd + lane] = v[q];
+        }
+        __syncwarp();
+        if (rt) {
+            const double* srow = stage + lane * kStageLd - c0;
+            np_dot_span(acc, c0, c0 + w, [&](int64_t l) {
+                if (DIFF) {
+                    const double t = __dsub_rn(srow[l], ri[l]);
+                    return __dmul_rn(t, t);
+                }
+                return __dmul_rn(ri[l], srow[l]);
+            });
+        }
+    }
+    return acc.result();
+}
+
 // order-preserving 64-bit key of a double (any sign), 0 reserved
 __device__ __forceinline__ unsigned long long ordered_key(double s) {
     const unsigned long long u = (unsigned long long)__double_as_longlong(s);
@@ -288,52 +350,142 @@ __global__ void __launch_bounds__(256) knn_recheck_kernel(int64_t n, int64_t p0,
                                                           double cdelta, const int32_t* __restrict__ perm,
                                                           int32_t* __restrict__ sel,
                                                           int32_t* __restrict__ flagged,
-                                                          unsigned long long* __restrict__ nflag, KnnMeasure ms) {
+                                                          unsigned long long* __restrict__ nflag, KnnMeasure ms,
+                                                          const double* __restrict__ xs, double* __restrict__ selv) {
     // lists/counts/taus/sel are in scan order relative to p0 (position ip
     // holds point perm[ip]); distances, norms and the (-s, j) tie-break use
     // original indices; flagged rows are recorded by scan position
     extern __shared__ unsigned char rsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    double* S = reinterpret_cast<double*>(rsm) + (size_t)warp * cap;
-    int* J = reinterpret_cast<int*>(reinterpret_cast<double*>(rsm) + (size_t)8 * cap) + (size_t)warp * cap;
+    double* stage = reinterpret_cast<double*>(rsm) + (size_t)warp * kStageWarp;
+    double* S = reinterpret_cast<double*>(rsm) + (size_t)8 * kStageWarp + (size_t)warp * cap;
+    double* D = reinterpret_cast<double*>(rsm) + (size_t)8 * kStageWarp + (size_t)8 * cap + (size_t)warp * cap;
+    int* J = reinterpret_cast<int*>(reinterpret_cast<double*>(rsm) + (size_t)8 * kStageWarp + (size_t)16 * cap) +
+             (size_t)warp * cap;
     const int64_t lp = (int64_t)blockIdx.x * 8 + warp;
     const int64_t ip = p0 + lp;
     if (ip >= p1) return;
     const int64_t i = perm ? (int64_t)perm[ip] : ip;
     const int cnt = counts[lp];
     const float2* L = lists + lp * (int64_t)cap;
-    const double* xi = x + i * d;
-    for (int t = lane; t < cnt; t += 32) {
-        int j = __float_as_int(L[t].y);
-        if (perm) j = perm[j];
-        S[t] = ms.kind == 0 ? exp(inv * exact_d2(xi, x + (int64_t)j * d, d)) : knn_corr(ms, d, i, j);
-        J[t] = j;
+    // xs: the points in scan order (row p = point perm[p]); the candidates of a
+    // row are its scan-order neighbours, so their rows are L2-resident there
+    const double* xi = xs ? xs + ip * d : x + i * d;
+    const float tau = taus[lp];
+    const double rr = rn[i] + __longlong_as_double((long long)*rmax_bits);
+    const double delta = cdelta * rr * rr;  // |approximate key - exact (d2 - qn_i)| bound
+    // Prune the list with its approximate keys: with T the knn-th smallest
+    // key, at least knn candidates have d2 <= qn + T + delta, so a candidate
+    // whose key exceeds T + 2 delta (+ slack) cannot be selected.  The dropped
+    // keys join the non-candidates in the certificate below (lower bound
+    // qn + key - delta), so a wrong prune is caught there like a short list.
+    constexpr int PL = TC_LIST_P / 32;
+    float kv[PL];
+    unsigned uk[PL];
+#pragma unroll
+    for (int q = 0; q < PL; ++q) {
+        const int t = lane + 32 * q;
+        kv[q] = t < cnt ? L[t].x : INFINITY;
+        const unsigned u = __float_as_uint(kv[q]);
+        uk[q] = t < cnt ? ((u >> 31) ? ~u : (u | 0x80000000u)) : 0xffffffffu;
+    }
+    float kdrop = INFINITY;  // smallest dropped key
+    int* K = J;              // kept list positions (J is rewritten in place below)
+    int m = cnt;
+    if (cnt > knn + 8) {
+        unsigned pre = 0;  // knn-th smallest ordered key (radix select over the warp)
+        for (int b = 31; b >= 0; --b) {
+            const unsigned trial = pre | ((1u << b) - 1u);
+            int c = 0;
+#pragma unroll
+            for (int q = 0; q < PL; ++q) c += (lane + 32 * q < cnt) && uk[q] <= trial;
+            if (__reduce_add_sync(0xffffffffu, c) < (int)knn) pre |= 1u << b;
+        }
+        const unsigned tb = (pre >> 31) ? (pre & 0x7fffffffu) : ~pre;
+        const double T = (double)__uint_as_float(tb);
+        const double thr = T + 2.0 * delta + 1e-9 * (fabs(qn[i] + T) + delta);
+        m = 0;
+#pragma unroll
+        for (int q = 0; q < PL; ++q) {
+            const int t = lane + 32 * q;
+            const bool keep = t < cnt && (double)kv[q] <= thr;
+            if (t < cnt && !keep) kdrop = fminf(kdrop, kv[q]);
+            const unsigned bal = __ballot_sync(0xffffffffu, keep);
+            if (keep) K[m + __popc(bal & ((1u << lane) - 1u))] = t;
+            m += __popc(bal);
+        }
+        for (int o = 16; o > 0; o >>= 1) kdrop = fminf(kdrop, __shfl_xor_sync(0xffffffffu, kdrop, o));
+    } else {
+        for (int t = lane; t < cnt; t += 32) K[t] = t;
     }
     __syncwarp();
-    // rank each candidate; the knn first ranks are selected
+    for (int t0 = 0; t0 < m; t0 += 32) {
+        const int t = t0 + lane;
+        int js = 0, j = 0;
+        if (t < m) {
+            js = __float_as_int(L[K[t]].y);
+            j = perm ? perm[js] : js;
+        }
+        if (ms.kind == 0) {
+            const double* rt = t < m ? (xs ? xs + (int64_t)js * d : x + (int64_t)j * d) : nullptr;
+            const double d2 = warp_rows_np<true>(xi, rt, d, stage);
+            if (t < m) {
+                S[t] = exp(inv * d2);
+                D[t] = d2;
+            }
+        } else {
+            const double dot = warp_rows_np<false>(ms.xc + i * d, t < m ? ms.xc + (int64_t)j * d : nullptr, d, stage);
+            if (t < m) S[t] = D[t] = knn_corr_of(ms, dot, i, j);
+        }
+        __syncwarp();
+        if (t < m) J[t] = j;
+    }
+    __syncwarp();
+    // rank each kept candidate; the knn first ranks are selected (s_k: the
+    // knn-th value).  The selection is written in ascending j order: its
+    // slot is the number of selected candidates with a smaller index.
     double s_k = INFINITY;
-    for (int t = lane; t < cnt; t += 32) {
-        double st = S[t];
-        int jt = J[t];
-        int r = 0;
-        for (int u = 0; u < cnt; ++u) r += precedes(S[u], J[u], st, jt);
-        if (r < knn) sel[lp * knn + r] = jt;
-        if (r == knn - 1) s_k = st;
+    int ranks[TC_LIST_P / 32];
+#pragma unroll
+    for (int q = 0; q < TC_LIST_P / 32; ++q) {
+        const int t = lane + 32 * q;
+        ranks[q] = INT_MAX;
+        if (t < m) {
+            const double st = S[t];
+            const int jt = J[t];
+            int r = 0;
+            for (int u = 0; u < m; ++u) r += precedes(S[u], J[u], st, jt);
+            ranks[q] = r;
+            if (r == knn - 1) s_k = st;
+        }
     }
     // broadcast s_k (held by exactly one lane)
     for (int o = 16; o > 0; o >>= 1) s_k = fmin(s_k, __shfl_xor_sync(0xffffffffu, s_k, o));
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < TC_LIST_P / 32; ++q)  // non-selected candidates leave the index order
+        if (lane + 32 * q < m && ranks[q] >= knn) J[lane + 32 * q] = INT_MAX;
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < TC_LIST_P / 32; ++q) {
+        const int t = lane + 32 * q;
+        if (t < m && ranks[q] < knn) {
+            const int jt = J[t];
+            int slot = 0;
+            for (int u = 0; u < m; ++u) slot += J[u] < jt;
+            sel[lp * knn + slot] = jt;
+            if (selv) selv[lp * knn + slot] = D[t];  // the edge's d2 (exp_decay) or correlation
+        }
+    }
     if (lane != 0) return;
-    float tau = taus[lp];
     bool ok;
-    if (cnt < knn) {
+    const float tlow = fminf(tau, kdrop);  // smallest key of any point not evaluated exactly
+    if (m < knn) {
         ok = false;
-    } else if (isinf(tau)) {
-        ok = true;  // never compacted: every other point is a candidate
+    } else if (isinf(tlow)) {
+        ok = true;  // never compacted, nothing dropped: every other point was evaluated
     } else {
-        double rmax = __longlong_as_double((long long)*rmax_bits);
-        double r = rn[i] + rmax;
-        double delta = cdelta * r * r;
-        double lower = qn[i] + (double)tau - delta;  // lower bound of d2 for non-candidates
+        double lower = qn[i] + (double)tlow - delta;  // lower bound of d2 for the others
         lower = lower * (1.0 - 1e-12) - 1e-300;
         // cosine: unit rows, so a non-candidate has cos <= 1 - lower / 2
         ok = ms.kind == 0 ? (lower > 0.0 && s_k > exp(inv * lower)) : s_k > 1.0 - 0.5 * lower + 1e-12;
@@ -351,7 +503,8 @@ __global__ void __launch_bounds__(512) knn_fallback_kernel(int64_t n, int64_t p0
                                                            const int32_t* __restrict__ perm,
                                                            const int32_t* __restrict__ flagged, int64_t nflag,
                                                            unsigned long long* __restrict__ scratch,
-                                                           int32_t* __restrict__ sel, KnnMeasure ms) {
+                                                           int32_t* __restrict__ sel, KnnMeasure ms,
+                                                           double* __restrict__ selv) {
     __shared__ unsigned int hist[256];
     __shared__ unsigned long long s_prefix;
     __shared__ long long s_remaining;
@@ -442,23 +595,36 @@ __global__ void __launch_bounds__(512) knn_fallback_kernel(int64_t n, int64_t p0
             if (s_base >= take_eq) break;
         }
         __syncthreads();
+        if (selv)
+            for (int64_t t = threadIdx.x; t < knn; t += blockDim.x) {
+                const int64_t j = srow[t];
+                selv[(ip - p0) * knn + t] = ms.kind == 0 ? exact_d2(xi, x + j * d, d) : knn_corr(ms, d, i, j);
+            }
+        __syncthreads();
     }
 }
 
 // ---------------------------------------------------------------------------
 // union + CSR
-__global__ void sort_rows_kernel(int64_t n, int64_t knn, int32_t* __restrict__ sel) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+// ascending j order of the fallback rows (the recheck writes its rows sorted)
+__global__ void sort_rows_kernel(int64_t nrows, const int32_t* __restrict__ rows, int64_t p0, int64_t knn,
+                                 int32_t* __restrict__ sel, double* __restrict__ selv) {
+    const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= nrows) return;
+    const int64_t i = rows[f] - p0;
     int32_t* r = sel + i * knn;
+    double* w = selv ? selv + i * knn : nullptr;  // values travel with their columns
     for (int64_t a = 1; a < knn; ++a) {
         int32_t v = r[a];
+        const double wv = w ? w[a] : 0.0;
         int64_t b = a - 1;
         while (b >= 0 && r[b] > v) {
             r[b + 1] = r[b];
+            if (w) w[b + 1] = w[b];
             --b;
         }
         r[b + 1] = v;
+        if (w) w[b + 1] = wv;
     }
 }
 
@@ -480,7 +646,8 @@ __global__ void rev_count_kernel(int64_t total, int64_t r0, int64_t r1, const in
 
 __global__ void rev_fill_kernel(int64_t n, int64_t knn, int64_t r0, int64_t r1, const int32_t* __restrict__ sel,
                                 const int32_t* __restrict__ perm, const int64_t* __restrict__ rev_ptr,
-                                unsigned int* __restrict__ fill, int32_t* __restrict__ rev) {
+                                unsigned int* __restrict__ fill, int32_t* __restrict__ rev,
+                                int64_t* __restrict__ rev_src) {
     int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n * knn) return;
     const int64_t j = sel[p];
@@ -488,6 +655,7 @@ __global__ void rev_fill_kernel(int64_t n, int64_t knn, int64_t r0, int64_t r1, 
     unsigned int slot = atomicAdd(fill + (j - r0), 1u);
     const int64_t q = p / knn;
     rev[rev_ptr[j - r0] + slot] = perm ? perm[q] : (int32_t)q;
+    if (rev_src) rev_src[rev_ptr[j - r0] + slot] = p;  // the selection slot (its value)
 }
 
 __device__ __forceinline__ bool in_sorted(const int32_t* __restrict__ a, int64_t len, int32_t v) {
@@ -518,52 +686,309 @@ __global__ void row_count_kernel(int64_t nl, int64_t r0, int64_t knn, const int3
     if (lane == 0) len[i] = knn + c;
 }
 
-// edge value of the pair (i, e): exp_decay exp((-d2) / (2 sigma^2)) or the
-// correlation under the negative policy (graph.py:136-147, 229-236)
-__device__ __forceinline__ double edge_value(const KnnMeasure& ms, const double* __restrict__ x, int64_t d,
-                                             double den, int64_t i, int64_t e) {
-    if (ms.kind == 0) return exp(-exact_d2(x + i * d, x + e * d, d) / den);
-    const double v = knn_corr(ms, d, i, e);
-    return ms.policy == 0 ? (v > 0.0 ? v : 0.0) : (ms.policy == 1 ? fabs(v) : v);
-}
-
-__global__ void row_fill_kernel(int64_t nl, int64_t r0, int64_t d, int64_t knn, const double* __restrict__ x,
-                                double den, const int32_t* __restrict__ sel, const int32_t* __restrict__ pos,
-                                const int64_t* __restrict__ rev_ptr, const int32_t* __restrict__ rev,
-                                const uint8_t* __restrict__ dup, const int64_t* __restrict__ row_ptr,
-                                int32_t* __restrict__ col, double* __restrict__ vals,
-                                const int32_t* __restrict__ order, KnnMeasure ms) {
-    // local row; with `order` (whole graph only) the rows are visited in the
-    // kNN locality order so the x rows of their neighbours are L2-resident
+// CSR fill from the exact values the recheck kept (selv: the d2 or the
+// correlation of every selection slot, rev_src: the slot of each reverse
+// entry): no distances are recomputed.  The value of a reverse entry comes
+// from the other endpoint's slot, which is the same number (|a - b|^2 and the
+// dot product are symmetric bit for bit in the einsum order).  Warp per row;
+// the row's non-duplicate reverse entries are counted from shared memory.
+__global__ void __launch_bounds__(256) row_fill_vals_kernel(
+    int64_t nl, int64_t r0, int64_t knn, double den, const int32_t* __restrict__ sel, const double* __restrict__ selv,
+    const int32_t* __restrict__ pos, const int64_t* __restrict__ rev_ptr, const int32_t* __restrict__ rev,
+    const int64_t* __restrict__ rev_src, const uint8_t* __restrict__ dup, const int64_t* __restrict__ row_ptr,
+    int32_t* __restrict__ col, double* __restrict__ vals, const int32_t* __restrict__ order, int kind, int policy,
+    int64_t* __restrict__ long_rows, unsigned int* __restrict__ nlong) {
+    constexpr int FILL_CAP = 192;
+    __shared__ int32_t cin_all[8][FILL_CAP];
     int64_t i = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-    int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31;
+    int32_t* C = cin_all[threadIdx.x / 32];
     if (i >= nl) return;
     if (order) i = order[i];
-    const int32_t* s = sel + (int64_t)pos[r0 + i] * knn;
+    const int64_t slot0 = (int64_t)pos[r0 + i] * knn;
+    const int32_t* s = sel + slot0;
     const int64_t rb = rev_ptr[i], re = rev_ptr[i + 1];
     const int64_t out0 = row_ptr[i];
-    const double* xi = x + (r0 + i) * d;
-    // selected entries
-    for (int64_t t = lane; t < knn; t += 32) {
-        int32_t e = s[t];
-        int64_t r = t;
-        for (int64_t p = rb; p < re; ++p) r += (!dup[p] && rev[p] < e);
-        col[out0 + r] = e;
-        vals[out0 + r] = edge_value(ms, x, d, den, r0 + i, e);
+    auto value = [&](double v) {
+        if (kind == 0) return exp(-v / den);
+        return policy == 0 ? (v > 0.0 ? v : 0.0) : (policy == 1 ? fabs(v) : v);
+    };
+    // the non-duplicate reverse columns (shared memory when they fit; longer
+    // rows -- hubs selected by many points -- go to row_fill_long_kernel)
+    int nr = 0;
+    const bool fits = re - rb <= FILL_CAP;
+    if (!fits && long_rows) {
+        if (lane == 0) long_rows[atomicAdd(nlong, 1u)] = i;
+        return;
     }
-    // reverse-only entries
+    if (fits) {
+        for (int64_t p0 = rb; p0 < re; p0 += 32) {
+            const int64_t p = p0 + lane;
+            const bool a = p < re && !dup[p];
+            const unsigned bal = __ballot_sync(0xffffffffu, a);
+            if (a) C[nr + __popc(bal & ((1u << lane) - 1u))] = rev[p];
+            nr += __popc(bal);
+        }
+        __syncwarp();
+    }
+    auto rev_less = [&](int32_t e) {
+        int64_t r = 0;
+        if (fits)
+            for (int q = 0; q < nr; ++q) r += C[q] < e;
+        else
+            for (int64_t q = rb; q < re; ++q) r += (!dup[q] && rev[q] < e);
+        return r;
+    };
+    for (int64_t t = lane; t < knn; t += 32) {
+        const int32_t e = s[t];
+        const int64_t r = t + rev_less(e);
+        col[out0 + r] = e;
+        vals[out0 + r] = value(selv[slot0 + t]);
+    }
     for (int64_t p = rb + lane; p < re; p += 32) {
         if (dup[p]) continue;
-        int32_t e = rev[p];
+        const int32_t e = rev[p];
         int64_t lo = 0, hi = knn;
         while (lo < hi) {
-            int64_t mid = (lo + hi) >> 1;
+            const int64_t mid = (lo + hi) >> 1;
             if (s[mid] < e) lo = mid + 1; else hi = mid;
         }
-        int64_t r = lo;
-        for (int64_t q = rb; q < re; ++q) r += (!dup[q] && rev[q] < e);
+        const int64_t r = lo + rev_less(e);
         col[out0 + r] = e;
-        vals[out0 + r] = edge_value(ms, x, d, den, r0 + i, e);
+        vals[out0 + r] = value(selv[rev_src[p]]);
+    }
+}
+
+// The long rows of row_fill_vals_kernel, a block per row: the row's
+// non-duplicate reverse entries are sorted in shared memory (bitonic, with
+// their positions as payload) and merged with the sorted selection, instead
+// of the warp kernel's per-entry counting, which is quadratic in the row
+// length.  Rows longer than FILL_LONG fall back to counting.
+constexpr int FILL_LONG = 4096;
+__global__ void __launch_bounds__(256) row_fill_long_kernel(
+    int64_t r0, int64_t knn, double den, const int32_t* __restrict__ sel, const double* __restrict__ selv,
+    const int32_t* __restrict__ pos, const int64_t* __restrict__ rev_ptr, const int32_t* __restrict__ rev,
+    const int64_t* __restrict__ rev_src, const uint8_t* __restrict__ dup, const int64_t* __restrict__ row_ptr,
+    int32_t* __restrict__ col, double* __restrict__ vals, int kind, int policy, const int64_t* __restrict__ long_rows,
+    const unsigned int* __restrict__ nlong) {
+    __shared__ int32_t E[FILL_LONG];
+    __shared__ int32_t P[FILL_LONG];  // offsets in the row's reverse list
+    __shared__ int s_nr;
+    const int tid = threadIdx.x, lane = tid & 31;
+    auto value = [&](double v) {
+        if (kind == 0) return exp(-v / den);
+        return policy == 0 ? (v > 0.0 ? v : 0.0) : (policy == 1 ? fabs(v) : v);
+    };
+    const unsigned nrows = *nlong;
+    for (unsigned f = blockIdx.x; f < nrows; f += gridDim.x) {
+        const int64_t i = long_rows[f];
+        const int64_t slot0 = (int64_t)pos[r0 + i] * knn;
+        const int32_t* s = sel + slot0;
+        const int64_t rb = rev_ptr[i], re = rev_ptr[i + 1];
+        const int64_t out0 = row_ptr[i];
+        __syncthreads();
+        if (tid < 32) {  // warp 0 compacts the non-duplicate entries
+            int nr = 0;
+            for (int64_t p0 = rb; p0 < re; p0 += 32) {
+                const int64_t p = p0 + lane;
+                const bool a = p < re && !dup[p];
+                const unsigned bal = __ballot_sync(0xffffffffu, a);
+                const int q = nr + __popc(bal & ((1u << lane) - 1u));
+                if (a && q < FILL_LONG) {
+                    E[q] = rev[p];
+                    P[q] = (int32_t)(p - rb);
+                }
+                nr += __popc(bal);
+            }
+            if (lane == 0) s_nr = nr;
+        }
+        __syncthreads();
+        const int nr = s_nr;
+        if (nr <= FILL_LONG) {
+            int np2 = 1;
+            while (np2 < nr) np2 <<= 1;
+            for (int q = nr + tid; q < np2; q += blockDim.x) E[q] = INT_MAX;
+            __syncthreads();
+            for (int k = 2; k <= np2; k <<= 1)
+                for (int j = k >> 1; j > 0; j >>= 1) {
+                    for (int q = tid; q < np2; q += blockDim.x) {
+                        const int o = q ^ j;
+                        if (o > q) {
+                            const bool up = (q & k) == 0;
+                            if ((E[q] > E[o]) == up) {
+                                const int32_t te = E[q];
+                                E[q] = E[o];
+                                E[o] = te;
+                                const int32_t tp = P[q];
+                                P[q] = P[o];
+                                P[o] = tp;
+                            }
+                        }
+                    }
+                    __syncthreads();
+                }
+            for (int q = tid; q < nr; q += blockDim.x) {
+                const int32_t e = E[q];
+                int64_t lo = 0, hi = knn;
+                while (lo < hi) {
+                    const int64_t mid = (lo + hi) >> 1;
+                    if (s[mid] < e) lo = mid + 1; else hi = mid;
+                }
+                col[out0 + q + lo] = e;
+                vals[out0 + q + lo] = value(selv[rev_src[rb + P[q]]]);
+            }
+            for (int64_t t = tid; t < knn; t += blockDim.x) {
+                const int32_t e = s[t];
+                int lo = 0, hi = nr;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (E[mid] < e) lo = mid + 1; else hi = mid;
+                }
+                col[out0 + t + lo] = e;
+                vals[out0 + t + lo] = value(selv[slot0 + t]);
+            }
+        } else {
+            for (int64_t t = tid; t < knn; t += blockDim.x) {
+                const int32_t e = s[t];
+                int64_t r = t;
+                for (int64_t q = rb; q < re; ++q) r += (!dup[q] && rev[q] < e);
+                col[out0 + r] = e;
+                vals[out0 + r] = value(selv[slot0 + t]);
+            }
+            for (int64_t p = rb + tid; p < re; p += blockDim.x) {
+                if (dup[p]) continue;
+                const int32_t e = rev[p];
+                int64_t lo = 0, hi = knn;
+                while (lo < hi) {
+                    const int64_t mid = (lo + hi) >> 1;
+                    if (s[mid] < e) lo = mid + 1; else hi = mid;
+                }
+                int64_t r = lo;
+                for (int64_t q = rb; q < re; ++q) r += (!dup[q] && rev[q] < e);
+                col[out0 + r] = e;
+                vals[out0 + r] = value(selv[rev_src[p]]);
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(128) row_fill_kernel(int64_t nl, int64_t r0, int64_t d, int64_t knn,
+                                                       const double* __restrict__ x, double den,
+                                                       const int32_t* __restrict__ sel, const int32_t* __restrict__ pos,
+                                                       const int64_t* __restrict__ rev_ptr,
+                                                       const int32_t* __restrict__ rev, const uint8_t* __restrict__ dup,
+                                                       const int64_t* __restrict__ row_ptr, int32_t* __restrict__ col,
+                                                       double* __restrict__ vals, const int32_t* __restrict__ order,
+                                                       KnnMeasure ms, const double* __restrict__ xs) {
+    // warp per local row; with `order` (whole graph only) the rows are visited
+    // in the kNN locality order, and with xs (the points in that order) the x
+    // rows of a row's neighbours sit next to its own
+    constexpr int FILL_CAP = 256;
+    __shared__ double stage_all[4][kStageWarp];
+    __shared__ int32_t cin_all[4][FILL_CAP], cout_all[4][FILL_CAP];
+    int64_t i = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    double* stage = stage_all[threadIdx.x / 32];
+    int32_t* C = cin_all[threadIdx.x / 32];
+    int32_t* O = cout_all[threadIdx.x / 32];
+    if (i >= nl) return;
+    if (order) i = order[i];
+    const int64_t gi = r0 + i;
+    const int32_t* s = sel + (int64_t)pos[gi] * knn;
+    const int64_t rb = rev_ptr[i], re = rev_ptr[i + 1];
+    const int64_t out0 = row_ptr[i];
+    const double* ri = ms.kind == 0 ? (xs ? xs + (int64_t)pos[gi] * d : x + gi * d) : ms.xc + gi * d;
+    // value of the edge (gi, e) for the active lanes (warp-collective)
+    auto edge = [&](bool act, int32_t e) {
+        const double* rt =
+            act ? (ms.kind == 0 ? (xs ? xs + (int64_t)pos[e] * d : x + (int64_t)e * d) : ms.xc + (int64_t)e * d)
+                : nullptr;
+        if (ms.kind == 0) return exp(-warp_rows_np<true>(ri, rt, d, stage) / den);
+        const double v = act ? knn_corr_of(ms, warp_rows_np<false>(ri, rt, d, stage), gi, e)
+                             : warp_rows_np<false>(ri, rt, d, stage);
+        return ms.policy == 0 ? (v > 0.0 ? v : 0.0) : (ms.policy == 1 ? fabs(v) : v);
+    };
+    const int64_t len = row_ptr[i + 1] - out0;
+    if (len <= FILL_CAP) {
+        // merge in shared memory: C = the sorted selection, then the reverse
+        // entries not already selected; O = the row's columns in order
+        for (int t = lane; t < knn; t += 32) C[t] = s[t];
+        int nr = 0;
+        for (int64_t p0 = rb; p0 < re; p0 += 32) {
+            const int64_t p = p0 + lane;
+            const bool a = p < re && !dup[p];
+            const unsigned bal = __ballot_sync(0xffffffffu, a);
+            if (a) C[knn + nr + __popc(bal & ((1u << lane) - 1u))] = rev[p];
+            nr += __popc(bal);
+        }
+        __syncwarp();
+        const int32_t* Rv = C + knn;
+        for (int t = lane; t < len; t += 32) {
+            const int32_t e = C[t];
+            int r = 0;
+            if (t < knn) {
+                r = t;
+            } else {
+                int lo = 0, hi = (int)knn;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (C[mid] < e) lo = mid + 1; else hi = mid;
+                }
+                r = lo;
+            }
+            for (int q = 0; q < nr; ++q) r += Rv[q] < e;
+            O[r] = e;
+        }
+        __syncwarp();
+        for (int t0 = 0; t0 < len; t0 += 32) {
+            const int t = t0 + lane;
+            const bool act = t < len;
+            const int32_t e = act ? O[t] : 0;
+            const double v = edge(act, e);
+            if (act) {
+                col[out0 + t] = e;
+                vals[out0 + t] = v;
+            }
+        }
+        return;
+    }
+    // long rows: selected entries
+    for (int64_t t0 = 0; t0 < knn; t0 += 32) {
+        const int64_t t = t0 + lane;
+        const bool act = t < knn;
+        int32_t e = 0;
+        int64_t r = t;
+        if (act) {
+            e = s[t];
+            for (int64_t p = rb; p < re; ++p) r += (!dup[p] && rev[p] < e);
+        }
+        const double v = edge(act, e);
+        if (act) {
+            col[out0 + r] = e;
+            vals[out0 + r] = v;
+        }
+    }
+    // reverse-only entries
+    for (int64_t p0 = rb; p0 < re; p0 += 32) {
+        const int64_t p = p0 + lane;
+        const bool act = p < re && !dup[p];
+        int32_t e = 0;
+        int64_t r = 0;
+        if (act) {
+            e = rev[p];
+            int64_t lo = 0, hi = knn;
+            while (lo < hi) {
+                int64_t mid = (lo + hi) >> 1;
+                if (s[mid] < e) lo = mid + 1; else hi = mid;
+            }
+            r = lo;
+            for (int64_t q = rb; q < re; ++q) r += (!dup[q] && rev[q] < e);
+        }
+        const double v = edge(act, e);
+        if (act) {
+            col[out0 + r] = e;
+            vals[out0 + r] = v;
+        }
     }
 }
 
@@ -753,7 +1178,8 @@ __global__ void iota_kernel(int64_t n, int32_t* __restrict__ out) {
 // written to sel ((p1 - p0) x knn, each row ascending), plus the scan order
 // perm (n entries; identical on every caller for the same x).
 int knn_select(int64_t n, int64_t d, const double* x, int64_t knn, double two_sigma_sq, int64_t p0, int64_t p1,
-               int32_t* sel, int32_t* perm_out, int64_t* stats, cudaStream_t st, KnnMeasure ms = KnnMeasure()) {
+               int32_t* sel, int32_t* perm_out, int64_t* stats, cudaStream_t st, KnnMeasure ms = KnnMeasure(),
+               double* selv = nullptr) {
     const double inv = -1.0 / two_sigma_sq;  // graph.py:154
     const int64_t dp = (d + 15) / 16 * 16;
     const char* kenv = std::getenv("SPECLUST_KNN_KERNEL");
@@ -904,13 +1330,19 @@ int knn_select(int64_t n, int64_t d, const double* x, int64_t knn, double two_si
     // list slots start at tile qtile0; the recheck addresses them from p0
     const int64_t slot0 = p0 - qtile0 * 128;
     // ---- exact recheck + certificate
+    DevBuf<double> xs;  // points in scan order (exp_decay with a locality order)
+    if (perm && ms.kind == 0) {
+        if ((rc = xs.alloc((size_t)n * d))) return rc;
+        gather_rows_i32_kernel<<<(unsigned)ceil_div(n * d, 256), 256, 0, st>>>(n, d, x, perm, xs.p);
+        SC_LAUNCHED(1);
+    }
     {
-        size_t smem = (size_t)8 * cap * (sizeof(double) + sizeof(int));
+        size_t smem = (size_t)8 * (kStageWarp * sizeof(double) + cap * (2 * sizeof(double) + sizeof(int)));
         cudaFuncSetAttribute(knn_recheck_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         ProfScope prof("knn_recheck", st, (double)np * cap * d * 8.0);
         knn_recheck_kernel<<<(unsigned)ceil_div(np, 8), 256, smem, st>>>(
             n, p0, p1, d, x, knn, inv, cap, lists.p + slot0 * cap, counts.p + slot0, taus.p + slot0, rn.p, qn.p,
-            rmax.p, cdelta, perm, sel, flagged.p, nflag.p, ms);
+            rmax.p, cdelta, perm, sel, flagged.p, nflag.p, ms, xs.p, selv);
         SC_LAUNCHED(1);
     }
     unsigned long long hflag = 0;
@@ -925,17 +1357,19 @@ int knn_select(int64_t n, int64_t d, const double* x, int64_t knn, double two_si
         if ((rc = scratch.alloc((size_t)grid * n))) return rc;
         ProfScope prof("knn_fallback", st, (double)hflag * n * d * 8.0);
         knn_fallback_kernel<<<(unsigned)grid, 512, 0, st>>>(n, p0, d, x, knn, inv, perm, flagged.p, (int64_t)hflag,
-                                                            scratch.p, sel, ms);
+                                                            scratch.p, sel, ms, selv);
         SC_LAUNCHED(1);
     }
     {
         ProfScope prof("knn_union", st, 0.0);
-        sort_rows_kernel<<<(unsigned)ceil_div(np, 128), 128, 0, st>>>(np, knn, sel);
+        if (hflag > 0)
+            sort_rows_kernel<<<(unsigned)ceil_div((int64_t)hflag, 128), 128, 0, st>>>((int64_t)hflag, flagged.p, p0,
+                                                                                     knn, sel, selv);
         if (perm)
             SC_CUDA(cudaMemcpyAsync(perm_out, perm, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, st));
         else
             iota_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, perm_out);
-        SC_LAUNCHED(2);
+        SC_LAUNCHED((hflag > 0 ? 1 : 0) + (perm ? 0 : 1));
     }
     // the pooled scratch above is released on st; callers see sel/perm ordered on st
     if (stats) {
@@ -951,7 +1385,7 @@ int knn_select(int64_t n, int64_t d, const double* x, int64_t knn, double two_si
 // symmetrised kNN graph from the selections of all n points.
 int knn_union(int64_t n, int64_t d, const double* x, int64_t knn, double two_sigma_sq, const int32_t* sel,
               const int32_t* perm, int64_t r0, int64_t r1, int64_t* row_ptr, int32_t* col, double* vals, int64_t cap,
-              int64_t* nnz_out, cudaStream_t st, KnnMeasure ms = KnnMeasure()) {
+              int64_t* nnz_out, cudaStream_t st, KnnMeasure ms = KnnMeasure(), const double* selv = nullptr) {
     const int64_t nl = r1 - r0;
     int rc;
     DevBuf<int32_t> pos, rev;
@@ -971,9 +1405,11 @@ int knn_union(int64_t n, int64_t d, const double* x, int64_t knn, double two_sig
     int64_t nrev = 0;
     SC_CUDA(cudaMemcpyAsync(&nrev, rev_ptr.p + nl, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     SC_CUDA(cudaStreamSynchronize(st));
+    DevBuf<int64_t> rev_src;  // with selv: the selection slot of each reverse entry
     if ((rc = rev.alloc(std::max<int64_t>(nrev, 1))) || (rc = dup.alloc(std::max<int64_t>(nrev, 1)))) return rc;
+    if (selv && (rc = rev_src.alloc(std::max<int64_t>(nrev, 1)))) return rc;
     rev_fill_kernel<<<(unsigned)ceil_div(n * knn, 256), 256, 0, st>>>(n, knn, r0, r1, sel, perm, rev_ptr.p, fill.p,
-                                                                      rev.p);
+                                                                      rev.p, rev_src.p);
     row_count_kernel<<<(unsigned)ceil_div(nl, 8), 256, 0, st>>>(nl, r0, knn, sel, pos.p, rev_ptr.p, rev.p, dup.p,
                                                                 len.p);
     SC_LAUNCHED(2);
@@ -985,9 +1421,29 @@ int knn_union(int64_t n, int64_t d, const double* x, int64_t knn, double two_sig
     if (nnz > cap)
         return fail(SC_ERR_VALUE, "knn union: " + std::to_string(nnz) + " entries exceed the output capacity " +
                                       std::to_string(cap));
-    row_fill_kernel<<<(unsigned)ceil_div(nl, 8), 256, 0, st>>>(nl, r0, d, knn, x, two_sigma_sq, sel, pos.p, rev_ptr.p,
+    if (selv) {
+        DevBuf<int64_t> long_rows;
+        DevBuf<unsigned int> nlong;
+        if ((rc = long_rows.alloc(nl)) || (rc = nlong.alloc(1))) return rc;
+        SC_CUDA(cudaMemsetAsync(nlong.p, 0, sizeof(unsigned int), st));
+        row_fill_vals_kernel<<<(unsigned)ceil_div(nl, 8), 256, 0, st>>>(
+            nl, r0, knn, two_sigma_sq, sel, selv, pos.p, rev_ptr.p, rev.p, rev_src.p, dup.p, row_ptr, col, vals,
+            (r0 == 0 && nl == n) ? perm : nullptr, ms.kind, ms.policy, long_rows.p, nlong.p);
+        row_fill_long_kernel<<<(unsigned)(2 * kNumSMs), 256, 0, st>>>(r0, knn, two_sigma_sq, sel, selv, pos.p,
+                                                                      rev_ptr.p, rev.p, rev_src.p, dup.p, row_ptr, col,
+                                                                      vals, ms.kind, ms.policy, long_rows.p, nlong.p);
+        SC_LAUNCHED(2);
+        return SC_OK;
+    }
+    DevBuf<double> xs;  // points in scan order: the neighbours of a row are close there
+    if (perm && r0 == 0 && nl == n && ms.kind == 0) {
+        if ((rc = xs.alloc((size_t)n * d))) return rc;
+        gather_rows_i32_kernel<<<(unsigned)ceil_div(n * d, 256), 256, 0, st>>>(n, d, x, perm, xs.p);
+        SC_LAUNCHED(1);
+    }
+    row_fill_kernel<<<(unsigned)ceil_div(nl, 4), 128, 0, st>>>(nl, r0, d, knn, x, two_sigma_sq, sel, pos.p, rev_ptr.p,
                                                                rev.p, dup.p, row_ptr, col, vals,
-                                                               (r0 == 0 && nl == n) ? perm : nullptr, ms);
+                                                               (r0 == 0 && nl == n) ? perm : nullptr, ms, xs.p);
     SC_LAUNCHED(1);
     return SC_OK;
 }
@@ -995,11 +1451,13 @@ int knn_union(int64_t n, int64_t d, const double* x, int64_t knn, double two_sig
 int knn_graph_build(int64_t n, int64_t d, const double* x, int64_t knn, double two_sigma_sq, int64_t* row_ptr,
                     int32_t* col, double* vals, int64_t* nnz_out, int64_t* stats, cudaStream_t st) {
     DevBuf<int32_t> sel, perm;
+    DevBuf<double> selv;  // exact d2 of every selection slot, reused by the CSR fill
     int rc;
-    if ((rc = sel.alloc((size_t)n * knn)) || (rc = perm.alloc(n))) return rc;
-    if ((rc = knn_select(n, d, x, knn, two_sigma_sq, 0, n, sel.p, perm.p, stats, st))) return rc;
+    if ((rc = sel.alloc((size_t)n * knn)) || (rc = perm.alloc(n)) || (rc = selv.alloc((size_t)n * knn))) return rc;
+    if ((rc = knn_select(n, d, x, knn, two_sigma_sq, 0, n, sel.p, perm.p, stats, st, KnnMeasure(), selv.p)))
+        return rc;
     if ((rc = knn_union(n, d, x, knn, two_sigma_sq, sel.p, perm.p, 0, n, row_ptr, col, vals, 2 * n * knn, nnz_out,
-                        st)))
+                        st, KnnMeasure(), selv.p)))
         return rc;
     if (stats) stats[3] = *nnz_out;
     return SC_OK;
@@ -1025,8 +1483,9 @@ extern "C" int sc_knn_graph_f64(int64_t n, int64_t d, const double* x, int64_t k
     return knn_graph_build(n, d, x, knn, two_sigma_sq, row_ptr, col, vals, nnz_out, stats_out, as_stream(stream));
 }
 
-extern "C" int sc_knn_select_f64(int64_t n, int64_t d, const double* x, int64_t knn, double two_sigma_sq, int64_t p0,
-                                 int64_t p1, int32_t* sel, int32_t* perm, int64_t* stats_out, sc_stream_t stream) {
+extern "C" int sc_knn_select_vals_f64(int64_t n, int64_t d, const double* x, int64_t knn, double two_sigma_sq,
+                                      int64_t p0, int64_t p1, int32_t* sel, double* sel_vals, int32_t* perm,
+                                      int64_t* stats_out, sc_stream_t stream) {
     if (int rc = check_knn_args(n, d, knn, two_sigma_sq)) return rc;
     if (!(0 <= p0 && p0 <= p1 && p1 <= n) || p0 % 128 != 0)
         return fail(SC_ERR_VALUE, "scan range [p0, p1) must lie in [0, n] with p0 a multiple of 128");
@@ -1039,12 +1498,19 @@ extern "C" int sc_knn_select_f64(int64_t n, int64_t d, const double* x, int64_t 
         return knn_select(n, d, x, knn, two_sigma_sq, q0, q0 + 1, s1.p, perm, stats_out ? stats_out : tmp,
                           as_stream(stream));
     }
-    return knn_select(n, d, x, knn, two_sigma_sq, p0, p1, sel, perm, stats_out, as_stream(stream));
+    return knn_select(n, d, x, knn, two_sigma_sq, p0, p1, sel, perm, stats_out, as_stream(stream), KnnMeasure(),
+                      sel_vals);
 }
 
-extern "C" int sc_knn_union_f64(int64_t n, int64_t d, const double* x, int64_t knn, double two_sigma_sq,
-                                const int32_t* sel, const int32_t* perm, int64_t r0, int64_t r1, int64_t* row_ptr,
-                                int32_t* col, double* vals, int64_t cap, int64_t* nnz_out, sc_stream_t stream) {
+extern "C" int sc_knn_select_f64(int64_t n, int64_t d, const double* x, int64_t knn, double two_sigma_sq, int64_t p0,
+                                 int64_t p1, int32_t* sel, int32_t* perm, int64_t* stats_out, sc_stream_t stream) {
+    return sc_knn_select_vals_f64(n, d, x, knn, two_sigma_sq, p0, p1, sel, nullptr, perm, stats_out, stream);
+}
+
+extern "C" int sc_knn_union_vals_f64(int64_t n, int64_t d, const double* x, int64_t knn, double two_sigma_sq,
+                                     const int32_t* sel, const double* sel_vals, const int32_t* perm, int64_t r0,
+                                     int64_t r1, int64_t* row_ptr, int32_t* col, double* vals, int64_t cap,
+                                     int64_t* nnz_out, sc_stream_t stream) {
     if (int rc = check_knn_args(n, d, knn, two_sigma_sq)) return rc;
     if (!(0 <= r0 && r0 <= r1 && r1 <= n)) return fail(SC_ERR_VALUE, "row range [r0, r1) must lie in [0, n]");
     StreamScope stream_scope(as_stream(stream));
@@ -1056,7 +1522,14 @@ extern "C" int sc_knn_union_f64(int64_t n, int64_t d, const double* x, int64_t k
         return SC_OK;
     }
     return knn_union(n, d, x, knn, two_sigma_sq, sel, perm, r0, r1, row_ptr, col, vals, cap, nnz_out,
-                     as_stream(stream));
+                     as_stream(stream), KnnMeasure(), sel_vals);
+}
+
+extern "C" int sc_knn_union_f64(int64_t n, int64_t d, const double* x, int64_t knn, double two_sigma_sq,
+                                const int32_t* sel, const int32_t* perm, int64_t r0, int64_t r1, int64_t* row_ptr,
+                                int32_t* col, double* vals, int64_t cap, int64_t* nnz_out, sc_stream_t stream) {
+    return sc_knn_union_vals_f64(n, d, x, knn, two_sigma_sq, sel, nullptr, perm, r0, r1, row_ptr, col, vals, cap,
+                                 nnz_out, stream);
 }
 
 // exp(-d2 / (2 sigma^2)) per given pair (graph.py:136-141; build_similarity)
@@ -1120,9 +1593,10 @@ extern "C" int sc_knn_graph_measure_f64(int64_t n, int64_t d, const double* x, i
     DevBuf<double> xc, sq, xn;
     DevBuf<unsigned long long> bad;
     DevBuf<int32_t> sel, perm;
+    DevBuf<double> selv;
     int rc;
     if ((rc = xc.alloc((size_t)n * d)) || (rc = sq.alloc(n)) || (rc = xn.alloc((size_t)n * d)) || (rc = bad.alloc(1)) ||
-        (rc = sel.alloc((size_t)n * knn)) || (rc = perm.alloc(n)))
+        (rc = sel.alloc((size_t)n * knn)) || (rc = perm.alloc(n)) || (rc = selv.alloc((size_t)n * knn)))
         return rc;
     SC_CUDA(cudaMemsetAsync(bad.p, 0xff, sizeof(unsigned long long), st));
     corr_prep_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(n, d, x, kind == 2, xc.p, sq.p, xn.p, bad.p);
@@ -1141,9 +1615,9 @@ extern "C" int sc_knn_graph_measure_f64(int64_t n, int64_t d, const double* x, i
     ms.policy = negative_policy;
     int64_t tmp[8];
     int64_t* stats = stats_out ? stats_out : tmp;
-    if ((rc = knn_select(n, d, xn.p, knn, 1.0, 0, n, sel.p, perm.p, stats, st, ms))) return rc;
+    if ((rc = knn_select(n, d, xn.p, knn, 1.0, 0, n, sel.p, perm.p, stats, st, ms, selv.p))) return rc;
     if ((rc = knn_union(n, d, xn.p, knn, 1.0, sel.p, perm.p, 0, n, row_ptr, col, vals, 2 * n * knn, nnz_out, st,
-                        ms)))
+                        ms, selv.p)))
         return rc;
     stats[3] = *nnz_out;
     return SC_OK;

@@ -176,14 +176,17 @@ def knn_graph_device(x, knn: int, m: SimilarityMeasure, return_stats: bool = Fal
         return _knn_graph_corr(xd, knn, m, negative_policy, return_stats)
     # selection (sc_knn_select_f64) + union (sc_knn_union_f64) == sc_knn_graph_f64;
     # the two-stage form keeps the locality scan order for the eigensolver
+    # the selection also returns each slot's exact d2, so the union fills the
+    # CSR values without recomputing distances
     sel = torch.empty((n, knn), dtype=torch.int32, device="cuda")
+    sel_vals = torch.empty((n, knn), dtype=torch.float64, device="cuda")
     perm = torch.empty(n, dtype=torch.int32, device="cuda")
     stats = (nat.C.c_int64 * 8)()
     lib = nat.load()
-    nat.check(lib.sc_knn_select_f64(n, d, nat.ptr(xd), knn, m.two_sigma_sq(), 0, n, nat.ptr(sel), nat.ptr(perm),
-                                    stats, nat.stream_handle()))
-    w = knn_union_device(xd, knn, m, sel, perm, 0, n)
-    del sel
+    nat.check(lib.sc_knn_select_vals_f64(n, d, nat.ptr(xd), knn, m.two_sigma_sq(), 0, n, nat.ptr(sel),
+                                         nat.ptr(sel_vals), nat.ptr(perm), stats, nat.stream_handle()))
+    w = knn_union_device(xd, knn, m, sel, perm, 0, n, sel_vals)
+    del sel, sel_vals
     w.locality_perm = perm  # scan position -> point
     if return_stats:
         keys = ("list_R", "list_cap", "fallback_rows")
@@ -217,9 +220,12 @@ def knn_select_device(x, knn: int, m: SimilarityMeasure, p0: int, p1: int):
     return sel[: p1 - p0], perm
 
 
-def knn_union_device(x, knn: int, m: SimilarityMeasure, sel, perm, r0: int, r1: int) -> DeviceCsr:
+def knn_union_device(x, knn: int, m: SimilarityMeasure, sel, perm, r0: int, r1: int,
+                     sel_vals=None) -> DeviceCsr:
     """Union stage: CSR rows [r0, r1) of W (global columns) from the full
-    scan-order selection (sc_knn_union_f64)."""
+    scan-order selection (sc_knn_union_f64; with ``sel_vals``, the exact
+    per-slot d2 of the selection, sc_knn_union_vals_f64 fills the values
+    without recomputing distances)."""
     torch = nat.torch_cuda()
     xd = _points_device(x)
     n, d = xd.shape
@@ -231,9 +237,10 @@ def knn_union_device(x, knn: int, m: SimilarityMeasure, sel, perm, r0: int, r1: 
     for _ in range(2):  # a shard whose reverse edges exceed 2*knn per row retries at the exact size
         col = torch.empty(cap, dtype=torch.int32, device="cuda")
         vals = torch.empty(cap, dtype=torch.float64, device="cuda")
-        rc = lib.sc_knn_union_f64(n, d, nat.ptr(xd), knn, m.two_sigma_sq(), nat.ptr(sel), nat.ptr(perm), r0, r1,
-                                  nat.ptr(row_ptr), nat.ptr(col), nat.ptr(vals), cap, nat.C.byref(nnz),
-                                  nat.stream_handle())
+        rc = lib.sc_knn_union_vals_f64(n, d, nat.ptr(xd), knn, m.two_sigma_sq(), nat.ptr(sel),
+                                       None if sel_vals is None else nat.ptr(sel_vals), nat.ptr(perm), r0, r1,
+                                       nat.ptr(row_ptr), nat.ptr(col), nat.ptr(vals), cap, nat.C.byref(nnz),
+                                       nat.stream_handle())
         if rc == 0:
             k = nnz.value
             return DeviceCsr(nl, n, row_ptr, col[:k], vals[:k])

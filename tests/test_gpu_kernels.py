@@ -142,6 +142,32 @@ def test_knn_small_examples():
         sc.build_edges_knn(np.zeros((3, 1)), 3, m)
 
 
+@pytest.mark.parametrize("n,d", [(1200, 128), (6000, 256)])
+def test_knn_hub_rows_value_carrying_fill(n, d):
+    """A hub point selected by (almost) every other point: its CSR row has far
+    more reverse entries than the fill's shared-memory merge holds, so it takes
+    the long-row path.  The value-carrying union (exact d2 of each selection
+    slot reused) must equal the recomputing union and the oracle."""
+    from paper_1802_04450_b200 import _native as nat
+    from paper_1802_04450_b200.graph import knn_graph_device, knn_select_device, knn_union_device
+
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal((n, d))
+    x /= np.linalg.norm(x, axis=1, keepdims=True)
+    x[0] = 0.0  # the hub: at distance 1 from every point, the others ~sqrt(2) apart
+    sigma = 0.8
+    m = sc.SimilarityMeasure.exp_decay(sigma)
+    w = knn_graph_device(x, 2, m).to_host()
+    assert np.diff(w.row_ptr)[0] > 256
+    e = orc.knn_edges(x, 2, sigma)
+    want = orc.csr_from_edges(n, e, orc.edge_weights(x, e, sigma))
+    assert np.array_equal(w.row_ptr, want[0]) and np.array_equal(w.col_idx, want[1])
+    assert_ulp(w.vals, want[2], 2)
+    sel, perm = knn_select_device(x, 2, m, 0, n)
+    w2 = knn_union_device(x, 2, m, sel, perm, 0, n).to_host()  # recomputes the distances
+    assert np.array_equal(w2.col_idx, w.col_idx) and np.array_equal(w2.vals, w.vals)
+
+
 def test_knn_matches_oracle_random_shapes():
     rng = np.random.default_rng(5)
     for n, d, knn, scale in [(300, 3, 4, 1.0), (513, 17, 9, 0.3), (130, 64, 31, 3.0), (1000, 5, 1, 10.0),

@@ -7,17 +7,18 @@ from paper_1802_04450_b200 import _native as nat
 from paper_1802_04450_b200.graph import knn_graph_device
 from bench import make_blobs
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000
-x, _ = make_blobs(n, 64, 100, 0.7)
+d = int(sys.argv[2]) if len(sys.argv) > 2 else 64
+x, _ = make_blobs(n, d, 100, 0.7)
 xd = torch.from_numpy(x).cuda()
 lib = nat.load()
 try:
-    knn_graph_device(xd, 32, sc.SimilarityMeasure.exp_decay(8.0))
+    knn_graph_device(xd, 32, sc.SimilarityMeasure.exp_decay(float(np.sqrt(d))))
 except Exception as e:
     print("error", e)
 torch.cuda.synchronize()
 lib.sc_profile_reset(); lib.sc_profile_enable(1)
 try:
-    knn_graph_device(xd, 32, sc.SimilarityMeasure.exp_decay(8.0))
+    knn_graph_device(xd, 32, sc.SimilarityMeasure.exp_decay(float(np.sqrt(d))))
 except Exception as e:
     print("error", e)
 torch.cuda.synchronize()
