@@ -202,6 +202,55 @@ __device__ __forceinline__ double np_sqnorm(const double* __restrict__ a, int64_
     return s.result();
 }
 
+// Warp-cooperative dot(a_t, b_t) in the einsum order for one row pair per
+// lane (nullptr: none).  Each row is read with coalesced warp loads into a
+// shared-memory tile, 32 columns at a time, and every lane then folds its own
+// pair from the tiles -- a lane-per-row loop would cost one L1 wavefront per
+// lane per element.  stage: kPairStage doubles per warp.  Bit-identical to
+// np_dot_span over __dmul_rn(a[l], b[l]).
+constexpr int kPairLd = 33;
+constexpr int kPairStage = 2 * 32 * kPairLd + 64;
+__device__ __forceinline__ double warp_pair_dot_np(const double* a, const double* b, int64_t d,
+                                                   double* __restrict__ stage) {
+    const int lane = threadIdx.x & 31;
+    double* sa = stage;
+    double* sb = stage + 32 * kPairLd;
+    const double** pa = reinterpret_cast<const double**>(stage + 2 * 32 * kPairLd);
+    const double** pb = pa + 32;
+    __syncwarp();
+    pa[lane] = a;
+    pb[lane] = b;
+    NpDot acc;
+    for (int64_t c0 = 0; c0 < d; c0 += 32) {
+        const int w = (int)(d - c0 < 32 ? d - c0 : 32);
+        __syncwarp();
+#pragma unroll
+        for (int r0 = 0; r0 < 32; r0 += 8) {
+            double va[8], vb[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const double* ra = pa[r0 + q];
+                const double* rb = pb[r0 + q];
+                const bool ok = ra && lane < w;
+                va[q] = ok ? __ldg(ra + c0 + lane) : 0.0;
+                vb[q] = ok ? __ldg(rb + c0 + lane) : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                sa[(r0 + q) * kPairLd + lane] = va[q];
+                sb[(r0 + q) * kPairLd + lane] = vb[q];
+            }
+        }
+        __syncwarp();
+        if (a) {
+            const double* ra = sa + lane * kPairLd - c0;
+            const double* rb = sb + lane * kPairLd - c0;
+            np_dot_span(acc, c0, c0 + w, [&](int64_t l) { return __dmul_rn(ra[l], rb[l]); });
+        }
+    }
+    return acc.result();
+}
+
 // numpy's pairwise summation of a contiguous float64 run (pairwise.c: blocks
 // of 8 accumulators up to 128 elements, halving above)
 inline __device__ double np_pairwise_sum_dev(const double* a, int64_t n) {

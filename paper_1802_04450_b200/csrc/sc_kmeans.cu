@@ -457,53 +457,24 @@ __global__ void reseed_finish_kernel(int nb, const double* __restrict__ pv, cons
 // candidate partials (count, weight sum) over untaken rows with d2 > 0.
 // `prow` = coordinates of the drawn row; `pick` = its local index (or -1 when
 // the row lives on another shard)
+// Points in 8-column panels (panel b = columns 8b..8b+7 of every row, n x 8,
+// zero-padded): a thread's 64-byte piece of a row is contiguous with its
+// neighbours', so the k-means++ update reads the panels coalesced and stops
+// at the first panel whose partial sum reaches the row's d2.
+__global__ void to_panels_kernel(int64_t n, int64_t d, const double* __restrict__ v, double* __restrict__ v8) {
+    const int64_t nch = (d + 7) / 8;
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= nch * n * 8) return;
+    const int64_t b = e / (n * 8), rem = e - b * n * 8, i = rem >> 3, q = rem & 7;
+    const int64_t c = 8 * b + q;
+    v8[e] = c < d ? v[i * d + c] : 0.0;
+}
+
 constexpr int KPP_UPD_ROWS = 128, KPP_UPD_COLS = 32;
 
-__global__ void __launch_bounds__(KPP_UPD_ROWS) kpp_update_kernel(int64_t n, int64_t d, const double* __restrict__ v, const double* __restrict__ prow,
-                                  int64_t pick, int first, double* __restrict__ d2, uint8_t* __restrict__ taken,
-                                  double* __restrict__ pw, int64_t* __restrict__ pc) {
-    // one thread per row, folding its row against the new centre in numpy's
-    // einsum order (_dist_to_one, kmeans.py:101-104).  Rows are read
-    // directly, 32 columns at a time; once the partial sum already reaches the
-    // row's current d2 the rest is skipped: rounded additions of nonnegative
-    // terms never decrease the sum, so the full distance could not lower d2
-    // and min(d2, dist) = d2 exactly (most rows, once the seeding has covered
-    // their region).
-    __shared__ double sw[KPP_UPD_ROWS / 32];
-    __shared__ int64_t scn[KPP_UPD_ROWS / 32];
+__device__ __forceinline__ void kpp_block_partials(double w, int64_t cnt, double* sw, int64_t* scn,
+                                                   double* __restrict__ pw, int64_t* __restrict__ pc) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int64_t i = (int64_t)blockIdx.x * KPP_UPD_ROWS + tid;
-    NpDot acc;
-    bool pruned = false;
-    double old = 0.0;
-    if (i < n) {
-        const double* row = v + i * d;
-        if (!first) old = d2[i];
-        for (int64_t c0 = 0; c0 < d; c0 += KPP_UPD_COLS) {
-            const int64_t c1 = imin64(d, c0 + KPP_UPD_COLS);
-            np_dot_span(acc, c0, c1, [&](int64_t l) {
-                const double t = __dsub_rn(__ldg(row + l), __ldg(prow + l));
-                return __dmul_rn(t, t);
-            });
-            if (!first && c1 < d && acc.result() >= old) {
-                pruned = true;
-                break;
-            }
-        }
-    }
-    double w = 0.0;
-    int64_t cnt = 0;
-    if (i < n) {
-        const double dist = acc.result();
-        const double nv = first ? dist : (pruned ? old : fmin(old, dist));
-        if (i == pick) taken[i] = 1;
-        const bool tk = (i == pick) || taken[i];
-        d2[i] = nv;
-        if (!tk && nv > 0.0) {
-            w = nv;
-            cnt = 1;
-        }
-    }
     // fixed-order block partials (deterministic)
     for (int o = 16; o > 0; o >>= 1) {
         w += __shfl_down_sync(0xffffffffu, w, o);
@@ -525,6 +496,157 @@ __global__ void __launch_bounds__(KPP_UPD_ROWS) kpp_update_kernel(int64_t n, int
         pc[blockIdx.x] = c;
     }
 }
+
+__global__ void __launch_bounds__(KPP_UPD_ROWS) kpp_update_kernel(int64_t n, int64_t d, const double* __restrict__ v, const double* __restrict__ prow,
+                                  int64_t pick, int first, double* __restrict__ d2, uint8_t* __restrict__ taken,
+                                  double* __restrict__ pw, int64_t* __restrict__ pc) {
+    // one thread per row, folding its row against the new centre in numpy's
+    // einsum order (_dist_to_one, kmeans.py:101-104).  Rows are read
+    // directly, 32 columns at a time; once the partial sum already reaches the
+    // row's current d2 the rest is skipped: rounded additions of nonnegative
+    // terms never decrease the sum, so the full distance could not lower d2
+    // and min(d2, dist) = d2 exactly (most rows, once the seeding has covered
+    // their region).
+    // The warp's 32 rows are staged through shared memory a 32-column chunk at
+    // a time with coalesced loads (a thread-per-row read costs one L1
+    // wavefront per lane per element); pruned rows stop loading.
+    __shared__ double sw[KPP_UPD_ROWS / 32];
+    __shared__ int64_t scn[KPP_UPD_ROWS / 32];
+    __shared__ double stg_all[KPP_UPD_ROWS / 32][32 * (KPP_UPD_COLS + 1)];
+    __shared__ const double* rows_all[KPP_UPD_ROWS / 32][32];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t i = (int64_t)blockIdx.x * KPP_UPD_ROWS + tid;
+    double* stg = stg_all[warp];
+    const double** rows = rows_all[warp];
+    NpDot acc;
+    bool pruned = false;
+    double old = 0.0;
+    const double* row = i < n ? v + i * d : nullptr;
+    if (i < n && !first) old = d2[i];
+    for (int64_t c0 = 0; c0 < d; c0 += KPP_UPD_COLS) {
+        const bool active = row && !pruned;
+        if (!__any_sync(0xffffffffu, active)) break;
+        const int w = (int)imin64(KPP_UPD_COLS, d - c0);
+        rows[lane] = active ? row : nullptr;
+        __syncwarp();
+#pragma unroll
+        for (int r0 = 0; r0 < 32; r0 += 8) {
+            double vv[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const double* pr = rows[r0 + q];
+                vv[q] = (pr && lane < w) ? __ldg(pr + c0 + lane) : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) stg[(r0 + q) * (KPP_UPD_COLS + 1) + lane] = vv[q];
+        }
+        __syncwarp();
+        if (active) {
+            const double* sr = stg + lane * (KPP_UPD_COLS + 1) - c0;
+            np_dot_span(acc, c0, c0 + w, [&](int64_t l) {
+                const double t = __dsub_rn(sr[l], __ldg(prow + l));
+                return __dmul_rn(t, t);
+            });
+            if (!first && c0 + w < d && acc.result() >= old) pruned = true;
+        }
+        __syncwarp();
+    }
+    double w = 0.0;
+    int64_t cnt = 0;
+    if (i < n) {
+        const double dist = acc.result();
+        const double nv = first ? dist : (pruned ? old : fmin(old, dist));
+        if (i == pick) taken[i] = 1;
+        const bool tk = (i == pick) || taken[i];
+        d2[i] = nv;
+        if (!tk && nv > 0.0) {
+            w = nv;
+            cnt = 1;
+        }
+    }
+    kpp_block_partials(w, cnt, sw, scn, pw, pc);
+}
+
+// |c_t - c_j|^2 for the centres drawn before c_t (plain fp64: only used in
+// the bound below, with a margin)
+__global__ void kpp_centre_dist_kernel(int64_t d, int t, const double* __restrict__ cent, double* __restrict__ cc) {
+    const int j = (int)(blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32), lane = threadIdx.x & 31;
+    if (j >= t) return;
+    double a = 0.0;
+    for (int64_t l = lane; l < d; l += 32) {
+        const double u = cent[(int64_t)t * d + l] - cent[(int64_t)j * d + l];
+        a = fma(u, u, a);
+    }
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) cc[j] = a;
+}
+
+// the same update over 8-column panels (to_panels_kernel), pruning per panel;
+// d2 is identical (the prune is exact whatever the granularity).  With cc
+// (the distances of the new centre c_t to the earlier ones) a row whose
+// nearest centre c_a = ctr[i] has |c_t - c_a|^2 > 4 d2 (1 + 1e-6) is skipped
+// unread: |x - c_t| >= |c_t - c_a| - |x - c_a| > |x - c_a| (the margin is
+// far above the rounding of the computed squares), so min(d2, dist) = d2.
+__global__ void __launch_bounds__(KPP_UPD_ROWS) kpp_update_panel_kernel(int64_t n, int64_t d,
+                                                                        const double* __restrict__ v8,
+                                                                        const double* __restrict__ prow, int64_t pick,
+                                                                        int first, double* __restrict__ d2,
+                                                                        uint8_t* __restrict__ taken,
+                                                                        double* __restrict__ pw,
+                                                                        int64_t* __restrict__ pc,
+                                                                        const double* __restrict__ cc,
+                                                                        int32_t* __restrict__ ctr, int t) {
+    __shared__ double sw[KPP_UPD_ROWS / 32];
+    __shared__ int64_t scn[KPP_UPD_ROWS / 32];
+    const int64_t i = (int64_t)blockIdx.x * KPP_UPD_ROWS + threadIdx.x;
+    NpDot acc;
+    bool pruned = false;
+    double old = 0.0;
+    if (i < n) {
+        if (!first) old = d2[i];
+        if (!first && cc && cc[ctr[i]] > 4.0 * old * (1.0 + 1e-6)) pruned = true;
+        for (int64_t c0 = 0; c0 < d && !pruned; c0 += 8) {
+            const double2* src = reinterpret_cast<const double2*>(v8 + ((c0 >> 3) * n + i) * 8);
+            const double2 a0 = __ldg(src), a1 = __ldg(src + 1), a2 = __ldg(src + 2), a3 = __ldg(src + 3);
+            const double x[8] = {a0.x, a0.y, a1.x, a1.y, a2.x, a2.y, a3.x, a3.y};
+            auto f = [&](int q) {
+                const double t = __dsub_rn(x[q], __ldg(prow + c0 + q));
+                return __dmul_rn(t, t);
+            };
+            const int rem = (int)(d - c0 < 8 ? d - c0 : 8);
+            if (rem == 8) {
+                acc.block(f(0), f(1), f(2), f(3), f(4), f(5), f(6), f(7));
+            } else {  // the tail: pairs, then a single (np_dot_span)
+#pragma unroll
+                for (int q = 0; q < 8; q += 2)
+                    if (q + 2 <= rem) acc.pair(f(q), f(q + 1));
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    if ((rem & 1) && q == rem - 1) acc.single(f(q));
+            }
+            if (!first && c0 + 8 < d && acc.result() >= old) {
+                pruned = true;
+                break;
+            }
+        }
+    }
+    double w = 0.0;
+    int64_t cnt = 0;
+    if (i < n) {
+        const double dist = acc.result();
+        const double nv = first ? dist : (pruned ? old : fmin(old, dist));
+        if (ctr && (first || (!pruned && dist < old))) ctr[i] = t;  // the nearest centre so far
+        if (i == pick) taken[i] = 1;
+        const bool tk = (i == pick) || taken[i];
+        d2[i] = nv;
+        if (!tk && nv > 0.0) {
+            w = nv;
+            cnt = 1;
+        }
+    }
+    kpp_block_partials(w, cnt, sw, scn, pw, pc);
+}
+
 
 __global__ void kpp_total_kernel(int64_t nb, const double* __restrict__ pw, const int64_t* __restrict__ pc,
                                  double* __restrict__ out_total, int64_t* __restrict__ out_count) {
@@ -864,8 +986,11 @@ __global__ void as_finalize_kernel(int64_t n, int64_t d, int64_t dp, double s, c
                                    const int64_t* __restrict__ old_labels, int64_t* __restrict__ labels,
                                    double* __restrict__ cost, int32_t* __restrict__ flagged,
                                    unsigned long long* __restrict__ nflag, unsigned long long* __restrict__ changes) {
+    extern __shared__ double fin_stage[];
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int chg = 0;
+    bool certified = false;
+    int32_t b = -1;
     if (i < n) {
         const double cnmax = __longlong_as_double((long long)*cnmax_bits);
         const double cmax = sqrt(cnmax);
@@ -874,14 +999,18 @@ __global__ void as_finalize_kernel(int64_t n, int64_t d, int64_t dp, double s, c
                                      0x1p-24 * (2.0 * cnmax + 2.0 * va * cmax) +
                                      0x1p-24 * sqrt((double)dp) * (va + cmax) / s);
         const float2 bk = best_keys[i];
-        const int32_t b = best_idx[i];
-        if (b >= 0 && (double)bk.y - (double)bk.x > 2.0 * delta) {
-            labels[i] = b;
-            cost[i] = exact_s(v + i * d, vn[i], c + (int64_t)b * d, cn[b], d);
-            if (old_labels) chg = old_labels[i] != b;
-        } else {
-            flagged[atomicAdd(nflag, 1ull)] = (int32_t)i;
-        }
+        b = best_idx[i];
+        certified = b >= 0 && (double)bk.y - (double)bk.x > 2.0 * delta;
+        if (!certified) flagged[atomicAdd(nflag, 1ull)] = (int32_t)i;
+    }
+    // exact cost of the certified rows (exact_s, with the rows staged per warp)
+    const double dot = warp_pair_dot_np(certified ? v + i * d : nullptr, certified ? c + (int64_t)b * d : nullptr, d,
+                                        fin_stage + (threadIdx.x >> 5) * kPairStage);
+    if (certified) {
+        labels[i] = b;
+        const double r = __dsub_rn(__dadd_rn(vn[i], cn[b]), __dmul_rn(2.0, dot));
+        cost[i] = r > 0.0 ? r : 0.0;
+        if (old_labels) chg = old_labels[i] != b;
     }
     const unsigned bal = __ballot_sync(0xffffffffu, chg);
     if ((threadIdx.x & 31) == 0 && bal) atomicAdd(changes, (unsigned long long)__popc(bal));
@@ -1045,9 +1174,11 @@ struct AssignTc {
             SC_LAUNCHED(1);
             return SC_OK;
         }
-        as_finalize_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, d, dp, s, v, vn, c, cn, scal.p + 1, bidx.p,
-                                                                        bkeys.p, old_labels, labels, cost, flagged.p,
-                                                                        scal.p, changes);
+        constexpr int fin_smem = 4 * kPairStage * (int)sizeof(double);
+        SC_CUDA(cudaFuncSetAttribute(as_finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fin_smem));
+        as_finalize_kernel<<<(unsigned)ceil_div(n, 128), 128, fin_smem, st>>>(n, d, dp, s, v, vn, c, cn, scal.p + 1,
+                                                                             bidx.p, bkeys.p, old_labels, labels,
+                                                                             cost, flagged.p, scal.p, changes);
         SC_LAUNCHED(1);
         // uncertified rows: exact re-scan.  Few rows or few centroids: a warp
         // per row; otherwise the rows are gathered and run through the tiled
@@ -1123,9 +1254,46 @@ struct sc_kmeanspp {
     cudaStream_t st = nullptr;
     bool first = true;
     int64_t taken_count = 0;
-    DevBuf<double> d2, pw, bsum, total;
+    DevBuf<double> d2, pw, bsum, total, v8;  // v8: the points in 8-column panels
     DevBuf<int64_t> pc, count, pick;
     DevBuf<uint8_t> taken;
+    // centres drawn so far (up to ccap), their distances to the newest one and
+    // each row's nearest centre: the triangle-inequality skip of the update
+    static constexpr int ccap = 1024;
+    DevBuf<double> cent, cc;
+    DevBuf<int32_t> ctr;
+    int ncent = 0;
+    bool bound = false;
+
+    // d2 <- min(d2, |v - row|^2) and the candidate partials (row: the drawn
+    // point's coordinates, device; pick: its local index or -1)
+    int update(const double* row, int64_t pick_index) {
+        ProfScope prof("kmeanspp", st, (double)n * d * 8.0);
+        if (v8.p) {
+            const double* ccp = nullptr;
+            int t = -1;
+            if (bound && ncent < ccap) {
+                t = ncent++;
+                SC_CUDA(cudaMemcpyAsync(cent.p + (int64_t)t * d, row, sizeof(double) * d, cudaMemcpyDeviceToDevice,
+                                        st));
+                if (t > 0) {
+                    kpp_centre_dist_kernel<<<(unsigned)ceil_div(t, 8), 256, 0, st>>>(d, t, cent.p, cc.p);
+                    SC_LAUNCHED(1);
+                    ccp = cc.p;
+                }
+            } else {
+                bound = false;  // past ccap centres: plain updates from here on
+            }
+            kpp_update_panel_kernel<<<(unsigned)nb_upd, KPP_UPD_ROWS, 0, st>>>(
+                n, d, v8.p, row, pick_index, first ? 1 : 0, d2.p, taken.p, pw.p, pc.p, ccp, bound ? ctr.p : nullptr,
+                t);
+        } else {
+            kpp_update_kernel<<<(unsigned)nb_upd, KPP_UPD_ROWS, 0, st>>>(n, d, v, row, pick_index, first ? 1 : 0, d2.p,
+                                                                         taken.p, pw.p, pc.p);
+        }
+        SC_LAUNCHED(1);
+        return SC_OK;
+    }
 };
 
 extern "C" {
@@ -1278,6 +1446,14 @@ int sc_kmeanspp_create(int64_t n, int64_t d, const double* v, sc_stream_t stream
         return rc;
     }
     cudaMemsetAsync(s->taken.p, 0, n, s->st);
+    // 8-column panels of the points for the update (skipped when memory is short)
+    const int64_t nch = ceil_div(d, 8);
+    if (s->v8.alloc((size_t)nch * n * 8) == SC_OK) {
+        to_panels_kernel<<<(unsigned)ceil_div(nch * n * 8, 256), 256, 0, s->st>>>(n, d, v, s->v8.p);
+        SC_LAUNCHED(1);
+        s->bound = s->cent.alloc((size_t)sc_kmeanspp::ccap * d) == SC_OK &&
+                   s->cc.alloc(sc_kmeanspp::ccap) == SC_OK && s->ctr.alloc(n) == SC_OK;
+    }
     *out = s;
     return SC_OK;
 }
@@ -1286,14 +1462,9 @@ void sc_kmeanspp_destroy(sc_kmeanspp_t* s) { delete s; }
 
 int sc_kmeanspp_take(sc_kmeanspp_t* s, int64_t index) {
     if (index < 0 || index >= s->n) return fail(SC_ERR_VALUE, "k-means++ index out of range");
-    {
-        ProfScope prof("kmeanspp", s->st, (double)s->n * s->d * 8.0);
-        kpp_update_kernel<<<(unsigned)s->nb_upd, KPP_UPD_ROWS, 0, s->st>>>(s->n, s->d, s->v, s->v + index * s->d, index,
-                                                                  s->first ? 1 : 0, s->d2.p, s->taken.p, s->pw.p,
-                                                                  s->pc.p);
-    }
+    if (int rc = s->update(s->v + index * s->d, index)) return rc;
     kpp_total_kernel<<<1, 1024, 0, s->st>>>(s->nb_upd, s->pw.p, s->pc.p, s->total.p, s->count.p);
-    SC_LAUNCHED(2);
+    SC_LAUNCHED(1);
     s->first = false;
     s->taken_count += 1;
     return SC_OK;
@@ -1326,14 +1497,9 @@ int sc_kmeanspp_pick(sc_kmeanspp_t* s, int mode, double u, int64_t r, int64_t* i
 
 // ---- shard-aware k-means++ steps (point shards, global draw order = rank order)
 int sc_kmeanspp_take_row(sc_kmeanspp_t* s, const double* row, int64_t local_index) {
-    {
-        ProfScope prof("kmeanspp", s->st, (double)s->n * s->d * 8.0);
-        kpp_update_kernel<<<(unsigned)s->nb_upd, KPP_UPD_ROWS, 0, s->st>>>(s->n, s->d, s->v, row, local_index,
-                                                                  s->first ? 1 : 0, s->d2.p, s->taken.p, s->pw.p,
-                                                                  s->pc.p);
-    }
+    if (int rc = s->update(row, local_index)) return rc;
     kpp_total_kernel<<<1, 1024, 0, s->st>>>(s->nb_upd, s->pw.p, s->pc.p, s->total.p, s->count.p);
-    SC_LAUNCHED(2);
+    SC_LAUNCHED(1);
     s->first = false;
     if (local_index >= 0) s->taken_count += 1;
     return SC_OK;

@@ -344,6 +344,60 @@ __global__ void residual_partial_kernel(int64_t n, int64_t k, const int64_t* __r
     }
 }
 
+// The same partials with every column of a row in one pass (k <= 32 KC):
+// lane c accumulates columns c, c + 32, ..., so A is read once and each
+// neighbour's V row (k doubles) is read whole.  Per-column arithmetic and
+// order are those of residual_partial_kernel.
+template <int KC>
+__global__ void __launch_bounds__(256) residual_rows_kernel(int64_t n, int64_t k, const int64_t* __restrict__ row_ptr,
+                                                            const int32_t* __restrict__ col,
+                                                            const double* __restrict__ vals,
+                                                            const double* __restrict__ V,
+                                                            const double* __restrict__ theta,
+                                                            double* __restrict__ part) {
+    __shared__ double red[8][32 * KC];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t r0 = (int64_t)blockIdx.x * RS_ROWS;
+    double acc2[KC];
+#pragma unroll
+    for (int q = 0; q < KC; ++q) acc2[q] = 0.0;
+    for (int64_t r = r0 + warp; r < imin64(n, r0 + RS_ROWS); r += 8) {
+        double a[KC];
+#pragma unroll
+        for (int q = 0; q < KC; ++q) a[q] = 0.0;
+        const int64_t pe = row_ptr[r + 1];
+        for (int64_t p = row_ptr[r]; p < pe; ++p) {
+            const double v = vals[p];
+            const double* vr = V + (int64_t)col[p] * k;
+#pragma unroll
+            for (int q = 0; q < KC; ++q)
+                if (lane + 32 * q < k) a[q] = fma(v, vr[lane + 32 * q], a[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < KC; ++q) {
+            const int64_t c = lane + 32 * q;
+            if (c < k) {
+                const double res = a[q] - theta[c] * V[r * k + c];
+                acc2[q] = fma(res, res, acc2[q]);
+            }
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < KC; ++q) red[warp][lane + 32 * q] = acc2[q];
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int q = 0; q < KC; ++q) {
+            const int64_t c = lane + 32 * q;
+            if (c < k) {
+                double t = 0.0;
+                for (int w = 0; w < 8; ++w) t += red[w][lane + 32 * q];
+                part[blockIdx.x * k + c] = t;
+            }
+        }
+    }
+}
+
 // max |v| as ordered bits of a non-negative double
 __global__ void absmax_kernel(int64_t m, const double* __restrict__ v, unsigned long long* __restrict__ out) {
     double a = 0.0;
@@ -673,7 +727,14 @@ static int residuals_launch(int64_t n, int64_t k, const int64_t* row_ptr, const 
     DevBuf<double> p, nr;
     int rc;
     if ((rc = p.alloc((size_t)nb * k)) || (rc = nr.alloc(k))) return rc;
-    residual_partial_kernel<<<(unsigned)nb, 256, 0, st>>>(n, k, row_ptr, col, vals, V, theta_dev, p.p);
+    if (k <= 32)
+        residual_rows_kernel<1><<<(unsigned)nb, 256, 0, st>>>(n, k, row_ptr, col, vals, V, theta_dev, p.p);
+    else if (k <= 64)
+        residual_rows_kernel<2><<<(unsigned)nb, 256, 0, st>>>(n, k, row_ptr, col, vals, V, theta_dev, p.p);
+    else if (k <= 128)
+        residual_rows_kernel<4><<<(unsigned)nb, 256, 0, st>>>(n, k, row_ptr, col, vals, V, theta_dev, p.p);
+    else
+        residual_partial_kernel<<<(unsigned)nb, 256, 0, st>>>(n, k, row_ptr, col, vals, V, theta_dev, p.p);
     colnorm_finish_kernel<<<(unsigned)ceil_div(k, 128), 128, 0, st>>>(nb, k, p.p, nr.p);
     SC_LAUNCHED(2);
     SC_CUDA(cudaMemcpyAsync(res_host, nr.p, sizeof(double) * k, cudaMemcpyDeviceToHost, st));

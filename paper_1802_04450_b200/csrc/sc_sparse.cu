@@ -623,14 +623,18 @@ __global__ void perm_row_len_kernel(int64_t n, const int64_t* __restrict__ row_p
 
 // warp per output row: rows of <= 64 entries are sorted by their new column
 // with a register bitonic network (2 keys per lane, key = new column << 32 |
-// source slot, all keys distinct); longer rows rank every entry by counting
+// source slot, all keys distinct), rows of <= PERM_SMEM by a bitonic sort in
+// shared memory; longer rows are listed for perm_long_kernel
 __device__ __forceinline__ int64_t cas64(int64_t v, int64_t o, bool keep_min) {
     return keep_min ? (v < o ? v : o) : (v > o ? v : o);
 }
-__global__ void perm_row_fill_kernel(int64_t n, const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+constexpr int PERM_SMEM = 512;  // rows up to this length sort in shared memory (8 warps x 4 KB)
+__global__ void __launch_bounds__(256) perm_row_fill_kernel(int64_t n, const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
                                      const double* __restrict__ vals, const int32_t* __restrict__ perm,
                                      const int32_t* __restrict__ pos, const int64_t* __restrict__ out_ptr,
-                                     int32_t* __restrict__ out_col, double* __restrict__ out_vals) {
+                                     int32_t* __restrict__ out_col, double* __restrict__ out_vals,
+                                     int64_t* __restrict__ long_rows, unsigned int* __restrict__ nlong) {
+    __shared__ int64_t perm_keys[8][PERM_SMEM];
     const int64_t p = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
     if (p >= n) return;
@@ -667,12 +671,91 @@ __global__ void perm_row_fill_kernel(int64_t n, const int64_t* __restrict__ row_
         }
         return;
     }
-    for (int64_t e = lane; e < len; e += 32) {
-        const int32_t key = pos[col[b + e]];
-        int64_t r = 0;
-        for (int64_t f = 0; f < len; ++f) r += pos[col[b + f]] < key;
-        out_col[o + r] = key;
-        out_vals[o + r] = vals[b + e];
+    if (len <= PERM_SMEM) {
+        // shared-memory bitonic sort of the keys, padded to a power of two
+        int64_t* K = perm_keys[threadIdx.x / 32];
+        int np2 = 128;
+        while (np2 < len) np2 <<= 1;
+        for (int e = lane; e < np2; e += 32) K[e] = e < len ? ((int64_t)pos[col[b + e]] << 32) | e : INT64_MAX;
+        __syncwarp();
+        for (int k = 2; k <= np2; k <<= 1)
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int q = lane; q < np2; q += 32) {
+                    const int pq = q ^ j;
+                    if (pq > q) {
+                        const int64_t a = K[q], c = K[pq];
+                        if ((a > c) == ((q & k) == 0)) {
+                            K[q] = c;
+                            K[pq] = a;
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+        for (int e = lane; e < len; e += 32) {
+            const int64_t v = K[e];
+            out_col[o + e] = (int32_t)(v >> 32);
+            out_vals[o + e] = vals[b + (int32_t)(v & 0xffffffff)];
+        }
+        return;
+    }
+    if (lane == 0) long_rows[atomicAdd(nlong, 1u)] = p;  // perm_long_kernel
+}
+
+// rows longer than PERM_SMEM (hubs), a block per row: bitonic sort of up to
+// PERM_LONG keys in (dynamic) shared memory, counting beyond
+constexpr int PERM_LONG = 8192;
+__global__ void __launch_bounds__(512) perm_long_kernel(const int64_t* __restrict__ row_ptr,
+                                                        const int32_t* __restrict__ col,
+                                                        const double* __restrict__ vals,
+                                                        const int32_t* __restrict__ perm,
+                                                        const int32_t* __restrict__ pos,
+                                                        const int64_t* __restrict__ out_ptr,
+                                                        int32_t* __restrict__ out_col, double* __restrict__ out_vals,
+                                                        const int64_t* __restrict__ long_rows,
+                                                        const unsigned int* __restrict__ nlong) {
+    extern __shared__ int64_t K[];
+    const int tid = threadIdx.x;
+    const unsigned nrows = *nlong;
+    for (unsigned f = blockIdx.x; f < nrows; f += gridDim.x) {
+        const int64_t p = long_rows[f];
+        const int64_t i = perm[p];
+        const int64_t b = row_ptr[i], len = row_ptr[i + 1] - b, o = out_ptr[p];
+        __syncthreads();
+        if (len <= PERM_LONG) {
+            int np2 = 1;
+            while (np2 < len) np2 <<= 1;
+            for (int e = tid; e < np2; e += blockDim.x)
+                K[e] = e < len ? ((int64_t)pos[col[b + e]] << 32) | e : INT64_MAX;
+            __syncthreads();
+            for (int k = 2; k <= np2; k <<= 1)
+                for (int j = k >> 1; j > 0; j >>= 1) {
+                    for (int q = tid; q < np2; q += blockDim.x) {
+                        const int pq = q ^ j;
+                        if (pq > q) {
+                            const int64_t a = K[q], c = K[pq];
+                            if ((a > c) == ((q & k) == 0)) {
+                                K[q] = c;
+                                K[pq] = a;
+                            }
+                        }
+                    }
+                    __syncthreads();
+                }
+            for (int e = tid; e < len; e += blockDim.x) {
+                const int64_t v = K[e];
+                out_col[o + e] = (int32_t)(v >> 32);
+                out_vals[o + e] = vals[b + (int32_t)(v & 0xffffffff)];
+            }
+        } else {
+            for (int64_t e = tid; e < len; e += blockDim.x) {
+                const int32_t key = pos[col[b + e]];
+                int64_t r = 0;
+                for (int64_t q = 0; q < len; ++q) r += pos[col[b + q]] < key;
+                out_col[o + r] = key;
+                out_vals[o + r] = vals[b + e];
+            }
+        }
     }
 }
 }  // namespace sc
@@ -690,9 +773,17 @@ extern "C" int sc_csr_permute_f64(int64_t n, const int64_t* row_ptr, const int32
     perm_row_len_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, row_ptr, perm, len.p);
     SC_LAUNCHED(1);
     if ((rc = exclusive_scan_i64(n, len.p, out_row_ptr, tmp.p, st))) return rc;
+    DevBuf<int64_t> long_rows;
+    DevBuf<unsigned int> nlong;
+    if ((rc = long_rows.alloc(n)) || (rc = nlong.alloc(1))) return rc;
+    SC_CUDA(cudaMemsetAsync(nlong.p, 0, sizeof(unsigned int), st));
     perm_row_fill_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, st>>>(n, row_ptr, col, vals, perm, pos, out_row_ptr,
-                                                                   out_col, out_vals);
-    SC_LAUNCHED(1);
+                                                                   out_col, out_vals, long_rows.p, nlong.p);
+    constexpr int long_smem = PERM_LONG * (int)sizeof(int64_t);
+    SC_CUDA(cudaFuncSetAttribute(perm_long_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, long_smem));
+    perm_long_kernel<<<(unsigned)(2 * kNumSMs), 512, long_smem, st>>>(row_ptr, col, vals, perm, pos, out_row_ptr,
+                                                                       out_col, out_vals, long_rows.p, nlong.p);
+    SC_LAUNCHED(2);
     return SC_OK;
 }
 

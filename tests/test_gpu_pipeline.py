@@ -147,6 +147,41 @@ def test_csr_permute_and_gather_rows():
     assert np.array_equal(g.cpu().numpy(), v.cpu().numpy()[pos.cpu().numpy()])
 
 
+def test_csr_permute_hub_rows():
+    """Rows past the warp kernel's shared-memory sort (> 512 entries) go to
+    the block kernel: sorted in shared memory up to 8192 entries, counted
+    beyond."""
+    import scipy.sparse as sps
+    import torch
+
+    from paper_1802_04450_b200.pipeline import permute_device
+
+    rng = np.random.default_rng(11)
+    n = 12000
+    r = rng.integers(0, n, 60000)
+    c = rng.integers(0, n, 60000)
+    hubs = {0: 9500, 1: 3000, 2: 600, 3: 513}  # row -> number of extra neighbours
+    for h, cnt in hubs.items():
+        nb = rng.choice(n, cnt, replace=False)
+        r = np.concatenate([r, np.full(cnt, h)])
+        c = np.concatenate([c, nb])
+    a = sps.coo_matrix((rng.standard_normal(len(r)), (r, c)), shape=(n, n)).tocsr()
+    a = (a + a.T).tocsr()
+    a.sum_duplicates()
+    a.sort_indices()
+    lens = np.diff(a.indptr)
+    assert lens.max() > 8192 and np.any((lens > 512) & (lens <= 8192))
+    m = sc.CsrMatrix(n, n, a.indptr.astype(np.int64), a.indices.astype(np.int32), a.data).device()
+    perm = rng.permutation(n).astype(np.int32)
+    ap, _ = permute_device(m, torch.from_numpy(perm).cuda())
+    got = ap.to_host()
+    want = a[perm][:, perm].tocsr()
+    want.sort_indices()
+    assert np.array_equal(got.row_ptr, want.indptr)
+    assert np.array_equal(got.col_idx, want.indices)
+    assert np.array_equal(got.vals, want.data)
+
+
 @pytest.mark.parametrize("flag", ["0", "1"])
 def test_pipeline_locality_order_eigen(golden, monkeypatch, flag):
     """Eigen stage on P A P^T (kNN locality order) gives the reference's
