@@ -203,16 +203,17 @@ __device__ __forceinline__ double np_sqnorm(const double* __restrict__ a, int64_
 }
 
 // Warp-cooperative dot(a_t, b_t) in the einsum order for one row pair per
-// lane (nullptr: none).  Each row is read with coalesced warp loads into a
-// shared-memory tile, 32 columns at a time, and every lane then folds its own
-// pair from the tiles -- a lane-per-row loop would cost one L1 wavefront per
-// lane per element.  stage: kPairStage doubles per warp.  Bit-identical to
-// np_dot_span over __dmul_rn(a[l], b[l]).
-constexpr int kPairLd = 33;
+// lane (nullptr: none).  Each row is read with coalesced warp loads (two rows
+// of 16 columns per load) into a shared-memory tile, 16 columns at a time,
+// and every lane then folds its own pair from the tiles -- a lane-per-row
+// loop would cost one L1 wavefront per lane per element.  stage: kPairStage
+// doubles per warp.  Bit-identical to np_dot_span over __dmul_rn(a[l], b[l]).
+constexpr int kPairW = 16;
+constexpr int kPairLd = kPairW + 1;
 constexpr int kPairStage = 2 * 32 * kPairLd + 64;
 __device__ __forceinline__ double warp_pair_dot_np(const double* a, const double* b, int64_t d,
                                                    double* __restrict__ stage) {
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, half = lane >> 4, cl = lane & 15;
     double* sa = stage;
     double* sb = stage + 32 * kPairLd;
     const double** pa = reinterpret_cast<const double**>(stage + 2 * 32 * kPairLd);
@@ -221,24 +222,26 @@ __device__ __forceinline__ double warp_pair_dot_np(const double* a, const double
     pa[lane] = a;
     pb[lane] = b;
     NpDot acc;
-    for (int64_t c0 = 0; c0 < d; c0 += 32) {
-        const int w = (int)(d - c0 < 32 ? d - c0 : 32);
+    for (int64_t c0 = 0; c0 < d; c0 += kPairW) {
+        const int w = (int)(d - c0 < kPairW ? d - c0 : kPairW);
         __syncwarp();
 #pragma unroll
-        for (int r0 = 0; r0 < 32; r0 += 8) {
+        for (int r0 = 0; r0 < 32; r0 += 16) {
             double va[8], vb[8];
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-                const double* ra = pa[r0 + q];
-                const double* rb = pb[r0 + q];
-                const bool ok = ra && lane < w;
-                va[q] = ok ? __ldg(ra + c0 + lane) : 0.0;
-                vb[q] = ok ? __ldg(rb + c0 + lane) : 0.0;
+                const int r = r0 + 2 * q + half;
+                const double* ra = pa[r];
+                const double* rb = pb[r];
+                const bool ok = ra && cl < w;
+                va[q] = ok ? __ldg(ra + c0 + cl) : 0.0;
+                vb[q] = ok ? __ldg(rb + c0 + cl) : 0.0;
             }
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-                sa[(r0 + q) * kPairLd + lane] = va[q];
-                sb[(r0 + q) * kPairLd + lane] = vb[q];
+                const int r = r0 + 2 * q + half;
+                sa[r * kPairLd + cl] = va[q];
+                sb[r * kPairLd + cl] = vb[q];
             }
         }
         __syncwarp();

@@ -1174,9 +1174,9 @@ struct AssignTc {
             SC_LAUNCHED(1);
             return SC_OK;
         }
-        constexpr int fin_smem = 4 * kPairStage * (int)sizeof(double);
+        constexpr int fin_smem = 8 * kPairStage * (int)sizeof(double);
         SC_CUDA(cudaFuncSetAttribute(as_finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fin_smem));
-        as_finalize_kernel<<<(unsigned)ceil_div(n, 128), 128, fin_smem, st>>>(n, d, dp, s, v, vn, c, cn, scal.p + 1,
+        as_finalize_kernel<<<(unsigned)ceil_div(n, 256), 256, fin_smem, st>>>(n, d, dp, s, v, vn, c, cn, scal.p + 1,
                                                                              bidx.p, bkeys.p, old_labels, labels,
                                                                              cost, flagged.p, scal.p, changes);
         SC_LAUNCHED(1);
