@@ -150,8 +150,10 @@ __global__ void __launch_bounds__(256) symeig_ql_kernel(int m, int rb, const dou
         __syncthreads();  // everyone has read s_zero before thread 0 resets it
         if (zero) continue;  // uniform
         // warp-cooperative per row: 8 lanes per row, rows strided over the CTA
+        // (the loop bound is CTA-uniform so every lane reaches the shuffles)
         const int g = tid >> 3, sub = tid & 7, ng = nt >> 3;
-        for (int rr = g; rr < rb; rr += ng) {
+        for (int rbase = 0; rbase < rb; rbase += ng) {
+            const int rr = rbase + g;
             double dot = 0.0;
             if (rr < rows)
                 for (int i = sub; i < len; i += 8) dot = fma(zb[(size_t)(k + 1 + i) * rb + rr], v[i], dot);

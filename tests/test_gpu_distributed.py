@@ -51,7 +51,7 @@ def test_div_and_normal_shard_independent(ops):
     assert np.array_equal(ops.host(dst), np.arange(10.0) / 4.0)
 
 
-@pytest.mark.parametrize("m,k", [(2, 1), (9, 3), (40, 10), (200, 100)])
+@pytest.mark.parametrize("m,k", [(2, 1), (9, 3), (40, 10), (200, 100), (1000, 20), (2000, 40)])
 def test_symeig_block(ops, m, k):
     rng = np.random.default_rng(m)
     T = rng.standard_normal((m, m))

@@ -10,6 +10,6 @@ timeout 600 ncu --set full --import-source on --clock-control none -k regex:gemv
   -o gpurun_out/ncu_gemv_n python tools/prof_lanczos.py > /dev/null 2>&1
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:spmv_local -s 5 -c 1 \
   -o gpurun_out/ncu_spmv python tools/prof_spmv.py perm > /dev/null 2>&1
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:assign_tc -s 3 -c 1 \
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:"assign_tc_kernel<2" -s 3 -c 1 \
   -o gpurun_out/ncu_assign python tools/prof_lanczos.py > /dev/null 2>&1
 ls -la gpurun_out
