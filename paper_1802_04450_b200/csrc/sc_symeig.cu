@@ -13,6 +13,8 @@
 //
 // Replaces np.linalg.eigh(proj) + argsort(-theta, kind="stable") in
 // eigen.py:189-192 (the reference's LAPACK dsyevd call on the host).
+#include <algorithm>
+
 #include "sc_common.cuh"
 #include "sc_symeig.cuh"
 
@@ -108,18 +110,30 @@ __global__ void __launch_bounds__(SE_THREADS, 1) symeig_tridiag_kernel(int m, do
     if (m >= 2 && tid == 0) a[(size_t)(m - 1) * m + (m - 2)] = a[(size_t)(m - 2) * m + (m - 1)];
 }
 
+// named CTA barriers (non-.aligned forms, after a warp reconvergence)
+__device__ __forceinline__ void named_sync(int id, int n) {
+    __syncwarp();
+    asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int n) {
+    __syncwarp();
+    asm volatile("barrier.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
 // CTA b: rows [b*rb, b*rb + rb) of the eigenvector matrix Z = Q * (QL rotations)
 __global__ void __launch_bounds__(256) symeig_ql_kernel(int m, int rb, const double* __restrict__ a,
                                                         double* __restrict__ z, double* __restrict__ w,
-                                                        int* __restrict__ info) {
+                                                        int* __restrict__ info, double* __restrict__ zglob) {
     extern __shared__ double sm[];
-    double* zb = sm;                       // m x rb: zb[i * rb + rr] = Z[r0 + rr][i]
-    double* d = zb + (size_t)m * rb;       // m
+    // the CTA's rows of Z: shared memory, or (large m, one wave) a private
+    // global block that stays L2-resident
+    double* zb = zglob ? zglob + (size_t)blockIdx.x * m * rb : sm;  // zb[i * rb + rr] = Z[r0 + rr][i]
+    double* d = zglob ? sm : zb + (size_t)m * rb;                   // m
     double* e = d + m;                     // m
-    double* cs = e + m;                    // m
-    double* sn = cs + m;                   // m
-    double* v = sn + m;                    // m
-    __shared__ int s_lo, s_hi, s_state, s_zero;
+    double* v = e + m;                     // m
+    double* cs2 = v + m;                   // 2 x m (double-buffered rotation chains)
+    double* sn2 = cs2 + 2 * (size_t)m;     // 2 x m
+    __shared__ int s_lo2[2], s_hi2[2], s_zero;
     const int tid = threadIdx.x, nt = blockDim.x;
     const int r0 = blockIdx.x * rb;
     const int rows = min(rb, m - r0);
@@ -166,21 +180,42 @@ __global__ void __launch_bounds__(256) symeig_ql_kernel(int m, int rb, const dou
         __syncthreads();
     }
 
-    // ---- implicit QL on (d, e): thread 0 forms each rotation chain, the rows apply it
-    if (tid == 0) {
-        s_state = 0;
-        if (blockIdx.x == 0) *info = 0;
-    }
+    // ---- implicit QL on (d, e), pipelined: warp 0 forms the rotation chains
+    // (lane 0 the serial chain, the whole warp the search for the next
+    // negligible off-diagonal) into a double buffer while warps 1..7 apply
+    // the previous chain to the CTA's rows; named barriers FULL[b] / EMPTY[b]
+    // hand the buffers over.  Same rotations in the same order as a serial
+    // compute-then-apply loop.
+    if (tid == 0 && blockIdx.x == 0) *info = 0;
     __syncthreads();
-    int l = 0, iter = 0;  // only meaningful in thread 0
-    while (true) {
-        if (tid == 0) {
-            s_lo = s_hi = -1;
+    const int warp = tid >> 5, lane = tid & 31;
+    constexpr int BAR_FULL = 1, BAR_EMPTY = 3;  // ids 1,2 and 3,4
+    if (warp == 0) {
+        int l = 0, iter = 0, c = 0;
+        bool pending[2] = {false, false};  // a handed-over chain whose EMPTY is not yet awaited
+        while (true) {
+            const int buf = c & 1;
+            if (pending[buf]) {
+                named_sync(BAR_EMPTY + buf, nt);
+                pending[buf] = false;
+            }
+            double* csb = cs2 + (size_t)buf * m;
+            double* snb = sn2 + (size_t)buf * m;
+            int lo = -1, hi = -1;
             while (l < m) {
-                int mm;
-                for (mm = l; mm < m - 1; ++mm) {
-                    double dd = fabs(d[mm]) + fabs(d[mm + 1]);
-                    if (fabs(e[mm]) + dd == dd) break;
+                int mm = m - 1;
+                for (int base = l; base < m - 1; base += 32) {
+                    const int idx = base + lane;
+                    bool neg = false;
+                    if (idx < m - 1) {
+                        const double dd = fabs(d[idx]) + fabs(d[idx + 1]);
+                        neg = fabs(e[idx]) + dd == dd;
+                    }
+                    const unsigned bal = __ballot_sync(0xffffffffu, neg);
+                    if (bal) {
+                        mm = base + __ffs(bal) - 1;
+                        break;
+                    }
                 }
                 if (mm == l) {
                     ++l;
@@ -188,81 +223,100 @@ __global__ void __launch_bounds__(256) symeig_ql_kernel(int m, int rb, const dou
                     continue;
                 }
                 if (++iter > 60) {
-                    if (blockIdx.x == 0) *info = l + 1;
+                    if (lane == 0 && blockIdx.x == 0) *info = l + 1;
                     l = m;
                     break;
                 }
-                double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
-                double r = hypot(g, 1.0);
-                g = d[mm] - d[l] + e[l] / (g + (g >= 0.0 ? fabs(r) : -fabs(r)));
-                double s = 1.0, c = 1.0, p = 0.0;
-                int i;
-                bool early = false;
                 int cnt = 0;
-                // The chain is serial, so its latency is the QL cost: d[i],
-                // e[i] are prefetched into registers one rotation ahead (in
-                // program order a shared-memory load would otherwise wait
-                // behind the previous rotation's stores), and one rsqrt
-                // (1 ulp) replaces sqrt + reciprocal; c, s stay orthonormal
-                // to ~1 ulp.  |f|, |g| are O(|T|): no hypot rescaling.
-                double ei = e[mm - 1], di = d[mm - 1], di1 = d[mm];
-                for (i = mm - 1; i >= l; --i) {
-                    const double e_nx = i > l ? e[i - 1] : 0.0;
-                    const double d_nx = i > l ? d[i - 1] : 0.0;
-                    const double f = s * ei, b = c * ei;
-                    const double r2 = fma(f, f, g * g);
-                    if (r2 == 0.0) {
-                        e[i + 1] = 0.0;
-                        d[i + 1] = di1 - p;
-                        e[mm] = 0.0;
-                        early = true;
-                        break;
+                if (lane == 0) {
+                    double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
+                    double r = hypot(g, 1.0);
+                    g = d[mm] - d[l] + e[l] / (g + (g >= 0.0 ? fabs(r) : -fabs(r)));
+                    double s = 1.0, c2 = 1.0, p = 0.0;
+                    int i;
+                    bool early = false;
+                    // The chain is serial, so its latency is the QL cost: d[i],
+                    // e[i] are prefetched into registers one rotation ahead, and
+                    // one rsqrt (1 ulp) replaces sqrt + reciprocal; c, s stay
+                    // orthonormal to ~1 ulp.  |f|, |g| are O(|T|): no rescaling.
+                    double ei = e[mm - 1], di = d[mm - 1], di1 = d[mm];
+                    for (i = mm - 1; i >= l; --i) {
+                        const double e_nx = i > l ? e[i - 1] : 0.0;
+                        const double d_nx = i > l ? d[i - 1] : 0.0;
+                        const double f = s * ei, b = c2 * ei;
+                        const double r2 = fma(f, f, g * g);
+                        if (r2 == 0.0) {
+                            e[i + 1] = 0.0;
+                            d[i + 1] = di1 - p;
+                            e[mm] = 0.0;
+                            early = true;
+                            break;
+                        }
+                        const double ri = rsqrt(r2);
+                        e[i + 1] = r2 * ri;
+                        s = f * ri;
+                        c2 = g * ri;
+                        g = di1 - p;
+                        r = (di - g) * s + 2.0 * c2 * b;
+                        p = s * r;
+                        d[i + 1] = g + p;
+                        g = c2 * r - b;
+                        csb[cnt] = c2;
+                        snb[cnt] = s;
+                        ++cnt;
+                        di1 = di;  // d[i] is untouched by this rotation
+                        di = d_nx;
+                        ei = e_nx;
                     }
-                    const double ri = rsqrt(r2);
-                    e[i + 1] = r2 * ri;
-                    s = f * ri;
-                    c = g * ri;
-                    g = di1 - p;
-                    r = (di - g) * s + 2.0 * c * b;
-                    p = s * r;
-                    d[i + 1] = g + p;
-                    g = c * r - b;
-                    cs[cnt] = c;
-                    sn[cnt] = s;
-                    ++cnt;
-                    di1 = di;  // d[i] is untouched by this rotation
-                    di = d_nx;
-                    ei = e_nx;
+                    if (!(early && i >= l)) {
+                        d[l] -= p;
+                        e[l] = g;
+                        e[mm] = 0.0;
+                    }
                 }
-                if (!(early && i >= l)) {
-                    d[l] -= p;
-                    e[l] = g;
-                    e[mm] = 0.0;
-                }
+                cnt = __shfl_sync(0xffffffffu, cnt, 0);
+                __syncwarp();  // lane 0's d / e updates before the next search
                 if (cnt > 0) {
-                    s_hi = mm - 1;    // first rotation acts on (mm-1, mm)
-                    s_lo = mm - cnt;  // last rotation acts on (mm-cnt, mm-cnt+1)
-                    break;            // hand the chain to the rows
+                    hi = mm - 1;    // first rotation acts on (mm-1, mm)
+                    lo = mm - cnt;  // last rotation acts on (mm-cnt, mm-cnt+1)
+                    break;
                 }
             }
-            if (l >= m && s_hi < 0) s_state = 1;
-        }
-        __syncthreads();
-        if (s_state) break;
-        const int hi = s_hi, lo = s_lo;
-        for (int rr = tid; rr < rows; rr += nt) {
-            double carry = zb[(size_t)(hi + 1) * rb + rr];
-            int t = 0;
-            for (int i = hi; i >= lo; --i, ++t) {
-                const double c = cs[t], s = sn[t];
-                const double zi = zb[(size_t)i * rb + rr];
-                zb[(size_t)(i + 1) * rb + rr] = s * zi + c * carry;
-                carry = c * zi - s * carry;
+            if (lane == 0) {
+                s_lo2[buf] = lo;
+                s_hi2[buf] = hi;
             }
-            zb[(size_t)lo * rb + rr] = carry;
+            named_arrive(BAR_FULL + buf, nt);
+            if (lo < 0) {  // finished: settle the other buffer's hand-over
+                if (pending[buf ^ 1]) named_sync(BAR_EMPTY + (buf ^ 1), nt);
+                break;
+            }
+            pending[buf] = true;
+            ++c;
         }
-        __syncthreads();
+    } else {
+        for (int c = 0;; ++c) {
+            const int buf = c & 1;
+            named_sync(BAR_FULL + buf, nt);
+            const int hi = s_hi2[buf], lo = s_lo2[buf];
+            if (lo < 0) break;
+            const double* csb = cs2 + (size_t)buf * m;
+            const double* snb = sn2 + (size_t)buf * m;
+            for (int rr = tid - 32; rr < rows; rr += nt - 32) {
+                double carry = zb[(size_t)(hi + 1) * rb + rr];
+                int t = 0;
+                for (int i = hi; i >= lo; --i, ++t) {
+                    const double c2 = csb[t], s = snb[t];
+                    const double zi = zb[(size_t)i * rb + rr];
+                    zb[(size_t)(i + 1) * rb + rr] = s * zi + c2 * carry;
+                    carry = c2 * zi - s * carry;
+                }
+                zb[(size_t)lo * rb + rr] = carry;
+            }
+            named_arrive(BAR_EMPTY + buf, nt);
+        }
     }
+    __syncthreads();
     for (int idx = tid; idx < m * rows; idx += nt) {
         const int i = idx / rows, rr = idx - i * rows;
         z[(size_t)i * m + r0 + rr] = zb[(size_t)i * rb + rr];
@@ -305,16 +359,24 @@ int symeig_launch(int m, int kout, double* a, double* z, double* w_raw, double* 
         cudaFuncSetAttribute(symeig_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SE_SMEM_MAX);
         attr_set = true;
     }
-    // rows per CTA: as many as fit (at most 64) next to the 5 m-vectors
+    // rows per CTA: as many as fit (at most 64) next to the 7 m-vectors
     int rb = 64;
-    while (rb > 1 && sizeof(double) * ((size_t)m * rb + 5 * (size_t)m) > (size_t)SE_SMEM_MAX) rb >>= 1;
-    const size_t ql_smem = sizeof(double) * ((size_t)m * rb + 5 * (size_t)m);
+    while (rb > 1 && sizeof(double) * ((size_t)m * rb + 7 * (size_t)m) > (size_t)SE_SMEM_MAX) rb >>= 1;
+    // every CTA recomputes the same rotation chains: when the shared-memory
+    // row blocks need more CTAs than one wave, the rows go to global blocks
+    // (L2-resident) with one CTA per SM instead
+    const bool global_z = (m + rb - 1) / rb > kNumSMs;
+    if (global_z) rb = (m + kNumSMs - 1) / kNumSMs;
+    const size_t ql_smem = sizeof(double) * ((global_z ? 0 : (size_t)m * rb) + 7 * (size_t)m);
     if (ql_smem > (size_t)SE_SMEM_MAX) return fail(SC_ERR_VALUE, "projected matrix too large for the device eigensolver");
     const int nblk = (m + rb - 1) / rb;
+    DevBuf<double> zglob;
+    if (global_z)
+        if (int rc = zglob.alloc((size_t)nblk * m * rb)) return rc;
     {
         ProfScope prof("symeig", st, 0.0);
         symeig_tridiag_kernel<<<1, SE_THREADS, sizeof(double) * (2 * (size_t)m + 40), st>>>(m, a);
-        symeig_ql_kernel<<<nblk, 256, ql_smem, st>>>(m, rb, a, z, w_raw, info);
+        symeig_ql_kernel<<<nblk, 256, ql_smem, st>>>(m, rb, a, z, w_raw, info, zglob.p);
         symeig_sort_kernel<<<1, 1024, sizeof(int) * (size_t)m, st>>>(m, kout, w_raw, z, w_sorted, z_sorted);
     }
     SC_LAUNCHED(3);
