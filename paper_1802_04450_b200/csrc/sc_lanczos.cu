@@ -181,6 +181,46 @@ __global__ void scale_copy_kernel(int64_t n, const double* __restrict__ src, con
     if (i < n) dst[i] = src[i] / scal[idx];
 }
 
+// One launch for the end of a Lanczos step's first CGS pass: scal[0] = |w|
+// (sqp partials), scal[3] = |w0| (sq0 partials), T[j,j] = scal[2] = alpha =
+// h[j] -- the arithmetic of finish_norm_kernel x 2 + commit_alpha_kernel.
+__global__ void __launch_bounds__(1024) step_norms_kernel(int64_t nb_n, const double* __restrict__ sqp, int64_t nb_t,
+                                                          const double* __restrict__ sq0, int64_t m, int64_t j,
+                                                          const double* __restrict__ h, double* __restrict__ T,
+                                                          double* __restrict__ scal) {
+    __shared__ double red[1024];
+    for (int pass = 0; pass < 2; ++pass) {
+        const double* part = pass ? sq0 : sqp;
+        const int64_t nb = pass ? nb_t : nb_n;
+        double a = 0.0;
+        for (int64_t b = threadIdx.x; b < nb; b += blockDim.x) a += part[b];
+        red[threadIdx.x] = a;
+        __syncthreads();
+        for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+            if ((int)threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) scal[pass ? 3 : 0] = sqrt(red[0]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        T[j * m + j] = h[j];
+        scal[2] = h[j];
+    }
+}
+
+// next = w / scal[0] and T[j,j+1] = T[j+1,j] = beta in one launch
+__global__ void scale_copy_couple_kernel(int64_t n, const double* __restrict__ src, const double* __restrict__ scal,
+                                         double* __restrict__ dst, int64_t m, int64_t j, double* __restrict__ T) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = src[i] / scal[0];
+    if (i == 0) {
+        const double b = scal[0];
+        T[j * m + j + 1] = b;
+        T[(j + 1) * m + j] = b;
+    }
+}
+
 // T[j,j] = alpha (= h[j] after the first projection), scal[2] = alpha
 __global__ void commit_alpha_kernel(int64_t m, int64_t j, const double* __restrict__ h,
                                     double* __restrict__ T, double* __restrict__ scal) {
@@ -588,12 +628,9 @@ struct sc_lanczos {
             // result is orthogonal to working precision after one pass.
             ProfScope prof("reorth", st, 2.0 * (double)n * cnt * 8.0);
             if ((rc = project(w.p, cnt, sq0.p))) return rc;
-            commit_alpha_kernel<<<1, 32, 0, st>>>(m, j, h.p, T.p, scal.p);
-            SC_LAUNCHED(1);
             if ((rc = subtract(w.p, cnt, true))) return rc;
-            finish_norm_kernel<<<1, 1024, 0, st>>>(nb_n, sqp.p, scal.p, 0);
-            finish_norm_kernel<<<1, 1024, 0, st>>>(nb_t, sq0.p, scal.p, 3);
-            SC_LAUNCHED(2);
+            step_norms_kernel<<<1, 1024, 0, st>>>(nb_n, sqp.p, nb_t, sq0.p, m, j, h.p, T.p, scal.p);
+            SC_LAUNCHED(1);
             SC_CUDA(cudaMemcpyAsync(ab, scal.p, sizeof(double) * 4, cudaMemcpyDeviceToHost, st));
             SC_CUDA(cudaStreamSynchronize(st));
         }
@@ -611,9 +648,8 @@ struct sc_lanczos {
         if (j + 1 == m) return finish_sweep(beta);
         double* next = B.p + (j + 1) * ld;
         if (beta > kBreakdownRtol * std::max(1.0, scale)) {
-            set_coupling_kernel<<<1, 32, 0, st>>>(m, j, scal.p, T.p, 1);
-            scale_copy_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, w.p, scal.p, 0, next);
-            SC_LAUNCHED(2);
+            scale_copy_couple_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, w.p, scal.p, next, m, j, T.p);
+            SC_LAUNCHED(1);
         } else {
             set_coupling_kernel<<<1, 32, 0, st>>>(m, j, scal.p, T.p, 0);
             SC_LAUNCHED(1);
