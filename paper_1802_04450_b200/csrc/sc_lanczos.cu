@@ -71,11 +71,45 @@ __global__ void __launch_bounds__(256) gemv_t_partial_kernel(int64_t n, int64_t 
         s = warp_sum(s);
         if (lane == 0) sq_part[blockIdx.x] = s;
     }
-    for (int c = warp; c < ncols; c += 8) {
+    // two columns per warp pass (twice the loads in flight per warp, one
+    // shuffle tree per column as before); per-column arithmetic unchanged
+    int c = warp * 2;
+    for (; c + 1 < ncols; c += 16) {
+        const double* col = B + (int64_t)c * ld + r0;
+        const double* col2 = col + ld;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        double b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;
+        int t = lane;
+        for (; t + 96 < rows; t += 128) {
+            const double x0 = __ldg(col + t), x1 = __ldg(col + t + 32), x2 = __ldg(col + t + 64),
+                         x3 = __ldg(col + t + 96);
+            const double y0 = __ldg(col2 + t), y1 = __ldg(col2 + t + 32), y2 = __ldg(col2 + t + 64),
+                         y3 = __ldg(col2 + t + 96);
+            const double w0 = ws[t], w1 = ws[t + 32], w2 = ws[t + 64], w3 = ws[t + 96];
+            a0 = fma(x0, w0, a0);
+            a1 = fma(x1, w1, a1);
+            a2 = fma(x2, w2, a2);
+            a3 = fma(x3, w3, a3);
+            b0 = fma(y0, w0, b0);
+            b1 = fma(y1, w1, b1);
+            b2 = fma(y2, w2, b2);
+            b3 = fma(y3, w3, b3);
+        }
+        for (; t < rows; t += 32) {
+            a0 = fma(__ldg(col + t), ws[t], a0);
+            b0 = fma(__ldg(col2 + t), ws[t], b0);
+        }
+        const double acc = warp_sum((a0 + a1) + (a2 + a3));
+        const double acc2 = warp_sum((b0 + b1) + (b2 + b3));
+        if (lane == 0) {
+            part[blockIdx.x * (int64_t)ncols + c] = acc;
+            part[blockIdx.x * (int64_t)ncols + c + 1] = acc2;
+        }
+    }
+    if (c < ncols) {  // the odd last column
         const double* col = B + (int64_t)c * ld + r0;
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
         int t = lane;
-#pragma unroll 2
         for (; t + 96 < rows; t += 128) {
             a0 = fma(__ldg(col + t), ws[t], a0);
             a1 = fma(__ldg(col + t + 32), ws[t + 32], a1);
@@ -83,7 +117,7 @@ __global__ void __launch_bounds__(256) gemv_t_partial_kernel(int64_t n, int64_t 
             a3 = fma(__ldg(col + t + 96), ws[t + 96], a3);
         }
         for (; t < rows; t += 32) a0 = fma(__ldg(col + t), ws[t], a0);
-        double acc = warp_sum((a0 + a1) + (a2 + a3));
+        const double acc = warp_sum((a0 + a1) + (a2 + a3));
         if (lane == 0) part[blockIdx.x * (int64_t)ncols + c] = acc;
     }
 }
