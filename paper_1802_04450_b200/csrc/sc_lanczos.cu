@@ -149,7 +149,8 @@ __global__ void __launch_bounds__(GN_THREADS) gemv_n_update_kernel(int64_t n, in
         const double* p = B + r;
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
         int c = 0;
-        for (; c + 4 <= ncols; c += 4) {
+#pragma unroll 4
+        for (; c + 4 <= ncols; c += 4) {  // unrolled: 16 column loads in flight per row
             a0 = fma(__ldg(p + (int64_t)c * ld), hs[c], a0);
             a1 = fma(__ldg(p + (int64_t)(c + 1) * ld), hs[c + 1], a1);
             a2 = fma(__ldg(p + (int64_t)(c + 2) * ld), hs[c + 2], a2);
