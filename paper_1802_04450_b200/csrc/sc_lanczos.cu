@@ -80,6 +80,7 @@ __global__ void __launch_bounds__(256) gemv_t_partial_kernel(int64_t n, int64_t 
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
         double b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;
         int t = lane;
+#pragma unroll 2
         for (; t + 96 < rows; t += 128) {
             const double x0 = __ldg(col + t), x1 = __ldg(col + t + 32), x2 = __ldg(col + t + 64),
                          x3 = __ldg(col + t + 96);
@@ -149,8 +150,8 @@ __global__ void __launch_bounds__(GN_THREADS) gemv_n_update_kernel(int64_t n, in
         const double* p = B + r;
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
         int c = 0;
-#pragma unroll 4
-        for (; c + 4 <= ncols; c += 4) {  // unrolled: 16 column loads in flight per row
+#pragma unroll 8
+        for (; c + 4 <= ncols; c += 4) {  // unrolled: 32 column loads in flight per row
             a0 = fma(__ldg(p + (int64_t)c * ld), hs[c], a0);
             a1 = fma(__ldg(p + (int64_t)(c + 1) * ld), hs[c + 1], a1);
             a2 = fma(__ldg(p + (int64_t)(c + 2) * ld), hs[c + 2], a2);
