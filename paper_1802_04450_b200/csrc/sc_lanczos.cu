@@ -130,6 +130,7 @@ __global__ void reduce_cols_kernel(int64_t nb, int ncols, const double* __restri
     int lane = threadIdx.x & 31;
     if (c >= ncols) return;
     double acc = 0.0;
+#pragma unroll 8
     for (int64_t b = lane; b < nb; b += 32) acc += part[b * ncols + c];
     acc = warp_sum(acc);
     if (lane == 0) h[c] = acc;
