@@ -27,7 +27,7 @@
 
 namespace sc {
 
-constexpr int GT_ROWS = 1024;     // rows per gemv_t partial block
+constexpr int GT_ROWS = 2048;     // rows per gemv_t partial block (max)
 constexpr int GN_THREADS = 256;   // rows per gemv_n block
 constexpr double kBreakdownRtol = 1e-13;  // eigen.py:50
 // second CGS pass when the first one removed more than 1 - eta^2 of |w|^2
@@ -121,6 +121,17 @@ __global__ void __launch_bounds__(256) gemv_t_partial_kernel(int64_t n, int64_t 
         const double acc = warp_sum((a0 + a1) + (a2 + a3));
         if (lane == 0) part[blockIdx.x * (int64_t)ncols + c] = acc;
     }
+}
+
+// rows per gemv_t block: one balanced wave at the kernel's real occupancy,
+// 32-row granules
+static int gemv_t_rows_per_block(int64_t n) {
+    static int bps = 0;
+    if (!bps) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, gemv_t_partial_kernel, 256, 0);
+        if (bps < 1) bps = 1;
+    }
+    return (int)std::min<int64_t>(GT_ROWS, std::max<int64_t>(32, ceil_div(ceil_div(n, kNumSMs * bps), 32) * 32));
 }
 
 // h[c] = sum_b part[b * ncols + c] (fixed order), warp per column
@@ -609,8 +620,8 @@ struct sc_lanczos {
         seed = seed_;
         st = st_;
         ld = (n + 31) / 32 * 32;
-        // one balanced wave (kNumSMs x 8 blocks) while the rows fit, 32-row granules
-        rpb_t = (int)std::min<int64_t>(GT_ROWS, std::max<int64_t>(32, ceil_div(ceil_div(n, kNumSMs * 8), 32) * 32));
+        // one balanced wave at the kernel occupancy while the rows fit, 32-row granules
+        rpb_t = gemv_t_rows_per_block(n);
         nb_t = ceil_div(n, rpb_t);
         nb_n = ceil_div(n, GN_THREADS);
         int rc;
@@ -977,7 +988,7 @@ int sc_gemv_t_f64(int64_t n, int64_t ld, int64_t ncols, const double* B, const d
         SC_CUDA(cudaMemsetAsync(h, 0, sizeof(double) * ncols, st));
         return SC_OK;
     }
-    const int rpb = (int)std::min<int64_t>(GT_ROWS, std::max<int64_t>(32, ceil_div(ceil_div(n, kNumSMs * 8), 32) * 32));
+    const int rpb = gemv_t_rows_per_block(n);
     const int64_t nb = ceil_div(n, rpb);
     DevBuf<double> part;
     if (int rc = part.alloc((size_t)nb * ncols)) return rc;
