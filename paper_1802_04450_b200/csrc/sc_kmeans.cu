@@ -893,7 +893,28 @@ __global__ void ncut_parts_kernel(int64_t k, const double* __restrict__ deg, con
     int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= k) return;
     double b = 0.0, v = 0.0;
-    for (int64_t m = start[c]; m < start[c + 1]; ++m) {
+    const int64_t e = start[c + 1];
+    int64_t m = start[c];
+    // the gathers of 16 members are issued before the (sequential, point
+    // order) additions consume them
+    constexpr int B = 16;
+    for (; m + B <= e; m += B) {
+        int64_t idx[B];
+        double dv[B], cv[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) idx[u] = members[m + u];
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            dv[u] = deg[idx[u]];
+            cv[u] = cross[idx[u]];
+        }
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            v += dv[u];
+            b += cv[u];
+        }
+    }
+    for (; m < e; ++m) {
         const int64_t i = members[m];
         v += deg[i];
         b += cross[i];
