@@ -1037,6 +1037,61 @@ __global__ void as_finalize_kernel(int64_t n, int64_t d, int64_t dp, double s, c
     if ((threadIdx.x & 31) == 0 && bal) atomicAdd(changes, (unsigned long long)__popc(bal));
 }
 
+// as_finalize_kernel over the points' 8-column panels (to_panels_kernel):
+// thread per row, its 64-byte panel pieces read coalesced with the
+// neighbouring rows'; exact_s's products and order
+__global__ void as_finalize_panel_kernel(int64_t n, int64_t d, int64_t dp, double s, const double* __restrict__ v8,
+                                         const double* __restrict__ vn, const double* __restrict__ c,
+                                         const double* __restrict__ cn,
+                                         const unsigned long long* __restrict__ cnmax_bits,
+                                         const int32_t* __restrict__ best_idx, const float2* __restrict__ best_keys,
+                                         const int64_t* __restrict__ old_labels, int64_t* __restrict__ labels,
+                                         double* __restrict__ cost, int32_t* __restrict__ flagged,
+                                         unsigned long long* __restrict__ nflag,
+                                         unsigned long long* __restrict__ changes) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int chg = 0;
+    if (i < n) {
+        const double cnmax = __longlong_as_double((long long)*cnmax_bits);
+        const double cmax = sqrt(cnmax);
+        const double va = sqrt(vn[i]);
+        const double delta = 1.25 * (2.0 * (0x1p-10 + (double)(dp + 1) * 0x1p-24) * va * cmax +
+                                     0x1p-24 * (2.0 * cnmax + 2.0 * va * cmax) +
+                                     0x1p-24 * sqrt((double)dp) * (va + cmax) / s);
+        const float2 bk = best_keys[i];
+        const int32_t b = best_idx[i];
+        if (b >= 0 && (double)bk.y - (double)bk.x > 2.0 * delta) {
+            const double* cb = c + (int64_t)b * d;
+            NpDot acc;
+            for (int64_t c0 = 0; c0 < d; c0 += 8) {
+                const double2* src = reinterpret_cast<const double2*>(v8 + ((c0 >> 3) * n + i) * 8);
+                const double2 a0 = __ldg(src), a1 = __ldg(src + 1), a2 = __ldg(src + 2), a3 = __ldg(src + 3);
+                const double x[8] = {a0.x, a0.y, a1.x, a1.y, a2.x, a2.y, a3.x, a3.y};
+                auto f = [&](int q) { return __dmul_rn(x[q], __ldg(cb + c0 + q)); };
+                const int rem = (int)(d - c0 < 8 ? d - c0 : 8);
+                if (rem == 8) {
+                    acc.block(f(0), f(1), f(2), f(3), f(4), f(5), f(6), f(7));
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 8; q += 2)
+                        if (q + 2 <= rem) acc.pair(f(q), f(q + 1));
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        if ((rem & 1) && q == rem - 1) acc.single(f(q));
+                }
+            }
+            labels[i] = b;
+            const double r = __dsub_rn(__dadd_rn(vn[i], cn[b]), __dmul_rn(2.0, acc.result()));
+            cost[i] = r > 0.0 ? r : 0.0;
+            if (old_labels) chg = old_labels[i] != b;
+        } else {
+            flagged[atomicAdd(nflag, 1ull)] = (int32_t)i;
+        }
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, chg);
+    if ((threadIdx.x & 31) == 0 && bal) atomicAdd(changes, (unsigned long long)__popc(bal));
+}
+
 __global__ void as_take_best_kernel(int64_t n, const int32_t* __restrict__ best_idx, int64_t* __restrict__ labels) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) labels[i] = best_idx[i] < 0 ? 0 : best_idx[i];
@@ -1136,6 +1191,7 @@ struct AssignTc {
     DevBuf<int32_t> bidx, flagged;
     DevBuf<float2> bkeys;
     DevBuf<unsigned long long> scal;  // [0] nflag, [1] cnmax bits, [2] absmax bits
+    DevBuf<double> v8;                // the points in 8-column panels (exact costs)
     // eligible: d <= 256, enough rows to pay for the conversion; SPECLUST_ASSIGN=fp64 disables
     int init(int64_t n_, int64_t d_, int64_t k, const double* v, cudaStream_t st) {
         n = n_;
@@ -1162,6 +1218,11 @@ struct AssignTc {
         s = amax > 0 ? std::ldexp(1.0, (int)std::floor(std::log2(128.0 / amax))) : 1.0;
         as_prep_rows_kernel<<<(unsigned)ceil_div(n_pad, 8), 256, 0, st>>>(n, n_pad, d, dp, v, s, vh.p);
         SC_LAUNCHED(1);
+        const int64_t nch = ceil_div(d, 8);
+        if (v8.alloc((size_t)nch * n * 8) == SC_OK) {  // optional: the staged kernel otherwise
+            to_panels_kernel<<<(unsigned)ceil_div(nch * n * 8, 256), 256, 0, st>>>(n, d, v, v8.p);
+            SC_LAUNCHED(1);
+        }
         return make_f16_tile_map(&vmap, vh.p, n_pad, dp);
     }
     // labels / cost / change count of one assignment step
@@ -1195,11 +1256,18 @@ struct AssignTc {
             SC_LAUNCHED(1);
             return SC_OK;
         }
-        constexpr int fin_smem = 8 * kPairStage * (int)sizeof(double);
-        SC_CUDA(cudaFuncSetAttribute(as_finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fin_smem));
-        as_finalize_kernel<<<(unsigned)ceil_div(n, 256), 256, fin_smem, st>>>(n, d, dp, s, v, vn, c, cn, scal.p + 1,
-                                                                             bidx.p, bkeys.p, old_labels, labels,
-                                                                             cost, flagged.p, scal.p, changes);
+        if (v8.p) {
+            as_finalize_panel_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(
+                n, d, dp, s, v8.p, vn, c, cn, scal.p + 1, bidx.p, bkeys.p, old_labels, labels, cost, flagged.p,
+                scal.p, changes);
+        } else {
+            constexpr int fin_smem = 8 * kPairStage * (int)sizeof(double);
+            SC_CUDA(cudaFuncSetAttribute(as_finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fin_smem));
+            as_finalize_kernel<<<(unsigned)ceil_div(n, 256), 256, fin_smem, st>>>(n, d, dp, s, v, vn, c, cn,
+                                                                                 scal.p + 1, bidx.p, bkeys.p,
+                                                                                 old_labels, labels, cost, flagged.p,
+                                                                                 scal.p, changes);
+        }
         SC_LAUNCHED(1);
         // uncertified rows: exact re-scan.  Few rows or few centroids: a warp
         // per row; otherwise the rows are gathered and run through the tiled
