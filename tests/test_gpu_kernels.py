@@ -142,7 +142,7 @@ def test_knn_small_examples():
         sc.build_edges_knn(np.zeros((3, 1)), 3, m)
 
 
-@pytest.mark.parametrize("n,d", [(1200, 128), (6000, 256)])
+@pytest.mark.parametrize("n,d", [(1200, 128), (6000, 256), (20000, 256)])
 def test_knn_hub_rows_value_carrying_fill(n, d):
     """A hub point selected by (almost) every other point: its CSR row has far
     more reverse entries than the fill's shared-memory merge holds, so it takes
@@ -159,10 +159,11 @@ def test_knn_hub_rows_value_carrying_fill(n, d):
     m = sc.SimilarityMeasure.exp_decay(sigma)
     w = knn_graph_device(x, 2, m).to_host()
     assert np.diff(w.row_ptr)[0] > 256
-    e = orc.knn_edges(x, 2, sigma)
-    want = orc.csr_from_edges(n, e, orc.edge_weights(x, e, sigma))
-    assert np.array_equal(w.row_ptr, want[0]) and np.array_equal(w.col_idx, want[1])
-    assert_ulp(w.vals, want[2], 2)
+    if n <= 10000:  # the largest hub (past the shared-memory sort) is checked against the recomputing union
+        e = orc.knn_edges(x, 2, sigma)
+        want = orc.csr_from_edges(n, e, orc.edge_weights(x, e, sigma))
+        assert np.array_equal(w.row_ptr, want[0]) and np.array_equal(w.col_idx, want[1])
+        assert_ulp(w.vals, want[2], 2)
     sel, perm = knn_select_device(x, 2, m, 0, n)
     w2 = knn_union_device(x, 2, m, sel, perm, 0, n).to_host()  # recomputes the distances
     assert np.array_equal(w2.col_idx, w.col_idx) and np.array_equal(w2.vals, w.vals)
