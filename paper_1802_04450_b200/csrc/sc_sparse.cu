@@ -462,13 +462,24 @@ __global__ void sym_scale_kernel(int64_t n, const int64_t* __restrict__ row_ptr,
 
 // Every entry (i, j, v) must have a mirror (j, i, v); rows hold unique
 // columns, so this is equivalent to A == A^T (sparse.py:210-222).
+// Only the strictly upper entries (i, j > i) look up their mirror (j, i);
+// the lower ones are counted: every upper entry has an equal mirror and
+// #upper == #lower  <=>  the matrix is symmetric (the mirror map is then a
+// bijection onto the lower entries).
 __global__ void symmetric_check_kernel(int64_t n, const int64_t* __restrict__ row_ptr,
                                        const int32_t* __restrict__ col,
-                                       const double* __restrict__ vals, int* __restrict__ bad) {
+                                       const double* __restrict__ vals, int* __restrict__ bad,
+                                       unsigned long long* __restrict__ ul) {
     int64_t i = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     if (i >= n) return;
+    unsigned long long nu = 0, nl = 0;
     for (int64_t p = row_ptr[i] + (threadIdx.x & 31), e = row_ptr[i + 1]; p < e; p += 32) {
         int64_t j = col[p];
+        if (j <= i) {
+            nl += j < i;
+            continue;
+        }
+        ++nu;
         int64_t lo = row_ptr[j], hi = row_ptr[j + 1];
         // binary search for column i in row j
         while (lo < hi) {
@@ -476,6 +487,14 @@ __global__ void symmetric_check_kernel(int64_t n, const int64_t* __restrict__ ro
             if (col[mid] < i) lo = mid + 1; else hi = mid;
         }
         if (lo >= row_ptr[j + 1] || col[lo] != i || !(vals[lo] == vals[p])) atomicOr(bad, 1);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        nu += __shfl_xor_sync(0xffffffffu, nu, o);
+        nl += __shfl_xor_sync(0xffffffffu, nl, o);
+    }
+    if ((threadIdx.x & 31) == 0 && (nu | nl)) {
+        atomicAdd(ul, nu);
+        atomicAdd(ul + 1, nl);
     }
 }
 
@@ -592,14 +611,19 @@ int sc_csr_is_symmetric(int64_t n, int64_t nnz, const int64_t* row_ptr, const in
     cudaStream_t st = as_stream(stream);
     StreamScope stream_scope(st);
     DevBuf<int> bad;
+    DevBuf<unsigned long long> ul;
     if (int rc = bad.alloc(1)) return rc;
+    if (int rc = ul.alloc(2)) return rc;
     SC_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
-    symmetric_check_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, st>>>(n, row_ptr, col, vals, bad.p);
+    SC_CUDA(cudaMemsetAsync(ul.p, 0, 2 * sizeof(unsigned long long), st));
+    symmetric_check_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, st>>>(n, row_ptr, col, vals, bad.p, ul.p);
     SC_LAUNCHED(1);
     int h = 0;
+    unsigned long long hul[2] = {0, 0};
     SC_CUDA(cudaMemcpyAsync(&h, bad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    SC_CUDA(cudaMemcpyAsync(hul, ul.p, sizeof(hul), cudaMemcpyDeviceToHost, st));
     SC_CUDA(cudaStreamSynchronize(st));
-    *result = h ? 0 : 1;
+    *result = (h || hul[0] != hul[1]) ? 0 : 1;
     return SC_OK;
 }
 

@@ -88,6 +88,25 @@ def test_symmetry_gate():
     assert not sc.sparse.is_symmetric(a)
     b = sc.coo_to_csr(sc.CooMatrix(2, 2, [0, 1], [1, 0], [1.0, 2.0]))
     assert not sc.sparse.is_symmetric(b)
+    lower_only = sc.coo_to_csr(sc.CooMatrix(2, 2, [1], [0], [1.0]))
+    assert not sc.sparse.is_symmetric(lower_only)
+    # random symmetric pattern with a diagonal; then one extra lower entry
+    rng = np.random.default_rng(8)
+    n = 3000
+    r = rng.integers(0, n, 20000)
+    c = rng.integers(0, n, 20000)
+    v = rng.standard_normal(20000)
+    rr = np.concatenate([r, c, np.arange(n)])
+    cc = np.concatenate([c, r, np.arange(n)])
+    vv = np.concatenate([v, v, np.ones(n)])
+    sym = sc.coo_to_csr(sc.coo_canonicalize(sc.CooMatrix(n, n, rr, cc, vv)))
+    assert sc.sparse.is_symmetric(sym)
+    keys = set(zip(rr.tolist(), cc.tolist()))
+    extra = next((i, j) for i, j in zip(rng.integers(1, n, 100).tolist(), rng.integers(0, n, 100).tolist())
+                 if j < i and (i, j) not in keys)
+    asym = sc.coo_to_csr(sc.coo_canonicalize(sc.CooMatrix(n, n, np.append(rr, extra[0]), np.append(cc, extra[1]),
+                                                            np.append(vv, 1.0))))
+    assert not sc.sparse.is_symmetric(asym)
 
 
 def test_isolated_and_zero_degree():
