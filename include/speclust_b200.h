@@ -191,6 +191,9 @@ typedef struct {
     int64_t n_history;       /* valid entries in history    */
     double history[512];     /* residual_history (first 512 sweeps) */
     int64_t second_passes;   /* steps that needed a second CGS pass */
+    int64_t flushes;         /* block reorthogonalisations of the window */
+    double max_loss;         /* largest |B_old^T V| found by a flush */
+    double mean_window;      /* average window length between flushes */
 } sc_lanczos_stats;
 
 /* RCI session (eigen.py:86-266).  m <= 0 selects default_subspace_dim. */
@@ -274,6 +277,19 @@ int sc_fill_normal(int64_t n, int64_t offset, uint64_t seed, uint64_t stream_id,
 /* eigen-decomposition of the m x m projected matrix (eigen.py:189-192):
  * theta (dev, m) stable descending, S (dev, m x kout column-major) */
 int sc_symeig_f64(int64_t m, int64_t kout, const double* T, double* theta, double* S, sc_stream_t stream);
+/* the same for the structured projected matrix of the thick restart
+ * (eigen.py:189-192, 226-235): rows 0..p-1 diag(theta) coupled only to row p,
+ * rows p..m-1 tridiagonal (p = 0 before the first restart).  Arrowhead
+ * divide and conquer; theta (dev, m) descending, S (dev, m x kout). */
+int sc_symeig_arrow_f64(int64_t m, int64_t p, int64_t kout, const double* T, double* theta, double* S,
+                        sc_stream_t stream);
+/* block Gram-Schmidt against basis columns as DMMA GEMMs (B, V column-major,
+ * leading dimension ld, 1 <= c <= 40):  H (nb x c row-major) = B[:, :nb]^T V */
+int sc_block_tn_f64(int64_t n, int64_t ld, int64_t nb, const double* B, const double* V, int64_t c,
+                    double* H, sc_stream_t stream);
+/* V -= B[:, :nb] H */
+int sc_block_nn_f64(int64_t n, int64_t ld, int64_t nb, const double* B, const double* H, int64_t c,
+                    double* V, sc_stream_t stream);
 /* C = A (n x kk, col-major lda) * S (kk x kc, col-major lds); C col-major ldc or row-major */
 int sc_dgemm_tall(int64_t n, int64_t kk, int64_t kc, const double* A, int64_t lda, const double* S,
                   int64_t lds, double* C, int64_t ldc, int rowmajor, sc_stream_t stream);

@@ -33,6 +33,9 @@ class LanczosStats(C.Structure):
         ("n_history", C.c_int64),
         ("history", C.c_double * 512),
         ("second_passes", C.c_int64),
+        ("flushes", C.c_int64),
+        ("max_loss", C.c_double),
+        ("mean_window", C.c_double),
     ]
 
 
@@ -100,6 +103,9 @@ SIGNATURES = {
     "sc_fill_normal": (i32, [i64, i64, C.c_uint64, C.c_uint64, vp, vp]),
     "sc_div_copy_f64": (i32, [i64, vp, f64, vp, vp]),
     "sc_symeig_f64": (i32, [i64, i64, vp, vp, vp, vp]),
+    "sc_symeig_arrow_f64": (i32, [i64, i64, i64, vp, vp, vp, vp]),
+    "sc_block_tn_f64": (i32, [i64, i64, i64, vp, vp, i64, vp, vp]),
+    "sc_block_nn_f64": (i32, [i64, i64, i64, vp, vp, i64, vp, vp]),
     "sc_dgemm_tall": (i32, [i64, i64, i64, vp, i64, vp, i64, vp, i64, i32, vp]),
     "sc_kmeans_assign": (i32, [i64, i64, i64, vp, vp, vp, vp, vp, P_i64, P_f64, vp]),
     "sc_kmeans_local_sums": (i32, [i64, i64, i64, vp, vp, vp, vp, vp]),

@@ -23,6 +23,8 @@
 
 #include "sc_common.cuh"
 #include "sc_sparse.cuh"
+#include "sc_block.cuh"
+#include "sc_dc.cuh"
 #include "sc_symeig.cuh"
 
 namespace sc {
@@ -36,6 +38,7 @@ constexpr double kReorthEta = 0.05;
 // kNN operator the x gathers are L2-sector bound and the warp-per-row CSR
 // kernel measured faster (161 vs 183 ms per 500 matvecs, profiles/)
 constexpr int64_t kSellMinRows = INT64_MAX;
+constexpr int64_t kMaxWindow = 32;
 
 // ---- kernels ------------------------------------------------------------------
 __global__ void fill_normal_kernel(int64_t n, uint64_t seed, uint64_t stream_id, double* __restrict__ out) {
@@ -234,8 +237,8 @@ __global__ void scale_copy_kernel(int64_t n, const double* __restrict__ src, con
 // h[j] -- the arithmetic of finish_norm_kernel x 2 + commit_alpha_kernel.
 __global__ void __launch_bounds__(1024) step_norms_kernel(int64_t nb_n, const double* __restrict__ sqp, int64_t nb_t,
                                                           const double* __restrict__ sq0, int64_t m, int64_t j,
-                                                          const double* __restrict__ h, double* __restrict__ T,
-                                                          double* __restrict__ scal) {
+                                                          const double* __restrict__ h, int64_t hidx,
+                                                          double* __restrict__ T, double* __restrict__ scal) {
     __shared__ double red[1024];
     for (int pass = 0; pass < 2; ++pass) {
         const double* part = pass ? sq0 : sqp;
@@ -252,8 +255,8 @@ __global__ void __launch_bounds__(1024) step_norms_kernel(int64_t nb_n, const do
         __syncthreads();
     }
     if (threadIdx.x == 0) {
-        T[j * m + j] = h[j];
-        scal[2] = h[j];
+        T[j * m + j] = h[hidx];
+        scal[2] = h[hidx];
     }
 }
 
@@ -538,6 +541,13 @@ struct sc_lanczos {
     int state = 0;  // 0 need_matvec, 1 converged, 2 failed
     int64_t j = 0;
     int64_t restarts = 0, breakdowns = 0, matvecs = 0, second_passes = 0;
+    // windowed reorthogonalisation: columns < j0 are orthogonalised against
+    // each other; win = current window length
+    bool windowed = true;
+    int64_t j0 = 0, win = 8, flushes = 0, window_sum = 0;
+    double max_loss = 0.0;
+    DevBuf<double> bpart, bH;
+    DevBuf<unsigned long long> bmax;
     uint64_t rng_stream = 0;
     double scale = 0.0;
     std::vector<double> history, pending, theta_k, est_k;
@@ -550,15 +560,16 @@ struct sc_lanczos {
     static constexpr int64_t fz_blocks = 4 * kNumSMs;  // persistent grid of the fused pass
 
     // ---- building blocks
-    int project(const double* x, int ncols, double* sq_part = nullptr) {
-        gemv_t_partial_kernel<<<(unsigned)nb_t, 256, 0, st>>>(n, ld, ncols, rpb_t, B.p, x, part.p, sq_part);
+    int project(const double* x, int ncols, double* sq_part = nullptr, int64_t col0 = 0) {
+        gemv_t_partial_kernel<<<(unsigned)nb_t, 256, 0, st>>>(n, ld, ncols, rpb_t, B.p + col0 * ld, x, part.p,
+                                                               sq_part);
         reduce_cols_kernel<<<(unsigned)ceil_div((int64_t)ncols * 32, 256), 256, 0, st>>>(nb_t, ncols, part.p, h.p);
         SC_LAUNCHED(2);
         return SC_OK;
     }
-    int subtract(double* x, int ncols, bool with_norm) {
+    int subtract(double* x, int ncols, bool with_norm, int64_t col0 = 0) {
         gemv_n_update_kernel<<<(unsigned)nb_n, GN_THREADS, sizeof(double) * (size_t)ncols, st>>>(
-            n, ld, ncols, B.p, h.p, x, with_norm ? sqp.p : nullptr);
+            n, ld, ncols, B.p + col0 * ld, h.p, x, with_norm ? sqp.p : nullptr);
         SC_LAUNCHED(1);
         return SC_OK;
     }
@@ -630,8 +641,12 @@ struct sc_lanczos {
             (rc = sqp.alloc(nb_n)) || (rc = sq0.alloc(nb_t)) ||
             (rc = scal.alloc(8)) || (rc = A.alloc((size_t)m * m)) || (rc = Z.alloc((size_t)m * m)) ||
             (rc = wraw.alloc(m)) || (rc = wsort.alloc(m)) || (rc = S.alloc((size_t)m * k)) ||
-            (rc = lastrow.alloc(k)) || (rc = info.alloc(1)) || (rc = nonfinite.alloc(1)))
+            (rc = lastrow.alloc(k)) || (rc = info.alloc(1)) || (rc = nonfinite.alloc(1)) || (rc = bmax.alloc(1)))
             return rc;
+        {
+            const char* e = std::getenv("SPECLUST_REORTH");
+            windowed = !(e && std::strcmp(e, "full") == 0);
+        }
         SC_CUDA(cudaMemsetAsync(T.p, 0, sizeof(double) * m * m, st));
         SC_CUDA(cudaMemsetAsync(w.p, 0, sizeof(double) * ld, st));
         // start vector: normal draws, normalised (eigen.py:113-115)
@@ -663,29 +678,52 @@ struct sc_lanczos {
             SC_CUDA(cudaStreamSynchronize(st));
             if (bad) return fail(SC_ERR_VALUE, "out_slot contains non-finite values");
         }
-        const int cnt = (int)(j + 1);
+        // Orthogonalisation (reference: recurrence + CGS2 over the whole
+        // basis every step, eigen.py:157-163).  Windowed mode (default): two
+        // CGS passes over the window [lo, j] of recent vectors (it always
+        // holds q_{j-1} and q_j, so the three-term components are removed;
+        // the first step after a restart projects on the whole retained block
+        // for the arrowhead couplings), and every `win` steps the window is
+        // orthogonalised against the older basis with two DMMA GEMMs
+        // (flush()).  The loss of orthogonality a window accumulates is
+        // measured exactly at each flush and the window length adapts to
+        // keep it below 1e-9 (semi-orthogonality is sqrt(eps) ~ 1.5e-8).
+        // SPECLUST_REORTH=full: one CGS pass over the whole basis every step
+        // (+ a DGKS-guarded second pass), the round-1 scheme.
+        const bool arrow_step = restarts > 0 && j == k;
+        const int64_t lo = (!windowed || arrow_step) ? 0 : std::max<int64_t>(0, std::min<int64_t>(j0, j - 1));
+        const int cnt = (int)(j + 1 - lo);
         double ab[4];
         {
-            // Full classical Gram-Schmidt against the whole basis; the first
-            // pass also removes the three-term-recurrence components (h[j] =
-            // alpha = q_j^T w).  The reference always runs the recurrence plus
-            // two CGS passes (eigen.py:157-163); here a second pass runs only
-            // when the first one cancelled most of |w| (|w1| < kReorthEta |w0|),
-            // the case in which one pass can leave w non-orthogonal beyond
-            // working precision ("twice is enough", DGKS).  Otherwise the
-            // result is orthogonal to working precision after one pass.
             ProfScope prof("reorth", st, 2.0 * (double)n * cnt * 8.0);
-            if ((rc = project(w.p, cnt, sq0.p))) return rc;
-            if ((rc = subtract(w.p, cnt, true))) return rc;
-            step_norms_kernel<<<1, 1024, 0, st>>>(nb_n, sqp.p, nb_t, sq0.p, m, j, h.p, T.p, scal.p);
+            if ((rc = project(w.p, cnt, sq0.p, lo))) return rc;
+            if ((rc = subtract(w.p, cnt, true, lo))) return rc;
+            step_norms_kernel<<<1, 1024, 0, st>>>(nb_n, sqp.p, nb_t, sq0.p, m, j, h.p, j - lo, T.p, scal.p);
             SC_LAUNCHED(1);
+            if (windowed) {  // second pass over the (short) window, always
+                if ((rc = project(w.p, cnt, nullptr, lo)) || (rc = subtract(w.p, cnt, true, lo))) return rc;
+                finish_norm_kernel<<<1, 1024, 0, st>>>(nb_n, sqp.p, scal.p, 0);
+                SC_LAUNCHED(1);
+            }
             SC_CUDA(cudaMemcpyAsync(ab, scal.p, sizeof(double) * 4, cudaMemcpyDeviceToHost, st));
             SC_CUDA(cudaStreamSynchronize(st));
         }
-        if (ab[0] < kReorthEta * ab[3]) {
+        if (!windowed && ab[0] < kReorthEta * ab[3]) {
             ProfScope prof("reorth", st, 2.0 * (double)n * cnt * 8.0);
             ++second_passes;
             if ((rc = project(w.p, cnt)) || (rc = subtract(w.p, cnt, true))) return rc;
+            finish_norm_kernel<<<1, 1024, 0, st>>>(nb_n, sqp.p, scal.p, 0);
+            SC_LAUNCHED(1);
+            SC_CUDA(cudaMemcpyAsync(ab, scal.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+            SC_CUDA(cudaStreamSynchronize(st));
+        }
+        if (windowed && j + 1 == m) {
+            // end of the sweep: the last window against the older basis, then
+            // one pass of w over the whole (now orthonormal) basis -- w seeds
+            // the next sweep (eigen.py:232) and its norm is the residual scale
+            if ((rc = flush(j0, m - 1))) return rc;
+            ProfScope prof("reorth", st, 2.0 * (double)n * m * 8.0);
+            if ((rc = project(w.p, (int)m)) || (rc = subtract(w.p, (int)m, true))) return rc;
             finish_norm_kernel<<<1, 1024, 0, st>>>(nb_n, sqp.p, scal.p, 0);
             SC_LAUNCHED(1);
             SC_CUDA(cudaMemcpyAsync(ab, scal.p, sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -704,6 +742,55 @@ struct sc_lanczos {
             if ((rc = fresh(j + 1, j + 1, true))) return rc;
         }
         ++j;
+        if (windowed && j - j0 >= win) {
+            if ((rc = flush(j0, j))) return rc;
+            j0 = j + 1;
+        }
+        return SC_OK;
+    }
+
+    // columns [c0, c1] -= B[:, :c0] (B[:, :c0]^T B[:, c0..c1]): one block CGS
+    // pass (the window is within ~1e-9 of orthogonal to the older basis, so a
+    // second pass would change nothing at working precision); the measured
+    // loss adapts the window length
+    int flush(int64_t c0, int64_t c1) {
+        if (c0 <= 0 || c1 < c0) return SC_OK;
+        const int c = (int)(c1 - c0 + 1);
+        int rc;
+        ProfScope prof("reorth", st, 2.0 * (double)n * (double)(c0 + c) * 8.0);
+        const size_t need = block_part_size(n, (int)c0, c);
+        if (bpart.n < need && (rc = bpart.alloc(need))) return rc;
+        if (bH.n < (size_t)c0 * c && (rc = bH.alloc((size_t)m * 48))) return rc;
+        SC_CUDA(cudaMemsetAsync(bmax.p, 0, sizeof(unsigned long long), st));
+        if ((rc = block_tn(n, ld, (int)c0, B.p, B.p + c0 * ld, c, bH.p, bpart.p, bmax.p, st))) return rc;
+        if ((rc = block_nn(n, ld, (int)c0, B.p, bH.p, c, B.p + c0 * ld, st))) return rc;
+        unsigned long long bits = 0;
+        SC_CUDA(cudaMemcpyAsync(&bits, bmax.p, sizeof(bits), cudaMemcpyDeviceToHost, st));
+        SC_CUDA(cudaStreamSynchronize(st));
+        double loss;
+        memcpy(&loss, &bits, sizeof(loss));
+        ++flushes;
+        window_sum += c;
+        max_loss = std::max(max_loss, loss);
+        if (loss > 1e-8) {
+            // far from orthogonal: re-orthonormalise the window in order
+            for (int64_t col = c0; col <= c1; ++col) {
+                double* x = B.p + col * ld;
+                const int cc = (int)(col - c0);
+                if (cc > 0) {
+                    for (int pass = 0; pass < 2; ++pass)
+                        if ((rc = project(x, cc, nullptr, c0)) || (rc = subtract(x, cc, false, c0))) return rc;
+                }
+                sumsq_partial_kernel<<<(unsigned)nb_n, 256, 0, st>>>(n, x, sqp.p, nullptr);
+                finish_norm_kernel<<<1, 1024, 0, st>>>(nb_n, sqp.p, scal.p, 5);
+                scale_copy_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, x, scal.p, 5, x);
+                SC_LAUNCHED(3);
+            }
+        }
+        if (loss > 1e-9)
+            win = std::max<int64_t>(2, win / 2);
+        else if (loss < 1e-11)
+            win = std::min<int64_t>(kMaxWindow, win + std::max<int64_t>(1, win / 4));
         return SC_OK;
     }
     // Y = B[:, :m] S[:, :k]
@@ -718,8 +805,20 @@ struct sc_lanczos {
     // eigen.py:187-239
     int finish_sweep(double beta) {
         int rc;
-        SC_CUDA(cudaMemcpyAsync(A.p, T.p, sizeof(double) * m * m, cudaMemcpyDeviceToDevice, st));
-        if ((rc = symeig_launch((int)m, (int)k, A.p, Z.p, wraw.p, wsort.p, S.p, info.p, st))) return rc;
+        // T is diag(theta) + arrow at row k after a restart, tridiagonal
+        // before the first one: arrowhead divide and conquer (sc_dc.cu);
+        // SPECLUST_SYMEIG=dense keeps the dense Householder + QL solver
+        static const bool dense = [] {
+            const char* e = std::getenv("SPECLUST_SYMEIG");
+            return e && std::strcmp(e, "dense") == 0;
+        }();
+        if (dense) {
+            SC_CUDA(cudaMemcpyAsync(A.p, T.p, sizeof(double) * m * m, cudaMemcpyDeviceToDevice, st));
+            if ((rc = symeig_launch((int)m, (int)k, A.p, Z.p, wraw.p, wsort.p, S.p, info.p, st))) return rc;
+        } else {
+            SC_CUDA(cudaMemsetAsync(info.p, 0, sizeof(int), st));
+            if ((rc = dc_symeig_launch((int)m, restarts > 0 ? (int)k : 0, T.p, (int)k, wsort.p, S.p, st))) return rc;
+        }
         last_row_kernel<<<1, 256, 0, st>>>(m, k, S.p, lastrow.p);
         SC_LAUNCHED(1);
         theta_k.assign(k, 0.0);
@@ -788,6 +887,7 @@ struct sc_lanczos {
             }
         }
         j = k;
+        j0 = k;
         return SC_OK;
     }
 
@@ -859,6 +959,9 @@ int sc_lanczos_get_stats(const sc_lanczos_t* s, sc_lanczos_stats* st) {
     st->matvecs = s->matvecs;
     st->n_history = (int64_t)std::min<size_t>(s->history.size(), 512);
     st->second_passes = s->second_passes;
+    st->flushes = s->flushes;
+    st->max_loss = s->max_loss;
+    st->mean_window = s->flushes ? (double)s->window_sum / (double)s->flushes : 0.0;
     for (int64_t i = 0; i < st->n_history; ++i) st->history[i] = s->history[i];
     return SC_OK;
 }

@@ -130,55 +130,93 @@ __global__ void sbm_scatter_kernel(int64_t n, const int64_t* __restrict__ up_ptr
     }
 }
 
-// sort each row's lower segment (warp per row; <= 64 entries in registers,
-// longer ones by rank counting)
+// sort each row's lower segment: warp per row for <= 64 entries (registers);
+// longer rows are appended to `longs` for sbm_sort_long_kernel
 __global__ void sbm_sort_lower_kernel(int64_t n, const int64_t* __restrict__ row_ptr,
-                                      const unsigned int* __restrict__ low_cnt, int32_t* __restrict__ col) {
+                                      const unsigned int* __restrict__ low_cnt, int32_t* __restrict__ col,
+                                      int64_t* __restrict__ longs, unsigned int* __restrict__ nlong) {
     const int64_t i = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
     if (i >= n) return;
     int32_t* c = col + row_ptr[i];
     const int len = (int)low_cnt[i];
     if (len <= 1) return;
-    if (len <= 64) {
-        int32_t v0 = lane < len ? c[lane] : INT32_MAX;
-        int32_t v1 = lane + 32 < len ? c[lane + 32] : INT32_MAX;
-#pragma unroll
-        for (int k = 2; k <= 64; k <<= 1) {
-#pragma unroll
-            for (int j = k >> 1; j > 0; j >>= 1) {
-                if (j == 32) {
-                    const bool up = (lane & k) == 0;
-                    const int32_t lo = min(v0, v1), hi = max(v0, v1);
-                    v0 = up ? lo : hi;
-                    v1 = up ? hi : lo;
-                } else {
-                    const int32_t o0 = __shfl_xor_sync(0xffffffffu, v0, j);
-                    const int32_t o1 = __shfl_xor_sync(0xffffffffu, v1, j);
-                    const bool lower = (lane & j) == 0;
-                    const bool a0 = lower == ((lane & k) == 0), a1 = lower == (((lane + 32) & k) == 0);
-                    v0 = a0 ? min(v0, o0) : max(v0, o0);
-                    v1 = a1 ? min(v1, o1) : max(v1, o1);
-                }
-            }
-        }
-        __syncwarp();
-        if (lane < len) c[lane] = v0;
-        if (lane + 32 < len) c[lane + 32] = v1;
+    if (len > 64) {
+        if (lane == 0) longs[atomicAdd(nlong, 1u)] = i;
         return;
     }
-    // long lower segments: rank counting into registers, then write
-    int32_t mine[8];
-    int rank[8];
-    int cntm = 0;
-    for (int e = lane; e < len && cntm < 8; e += 32) mine[cntm++] = c[e];
-    for (int t = 0; t < cntm; ++t) {
-        int r = 0;
-        for (int f = 0; f < len; ++f) r += c[f] < mine[t];
-        rank[t] = r;
+    int32_t v0 = lane < len ? c[lane] : INT32_MAX;
+    int32_t v1 = lane + 32 < len ? c[lane + 32] : INT32_MAX;
+#pragma unroll
+    for (int k = 2; k <= 64; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j == 32) {
+                const bool up = (lane & k) == 0;
+                const int32_t lo = min(v0, v1), hi = max(v0, v1);
+                v0 = up ? lo : hi;
+                v1 = up ? hi : lo;
+            } else {
+                const int32_t o0 = __shfl_xor_sync(0xffffffffu, v0, j);
+                const int32_t o1 = __shfl_xor_sync(0xffffffffu, v1, j);
+                const bool lower = (lane & j) == 0;
+                const bool a0 = lower == ((lane & k) == 0), a1 = lower == (((lane + 32) & k) == 0);
+                v0 = a0 ? min(v0, o0) : max(v0, o0);
+                v1 = a1 ? min(v1, o1) : max(v1, o1);
+            }
+        }
     }
     __syncwarp();
-    for (int t = 0; t < cntm; ++t) c[rank[t]] = mine[t];
+    if (lane < len) c[lane] = v0;
+    if (lane + 32 < len) c[lane + 32] = v1;
+}
+
+// one CTA per long row (any length): shared-memory bitonic sort up to
+// kSbmSmemSort entries, rank counting (distinct values) beyond
+constexpr int kSbmSmemSort = 16384;
+__global__ void __launch_bounds__(1024) sbm_sort_long_kernel(const int64_t* __restrict__ longs,
+                                                             const unsigned int* __restrict__ nlong,
+                                                             const int64_t* __restrict__ row_ptr,
+                                                             const unsigned int* __restrict__ low_cnt,
+                                                             int32_t* __restrict__ col, int32_t* __restrict__ scratch) {
+    extern __shared__ int32_t sk[];
+    for (unsigned int t = blockIdx.x; t < *nlong; t += gridDim.x) {
+        const int64_t i = longs[t];
+        int32_t* c = col + row_ptr[i];
+        const int len = (int)low_cnt[i];
+        if (len <= kSbmSmemSort) {
+            int np2 = 1;
+            while (np2 < len) np2 <<= 1;
+            for (int e = threadIdx.x; e < np2; e += blockDim.x) sk[e] = e < len ? c[e] : INT32_MAX;
+            __syncthreads();
+            for (int size = 2; size <= np2; size <<= 1)
+                for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                    for (int q = threadIdx.x; q < np2 / 2; q += blockDim.x) {
+                        const int lo = 2 * q - (q & (stride - 1)), hi = lo + stride;
+                        const bool up = (lo & size) == 0;
+                        const int32_t a = sk[lo], b = sk[hi];
+                        if ((a > b) == up) {
+                            sk[lo] = b;
+                            sk[hi] = a;
+                        }
+                    }
+                    __syncthreads();
+                }
+            for (int e = threadIdx.x; e < len; e += blockDim.x) c[e] = sk[e];
+        } else {
+            // sources of one row are distinct: rank = number of smaller ones
+            int32_t* out = scratch + row_ptr[i];
+            for (int e = threadIdx.x; e < len; e += blockDim.x) {
+                const int32_t v = c[e];
+                int r = 0;
+                for (int f = 0; f < len; ++f) r += c[f] < v;
+                out[r] = v;
+            }
+            __syncthreads();
+            for (int e = threadIdx.x; e < len; e += blockDim.x) c[e] = out[e];
+        }
+        __syncthreads();
+    }
 }
 
 }  // namespace sc
@@ -189,8 +227,7 @@ extern "C" {
 
 // Two calls: with col == NULL the total nnz comes back in *nnz_out (host);
 // then with caller-allocated row_ptr (n+1), col / vals (nnz) (dev).  offsets
-// (dev int64, nblocks + 1): block boundaries.  Rows with more than 256
-// lower-triangle neighbours are rejected (SC_ERR_VALUE).
+// (dev int64, nblocks + 1): block boundaries.  Any row length.
 int sc_sbm_csr(int64_t n, const int64_t* offsets, int64_t nblocks, double p_in, double p_out, uint64_t seed,
                int64_t* row_ptr, int32_t* col, double* vals, int64_t* nnz_out, sc_stream_t stream) {
     cudaStream_t st = as_stream(stream);
@@ -227,12 +264,27 @@ int sc_sbm_csr(int64_t n, const int64_t* offsets, int64_t nblocks, double p_in, 
     unsigned int hmax = 0;
     SC_CUDA(cudaMemcpyAsync(&hmax, maxlow.p, sizeof(hmax), cudaMemcpyDeviceToHost, st));
     SC_CUDA(cudaStreamSynchronize(st));
-    // the per-row sort of the lower segment holds at most 8 x 32 entries
-    if (hmax > 256) return fail(SC_ERR_VALUE, "sbm: a row has more than 256 lower-triangle neighbours");
     if ((rc = exclusive_scan_i64(n, len.p, row_ptr, tmp.p, st))) return rc;
     sbm_scatter_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, up_ptr.p, up_col.p, low_cnt.p, row_ptr, cursor.p,
                                                                    col, vals);
-    sbm_sort_lower_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, st>>>(n, row_ptr, low_cnt.p, col);
+    // lower segments in ascending column order (unbounded length)
+    DevBuf<int64_t> longs;
+    DevBuf<unsigned int> nlong;
+    DevBuf<int32_t> scratch;
+    if ((rc = longs.alloc(n)) || (rc = nlong.alloc(1))) return rc;
+    if (hmax > (unsigned)kSbmSmemSort && (rc = scratch.alloc(2 * nup + 1))) return rc;
+    SC_CUDA(cudaMemsetAsync(nlong.p, 0, sizeof(unsigned int), st));
+    sbm_sort_lower_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, st>>>(n, row_ptr, low_cnt.p, col, longs.p, nlong.p);
+    if (hmax > 64) {
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(sbm_sort_long_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kSbmSmemSort * (int)sizeof(int32_t));
+            attr = true;
+        }
+        sbm_sort_long_kernel<<<4 * kNumSMs, 1024, kSbmSmemSort * sizeof(int32_t), st>>>(longs.p, nlong.p, row_ptr,
+                                                                                      low_cnt.p, col, scratch.p);
+    }
     SC_LAUNCHED(2);
     SC_CUDA(cudaStreamSynchronize(st));
     return SC_OK;

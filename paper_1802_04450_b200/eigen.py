@@ -240,7 +240,8 @@ def eigensolve_device(a: DeviceCsr, cfg: LanczosConfig, probe: bool = True):
         nat.check(rc, values=vals.copy(), residuals=res.copy())
     nat.check(rc)
     stats = dict(restarts=int(st.restarts), breakdowns=int(st.breakdowns), matvecs=int(st.matvecs),
-                 second_passes=int(st.second_passes),
+                 second_passes=int(st.second_passes), flushes=int(st.flushes), max_loss=float(st.max_loss),
+                 mean_window=float(st.mean_window),
                  history=[float(st.history[i]) for i in range(st.n_history)], m=m)
     return vals, vecs, res, stats
 

@@ -564,21 +564,23 @@ def _lloyd_cases():
 
 
 def test_lloyd_tensor_core_assignment_bit_identical(monkeypatch):
-    """The tcgen05 assignment with certified argmin (d <= 256, n >= 4096)
-    yields bit-identical labels, centroids, SSE history and iteration counts
-    to the fp64 Gram-expansion path (itself bit-exact with the reference), on
-    unit-norm embeddings, raw large-magnitude data and data with exact
-    duplicate rows."""
+    """The tcgen05 assignment with certified argmin (n >= 4096) yields
+    labels, centroids, SSE history and iteration counts bit-identical to the
+    CPU oracle's restatement of kmeans.py:159-196 (pinned to the reference by
+    tests/test_oracle_golden.py) and to the library's fp64 path, on unit-norm
+    embeddings, raw large-magnitude data and data with exact duplicate rows."""
     for v, init, k in _lloyd_cases():
         cfg = sc.KmeansConfig(k=k, max_iters=40)
+        got = sc.lloyd(v, init, cfg)
+        labels, cent, sse, iters, hist = orc.lloyd(v, init, max_iters=40)
+        assert got.iters_run == iters, v.shape
+        assert np.array_equal(got.labels, labels), v.shape
+        assert np.array_equal(got.centroids, cent), v.shape
+        assert np.array_equal(got.sse_history, hist), v.shape
         monkeypatch.setenv("SPECLUST_ASSIGN", "fp64")
         ref = sc.lloyd(v, init, cfg)
         monkeypatch.delenv("SPECLUST_ASSIGN")
-        got = sc.lloyd(v, init, cfg)
-        assert got.iters_run == ref.iters_run, v.shape
-        assert np.array_equal(got.labels, ref.labels), v.shape
-        assert np.array_equal(got.centroids, ref.centroids), v.shape
-        assert np.array_equal(got.sse_history, ref.sse_history), v.shape
+        assert np.array_equal(got.labels, ref.labels) and np.array_equal(got.sse_history, ref.sse_history)
 
 
 # ---------------------------------------------------------------- §8(f) rows
@@ -689,6 +691,33 @@ def test_sbm_generator_statistics():
     assert full.nnz == 5 * 4 + 4 * 3
     empty, _ = sc.sbm_generate(sc.SbmConfig(block_sizes=(5, 4), p_in=0.0, p_out=0.0))
     assert empty.nnz == 0
+
+
+@pytest.mark.parametrize("sizes,p_in,p_out", [((100,) * 200, 0.3, 0.01),   # Syn200 (test_acceptance.py:186)
+                                              ((300,), 1.0, 0.0),           # dense: 299 lower neighbours
+                                              ((3000,), 1.0, 0.0),          # past the shared-memory bitonic? no: 2999
+                                              ((20000,), 1.0, 0.0)])        # rank-counting path (19999 > 16384)
+def test_sbm_long_rows(sizes, p_in, p_out):
+    """Rows with more than 256 (and more than 16384) lower-triangle
+    neighbours: canonical CSR, exact edge count when p = 1."""
+    import torch
+    from paper_1802_04450_b200.sbm import sbm_generate_device
+
+    w, _ = sbm_generate_device(sc.SbmConfig(block_sizes=sizes, p_in=p_in, p_out=p_out, seed=5))
+    rp = w.row_ptr.cpu().numpy()
+    col = w.col.cpu().numpy().astype(np.int64)
+    n = rp.size - 1
+    rows = np.repeat(np.arange(n), np.diff(rp))
+    assert np.all(np.diff(col)[np.diff(rows) == 0] > 0)  # strictly increasing per row
+    assert not np.any(col == rows)
+    if p_in == 1.0:
+        assert w.nnz == n * (n - 1)
+    else:
+        assert abs(w.nnz / 2 - 2_288_817) < 30_000  # Syn200's edge count in the reference (SURVEY §6)
+    # symmetric: the transpose has the same canonical order
+    t = np.lexsort((rows, col))
+    assert np.array_equal(col[t], rows) and np.array_equal(rows[t], col)
+    del torch
 
 
 def test_sbm_pipeline_and_binary_input(tmp_path):
