@@ -322,7 +322,7 @@ __global__ void centroid_mean_kernel(int64_t k, int64_t d, const double* __restr
 // sequentially (warp = segment x 32 features), level 2 adds the segment sums
 // of a cluster in segment order and divides by the count.  Deterministic;
 // identical to the point-order chain for clusters of <= CM_SEG members.
-constexpr int64_t CM_SEG = 512;
+constexpr int64_t CM_SEG = INT64_MAX / 4;  // one segment per cluster: the exact point-order chain
 __global__ void centroid_segsum_kernel(int64_t k, int64_t d, int64_t nseg, const double* __restrict__ v,
                                        const int64_t* __restrict__ start, const int32_t* __restrict__ members,
                                        const int64_t* __restrict__ seg_off, double* __restrict__ part) {
@@ -341,19 +341,27 @@ __global__ void centroid_segsum_kernel(int64_t k, int64_t d, int64_t nseg, const
     const int64_t cl = lo;
     const int64_t b = start[cl] + (s - seg_off[cl]) * CM_SEG;
     const int64_t e = imin64(start[cl + 1], b + CM_SEG);
-    if (dim >= d) return;
+    // the chain is strictly sequential in point order (np.add.at); the warp
+    // loads 64 member indices per batch (two coalesced loads, shuffled to
+    // every lane) and then the 64 rows' values of its 32 features, so 64
+    // independent loads are in flight per lane ahead of the dependent adds
+    const bool on = dim < d;
     double acc = 0.0;
     int64_t m = b;
-    constexpr int B = 16;
+    constexpr int B = 64;
     for (; m + B <= e; m += B) {
+        const int32_t i0 = __ldg(members + m + lane), i1 = __ldg(members + m + 32 + lane);
         double x[B];
 #pragma unroll
-        for (int u = 0; u < B; ++u) x[u] = __ldg(v + (int64_t)__ldg(members + m + u) * d + dim);
+        for (int u = 0; u < B; ++u) {
+            const int32_t r = __shfl_sync(0xffffffffu, u < 32 ? i0 : i1, u & 31);
+            x[u] = on ? __ldg(v + (int64_t)r * d + dim) : 0.0;
+        }
 #pragma unroll
         for (int u = 0; u < B; ++u) acc = __dadd_rn(acc, x[u]);
     }
-    for (; m < e; ++m) acc = __dadd_rn(acc, v[(int64_t)members[m] * d + dim]);
-    part[s * d + dim] = acc;
+    for (; m < e; ++m) acc = __dadd_rn(acc, on ? v[(int64_t)members[m] * d + dim] : 0.0);
+    if (on) part[s * d + dim] = acc;
 }
 
 __global__ void centroid_segmean_kernel(int64_t k, int64_t d, const int64_t* __restrict__ start,
@@ -946,6 +954,81 @@ static double np_pairwise_sum(const double* a, int64_t n) {
     return np_pairwise_sum(a, n2) + np_pairwise_sum(a + n2, n - n2);
 }
 
+// numpy's sum of a device array (np.add.reduce over a contiguous float64
+// array = DOUBLE_pairwise_sum of the whole array): the recursion's leaves
+// (<= 128 elements, 8 accumulators) are summed on the device, one thread per
+// leaf, and combined on the host in the recursion's order.  The reference's
+// SSE history is float(point_cost.sum()) (kmeans.py:176, 184).
+__global__ void np_leaf_sum_kernel(int64_t nleaf, const int64_t* __restrict__ off, const double* __restrict__ a,
+                                   double* __restrict__ out) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nleaf) return;
+    const double* x = a + off[t];
+    const int64_t n = off[t + 1] - off[t];
+    double res;
+    if (n < 8) {
+        res = 0.0;
+        for (int64_t i = 0; i < n; ++i) res = __dadd_rn(res, x[i]);
+    } else {
+        double r[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = x[j];
+        int64_t i = 8;
+        for (; i < n - (n % 8); i += 8)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], x[i + j]);
+        res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                        __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+        for (; i < n; ++i) res = __dadd_rn(res, x[i]);
+    }
+    out[t] = res;
+}
+
+struct NpSum {
+    int64_t n = -1;
+    std::vector<int64_t> off;  // leaf boundaries
+    std::vector<double> h;
+    DevBuf<int64_t> d_off;
+    DevBuf<double> d_leaf;
+    static void leaves(int64_t o, int64_t n, std::vector<int64_t>& out) {
+        if (n <= 128) {
+            out.push_back(o + n);
+            return;
+        }
+        int64_t n2 = n / 2;
+        n2 -= n2 % 8;
+        leaves(o, n2, out);
+        leaves(o + n2, n - n2, out);
+    }
+    double combine(int64_t n, size_t& li) const {
+        if (n <= 128) return h[li++];
+        int64_t n2 = n / 2;
+        n2 -= n2 % 8;
+        const double a = combine(n2, li);
+        const double b = combine(n - n2, li);
+        return a + b;
+    }
+    int sum(const double* a, int64_t n_, double* result, cudaStream_t st) {
+        int rc;
+        if (n_ != n) {
+            n = n_;
+            off.assign(1, 0);
+            leaves(0, n, off);
+            if ((rc = d_off.alloc(off.size())) || (rc = d_leaf.alloc(off.size()))) return rc;
+            SC_CUDA(cudaMemcpyAsync(d_off.p, off.data(), sizeof(int64_t) * off.size(), cudaMemcpyHostToDevice, st));
+            h.assign(off.size() - 1, 0.0);
+        }
+        const int64_t nl = (int64_t)off.size() - 1;
+        np_leaf_sum_kernel<<<(unsigned)ceil_div(nl, 128), 128, 0, st>>>(nl, d_off.p, a, d_leaf.p);
+        SC_LAUNCHED(1);
+        SC_CUDA(cudaMemcpyAsync(h.data(), d_leaf.p, sizeof(double) * nl, cudaMemcpyDeviceToHost, st));
+        SC_CUDA(cudaStreamSynchronize(st));
+        size_t li = 0;
+        *result = n > 0 ? combine(n, li) : 0.0;
+        return SC_OK;
+    }
+};
+
 // labels[i] = nearest of the k rows of c (fp64 distance tiles, ties -> lowest)
 
 }  // namespace sc
@@ -1451,10 +1534,8 @@ int sc_lloyd(int64_t n, int64_t d, int64_t k, const double* v, const double* c_i
     };
     SC_LAUNCHED(2);
     if ((rc = assign_step(nullptr, labels))) return rc;
-    sum_partials_kernel<<<1, 1024, 0, st>>>(nb, part.p, sse.p);
-    SC_LAUNCHED(1);
-    SC_CUDA(cudaMemcpyAsync(&sse_history[0], sse.p, sizeof(double), cudaMemcpyDeviceToHost, st));
-    SC_CUDA(cudaStreamSynchronize(st));
+    NpSum npsum;
+    if ((rc = npsum.sum(cost.p, n, &sse_history[0], st))) return rc;
 
     int64_t* cur = labels;
     int64_t* nxt = lab2.p;
@@ -1501,12 +1582,10 @@ int sc_lloyd(int64_t n, int64_t d, int64_t k, const double* v, const double* c_i
         rownorm_kernel<<<(unsigned)ceil_div(k, 256), 256, 0, st>>>(k, d, centroids, cn.p);
         SC_CUDA(cudaMemsetAsync(changes.p, 0, sizeof(unsigned long long), st));
         if ((rc = assign_step(cur, nxt))) return rc;
-        sum_partials_kernel<<<1, 1024, 0, st>>>(nb, part.p, sse.p);
-        SC_LAUNCHED(2);
+        SC_LAUNCHED(1);
         unsigned long long hchg = 0;
-        SC_CUDA(cudaMemcpyAsync(&sse_history[iters + 1], sse.p, sizeof(double), cudaMemcpyDeviceToHost, st));
         SC_CUDA(cudaMemcpyAsync(&hchg, changes.p, sizeof(hchg), cudaMemcpyDeviceToHost, st));
-        SC_CUDA(cudaStreamSynchronize(st));
+        if ((rc = npsum.sum(cost.p, n, &sse_history[iters + 1], st))) return rc;
         ++iters;
         std::swap(cur, nxt);
         if ((int64_t)hchg <= tol_changes) break;

@@ -21,6 +21,8 @@
 #include <cstring>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "sc_common.cuh"
 #include "sc_sparse.cuh"
 #include "sc_block.cuh"
@@ -38,7 +40,7 @@ constexpr double kReorthEta = 0.05;
 // kNN operator the x gathers are L2-sector bound and the warp-per-row CSR
 // kernel measured faster (161 vs 183 ms per 500 matvecs, profiles/)
 constexpr int64_t kSellMinRows = INT64_MAX;
-constexpr int64_t kMaxWindow = 32;
+constexpr int64_t kMaxWindow = 16;
 
 // ---- kernels ------------------------------------------------------------------
 __global__ void fill_normal_kernel(int64_t n, uint64_t seed, uint64_t stream_id, double* __restrict__ out) {
@@ -186,6 +188,128 @@ __global__ void __launch_bounds__(GN_THREADS) gemv_n_update_kernel(int64_t n, in
             for (int i = 0; i < GN_THREADS / 32; ++i) t += red[i];
             sq_part[blockIdx.x] = t;
         }
+    }
+}
+
+// Two classical Gram-Schmidt passes of w against the window columns
+// B[:, lo .. lo+cnt) in ONE cooperative launch (the window is short: the
+// per-step cost was launch latency, ~10 kernels):
+//   h1 = Bw^T w;  w -= Bw h1;  h2 = Bw^T w;  w -= Bw h2;  beta = |w|
+// with the second projection accumulated in the same row sweep as the first
+// update (Bw read three times, not four).  Fixed-order reductions (every
+// block sums the per-block partials in block order), so the result does not
+// depend on scheduling.  Outputs: T[j,j] = scal[2] = alpha = h1[cnt-1]
+// (q_j is the last window column), scal[0] = |w|, scal[3] = |w0|.
+#define WCG_BLOCK_REDUCE_STORE(ACC, NCOL)                                       \
+    do {                                                                        \
+        _Pragma("unroll") for (int c_ = 0; c_ <= NC; ++c_) {                    \
+            if (c_ < (NCOL)) {                                                  \
+                const double v_ = warp_sum(ACC[c_]);                            \
+                if (lane == 0) red[warp][c_] = v_;                              \
+            }                                                                   \
+        }                                                                       \
+        __syncthreads();                                                        \
+        for (int c_ = threadIdx.x; c_ < (NCOL); c_ += blockDim.x) {             \
+            double t_ = 0.0;                                                    \
+            for (int q_ = 0; q_ < 8; ++q_) t_ += red[q_][c_];                   \
+            part[(int64_t)blockIdx.x * stride + c_] = t_;                       \
+        }                                                                       \
+        __syncthreads();                                                        \
+    } while (0)
+constexpr int WCG_MAX = 40;
+template <int NC>
+__global__ void __launch_bounds__(256) window_cgs2_kernel(int64_t n, int64_t ld, const double* __restrict__ Bw, int cnt,
+                                                          double* __restrict__ w, double* __restrict__ part,
+                                                          int64_t m, int64_t j, double* __restrict__ T,
+                                                          double* __restrict__ scal) {
+    cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+    __shared__ double red[8][NC + 1];
+    __shared__ double hs[NC];
+    const int nb = gridDim.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t per = ceil_div_dev(n, nb);
+    const int64_t r0 = (int64_t)blockIdx.x * per, r1 = r0 + per < n ? r0 + per : n;
+    const int stride = WCG_MAX + 1;  // part[b * stride + c], c == cnt: |w|^2
+    auto gather_h = [&](int ncol) {
+        for (int c = threadIdx.x; c < ncol; c += blockDim.x) {
+            double t = 0.0;
+            for (int b = 0; b < nb; ++b) t += part[(int64_t)b * stride + c];
+            hs[c] = t;
+        }
+        __syncthreads();
+    };
+    double acc[NC + 1];
+    // pass 1: projections of the raw w and |w0|^2
+#pragma unroll
+    for (int c = 0; c <= NC; ++c) acc[c] = 0.0;
+    for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+        const double x = w[r];
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+            if (c < cnt) acc[c] = fma(__ldg(Bw + (int64_t)c * ld + r), x, acc[c]);
+        acc[NC] = fma(x, x, acc[NC]);
+    }
+    {
+        const double v = warp_sum(acc[NC]);
+        if (lane == 0) red[warp][NC] = v;
+    }
+    WCG_BLOCK_REDUCE_STORE(acc, cnt);  // (its barriers also publish red[][NC])
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int q = 0; q < 8; ++q) t += red[q][NC];
+        part[(int64_t)blockIdx.x * stride + WCG_MAX] = t;
+    }
+    grid.sync();
+    gather_h(cnt);
+    double w0sq = 0.0;
+    for (int b = 0; b < nb; ++b) w0sq += part[(int64_t)b * stride + WCG_MAX];
+    const double alpha = hs[cnt - 1];
+    // update 1 fused with the projections of the updated w (pass 2)
+#pragma unroll
+    for (int c = 0; c <= NC; ++c) acc[c] = 0.0;
+    for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+        double s = 0.0;
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+            if (c < cnt) s = fma(__ldg(Bw + (int64_t)c * ld + r), hs[c], s);
+        const double x = w[r] - s;
+        w[r] = x;
+#pragma unroll
+        for (int c = 0; c < NC; ++c)  // the same lines again: L1 hits
+            if (c < cnt) acc[c] = fma(__ldg(Bw + (int64_t)c * ld + r), x, acc[c]);
+    }
+    grid.sync();  // every block has read hs-dependent part[] before it is overwritten
+    WCG_BLOCK_REDUCE_STORE(acc, cnt);
+    grid.sync();
+    gather_h(cnt);
+    // update 2 and |w|^2
+    double sq = 0.0;
+    for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+        double s = 0.0;
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+            if (c < cnt) s = fma(__ldg(Bw + (int64_t)c * ld + r), hs[c], s);
+        const double x = w[r] - s;
+        w[r] = x;
+        sq = fma(x, x, sq);
+    }
+    {
+        const double v = warp_sum(sq);
+        if (lane == 0) red[warp][0] = v;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int q = 0; q < 8; ++q) t += red[q][0];
+            part[(int64_t)blockIdx.x * stride + WCG_MAX] = t;
+        }
+    }
+    grid.sync();
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        double t = 0.0;
+        for (int b = 0; b < nb; ++b) t += part[(int64_t)b * stride + WCG_MAX];
+        scal[0] = sqrt(t);
+        scal[2] = alpha;
+        scal[3] = sqrt(w0sq);
+        T[j * m + j] = alpha;
     }
 }
 
@@ -544,9 +668,9 @@ struct sc_lanczos {
     // windowed reorthogonalisation: columns < j0 are orthogonalised against
     // each other; win = current window length
     bool windowed = true;
-    int64_t j0 = 0, win = 8, flushes = 0, window_sum = 0;
+    int64_t j0 = 0, win = 6, flushes = 0, window_sum = 0;
     double max_loss = 0.0;
-    DevBuf<double> bpart, bH;
+    DevBuf<double> bpart, bH, wpart;
     DevBuf<unsigned long long> bmax;
     uint64_t rng_stream = 0;
     double scale = 0.0;
@@ -694,7 +818,12 @@ struct sc_lanczos {
         const int64_t lo = (!windowed || arrow_step) ? 0 : std::max<int64_t>(0, std::min<int64_t>(j0, j - 1));
         const int cnt = (int)(j + 1 - lo);
         double ab[4];
-        {
+        if (windowed && !arrow_step && cnt <= WCG_MAX) {
+            ProfScope prof("reorth", st, 3.0 * (double)n * cnt * 8.0);
+            if ((rc = window_cgs2(lo, cnt))) return rc;
+            SC_CUDA(cudaMemcpyAsync(ab, scal.p, sizeof(double) * 4, cudaMemcpyDeviceToHost, st));
+            SC_CUDA(cudaStreamSynchronize(st));
+        } else {
             ProfScope prof("reorth", st, 2.0 * (double)n * cnt * 8.0);
             if ((rc = project(w.p, cnt, sq0.p, lo))) return rc;
             if ((rc = subtract(w.p, cnt, true, lo))) return rc;
@@ -749,6 +878,37 @@ struct sc_lanczos {
         return SC_OK;
     }
 
+    int window_cgs2(int64_t lo, int cnt) {
+        void* fn = cnt <= 8    ? (void*)window_cgs2_kernel<8>
+                   : cnt <= 16 ? (void*)window_cgs2_kernel<16>
+                   : cnt <= 24 ? (void*)window_cgs2_kernel<24>
+                               : (void*)window_cgs2_kernel<40>;
+        const int bucket = cnt <= 8 ? 0 : cnt <= 16 ? 1 : cnt <= 24 ? 2 : 3;
+        static int bps_tab[4] = {0, 0, 0, 0};
+        int& bps = bps_tab[bucket];
+        if (!bps) {
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, fn, 256, 0);
+            if (bps < 1) bps = 1;
+        }
+        int dev = 0, nsm = kNumSMs;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)bps * nsm, ceil_div(n, 256)));
+        int rc;
+        if (wpart.n < (size_t)grid * (WCG_MAX + 1) && (rc = wpart.alloc((size_t)grid * (WCG_MAX + 1)))) return rc;
+        const double* Bw = B.p + lo * ld;
+        double* wp = w.p;
+        double* pp = wpart.p;
+        double* Tp = T.p;
+        double* sp = scal.p;
+        int64_t nn = n, ldd = ld, mm = m, jj = j;
+        int c = cnt;
+        void* args[] = {&nn, &ldd, (void*)&Bw, &c, &wp, &pp, &mm, &jj, &Tp, &sp};
+        SC_CUDA(cudaLaunchCooperativeKernel(fn, grid, 256, args, 0, st));
+        SC_LAUNCHED(1);
+        return SC_OK;
+    }
+
     // columns [c0, c1] -= B[:, :c0] (B[:, :c0]^T B[:, c0..c1]): one block CGS
     // pass (the window is within ~1e-9 of orthogonal to the older basis, so a
     // second pass would change nothing at working precision); the measured
@@ -787,10 +947,16 @@ struct sc_lanczos {
                 SC_LAUNCHED(3);
             }
         }
-        if (loss > 1e-9)
-            win = std::max<int64_t>(2, win / 2);
-        else if (loss < 1e-11)
-            win = std::min<int64_t>(kMaxWindow, win + std::max<int64_t>(1, win / 4));
+        // the loss grows geometrically with the window length: aim the next
+        // window at 1e-9 from the growth rate this one showed, growing by at
+        // most two vectors per flush
+        // (aim at 1e-11: the growth rate is not steady -- it rises as Ritz
+        // values converge inside a sweep -- so keep two decades of headroom
+        // below the 1e-9 the window must not exceed)
+        double target = (double)kMaxWindow;
+        if (loss > 1e-16) target = (double)c * 5.0 / std::log10(loss / 1e-16);
+        if (loss > 1e-9) target = std::min(target, (double)c / 2);
+        win = std::max<int64_t>(2, std::min<int64_t>({kMaxWindow, (int64_t)target, (int64_t)c + 1}));
         return SC_OK;
     }
     // Y = B[:, :m] S[:, :k]

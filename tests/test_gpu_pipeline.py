@@ -76,6 +76,17 @@ def test_pipeline_config1_full(golden):
     assert sha(w.col_idx) == str(g["col_sha"])
     assert np.max(np.abs(rep.eigenvalues - g["values"]) / np.abs(g["values"])) < 1e-5
     assert orc.ari(rep.labeling.labels, g["labels"]) >= 0.999
+    # eigenvector subspace vs the reference's (shape_c1p.npz: projector sketch,
+    # tests/golden/make_golden_r2.py --case c1p); sin(max angle) <= |P - P_ref|_F
+    p = golden("shape_c1p")
+    assert np.array_equal(rep.eigenvalues, rep.eigenvalues) and sha(x) == str(p["x_sha"])
+    d = sc.degrees(w)
+    b = sc.eigensolve(sc.sym_scale(w, d), sc.LanczosConfig(k=k, seed=0))
+    gk = np.random.default_rng(777).standard_normal((w.n_rows, 16))
+    q, _ = np.linalg.qr(b.vectors)
+    dist = np.linalg.norm(q @ (q.T @ gk) - p["psketch"]) / 4.0
+    assert dist < 1e-4, dist
+    assert np.max(np.abs(b.values - p["values"]) / np.abs(p["values"])) < 1e-5
 
 
 def test_matrix_input_two_triangles():
