@@ -2,7 +2,7 @@
 (kNN exp_decay graph -> Lanczos -> k-means) on BASELINE.json's configs[1]
 workload (synthetic blobs N=1M, d=64, kNN=32, k=100) on one B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c1]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c1|c3|c3h]
     python bench.py --impl reference ...   # CPU reference arm (oracle port)
 
 One JSON line on rank 0.  ``value`` = seconds per clustering with X already
@@ -32,7 +32,11 @@ WORKLOADS = {
     # name: (n, d, knn, k, center_scale)
     "c1": (20_000, 32, 16, 20, 1.0),
     "c2": (1_000_000, 64, 32, 100, 0.7),
+    "c3": (4_000_000, 128, 32, 1000, 1.0),
+    "c3h": (1_000_000, 128, 32, 1000, 1.0),
 }
+CONFIG_NOTE = {"c1": "BASELINE.json configs[0]", "c2": "BASELINE.json configs[1]",
+               "c3": "BASELINE.json configs[2] at 1 GPU", "c3h": "BASELINE.json configs[2] shape at N/4"}
 
 
 def peaks():
@@ -98,49 +102,75 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-def cpu_reference(n, d, knn, k, cs, sample_n, steps, warmup):
-    """Time the CPU oracle (a port of the reference's algorithm) on a bounded
-    sample of the workload and extrapolate each stage to full size:
-    graph ~ N^2 (all-pairs scan), eigen and k-means ~ N (same iteration
-    counts assumed)."""
+def host_cpu():
+    model = ""
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "model": model}
+
+
+def oracle_run(n, d, knn, k, cs, seed=0):
+    """One timed CPU-oracle clustering (a numpy port of the reference's
+    algorithm, test infrastructure) of the blobs workload; numpy's BLAS uses
+    every host core.  Returns (wall seconds, stage seconds, labels, planted)."""
     from oracle import speclust_oracle as orc
 
-    x, _ = make_blobs(sample_n, d, k, cs, seed=0)
-    sigma = float(np.sqrt(d))
-    times = []
-    stages = None
-    for it in range(warmup + steps):
-        tm = {}
-        t0 = time.perf_counter()
-        orc.run_points(x, knn, sigma, k, timings=tm)
-        wall = time.perf_counter() - t0
-        if it >= warmup:
-            times.append(wall)
-            stages = tm
+    x, y = make_blobs(n, d, k, cs, seed=seed)
+    tm = {}
+    t0 = time.perf_counter()
+    out = orc.run_points(x, knn, float(np.sqrt(d)), k, timings=tm)
+    return time.perf_counter() - t0, tm, out["labels"], y
+
+
+def extrapolate(stages, n, sample_n):
+    """Model only (never a measured value): graph ~ N^2 (all-pairs scan), the
+    other stages ~ N at the sample's iteration counts."""
     r = n / sample_n
-    est = stages["graph"] * r * r + (stages["degrees"] + stages["eigen"] + stages["kmeans"] + stages["metrics"]) * r
-    sample = (f"oracle run_points on N={sample_n} (d={d}, kNN={knn}, k={k}); median wall "
-              f"{np.median(times):.2f}s; stages {{{', '.join(f'{a}: {b:.2f}' for a, b in stages.items())}}} s; "
-              f"extrapolated to N={n}: graph x(N/n)^2, other stages x(N/n)")
-    return est, sample, stages
+    return stages["graph"] * r * r + sum(v for s, v in stages.items() if s != "graph") * r
 
 
 def run_reference_arm(args, wl):
+    """The reference arm: the CPU oracle timed on a bounded sample of the
+    workload (N = --ref-sample points of the same distribution), every step
+    measured; ``value`` is that measured sample time.  The full-size
+    extrapolation is a separate, labelled estimate."""
     n, d, knn, k, cs = wl
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    cores = os.cpu_count()
-    sample_n = args.ref_sample
-    est, sample, _ = cpu_reference(n, d, knn, k, cs, sample_n, args.steps, args.warmup)
+    sn = min(args.ref_sample, n)
+    times, stages = [], None
+    t_run0 = time.perf_counter()
+    for it in range(args.warmup + args.steps):
+        wall, tm, _, _ = oracle_run(sn, d, knn, k, cs)
+        if it >= args.warmup:
+            times.append(wall)
+            stages = tm
+    run_s = time.perf_counter() - t_run0
+    v = float(np.median(times))
+    cpu = host_cpu()
+    sample = (f"oracle run_points on N={sn} blobs (d={d}, kNN={knn}, k={k}, cs={cs}) per step, measured; "
+              f"stages {{{', '.join(f'{a}: {b:.3f}' for a, b in stages.items())}}} s")
     line = {
-        "metric": METRIC, "value": est, "unit": "s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": est * 1e3, "higher_is_better": False, "scaling": "strong",
+        "metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.workload}: blobs N={n} d={d} kNN={knn} k={k} (BASELINE.json configs[1])"},
+        "config": {"workload": f"{args.workload}-sample: blobs N={sn} d={d} kNN={knn} k={k} cs={cs} "
+                               f"(bounded sample of {CONFIG_NOTE[args.workload]}, N={n})",
+                   "same_config": sn == n},
         "impl": "reference",
-        "cpu_baseline": {"value": est, "unit": "s", "cores": cores, "kind": "port", "sample": sample},
-        "e2e": {"value": est, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "cpu_baseline": {"value": v, "unit": "s", "cores": cpu["nproc"], "kind": "port", "sample": sample,
+                         "cpu_model": cpu["model"]},
+        "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "step_times_s": [round(t, 3) for t in times],
+        "run_s": round(run_s, 2),
+        "estimate_full_s": {"value": extrapolate(stages, n, sn), "n": n,
+                            "model": "graph x (N/n)^2, other stages x (N/n); an estimate, not a measurement"},
     }
     print(json.dumps(line), flush=True)
 
@@ -190,7 +220,7 @@ def main():
             dist.barrier()
 
     n, d, knn, k, cs = wl
-    x_host, _ = make_blobs(n, d, k, cs, seed=0)
+    x_host, y_planted = make_blobs(n, d, k, cs, seed=0)
     x_pin = torch.from_numpy(x_host).pin_memory()
     x_dev = x_pin.to("cuda")
     sigma = float(np.sqrt(d))
@@ -216,8 +246,8 @@ def main():
         device_step()
     torch.cuda.synchronize()
 
-    lib.sc_profile_reset()
-    lib.sc_profile_enable(1)
+    # timed steps: no per-kernel profiling events inside the timed region
+    lib.sc_profile_enable(0)
     lib.sc_launch_count_reset()
     times = []
     reports = []
@@ -235,12 +265,24 @@ def main():
     barrier()
     torch.cuda.synchronize()
     launches = int(lib.sc_launch_count())
+
+    # one more step with the library's per-kernel CUDA events on (kernel
+    # breakdown and the roofline's kernel time; not part of `value`)
+    lib.sc_profile_reset()
+    lib.sc_profile_enable(1)
+    prof_steps = 1
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    device_step()
+    e1.record()
+    torch.cuda.synchronize()
+    profiled_step_s = e0.elapsed_time(e1) / 1e3
     lib.sc_profile_enable(0)
 
     def prof(name):
         ms, cnt, work = nat.C.c_double(), nat.C.c_int64(), nat.C.c_double()
         lib.sc_profile_query(name.encode(), nat.C.byref(ms), nat.C.byref(cnt), nat.C.byref(work))
-        return ms.value / max(1, args.steps), cnt.value / max(1, args.steps), work.value / max(1, args.steps)
+        return ms.value / prof_steps, cnt.value / prof_steps, work.value / prof_steps
 
     kernel_classes = ["knn_order", "knn_tile", "knn_recheck", "knn_fallback", "knn_union", "spmv", "reorth", "ritz", "symeig",
                       "embed", "kmeanspp", "kmeans_assign", "kmeans_update", "ncut"]
@@ -295,8 +337,9 @@ def main():
         "metric": METRIC, "value": step_max, "unit": "s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_max * 1e3, "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.workload}: blobs N={n} d={d} kNN={knn} k={k} cs={cs} (BASELINE.json configs[1])",
-                   "inputs": "X resident in HBM (512 MB > L2) between steps", "parallelism":
+        "config": {"workload": f"{args.workload}: blobs N={n} d={d} kNN={knn} k={k} cs={cs} ({CONFIG_NOTE[args.workload]})",
+                   "inputs": f"X resident in HBM ({x_host.nbytes / 1e6:.0f} MB; every stage's working set > L2)",
+                   "parallelism":
                    f"sharded x{world} (query tiles / row blocks / point shards, NCCL)" if sharded else "single-gpu",
                    "nnz": nnz},
         "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(x_host.nbytes),
@@ -309,14 +352,47 @@ def main():
         "kmeans_iters": km_iters,
         "kernels_ms_per_step": {c: round(v[0], 3) for c, v in kstats.items() if v[0] > 0},
         "step_times_s": [round(t, 4) for t in times],
+        "profiled_step_s": round(profiled_step_s, 4),
+        "quality": {"ari_vs_planted": float(sc.adjusted_rand_index(rep.labeling.labels, y_planted)),
+                    "max_eigen_residual": float(np.max(rep.eigen_residuals)),
+                    "lambda_1": float(rep.eigenvalues[0]), "lambda_k": float(rep.eigenvalues[-1]),
+                    "ncut": float(rep.ncut_value)},
         "eigen": {kk: v for kk, v in (dsc.last_info if sharded else __import__(
             "paper_1802_04450_b200.pipeline", fromlist=["x"]).last_info).get("eigen", {}).items() if kk != "history"},
     }
     clk = clocks.summary()
     line["clocks"] = clk
-    if rank == 0 and not args.no_cpu_baseline:
-        est, sample, _ = cpu_reference(n, d, knn, k, cs, args.ref_sample, 1, 0)
-        line["cpu_baseline"] = {"value": est, "unit": "s", "cores": 1, "kind": "port", "sample": sample}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        # measured CPU baseline: the oracle port on the full C1 workload
+        # (BASELINE.json configs[0], the reference's own CPU-runnable case),
+        # and this engine on the same input, so the ratio is measured
+        c1 = WORKLOADS["c1"]
+        cpu_s, cpu_stages, cpu_labels, c1_y = oracle_run(*c1)
+        xc1, _ = make_blobs(*[c1[i] for i in (0, 1, 3, 4)])
+        n1, d1, knn1, k1, _ = c1
+        cfg1 = sc.PipelineConfig(
+            input=sc.PointsInput(measure=sc.SimilarityMeasure.exp_decay(float(np.sqrt(d1))), pattern="knn",
+                                 points=xc1, knn=knn1),
+            k_clusters=k1, eigen=sc.LanczosConfig(k=k1, seed=0), kmeans=sc.KmeansConfig(k=k1, seed=0),
+            normalize_rows=True)
+        sc.run(cfg1)
+        g1 = []
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            rep1 = sc.run(cfg1)
+            torch.cuda.synchronize()
+            g1.append(time.perf_counter() - t0)
+        cpu = host_cpu()
+        line["cpu_baseline"] = {
+            "value": cpu_s, "unit": "s", "cores": cpu["nproc"], "kind": "port", "cpu_model": cpu["model"],
+            "sample": f"c1: oracle run_points on the full BASELINE configs[0] workload (blobs N={n1} d={d1} "
+                      f"kNN={knn1} k={k1}), measured once; stages "
+                      f"{{{', '.join(f'{a}: {b:.2f}' for a, b in cpu_stages.items())}}} s",
+            "gpu_same_workload_s": float(np.median(g1)),
+            "measured_ratio_c1": cpu_s / float(np.median(g1)),
+            "ari_gpu_vs_cpu_labels": float(sc.adjusted_rand_index(rep1.labeling.labels, cpu_labels)),
+        }
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

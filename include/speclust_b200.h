@@ -138,6 +138,11 @@ int sc_gather_rows_f64(int64_t n, int64_t k, const double* src, const int32_t* i
 /* *result (host) = 1 iff A == A^T bit-for-bit (sparse.py:210-222). */
 int sc_csr_is_symmetric(int64_t n, int64_t nnz, const int64_t* row_ptr, const int32_t* col,
                         const double* vals, int* result, sc_stream_t stream);
+/* CSR invariants of a device container (sparse.py:83-142, CsrMatrix checks):
+ * row_ptr from 0 to nnz and non-decreasing, columns in range and strictly
+ * increasing per row, finite values.  SC_ERR_FORMAT names the violation. */
+int sc_csr_validate(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* row_ptr, const int32_t* col,
+                    const double* vals, sc_stream_t stream);
 
 /* ---- stage 1: kNN + exp_decay similarity graph straight into CSR ---------- */
 /* x: (dev) n x d row-major f64.  Outputs (dev): row_ptr[n+1], col/vals with

@@ -1,4 +1,5 @@
 // Error state, launch accounting and kernel timing for the C ABI.
+#include <atomic>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -10,7 +11,7 @@
 namespace sc {
 
 static thread_local std::string g_last_error;
-static int64_t g_launches = 0;
+static std::atomic<int64_t> g_launches{0};
 
 void set_error(const std::string& msg) { g_last_error = msg; }
 int fail(int code, const std::string& msg) {
@@ -21,7 +22,7 @@ int cuda_fail(cudaError_t e, const char* what) {
     g_last_error = std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e);
     return e == cudaErrorMemoryAllocation ? SC_ERR_NO_MEMORY : SC_ERR_CUDA;
 }
-void count_launch(int n) { g_launches += n; }
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 cudaStream_t& tl_stream() {
     static thread_local cudaStream_t s = nullptr;

@@ -603,6 +603,72 @@ int sc_sym_scale_shard_f64(int64_t n_local, int64_t row_offset, const int64_t* r
     return SC_OK;
 }
 
+}  // extern "C"
+
+// CSR container invariants (sparse.py:83-142 CsrMatrix checks) on the device:
+// row_ptr non-decreasing inside [0, nnz], columns in [0, n_cols) and strictly
+// increasing within a row, values finite.  Warp per row; the first violation
+// of each kind is counted (flags[0..3]).
+__global__ void __launch_bounds__(256) csr_validate_kernel(int64_t n, int64_t n_cols, int64_t nnz,
+                                                           const int64_t* __restrict__ row_ptr,
+                                                           const int32_t* __restrict__ col,
+                                                           const double* __restrict__ vals,
+                                                           unsigned long long* __restrict__ flags) {
+    const int lane = threadIdx.x & 31;
+    const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (row >= n) return;
+    const int64_t a = row_ptr[row], b = row_ptr[row + 1];
+    if (a > b || a < 0 || b > nnz) {
+        if (lane == 0) atomicAdd(&flags[0], 1ull);
+        return;
+    }
+    bool bad_range = false, bad_order = false, bad_val = false;
+    for (int64_t e = a + lane; e < b; e += 32) {
+        const int32_t c = col[e];
+        bad_range |= c < 0 || (int64_t)c >= n_cols;
+        bad_order |= e > a && col[e - 1] >= c;
+        bad_val |= !isfinite(vals[e]);
+    }
+    bad_range = __any_sync(0xffffffffu, bad_range);
+    bad_order = __any_sync(0xffffffffu, bad_order);
+    bad_val = __any_sync(0xffffffffu, bad_val);
+    if (lane == 0) {
+        if (bad_range) atomicAdd(&flags[1], 1ull);
+        if (bad_order) atomicAdd(&flags[2], 1ull);
+        if (bad_val) atomicAdd(&flags[3], 1ull);
+    }
+}
+
+extern "C" {
+
+int sc_csr_validate(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* row_ptr, const int32_t* col,
+                    const double* vals, sc_stream_t stream) {
+    if (n_rows < 0 || n_cols < 0 || nnz < 0) return fail(SC_ERR_FORMAT, "negative CSR dimension");
+    if (n_cols > INT32_MAX) return fail(SC_ERR_FORMAT, "device CSR columns must fit int32");
+    cudaStream_t st = as_stream(stream);
+    StreamScope stream_scope(st);
+    int64_t ends[2] = {0, 0};
+    SC_CUDA(cudaMemcpyAsync(&ends[0], row_ptr, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    SC_CUDA(cudaMemcpyAsync(&ends[1], row_ptr + n_rows, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    SC_CUDA(cudaStreamSynchronize(st));
+    if (ends[0] != 0 || ends[1] != nnz) return fail(SC_ERR_FORMAT, "row_ptr must start at 0 and end at nnz");
+    if (n_rows == 0) return SC_OK;
+    DevBuf<unsigned long long> flags;
+    if (int rc = flags.alloc(4)) return rc;
+    SC_CUDA(cudaMemsetAsync(flags.p, 0, 4 * sizeof(unsigned long long), st));
+    csr_validate_kernel<<<(unsigned)ceil_div(n_rows, 8), 256, 0, st>>>(n_rows, n_cols, nnz, row_ptr, col, vals,
+                                                                       flags.p);
+    SC_LAUNCHED(1);
+    unsigned long long h[4];
+    SC_CUDA(cudaMemcpyAsync(h, flags.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+    SC_CUDA(cudaStreamSynchronize(st));
+    if (h[0]) return fail(SC_ERR_FORMAT, "row_ptr must be non-decreasing");
+    if (h[1]) return fail(SC_ERR_FORMAT, "column index out of range");
+    if (h[2]) return fail(SC_ERR_FORMAT, "column indices must strictly increase within rows");
+    if (h[3]) return fail(SC_ERR_FORMAT, "values must be finite");
+    return SC_OK;
+}
+
 int sc_csr_is_symmetric(int64_t n, int64_t nnz, const int64_t* row_ptr, const int32_t* col,
                         const double* vals, int* result, sc_stream_t stream) {
     (void)nnz;

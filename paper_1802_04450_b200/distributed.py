@@ -37,7 +37,8 @@ import numpy as np
 
 from . import _native as nat
 from .eigen import LanczosConfig, default_subspace_dim
-from .errors import BadConfig, Breakdown, EigenNotConverged, IsolatedNode, MaxRestartsExceeded, ZeroVolumePart
+from .errors import (BadConfig, Breakdown, EigenNotConverged, IsolatedNode, MaxRestartsExceeded, NotSymmetric,
+                     ZeroVolumePart)
 from .kmeans import KmeansConfig, Labeling
 from .sparse import DeviceCsr
 
@@ -148,6 +149,11 @@ class CudaOps:
         from .graph import knn_union_device
 
         return knn_union_device(x, knn, measure, sel, perm, r0, r1)
+
+    def is_symmetric(self, w: DeviceCsr) -> bool:
+        from .sparse import is_symmetric
+
+        return is_symmetric(w)
 
     def slice_rows(self, w: DeviceCsr, r0: int, r1: int) -> DeviceCsr:
         rp = w.row_ptr[r0 : r1 + 1]
@@ -683,6 +689,13 @@ def run_sharded(cfg, comm: Comm, ops=None):
         host = m if isinstance(m, CsrMatrix) else coo_to_csr(coo_canonicalize(m))
         w = ops.from_host_csr(host) if hasattr(ops, "from_host_csr") else host.device()
         n = w.n_rows
+        # the reference's _resolve_graph gates (pipeline.py:181-192): exact
+        # symmetry (every rank holds the whole matrix here) and the
+        # negative-weight warning
+        if not ops.is_symmetric(w):
+            raise NotSymmetric("similarity matrix must be symmetric")
+        if host.nnz and host.vals.min() < 0.0:
+            warnings.append("similarity matrix contains negative weights")
         bounds = row_bounds(n, comm.world)
         w_loc = ops.slice_rows(w, bounds[comm.rank], bounds[comm.rank + 1])
         del w

@@ -10,6 +10,7 @@ import numpy as np
 import paper_1802_04450_b200 as sc
 from oracle import speclust_oracle as orc
 from paper_1802_04450_b200.distributed import Comm, lanczos_sharded, row_bounds, run_sharded
+from paper_1802_04450_b200.errors import NotSymmetric
 from tests.np_ops import HostCsr, NumpyOps
 
 
@@ -72,7 +73,27 @@ def graph_worker(rank, world):
     return dict(row_ptr=row_ptr, col=col, vals=vals)
 
 
-WORKERS = {"lanczos": lanczos_worker, "pipeline": pipeline_worker, "graph": graph_worker}
+def matrix_gates_worker(rank, world):
+    """Sharded MatrixInput keeps the reference _resolve_graph gates
+    (pipeline.py:181-192): NotSymmetric for A != A^T, a warning for negative
+    weights."""
+    a, m = random_symmetric(n=60, density=0.2, seed=5)
+    a = np.abs(a) + np.eye(60)
+    a[0, 1] += 0.5  # break symmetry in one entry
+    r, c = np.nonzero(a)
+    bad = sc.coo_to_csr(sc.coo_canonicalize(sc.CooMatrix(60, 60, r, c, a[r, c])))
+    cfg = sc.PipelineConfig(input=sc.MatrixInput(matrix=bad), k_clusters=2, eigen=sc.LanczosConfig(k=2, seed=0),
+                            kmeans=sc.KmeansConfig(k=2, seed=0))
+    raised = 0
+    try:
+        run_sharded(cfg, Comm("cpu"), NumpyOps())
+    except NotSymmetric:
+        raised = 1
+    return dict(raised=np.array(raised))
+
+
+WORKERS = {"lanczos": lanczos_worker, "pipeline": pipeline_worker, "graph": graph_worker,
+           "matrix_gates": matrix_gates_worker}
 
 
 def spawn_entry(rank, world, port, name, out_dir):

@@ -83,6 +83,12 @@ class NumpyOps:
     def from_host_csr(self, m):
         return HostCsr(m.n_rows, m.n_cols, _t(m.row_ptr, torch.int64), _t(m.col_idx, torch.int64), _t(m.vals))
 
+    def is_symmetric(self, w):
+        a = np.zeros((w.n_rows, w.n_cols))
+        rows = np.repeat(np.arange(w.n_rows), np.diff(w.row_ptr.numpy()))
+        a[rows, w.col.numpy()] = w.vals.numpy()
+        return w.n_rows == w.n_cols and np.array_equal(a, a.T)
+
     def slice_rows(self, w, r0, r1):
         rp = w.row_ptr[r0 : r1 + 1]
         b, e = int(rp[0]), int(rp[-1])

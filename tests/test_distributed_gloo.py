@@ -80,6 +80,12 @@ def test_knn_graph_sharded_rows_match_oracle(tmp_path):
         assert np.array_equal(got["vals"], vals)
 
 
+def test_sharded_matrix_input_symmetry_gate(tmp_path):
+    for world in (1, 2):
+        for r in run_world("matrix_gates", world, tmp_path):
+            assert int(r["raised"]) == 1
+
+
 @pytest.mark.parametrize("world", [1, 2, 3])
 def test_row_bounds_partition(world):
     from paper_1802_04450_b200.distributed import row_bounds

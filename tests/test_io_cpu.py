@@ -74,3 +74,59 @@ def test_sbm_config_validation():
     with pytest.raises(sc.errors.BadConfig):
         sc.SbmConfig(block_sizes=(10, 10), p_in=0.1, p_out=0.5)
     assert sc.SbmConfig(block_sizes=[3, 4], p_in=0.5, p_out=0.1).block_sizes == (3, 4)
+
+
+_REF = "/root/reference/pkg/src"
+
+
+@pytest.mark.skipif(not __import__("os").path.isdir(_REF), reason="reference tree not present (build container only)")
+def test_text_io_matches_reference_module(tmp_path):
+    """Byte-identical files and identical parses / error classes against the
+    reference's own io module (io.py:32-134), incl. extreme doubles and
+    malformed inputs."""
+    import importlib
+    import sys
+
+    sys.path.insert(0, _REF)
+    try:
+        rio = importlib.import_module("speclust.io")
+        rsp = importlib.import_module("speclust.sparse")
+    finally:
+        sys.path.remove(_REF)
+    rng = np.random.default_rng(7)
+    vals = np.concatenate([rng.standard_normal(30) * 10.0 ** rng.integers(-300, 300, 30),
+                           [5e-324, -0.0, 1.7976931348623157e308, 0.1, 1e16, 123456789.0]])
+    n = 12
+    rows, cols = rng.integers(0, n, len(vals)), rng.integers(0, n, len(vals))
+    ours = sc.CooMatrix(n, n, rows, cols, vals)
+    theirs = rsp.CooMatrix(n, n, rows, cols, vals)
+    io.save_matrix(tmp_path / "a.txt", ours)
+    rio.save_matrix(tmp_path / "b.txt", theirs)
+    assert (tmp_path / "a.txt").read_bytes() == (tmp_path / "b.txt").read_bytes()
+    got, want = io.load_matrix(tmp_path / "b.txt"), rio.load_matrix(tmp_path / "b.txt")
+    assert np.array_equal(got.rows, want.rows) and np.array_equal(got.cols, want.cols)
+    assert got.vals.tobytes() == want.vals.tobytes()
+    x = vals[:36].reshape(6, 6)
+    io.save_dense(tmp_path / "x1.txt", x)
+    rio.save_dense(tmp_path / "x2.txt", x)
+    assert (tmp_path / "x1.txt").read_bytes() == (tmp_path / "x2.txt").read_bytes()
+    assert io.load_dense(tmp_path / "x2.txt").tobytes() == rio.load_dense(tmp_path / "x2.txt").tobytes()
+    for fn_ours, fn_ref, arr in ((io.save_labels, rio.save_labels, rng.integers(-5, 9, 20)),
+                                 (io.save_edges, rio.save_edges, rng.integers(0, 9, (7, 2)))):
+        fn_ours(tmp_path / "o.txt", arr)
+        fn_ref(tmp_path / "r.txt", arr)
+        assert (tmp_path / "o.txt").read_bytes() == (tmp_path / "r.txt").read_bytes()
+    bad = {"m_short.txt": ("load_matrix", "3 3 2\n0 1 0.5\n"), "m_tok.txt": ("load_matrix", "3 3 1\n0 1\n"),
+           "m_hdr.txt": ("load_matrix", "3 3\n"), "d_row.txt": ("load_dense", "2 2\n1 2\n3\n"),
+           "d_hdr.txt": ("load_dense", "2\n"), "e_bad.txt": ("load_edges", "0 1\n\n2 3 4\n"),
+           "e_empty.txt": ("load_edges", "\n\n"), "l_blank.txt": ("load_labels", "1\n\n2\n")}
+    for name, (fn, text) in bad.items():
+        (tmp_path / name).write_text(text)
+        outs = []
+        for mod in (io, rio):
+            try:
+                r = getattr(mod, fn)(tmp_path / name)
+                outs.append(("ok", np.asarray(getattr(r, "vals", r)).tolist()))
+            except Exception as e:  # noqa: BLE001 - the class name and message are the contract
+                outs.append((type(e).__name__, str(e)))
+        assert outs[0] == outs[1], name
