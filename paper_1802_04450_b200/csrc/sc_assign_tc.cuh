@@ -214,4 +214,198 @@ __global__ void __launch_bounds__(64 + QT * 128, 1)
     }
 }
 
+// Wide embeddings (dp > 256, e.g. C3's d = k = 1000): a 128-row point tile
+// no longer fits shared memory next to a centroid ring, so both operands
+// stream through the ring in 64-column K chunks.  Stage = QT point chunks +
+// one centroid chunk (QT+1 TMA boxes of 128 x 64 fp16); the MMA thread runs
+// the K loop of a centroid tile into one of two TMEM accumulator sets and
+// commits it to the epilogue, which is the same key / (best, second-best)
+// pass as assign_tc_kernel.  The point chunks are re-read (from L2) once per
+// centroid tile; QT point tiles share every centroid chunk.
+template <int STAGES, int QT>
+struct AsKlLayout {
+    static constexpr uint32_t kStageBytes = (QT + 1) * TC_TILE_BYTES;
+    static constexpr uint32_t kStage = QT * 4 * 32 * 16 * 4;
+    static constexpr uint32_t kCn = AS_CN_RING * 128 * 4;
+    static constexpr uint32_t kBar = 8 * (2 * STAGES + 4 + 2 * AS_CN_RING) + 8;
+    static constexpr uint32_t total = 1024 + STAGES * kStageBytes + kStage + kCn + kBar;
+};
+
+template <int STAGES, int QT>
+__global__ void __launch_bounds__(64 + QT * 128, 1)
+    assign_tc_kl_kernel(const __grid_constant__ CUtensorMap vmap, const __grid_constant__ CUtensorMap cmap, int64_t n,
+                        int64_t nptiles, int64_t nctiles, int nkb, const float* __restrict__ cnk, float key_scale,
+                        int32_t* __restrict__ best_idx, float2* __restrict__ best_keys) {
+    using Lay = AsKlLayout<STAGES, QT>;
+    constexpr int NEPI = 4 * QT;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sRing = base;
+    float* sStage = reinterpret_cast<float*>(sRing + STAGES * Lay::kStageBytes);
+    float* sCn = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(sStage) + Lay::kStage);
+    uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sCn) + Lay::kCn);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint64_t* cfull = tempty + 2;
+    uint64_t* cempty = cfull + AS_CN_RING;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cempty + AS_CN_RING);
+    constexpr uint32_t kTmemCols = QT * 256;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t pt0 = (int64_t)blockIdx.x * QT;
+    const int nq = (int)(nptiles - pt0 < QT ? nptiles - pt0 : QT);  // point tiles this CTA owns
+
+    if (warp == 0 && lane == 0) {
+        tc::tma_prefetch(&vmap);
+        tc::tma_prefetch(&cmap);
+    }
+    if (warp == 1) {
+        if (lane == 0) {
+            for (int s = 0; s < STAGES; ++s) {
+                tc::mbar_init(&full[s], 1);
+                tc::mbar_init(&empty[s], 1);
+            }
+            for (int b = 0; b < 2; ++b) {
+                tc::mbar_init(&tfull[b], 1);
+                tc::mbar_init(&tempty[b], NEPI);
+            }
+            for (int c = 0; c < AS_CN_RING; ++c) {
+                tc::mbar_init(&cfull[c], 1);
+                tc::mbar_init(&cempty[c], NEPI);
+            }
+            tc::fence_mbar_init();
+        }
+        __syncwarp();
+        tc::tmem_alloc(tmem_slot, kTmemCols);
+    }
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int64_t it = 0;
+            for (int64_t t = 0; t < nctiles; ++t) {
+                const int c = (int)(t % AS_CN_RING);
+                mbar_wait_hw<true>(&cempty[c], (uint32_t)(((t / AS_CN_RING) & 1) ^ 1));
+                tc::mbar_expect_tx(&cfull[c], 128 * 4);
+                tc::bulk_g2s(sCn + c * 128, cnk + t * 128, 128 * 4, &cfull[c]);
+                for (int kb = 0; kb < nkb; ++kb, ++it) {
+                    const int s = (int)(it % STAGES);
+                    mbar_wait_hw<true>(&empty[s], (uint32_t)(((it / STAGES) & 1) ^ 1));
+                    uint8_t* st = sRing + s * Lay::kStageBytes;
+                    tc::mbar_expect_tx(&full[s], (uint32_t)(nq + 1) * TC_TILE_BYTES);
+                    for (int q = 0; q < nq; ++q)
+                        tc::tma_load_2d(st + q * TC_TILE_BYTES, &vmap, &full[s], kb * 64, (int)((pt0 + q) * 128));
+                    tc::tma_load_2d(st + QT * TC_TILE_BYTES, &cmap, &full[s], kb * 64, (int)(t * 128));
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = tc::idesc_f16_f32(128, 128);
+            int64_t it = 0;
+            for (int64_t t = 0; t < nctiles; ++t) {
+                const int buf = (int)(t & 1);
+                mbar_wait_hw<true>(&tempty[buf], (uint32_t)(((t >> 1) & 1) ^ 1));
+                tc::fence_after();
+                for (int kb = 0; kb < nkb; ++kb, ++it) {
+                    const int s = (int)(it % STAGES);
+                    mbar_wait_hw<true>(&full[s], (uint32_t)((it / STAGES) & 1));
+                    tc::fence_after();
+                    uint8_t* st = sRing + s * Lay::kStageBytes;
+                    const uint64_t bd = tc::desc_k_sw128(st + QT * TC_TILE_BYTES);
+#pragma unroll
+                    for (int q = 0; q < QT; ++q) {
+                        if (q >= nq) break;
+                        const uint64_t ad = tc::desc_k_sw128(st + q * TC_TILE_BYTES);
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            tc::umma_f16(tmem + buf * (QT * 128) + q * 128, ad + 2 * k, bd + 2 * k, idesc,
+                                         (kb | k) != 0);
+                    }
+                    tc::umma_commit(&empty[s]);
+                }
+                tc::umma_commit(&tfull[buf]);
+            }
+        }
+    } else {
+        const int quad = warp & 3;
+        const int qi = (warp - 2) >> 2;
+        const int64_t row = (pt0 + qi) * 128 + quad * 32 + lane;
+        const bool valid = qi < nq && row < n;
+        float* stage = sStage + ((size_t)(warp - 2) * 32 + lane) * 16;
+        float b1 = INFINITY, b2 = INFINITY;
+        int32_t i1 = -1;
+        const float2 ks = make_float2(key_scale, key_scale);
+        for (int64_t t = 0; t < nctiles; ++t) {
+            const int buf = (int)(t & 1);
+            const int cslot = (int)(t % AS_CN_RING);
+            mbar_wait_hw<true>(&cfull[cslot], (uint32_t)((t / AS_CN_RING) & 1));
+            mbar_wait_hw<true>(&tfull[buf], (uint32_t)((t >> 1) & 1));
+            tc::fence_after();
+            const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * (QT * 128) + qi * 128);
+            float v[128];
+            tc::tmem_ld64(taddr, v);
+            tc::tmem_ld64(taddr + 64, v + 64);
+            tc::tmem_wait_ld();
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&tempty[buf]);
+            const uint32_t cn_s = tc::smem_u32(sCn + cslot * 128);
+            float qm[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                float m = INFINITY;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const float4 cn4 = lds_f4(cn_s + (uint32_t)(16 * (4 * q + u)));
+                    float* e = v + 16 * q + 4 * u;
+                    const float2 k01 = ffma2(ks, make_float2(e[0], e[1]), make_float2(cn4.x, cn4.y));
+                    const float2 k23 = ffma2(ks, make_float2(e[2], e[3]), make_float2(cn4.z, cn4.w));
+                    e[0] = k01.x;
+                    e[1] = k01.y;
+                    e[2] = k23.x;
+                    e[3] = k23.y;
+                    m = fmin3(m, fmin3(k01.x, k01.y, k23.x), k23.y);
+                }
+                qm[q] = m;
+            }
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&cempty[cslot]);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                if (!(valid && qm[q] < b2)) continue;
+                float4* st4 = reinterpret_cast<float4*>(stage);
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    st4[u] = make_float4(v[16 * q + 4 * u], v[16 * q + 4 * u + 1], v[16 * q + 4 * u + 2],
+                                         v[16 * q + 4 * u + 3]);
+                const int32_t cb = (int32_t)(t * 128 + q * 16);
+#pragma unroll 1
+                for (int u = 0; u < 16; ++u) {
+                    const float k = stage[u];
+                    if (k < b1) {
+                        b2 = b1;
+                        b1 = k;
+                        i1 = cb + u;
+                    } else if (k < b2) {
+                        b2 = k;
+                    }
+                }
+            }
+        }
+        if (valid) {
+            best_idx[row] = i1;
+            best_keys[row] = make_float2(b1, b2);
+        }
+    }
+    __syncthreads();
+    if (warp == 1) {
+        tc::fence_after();
+        tc::tmem_dealloc(tmem, kTmemCols);
+    }
+}
+
 }  // namespace sc

@@ -36,11 +36,24 @@ void ensure_pool() {
     cudaGetDevice(&dev);
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;  // keep freed blocks cached in the pool
+        // keep up to 2 GiB of freed blocks cached for the many small
+        // per-call buffers; anything above is returned at the next
+        // synchronisation, so multi-GB stage buffers (Krylov basis,
+        // candidate lists) do not stay reserved against PyTorch's allocator
+        uint64_t thr = 2ull << 30;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
     (void)cudaGetLastError();
     done = true;
+}
+
+void trim_pool() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceSynchronize();
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+    (void)cudaGetLastError();
 }
 
 // ---- profiling ---------------------------------------------------------------

@@ -57,6 +57,7 @@ struct ProfMute {
 // Entry points set the thread's working stream with StreamScope.
 cudaStream_t& tl_stream();
 void ensure_pool();
+void trim_pool();
 struct StreamScope {
     cudaStream_t prev;
     explicit StreamScope(cudaStream_t s) : prev(tl_stream()) { tl_stream() = s; }
@@ -75,6 +76,11 @@ struct DevBuf {
         ensure_pool();
         s = tl_stream();
         cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), s);
+        if (e == cudaErrorMemoryAllocation) {  // return the pool's cached blocks, then retry once
+            (void)cudaGetLastError();
+            trim_pool();
+            e = cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), s);
+        }
         if (e != cudaSuccess) {
             p = nullptr;
             n = 0;

@@ -1264,6 +1264,19 @@ static int launch_assign_tc(const CUtensorMap& vmap, const CUtensorMap& cmap, in
     return SC_OK;
 }
 
+template <int STAGES, int QT>
+static int launch_assign_tc_kl(const CUtensorMap& vmap, const CUtensorMap& cmap, int64_t n, int64_t nptiles,
+                               int64_t nctiles, int nkb, const float* cnk, float key_scale, int32_t* best_idx,
+                               float2* best_keys, cudaStream_t st) {
+    const uint32_t smem = AsKlLayout<STAGES, QT>::total;
+    SC_CUDA(cudaFuncSetAttribute(assign_tc_kl_kernel<STAGES, QT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    assign_tc_kl_kernel<STAGES, QT><<<(unsigned)ceil_div(nptiles, QT), 64 + QT * 128, smem, st>>>(
+        vmap, cmap, n, nptiles, nctiles, nkb, cnk, key_scale, best_idx, best_keys);
+    SC_LAUNCHED(1);
+    return SC_OK;
+}
+
 // Per-lloyd-call state of the tensor-core assignment (V converted once).
 struct AssignTc {
     int64_t n = 0, d = 0, dp = 0, n_pad = 0;
@@ -1275,13 +1288,14 @@ struct AssignTc {
     DevBuf<float2> bkeys;
     DevBuf<unsigned long long> scal;  // [0] nflag, [1] cnmax bits, [2] absmax bits
     DevBuf<double> v8;                // the points in 8-column panels (exact costs)
-    // eligible: d <= 256, enough rows to pay for the conversion; SPECLUST_ASSIGN=fp64 disables
+    // eligible: enough rows to pay for the conversion; SPECLUST_ASSIGN=fp64 disables.
+    // dp <= 256: point tiles resident in shared memory; wider: K-chunk ring
     int init(int64_t n_, int64_t d_, int64_t k, const double* v, cudaStream_t st) {
         n = n_;
         d = d_;
         dp = (d + 63) / 64 * 64;
         const char* env = std::getenv("SPECLUST_ASSIGN");
-        active = !(env && std::strcmp(env, "fp64") == 0) && d >= 1 && dp <= 256 && n >= 4096 && k >= 8;
+        active = !(env && std::strcmp(env, "fp64") == 0) && d >= 1 && n >= 4096 && k >= 8;
         if (!active) return SC_OK;
         n_pad = (n + 127) / 128 * 128;
         int rc;
@@ -1331,7 +1345,8 @@ struct AssignTc {
             case 1: rc = launch_assign_tc<1, 4, 2>(vmap, cmap, n, nptiles, nctiles, cnk.p, key_scale, bidx.p, bkeys.p, st); break;
             case 2: rc = launch_assign_tc<2, 3, 2>(vmap, cmap, n, nptiles, nctiles, cnk.p, key_scale, bidx.p, bkeys.p, st); break;
             case 3: rc = launch_assign_tc<3, 2, 2>(vmap, cmap, n, nptiles, nctiles, cnk.p, key_scale, bidx.p, bkeys.p, st); break;
-            default: rc = launch_assign_tc<4, 2, 1>(vmap, cmap, n, nptiles, nctiles, cnk.p, key_scale, bidx.p, bkeys.p, st); break;
+            case 4: rc = launch_assign_tc<4, 2, 1>(vmap, cmap, n, nptiles, nctiles, cnk.p, key_scale, bidx.p, bkeys.p, st); break;
+            default: rc = launch_assign_tc_kl<4, 2>(vmap, cmap, n, nptiles, nctiles, (int)(dp / 64), cnk.p, key_scale, bidx.p, bkeys.p, st); break;
         }
         if (rc) return rc;
         if (!certify) {

@@ -502,6 +502,15 @@ __global__ void copy_cols_kernel(int64_t n, int64_t k, int64_t ld, const double*
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x)
         if ((i % ld) < n) dst[i] = src[i];
 }
+// dst[c * ldd + r] = src[c * lds + r], r < rows, c < k (row chunk of a column-major block)
+__global__ void copy_chunk_cols_kernel(int64_t rows, int64_t k, const double* __restrict__ src, int64_t lds,
+                                       double* __restrict__ dst, int64_t ldd) {
+    const int64_t total = rows * k;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = i / rows, r = i - c * rows;
+        dst[c * ldd + r] = src[c * lds + r];
+    }
+}
 
 // per-block column sums of squares of a row-major n x k matrix
 constexpr int CN_ROWS = 256;
@@ -678,6 +687,7 @@ struct sc_lanczos {
     bool has_pending = false;
 
     DevBuf<double> B, T, w, part, h, sqp, sq0, scal, Y, A, Z, wraw, wsort, S, lastrow, vectors;
+    double* vec_out = nullptr;  // converged Ritz vectors (row-major n x k): `vectors` or a caller buffer
     DevBuf<int> info, nonfinite;
     int64_t nb_t = 0, nb_n = 0;
     int rpb_t = GT_ROWS;  // rows per gemv_t block
@@ -960,10 +970,11 @@ struct sc_lanczos {
         return SC_OK;
     }
     // Y = B[:, :m] S[:, :k]
-    int ritz(double* out, int64_t ldc, int rowmajor) {
-        dim3 grid((unsigned)ceil_div(n, GB_M), (unsigned)ceil_div(k, GB_N));
-        ProfScope prof("ritz", st, 2.0 * (double)n * m * k);
-        dgemm_tall_kernel<<<grid, 256, 0, st>>>(n, (int)m, (int)k, B.p, ld, S.p, m, out, ldc, rowmajor);
+    int ritz(double* out, int64_t ldc, int rowmajor, int64_t r0 = 0, int64_t rows = -1) {
+        if (rows < 0) rows = n;
+        dim3 grid((unsigned)ceil_div(rows, GB_M), (unsigned)ceil_div(k, GB_N));
+        ProfScope prof("ritz", st, 2.0 * (double)rows * m * k);
+        dgemm_tall_kernel<<<grid, 256, 0, st>>>(rows, (int)m, (int)k, B.p + r0, ld, S.p, m, out, ldc, rowmajor);
         SC_LAUNCHED(1);
         return SC_OK;
     }
@@ -1016,8 +1027,12 @@ struct sc_lanczos {
             }
         }
         if (converged && (m == n || verified)) {
-            if ((rc = vectors.alloc((size_t)n * k))) return rc;
-            if ((rc = ritz(vectors.p, k, 1))) return rc;
+            Y.free();
+            if (!vec_out) {
+                if ((rc = vectors.alloc((size_t)n * k))) return rc;
+                vec_out = vectors.p;
+            }
+            if ((rc = ritz(vec_out, k, 1))) return rc;
             if ((rc = normalize_vectors())) return rc;
             state = 1;
             return SC_OK;
@@ -1030,12 +1045,17 @@ struct sc_lanczos {
             return fail(SC_ERR_MAX_RESTARTS, buf);
         }
         ++restarts;
-        if (!Y.p) {
-            if ((rc = Y.alloc((size_t)ld * k))) return rc;
+        // B[:, :k] = B[:, :m] S[:, :k] in place, one row chunk at a time
+        // through a chunk-sized temporary (rows of the product depend only on
+        // the same rows of B), so the restart needs no n x k copy
+        const int64_t chunk = std::min<int64_t>(n, std::max<int64_t>(GB_M, ((int64_t)1 << 28) / (8 * k) / GB_M * GB_M));
+        if (!Y.p && (rc = Y.alloc((size_t)chunk * k))) return rc;
+        for (int64_t r0 = 0; r0 < n; r0 += chunk) {
+            const int64_t rows = std::min<int64_t>(chunk, n - r0);
+            if ((rc = ritz(Y.p, chunk, 0, r0, rows))) return rc;
+            copy_chunk_cols_kernel<<<4 * kNumSMs, 256, 0, st>>>(rows, k, Y.p, chunk, B.p + r0, ld);
+            SC_LAUNCHED(1);
         }
-        if ((rc = ritz(Y.p, ld, 0))) return rc;
-        copy_cols_kernel<<<4 * kNumSMs, 256, 0, st>>>(n, k, ld, Y.p, B.p);
-        SC_LAUNCHED(1);
         const bool coupled = !converged && beta > kBreakdownRtol * std::max(1.0, scale);
         restart_T_kernel<<<1, 1024, 0, st>>>(m, k, wsort.p, S.p, scal.p, coupled ? 1 : 0, T.p);
         SC_LAUNCHED(1);
@@ -1062,9 +1082,9 @@ struct sc_lanczos {
         DevBuf<double> p, nr;
         int rc;
         if ((rc = p.alloc((size_t)nb * k)) || (rc = nr.alloc(k))) return rc;
-        colsq_partial_kernel<<<(unsigned)nb, 256, 0, st>>>(n, k, vectors.p, p.p);
+        colsq_partial_kernel<<<(unsigned)nb, 256, 0, st>>>(n, k, vec_out, p.p);
         colnorm_finish_kernel<<<(unsigned)ceil_div(k, 128), 128, 0, st>>>(nb, k, p.p, nr.p);
-        scale_cols_rowmajor_kernel<<<4 * kNumSMs, 256, 0, st>>>(n, k, nr.p, vectors.p);
+        scale_cols_rowmajor_kernel<<<4 * kNumSMs, 256, 0, st>>>(n, k, nr.p, vec_out);
         SC_LAUNCHED(3);
         SC_CUDA(cudaStreamSynchronize(st));
         return SC_OK;
@@ -1144,7 +1164,7 @@ int sc_lanczos_ritz(const sc_lanczos_t* s, double* values, double* estimates) {
 int sc_lanczos_extract(sc_lanczos_t* s, double* values, double* vectors) {
     if (s->state != 1) return fail(SC_ERR_NOT_CONVERGED, "extract called before convergence");
     for (int64_t i = 0; i < s->k; ++i) values[i] = s->theta_k[i];
-    SC_CUDA(cudaMemcpyAsync(vectors, s->vectors.p, sizeof(double) * s->n * s->k, cudaMemcpyDeviceToDevice, s->st));
+    SC_CUDA(cudaMemcpyAsync(vectors, s->vec_out, sizeof(double) * s->n * s->k, cudaMemcpyDeviceToDevice, s->st));
     SC_CUDA(cudaStreamSynchronize(s->st));
     return SC_OK;
 }
@@ -1157,6 +1177,7 @@ int sc_eigensolve_csr(int64_t n, const int64_t* row_ptr, const int32_t* col, con
     sc_lanczos s;
     int rc = s.init(n, k, m, tol, max_restarts, seed, st);
     if (rc) return rc;
+    s.vec_out = vectors;  // the converged Ritz vectors go straight to the caller's buffer
     int64_t nnz = 0;
     SC_CUDA(cudaMemcpyAsync(&nnz, row_ptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     SC_CUDA(cudaStreamSynchronize(st));
@@ -1184,7 +1205,6 @@ int sc_eigensolve_csr(int64_t n, const int64_t* row_ptr, const int32_t* col, con
         }
     }
     for (int64_t i = 0; i < k; ++i) values[i] = s.theta_k[i];
-    SC_CUDA(cudaMemcpyAsync(vectors, s.vectors.p, sizeof(double) * n * k, cudaMemcpyDeviceToDevice, st));
     // true residuals |A v - theta v| (eigen.py:241-248)
     if ((rc = residuals_launch(n, k, row_ptr, col, vals, vectors, s.wsort.p, residuals, st))) return rc;
     if (stats) sc_lanczos_get_stats(&s, stats);

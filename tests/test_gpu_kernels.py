@@ -549,7 +549,9 @@ def _lloyd_cases():
     rng = np.random.default_rng(23)
     out = []
     for n, d, k, kind in [(20_000, 100, 100, "unit"), (9_000, 16, 10, "unit"), (12_000, 200, 300, "unit"),
-                          (8_192, 64, 50, "raw"), (6_000, 33, 40, "dup")]:
+                          (8_192, 64, 50, "raw"), (6_000, 33, 40, "dup"),
+                          # dp > 256: the K-chunk-streaming kernel (odd tile count: a half-full last CTA)
+                          (4_200, 300, 130, "unit"), (5_000, 520, 64, "dup")]:
         centers = rng.normal(0.0, 1.0, (k, d))
         v = centers[rng.integers(0, k, n)] + 0.3 * rng.standard_normal((n, d))
         if kind == "unit":
