@@ -176,6 +176,69 @@ def run_reference_arm(args, wl):
 
 
 # ---------------------------------------------------------------------------
+def c3_run(torch, sc, nat, run_device, lib):
+    """One full-size C3 clustering (BASELINE.json configs[2]: blobs N=4M,
+    d=128, kNN=32, k=1000, m=2000) on this GPU with X resident in HBM, timed
+    with CUDA events and no profiling; plus one profiled Lloyd assignment at
+    C3's embedding shape for the tensor-core fraction of the assignment GEMM."""
+    from paper_1802_04450_b200 import pipeline as pl
+
+    free, total = torch.cuda.mem_get_info()
+    if total < 150e9:
+        return {"skipped": f"needs ~150 GB of device memory, this GPU has {total / 1e9:.0f} GB"}
+    n, d, knn, k, cs = WORKLOADS["c3"]
+    x, y = make_blobs(n, d, k, cs, seed=0)
+    xd = torch.from_numpy(x).cuda()
+    del x
+    cfg = sc.PipelineConfig(
+        input=sc.PointsInput(measure=sc.SimilarityMeasure.exp_decay(float(np.sqrt(d))), pattern="knn", points=xd,
+                             knn=knn),
+        k_clusters=k, eigen=sc.LanczosConfig(k=k, seed=0), kmeans=sc.KmeansConfig(k=k, seed=0), normalize_rows=True)
+    lib.sc_profile_enable(0)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    rep, w = run_device(cfg)
+    e1.record()
+    torch.cuda.synchronize()
+    secs = e0.elapsed_time(e1) / 1e3
+    out = {"workload": f"c3: blobs N={n} d={d} kNN={knn} k={k} cs={cs} (BASELINE.json configs[2]), X resident",
+           "seconds": secs, "stages_s": {a: round(b, 3) for a, b in rep.timings.items()}, "nnz": w.nnz,
+           "eigen": {a: b for a, b in pl.last_info.get("eigen", {}).items() if a != "history"},
+           "kmeans_iters": rep.labeling.iters_run,
+           "max_eigen_residual": float(np.max(rep.eigen_residuals)),
+           "lambda_1": float(rep.eigenvalues[0]), "lambda_k": float(rep.eigenvalues[-1]),
+           "ari_vs_planted": float(sc.adjusted_rand_index(rep.labeling.labels, y))}
+    del rep, w, xd, cfg
+    nat.load().sc_trim_pool()
+    torch.cuda.empty_cache()
+    # assignment GEMM at C3's embedding shape (n x k unit rows, k centroids)
+    g = torch.Generator(device="cuda").manual_seed(1)
+    cen = torch.randn((k, k), generator=g, device="cuda", dtype=torch.float64)
+    lab = torch.randint(0, k, (n,), generator=g, device="cuda")
+    v = cen[lab] + 0.05 * torch.randn((n, k), generator=g, device="cuda", dtype=torch.float64)
+    v /= v.norm(dim=1, keepdim=True)
+    init = v[torch.randperm(n, generator=g, device="cuda")[:k]].contiguous()
+    del cen, lab
+    km = __import__("paper_1802_04450_b200.kmeans", fromlist=["lloyd_device"])
+    lib.sc_profile_reset()
+    lib.sc_profile_enable(1)
+    km.lloyd_device(v, init, sc.KmeansConfig(k=k, max_iters=2))
+    torch.cuda.synchronize()
+    lib.sc_profile_enable(0)
+    ms, cnt, work = nat.C.c_double(), nat.C.c_int64(), nat.C.c_double()
+    lib.sc_profile_query(b"kmeans_assign", nat.C.byref(ms), nat.C.byref(cnt), nat.C.byref(work))
+    pk = peaks()
+    tf = work.value / (ms.value / 1e3) / 1e12 if ms.value > 0 else None
+    out["assign_gemm"] = {"shape": f"{n} x {k} embedding, {k} centroids", "launches": cnt.value,
+                          "ms_per_launch": ms.value / max(1, cnt.value), "tflops": tf,
+                          "frac_of_bf16_peak": tf / pk["bf16"] if tf else None}
+    del v, init
+    nat.load().sc_trim_pool()
+    torch.cuda.empty_cache()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -186,6 +249,8 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=8000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the public-API end-to-end timing (ncu runs)")
+    ap.add_argument("--no-c3", action="store_true",
+                    help="skip the extra full-size C3 run (BASELINE.json configs[2] on this GPU) reported under 'c3'")
     ap.add_argument("--sharded", action="store_true",
                     help="use the sharded driver (distributed.run_sharded) even at N=1; it is always used for N>1")
     args = ap.parse_args()
@@ -362,6 +427,8 @@ def main():
     }
     clk = clocks.summary()
     line["clocks"] = clk
+    if rank == 0 and world == 1 and not args.no_c3 and args.workload != "c3":
+        line["c3"] = c3_run(torch, sc, nat, run_device, lib)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         # measured CPU baseline: the oracle port on the full C1 workload
         # (BASELINE.json configs[0], the reference's own CPU-runnable case),

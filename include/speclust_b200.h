@@ -71,6 +71,9 @@ typedef struct sc_lanczos sc_lanczos_t;    /* opaque RCI session (library-owned)
 const char* sc_last_error(void);
 int sc_version(void);
 /* number of kernel launches issued by this library since the last reset */
+/* return the library's cached device memory (stream-ordered pool) to the
+ * driver; the pipeline calls it between stages */
+void sc_trim_pool(void);
 int64_t sc_launch_count(void);
 void sc_launch_count_reset(void);
 

@@ -54,6 +54,7 @@ SIGNATURES = {
     "sc_sym_scale_f64": (i32, [i64, vp, vp, vp, vp, vp, vp]),
     "sc_csr_is_symmetric": (i32, [i64, i64, vp, vp, vp, P_int, vp]),
     "sc_csr_validate": (i32, [i64, i64, i64, vp, vp, vp, vp]),
+    "sc_trim_pool": (None, []),
     "sc_csr_permute_f64": (i32, [i64, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "sc_invert_perm": (i32, [i64, vp, vp, vp]),
     "sc_sell_create": (i32, [i64, vp, vp, vp, vp, C.POINTER(vp)]),

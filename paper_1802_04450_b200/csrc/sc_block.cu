@@ -10,59 +10,109 @@
 // four times per Lanczos vector; here every step orthogonalises against a
 // short window of recent vectors and the window is orthogonalised against the
 // older basis once per c vectors, reading it twice per block instead.
+#include <algorithm>
+
 #include "sc_block.cuh"
 
 namespace sc {
 
 namespace {
 
-constexpr int BK_ROWS = 32;  // rows per staged chunk (tn) / columns per chunk (nn)
+constexpr int BK_ROWS = 32;  // rows per staged chunk (tn) / basis columns per chunk (nn)
 constexpr int BK_COLS = 64;  // basis columns per CTA (tn) / rows per CTA (nn)
 constexpr int BK_MAXT = 5;   // N tiles of 8 (c <= 40)
+constexpr int BK_STAGES = 3; // cp.async ring depth
+// shared-memory strides (doubles): a column of 32 rows padded to 36 (tn), a
+// basis column of 64 rows padded to 68 (nn) -- 16-byte aligned and
+// conflict-free for the m8n8k4 fragment loads of a half warp
+constexpr int TN_LDA = 36, NN_LDA = 68;
 
 __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(d[0]), "+d"(d[1])
                  : "d"(a), "d"(b));
 }
+// 16-byte async copy of `bytes` (0, 8 or 16) valid bytes; the rest of the
+// 16 is zero-filled
+__device__ __forceinline__ void cp16n(void* smem, const void* gmem, int bytes) {
+    const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp16(void* smem, const void* gmem, bool pred) { cp16n(smem, gmem, pred ? 16 : 0); }
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
-// partial[g][col][o] = sum_{rows of split g} B[col*ld + r] * V[o*ld + r]
+template <int NT>
+struct TnSmem {
+    static constexpr int kA = BK_COLS * TN_LDA;     // [col][row]
+    static constexpr int kV = NT * 8 * TN_LDA;      // [o][row]
+    static constexpr int kStage = kA + kV;
+    static constexpr size_t bytes = (size_t)BK_STAGES * kStage * sizeof(double);
+};
+
+// partial[g][col][o] = sum_{rows of split g} B[col*ld + r] * V[o*ld + r].
+// CTA = 64 basis columns x one row split; 32-row chunks stream through a
+// BK_STAGES-deep cp.async ring (16-byte copies; ld and the row splits are
+// multiples of 2 rows so every copy is aligned), m8n8k4 DMMA per warp.
 template <int NT>
 __global__ void __launch_bounds__(256) block_tn_kernel(int64_t n, int64_t ld, int nb, const double* __restrict__ B,
                                                        const double* __restrict__ V, int c, int64_t rows_per_split,
                                                        double* __restrict__ part) {
-    __shared__ double As[BK_ROWS][BK_COLS + 1];
-    __shared__ double Vs[BK_ROWS][NT * 8 + 1];
+    using L = TnSmem<NT>;
+    extern __shared__ __align__(16) double tn_smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int col0 = blockIdx.x * BK_COLS;
     const int64_t r_begin = (int64_t)blockIdx.y * rows_per_split;
     const int64_t r_end = imin64(n, r_begin + rows_per_split);
+    const int64_t nchunks = r_end > r_begin ? (r_end - r_begin + BK_ROWS - 1) / BK_ROWS : 0;
+    auto load = [&](int64_t ch, int stage) {
+        double* As = tn_smem + stage * L::kStage;
+        double* Vs = As + L::kA;
+        const int64_t r0 = r_begin + ch * BK_ROWS;
+        // B: 64 columns x 16 pairs of rows
+        for (int e = threadIdx.x; e < BK_COLS * 16; e += 256) {
+            const int cc = e >> 4, pr = (e & 15) * 2;
+            const int col = col0 + cc;
+            const int64_t r = r0 + pr;
+            // a last odd row (r_end = n odd) copies 8 bytes: the padding row
+            // past n is never read
+            const int bytes = (col < nb && r < r_end) ? (r + 1 < r_end ? 16 : 8) : 0;
+            cp16n(As + cc * TN_LDA + pr, bytes ? B + (int64_t)col * ld + r : B, bytes);
+        }
+        for (int e = threadIdx.x; e < NT * 8 * 16; e += 256) {
+            const int o = e >> 4, pr = (e & 15) * 2;
+            const int64_t r = r0 + pr;
+            const int bytes = (o < c && r < r_end) ? (r + 1 < r_end ? 16 : 8) : 0;
+            cp16n(Vs + o * TN_LDA + pr, bytes ? V + (int64_t)o * ld + r : V, bytes);
+        }
+    };
     double acc[NT][2];
 #pragma unroll
     for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
-    const int lr = threadIdx.x & 31, lc = threadIdx.x >> 5;  // loader: row, column group
-    for (int64_t r0 = r_begin; r0 < r_end; r0 += BK_ROWS) {
-        const int64_t r = r0 + lr;
-        const bool rok = r < r_end;
 #pragma unroll
-        for (int i = 0; i < BK_COLS / 8; ++i) {
-            const int cc = lc + 8 * i;
-            const int col = col0 + cc;
-            As[lr][cc] = (rok && col < nb) ? __ldg(B + (int64_t)col * ld + r) : 0.0;
-        }
-        for (int o = lc; o < NT * 8; o += 8) Vs[lr][o] = (rok && o < c) ? __ldg(V + (int64_t)o * ld + r) : 0.0;
+    for (int s = 0; s < BK_STAGES - 1; ++s) {
+        if (s < nchunks) load(s, s);
+        cp_commit();
+    }
+    for (int64_t ch = 0; ch < nchunks; ++ch) {
+        cp_wait<BK_STAGES - 2>();
         __syncthreads();
+        // refill the stage consumed in the previous iteration
+        if (ch + BK_STAGES - 1 < nchunks) load(ch + BK_STAGES - 1, (int)((ch + BK_STAGES - 1) % BK_STAGES));
+        cp_commit();
+        const double* As = tn_smem + (ch % BK_STAGES) * L::kStage;
+        const double* Vs = As + L::kA;
+        const double* ap = As + (warp * 8 + (lane >> 2)) * TN_LDA + (lane & 3);
+        const double* bp = Vs + (lane >> 2) * TN_LDA + (lane & 3);
 #pragma unroll
         for (int k4 = 0; k4 < BK_ROWS; k4 += 4) {
-            const double a = As[k4 + (lane & 3)][warp * 8 + (lane >> 2)];
+            const double a = ap[k4];
 #pragma unroll
-            for (int t = 0; t < NT; ++t) {
-                const double b = Vs[k4 + (lane & 3)][t * 8 + (lane >> 2)];
-                dmma884(acc[t], a, b);
-            }
+            for (int t = 0; t < NT; ++t) dmma884(acc[t], a, bp[t * 8 * TN_LDA + k4]);
         }
-        __syncthreads();
     }
+    cp_wait<0>();
     const int col = col0 + warp * 8 + (lane >> 2);
     if (col < nb) {
         double* p = part + ((int64_t)blockIdx.y * nb + col) * (NT * 8);
@@ -91,43 +141,85 @@ __global__ void block_reduce_kernel(int nsplit, int nb, int c, int ldp, const do
     }
 }
 
-// V[o*ld + r] -= sum_col B[col*ld + r] * H[col][o], rows of this CTA
+template <int NT>
+struct NnSmem {
+    static constexpr int kHs = NT * 8 + 4;           // H row stride (doubles)
+    static constexpr int kA = BK_ROWS * NN_LDA;      // [basis col][row]
+    static constexpr int kH = BK_ROWS * kHs;         // [basis col][o]
+    static constexpr int kStage = kA + kH;
+    static constexpr size_t bytes = (size_t)BK_STAGES * kStage * sizeof(double);
+};
+
+// V[o*ld + r] -= sum_col B[col*ld + r] * H[col][o] for the 64 rows of this CTA;
+// 32 basis columns per chunk through the cp.async ring (B rows and the H
+// chunk), m8n8k4 DMMA with the rows as M
 template <int NT>
 __global__ void __launch_bounds__(256) block_nn_kernel(int64_t n, int64_t ld, int nb, const double* __restrict__ B,
                                                        const double* __restrict__ H, int c, double* __restrict__ V) {
-    __shared__ double As[BK_ROWS][BK_COLS + 1];  // [k = basis column][row]
-    __shared__ double Hs[BK_ROWS][NT * 8 + 1];
+    using L = NnSmem<NT>;
+    extern __shared__ __align__(16) double nn_smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t row0 = (int64_t)blockIdx.x * BK_COLS;
+    const int nchunks = (nb + BK_ROWS - 1) / BK_ROWS;
+    const bool hvec = (c & 1) == 0;  // H rows 16-byte aligned: pairwise copies
+    auto load = [&](int ch, int stage) {
+        double* As = nn_smem + stage * L::kStage;
+        double* Hs = As + L::kA;
+        const int k0 = ch * BK_ROWS;
+        for (int e = threadIdx.x; e < BK_ROWS * 32; e += 256) {
+            const int kk = e >> 5, pr = (e & 31) * 2;
+            const int k = k0 + kk;
+            const int64_t r = row0 + pr;
+            const bool ok = k < nb && r < n;
+            cp16(As + kk * NN_LDA + pr, ok ? B + (int64_t)k * ld + r : B, ok);
+        }
+        if (hvec) {
+            const int pairs = c / 2;
+            for (int e = threadIdx.x; e < BK_ROWS * pairs; e += 256) {
+                const int kk = e / pairs, o = (e % pairs) * 2;
+                const int k = k0 + kk;
+                cp16(Hs + kk * L::kHs + o, k < nb ? H + (int64_t)k * c + o : H, k < nb);
+            }
+        } else {
+            for (int e = threadIdx.x; e < BK_ROWS * c; e += 256) {
+                const int kk = e / c, o = e % c;
+                const int k = k0 + kk;
+                Hs[kk * L::kHs + o] = k < nb ? H[(int64_t)k * c + o] : 0.0;
+            }
+        }
+    };
+    // columns o >= c of the staged H chunk are never written by the loads:
+    // zero them once in every stage
+    for (int e = threadIdx.x; e < BK_STAGES * BK_ROWS * (NT * 8 - c); e += 256) {
+        const int s = e / (BK_ROWS * (NT * 8 - c)), rem = e % (BK_ROWS * (NT * 8 - c));
+        const int kk = rem / (NT * 8 - c), o = c + rem % (NT * 8 - c);
+        nn_smem[s * L::kStage + L::kA + kk * L::kHs + o] = 0.0;
+    }
     double acc[NT][2];
 #pragma unroll
     for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
-    const int lrow = threadIdx.x & 63, lk = threadIdx.x >> 6;  // loader: row, column group (4)
-    for (int k0 = 0; k0 < nb; k0 += BK_ROWS) {
-        const int64_t r = row0 + lrow;
 #pragma unroll
-        for (int i = 0; i < BK_ROWS / 4; ++i) {
-            const int kk = lk + 4 * i;
-            const int k = k0 + kk;
-            As[kk][lrow] = (r < n && k < nb) ? __ldg(B + (int64_t)k * ld + r) : 0.0;
-        }
-        for (int e = threadIdx.x; e < BK_ROWS * NT * 8; e += 256) {
-            const int kk = e / (NT * 8), o = e % (NT * 8);
-            const int k = k0 + kk;
-            Hs[kk][o] = (k < nb && o < c) ? H[(int64_t)k * c + o] : 0.0;
-        }
+    for (int s = 0; s < BK_STAGES - 1; ++s) {
+        if (s < nchunks) load(s, s);
+        cp_commit();
+    }
+    for (int ch = 0; ch < nchunks; ++ch) {
+        cp_wait<BK_STAGES - 2>();
         __syncthreads();
+        if (ch + BK_STAGES - 1 < nchunks) load(ch + BK_STAGES - 1, (ch + BK_STAGES - 1) % BK_STAGES);
+        cp_commit();
+        const double* As = nn_smem + (ch % BK_STAGES) * L::kStage;
+        const double* Hs = As + L::kA;
+        const double* ap = As + (lane & 3) * NN_LDA + warp * 8 + (lane >> 2);
+        const double* bp = Hs + (lane & 3) * L::kHs + (lane >> 2);
 #pragma unroll
         for (int k4 = 0; k4 < BK_ROWS; k4 += 4) {
-            const double a = As[k4 + (lane & 3)][warp * 8 + (lane >> 2)];
+            const double a = ap[k4 * NN_LDA];
 #pragma unroll
-            for (int t = 0; t < NT; ++t) {
-                const double b = Hs[k4 + (lane & 3)][t * 8 + (lane >> 2)];
-                dmma884(acc[t], a, b);
-            }
+            for (int t = 0; t < NT; ++t) dmma884(acc[t], a, bp[k4 * L::kHs + t * 8]);
         }
-        __syncthreads();
     }
+    cp_wait<0>();
     const int64_t r = row0 + warp * 8 + (lane >> 2);
     if (r < n) {
 #pragma unroll
@@ -141,43 +233,68 @@ __global__ void __launch_bounds__(256) block_nn_kernel(int64_t n, int64_t ld, in
     }
 }
 
+int resident_ctas(const void* fn, size_t smem) {
+    int bps = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, fn, 256, smem);
+    int dev = 0, nsm = kNumSMs;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    return std::max(1, bps) * nsm;
+}
+
 template <int NT>
-void launch_tn(dim3 g, int64_t n, int64_t ld, int nb, const double* B, const double* V, int c, int64_t rps,
-               double* part, cudaStream_t st) {
-    block_tn_kernel<NT><<<g, 256, 0, st>>>(n, ld, nb, B, V, c, rps, part);
+int launch_tn(int64_t n, int64_t ld, int nb, const double* B, const double* V, int c, int* nsplit, double* part,
+              cudaStream_t st, bool query_only = false) {
+    const size_t smem = TnSmem<NT>::bytes;
+    static int slots = 0;
+    if (!slots) {
+        cudaFuncSetAttribute(block_tn_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        slots = resident_ctas((const void*)block_tn_kernel<NT>, smem);
+    }
+    // one wave: column tiles x row splits <= resident CTAs, splits of >= 2K rows
+    const int cb = (nb + BK_COLS - 1) / BK_COLS;
+    int64_t g = std::max<int64_t>(1, slots / cb);
+    g = std::min<int64_t>(g, std::max<int64_t>(1, ceil_div(n, 2048)));
+    const int64_t rps = ceil_div(ceil_div(n, g), BK_ROWS) * BK_ROWS;
+    *nsplit = (int)ceil_div(n, rps);
+    if (query_only) return SC_OK;
+    dim3 grid((unsigned)cb, (unsigned)*nsplit);
+    block_tn_kernel<NT><<<grid, 256, smem, st>>>(n, ld, nb, B, V, c, rps, part);
+    return SC_OK;
 }
 template <int NT>
-void launch_nn(unsigned g, int64_t n, int64_t ld, int nb, const double* B, const double* H, int c, double* V,
-               cudaStream_t st) {
-    block_nn_kernel<NT><<<g, 256, 0, st>>>(n, ld, nb, B, H, c, V);
+void launch_nn(int64_t n, int64_t ld, int nb, const double* B, const double* H, int c, double* V, cudaStream_t st) {
+    const size_t smem = NnSmem<NT>::bytes;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(block_nn_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    block_nn_kernel<NT><<<(unsigned)ceil_div(n, BK_COLS), 256, smem, st>>>(n, ld, nb, B, H, c, V);
+}
+
+int tn_dispatch(int nt, int64_t n, int64_t ld, int nb, const double* B, const double* V, int c, int* nsplit,
+                double* part, cudaStream_t st, bool query_only) {
+    switch (nt) {
+        case 1: return launch_tn<1>(n, ld, nb, B, V, c, nsplit, part, st, query_only);
+        case 2: return launch_tn<2>(n, ld, nb, B, V, c, nsplit, part, st, query_only);
+        case 3: return launch_tn<3>(n, ld, nb, B, V, c, nsplit, part, st, query_only);
+        case 4: return launch_tn<4>(n, ld, nb, B, V, c, nsplit, part, st, query_only);
+        default: return launch_tn<5>(n, ld, nb, B, V, c, nsplit, part, st, query_only);
+    }
 }
 
 }  // namespace
-
-int block_tn_splits(int64_t n, int nb) {
-    const int64_t cb = ceil_div(nb, BK_COLS);
-    // about four waves of 256-thread CTAs, each split at least 4K rows
-    int64_t g = ceil_div(4 * 2 * kNumSMs, cb);
-    g = std::max<int64_t>(1, std::min<int64_t>(g, ceil_div(n, 4096)));
-    return (int)g;
-}
 
 int block_tn(int64_t n, int64_t ld, int nb, const double* B, const double* V, int c, double* H, double* part,
              unsigned long long* maxabs, cudaStream_t st) {
     if (c < 1 || c > BK_MAXT * 8) return fail(SC_ERR_VALUE, "block width must be in [1, 40]");
     if (nb <= 0) return SC_OK;
+    if ((ld & 1) || (reinterpret_cast<uintptr_t>(B) & 15) || (reinterpret_cast<uintptr_t>(V) & 15))
+        return fail(SC_ERR_VALUE, "block GEMMs need 16-byte aligned columns (even ld)");
     const int nt = (c + 7) / 8;
-    const int g = block_tn_splits(n, nb);
-    const int64_t rps = ceil_div(ceil_div(n, g), BK_ROWS) * BK_ROWS;
-    const int gs = (int)ceil_div(n, rps);
-    dim3 grid((unsigned)ceil_div(nb, BK_COLS), (unsigned)gs);
-    switch (nt) {
-        case 1: launch_tn<1>(grid, n, ld, nb, B, V, c, rps, part, st); break;
-        case 2: launch_tn<2>(grid, n, ld, nb, B, V, c, rps, part, st); break;
-        case 3: launch_tn<3>(grid, n, ld, nb, B, V, c, rps, part, st); break;
-        case 4: launch_tn<4>(grid, n, ld, nb, B, V, c, rps, part, st); break;
-        default: launch_tn<5>(grid, n, ld, nb, B, V, c, rps, part, st); break;
-    }
+    int gs = 0;
+    tn_dispatch(nt, n, ld, nb, B, V, c, &gs, part, st, false);
     const int64_t tot = (int64_t)nb * c;
     block_reduce_kernel<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(gs, nb, c, nt * 8, part, H, maxabs);
     SC_LAUNCHED(2);
@@ -187,14 +304,14 @@ int block_tn(int64_t n, int64_t ld, int nb, const double* B, const double* V, in
 int block_nn(int64_t n, int64_t ld, int nb, const double* B, const double* H, int c, double* V, cudaStream_t st) {
     if (c < 1 || c > BK_MAXT * 8) return fail(SC_ERR_VALUE, "block width must be in [1, 40]");
     if (nb <= 0) return SC_OK;
-    const int nt = (c + 7) / 8;
-    const unsigned g = (unsigned)ceil_div(n, BK_COLS);
-    switch (nt) {
-        case 1: launch_nn<1>(g, n, ld, nb, B, H, c, V, st); break;
-        case 2: launch_nn<2>(g, n, ld, nb, B, H, c, V, st); break;
-        case 3: launch_nn<3>(g, n, ld, nb, B, H, c, V, st); break;
-        case 4: launch_nn<4>(g, n, ld, nb, B, H, c, V, st); break;
-        default: launch_nn<5>(g, n, ld, nb, B, H, c, V, st); break;
+    if ((ld & 1) || (reinterpret_cast<uintptr_t>(B) & 15) || (reinterpret_cast<uintptr_t>(H) & 15))
+        return fail(SC_ERR_VALUE, "block GEMMs need 16-byte aligned columns (even ld)");
+    switch ((c + 7) / 8) {
+        case 1: launch_nn<1>(n, ld, nb, B, H, c, V, st); break;
+        case 2: launch_nn<2>(n, ld, nb, B, H, c, V, st); break;
+        case 3: launch_nn<3>(n, ld, nb, B, H, c, V, st); break;
+        case 4: launch_nn<4>(n, ld, nb, B, H, c, V, st); break;
+        default: launch_nn<5>(n, ld, nb, B, H, c, V, st); break;
     }
     SC_LAUNCHED(1);
     return SC_OK;
@@ -202,7 +319,9 @@ int block_nn(int64_t n, int64_t ld, int nb, const double* B, const double* H, in
 
 size_t block_part_size(int64_t n, int nb, int c) {
     const int nt = (c + 7) / 8;
-    return (size_t)block_tn_splits(n, nb) * (size_t)nb * (size_t)(nt * 8);
+    int gs = 0;
+    tn_dispatch(nt, n, 0, nb, nullptr, nullptr, c, &gs, nullptr, nullptr, true);
+    return (size_t)gs * (size_t)nb * (size_t)(nt * 8);
 }
 
 }  // namespace sc

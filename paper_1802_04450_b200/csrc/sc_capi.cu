@@ -36,11 +36,12 @@ void ensure_pool() {
     cudaGetDevice(&dev);
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        // keep up to 2 GiB of freed blocks cached for the many small
-        // per-call buffers; anything above is returned at the next
-        // synchronisation, so multi-GB stage buffers (Krylov basis,
-        // candidate lists) do not stay reserved against PyTorch's allocator
-        uint64_t thr = 2ull << 30;
+        // keep freed blocks cached (per-step temporaries must not re-map
+        // memory after every synchronisation); the pipeline returns the
+        // cache to the driver between stages with sc_trim_pool(), so the
+        // multi-GB stage buffers (candidate lists, Krylov basis) do not stay
+        // reserved against PyTorch's allocator
+        uint64_t thr = UINT64_MAX;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
     (void)cudaGetLastError();
@@ -119,6 +120,7 @@ extern "C" {
 const char* sc_last_error(void) { return g_last_error.c_str(); }
 int sc_version(void) { return 100; }
 int64_t sc_launch_count(void) { return g_launches; }
+void sc_trim_pool(void) { trim_pool(); }
 void sc_launch_count_reset(void) { g_launches = 0; }
 
 void sc_profile_enable(int on) { g_prof = on != 0; }

@@ -13,6 +13,8 @@
 #include <cstring>
 #include <vector>
 
+#include <cuda_fp16.h>
+
 #include "sc_common.cuh"
 #include "sc_sparse.cuh"
 
@@ -478,6 +480,31 @@ __global__ void to_panels_kernel(int64_t n, int64_t d, const double* __restrict_
     v8[e] = c < d ? v[i * d + c] : 0.0;
 }
 
+// fp16 copy of s * v in 8-column panels (panel p of row i at p * n + i)
+__global__ void to_half_panels_kernel(int64_t n, int64_t d, const double* __restrict__ v, double s,
+                                      uint4* __restrict__ vh8) {
+    const int64_t nch = (d + 7) / 8;
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= nch * n) return;
+    const int64_t p = e / n, i = e - p * n;
+    __align__(16) __half h[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const int64_t c = 8 * p + q;
+        h[q] = __double2half(c < d ? s * v[i * d + c] : 0.0);
+    }
+    vh8[e] = *reinterpret_cast<const uint4*>(h);
+}
+
+// |v_i| (plain fp64; used only inside error bounds)
+__global__ void rownorm_sqrt_kernel(int64_t n, int64_t d, const double* __restrict__ v, double* __restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double a = 0.0;
+    for (int64_t l = 0; l < d; ++l) a = fma(v[i * d + l], v[i * d + l], a);
+    out[i] = sqrt(a);
+}
+
 constexpr int KPP_UPD_ROWS = 128, KPP_UPD_COLS = 32;
 
 __device__ __forceinline__ void kpp_block_partials(double w, int64_t cnt, double* sw, int64_t* scn,
@@ -595,6 +622,39 @@ __global__ void kpp_centre_dist_kernel(int64_t d, int t, const double* __restric
 // nearest centre c_a = ctr[i] has |c_t - c_a|^2 > 4 d2 (1 + 1e-6) is skipped
 // unread: |x - c_t| >= |c_t - c_a| - |x - c_a| > |x - c_a| (the margin is
 // far above the rounding of the computed squares), so min(d2, dist) = d2.
+// fp16 screen of the k-means++ update (optional): the points as 8-column
+// fp16 panels of s * v, the new centre likewise (scaled, in shared memory),
+// fp64 row norms and |c|.  A row whose certified lower bound on |v - c|^2
+// exceeds its current d2 cannot change (min(d2, dist) = d2) and is not read
+// in fp64; the rest go through the exact numpy-order path unchanged.
+struct KppScreen {
+    const uint4* vh8 = nullptr;    // [ceil(d/8)][n] x 8 halves
+    const __half* ch = nullptr;    // ceil(d/8) * 8 halves (device)
+    const double* vnorm = nullptr; // |v_i|
+    const double* cnorm = nullptr; // |c| (device scalar)
+    double s = 1.0;
+};
+
+__global__ void kpp_centre_half_kernel(int64_t d, const double* __restrict__ row, double s, __half* __restrict__ ch,
+                                       double* __restrict__ cnorm) {
+    __shared__ double part[32];
+    double a = 0.0;
+    const int64_t dp = (d + 7) / 8 * 8;
+    for (int64_t l = threadIdx.x; l < dp; l += blockDim.x) {
+        const double x = l < d ? row[l] : 0.0;
+        ch[l] = __double2half(s * x);
+        a = fma(x, x, a);
+    }
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = a;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += part[w];
+        cnorm[0] = sqrt(t);
+    }
+}
+
 __global__ void __launch_bounds__(KPP_UPD_ROWS) kpp_update_panel_kernel(int64_t n, int64_t d,
                                                                         const double* __restrict__ v8,
                                                                         const double* __restrict__ prow, int64_t pick,
@@ -603,16 +663,49 @@ __global__ void __launch_bounds__(KPP_UPD_ROWS) kpp_update_panel_kernel(int64_t 
                                                                         double* __restrict__ pw,
                                                                         int64_t* __restrict__ pc,
                                                                         const double* __restrict__ cc,
-                                                                        int32_t* __restrict__ ctr, int t) {
+                                                                        int32_t* __restrict__ ctr, int t,
+                                                                        KppScreen scr) {
     __shared__ double sw[KPP_UPD_ROWS / 32];
     __shared__ int64_t scn[KPP_UPD_ROWS / 32];
+    extern __shared__ __align__(16) __half kpp_ch[];
     const int64_t i = (int64_t)blockIdx.x * KPP_UPD_ROWS + threadIdx.x;
+    const int64_t nch = (d + 7) / 8;
+    if (scr.vh8) {
+        for (int64_t l = threadIdx.x; l < nch * 8; l += blockDim.x) kpp_ch[l] = scr.ch[l];
+        __syncthreads();
+    }
     NpDot acc;
     bool pruned = false;
     double old = 0.0;
     if (i < n) {
         if (!first) old = d2[i];
         if (!first && cc && cc[ctr[i]] > 4.0 * old * (1.0 + 1e-6)) pruned = true;
+        if (!first && !pruned && scr.vh8) {
+            // f = |fp16(s v) - fp16(s c)|^2 in fp32; per element the fp16
+            // rounding moves each difference by <= 2^-11 (|s v_l| + |s c_l|)
+            // + 2^-24 (subnormals), so |s(v - c)| >= sqrt(f) - |Delta| with
+            // |Delta| <= 2^-11 s (|v| + |c|) + 2^-24 sqrt(d) (triangle
+            // inequality in l2); fp32 rounding of the d-term sum is covered
+            // by shrinking f by (d + 8) 2^-23
+            float f = 0.0f;
+            const uint4* src = scr.vh8 + i;
+            for (int64_t p = 0; p < nch; ++p) {
+                const uint4 raw = __ldg(src + p * n);
+                const __half2* hv = reinterpret_cast<const __half2*>(&raw);
+                const __half2* hc = reinterpret_cast<const __half2*>(kpp_ch + 8 * p);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float2 a = __half22float2(hv[q]), b = __half22float2(hc[q]);
+                    const float dx = a.x - b.x, dy = a.y - b.y;
+                    f = fmaf(dx, dx, f);
+                    f = fmaf(dy, dy, f);
+                }
+            }
+            const double delta = 0x1p-11 * scr.s * (scr.vnorm[i] + scr.cnorm[0]) + 0x1p-24 * sqrt((double)d);
+            const double rf = sqrt(fmax(0.0, (double)f * (1.0 - (double)(d + 8) * 0x1p-23)));
+            const double lb = rf - delta;
+            if (lb > 0.0 && lb * lb > old * scr.s * scr.s * (1.0 + 1e-9)) pruned = true;
+        }
         for (int64_t c0 = 0; c0 < d && !pruned; c0 += 8) {
             const double2* src = reinterpret_cast<const double2*>(v8 + ((c0 >> 3) * n + i) * 8);
             const double2 a0 = __ldg(src), a1 = __ldg(src + 1), a2 = __ldg(src + 2), a3 = __ldg(src + 3);
@@ -1451,6 +1544,12 @@ struct sc_kmeanspp {
     DevBuf<int32_t> ctr;
     int ncent = 0;
     bool bound = false;
+    // fp16 screen (KppScreen): points as fp16 panels, the centre in fp16
+    DevBuf<uint4> vh8;
+    DevBuf<__half> ch;
+    DevBuf<double> vnorm, cnorm;
+    double hs = 1.0;
+    bool screen = false;
 
     // d2 <- min(d2, |v - row|^2) and the candidate partials (row: the drawn
     // point's coordinates, device; pick: its local index or -1)
@@ -1471,9 +1570,21 @@ struct sc_kmeanspp {
             } else {
                 bound = false;  // past ccap centres: plain updates from here on
             }
-            kpp_update_panel_kernel<<<(unsigned)nb_upd, KPP_UPD_ROWS, 0, st>>>(
+            KppScreen scr;
+            size_t smem = 0;
+            if (screen && !first) {
+                kpp_centre_half_kernel<<<1, 256, 0, st>>>(d, row, hs, ch.p, cnorm.p);
+                SC_LAUNCHED(1);
+                scr.vh8 = vh8.p;
+                scr.ch = ch.p;
+                scr.vnorm = vnorm.p;
+                scr.cnorm = cnorm.p;
+                scr.s = hs;
+                smem = (size_t)ceil_div(d, 8) * 8 * sizeof(__half);
+            }
+            kpp_update_panel_kernel<<<(unsigned)nb_upd, KPP_UPD_ROWS, smem, st>>>(
                 n, d, v8.p, row, pick_index, first ? 1 : 0, d2.p, taken.p, pw.p, pc.p, ccp, bound ? ctr.p : nullptr,
-                t);
+                t, scr);
         } else {
             kpp_update_kernel<<<(unsigned)nb_upd, KPP_UPD_ROWS, 0, st>>>(n, d, v, row, pick_index, first ? 1 : 0, d2.p,
                                                                          taken.p, pw.p, pc.p);
@@ -1528,7 +1639,7 @@ int sc_lloyd(int64_t n, int64_t d, int64_t k, const double* v, const double* c_i
     rownorm_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, d, v, vn.p);
     rownorm_kernel<<<(unsigned)ceil_div(k, 256), 256, 0, st>>>(k, d, centroids, cn.p);
     double flops = 2.0 * (double)n * (double)k * (double)d;
-    // tensor-core assignment with certified argmin when eligible (d <= 256)
+    // tensor-core assignment with certified argmin when eligible (any width)
     AssignTc atc;
     if ((rc = atc.init(n, d, k, v, st))) return rc;
     auto assign_step = [&](const int64_t* old_lab, int64_t* out_lab) -> int {
@@ -1636,6 +1747,31 @@ int sc_kmeanspp_create(int64_t n, int64_t d, const double* v, sc_stream_t stream
         SC_LAUNCHED(1);
         s->bound = s->cent.alloc((size_t)sc_kmeanspp::ccap * d) == SC_OK &&
                    s->cc.alloc(sc_kmeanspp::ccap) == SC_OK && s->ctr.alloc(n) == SC_OK;
+        // the fp16 screen pays for itself once a row is wider than a few
+        // panels; optional (memory) and off with SPECLUST_KPP_SCREEN=0
+        const char* env = std::getenv("SPECLUST_KPP_SCREEN");
+        const bool want = !(env && env[0] == '0') && d >= 32 && d <= 8192;
+        if (want && s->vh8.alloc((size_t)nch * n) == SC_OK && s->ch.alloc((size_t)nch * 8) == SC_OK &&
+            s->vnorm.alloc(n) == SC_OK && s->cnorm.alloc(1) == SC_OK) {
+            DevBuf<unsigned long long> amax;
+            if (amax.alloc(1) == SC_OK) {
+                cudaMemsetAsync(amax.p, 0, sizeof(unsigned long long), s->st);
+                as_absmax_kernel<<<kNumSMs * 4, 256, 0, s->st>>>(n * d, v, amax.p);
+                rownorm_sqrt_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s->st>>>(n, d, v, s->vnorm.p);
+                SC_LAUNCHED(2);
+                unsigned long long hb = 0;
+                SC_CUDA(cudaMemcpyAsync(&hb, amax.p, sizeof(hb), cudaMemcpyDeviceToHost, s->st));
+                SC_CUDA(cudaStreamSynchronize(s->st));
+                double am;
+                std::memcpy(&am, &hb, sizeof(am));
+                // |s v| <= 2^14: far from the fp16 overflow at 65504
+                s->hs = am > 0 ? std::ldexp(1.0, (int)std::floor(std::log2(16384.0 / am))) : 1.0;
+                to_half_panels_kernel<<<(unsigned)ceil_div(nch * n, 256), 256, 0, s->st>>>(n, d, v, s->hs,
+                                                                                            s->vh8.p);
+                SC_LAUNCHED(1);
+                s->screen = true;
+            }
+        }
     }
     *out = s;
     return SC_OK;

@@ -42,7 +42,7 @@ template <int NKB, int STAGES>
 struct Tc2Layout {
     static constexpr uint32_t kA = 2 * NKB * TC_TILE_BYTES;  // two query tiles
     static constexpr uint32_t kB = NKB * TC_TILE_BYTES;
-    static constexpr uint32_t kL = 8 * TC_LIST_P * 8;  // per-epilogue-warp sort scratch
+    static constexpr uint32_t kL = 256 * 16 * 4;  // 16 staged keys per epilogue thread
     static constexpr uint32_t kCn = TC2_CN_RING * 128 * 4;
     static constexpr uint32_t kBar = 8 * (2 * STAGES + 5 + 2 * TC2_CN_RING) + 8;
     static constexpr uint32_t total = 1024 + kA + STAGES * kB + kL + kCn + kBar;
@@ -87,28 +87,88 @@ __device__ __forceinline__ float4 lds_f4(uint32_t addr) {
     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "r"(addr));
     return r;
 }
-// keep the R smallest of a row's c_src list entries (global) via a warp
-// bitonic sort in `scratch`; returns the new threshold (R-th key)
-static __device__ __noinline__ float tc2_compact(float2* Lg, float2* scratch, int c_src, int R, int lane) {
-    __syncwarp();  // the owner lane's appends are visible to the warp
-    for (int e = lane; e < TC_LIST_P; e += 32)
-        scratch[e] = e < c_src ? Lg[e] : make_float2(INFINITY, __int_as_float(-1));
-    __syncwarp();
-    warp_bitonic_sort(scratch, lane);
-    for (int e = lane; e < R; e += 32) Lg[e] = scratch[e];
-    const float t = scratch[R - 1].x;
-    __syncwarp();
-    return t;
-}
-
 // Candidate tile of scan step t for the query pair at tile qt0: outward from
 // the pair (qt0, qt0+1, qt0-1, qt0+2, qt0-2, ...), so that in the locality
 // order a row meets its own region first, from both sides, and its threshold
 // is near-final before the far tiles arrive.  Visits every tile once.
+// |offset| <= ntiles / 2 + 1 and 0 <= qt0 < ntiles, so one conditional
+// correction replaces the 64-bit modulo (which cost ~5 % of the kernel's
+// issue slots when every epilogue thread evaluated it per tile).
 __device__ __forceinline__ int64_t scan_tile(int64_t qt0, int64_t t, int64_t ntiles) {
     const int64_t off = (t & 1) ? ((t + 1) >> 1) : -(t >> 1);
-    int64_t c = (qt0 + off) % ntiles;
-    return c < 0 ? c + ntiles : c;
+    int64_t c = qt0 + off;
+    if (c >= ntiles) c -= ntiles;
+    if (c < 0) c += ntiles;
+    return c;
+}
+
+// order-preserving map of a float key onto uint32 (total order, -0 < +0)
+__device__ __forceinline__ uint32_t key_bits(float k) {
+    const uint32_t u = __float_as_uint(k);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+// keep the R smallest of a row's c_src list entries (global, c_src <= 128):
+// warp radix select of the R-th smallest key on its order-preserving bits (32
+// ballot-count rounds over 4 entries per lane), then one compaction pass that
+// writes the entries below it and the first ties at it to Lg[0..R).  Returns
+// the R-th key: every dropped entry is >= it.  (Replaces a full 128-wide
+// bitonic sort per compaction: ~20 % of the kernel's stall samples.)
+static __device__ __noinline__ float tc2_select_compact(float2* Lg, int c_src, int R, int lane) {
+    __syncwarp();  // the owner lane's appends are visible to the warp
+    float2 e[4];
+    uint32_t u[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int i = lane + 32 * q;
+        e[q] = i < c_src ? Lg[i] : make_float2(INFINITY, __int_as_float(-1));
+        u[q] = i < c_src ? key_bits(e[q].x) : 0xFFFFFFFFu;
+    }
+    // T = the (R-1)-th smallest (0-based) of the u's: build it bit by bit,
+    // keeping count(u < prefix) <= R - 1.  T lies between the smallest and
+    // the largest listed key, so the bits above their highest differing bit
+    // are fixed and the search starts below it (list keys share a narrow
+    // range once the threshold has tightened)
+    uint32_t lo = 0xFFFFFFFFu, hi = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        if (lane + 32 * q < c_src) {
+            lo = min(lo, u[q]);
+            hi = max(hi, u[q]);
+        }
+    lo = __reduce_min_sync(0xffffffffu, lo);
+    hi = __reduce_max_sync(0xffffffffu, hi);
+    const int b0 = lo == hi ? -1 : 31 - __clz(lo ^ hi);
+    uint32_t T = b0 < 0 ? lo : (b0 == 31 ? 0u : lo & ~((2u << b0) - 1u));
+#pragma unroll 1
+    for (int b = b0; b >= 0; --b) {
+        const uint32_t cand = T | (1u << b);
+        int c = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) c += u[q] < cand;
+        if ((int)__reduce_add_sync(0xffffffffu, (unsigned)c) <= R - 1) T = cand;
+    }
+    // entries < T first, then ties == T until R are placed (index order)
+    int below = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) below += u[q] < T;
+    below = (int)__reduce_add_sync(0xffffffffu, (unsigned)below);
+    __syncwarp();
+    int pos_lt = 0, pos_eq = below;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const bool lt = u[q] < T, eq = u[q] == T;
+        const unsigned blt = __ballot_sync(0xffffffffu, lt), beq = __ballot_sync(0xffffffffu, eq);
+        const unsigned lower = (1u << lane) - 1u;
+        const int slt = pos_lt + __popc(blt & lower), seq = pos_eq + __popc(beq & lower);
+        if (lt) Lg[slt] = e[q];
+        if (eq && seq < R) Lg[seq] = e[q];
+        pos_lt += __popc(blt);
+        pos_eq += __popc(beq);
+    }
+    __syncwarp();
+    const uint32_t tb = (T & 0x80000000u) ? (T & 0x7FFFFFFFu) : ~T;
+    return __uint_as_float(tb);
 }
 __device__ __forceinline__ float fmin3(float a, float b, float c) { return fminf(a, fminf(b, c)); }
 
@@ -227,9 +287,9 @@ __global__ void __launch_bounds__(TC2_THREADS, 1)
         const bool valid = tile_ok && row < n;
         const int64_t slot = lq0 * 128 + lrow;  // list slot of this row
         float2* L = lists + (valid ? slot : 0) * (int64_t)cap;
-        float2* scratch = sL + (size_t)(warp - 2) * TC_LIST_P;
         float2* H = sH + (size_t)lrow * R;
-        float* stage = sStage + ((size_t)(warp - 2) * 32 + lane) * 16;
+        float* stage = HEAP ? sStage + ((size_t)(warp - 2) * 32 + lane) * 16
+                            : reinterpret_cast<float*>(sL) + ((size_t)(warp - 2) * 32 + lane) * 16;
         int cnt = 0;
         float tau = INFINITY;
         long long dbg_c[3] = {0, 0, 0}, dbg_f[3] = {0, 0, 0};
@@ -284,6 +344,11 @@ __global__ void __launch_bounds__(TC2_THREADS, 1)
             tc::tmem_ld64(taddr, v);
             tc::tmem_ld64(taddr + 64, v + 64);
             tc::tmem_wait_ld();
+            // the accumulator is in registers: hand the TMEM buffer back now,
+            // so the MMA of tile t + 2 overlaps this tile's list work
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&tempty[buf]);
             const uint32_t cn_s = tc::smem_u32(sCn + cslot * 128);
             float qm[8];
 #pragma unroll
@@ -303,6 +368,8 @@ __global__ void __launch_bounds__(TC2_THREADS, 1)
                 }
                 qm[q] = m;
             }
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&cempty[cslot]);  // column norms consumed
             const float h0 = fminf(fminf(qm[0], qm[1]), fminf(qm[2], qm[3]));
             const float h1 = fminf(fminf(qm[4], qm[5]), fminf(qm[6], qm[7]));
             // rare path: append the passing keys of a 64-column half to the row's list
@@ -319,26 +386,32 @@ __global__ void __launch_bounds__(TC2_THREADS, 1)
                         const int c_src = __shfl_sync(0xffffffffu, cnt, src);
                         const int64_t sslot = __shfl_sync(0xffffffffu, slot, src);
                         float2* Lg = lists + sslot * (int64_t)cap;
-                        for (int e = lane; e < TC_LIST_P; e += 32)
-                            scratch[e] = e < c_src ? Lg[e] : make_float2(INFINITY, __int_as_float(-1));
-                        __syncwarp();
-                        warp_bitonic_sort(scratch, lane);
-                        for (int e = lane; e < R; e += 32) Lg[e] = scratch[e];
-                        const float new_tau = scratch[R - 1].x;
-                        __syncwarp();
+                        const float new_tau = tc2_select_compact(Lg, c_src, R, lane);
                         if (lane == src) {
                             cnt = R;
                             tau = new_tau;
                         }
                     }
                     if (pass) {
+                        // passing keys as a bit mask, walked with ffs: one
+                        // store per appended key instead of 16 predicated ones
                         const float* keys = keys64 + 16 * q;
                         const int64_t cb = cbase + q * 16;
+                        unsigned msk = 0;
 #pragma unroll
-                        for (int u = 0; u < 16; ++u) {
-                            const int64_t col = cb + u;
-                            if (keys[u] < tau && col != row && col < n)
-                                L[cnt++] = make_float2(keys[u], __int_as_float((int)col));
+                        for (int u = 0; u < 16; ++u) msk |= (keys[u] < tau ? 1u : 0u) << u;
+                        if (row >= cb && row < cb + 16) msk &= ~(1u << (int)(row - cb));
+                        if (cb + 16 > n) msk &= n > cb ? (1u << (int)(n - cb)) - 1u : 0u;
+                        if (msk) {
+                            float4* st4 = reinterpret_cast<float4*>(stage);
+#pragma unroll
+                            for (int u = 0; u < 4; ++u)
+                                st4[u] = make_float4(keys[4 * u], keys[4 * u + 1], keys[4 * u + 2], keys[4 * u + 3]);
+                            while (msk) {
+                                const int u = __ffs(msk) - 1;
+                                msk &= msk - 1;
+                                L[cnt++] = make_float2(stage[u], __int_as_float((int)(cb + u)));
+                            }
                         }
                     }
                 }
@@ -385,12 +458,6 @@ __global__ void __launch_bounds__(TC2_THREADS, 1)
                     dbg_c[bin] += clock64() - z0;
                     dbg_f[bin] += fired;
                 }
-            }
-            tc::fence_before();
-            __syncwarp();
-            if (lane == 0) {
-                tc::mbar_arrive(&tempty[buf]);
-                tc::mbar_arrive(&cempty[cslot]);
             }
         }
         if ((WMODE & 64) && lane == 0 && dbg) {

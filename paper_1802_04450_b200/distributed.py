@@ -471,17 +471,21 @@ def _lanczos_sharded(ops, comm, a_local, n, bounds, cfg, op):
         # one full CGS pass (subsumes the three-term recurrence, eigen.py:157-163)
         # and a second only when the first cancelled most of |w| (DGKS; the
         # same rule as the single-GPU session, sc_lanczos.cu advance())
-        w0 = norm_of(w)
-        h = dot_all(ops.gemv_t(B, cnt, w))
-        alpha = float(h[j].item())
+        # [B^T w; |w|^2] in ONE all-reduce, |w - B h|^2 in a second, and one
+        # host read of (alpha, |w|^2, beta^2) per step
+        torch = comm.torch
+        hs = torch.cat([ops.gemv_t(B, cnt, w), ops.gemv_n(B, 0, None, w, want_sq=True)])
+        comm.sum_(hs)
+        sq = ops.gemv_n(B, cnt, hs[:cnt], w, want_sq=True)
+        comm.sum_(sq)
+        alpha, w0sq, bsq = (float(v) for v in ops.host(torch.stack([hs[j], hs[cnt], sq[0]])))
         T[j, j] = alpha
-        sq = ops.gemv_n(B, cnt, h, w, want_sq=True)
-        beta = math.sqrt(float(comm.sum_(sq)[0].item()))
-        if beta < REORTH_ETA * w0:
+        beta = math.sqrt(bsq)
+        if beta < REORTH_ETA * math.sqrt(w0sq):
             st["second_passes"] += 1
             h = dot_all(ops.gemv_t(B, cnt, w))
             sq = ops.gemv_n(B, cnt, h, w, want_sq=True)
-            beta = math.sqrt(float(comm.sum_(sq)[0].item()))
+            beta = math.sqrt(float(ops.host(comm.sum_(sq))[0]))
         scale = max(scale, abs(alpha), beta)
         if j + 1 < m:
             if beta > BREAKDOWN_RTOL * max(1.0, scale):
