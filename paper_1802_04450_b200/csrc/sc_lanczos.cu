@@ -1062,6 +1062,17 @@ struct sc_lanczos {
         SC_CUDA(cudaStreamSynchronize(st));
         double loss;
         memcpy(&loss, &bits, sizeof(loss));
+        static const bool dbg = std::getenv("SPECLUST_FLUSH_DEBUG") != nullptr;
+        if (dbg && restarts > 0 && flushes % 10 == 0) {
+            // loss against the retained Ritz block (rows < k of H) vs the sweep's vectors
+            std::vector<double> hh((size_t)c0 * c);
+            SC_CUDA(cudaMemcpy(hh.data(), bH.p, sizeof(double) * hh.size(), cudaMemcpyDeviceToHost));
+            double lr = 0.0, ls = 0.0;
+            for (int64_t r = 0; r < c0; ++r)
+                for (int o = 0; o < c; ++o) (r < k ? lr : ls) = std::max(r < k ? lr : ls, std::fabs(hh[r * c + o]));
+            fprintf(stderr, "[flush] restart %lld j %lld c %d loss_ritz %.2e loss_sweep %.2e\n", (long long)restarts,
+                    (long long)c1, c, lr, ls);
+        }
         ++flushes;
         window_sum += c;
         max_loss = std::max(max_loss, loss);
