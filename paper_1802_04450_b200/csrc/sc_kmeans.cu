@@ -349,20 +349,35 @@ __global__ void centroid_segsum_kernel(int64_t k, int64_t d, int64_t nseg, const
     // independent loads are in flight per lane ahead of the dependent adds
     const bool on = dim < d;
     double acc = 0.0;
-    int64_t m = b;
-    constexpr int B = 64;
-    for (; m + B <= e; m += B) {
-        const int32_t i0 = __ldg(members + m + lane), i1 = __ldg(members + m + 32 + lane);
-        double x[B];
+    // software pipeline over batches of 32 members: the member indices are
+    // loaded two batches ahead and the feature values one batch ahead, so the
+    // dependent add chain of batch t overlaps the gathers of batch t + 1 and
+    // only one memory latency is exposed per batch
+    constexpr int B = 32;
+    const int64_t nfull = (e - b) / B;
+    auto ld_idx = [&](int64_t t) -> int32_t { return t < nfull ? __ldg(members + b + t * B + lane) : 0; };
+    auto gather = [&](int32_t idx, int64_t t, double (&x)[B]) {
 #pragma unroll
         for (int u = 0; u < B; ++u) {
-            const int32_t r = __shfl_sync(0xffffffffu, u < 32 ? i0 : i1, u & 31);
-            x[u] = on ? __ldg(v + (int64_t)r * d + dim) : 0.0;
+            const int32_t r = __shfl_sync(0xffffffffu, idx, u);
+            x[u] = (on && t < nfull) ? __ldg(v + (int64_t)r * d + dim) : 0.0;
         }
+    };
+    double xa[B], xb[B];
+    int32_t inext = ld_idx(1);
+    gather(ld_idx(0), 0, xa);
+    for (int64_t t = 0; t < nfull; t += 2) {
+        const int32_t i2 = ld_idx(t + 2);
+        gather(inext, t + 1, xb);
 #pragma unroll
-        for (int u = 0; u < B; ++u) acc = __dadd_rn(acc, x[u]);
+        for (int u = 0; u < B; ++u) acc = __dadd_rn(acc, xa[u]);
+        if (t + 1 >= nfull) break;
+        inext = ld_idx(t + 3);
+        gather(i2, t + 2, xa);
+#pragma unroll
+        for (int u = 0; u < B; ++u) acc = __dadd_rn(acc, xb[u]);
     }
-    for (; m < e; ++m) acc = __dadd_rn(acc, on ? v[(int64_t)members[m] * d + dim] : 0.0);
+    for (int64_t m = b + nfull * B; m < e; ++m) acc = __dadd_rn(acc, on ? v[(int64_t)members[m] * d + dim] : 0.0);
     if (on) part[s * d + dim] = acc;
 }
 

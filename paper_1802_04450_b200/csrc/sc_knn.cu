@@ -1200,7 +1200,14 @@ int knn_select(int64_t n, int64_t d, const double* x, int64_t knn, double two_si
         // capacity 2R + 16 (<= the sort width): each warp compaction frees
         // R + 16 slots (C2: 128 -> -9 ms of list maintenance vs 2R); tuning knob
         const char* cenv = std::getenv("SPECLUST_KNN_CAP");
-        cap = (int)std::min<int64_t>(std::max<int64_t>(cenv ? std::atoll(cenv) : 2 * R + 16, R + 16), TC_LIST_P);
+        // the query-pair kernel (d <= 128) compacts by radix select up to
+        // TC2_LIST_MAX entries and hands the recheck <= TC_LIST_P: a longer
+        // append list means ~3x fewer compactions (each frees cap - R slots)
+        const char* tenv = std::getenv("SPECLUST_KNN_TC");
+        const bool tc2 = dp64 <= 128 && !(tenv && std::strcmp(tenv, "1") == 0);
+        const int64_t cmax = tc2 ? TC2_LIST_MAX : TC_LIST_P;
+        cap = (int)std::min<int64_t>(std::max<int64_t>(cenv ? std::atoll(cenv) : (tc2 ? cmax : 2 * R + 16), R + 16),
+                                     cmax);
     } else {
         cap = 2 * R;
         if (cap > n - 1) cap = (int)(n - 1);  // lists can hold every other point

@@ -108,34 +108,35 @@ __device__ __forceinline__ uint32_t key_bits(float k) {
     return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
-// keep the R smallest of a row's c_src list entries (global, c_src <= 128):
-// warp radix select of the R-th smallest key on its order-preserving bits (32
-// ballot-count rounds over 4 entries per lane), then one compaction pass that
-// writes the entries below it and the first ties at it to Lg[0..R).  Returns
-// the R-th key: every dropped entry is >= it.  (Replaces a full 128-wide
-// bitonic sort per compaction: ~20 % of the kernel's stall samples.)
+// keep the R smallest of a row's c_src list entries (global, c_src <= 32 *
+// TC2_PER): warp radix select of the R-th smallest key on its
+// order-preserving bits (ballot-count rounds over TC2_PER entries per lane,
+// starting below the common prefix of the list's min and max), then one
+// compaction pass that writes the entries below it and the first ties at it
+// to Lg[0..R).  Returns the R-th key: every dropped entry is >= it.
+// (Replaces a full bitonic sort per compaction: ~20 % of the kernel's stall
+// samples in round 1.)
+constexpr int TC2_PER = 8;                  // list entries per lane in a compaction
+constexpr int TC2_LIST_MAX = 32 * TC2_PER;  // append capacity of the query-pair kernel
 static __device__ __noinline__ float tc2_select_compact(float2* Lg, int c_src, int R, int lane) {
     __syncwarp();  // the owner lane's appends are visible to the warp
-    float2 e[4];
-    uint32_t u[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const int i = lane + 32 * q;
-        e[q] = i < c_src ? Lg[i] : make_float2(INFINITY, __int_as_float(-1));
-        u[q] = i < c_src ? key_bits(e[q].x) : 0xFFFFFFFFu;
-    }
-    // T = the (R-1)-th smallest (0-based) of the u's: build it bit by bit,
-    // keeping count(u < prefix) <= R - 1.  T lies between the smallest and
-    // the largest listed key, so the bits above their highest differing bit
-    // are fixed and the search starts below it (list keys share a narrow
-    // range once the threshold has tightened)
+    float2 e[TC2_PER];
+    uint32_t u[TC2_PER];
     uint32_t lo = 0xFFFFFFFFu, hi = 0;
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-        if (lane + 32 * q < c_src) {
+    for (int q = 0; q < TC2_PER; ++q) {
+        const int i = lane + 32 * q;
+        const bool in = i < c_src;
+        e[q] = in ? Lg[i] : make_float2(INFINITY, __int_as_float(-1));
+        u[q] = in ? key_bits(e[q].x) : 0xFFFFFFFFu;
+        if (in) {
             lo = min(lo, u[q]);
             hi = max(hi, u[q]);
         }
+    }
+    // T = the (R-1)-th smallest (0-based): built bit by bit keeping
+    // count(u < prefix) <= R - 1; T lies in [lo, hi], so the bits above their
+    // highest differing bit are fixed
     lo = __reduce_min_sync(0xffffffffu, lo);
     hi = __reduce_max_sync(0xffffffffu, hi);
     const int b0 = lo == hi ? -1 : 31 - __clz(lo ^ hi);
@@ -145,21 +146,21 @@ static __device__ __noinline__ float tc2_select_compact(float2* Lg, int c_src, i
         const uint32_t cand = T | (1u << b);
         int c = 0;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) c += u[q] < cand;
+        for (int q = 0; q < TC2_PER; ++q) c += u[q] < cand;
         if ((int)__reduce_add_sync(0xffffffffu, (unsigned)c) <= R - 1) T = cand;
     }
     // entries < T first, then ties == T until R are placed (index order)
     int below = 0;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) below += u[q] < T;
+    for (int q = 0; q < TC2_PER; ++q) below += u[q] < T;
     below = (int)__reduce_add_sync(0xffffffffu, (unsigned)below);
     __syncwarp();
     int pos_lt = 0, pos_eq = below;
+    const unsigned lower = (1u << lane) - 1u;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < TC2_PER; ++q) {
         const bool lt = u[q] < T, eq = u[q] == T;
         const unsigned blt = __ballot_sync(0xffffffffu, lt), beq = __ballot_sync(0xffffffffu, eq);
-        const unsigned lower = (1u << lane) - 1u;
         const int slt = pos_lt + __popc(blt & lower), seq = pos_eq + __popc(beq & lower);
         if (lt) Lg[slt] = e[q];
         if (eq && seq < R) Lg[seq] = e[q];
@@ -464,6 +465,22 @@ __global__ void __launch_bounds__(TC2_THREADS, 1)
             for (int b = 0; b < 3; ++b) {
                 atomicAdd(reinterpret_cast<unsigned long long*>(dbg + b), (unsigned long long)dbg_c[b]);
                 atomicAdd(reinterpret_cast<unsigned long long*>(dbg + 3 + b), (unsigned long long)dbg_f[b]);
+            }
+        }
+        if (!HEAP) {
+            // the recheck sorts at most TC_LIST_P entries per row: longer lists
+            // are compacted to R once more (tau tightens accordingly)
+            unsigned want = __ballot_sync(0xffffffffu, valid && cnt > TC_LIST_P);
+            while (want) {
+                const int src = __ffs(want) - 1;
+                want &= want - 1;
+                const int c_src = __shfl_sync(0xffffffffu, cnt, src);
+                const int64_t sslot = __shfl_sync(0xffffffffu, slot, src);
+                const float new_tau = tc2_select_compact(lists + sslot * (int64_t)cap, c_src, R, lane);
+                if (lane == src) {
+                    cnt = R;
+                    tau = new_tau;
+                }
             }
         }
         if (valid) {

@@ -223,6 +223,7 @@ __global__ void __launch_bounds__(256) window_cgs2_kernel(int64_t n, int64_t ld,
                                                           int64_t m, int64_t j, double* __restrict__ T,
                                                           double* __restrict__ scal) {
     cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+    constexpr int WCG_U = NC <= 8 ? 4 : (NC <= 16 ? 2 : 1);  // rows per thread per load group (registers)
     __shared__ double red[8][NC + 1];
     __shared__ double hs[NC];
     const int nb = gridDim.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -241,7 +242,25 @@ __global__ void __launch_bounds__(256) window_cgs2_kernel(int64_t n, int64_t ld,
     // pass 1: projections of the raw w and |w0|^2
 #pragma unroll
     for (int c = 0; c <= NC; ++c) acc[c] = 0.0;
-    for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+    // rows in groups of WCG_U per thread (stride blockDim.x), every load of a
+    // group issued before its FMAs: WCG_U x (cnt + 1) loads in flight
+    int64_t r = r0 + threadIdx.x;
+    for (; r + (WCG_U - 1) * 256 < r1; r += WCG_U * 256) {
+        double x[WCG_U], b[WCG_U][NC];
+#pragma unroll
+        for (int u = 0; u < WCG_U; ++u) {
+            x[u] = w[r + u * 256];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) b[u][c] = c < cnt ? __ldg(Bw + (int64_t)c * ld + r + u * 256) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < WCG_U; ++u) {
+#pragma unroll
+            for (int c = 0; c < NC; ++c) acc[c] = fma(b[u][c], x[u], acc[c]);
+            acc[NC] = fma(x[u], x[u], acc[NC]);
+        }
+    }
+    for (; r < r1; r += blockDim.x) {
         const double x = w[r];
 #pragma unroll
         for (int c = 0; c < NC; ++c)
@@ -266,7 +285,27 @@ __global__ void __launch_bounds__(256) window_cgs2_kernel(int64_t n, int64_t ld,
     // update 1 fused with the projections of the updated w (pass 2)
 #pragma unroll
     for (int c = 0; c <= NC; ++c) acc[c] = 0.0;
-    for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+    r = r0 + threadIdx.x;
+    for (; r + (WCG_U - 1) * 256 < r1; r += WCG_U * 256) {
+        double x[WCG_U], b[WCG_U][NC];
+#pragma unroll
+        for (int u = 0; u < WCG_U; ++u) {
+            x[u] = w[r + u * 256];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) b[u][c] = c < cnt ? __ldg(Bw + (int64_t)c * ld + r + u * 256) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < WCG_U; ++u) {
+            double s = 0.0;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) s = fma(b[u][c], hs[c < cnt ? c : 0] * (c < cnt ? 1.0 : 0.0), s);
+            const double xv = x[u] - s;
+            w[r + u * 256] = xv;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) acc[c] = fma(b[u][c], xv, acc[c]);
+        }
+    }
+    for (; r < r1; r += blockDim.x) {
         double s = 0.0;
 #pragma unroll
         for (int c = 0; c < NC; ++c)
@@ -283,7 +322,26 @@ __global__ void __launch_bounds__(256) window_cgs2_kernel(int64_t n, int64_t ld,
     gather_h(cnt);
     // update 2 and |w|^2
     double sq = 0.0;
-    for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+    r = r0 + threadIdx.x;
+    for (; r + (WCG_U - 1) * 256 < r1; r += WCG_U * 256) {
+        double x[WCG_U], b[WCG_U][NC];
+#pragma unroll
+        for (int u = 0; u < WCG_U; ++u) {
+            x[u] = w[r + u * 256];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) b[u][c] = c < cnt ? __ldg(Bw + (int64_t)c * ld + r + u * 256) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < WCG_U; ++u) {
+            double s = 0.0;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) s = fma(b[u][c], hs[c < cnt ? c : 0] * (c < cnt ? 1.0 : 0.0), s);
+            const double xv = x[u] - s;
+            w[r + u * 256] = xv;
+            sq = fma(xv, xv, sq);
+        }
+    }
+    for (; r < r1; r += blockDim.x) {
         double s = 0.0;
 #pragma unroll
         for (int c = 0; c < NC; ++c)
