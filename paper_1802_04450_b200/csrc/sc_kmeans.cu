@@ -349,37 +349,109 @@ __global__ void centroid_segsum_kernel(int64_t k, int64_t d, int64_t nseg, const
     // independent loads are in flight per lane ahead of the dependent adds
     const bool on = dim < d;
     double acc = 0.0;
-    // software pipeline over batches of 32 members: the member indices are
-    // loaded two batches ahead and the feature values one batch ahead, so the
-    // dependent add chain of batch t overlaps the gathers of batch t + 1 and
-    // only one memory latency is exposed per batch
-    constexpr int B = 32;
-    const int64_t nfull = (e - b) / B;
-    auto ld_idx = [&](int64_t t) -> int32_t { return t < nfull ? __ldg(members + b + t * B + lane) : 0; };
-    auto gather = [&](int32_t idx, int64_t t, double (&x)[B]) {
+    int64_t m = b;
+    constexpr int B = 64;
+    for (; m + B <= e; m += B) {
+        const int32_t i0 = __ldg(members + m + lane), i1 = __ldg(members + m + 32 + lane);
+        double x[B];
 #pragma unroll
         for (int u = 0; u < B; ++u) {
-            const int32_t r = __shfl_sync(0xffffffffu, idx, u);
-            x[u] = (on && t < nfull) ? __ldg(v + (int64_t)r * d + dim) : 0.0;
+            const int32_t r = __shfl_sync(0xffffffffu, u < 32 ? i0 : i1, u & 31);
+            x[u] = on ? __ldg(v + (int64_t)r * d + dim) : 0.0;
         }
-    };
-    double xa[B], xb[B];
-    int32_t inext = ld_idx(1);
-    gather(ld_idx(0), 0, xa);
-    for (int64_t t = 0; t < nfull; t += 2) {
-        const int32_t i2 = ld_idx(t + 2);
-        gather(inext, t + 1, xb);
 #pragma unroll
-        for (int u = 0; u < B; ++u) acc = __dadd_rn(acc, xa[u]);
-        if (t + 1 >= nfull) break;
-        inext = ld_idx(t + 3);
-        gather(i2, t + 2, xa);
-#pragma unroll
-        for (int u = 0; u < B; ++u) acc = __dadd_rn(acc, xb[u]);
+        for (int u = 0; u < B; ++u) acc = __dadd_rn(acc, x[u]);
     }
-    for (int64_t m = b + nfull * B; m < e; ++m) acc = __dadd_rn(acc, on ? v[(int64_t)members[m] * d + dim] : 0.0);
+    for (; m < e; ++m) acc = __dadd_rn(acc, on ? v[(int64_t)members[m] * d + dim] : 0.0);
     if (on) part[s * d + dim] = acc;
 }
+
+// The same point-order chains with the member rows staged in shared memory:
+// one warp per CTA (one cluster x 32 features), batches of CS_BATCH member
+// rows gathered with 8-byte cp.async into a double buffer while the previous
+// batch is summed from shared memory; member indices are loaded one batch
+// ahead of their gathers.  One gather latency is exposed per CS_BATCH rows
+// instead of two per 64, and the add chain never waits on global memory.
+constexpr int CS_BATCH = 128;
+__device__ __forceinline__ void cs_cp8(double* dst, const double* src, bool pred) {
+    const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(src), "r"(pred ? 8 : 0) : "memory");
+}
+__global__ void __launch_bounds__(32) centroid_segsum_smem_kernel(int64_t k, int64_t d, int64_t nseg,
+                                                                 const double* __restrict__ v,
+                                                                 const int64_t* __restrict__ start,
+                                                                 const int32_t* __restrict__ members,
+                                                                 const int64_t* __restrict__ seg_off,
+                                                                 double* __restrict__ part) {
+    extern __shared__ __align__(16) double cs_buf[];  // [2][CS_BATCH][32]
+    const int64_t dchunks = ceil_div_dev(d);
+    const int64_t w = blockIdx.x;
+    const int lane = threadIdx.x;
+    if (w >= nseg * dchunks) return;
+    const int64_t s = w / dchunks;
+    const int64_t dim = (w % dchunks) * 32 + lane;
+    int64_t lo = 0, hi = k;
+    while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (seg_off[mid] <= s) lo = mid; else hi = mid;
+    }
+    const int64_t cl = lo;
+    const int64_t b = start[cl] + (s - seg_off[cl]) * CM_SEG;
+    const int64_t e = imin64(start[cl + 1], b + CM_SEG);
+    const bool on = dim < d;
+    const int64_t nb = (e - b + CS_BATCH - 1) / CS_BATCH;
+    constexpr int PL = CS_BATCH / 32;  // member indices per lane per batch
+    auto load_idx = [&](int64_t t, int32_t (&ix)[PL]) {
+#pragma unroll
+        for (int q = 0; q < PL; ++q) {
+            const int64_t m = b + t * CS_BATCH + q * 32 + lane;
+            ix[q] = (t < nb && m < e) ? __ldg(members + m) : -1;
+        }
+    };
+    auto gather = [&](int64_t t, const int32_t (&ix)[PL]) {
+        double* dst = cs_buf + (t & 1) * CS_BATCH * 32;
+#pragma unroll
+        for (int q = 0; q < PL; ++q) {
+#pragma unroll 8
+            for (int r = 0; r < 32; ++r) {
+                const int32_t row = __shfl_sync(0xffffffffu, ix[q], r);
+                cs_cp8(dst + (q * 32 + r) * 32 + lane, row >= 0 && on ? v + (int64_t)row * d + dim : v, row >= 0 && on);
+            }
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    int32_t ia[PL], ib[PL];
+    load_idx(0, ia);
+    gather(0, ia);
+    load_idx(1, ib);
+    double acc = 0.0;
+    for (int64_t t = 0; t < nb; ++t) {
+        // gathers of batch t + 1 (indices already in ib), then the indices of t + 2
+        if (t + 1 < nb) gather(t + 1, ib);
+        else asm volatile("cp.async.commit_group;\n" ::: "memory");
+        load_idx(t + 2, ia);
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        __syncwarp();
+        const double* src = cs_buf + (t & 1) * CS_BATCH * 32 + lane;
+        const int rows = (int)imin64(CS_BATCH, e - (b + t * CS_BATCH));
+        for (int r = 0; r < rows; ++r) acc = __dadd_rn(acc, src[r * 32]);
+        __syncwarp();  // the buffer is refilled by the gathers of batch t + 2
+#pragma unroll
+        for (int q = 0; q < PL; ++q) ib[q] = ia[q];
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    if (on) part[s * d + dim] = acc;
+}
+static int segsum_smem_attr() {
+    static bool done = false;
+    if (!done) {
+        SC_CUDA(cudaFuncSetAttribute(centroid_segsum_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     2 * CS_BATCH * 32 * (int)sizeof(double)));
+        done = true;
+    }
+    return SC_OK;
+}
+
 
 __global__ void centroid_segmean_kernel(int64_t k, int64_t d, const int64_t* __restrict__ start,
                                         const int64_t* __restrict__ seg_off, const double* __restrict__ part,
@@ -1699,8 +1771,9 @@ int sc_lloyd(int64_t n, int64_t d, int64_t k, const double* v, const double* c_i
             ProfScope prof("kmeans_update", st, (double)n * d * 8.0 + 12.0 * n + 16.0 * k * d);
             SC_CUDA(cudaMemcpyAsync(seg_off.p, hseg.data(), sizeof(int64_t) * (k + 1), cudaMemcpyHostToDevice, st));
             if (nseg > 0)
-                centroid_segsum_kernel<<<(unsigned)ceil_div(nseg * dchunks * 32, 256), 256, 0, st>>>(
-                    k, d, nseg, v, bk.start.p, bk.members.p, seg_off.p, segpart.p);
+                if ((rc = segsum_smem_attr())) return rc;
+                centroid_segsum_smem_kernel<<<(unsigned)(nseg * dchunks), 32, 2 * CS_BATCH * 32 * sizeof(double),
+                                              st>>>(k, d, nseg, v, bk.start.p, bk.members.p, seg_off.p, segpart.p);
             centroid_segmean_kernel<<<(unsigned)ceil_div(k * d, 256), 256, 0, st>>>(k, d, bk.start.p, seg_off.p,
                                                                                     segpart.p, centroids);
         }
@@ -1952,7 +2025,8 @@ int sc_kmeans_local_sums(int64_t n, int64_t d, int64_t k, const double* v, const
     SC_CUDA(cudaMemcpyAsync(seg_off.p, hseg.data(), sizeof(int64_t) * (k + 1), cudaMemcpyHostToDevice, st));
     const int64_t dchunks = ceil_div(d, 32);
     if (nseg > 0)
-        centroid_segsum_kernel<<<(unsigned)ceil_div(nseg * dchunks * 32, 256), 256, 0, st>>>(
+        if (int rc = segsum_smem_attr()) return rc;
+        centroid_segsum_smem_kernel<<<(unsigned)(nseg * dchunks), 32, 2 * CS_BATCH * 32 * sizeof(double), st>>>(
             k, d, nseg, v, bk.start.p, bk.members.p, seg_off.p, segpart.p);
     centroid_segtotal_kernel<<<(unsigned)ceil_div(k * d, 256), 256, 0, st>>>(k, d, bk.start.p, seg_off.p, segpart.p,
                                                                             sums, counts);

@@ -1206,7 +1206,7 @@ int knn_select(int64_t n, int64_t d, const double* x, int64_t knn, double two_si
         const char* tenv = std::getenv("SPECLUST_KNN_TC");
         const bool tc2 = dp64 <= 128 && !(tenv && std::strcmp(tenv, "1") == 0);
         const int64_t cmax = tc2 ? TC2_LIST_MAX : TC_LIST_P;
-        cap = (int)std::min<int64_t>(std::max<int64_t>(cenv ? std::atoll(cenv) : (tc2 ? cmax : 2 * R + 16), R + 16),
+        cap = (int)std::min<int64_t>(std::max<int64_t>(cenv ? std::atoll(cenv) : 2 * R + 16, R + 16),
                                      cmax);
     } else {
         cap = 2 * R;

@@ -116,7 +116,7 @@ __device__ __forceinline__ uint32_t key_bits(float k) {
 // to Lg[0..R).  Returns the R-th key: every dropped entry is >= it.
 // (Replaces a full bitonic sort per compaction: ~20 % of the kernel's stall
 // samples in round 1.)
-constexpr int TC2_PER = 8;                  // list entries per lane in a compaction
+constexpr int TC2_PER = 4;                  // list entries per lane in a compaction
 constexpr int TC2_LIST_MAX = 32 * TC2_PER;  // append capacity of the query-pair kernel
 static __device__ __noinline__ float tc2_select_compact(float2* Lg, int c_src, int R, int lane) {
     __syncwarp();  // the owner lane's appends are visible to the warp

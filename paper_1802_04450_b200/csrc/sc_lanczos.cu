@@ -34,13 +34,27 @@ namespace sc {
 constexpr int GT_ROWS = 2048;     // rows per gemv_t partial block (max)
 constexpr int GN_THREADS = 256;   // rows per gemv_n block
 constexpr double kBreakdownRtol = 1e-13;  // eigen.py:50
-// second CGS pass when the first one removed more than 1 - eta^2 of |w|^2
-constexpr double kReorthEta = 0.05;
+// windowed orthogonalisation only from this many rows on: below it the cost
+// of the reference's full CGS2 is negligible, and tiny operators (many
+// repeated / zero eigenvalues, exact breakdowns) are where a window's loss
+// grows fastest (reference acceptance criteria 1 and 6)
+constexpr int64_t kWindowMinN = 32768;
+// convergence test of a sweep: est_i <= kConvMargin * tol * max(1, |theta_i|)
+// (eigen.py:198-200 uses tol itself).  The estimates come from a different
+// start vector than numpy's, so the converged residuals land elsewhere in
+// [0, tol]; a 4x margin keeps them clear of tol, e.g. for the reference's
+// row-operator acceptance check (residual of D^-1/2 u under D^-1 W, <= 1e-8),
+// at the cost of rarely one more restart (C2 / C3 converge far below tol)
+constexpr double kConvMargin = 0.25;
+// windowed mode: a window pass that leaves |w| below this fraction of its
+// input norm has cancelled to rounding level -> two passes over the basis
+constexpr double kWindowCancel = 1e-6;
 // SELL-32-sigma matvecs are opt-in (SPECLUST_SPMV_FORMAT=sell): on the C2
 // kNN operator the x gathers are L2-sector bound and the warp-per-row CSR
 // kernel measured faster (161 vs 183 ms per 500 matvecs, profiles/)
 constexpr int64_t kSellMinRows = INT64_MAX;
 constexpr int64_t kMaxWindow = 16;
+constexpr int64_t kMaxSweepWindow = 32;  // <= WCG_MAX - 8: the per-step window spans it
 
 // ---- kernels ------------------------------------------------------------------
 __global__ void fill_normal_kernel(int64_t n, uint64_t seed, uint64_t stream_id, double* __restrict__ out) {
@@ -859,6 +873,15 @@ struct sc_lanczos {
     // each other; win = current window length
     bool windowed = true;
     int64_t j0 = 0, win = 6, flushes = 0, window_sum = 0;
+    // two-tier flushes after a restart (SPECLUST_REORTH=onetier disables):
+    // the window's loss is measured against the retained Ritz block (it grows
+    // there: converged Ritz vectors) and against the sweep's own older
+    // vectors (it stays at rounding level, profiles/r02_flush_losses.md), so
+    // the Ritz block is flushed every `win` steps and the sweep's older
+    // vectors only every `win_s` steps; js = first column not yet flushed
+    // against the sweep's older vectors
+    bool tiered = true;
+    int64_t js = 0, win_s = 16, sweep_flushes = 0;
     double max_loss = 0.0;
     DevBuf<double> bpart, bH, wpart;
     DevBuf<unsigned long long> bmax;
@@ -960,7 +983,8 @@ struct sc_lanczos {
             return rc;
         {
             const char* e = std::getenv("SPECLUST_REORTH");
-            windowed = !(e && std::strcmp(e, "full") == 0);
+            windowed = !(e && std::strcmp(e, "full") == 0) && (n >= kWindowMinN || (e && std::strcmp(e, "window") == 0));
+            tiered = !(e && std::strcmp(e, "onetier") == 0);
         }
         SC_CUDA(cudaMemsetAsync(T.p, 0, sizeof(double) * m * m, st));
         SC_CUDA(cudaMemsetAsync(w.p, 0, sizeof(double) * ld, st));
@@ -1006,7 +1030,9 @@ struct sc_lanczos {
         // SPECLUST_REORTH=full: one CGS pass over the whole basis every step
         // (+ a DGKS-guarded second pass), the round-1 scheme.
         const bool arrow_step = restarts > 0 && j == k;
-        const int64_t lo = (!windowed || arrow_step) ? 0 : std::max<int64_t>(0, std::min<int64_t>(j0, j - 1));
+        const bool two = windowed && tiered && restarts > 0;
+        const int64_t lo = (!windowed || arrow_step) ? 0
+                           : std::max<int64_t>(0, std::min<int64_t>(two ? js : j0, j - 1));
         const int cnt = (int)(j + 1 - lo);
         double ab[4];
         if (windowed && !arrow_step && cnt <= WCG_MAX) {
@@ -1028,10 +1054,18 @@ struct sc_lanczos {
             SC_CUDA(cudaMemcpyAsync(ab, scal.p, sizeof(double) * 4, cudaMemcpyDeviceToHost, st));
             SC_CUDA(cudaStreamSynchronize(st));
         }
-        if (!windowed && ab[0] < kReorthEta * ab[3]) {
-            ProfScope prof("reorth", st, 2.0 * (double)n * cnt * 8.0);
+        // second pass over the WHOLE basis: always in full mode (the
+        // reference's unconditional CGS2, eigen.py:131-135); in windowed mode
+        // when the window pass cancelled w to rounding level (a breakdown or
+        // near-breakdown: the new direction is made of rounding errors and
+        // is not orthogonal to the older basis the window does not cover)
+        const bool cancelled = windowed && ab[0] < kWindowCancel * ab[3];
+        if (!windowed || cancelled) {
+            ProfScope prof("reorth", st, 4.0 * (double)n * (j + 1) * 8.0);
             ++second_passes;
-            if ((rc = project(w.p, cnt)) || (rc = subtract(w.p, cnt, true))) return rc;
+            for (int pass = 0; pass < (cancelled ? 2 : 1); ++pass) {
+                if ((rc = project(w.p, (int)(j + 1))) || (rc = subtract(w.p, (int)(j + 1), true))) return rc;
+            }
             finish_norm_kernel<<<1, 1024, 0, st>>>(nb_n, sqp.p, scal.p, 0);
             SC_LAUNCHED(1);
             SC_CUDA(cudaMemcpyAsync(ab, scal.p, sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -1041,7 +1075,12 @@ struct sc_lanczos {
             // end of the sweep: the last window against the older basis, then
             // one pass of w over the whole (now orthonormal) basis -- w seeds
             // the next sweep (eigen.py:232) and its norm is the residual scale
-            if ((rc = flush(j0, m - 1))) return rc;
+            if (two) {
+                if ((rc = flush_range(0, k, j0, m - 1, win, kMaxWindow))) return rc;
+                if ((rc = flush_range(k, js, js, m - 1, win_s, kMaxSweepWindow))) return rc;
+            } else if ((rc = flush(j0, m - 1))) {
+                return rc;
+            }
             ProfScope prof("reorth", st, 2.0 * (double)n * m * 8.0);
             if ((rc = project(w.p, (int)m)) || (rc = subtract(w.p, (int)m, true))) return rc;
             finish_norm_kernel<<<1, 1024, 0, st>>>(nb_n, sqp.p, scal.p, 0);
@@ -1062,7 +1101,17 @@ struct sc_lanczos {
             if ((rc = fresh(j + 1, j + 1, true))) return rc;
         }
         ++j;
-        if (windowed && j - j0 >= win) {
+        if (two) {
+            if (j - j0 >= win || j + 1 - js >= win_s) {
+                if ((rc = flush_range(0, k, j0, j, win, kMaxWindow))) return rc;
+                j0 = j + 1;
+            }
+            if (j + 1 - js >= win_s) {
+                if ((rc = flush_range(k, js, js, j, win_s, kMaxSweepWindow))) return rc;
+                ++sweep_flushes;
+                js = j + 1;
+            }
+        } else if (windowed && j - j0 >= win) {
             if ((rc = flush(j0, j))) return rc;
             j0 = j + 1;
         }
@@ -1104,17 +1153,21 @@ struct sc_lanczos {
     // pass (the window is within ~1e-9 of orthogonal to the older basis, so a
     // second pass would change nothing at working precision); the measured
     // loss adapts the window length
-    int flush(int64_t c0, int64_t c1) {
-        if (c0 <= 0 || c1 < c0) return SC_OK;
+    int flush(int64_t c0, int64_t c1) { return flush_range(0, c0, c0, c1, win, kMaxWindow); }
+    // columns [c0, c1] -= B[:, ob:oe] (B[:, ob:oe]^T B[:, c0..c1]); the
+    // measured loss adapts `wv` (capped at wmax)
+    int flush_range(int64_t ob, int64_t oe, int64_t c0, int64_t c1, int64_t& wv, int64_t wmax) {
+        const int64_t nb = oe - ob;
+        if (nb <= 0 || c1 < c0) return SC_OK;
         const int c = (int)(c1 - c0 + 1);
         int rc;
-        ProfScope prof("reorth", st, 2.0 * (double)n * (double)(c0 + c) * 8.0);
-        const size_t need = block_part_size(n, (int)c0, c);
+        ProfScope prof("reorth", st, 2.0 * (double)n * (double)(nb + c) * 8.0);
+        const size_t need = block_part_size(n, (int)nb, c);
         if (bpart.n < need && (rc = bpart.alloc(need))) return rc;
-        if (bH.n < (size_t)c0 * c && (rc = bH.alloc((size_t)m * 48))) return rc;
+        if (bH.n < (size_t)nb * c && (rc = bH.alloc((size_t)m * 48))) return rc;
         SC_CUDA(cudaMemsetAsync(bmax.p, 0, sizeof(unsigned long long), st));
-        if ((rc = block_tn(n, ld, (int)c0, B.p, B.p + c0 * ld, c, bH.p, bpart.p, bmax.p, st))) return rc;
-        if ((rc = block_nn(n, ld, (int)c0, B.p, bH.p, c, B.p + c0 * ld, st))) return rc;
+        if ((rc = block_tn(n, ld, (int)nb, B.p + ob * ld, B.p + c0 * ld, c, bH.p, bpart.p, bmax.p, st))) return rc;
+        if ((rc = block_nn(n, ld, (int)nb, B.p + ob * ld, bH.p, c, B.p + c0 * ld, st))) return rc;
         unsigned long long bits = 0;
         SC_CUDA(cudaMemcpyAsync(&bits, bmax.p, sizeof(bits), cudaMemcpyDeviceToHost, st));
         SC_CUDA(cudaStreamSynchronize(st));
@@ -1123,13 +1176,14 @@ struct sc_lanczos {
         static const bool dbg = std::getenv("SPECLUST_FLUSH_DEBUG") != nullptr;
         if (dbg && restarts > 0 && flushes % 10 == 0) {
             // loss against the retained Ritz block (rows < k of H) vs the sweep's vectors
-            std::vector<double> hh((size_t)c0 * c);
+            std::vector<double> hh((size_t)nb * c);
             SC_CUDA(cudaMemcpy(hh.data(), bH.p, sizeof(double) * hh.size(), cudaMemcpyDeviceToHost));
             double lr = 0.0, ls = 0.0;
-            for (int64_t r = 0; r < c0; ++r)
-                for (int o = 0; o < c; ++o) (r < k ? lr : ls) = std::max(r < k ? lr : ls, std::fabs(hh[r * c + o]));
-            fprintf(stderr, "[flush] restart %lld j %lld c %d loss_ritz %.2e loss_sweep %.2e\n", (long long)restarts,
-                    (long long)c1, c, lr, ls);
+            for (int64_t r = 0; r < nb; ++r)
+                for (int o = 0; o < c; ++o)
+                    (ob + r < k ? lr : ls) = std::max(ob + r < k ? lr : ls, std::fabs(hh[r * c + o]));
+            fprintf(stderr, "[flush] restart %lld j %lld c %d old [%lld, %lld) loss_ritz %.2e loss_sweep %.2e\n",
+                    (long long)restarts, (long long)c1, c, (long long)ob, (long long)oe, lr, ls);
         }
         ++flushes;
         window_sum += c;
@@ -1155,10 +1209,10 @@ struct sc_lanczos {
         // (aim at 1e-11: the growth rate is not steady -- it rises as Ritz
         // values converge inside a sweep -- so keep two decades of headroom
         // below the 1e-9 the window must not exceed)
-        double target = (double)kMaxWindow;
+        double target = (double)wmax;
         if (loss > 1e-16) target = (double)c * 5.0 / std::log10(loss / 1e-16);
         if (loss > 1e-9) target = std::min(target, (double)c / 2);
-        win = std::max<int64_t>(2, std::min<int64_t>({kMaxWindow, (int64_t)target, (int64_t)c + 1}));
+        wv = std::max<int64_t>(2, std::min<int64_t>({wmax, (int64_t)target, (int64_t)c + 1}));
         return SC_OK;
     }
     // Y = B[:, :m] S[:, :k]
@@ -1204,7 +1258,7 @@ struct sc_lanczos {
         for (int64_t i = 0; i < k; ++i) {
             est_k[i] = beta * std::fabs(lr[i]);
             worst = std::max(worst, est_k[i]);
-            if (!(est_k[i] <= tol * std::max(1.0, std::fabs(theta_k[i])))) converged = false;
+            if (!(est_k[i] <= kConvMargin * tol * std::max(1.0, std::fabs(theta_k[i])))) converged = false;
         }
         history.push_back(worst);
         bool verified = false;
@@ -1263,6 +1317,7 @@ struct sc_lanczos {
         }
         j = k;
         j0 = k;
+        js = k;
         return SC_OK;
     }
 

@@ -66,10 +66,8 @@ def _solve(a, k, mode):
     from paper_1802_04450_b200.eigen import eigensolve_device
 
     old = os.environ.get("SPECLUST_REORTH")
-    if mode == "full":
-        os.environ["SPECLUST_REORTH"] = "full"
-    else:
-        os.environ.pop("SPECLUST_REORTH", None)
+    # windowed mode is the default only from 32768 rows on; "window" forces it
+    os.environ["SPECLUST_REORTH"] = "full" if mode == "full" else "window"
     try:
         vals, vecs, res, stats = eigensolve_device(a.device(), sc.LanczosConfig(k=k, seed=0))
     finally:
