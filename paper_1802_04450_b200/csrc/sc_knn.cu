@@ -18,6 +18,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -94,6 +95,26 @@ __global__ void gather_pivots_kernel(int64_t C, int64_t d, const double* __restr
 // step to the closest unvisited one; ties -> lower index).  Pivots of one
 // dense region are mutual near neighbours, so the tour visits them in a run
 // and their buckets become one contiguous range of the scan order.
+// SPECLUST_TIMING_DEBUG=1: host wall time of the ordering phases on stderr
+struct PhaseClock {
+    cudaStream_t st;
+    bool on;
+    std::chrono::steady_clock::time_point t0;
+    explicit PhaseClock(cudaStream_t s) : st(s), on(std::getenv("SPECLUST_TIMING_DEBUG") != nullptr) {
+        if (on) {
+            cudaStreamSynchronize(st);
+            t0 = std::chrono::steady_clock::now();
+        }
+    }
+    void lap(const char* what) {
+        if (!on) return;
+        cudaStreamSynchronize(st);
+        const auto t1 = std::chrono::steady_clock::now();
+        fprintf(stderr, "[knn_order] %s %.3f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
+        t0 = t1;
+    }
+};
+
 static void pivot_tour(int64_t C, const std::vector<float>& D, std::vector<int32_t>& order) {
     std::vector<char> used((size_t)C, 0);
     order.assign(1, 0);
@@ -1259,6 +1280,7 @@ int knn_select(int64_t n, int64_t d, const double* x, int64_t knn, double two_si
             const int64_t C = std::min<int64_t>(1024, std::max<int64_t>(8, n / 1024));
             if ((rc = piv.alloc((size_t)C * d)) || (rc = plab.alloc(n)) || (rc = bk.init(n, C))) return rc;
             ProfScope prof_order("knn_order", st, 0.0);
+            PhaseClock pc(st);
             gather_strided_rows_kernel<<<(unsigned)C, 128, 0, st>>>(n, d, C, x, piv.p);
             SC_LAUNCHED(1);
             if (!std::getenv("SPECLUST_KNN_NOREFINE")) {
@@ -1280,6 +1302,7 @@ int knn_select(int64_t n, int64_t d, const double* x, int64_t knn, double two_si
                                    reinterpret_cast<sc_stream_t>(st))))
                     return rc;
                 SC_CUDA(cudaMemcpyAsync(piv.p, cent.p, sizeof(double) * C * d, cudaMemcpyDeviceToDevice, st));
+                pc.lap("refine (lloyd on pivots)");
             }
             if (!std::getenv("SPECLUST_KNN_NOTOUR")) {
                 // renumber the pivots along a nearest-neighbour tour: bucket
@@ -1304,7 +1327,9 @@ int knn_select(int64_t n, int64_t d, const double* x, int64_t knn, double two_si
                 SC_CUDA(cudaStreamSynchronize(st));  // `order` leaves scope
                 SC_LAUNCHED(1);
             }
+            pc.lap("tour");
             if ((rc = assign_nearest(n, d, x, C, piv.p, plab.p, st)) || (rc = bk.run(plab.p, st))) return rc;
+            pc.lap("assign + buckets");
             perm = bk.members.p;
         }
         if ((rc = xh.alloc((size_t)n_pad * dp64)) || (rc = cnf.alloc(n_pad))) return rc;

@@ -16,6 +16,7 @@
 // advance()).  T, the breakdown rule, the convergence/verification logic and
 // the thick restart follow eigen.py:166-239 exactly.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -1223,8 +1224,18 @@ struct sc_lanczos {
     }
 
     // eigen.py:187-239
+    std::chrono::steady_clock::time_point sweep_t0 = std::chrono::steady_clock::now();
     int finish_sweep(double beta) {
         int rc;
+        static const bool tdbg = std::getenv("SPECLUST_TIMING_DEBUG") != nullptr;
+        if (tdbg) {
+            cudaStreamSynchronize(st);
+            const auto t1 = std::chrono::steady_clock::now();
+            fprintf(stderr, "[lanczos] sweep %lld: %.3f ms, matvecs %lld, flushes %lld\n", (long long)restarts,
+                    std::chrono::duration<double, std::milli>(t1 - sweep_t0).count(), (long long)matvecs,
+                    (long long)flushes);
+            sweep_t0 = t1;
+        }
         // T is diag(theta) + arrow at row k after a restart, tridiagonal
         // before the first one: arrowhead divide and conquer (sc_dc.cu);
         // SPECLUST_SYMEIG=dense keeps the dense Householder + QL solver

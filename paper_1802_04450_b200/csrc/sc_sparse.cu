@@ -6,6 +6,8 @@
 // increasing within a row (sparse.py:110-138).
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
+#include <vector>
 
 #include "sc_common.cuh"
 #include "sc_sparse.cuh"
@@ -351,14 +353,117 @@ static void spmv_local_launch(int64_t n, const int64_t* row_ptr, const int32_t* 
     spmv_local_kernel<G><<<kNumSMs * bps, 256, 0, st>>>(n, row_ptr, col, vals, x, y);
 }
 
-// SpMV kernel choice.  Default: the per-SM-range warp kernel ("local").
+// "placed": spmv_local_kernel's per-SM row ranges with the block -> SM
+// placement MEASURED instead of assumed.  A probe kernel with the identical
+// launch configuration records %smid per block once; the host turns it into
+// per-block descriptors (range = the SM the block ran on, sub-index among
+// that SM's blocks), so the blocks sharing an SM (and its L1) share one
+// contiguous row range and its x working set.  Correctness does not depend
+// on the placement repeating (every range is covered by its descriptors);
+// only the L1 hit rate does.
+__global__ void smid_probe_kernel(int* __restrict__ out) {
+    if (threadIdx.x == 0) {
+        unsigned sm;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        out[blockIdx.x] = (int)sm;
+    }
+}
+
+template <int G>
+__global__ void __launch_bounds__(256) spmv_placed_kernel(int64_t n, const int64_t* __restrict__ row_ptr,
+                                                          const int32_t* __restrict__ col,
+                                                          const double* __restrict__ vals,
+                                                          const double* __restrict__ x, double* __restrict__ y,
+                                                          const int4* __restrict__ desc) {
+    constexpr int RPW = 32 / G;
+    const int4 dsc = desc[blockIdx.x];  // (range, sub-index, blocks in the range, ranges)
+    const int64_t r0 = n * dsc.x / dsc.w, r1 = n * (dsc.x + 1) / dsc.w;
+    const int lane = threadIdx.x & 31, sl = lane % G;
+    const int wpb = blockDim.x >> 5;
+    const int64_t stride = (int64_t)dsc.z * wpb * RPW;
+    for (int64_t base = r0 + ((int64_t)dsc.y * wpb + (threadIdx.x >> 5)) * RPW; base < r1; base += stride) {
+        const int64_t row = base + lane / G;
+        const bool valid = row < r1;
+        int64_t p = 0, e = 0;
+        if (valid) {
+            p = ld_stream(row_ptr + row) + sl;
+            e = ld_stream(row_ptr + row + 1);
+        }
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        for (; p + 3 * G < e; p += 4 * G) {
+            const int32_t c0 = ld_stream(col + p), c1 = ld_stream(col + p + G), c2 = ld_stream(col + p + 2 * G),
+                          c3 = ld_stream(col + p + 3 * G);
+            const double v0 = ld_stream(vals + p), v1 = ld_stream(vals + p + G), v2 = ld_stream(vals + p + 2 * G),
+                         v3 = ld_stream(vals + p + 3 * G);
+            a0 = fma(v0, ld_keep(x + c0), a0);
+            a1 = fma(v1, ld_keep(x + c1), a1);
+            a2 = fma(v2, ld_keep(x + c2), a2);
+            a3 = fma(v3, ld_keep(x + c3), a3);
+        }
+        if (p + G < e) {
+            const int32_t c0 = ld_stream(col + p), c1 = ld_stream(col + p + G);
+            const double v0 = ld_stream(vals + p), v1 = ld_stream(vals + p + G);
+            a0 = fma(v0, ld_keep(x + c0), a0);
+            a1 = fma(v1, ld_keep(x + c1), a1);
+            p += 2 * G;
+        }
+        if (p < e) a2 = fma(ld_stream(vals + p), ld_keep(x + ld_stream(col + p)), a2);
+        double acc = (a0 + a1) + (a2 + a3);
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, G);
+        if (valid && sl == 0) y[row] = acc;
+    }
+}
+
+template <int G>
+static int spmv_placed_launch(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* vals,
+                              const double* x, double* y, cudaStream_t st) {
+    static int bps = 0, nblk = 0;
+    static int4* desc = nullptr;  // device, built once per process (same launch configuration)
+    if (!desc) {
+        cudaFuncSetAttribute(spmv_placed_kernel<G>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+        cudaFuncSetAttribute(smid_probe_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, spmv_placed_kernel<G>, 256, 0);
+        if (bps < 1) bps = 1;
+        int dev = 0, nsm = kNumSMs;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        nblk = nsm * bps;
+        int* dsm = nullptr;
+        SC_CUDA(cudaMalloc(&dsm, sizeof(int) * nblk));
+        SC_CUDA(cudaStreamSynchronize(st));
+        smid_probe_kernel<<<nblk, 256, 0, st>>>(dsm);
+        std::vector<int> sm(nblk);
+        SC_CUDA(cudaMemcpyAsync(sm.data(), dsm, sizeof(int) * nblk, cudaMemcpyDeviceToHost, st));
+        SC_CUDA(cudaStreamSynchronize(st));
+        cudaFree(dsm);
+        // ranges: the distinct SMs seen, in id order; blocks numbered within each
+        std::vector<int> ids(sm), cnt;
+        std::sort(ids.begin(), ids.end());
+        ids.erase(std::unique(ids.begin(), ids.end()), ids.end());
+        cnt.assign(ids.size(), 0);
+        std::vector<int4> h(nblk);
+        for (int b = 0; b < nblk; ++b) {
+            const int r = (int)(std::lower_bound(ids.begin(), ids.end(), sm[b]) - ids.begin());
+            h[b] = make_int4(r, cnt[r]++, 0, (int)ids.size());
+        }
+        for (int b = 0; b < nblk; ++b) h[b].z = cnt[h[b].x];
+        SC_CUDA(cudaMalloc(&desc, sizeof(int4) * nblk));
+        SC_CUDA(cudaMemcpy(desc, h.data(), sizeof(int4) * nblk, cudaMemcpyHostToDevice));
+    }
+    spmv_placed_kernel<G><<<nblk, 256, 0, st>>>(n, row_ptr, col, vals, x, y, desc);
+    return SC_OK;
+}
+
+// SpMV kernel choice.  Default: "placed" (per-SM row ranges on the measured
+// block placement); "local" assumes block b runs on SM b % 148.
 // SPECLUST_SPMV_KERNEL overrides it (tuning and tests): "vec" (one row per
 // warp, flat grid), "affine" (SM-id ranges with stealing), "pipe"
 // (software-pipelined), "batch2"/"batch4"/"batch8" (R rows per warp),
 // "bulk" (SpmvPlan only: cp.async.bulk staged chunks).
 int spmv_kind() {
     const char* kenv = std::getenv("SPECLUST_SPMV_KERNEL");
-    if (!kenv) return 6;
+    if (!kenv) return 10;  // "placed": 0.26 vs 0.29 ms per C2 matvec for "local" (tools/spmv_c2.py)
     if (!std::strcmp(kenv, "vec")) return 0;
     if (!std::strcmp(kenv, "affine")) return 1;
     if (!std::strcmp(kenv, "batch2")) return 2;
@@ -366,6 +471,8 @@ int spmv_kind() {
     if (!std::strcmp(kenv, "pipe")) return 5;
     if (!std::strcmp(kenv, "batch8")) return 8;
     if (!std::strcmp(kenv, "bulk")) return 9;
+    if (!std::strcmp(kenv, "local")) return 6;
+    if (!std::strcmp(kenv, "placed")) return 10;
     return 6;
 }
 
@@ -399,6 +506,10 @@ int spmv_launch(int64_t n, int64_t nnz, const int64_t* row_ptr, const int32_t* c
             spmv_local_launch<16>(n, row_ptr, col, vals, x, y, st);
         else
             spmv_local_launch<8>(n, row_ptr, col, vals, x, y, st);
+    } else if (kind == 10 && n >= 4096) {
+        const int rc = mean_len > 24 ? spmv_placed_launch<16>(n, row_ptr, col, vals, x, y, st)
+                                     : spmv_placed_launch<8>(n, row_ptr, col, vals, x, y, st);
+        if (rc) return rc;
     } else if (kind == 1 && n >= 4096) {
         DevBuf<int> cur;
         int rc;

@@ -477,7 +477,7 @@ def _ragged_csr(n_rows, n_cols, seed):
     return rp, col, vals, rng.standard_normal(n_cols)
 
 
-@pytest.mark.parametrize("kernel", ["local", "vec", "affine", "pipe", "batch2", "batch4", "batch8", "bulk"])
+@pytest.mark.parametrize("kernel", ["placed", "local", "vec", "affine", "pipe", "batch2", "batch4", "batch8", "bulk"])
 @pytest.mark.parametrize("n_rows,n_cols", [(60_001, 60_001), (5000, 5000), (1, 7), (20_000, 70_000)])
 def test_spmv_kernels_and_plan_ragged(monkeypatch, kernel, n_rows, n_cols):
     """Every SpMV kernel variant, through sc_spmv_f64 and through an
