@@ -140,15 +140,17 @@ class CudaOps:
 
         return _points_device(x)
 
+    carries_vals = True  # the selection hands each slot's exact d2 to the union
+
     def knn_select(self, x, knn, measure, p0, p1):
         from .graph import knn_select_device
 
-        return knn_select_device(x, knn, measure, p0, p1)
+        return knn_select_device(x, knn, measure, p0, p1, with_vals=True)
 
-    def knn_union(self, x, knn, measure, sel, perm, r0, r1):
+    def knn_union(self, x, knn, measure, sel, perm, r0, r1, sel_vals=None):
         from .graph import knn_union_device
 
-        return knn_union_device(x, knn, measure, sel, perm, r0, r1)
+        return knn_union_device(x, knn, measure, sel, perm, r0, r1, sel_vals)
 
     def is_symmetric(self, w: DeviceCsr) -> bool:
         from .sparse import is_symmetric
@@ -387,9 +389,18 @@ def knn_graph_sharded(ops, comm: Comm, x, knn: int, measure):
     xd = ops.points(x)
     n = int(xd.shape[0])
     pb = scan_bounds(n, comm.world)
+    bounds = row_bounds(n, comm.world)
+    if getattr(ops, "carries_vals", False):
+        # the value-carrying union (as on one GPU): the exact d2 of every
+        # selection slot travels with the selection, so no rank recomputes
+        # distances for its reverse edges
+        sel_loc, perm, vals_loc = ops.knn_select(xd, knn, measure, pb[comm.rank], pb[comm.rank + 1])
+        sel = comm.gather_rows(sel_loc.contiguous(), pb)
+        sel_vals = comm.gather_rows(vals_loc.contiguous(), pb)
+        w_loc = ops.knn_union(xd, knn, measure, sel, perm, bounds[comm.rank], bounds[comm.rank + 1], sel_vals)
+        return w_loc, bounds
     sel_loc, perm = ops.knn_select(xd, knn, measure, pb[comm.rank], pb[comm.rank + 1])
     sel = comm.gather_rows(sel_loc.contiguous(), pb)
-    bounds = row_bounds(n, comm.world)
     w_loc = ops.knn_union(xd, knn, measure, sel, perm, bounds[comm.rank], bounds[comm.rank + 1])
     return w_loc, bounds
 

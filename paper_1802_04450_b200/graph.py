@@ -203,10 +203,12 @@ def _points_device(x):
     return nat.to_device(as_points(x), torch.float64)
 
 
-def knn_select_device(x, knn: int, m: SimilarityMeasure, p0: int, p1: int):
+def knn_select_device(x, knn: int, m: SimilarityMeasure, p0: int, p1: int, with_vals: bool = False):
     """Selection stage of the kNN graph for the points at scan positions
     [p0, p1) (sc_knn_select_f64): returns (sel (p1-p0, knn) int32 CUDA,
-    perm (n,) int32 CUDA scan order)."""
+    perm (n,) int32 CUDA scan order), plus with ``with_vals`` each slot's
+    exact d2 (p1-p0, knn) fp64 (sc_knn_select_vals_f64) for the
+    value-carrying union."""
     _require_exp_decay(m, "knn graph")
     torch = nat.torch_cuda()
     xd = _points_device(x)
@@ -215,6 +217,11 @@ def knn_select_device(x, knn: int, m: SimilarityMeasure, p0: int, p1: int):
         raise ValueError(f"knn must satisfy 1 <= knn < n, got {knn} for n={n}")
     sel = torch.empty((max(p1 - p0, 1), knn), dtype=torch.int32, device="cuda")
     perm = torch.empty(n, dtype=torch.int32, device="cuda")
+    if with_vals:
+        vals = torch.empty((max(p1 - p0, 1), knn), dtype=torch.float64, device="cuda")
+        nat.check(nat.load().sc_knn_select_vals_f64(n, d, nat.ptr(xd), knn, m.two_sigma_sq(), p0, p1, nat.ptr(sel),
+                                                    nat.ptr(vals), nat.ptr(perm), None, nat.stream_handle()))
+        return sel[: p1 - p0], perm, vals[: p1 - p0]
     nat.check(nat.load().sc_knn_select_f64(n, d, nat.ptr(xd), knn, m.two_sigma_sq(), p0, p1, nat.ptr(sel),
                                            nat.ptr(perm), None, nat.stream_handle()))
     return sel[: p1 - p0], perm

@@ -15,6 +15,10 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import os
+import sys
+import time
+
 import numpy as np
 
 from . import _native as nat
@@ -166,11 +170,20 @@ def kmeans_device(vd, cfg: KmeansConfig):
     if cfg.k > vd.shape[0]:
         raise BadConfig(f"k={cfg.k} exceeds number of points n={vd.shape[0]}")
     best = None
+    dbg = os.environ.get("SPECLUST_TIMING_DEBUG") is not None
     for r in range(cfg.restarts):
         seed = cfg.seed if r == 0 else int(np.random.SeedSequence([cfg.seed, r]).generate_state(1)[0])
+        t0 = time.perf_counter()
         rows = _init_rows(vd, cfg, seed)
         init_c = vd[torch.from_numpy(np.asarray(rows, dtype=np.int64)).to("cuda")].contiguous()
+        if dbg:
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
         cand = lloyd_device(vd, init_c, cfg)
+        if dbg:
+            torch.cuda.synchronize()
+            print(f"[kmeans] init {t1 - t0:.3f} s, lloyd {time.perf_counter() - t1:.3f} s ({cand[3]} iterations)",
+                  file=sys.stderr)
         if best is None or cand[2][-1] < best[2][-1]:
             best = cand
     return best

@@ -210,18 +210,27 @@ def test_knn_select_union_shards_reassemble(ops, n, d, knn, world):
     m = sc.SimilarityMeasure.exp_decay(1.7)
     xd = cu(x)
     pb = scan_bounds(n, world)
-    sels, perms = [], []
+    sels, perms, svals = [], [], []
     for r in range(world):
-        s, p = ops.knn_select(xd, knn, m, pb[r], pb[r + 1])
+        s, p, v = ops.knn_select(xd, knn, m, pb[r], pb[r + 1])
         sels.append(s)
         perms.append(p)
+        svals.append(v)
     for p in perms[1:]:
         assert torch.equal(p, perms[0])  # the scan order is replicated
     sel = torch.cat(sels)
+    sel_vals = torch.cat(svals)
     rb = row_bounds(n, world)
-    parts = [ops.knn_union(xd, knn, m, sel, perms[0], rb[r], rb[r + 1]) for r in range(world)]
-    rp, col, vals = _assemble(parts)
     full = knn_graph_device(x, knn, m)
+    # the value-carrying union (the sharded driver's) and the recomputing one
+    for sv in (sel_vals, None):
+        parts = [ops.knn_union(xd, knn, m, sel, perms[0], rb[r], rb[r + 1], sv) for r in range(world)]
+        rp2, col2, vals2 = _assemble(parts)
+        assert np.array_equal(rp2, full.row_ptr.cpu().numpy())
+        assert np.array_equal(col2, full.col.cpu().numpy())
+        assert np.array_equal(vals2, full.vals.cpu().numpy())
+    parts = [ops.knn_union(xd, knn, m, sel, perms[0], rb[r], rb[r + 1], sel_vals) for r in range(world)]
+    rp, col, vals = _assemble(parts)
     assert np.array_equal(rp, full.row_ptr.cpu().numpy())
     assert np.array_equal(col, full.col.cpu().numpy())
     assert np.array_equal(vals, full.vals.cpu().numpy())
