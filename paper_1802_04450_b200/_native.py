@@ -209,6 +209,21 @@ def ptr(t) -> vp:
     return vp(t.data_ptr()) if t is not None else vp(0)
 
 
+def empty_device(shape, dtype):
+    """torch.empty on the device; on an out-of-memory error the library's
+    cached pool is returned to the driver (sc_trim_pool) and PyTorch's own
+    cache emptied once before retrying -- the multi-GB n x k tensors of the
+    large configurations (C3: 32 GB each) land after stages whose buffers the
+    library still caches."""
+    torch = torch_cuda()
+    try:
+        return torch.empty(shape, dtype=dtype, device="cuda")
+    except torch.OutOfMemoryError:
+        load().sc_trim_pool()
+        torch.cuda.empty_cache()
+        return torch.empty(shape, dtype=dtype, device="cuda")
+
+
 def to_device(a, dtype):
     """numpy / torch -> contiguous CUDA tensor of `dtype` (torch dtype)."""
     torch = torch_cuda()

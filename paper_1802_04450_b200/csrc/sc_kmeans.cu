@@ -720,6 +720,7 @@ struct KppScreen {
     const double* vnorm = nullptr; // |v_i|
     const double* cnorm = nullptr; // |c| (device scalar)
     double s = 1.0;
+    unsigned long long* stats = nullptr;  // [0] rows screened, [1] rows the screen pruned
 };
 
 __global__ void kpp_centre_half_kernel(int64_t d, const double* __restrict__ row, double s, __half* __restrict__ ch,
@@ -762,7 +763,7 @@ __global__ void __launch_bounds__(KPP_UPD_ROWS) kpp_update_panel_kernel(int64_t 
         __syncthreads();
     }
     NpDot acc;
-    bool pruned = false;
+    bool pruned = false, screened = false, screen_pruned = false;
     double old = 0.0;
     if (i < n) {
         if (!first) old = d2[i];
@@ -791,7 +792,9 @@ __global__ void __launch_bounds__(KPP_UPD_ROWS) kpp_update_panel_kernel(int64_t 
             const double delta = 0x1p-11 * scr.s * (scr.vnorm[i] + scr.cnorm[0]) + 0x1p-24 * sqrt((double)d);
             const double rf = sqrt(fmax(0.0, (double)f * (1.0 - (double)(d + 8) * 0x1p-23)));
             const double lb = rf - delta;
+            screened = true;
             if (lb > 0.0 && lb * lb > old * scr.s * scr.s * (1.0 + 1e-9)) pruned = true;
+            screen_pruned = pruned;
         }
         for (int64_t c0 = 0; c0 < d && !pruned; c0 += 8) {
             const double2* src = reinterpret_cast<const double2*>(v8 + ((c0 >> 3) * n + i) * 8);
@@ -830,6 +833,13 @@ __global__ void __launch_bounds__(KPP_UPD_ROWS) kpp_update_panel_kernel(int64_t 
         if (!tk && nv > 0.0) {
             w = nv;
             cnt = 1;
+        }
+    }
+    if (scr.stats) {  // screen effectiveness, warp-aggregated
+        const unsigned bs = __ballot_sync(0xffffffffu, screened), bp = __ballot_sync(0xffffffffu, screen_pruned);
+        if ((threadIdx.x & 31) == 0 && bs) {
+            atomicAdd(&scr.stats[0], (unsigned long long)__popc(bs));
+            atomicAdd(&scr.stats[1], (unsigned long long)__popc(bp));
         }
     }
     kpp_block_partials(w, cnt, sw, scn, pw, pc);
@@ -1635,8 +1645,21 @@ struct sc_kmeanspp {
     DevBuf<uint4> vh8;
     DevBuf<__half> ch;
     DevBuf<double> vnorm, cnorm;
+    DevBuf<unsigned long long> sstat;  // screened / pruned row counts (kpp_update_panel_kernel)
     double hs = 1.0;
     bool screen = false;
+    int screened_draws = 0;
+    // the screen only pays when it prunes: on embeddings whose clusters are
+    // all at the same distance (orthogonal unit rows, e.g. C3) the fp16 bound
+    // cannot separate a new distance from the old one and every row still
+    // needs the exact pass -- after a few draws such a screen is switched off
+    void screen_review() {
+        if (!screen || ++screened_draws != 8) return;
+        unsigned long long h[2] = {0, 0};
+        cudaMemcpyAsync(h, sstat.p, sizeof(h), cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        if (h[0] > 0 && (double)h[1] < 0.25 * (double)h[0]) screen = false;
+    }
 
     // d2 <- min(d2, |v - row|^2) and the candidate partials (row: the drawn
     // point's coordinates, device; pick: its local index or -1)
@@ -1667,6 +1690,7 @@ struct sc_kmeanspp {
                 scr.vnorm = vnorm.p;
                 scr.cnorm = cnorm.p;
                 scr.s = hs;
+                scr.stats = sstat.p;
                 smem = (size_t)ceil_div(d, 8) * 8 * sizeof(__half);
             }
             kpp_update_panel_kernel<<<(unsigned)nb_upd, KPP_UPD_ROWS, smem, st>>>(
@@ -1840,7 +1864,8 @@ int sc_kmeanspp_create(int64_t n, int64_t d, const double* v, sc_stream_t stream
         const char* env = std::getenv("SPECLUST_KPP_SCREEN");
         const bool want = !(env && env[0] == '0') && d >= 32 && d <= 8192;
         if (want && s->vh8.alloc((size_t)nch * n) == SC_OK && s->ch.alloc((size_t)nch * 8) == SC_OK &&
-            s->vnorm.alloc(n) == SC_OK && s->cnorm.alloc(1) == SC_OK) {
+            s->vnorm.alloc(n) == SC_OK && s->cnorm.alloc(1) == SC_OK && s->sstat.alloc(2) == SC_OK) {
+            cudaMemsetAsync(s->sstat.p, 0, 2 * sizeof(unsigned long long), s->st);
             DevBuf<unsigned long long> amax;
             if (amax.alloc(1) == SC_OK) {
                 cudaMemsetAsync(amax.p, 0, sizeof(unsigned long long), s->st);
@@ -1870,6 +1895,7 @@ void sc_kmeanspp_destroy(sc_kmeanspp_t* s) { delete s; }
 int sc_kmeanspp_take(sc_kmeanspp_t* s, int64_t index) {
     if (index < 0 || index >= s->n) return fail(SC_ERR_VALUE, "k-means++ index out of range");
     if (int rc = s->update(s->v + index * s->d, index)) return rc;
+    if (!s->first) s->screen_review();
     kpp_total_kernel<<<1, 1024, 0, s->st>>>(s->nb_upd, s->pw.p, s->pc.p, s->total.p, s->count.p);
     SC_LAUNCHED(1);
     s->first = false;

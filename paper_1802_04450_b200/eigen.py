@@ -230,7 +230,7 @@ def eigensolve_device(a: DeviceCsr, cfg: LanczosConfig, probe: bool = True):
         check_symmetric_device(a, cfg.seed)
     vals = np.zeros(cfg.k)
     res = np.zeros(cfg.k)
-    vecs = torch.empty((n, cfg.k), dtype=torch.float64, device="cuda")
+    vecs = nat.empty_device((n, cfg.k), torch.float64)
     st = nat.LanczosStats()
     rc = nat.load().sc_eigensolve_csr(n, nat.ptr(a.row_ptr), nat.ptr(a.col), nat.ptr(a.vals), cfg.k, m,
                                       float(cfg.tol), cfg.max_restarts, int(cfg.seed) & (2**64 - 1),

@@ -132,7 +132,7 @@ def recover_embedding_device(u, d, normalize_rows: bool):
     CUDA (n, k) float64 tensor."""
     torch = nat.torch_cuda()
     n, k = u.shape
-    out = torch.empty_like(u)
+    out = nat.empty_device(tuple(u.shape), u.dtype)
     nat.check(nat.load().sc_recover_embedding(n, k, nat.ptr(u), nat.ptr(d), 1 if normalize_rows else 0,
                                               nat.ptr(out), nat.stream_handle()))
     return out
