@@ -1480,7 +1480,9 @@ struct AssignTc {
     DevBuf<double> v8;                // the points in 8-column panels (exact costs)
     // eligible: enough rows to pay for the conversion; SPECLUST_ASSIGN=fp64 disables.
     // dp <= 256: point tiles resident in shared memory; wider: K-chunk ring
-    int init(int64_t n_, int64_t d_, int64_t k, const double* v, cudaStream_t st) {
+    // exact = false: only the uncertified argmin will be asked for (no exact
+    // costs), so the fp64 panel copy of the points is not built
+    int init(int64_t n_, int64_t d_, int64_t k, const double* v, cudaStream_t st, bool exact = true) {
         n = n_;
         d = d_;
         dp = (d + 63) / 64 * 64;
@@ -1506,7 +1508,7 @@ struct AssignTc {
         as_prep_rows_kernel<<<(unsigned)ceil_div(n_pad, 8), 256, 0, st>>>(n, n_pad, d, dp, v, s, vh.p);
         SC_LAUNCHED(1);
         const int64_t nch = ceil_div(d, 8);
-        if (v8.alloc((size_t)nch * n * 8) == SC_OK) {  // optional: the staged kernel otherwise
+        if (exact && v8.alloc((size_t)nch * n * 8) == SC_OK) {  // optional: the staged kernel otherwise
             to_panels_kernel<<<(unsigned)ceil_div(nch * n * 8, 256), 256, 0, st>>>(n, d, v, v8.p);
             SC_LAUNCHED(1);
         }
@@ -1611,7 +1613,7 @@ int assign_nearest(int64_t n, int64_t d, const double* v, int64_t k, const doubl
     rownorm_kernel<<<(unsigned)ceil_div(k, 256), 256, 0, st>>>(k, d, c, cn.p);
     SC_LAUNCHED(2);
     AssignTc atc;
-    if ((rc = atc.init(n, d, k, v, st))) return rc;
+    if ((rc = atc.init(n, d, k, v, st, false))) return rc;
     if (atc.active) return atc.assign(k, v, vn.p, c, cn.p, nullptr, labels, cost.p, changes.p, st, false);
     dist_tile_kernel<0><<<(unsigned)nb, 256, 0, st>>>(n, k, d, v, vn.p, c, cn.p, nullptr, labels, nullptr, cost.p,
                                                       changes.p, part.p);

@@ -249,7 +249,7 @@ def test_knn_union_capacity_error_reports_size(ops):
     x, _ = orc.blobs(500, 4, 3, 3.0, seed=1)
     m = sc.SimilarityMeasure.exp_decay(1.0)
     xd = cu(x)
-    sel, perm = ops.knn_select(xd, 5, m, 0, 500)
+    sel, perm, _ = ops.knn_select(xd, 5, m, 0, 500)
     rp = torch.empty(501, dtype=torch.int64, device="cuda")
     col = torch.empty(4, dtype=torch.int32, device="cuda")
     vals = torch.empty(4, dtype=torch.float64, device="cuda")
