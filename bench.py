@@ -298,6 +298,7 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=8000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the public-API end-to-end timing (ncu runs)")
+    ap.add_argument("--no-syn200", action="store_true", help="skip the extra Syn200 run (PAPER.md:536-550)")
     ap.add_argument("--no-c3", action="store_true",
                     help="skip the extra full-size C3 run (BASELINE.json configs[2] on this GPU) reported under 'c3'")
     ap.add_argument("--sharded", action="store_true",
@@ -478,7 +479,7 @@ def main():
     }
     clk = clocks.summary()
     line["clocks"] = clk
-    if rank == 0 and world == 1:
+    if rank == 0 and world == 1 and not args.no_syn200:
         line["syn200"] = syn200_run(torch, sc, run_device)
     if rank == 0 and world == 1 and not args.no_c3 and args.workload != "c3":
         line["c3"] = c3_run(torch, sc, nat, run_device, lib)
