@@ -98,6 +98,40 @@ class Comm:
         self.dist.all_gather(parts, t, group=self.group)
         return torch.stack(parts).cpu().numpy()
 
+    def exchange_rows(self, local, dest_rank, dest_idx, out_rows: int):
+        """Row permutation across ranks: row i of ``local`` goes to rank
+        dest_rank[i] as its row dest_idx[i]; returns this rank's (out_rows,
+        ...) result.  One all-to-all (counts first); gloo has no CUDA
+        all-to-all, so there the payload is staged through host memory."""
+        torch = self.torch
+        out = torch.empty((out_rows,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+        if self.world == 1:
+            out[dest_idx.long()] = local
+            return out
+        order = torch.argsort(dest_rank, stable=True)
+        send, send_idx = local[order].contiguous(), dest_idx[order].to(torch.int64).contiguous()
+        in_splits = torch.bincount(dest_rank.long(), minlength=self.world)
+        counts = torch.empty(self.world * self.world, dtype=torch.int64, device=in_splits.device)
+        self.dist.all_gather_into_tensor(counts, in_splits.to(torch.int64), group=self.group) if \
+            local.device.type == "cuda" and self.dist.get_backend(self.group) == "nccl" else \
+            self._all_gather_flat(counts, in_splits.to(torch.int64))
+        cm = counts.view(self.world, self.world).cpu()
+        ins = cm[self.rank].tolist()
+        outs = cm[:, self.rank].tolist()
+        host = local.device.type == "cuda" and self.dist.get_backend(self.group) != "nccl"
+        dev = torch.device("cpu") if host else local.device
+        recv = torch.empty((sum(outs),) + tuple(local.shape[1:]), dtype=local.dtype, device=dev)
+        recv_idx = torch.empty(sum(outs), dtype=torch.int64, device=dev)
+        self.dist.all_to_all_single(recv, send.to(dev), outs, ins, group=self.group)
+        self.dist.all_to_all_single(recv_idx, send_idx.to(dev), outs, ins, group=self.group)
+        out[recv_idx.to(out.device)] = recv.to(out.device)
+        return out
+
+    def _all_gather_flat(self, out, t):
+        parts = [self.torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(parts, t, group=self.group)
+        out.copy_(self.torch.cat(parts))
+
     def bcast_(self, t, src):
         if self.world > 1:
             self.dist.broadcast(t, src=src, group=self.group)
@@ -214,13 +248,20 @@ class CudaOps:
         nat.check(self.lib.sc_fill_normal(n, offset, seed & (2**64 - 1), stream_id, nat.ptr(out), self._s()))
         return out
 
-    def symeig(self, T: np.ndarray, k: int):
-        """(theta host (m,) stable descending, S device (k, m): row c = eigenvector c)."""
+    def symeig(self, T: np.ndarray, k: int, p=None):
+        """(theta host (m,) stable descending, S device (k, m): row c =
+        eigenvector c).  With p: T's rows 0..p-1 are diag(theta) coupled only
+        to row p (the thick restart's arrowhead), the rest tridiagonal -- the
+        arrowhead divide and conquer of the single-GPU solver; p=None: any
+        dense symmetric T (Householder + QL)."""
         m = T.shape[0]
         Td = nat.to_device(np.asfortranarray(T).ravel(order="F"), self.torch.float64)
         theta = self.torch.empty(m, dtype=self.torch.float64, device="cuda")
         S = self.torch.empty((k, m), dtype=self.torch.float64, device="cuda")
-        nat.check(self.lib.sc_symeig_f64(m, k, nat.ptr(Td), nat.ptr(theta), nat.ptr(S), self._s()))
+        if p is None:
+            nat.check(self.lib.sc_symeig_f64(m, k, nat.ptr(Td), nat.ptr(theta), nat.ptr(S), self._s()))
+        else:
+            nat.check(self.lib.sc_symeig_arrow_f64(m, p, k, nat.ptr(Td), nat.ptr(theta), nat.ptr(S), self._s()))
         return nat.to_host(theta), S
 
     def ritz(self, B, nl, m, S, k, rowmajor=False):
@@ -405,6 +446,21 @@ def knn_graph_sharded(ops, comm: Comm, x, knn: int, measure):
     return w_loc, bounds
 
 
+def knn_graph_sharded_full(ops, comm: Comm, x, knn: int, measure):
+    """Like knn_graph_sharded, but every rank emits the WHOLE union from the
+    gathered selection (O(nnz) replicated work; the O(N^2 d) candidate scan
+    stays sharded), so the eigensolver can run on the locality-ordered
+    operator P A P^T in scan-order row blocks, as on one GPU.  Returns (W,
+    perm)."""
+    xd = ops.points(x)
+    n = int(xd.shape[0])
+    pb = scan_bounds(n, comm.world)
+    sel_loc, perm, vals_loc = ops.knn_select(xd, knn, measure, pb[comm.rank], pb[comm.rank + 1])
+    sel = comm.gather_rows(sel_loc.contiguous(), pb)
+    sel_vals = comm.gather_rows(vals_loc.contiguous(), pb)
+    return ops.knn_union(xd, knn, measure, sel, perm, 0, n, sel_vals), perm
+
+
 # ---------------------------------------------------------------------------
 # row-sharded thick-restart Lanczos (eigen.py:86-302)
 def lanczos_sharded(ops, comm: Comm, a_local, n: int, bounds, cfg: LanczosConfig):
@@ -508,7 +564,7 @@ def _lanczos_sharded(ops, comm, a_local, n, bounds, cfg, op):
             j += 1
             continue
         # ---- sweep complete (eigen.py:187-239), replicated on every rank
-        theta, S = ops.symeig(T, k)
+        theta, S = ops.symeig(T, k, k if st["restarts"] > 0 else 0)
         last = ops.host(S[:, m - 1])
         est = beta * np.abs(last)
         st["history"].append(float(est.max()))
@@ -692,12 +748,21 @@ def run_sharded(cfg, comm: Comm, ops=None):
 
     t = time.perf_counter()
     src = cfg.input
+    # locality-ordered eigensolve (the single-GPU pipeline's P A P^T in scan
+    # order) whenever the ops carry the selection's values (CUDA shards)
+    locality = isinstance(src, PointsInput) and src.pattern == "knn" and getattr(ops, "carries_vals", False)
     if isinstance(src, PointsInput) and src.pattern == "knn":
         pts = src.points if isinstance(src.points, torch.Tensor) else as_points(src.points)
         if src.measure.kind != "exp_decay":
             raise NotImplementedError("the sharded kNN graph supports the exp_decay measure")
-        w_loc, bounds = knn_graph_sharded(ops, comm, pts, src.knn, src.measure)
-        n = bounds[-1]
+        if locality:
+            w_full, perm = knn_graph_sharded_full(ops, comm, pts, src.knn, src.measure)
+            n = w_full.n_rows
+            bounds = row_bounds(n, comm.world)
+            w_loc = ops.slice_rows(w_full, bounds[comm.rank], bounds[comm.rank + 1])
+        else:
+            w_loc, bounds = knn_graph_sharded(ops, comm, pts, src.knn, src.measure)
+            n = bounds[-1]
     elif isinstance(src, MatrixInput) and src.matrix is not None:
         from .sparse import CsrMatrix, coo_canonicalize, coo_to_csr
 
@@ -722,9 +787,14 @@ def run_sharded(cfg, comm: Comm, ops=None):
     timings["graph"] = time.perf_counter() - t
 
     t = time.perf_counter()
-    d_loc = ops.degrees(w_loc)
-    zeros = int(comm.gather_scalars([ops.zeros_count(d_loc)])[:, 0].sum())
-    d_full = comm.gather_rows(d_loc, bounds)
+    if locality:  # replicated: every rank holds the whole W
+        d_full = ops.degrees(w_full)
+        d_loc = d_full[r0:r1]
+        zeros = ops.zeros_count(d_full)
+    else:
+        d_loc = ops.degrees(w_loc)
+        zeros = int(comm.gather_scalars([ops.zeros_count(d_loc)])[:, 0].sum())
+        d_full = comm.gather_rows(d_loc, bounds)
     if zeros:
         if cfg.isolated_policy == "error":
             idx = np.flatnonzero(ops.host(d_full) == 0.0)
@@ -737,11 +807,25 @@ def run_sharded(cfg, comm: Comm, ops=None):
 
     t = time.perf_counter()
     ecfg = cfg.eigen if cfg.eigen is not None else LanczosConfig(k=cfg.k_clusters)
-    a_loc = ops.sym_scale_shard(w_loc, r0, d_full)
+    if locality:
+        from .pipeline import permute_device
+
+        a_p, pos = permute_device(ops.sym_scale_shard(w_full, 0, d_full), perm)
+        a_loc = ops.slice_rows(a_p, r0, r1)  # scan positions [r0, r1)
+        del a_p
+    else:
+        a_loc = ops.sym_scale_shard(w_loc, r0, d_full)
     try:
         values, U, residuals, est = lanczos_sharded(ops, comm, a_loc, n, bounds, ecfg)
     except MaxRestartsExceeded as e:
         raise EigenNotConverged(e) from e
+    if locality:
+        # the eigenvector rows back to point order (the k-means++ draws index
+        # points): scan position r0 + i holds point perm[r0 + i]
+        pts_ids = perm[r0:r1].to(torch.int64)
+        bt = torch.tensor(bounds, dtype=torch.int64, device=pts_ids.device)
+        owner = torch.searchsorted(bt, pts_ids, right=True) - 1
+        U = comm.exchange_rows(U.contiguous(), owner, pts_ids - bt[owner], r1 - r0)
     V, colsq = ops.embed_scale(U, d_loc)
     comm.sum_(colsq)
     V = ops.embed_finish(V, colsq, cfg.normalize_rows)
@@ -774,7 +858,7 @@ def run_sharded(cfg, comm: Comm, ops=None):
     lab = Labeling(labels, ops.host(C), float(hist[-1]), iters, hist)
     last_info.clear()
     last_info["nnz"] = int(comm.gather_scalars([w_loc.nnz])[:, 0].sum())
-    last_info["eigen"] = dict(est, world=comm.world)
+    last_info["eigen"] = dict(est, world=comm.world, locality_order=locality)
     rep = ClusterReport(labeling=lab, eigenvalues=nat.frozen(values), eigen_residuals=nat.frozen(residuals),
                         ncut_value=ncut_value, timings=timings, warnings=warnings,
                         index_map=np.arange(n, dtype=np.int64))

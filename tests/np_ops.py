@@ -127,7 +127,7 @@ class NumpyOps:
         full = np.random.default_rng([seed, stream_id]).standard_normal(offset + n)
         return _t(full[offset:])
 
-    def symeig(self, T, k):
+    def symeig(self, T, k, p=None):
         theta, s = np.linalg.eigh(T)
         order = np.argsort(-theta, kind="stable")
         return theta[order], _t(s[:, order[:k]].T)
