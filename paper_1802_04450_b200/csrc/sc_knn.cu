@@ -1180,7 +1180,7 @@ int knn_candidates_tc(int64_t n, int64_t n_pad, int64_t dp64, const __half* xh, 
     if (!(tenv && std::strcmp(tenv, "1") == 0) && dp64 <= 128) {
         if (dp64 == 64)
             return launch_tc2<1, 6>(map, n, ntiles, qtile0, nq, cnk, key_scale, cap, R, lists, counts, taus, st);
-        return launch_tc2<2, 3>(map, n, ntiles, qtile0, nq, cnk, key_scale, cap, R, lists, counts, taus, st);
+        return launch_tc2<2, 2>(map, n, ntiles, qtile0, nq, cnk, key_scale, cap, R, lists, counts, taus, st);
     }
     switch (dp64 / 64) {
         case 1: return launch_tc<1, 4, false>(map, n, ntiles, qtile0, nq, cnk, key_scale, cap, R, lists, counts, taus, st);

@@ -42,7 +42,7 @@ template <int NKB, int STAGES>
 struct Tc2Layout {
     static constexpr uint32_t kA = 2 * NKB * TC_TILE_BYTES;  // two query tiles
     static constexpr uint32_t kB = NKB * TC_TILE_BYTES;
-    static constexpr uint32_t kL = 256 * 16 * 4;  // 16 staged keys per epilogue thread
+    static constexpr uint32_t kL = 256 * 64 * 4;  // 64 staged keys per epilogue thread (first half / quarters)
     static constexpr uint32_t kCn = TC2_CN_RING * 128 * 4;
     static constexpr uint32_t kBar = 8 * (2 * STAGES + 5 + 2 * TC2_CN_RING) + 8;
     static constexpr uint32_t total = 1024 + kA + STAGES * kB + kL + kCn + kBar;
@@ -289,8 +289,10 @@ __global__ void __launch_bounds__(TC2_THREADS, 1)
         const int64_t slot = lq0 * 128 + lrow;  // list slot of this row
         float2* L = lists + (valid ? slot : 0) * (int64_t)cap;
         float2* H = sH + (size_t)lrow * R;
-        float* stage = HEAP ? sStage + ((size_t)(warp - 2) * 32 + lane) * 16
-                            : reinterpret_cast<float*>(sL) + ((size_t)(warp - 2) * 32 + lane) * 16;
+        // per thread: 64 floats of staged first-half keys, then (HEAP: its
+        // own slot) 16 floats of quarter staging for the append loop
+        float* skeys = reinterpret_cast<float*>(sL) + ((size_t)(warp - 2) * 32 + lane) * 64;
+        float* stage = HEAP ? sStage + ((size_t)(warp - 2) * 32 + lane) * 16 : skeys;
         int cnt = 0;
         float tau = INFINITY;
         long long dbg_c[3] = {0, 0, 0}, dbg_f[3] = {0, 0, 0};
@@ -340,38 +342,52 @@ __global__ void __launch_bounds__(TC2_THREADS, 1)
                 }
                 continue;
             }
-            // both 64-column halves of this row's accumulator in one TMEM round trip
-            float v[128];
-            tc::tmem_ld64(taddr, v);
-            tc::tmem_ld64(taddr + 64, v + 64);
+            // the accumulator in two 64-column halves through the same 64
+            // registers: the first half's keys go to shared memory only when
+            // its filter fires, so the tile loop needs half the registers
+            // (with both halves live, 168 registers and spills)
+            const uint32_t cn_s = tc::smem_u32(sCn + cslot * 128);
+            float va[64];
+            float qm[8];
+            auto keys_half = [&](int hf) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    float m = INFINITY;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const float4 cn4 = lds_f4(cn_s + (uint32_t)(16 * (4 * (4 * hf + q) + u)));  // smem broadcast
+                        float* e = va + 16 * q + 4 * u;
+                        const float2 k01 = ffma2(ks, make_float2(e[0], e[1]), make_float2(cn4.x, cn4.y));
+                        const float2 k23 = ffma2(ks, make_float2(e[2], e[3]), make_float2(cn4.z, cn4.w));
+                        e[0] = k01.x;
+                        e[1] = k01.y;
+                        e[2] = k23.x;
+                        e[3] = k23.y;
+                        m = fmin3(m, fmin3(k01.x, k01.y, k23.x), k23.y);
+                    }
+                    qm[4 * hf + q] = m;
+                }
+            };
+            tc::tmem_ld64(taddr, va);
             tc::tmem_wait_ld();
-            // the accumulator is in registers: hand the TMEM buffer back now,
-            // so the MMA of tile t + 2 overlaps this tile's list work
+            keys_half(0);
+            const float h0 = fminf(fminf(qm[0], qm[1]), fminf(qm[2], qm[3]));
+            const bool fire0 = !capneg && !(WMODE & 16) && __any_sync(0xffffffffu, valid && h0 < tau);
+            if (fire0) {
+                float4* d4 = reinterpret_cast<float4*>(skeys);
+#pragma unroll
+                for (int u = 0; u < 16; ++u) d4[u] = make_float4(va[4 * u], va[4 * u + 1], va[4 * u + 2], va[4 * u + 3]);
+            }
+            tc::tmem_ld64(taddr + 64, va);
+            tc::tmem_wait_ld();
+            // the accumulator is in registers / shared memory: hand the TMEM
+            // buffer back, so the MMA of tile t + 2 overlaps this tile's list work
             tc::fence_before();
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&tempty[buf]);
-            const uint32_t cn_s = tc::smem_u32(sCn + cslot * 128);
-            float qm[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                float m = INFINITY;
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const float4 cn4 = lds_f4(cn_s + (uint32_t)(16 * (4 * q + u)));  // smem broadcast
-                    float* e = v + 16 * q + 4 * u;
-                    const float2 k01 = ffma2(ks, make_float2(e[0], e[1]), make_float2(cn4.x, cn4.y));
-                    const float2 k23 = ffma2(ks, make_float2(e[2], e[3]), make_float2(cn4.z, cn4.w));
-                    e[0] = k01.x;
-                    e[1] = k01.y;
-                    e[2] = k23.x;
-                    e[3] = k23.y;
-                    m = fmin3(m, fmin3(k01.x, k01.y, k23.x), k23.y);
-                }
-                qm[q] = m;
-            }
+            keys_half(1);
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&cempty[cslot]);  // column norms consumed
-            const float h0 = fminf(fminf(qm[0], qm[1]), fminf(qm[2], qm[3]));
             const float h1 = fminf(fminf(qm[4], qm[5]), fminf(qm[6], qm[7]));
             // rare path: append the passing keys of a 64-column half to the row's list
             auto slow = [&](const float* keys64, const float* qm4, int64_t cbase) {
@@ -441,17 +457,17 @@ __global__ void __launch_bounds__(TC2_THREADS, 1)
             };
             if (capneg) {
             } else if (HEAP) {
-                if (!(WMODE & 16) && __any_sync(0xffffffffu, valid && h0 < tau)) slow_heap(v, qm, col0);
-                if (!(WMODE & 16) && __any_sync(0xffffffffu, valid && h1 < tau)) slow_heap(v + 64, qm + 4, col0 + 64);
+                if (fire0) slow_heap(skeys, qm, col0);
+                if (!(WMODE & 16) && __any_sync(0xffffffffu, valid && h1 < tau)) slow_heap(va, qm + 4, col0 + 64);
             } else {
                 const long long z0 = (WMODE & 64) ? clock64() : 0;
                 int fired = 0;
-                if (!(WMODE & 16) && __any_sync(0xffffffffu, valid && h0 < tau)) {
-                    slow(v, qm, col0);
+                if (fire0) {
+                    slow(skeys, qm, col0);
                     ++fired;
                 }
                 if (!(WMODE & 16) && __any_sync(0xffffffffu, valid && h1 < tau)) {
-                    slow(v + 64, qm + 4, col0 + 64);
+                    slow(va, qm + 4, col0 + 64);
                     ++fired;
                 }
                 if (WMODE & 64) {
