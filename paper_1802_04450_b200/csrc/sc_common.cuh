@@ -10,7 +10,11 @@
 
 namespace sc {
 
-constexpr int kNumSMs = 148;  // B200: 2 dies x 74 SMs
+// B200: 2 dies x 74 SMs.  Used only to size grids (one or a few resident
+// waves); no result depends on it -- the placement-sensitive SpMV measures
+// the block -> SM placement itself (sc_sparse.cu, "placed"), and the
+// occupancy-sized launches query the device's SM count.
+constexpr int kNumSMs = 148;
 
 // ---- error plumbing ---------------------------------------------------------
 void set_error(const std::string& msg);

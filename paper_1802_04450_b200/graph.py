@@ -9,8 +9,10 @@ follow graph.py:149-157 / 136-141 of the reference.
 
 The other measures (cosine, cross-correlation) over a given edge list and the
 eps / threshold patterns run on the GPU as well
-(sc_patterns.cu); the kNN pattern with cosine / cross-correlation is not
-implemented and raises ``NotImplementedError`` (no host fallback).
+(sc_patterns.cu); the kNN pattern with cosine / cross-correlation runs the
+same tensor-core candidate scan on row-normalised operands with a
+cosine-space certificate (``sc_knn_graph_measure_f64``).  There is no host
+fallback anywhere.
 """
 
 from __future__ import annotations

@@ -1,9 +1,9 @@
 """Partition quality measures (drop-in for speclust.metrics).
 
 ``ncut`` — the one the pipeline reports — runs on the GPU with the
-reference's accumulation order (metrics.py:34-39, 59-67).  ``cut`` /
-``ratio_cut`` (CLI ``eval`` only, outside the hot path) and the
-Adjusted Rand Index (the parity judge, O(n) host bookkeeping) are numpy.
+reference's accumulation order (metrics.py:34-39, 59-67); so do ``cut`` and
+``ratio_cut`` (``sc_partition_cuts``).  The Adjusted Rand Index (the parity
+judge, O(n) host bookkeeping on labels) is numpy.
 """
 
 from __future__ import annotations
