@@ -67,6 +67,7 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.samples = []  # (sm_mhz, max_mhz, [4 flags])
+        self.period = 0.1
         self._stop = threading.Event()
         self._t = None
         try:
@@ -100,7 +101,7 @@ class ClockSampler:
                 self.samples.append(self._sample())
             except Exception:
                 pass
-            self._stop.wait(0.1)
+            self._stop.wait(self.period)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -288,6 +289,91 @@ def c3_run(torch, sc, nat, run_device, lib):
     return out
 
 
+def make_c5(torch, n, d=256, k=10_000, seed=0):
+    """C5's embedding (SURVEY.md:594): k Gaussian centres N(0, 1) in d
+    dimensions, points = centre + N(0, 0.3^2) noise, rows normalised; drawn
+    on the device in fp32 (10 GB at full size) and held in fp64 for Lloyd.
+    Init rows = default_rng(0).choice(n, k, replace=False), the reference's
+    ``random_points`` init (kmeans.py:203-205)."""
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    cen = torch.randn((k, d), generator=g, device="cuda", dtype=torch.float32)
+    lab = torch.randint(0, k, (n,), generator=g, device="cuda")
+    v = torch.empty((n, d), dtype=torch.float64, device="cuda")
+    step = 1 << 21
+    for a in range(0, n, step):
+        b = min(n, a + step)
+        t = cen[lab[a:b]] + 0.3 * torch.randn((b - a, d), generator=g, device="cuda", dtype=torch.float32)
+        t /= t.norm(dim=1, keepdim=True)
+        v[a:b] = t
+    rows = np.random.default_rng(0).choice(n, size=k, replace=False)
+    init = v[torch.from_numpy(rows).to("cuda")].contiguous()
+    return v, init, lab
+
+
+def c5_run(torch, n=10_000_000, iters=20):
+    """C5 at full size (BASELINE.json configs[4]: k-means on a 10M x 256
+    embedding, k = 10,000): a fixed ``iters`` Lloyd iterations
+    (tol_changes = 0, max_iters = iters) timed with CUDA events and no
+    profiling, then a second profiled run for the per-kernel rates."""
+    import paper_1802_04450_b200 as sc
+    from paper_1802_04450_b200 import _native as nat
+    from paper_1802_04450_b200.kmeans import lloyd_device
+
+    free, total = torch.cuda.mem_get_info()
+    if total < 100e9:
+        return {"skipped": f"needs ~60 GB of device memory, this GPU has {total / 1e9:.0f} GB"}
+    k, d = 10_000, 256
+    lib = nat.load()
+    v, init, lab = make_c5(torch, n, d, k)
+    cfg = sc.KmeansConfig(k=k, max_iters=iters, init="random_points")
+    lib.sc_profile_enable(0)
+    lloyd_device(v[: 1 << 16], init[:256].contiguous(), sc.KmeansConfig(k=256, max_iters=2))  # warm-up
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    labels, cent, hist, it = lloyd_device(v, init, cfg)
+    e1.record()
+    torch.cuda.synchronize()
+    secs = e0.elapsed_time(e1) / 1e3
+    out = {"workload": f"c5: Lloyd on a {n} x {d} embedding, k={k}, {iters} iterations from random_points "
+                       "(BASELINE.json configs[4])",
+           "seconds": secs, "iters_run": it, "s_per_iter": secs / max(1, it),
+           "sse_first": float(hist[0]), "sse_last": float(hist[-1]),
+           "sse_monotone": bool(np.all(np.diff(hist) <= 1e-9 * abs(hist[0]))),
+           "ari_vs_planted": float(sc.adjusted_rand_index(labels.cpu().numpy(), lab.cpu().numpy()))}
+    del labels, cent
+    lib.sc_profile_reset()
+    lib.sc_profile_enable(1)
+    lloyd_device(v, init, sc.KmeansConfig(k=k, max_iters=3, init="random_points"))
+    torch.cuda.synchronize()
+    lib.sc_profile_enable(0)
+    pk = peaks()
+    kern = {}
+    for c in ("kmeans_assign", "kmeans_update"):
+        ms, cnt, work = nat.C.c_double(), nat.C.c_int64(), nat.C.c_double()
+        lib.sc_profile_query(c.encode(), nat.C.byref(ms), nat.C.byref(cnt), nat.C.byref(work))
+        kern[c] = {"launches": cnt.value, "ms_total": round(ms.value, 3), "work": work.value}
+    a = kern["kmeans_assign"]
+    if a["ms_total"] > 0:
+        tf = a["work"] / (a["ms_total"] / 1e3) / 1e12
+        a["tflops"] = tf
+        a["frac_of_bf16_peak"] = tf / pk["bf16"]
+    out["kernels"] = kern
+    del v, init, lab
+    lib.sc_trim_pool()
+    torch.cuda.empty_cache()
+    return out
+
+
+def _extra(fn):
+    """An extra full-size run reported beside the C2 line: a failure is
+    reported in its key instead of losing the line."""
+    try:
+        return fn()
+    except Exception as e:  # noqa: BLE001
+        return {"error": f"{type(e).__name__}: {e}"[:300]}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -301,6 +387,8 @@ def main():
     ap.add_argument("--no-syn200", action="store_true", help="skip the extra Syn200 run (PAPER.md:536-550)")
     ap.add_argument("--no-c3", action="store_true",
                     help="skip the extra full-size C3 run (BASELINE.json configs[2] on this GPU) reported under 'c3'")
+    ap.add_argument("--no-c5", action="store_true",
+                    help="skip the extra full-size C5 k-means run (BASELINE.json configs[4]) reported under 'c5'")
     ap.add_argument("--sharded", action="store_true",
                     help="use the sharded driver (distributed.run_sharded) even at N=1; it is always used for N>1")
     args = ap.parse_args()
@@ -482,7 +570,9 @@ def main():
     if rank == 0 and world == 1 and not args.no_syn200:
         line["syn200"] = syn200_run(torch, sc, run_device)
     if rank == 0 and world == 1 and not args.no_c3 and args.workload != "c3":
-        line["c3"] = c3_run(torch, sc, nat, run_device, lib)
+        line["c3"] = _extra(lambda: c3_run(torch, sc, nat, run_device, lib))
+    if rank == 0 and world == 1 and not args.no_c5:
+        line["c5"] = _extra(lambda: c5_run(torch))
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         # measured CPU baseline: the oracle port on the full C1 workload
         # (BASELINE.json configs[0], the reference's own CPU-runnable case),

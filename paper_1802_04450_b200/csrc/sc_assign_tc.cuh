@@ -11,8 +11,16 @@
 // product in numpy's summation order).  The rest (near ties, exact
 // duplicates, clamp cases) are re-scanned exactly over all centroids.
 //
+// Every row also keeps its third-best key and centroid and the fourth-best
+// key: a row that misses the certificate but has at most three candidates
+// within 2 delta of its best (a point between two or three centroids of a
+// split cluster) is settled by exact fp64 keys of those candidates alone
+// (as_resolve_kernel); only the rest are re-scanned.
+//
 // Layout: CTA = QT point tiles of 128 rows (A, loaded once by TMA) against
-// the centroid tiles (B, a STAGES-deep TMA ring); a single thread issues the
+// the centroid tiles (B, a STAGES-deep TMA ring of 64-column K chunks, so two
+// resident point tiles fit next to it at d = 256 and every centroid chunk
+// read from L2 feeds M = 256 rows of MMA); a single thread issues the
 // M=128 x N=128 x K=16 fp16 MMAs into QT x 2 TMEM accumulators; 4*QT
 // epilogue warps (thread <-> point row, TMEM lane quarter warp % 4) turn a
 // tile into keys with packed f32x2 FMAs against the centroid norms (their
@@ -28,10 +36,69 @@ namespace sc {
 
 constexpr int AS_CN_RING = 8;
 
+// best three approximate keys (and centroids) of a row plus the fourth-best
+// key; a key equal to a kept one goes behind it
+struct AsTop3 {
+    float b1 = INFINITY, b2 = INFINITY, b3 = INFINITY, b4 = INFINITY;
+    int32_t i1 = -1, i2 = -1, i3 = -1;
+    __device__ __forceinline__ void push(float k, int32_t j) {
+        if (k < b2) {
+            b4 = b3;
+            b3 = b2;
+            i3 = i2;
+            if (k < b1) {
+                b2 = b1;
+                i2 = i1;
+                b1 = k;
+                i1 = j;
+            } else {
+                b2 = k;
+                i2 = j;
+            }
+        } else if (k < b3) {
+            b4 = b3;
+            b3 = k;
+            i3 = j;
+        } else if (k < b4) {
+            b4 = k;
+        }
+    }
+    __device__ __forceinline__ void store(int64_t row, int32_t* best_idx, float2* best_keys, int2* alt_idx,
+                                          float2* alt_keys) const {
+        best_idx[row] = i1;
+        best_keys[row] = make_float2(b1, b2);
+        alt_idx[row] = make_int2(i2, i3);
+        alt_keys[row] = make_float2(b3, b4);
+    }
+};
+
+// One 16-column quarter whose minimum beat the row's fourth-best key: the
+// columns below it as a bit mask (compares on the registers), then only
+// those are pushed, read back from the thread's stage slots (layout
+// [4][32 lanes] float4 per warp: conflict-free stores).
+__device__ __forceinline__ void as_walk_quarter(AsTop3& top, const float* e, uint32_t stage, int32_t cb) {
+    uint32_t mask = 0;
+#pragma unroll
+    for (int u = 0; u < 16; ++u) mask |= (e[u] < top.b4 ? 1u : 0u) << u;
+    if (!mask) return;
+#pragma unroll
+    for (int u4 = 0; u4 < 4; ++u4)
+        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(stage + u4 * 512), "f"(e[4 * u4]),
+                     "f"(e[4 * u4 + 1]), "f"(e[4 * u4 + 2]), "f"(e[4 * u4 + 3])
+                     : "memory");
+    while (mask) {
+        const int u = __ffs(mask) - 1;
+        mask &= mask - 1;
+        float k;
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(k) : "r"(stage + (uint32_t)((u >> 2) * 512 + (u & 3) * 4)));
+        if (k < top.b4) top.push(k, cb + u);
+    }
+}
+
 template <int NKB, int STAGES, int QT>
 struct AsLayout {
     static constexpr uint32_t kA = QT * NKB * TC_TILE_BYTES;
-    static constexpr uint32_t kB = NKB * TC_TILE_BYTES;
+    static constexpr uint32_t kB = TC_TILE_BYTES;  // one 128 x 64 centroid chunk per stage
     static constexpr uint32_t kStage = QT * 4 * 32 * 16 * 4;  // 16 staged keys per epilogue thread
     static constexpr uint32_t kCn = AS_CN_RING * 128 * 4;
     static constexpr uint32_t kBar = 8 * (2 * STAGES + 5 + 2 * AS_CN_RING) + 8;
@@ -42,7 +109,8 @@ template <int NKB, int STAGES, int QT>
 __global__ void __launch_bounds__(64 + QT * 128, 1)
     assign_tc_kernel(const __grid_constant__ CUtensorMap vmap, const __grid_constant__ CUtensorMap cmap, int64_t n,
                      int64_t nptiles, int64_t nctiles, const float* __restrict__ cnk, float key_scale,
-                     int32_t* __restrict__ best_idx, float2* __restrict__ best_keys) {
+                     int32_t* __restrict__ best_idx, float2* __restrict__ best_keys, int2* __restrict__ alt_idx,
+                     float2* __restrict__ alt_keys) {
     using Lay = AsLayout<NKB, STAGES, QT>;
     constexpr int NEPI = 4 * QT;
     extern __shared__ uint8_t smem_raw[];
@@ -98,40 +166,45 @@ __global__ void __launch_bounds__(64 + QT * 128, 1)
             for (int q = 0; q < QT; ++q)
                 for (int kb = 0; kb < NKB; ++kb)
                     tc::tma_load_2d(sA + (q * NKB + kb) * TC_TILE_BYTES, &vmap, afull, kb * 64, (int)((pt0 + q) * 128));
+            int64_t it = 0;
             for (int64_t t = 0; t < nctiles; ++t) {
-                const int s = (int)(t % STAGES);
-                mbar_wait_hw<true>(&empty[s], (uint32_t)(((t / STAGES) & 1) ^ 1));
-                tc::mbar_expect_tx(&full[s], Lay::kB);
-                for (int kb = 0; kb < NKB; ++kb)
-                    tc::tma_load_2d(sB + s * Lay::kB + kb * TC_TILE_BYTES, &cmap, &full[s], kb * 64, (int)(t * 128));
                 const int c = (int)(t % AS_CN_RING);
                 mbar_wait_hw<true>(&cempty[c], (uint32_t)(((t / AS_CN_RING) & 1) ^ 1));
                 tc::mbar_expect_tx(&cfull[c], 128 * 4);
                 tc::bulk_g2s(sCn + c * 128, cnk + t * 128, 128 * 4, &cfull[c]);
+                for (int kb = 0; kb < NKB; ++kb, ++it) {
+                    const int s = (int)(it % STAGES);
+                    mbar_wait_hw<true>(&empty[s], (uint32_t)(((it / STAGES) & 1) ^ 1));
+                    tc::mbar_expect_tx(&full[s], Lay::kB);
+                    tc::tma_load_2d(sB + s * Lay::kB, &cmap, &full[s], kb * 64, (int)(t * 128));
+                }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
             constexpr uint32_t idesc = tc::idesc_f16_f32(128, 128);
             mbar_wait_hw<true>(afull, 0);
+            int64_t it = 0;
             for (int64_t t = 0; t < nctiles; ++t) {
-                const int s = (int)(t % STAGES);
                 const int buf = (int)(t & 1);
                 mbar_wait_hw<true>(&tempty[buf], (uint32_t)(((t >> 1) & 1) ^ 1));
-                mbar_wait_hw<true>(&full[s], (uint32_t)((t / STAGES) & 1));
                 tc::fence_after();
 #pragma unroll
-                for (int q = 0; q < QT; ++q)
+                for (int kb = 0; kb < NKB; ++kb, ++it) {
+                    const int s = (int)(it % STAGES);
+                    mbar_wait_hw<true>(&full[s], (uint32_t)((it / STAGES) & 1));
+                    tc::fence_after();
+                    const uint64_t bd = tc::desc_k_sw128(sB + s * Lay::kB);
 #pragma unroll
-                    for (int kb = 0; kb < NKB; ++kb) {
+                    for (int q = 0; q < QT; ++q) {
                         const uint64_t ad = tc::desc_k_sw128(sA + (q * NKB + kb) * TC_TILE_BYTES);
-                        const uint64_t bd = tc::desc_k_sw128(sB + s * Lay::kB + kb * TC_TILE_BYTES);
 #pragma unroll
                         for (int k = 0; k < 4; ++k)
                             tc::umma_f16(tmem + buf * (QT * 128) + q * 128, ad + 2 * k, bd + 2 * k, idesc,
                                          (kb | k) != 0);
                     }
-                tc::umma_commit(&empty[s]);
+                    tc::umma_commit(&empty[s]);
+                }
                 tc::umma_commit(&tfull[buf]);
             }
         }
@@ -140,9 +213,8 @@ __global__ void __launch_bounds__(64 + QT * 128, 1)
         const int qi = (warp - 2) >> 2;
         const int64_t row = (pt0 + qi) * 128 + quad * 32 + lane;
         const bool valid = pt0 + qi < nptiles && row < n;
-        float* stage = sStage + ((size_t)(warp - 2) * 32 + lane) * 16;
-        float b1 = INFINITY, b2 = INFINITY;
-        int32_t i1 = -1;
+        const uint32_t stage = tc::smem_u32(sStage + (size_t)(warp - 2) * 512) + (uint32_t)lane * 16;
+        AsTop3 top;
         const float2 ks = make_float2(key_scale, key_scale);
         for (int64_t t = 0; t < nctiles; ++t) {
             const int buf = (int)(t & 1);
@@ -182,30 +254,11 @@ __global__ void __launch_bounds__(64 + QT * 128, 1)
             // padded centroid columns carry +inf norms, so they never win
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-                if (!(valid && qm[q] < b2)) continue;
-                float4* st4 = reinterpret_cast<float4*>(stage);
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    st4[u] = make_float4(v[16 * q + 4 * u], v[16 * q + 4 * u + 1], v[16 * q + 4 * u + 2],
-                                         v[16 * q + 4 * u + 3]);
-                const int32_t cb = (int32_t)(t * 128 + q * 16);
-#pragma unroll 1
-                for (int u = 0; u < 16; ++u) {
-                    const float k = stage[u];
-                    if (k < b1) {
-                        b2 = b1;
-                        b1 = k;
-                        i1 = cb + u;
-                    } else if (k < b2) {
-                        b2 = k;
-                    }
-                }
+                if (!(valid && qm[q] < top.b4)) continue;
+                as_walk_quarter(top, v + 16 * q, stage, (int32_t)(t * 128 + q * 16));
             }
         }
-        if (valid) {
-            best_idx[row] = i1;
-            best_keys[row] = make_float2(b1, b2);
-        }
+        if (valid) top.store(row, best_idx, best_keys, alt_idx, alt_keys);
     }
     __syncthreads();
     if (warp == 1) {
@@ -235,7 +288,8 @@ template <int STAGES, int QT>
 __global__ void __launch_bounds__(64 + QT * 128, 1)
     assign_tc_kl_kernel(const __grid_constant__ CUtensorMap vmap, const __grid_constant__ CUtensorMap cmap, int64_t n,
                         int64_t nptiles, int64_t nctiles, int nkb, const float* __restrict__ cnk, float key_scale,
-                        int32_t* __restrict__ best_idx, float2* __restrict__ best_keys) {
+                        int32_t* __restrict__ best_idx, float2* __restrict__ best_keys, int2* __restrict__ alt_idx,
+                        float2* __restrict__ alt_keys) {
     using Lay = AsKlLayout<STAGES, QT>;
     constexpr int NEPI = 4 * QT;
     extern __shared__ uint8_t smem_raw[];
@@ -335,9 +389,8 @@ __global__ void __launch_bounds__(64 + QT * 128, 1)
         const int qi = (warp - 2) >> 2;
         const int64_t row = (pt0 + qi) * 128 + quad * 32 + lane;
         const bool valid = qi < nq && row < n;
-        float* stage = sStage + ((size_t)(warp - 2) * 32 + lane) * 16;
-        float b1 = INFINITY, b2 = INFINITY;
-        int32_t i1 = -1;
+        const uint32_t stage = tc::smem_u32(sStage + (size_t)(warp - 2) * 512) + (uint32_t)lane * 16;
+        AsTop3 top;
         const float2 ks = make_float2(key_scale, key_scale);
         for (int64_t t = 0; t < nctiles; ++t) {
             const int buf = (int)(t & 1);
@@ -376,30 +429,11 @@ __global__ void __launch_bounds__(64 + QT * 128, 1)
             if (lane == 0) tc::mbar_arrive(&cempty[cslot]);
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-                if (!(valid && qm[q] < b2)) continue;
-                float4* st4 = reinterpret_cast<float4*>(stage);
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    st4[u] = make_float4(v[16 * q + 4 * u], v[16 * q + 4 * u + 1], v[16 * q + 4 * u + 2],
-                                         v[16 * q + 4 * u + 3]);
-                const int32_t cb = (int32_t)(t * 128 + q * 16);
-#pragma unroll 1
-                for (int u = 0; u < 16; ++u) {
-                    const float k = stage[u];
-                    if (k < b1) {
-                        b2 = b1;
-                        b1 = k;
-                        i1 = cb + u;
-                    } else if (k < b2) {
-                        b2 = k;
-                    }
-                }
+                if (!(valid && qm[q] < top.b4)) continue;
+                as_walk_quarter(top, v + 16 * q, stage, (int32_t)(t * 128 + q * 16));
             }
         }
-        if (valid) {
-            best_idx[row] = i1;
-            best_keys[row] = make_float2(b1, b2);
-        }
+        if (valid) top.store(row, best_idx, best_keys, alt_idx, alt_keys);
     }
     __syncthreads();
     if (warp == 1) {

@@ -48,6 +48,38 @@ void ensure_pool() {
     done = true;
 }
 
+cudaError_t d2h_sync(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+    struct Staging {
+        void* p = nullptr;
+        size_t cap = 0;
+        ~Staging() {
+            if (p) cudaFreeHost(p);
+        }
+    };
+    static thread_local Staging sb;
+    if (bytes > ((size_t)8 << 20)) {  // bulk results: the plain copy
+        cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st);
+        return e != cudaSuccess ? e : cudaStreamSynchronize(st);
+    }
+    if (bytes > sb.cap) {
+        if (sb.p) cudaFreeHost(sb.p);
+        sb.p = nullptr;
+        sb.cap = 0;
+        const size_t want = std::max<size_t>(bytes, 1 << 16);
+        cudaError_t e = cudaMallocHost(&sb.p, want);
+        if (e != cudaSuccess) {  // no pinned memory: the plain copy
+            sb.p = nullptr;
+            e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st);
+            return e != cudaSuccess ? e : cudaStreamSynchronize(st);
+        }
+        sb.cap = want;
+    }
+    cudaError_t e = cudaMemcpyAsync(sb.p, src, bytes, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) std::memcpy(dst, sb.p, bytes);
+    return e;
+}
+
 void trim_pool() {
     int dev = 0;
     cudaGetDevice(&dev);

@@ -62,6 +62,12 @@ struct ProfMute {
 cudaStream_t& tl_stream();
 void ensure_pool();
 void trim_pool();
+// Blocking device->host read of a small result (scalars, flags, counts)
+// through a per-thread pinned staging buffer: the copy is a plain DMA and the
+// stream synchronisation spins; a read into pageable memory takes the
+// driver's staged path, whose completion wait sleeps and, on a virtualised
+// host, wakes late (measured: 0.1-1 s stalls per pipeline run at C2).
+cudaError_t d2h_sync(void* dst, const void* src, size_t bytes, cudaStream_t st);
 struct StreamScope {
     cudaStream_t prev;
     explicit StreamScope(cudaStream_t s) : prev(tl_stream()) { tl_stream() = s; }

@@ -1211,8 +1211,7 @@ struct NpSum {
         const int64_t nl = (int64_t)off.size() - 1;
         np_leaf_sum_kernel<<<(unsigned)ceil_div(nl, 128), 128, 0, st>>>(nl, d_off.p, a, d_leaf.p);
         SC_LAUNCHED(1);
-        SC_CUDA(cudaMemcpyAsync(h.data(), d_leaf.p, sizeof(double) * nl, cudaMemcpyDeviceToHost, st));
-        SC_CUDA(cudaStreamSynchronize(st));
+        SC_CUDA(d2h_sync(h.data(), d_leaf.p, sizeof(double) * nl, st));
         size_t li = 0;
         *result = n > 0 ? combine(n, li) : 0.0;
         return SC_OK;
@@ -1267,92 +1266,124 @@ __device__ __forceinline__ double exact_s(const double* __restrict__ vi, double 
     return r > 0.0 ? r : 0.0;
 }
 
-// certified rows: label = best, exact cost; others are listed for the rescan.
 // delta_i bounds |approx key - exact key| for row i (fp16 operands, fp32
 // accumulation of dp products, fp32 norms and FMA, fp16 subnormals):
 //   delta_i = 1.25 * ( 2 (2^-10 + (dp+1) 2^-24) |v_i| cmax
 //                      + 2^-24 (2 cnmax + 2 |v_i| cmax)
 //                      + 2^-24 sqrt(dp) (|v_i| + cmax) / s )
-__global__ void as_finalize_kernel(int64_t n, int64_t d, int64_t dp, double s, const double* __restrict__ v,
-                                   const double* __restrict__ vn, const double* __restrict__ c,
-                                   const double* __restrict__ cn, const unsigned long long* __restrict__ cnmax_bits,
-                                   const int32_t* __restrict__ best_idx, const float2* __restrict__ best_keys,
-                                   const int64_t* __restrict__ old_labels, int64_t* __restrict__ labels,
-                                   double* __restrict__ cost, int32_t* __restrict__ flagged,
-                                   unsigned long long* __restrict__ nflag, unsigned long long* __restrict__ changes) {
-    extern __shared__ double fin_stage[];
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    int chg = 0;
-    bool certified = false;
-    int32_t b = -1;
-    if (i < n) {
-        const double cnmax = __longlong_as_double((long long)*cnmax_bits);
-        const double cmax = sqrt(cnmax);
-        const double va = sqrt(vn[i]);
-        const double delta = 1.25 * (2.0 * (0x1p-10 + (double)(dp + 1) * 0x1p-24) * va * cmax +
-                                     0x1p-24 * (2.0 * cnmax + 2.0 * va * cmax) +
-                                     0x1p-24 * sqrt((double)dp) * (va + cmax) / s);
-        const float2 bk = best_keys[i];
-        b = best_idx[i];
-        certified = b >= 0 && (double)bk.y - (double)bk.x > 2.0 * delta;
-        if (!certified) flagged[atomicAdd(nflag, 1ull)] = (int32_t)i;
-    }
-    // exact cost of the certified rows (exact_s, with the rows staged per warp)
-    const double dot = warp_pair_dot_np(certified ? v + i * d : nullptr, certified ? c + (int64_t)b * d : nullptr, d,
-                                        fin_stage + (threadIdx.x >> 5) * kPairStage);
-    if (certified) {
-        labels[i] = b;
-        const double r = __dsub_rn(__dadd_rn(vn[i], cn[b]), __dmul_rn(2.0, dot));
-        cost[i] = r > 0.0 ? r : 0.0;
-        if (old_labels) chg = old_labels[i] != b;
-    }
-    const unsigned bal = __ballot_sync(0xffffffffu, chg);
-    if ((threadIdx.x & 31) == 0 && bal) atomicAdd(changes, (unsigned long long)__popc(bal));
+__device__ __forceinline__ double as_delta(double vni, double cnmax, int64_t dp, double s) {
+    const double cmax = sqrt(cnmax);
+    const double va = sqrt(vni);
+    return 1.25 * (2.0 * (0x1p-10 + (double)(dp + 1) * 0x1p-24) * va * cmax + 0x1p-24 * (2.0 * cnmax + 2.0 * va * cmax) +
+                   0x1p-24 * sqrt((double)dp) * (va + cmax) / s);
 }
 
-// as_finalize_kernel over the points' 8-column panels (to_panels_kernel):
-// thread per row, its 64-byte panel pieces read coalesced with the
-// neighbouring rows'; exact_s's products and order
-__global__ void as_finalize_panel_kernel(int64_t n, int64_t d, int64_t dp, double s, const double* __restrict__ v8,
-                                         const double* __restrict__ vn, const double* __restrict__ c,
-                                         const double* __restrict__ cn,
-                                         const unsigned long long* __restrict__ cnmax_bits,
-                                         const int32_t* __restrict__ best_idx, const float2* __restrict__ best_keys,
-                                         const int64_t* __restrict__ old_labels, int64_t* __restrict__ labels,
-                                         double* __restrict__ cost, int32_t* __restrict__ flagged,
-                                         unsigned long long* __restrict__ nflag,
-                                         unsigned long long* __restrict__ changes) {
+// Uncertified rows whose fourth-best approximate key is more than 2 delta
+// above the best: every centroid that can hold the exact minimum is among
+// the kept three, so their exact keys (exact_s's arithmetic, the reference's)
+// settle the row -- minimum, lowest index on ties.  Ten rows per warp, lanes
+// 3r..3r+2 evaluate row r's candidates through the warp-staged dot
+// (warp_pair_dot_np: coalesced row reads); rows with more near-ties go to
+// flagged2 for the full re-scan.  Dynamic shared memory: kPairStage doubles
+// per warp.
+__global__ void as_resolve_kernel(int64_t nf, int64_t d, int64_t dp, double s, const double* __restrict__ v,
+                                  const double* __restrict__ vn, const double* __restrict__ c,
+                                  const double* __restrict__ cn, const unsigned long long* __restrict__ cnmax_bits,
+                                  const int32_t* __restrict__ flagged, const float2* __restrict__ best_keys,
+                                  const float2* __restrict__ alt_keys, const int32_t* __restrict__ best_idx,
+                                  const int2* __restrict__ alt_idx, const int64_t* __restrict__ old_labels,
+                                  int64_t* __restrict__ labels, double* __restrict__ cost,
+                                  unsigned long long* __restrict__ changes, int32_t* __restrict__ flagged2,
+                                  unsigned long long* __restrict__ nflag2) {
+    extern __shared__ double res_stage[];
+    const int lane = threadIdx.x & 31, grp = lane / 3, slot = lane - 3 * grp;
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t r = w * 10 + grp;
+    const bool mine = grp < 10 && r < nf;
+    int64_t i = -1, q = -1;
+    bool settle = false;
+    if (mine) {
+        i = flagged[r];
+        const double delta = as_delta(vn[i], __longlong_as_double((long long)*cnmax_bits), dp, s);
+        const float2 bk = best_keys[i], ak = alt_keys[i];
+        const double lim = (double)bk.x + 2.0 * delta;
+        settle = best_idx[i] >= 0 && (double)ak.y > lim;
+        if (settle) {
+            const int2 ai = alt_idx[i];
+            if (slot == 0) q = best_idx[i];
+            if (slot == 1 && ai.x >= 0 && (double)bk.y <= lim) q = ai.x;
+            if (slot == 2 && ai.y >= 0 && (double)ak.x <= lim) q = ai.y;
+        } else if (slot == 0) {
+            flagged2[atomicAdd(nflag2, 1ull)] = (int32_t)i;
+        }
+    }
+    const double dot = warp_pair_dot_np(q >= 0 ? v + i * d : nullptr, q >= 0 ? c + q * d : nullptr, d,
+                                        res_stage + (threadIdx.x >> 5) * kPairStage);
+    double sv = INFINITY;
+    int64_t arg = INT64_MAX;
+    if (q >= 0) {
+        const double t = __dsub_rn(__dadd_rn(vn[i], cn[q]), __dmul_rn(2.0, dot));
+        sv = t > 0.0 ? t : 0.0;
+        arg = q;
+    }
+    const int base = 3 * grp < 30 ? 3 * grp : 0;
+#pragma unroll
+    for (int o = 1; o <= 2; ++o) {
+        const double os = __shfl_sync(0xffffffffu, sv, base + o);
+        const int64_t oa = __shfl_sync(0xffffffffu, arg, base + o);
+        if (slot == 0 && (os < sv || (os == sv && oa < arg))) {
+            sv = os;
+            arg = oa;
+        }
+    }
+    if (mine && settle && slot == 0) {
+        labels[i] = arg;
+        cost[i] = sv;
+        if (old_labels && old_labels[i] != arg) atomicAdd(changes, 1ull);
+    }
+}
+
+__global__ void as_take_best_kernel(int64_t n, const int32_t* __restrict__ best_idx, int64_t* __restrict__ labels) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) labels[i] = best_idx[i] < 0 ? 0 : best_idx[i];
+}
+
+// Certified rows (second-best approximate key more than 2 delta above the
+// best): label = best, exact cost (exact_s's products and order) with a
+// thread per row reading its row and its centroid in 64-byte pieces; the
+// rest are listed for as_resolve_kernel.  (Measured at C5: rows in point
+// order beat both an 8-column panel copy of the points and rows visited in
+// cluster order, whose point reads scatter.)
+__global__ void __launch_bounds__(256) as_finalize_rows_kernel(
+    int64_t n, int64_t d, int64_t dp, double s, const double* __restrict__ v, const double* __restrict__ vn,
+    const double* __restrict__ c, const double* __restrict__ cn, const unsigned long long* __restrict__ cnmax_bits,
+    const int32_t* __restrict__ best_idx, const float2* __restrict__ best_keys,
+    const int64_t* __restrict__ old_labels, int64_t* __restrict__ labels, double* __restrict__ cost,
+    int32_t* __restrict__ flagged, unsigned long long* __restrict__ nflag, unsigned long long* __restrict__ changes,
+    bool vec2) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int chg = 0;
     if (i < n) {
-        const double cnmax = __longlong_as_double((long long)*cnmax_bits);
-        const double cmax = sqrt(cnmax);
-        const double va = sqrt(vn[i]);
-        const double delta = 1.25 * (2.0 * (0x1p-10 + (double)(dp + 1) * 0x1p-24) * va * cmax +
-                                     0x1p-24 * (2.0 * cnmax + 2.0 * va * cmax) +
-                                     0x1p-24 * sqrt((double)dp) * (va + cmax) / s);
+        const double delta = as_delta(vn[i], __longlong_as_double((long long)*cnmax_bits), dp, s);
         const float2 bk = best_keys[i];
         const int32_t b = best_idx[i];
         if (b >= 0 && (double)bk.y - (double)bk.x > 2.0 * delta) {
+            const double* vi = v + i * d;
             const double* cb = c + (int64_t)b * d;
             NpDot acc;
-            for (int64_t c0 = 0; c0 < d; c0 += 8) {
-                const double2* src = reinterpret_cast<const double2*>(v8 + ((c0 >> 3) * n + i) * 8);
-                const double2 a0 = __ldg(src), a1 = __ldg(src + 1), a2 = __ldg(src + 2), a3 = __ldg(src + 3);
-                const double x[8] = {a0.x, a0.y, a1.x, a1.y, a2.x, a2.y, a3.x, a3.y};
-                auto f = [&](int q) { return __dmul_rn(x[q], __ldg(cb + c0 + q)); };
-                const int rem = (int)(d - c0 < 8 ? d - c0 : 8);
-                if (rem == 8) {
-                    acc.block(f(0), f(1), f(2), f(3), f(4), f(5), f(6), f(7));
-                } else {
-#pragma unroll
-                    for (int q = 0; q < 8; q += 2)
-                        if (q + 2 <= rem) acc.pair(f(q), f(q + 1));
-#pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        if ((rem & 1) && q == rem - 1) acc.single(f(q));
+            int64_t l = 0;
+            if (vec2) {  // rows 16-byte aligned (d even, aligned bases): 16-byte loads
+                for (; l + 8 <= d; l += 8) {
+                    const double2* pv = reinterpret_cast<const double2*>(vi + l);
+                    const double2* pc = reinterpret_cast<const double2*>(cb + l);
+                    const double2 x0 = __ldg(pv), x1 = __ldg(pv + 1), x2 = __ldg(pv + 2), x3 = __ldg(pv + 3);
+                    const double2 y0 = __ldg(pc), y1 = __ldg(pc + 1), y2 = __ldg(pc + 2), y3 = __ldg(pc + 3);
+                    acc.block(__dmul_rn(x0.x, y0.x), __dmul_rn(x0.y, y0.y), __dmul_rn(x1.x, y1.x),
+                              __dmul_rn(x1.y, y1.y), __dmul_rn(x2.x, y2.x), __dmul_rn(x2.y, y2.y),
+                              __dmul_rn(x3.x, y3.x), __dmul_rn(x3.y, y3.y));
                 }
             }
+            np_dot_span(acc, l, d, [&](int64_t j) { return __dmul_rn(__ldg(vi + j), __ldg(cb + j)); });
             labels[i] = b;
             const double r = __dsub_rn(__dadd_rn(vn[i], cn[b]), __dmul_rn(2.0, acc.result()));
             cost[i] = r > 0.0 ? r : 0.0;
@@ -1365,9 +1396,131 @@ __global__ void as_finalize_panel_kernel(int64_t n, int64_t d, int64_t dp, doubl
     if ((threadIdx.x & 31) == 0 && bal) atomicAdd(changes, (unsigned long long)__popc(bal));
 }
 
-__global__ void as_take_best_kernel(int64_t n, const int32_t* __restrict__ best_idx, int64_t* __restrict__ labels) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) labels[i] = best_idx[i] < 0 ? 0 : best_idx[i];
+// ct[l * k + q] = c[q * d + l] (the centroids column-major for the re-scan)
+__global__ void as_transpose_kernel(int64_t k, int64_t d, const double* __restrict__ c, double* __restrict__ ct) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= k * d) return;
+    const int64_t l = e / k, q = e - l * k;
+    ct[e] = c[q * d + l];
+}
+
+// Exact re-scan of rows with more near-ties than the kept candidates: CTA =
+// RS_R flagged rows (staged in shared memory) x 256 consecutive centroids,
+// thread = one centroid; the centroids are read column-major (coalesced) and
+// every product feeds RS_R rows.  Keys in exact_s's arithmetic; the CTA's
+// minimum per row (lowest index on ties) goes to pval / pidx[row][chunk].
+constexpr int RS_R = 8;
+__global__ void __launch_bounds__(256) as_rescan_tile_kernel(int64_t nf, int64_t d, int64_t k,
+                                                             const double* __restrict__ v,
+                                                             const double* __restrict__ vn,
+                                                             const double* __restrict__ ct,
+                                                             const double* __restrict__ cn,
+                                                             const int32_t* __restrict__ fl, int nchunks,
+                                                             double* __restrict__ pval, int32_t* __restrict__ pidx) {
+    extern __shared__ double rs_rows[];  // RS_R x d
+    __shared__ int64_t rid[RS_R];
+    __shared__ double rval[RS_R][8];
+    __shared__ int32_t ridx[RS_R][8];
+    const int64_t r0 = (int64_t)blockIdx.x * RS_R;
+    const int nr = (int)(nf - r0 < RS_R ? nf - r0 : RS_R);
+    if (threadIdx.x < RS_R) rid[threadIdx.x] = threadIdx.x < nr ? (int64_t)fl[r0 + threadIdx.x] : -1;
+    __syncthreads();
+    for (int64_t e = threadIdx.x; e < (int64_t)RS_R * d; e += blockDim.x) {
+        const int r = (int)(e / d);
+        rs_rows[e] = r < nr ? v[rid[r] * d + (e - (int64_t)r * d)] : 0.0;
+    }
+    __syncthreads();
+    const int64_t q = (int64_t)blockIdx.y * blockDim.x + threadIdx.x;
+    const bool ok = q < k;
+    NpDot acc[RS_R];
+    if (ok) {
+        int64_t l = 0;
+        for (; l + 8 <= d; l += 8) {
+            double cc[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) cc[u] = __ldg(ct + (l + u) * k + q);
+#pragma unroll
+            for (int r = 0; r < RS_R; ++r) {
+                const double* x = rs_rows + (int64_t)r * d + l;
+                acc[r].block(__dmul_rn(x[0], cc[0]), __dmul_rn(x[1], cc[1]), __dmul_rn(x[2], cc[2]),
+                             __dmul_rn(x[3], cc[3]), __dmul_rn(x[4], cc[4]), __dmul_rn(x[5], cc[5]),
+                             __dmul_rn(x[6], cc[6]), __dmul_rn(x[7], cc[7]));
+            }
+        }
+        for (; l + 2 <= d; l += 2) {
+            const double c0 = __ldg(ct + l * k + q), c1 = __ldg(ct + (l + 1) * k + q);
+#pragma unroll
+            for (int r = 0; r < RS_R; ++r)
+                acc[r].pair(__dmul_rn(rs_rows[(int64_t)r * d + l], c0), __dmul_rn(rs_rows[(int64_t)r * d + l + 1], c1));
+        }
+        if (l < d) {
+            const double c0 = __ldg(ct + l * k + q);
+#pragma unroll
+            for (int r = 0; r < RS_R; ++r) acc[r].single(__dmul_rn(rs_rows[(int64_t)r * d + l], c0));
+        }
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+    for (int r = 0; r < RS_R; ++r) {
+        double sv = INFINITY;
+        int32_t a = INT32_MAX;
+        if (ok && r < nr) {
+            const double t = __dsub_rn(__dadd_rn(vn[rid[r]], cn[q]), __dmul_rn(2.0, acc[r].result()));
+            sv = t > 0.0 ? t : 0.0;
+            a = (int32_t)q;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double os = __shfl_xor_sync(0xffffffffu, sv, o);
+            const int32_t oa = __shfl_xor_sync(0xffffffffu, a, o);
+            if (os < sv || (os == sv && oa < a)) {
+                sv = os;
+                a = oa;
+            }
+        }
+        if (lane == 0) {
+            rval[r][warp] = sv;
+            ridx[r][warp] = a;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < nr) {
+        const int r = threadIdx.x;
+        double sv = rval[r][0];
+        int32_t a = ridx[r][0];
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+            if (rval[r][w] < sv || (rval[r][w] == sv && ridx[r][w] < a)) {
+                sv = rval[r][w];
+                a = ridx[r][w];
+            }
+        pval[(r0 + r) * nchunks + blockIdx.y] = sv;
+        pidx[(r0 + r) * nchunks + blockIdx.y] = a;
+    }
+}
+
+// per re-scanned row: minimum over the chunks (ascending centroid order,
+// strict < keeps the lowest index on ties); labels / cost / change count
+__global__ void as_rescan_merge_kernel(int64_t nf, int nchunks, const int32_t* __restrict__ fl,
+                                       const double* __restrict__ pval, const int32_t* __restrict__ pidx,
+                                       const int64_t* __restrict__ old_labels, int64_t* __restrict__ labels,
+                                       double* __restrict__ cost, unsigned long long* __restrict__ changes) {
+    const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int chg = 0;
+    if (f < nf) {
+        double sv = pval[f * nchunks];
+        int32_t a = pidx[f * nchunks];
+        for (int j = 1; j < nchunks; ++j)
+            if (pval[f * nchunks + j] < sv) {
+                sv = pval[f * nchunks + j];
+                a = pidx[f * nchunks + j];
+            }
+        const int64_t i = fl[f];
+        labels[i] = a;
+        cost[i] = sv;
+        if (old_labels) chg = old_labels[i] != a;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, chg);
+    if ((threadIdx.x & 31) == 0 && bal) atomicAdd(changes, (unsigned long long)__popc(bal));
 }
 
 // flagged rows: exact scan over all centroids (warp per row, lowest index on ties)
@@ -1444,12 +1597,12 @@ __global__ void cost_block_sum_kernel(int64_t n, const double* __restrict__ cost
 template <int NKB, int STAGES, int QT>
 static int launch_assign_tc(const CUtensorMap& vmap, const CUtensorMap& cmap, int64_t n, int64_t nptiles,
                             int64_t nctiles, const float* cnk, float key_scale, int32_t* best_idx, float2* best_keys,
-                            cudaStream_t st) {
+                            int2* alt_idx, float2* alt_keys, cudaStream_t st) {
     const uint32_t smem = AsLayout<NKB, STAGES, QT>::total;
     SC_CUDA(cudaFuncSetAttribute(assign_tc_kernel<NKB, STAGES, QT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
     assign_tc_kernel<NKB, STAGES, QT><<<(unsigned)ceil_div(nptiles, QT), 64 + QT * 128, smem, st>>>(
-        vmap, cmap, n, nptiles, nctiles, cnk, key_scale, best_idx, best_keys);
+        vmap, cmap, n, nptiles, nctiles, cnk, key_scale, best_idx, best_keys, alt_idx, alt_keys);
     SC_LAUNCHED(1);
     return SC_OK;
 }
@@ -1457,12 +1610,12 @@ static int launch_assign_tc(const CUtensorMap& vmap, const CUtensorMap& cmap, in
 template <int STAGES, int QT>
 static int launch_assign_tc_kl(const CUtensorMap& vmap, const CUtensorMap& cmap, int64_t n, int64_t nptiles,
                                int64_t nctiles, int nkb, const float* cnk, float key_scale, int32_t* best_idx,
-                               float2* best_keys, cudaStream_t st) {
+                               float2* best_keys, int2* alt_idx, float2* alt_keys, cudaStream_t st) {
     const uint32_t smem = AsKlLayout<STAGES, QT>::total;
     SC_CUDA(cudaFuncSetAttribute(assign_tc_kl_kernel<STAGES, QT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
     assign_tc_kl_kernel<STAGES, QT><<<(unsigned)ceil_div(nptiles, QT), 64 + QT * 128, smem, st>>>(
-        vmap, cmap, n, nptiles, nctiles, nkb, cnk, key_scale, best_idx, best_keys);
+        vmap, cmap, n, nptiles, nctiles, nkb, cnk, key_scale, best_idx, best_keys, alt_idx, alt_keys);
     SC_LAUNCHED(1);
     return SC_OK;
 }
@@ -1475,14 +1628,13 @@ struct AssignTc {
     DevBuf<__half> vh;
     CUtensorMap vmap;
     DevBuf<int32_t> bidx, flagged;
-    DevBuf<float2> bkeys;
-    DevBuf<unsigned long long> scal;  // [0] nflag, [1] cnmax bits, [2] absmax bits
-    DevBuf<double> v8;                // the points in 8-column panels (exact costs)
+    DevBuf<float2> bkeys, akeys;
+    DevBuf<int2> aidx;
+    DevBuf<int32_t> flagged2;
+    DevBuf<unsigned long long> scal;  // [0] nflag, [1] cnmax bits, [2] absmax bits, [3] nflag after resolve
     // eligible: enough rows to pay for the conversion; SPECLUST_ASSIGN=fp64 disables.
     // dp <= 256: point tiles resident in shared memory; wider: K-chunk ring
-    // exact = false: only the uncertified argmin will be asked for (no exact
-    // costs), so the fp64 panel copy of the points is not built
-    int init(int64_t n_, int64_t d_, int64_t k, const double* v, cudaStream_t st, bool exact = true) {
+    int init(int64_t n_, int64_t d_, int64_t k, const double* v, cudaStream_t st) {
         n = n_;
         d = d_;
         dp = (d + 63) / 64 * 64;
@@ -1492,14 +1644,14 @@ struct AssignTc {
         n_pad = (n + 127) / 128 * 128;
         int rc;
         if ((rc = vh.alloc((size_t)n_pad * dp)) || (rc = bidx.alloc(n)) || (rc = bkeys.alloc(n)) ||
-            (rc = flagged.alloc(n)) || (rc = scal.alloc(3)))
+            (rc = flagged.alloc(n)) || (rc = scal.alloc(4)) || (rc = akeys.alloc(n)) || (rc = aidx.alloc(n)) ||
+            (rc = flagged2.alloc(n)))
             return rc;
-        SC_CUDA(cudaMemsetAsync(scal.p, 0, sizeof(unsigned long long) * 3, st));
+        SC_CUDA(cudaMemsetAsync(scal.p, 0, sizeof(unsigned long long) * 4, st));
         as_absmax_kernel<<<kNumSMs * 4, 256, 0, st>>>(n * d, v, scal.p + 2);
         SC_LAUNCHED(1);
         unsigned long long hb = 0;
-        SC_CUDA(cudaMemcpyAsync(&hb, scal.p + 2, sizeof(hb), cudaMemcpyDeviceToHost, st));
-        SC_CUDA(cudaStreamSynchronize(st));
+        SC_CUDA(d2h_sync(&hb, scal.p + 2, sizeof(hb), st));
         double amax;
         std::memcpy(&amax, &hb, sizeof(amax));
         // power-of-two scale: |s x| <= 128 for every element of V (centroids
@@ -1507,11 +1659,6 @@ struct AssignTc {
         s = amax > 0 ? std::ldexp(1.0, (int)std::floor(std::log2(128.0 / amax))) : 1.0;
         as_prep_rows_kernel<<<(unsigned)ceil_div(n_pad, 8), 256, 0, st>>>(n, n_pad, d, dp, v, s, vh.p);
         SC_LAUNCHED(1);
-        const int64_t nch = ceil_div(d, 8);
-        if (exact && v8.alloc((size_t)nch * n * 8) == SC_OK) {  // optional: the staged kernel otherwise
-            to_panels_kernel<<<(unsigned)ceil_div(nch * n * 8, 256), 256, 0, st>>>(n, d, v, v8.p);
-            SC_LAUNCHED(1);
-        }
         return make_f16_tile_map(&vmap, vh.p, n_pad, dp);
     }
     // labels / cost / change count of one assignment step
@@ -1526,6 +1673,7 @@ struct AssignTc {
         int rc;
         if ((rc = ch.alloc((size_t)k_pad * dp)) || (rc = cnk.alloc(k_pad))) return rc;
         SC_CUDA(cudaMemsetAsync(scal.p, 0, sizeof(unsigned long long) * 2, st));
+        SC_CUDA(cudaMemsetAsync(scal.p + 3, 0, sizeof(unsigned long long), st));
         as_prep_rows_kernel<<<(unsigned)ceil_div(k_pad, 8), 256, 0, st>>>(k, k_pad, d, dp, c, s, ch.p);
         as_cent_norms_kernel<<<(unsigned)ceil_div(k_pad, 256), 256, 0, st>>>(k, k_pad, cn, cnk.p, scal.p + 1);
         SC_LAUNCHED(2);
@@ -1533,61 +1681,109 @@ struct AssignTc {
         if ((rc = make_f16_tile_map(&cmap, ch.p, k_pad, dp))) return rc;
         const int64_t nptiles = n_pad / 128, nctiles = k_pad / 128;
         const float key_scale = (float)(-2.0 / (s * s));
+        static const bool dbg = std::getenv("SPECLUST_ASSIGN_DEBUG") != nullptr;
+        // SPECLUST_ASSIGN_DEBUG: per-phase device times on stderr
+        struct PhaseEv {
+            bool on;
+            cudaStream_t st;
+            int m = 0;
+            cudaEvent_t ev[8];
+            const char* name[8];
+            void mark(const char* nm) {
+                if (!on || m >= 8) return;
+                cudaEventCreate(&ev[m]);
+                cudaEventRecord(ev[m], st);
+                name[m++] = nm;
+            }
+            ~PhaseEv() {
+                if (!on) return;
+                mark("end");
+                cudaEventSynchronize(ev[m - 1]);
+                fprintf(stderr, "[assign_tc]");
+                for (int j = 1; j < m; ++j) {
+                    float t = 0;
+                    cudaEventElapsedTime(&t, ev[j - 1], ev[j]);
+                    fprintf(stderr, " %s %.3f ms", name[j - 1], t);
+                }
+                fprintf(stderr, "\n");
+                for (int j = 0; j < m; ++j) cudaEventDestroy(ev[j]);
+            }
+        } evp{dbg, st};
+        evp.mark("tc");
+        // STAGES counts 64-column centroid chunks (16 KB each)
+        int2* ai = aidx.p;
+        float2* ak = akeys.p;
         switch (dp / 64) {
-            case 1: rc = launch_assign_tc<1, 4, 2>(vmap, cmap, n, nptiles, nctiles, cnk.p, key_scale, bidx.p, bkeys.p, st); break;
-            case 2: rc = launch_assign_tc<2, 3, 2>(vmap, cmap, n, nptiles, nctiles, cnk.p, key_scale, bidx.p, bkeys.p, st); break;
-            case 3: rc = launch_assign_tc<3, 2, 2>(vmap, cmap, n, nptiles, nctiles, cnk.p, key_scale, bidx.p, bkeys.p, st); break;
-            case 4: rc = launch_assign_tc<4, 2, 1>(vmap, cmap, n, nptiles, nctiles, cnk.p, key_scale, bidx.p, bkeys.p, st); break;
-            default: rc = launch_assign_tc_kl<4, 2>(vmap, cmap, n, nptiles, nctiles, (int)(dp / 64), cnk.p, key_scale, bidx.p, bkeys.p, st); break;
+            case 1: rc = launch_assign_tc<1, 8, 2>(vmap, cmap, n, nptiles, nctiles, cnk.p, key_scale, bidx.p, bkeys.p, ai, ak, st); break;
+            case 2: rc = launch_assign_tc<2, 8, 2>(vmap, cmap, n, nptiles, nctiles, cnk.p, key_scale, bidx.p, bkeys.p, ai, ak, st); break;
+            case 3: rc = launch_assign_tc<3, 6, 2>(vmap, cmap, n, nptiles, nctiles, cnk.p, key_scale, bidx.p, bkeys.p, ai, ak, st); break;
+            case 4: rc = launch_assign_tc<4, 4, 2>(vmap, cmap, n, nptiles, nctiles, cnk.p, key_scale, bidx.p, bkeys.p, ai, ak, st); break;
+            default: rc = launch_assign_tc_kl<4, 2>(vmap, cmap, n, nptiles, nctiles, (int)(dp / 64), cnk.p, key_scale, bidx.p, bkeys.p, ai, ak, st); break;
         }
         if (rc) return rc;
+        evp.mark("finalize");
         if (!certify) {
             as_take_best_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, bidx.p, labels);
             SC_LAUNCHED(1);
             return SC_OK;
         }
-        if (v8.p) {
-            as_finalize_panel_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(
-                n, d, dp, s, v8.p, vn, c, cn, scal.p + 1, bidx.p, bkeys.p, old_labels, labels, cost, flagged.p,
-                scal.p, changes);
-        } else {
-            constexpr int fin_smem = 8 * kPairStage * (int)sizeof(double);
-            SC_CUDA(cudaFuncSetAttribute(as_finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fin_smem));
-            as_finalize_kernel<<<(unsigned)ceil_div(n, 256), 256, fin_smem, st>>>(n, d, dp, s, v, vn, c, cn,
-                                                                                 scal.p + 1, bidx.p, bkeys.p,
-                                                                                 old_labels, labels, cost, flagged.p,
-                                                                                 scal.p, changes);
-        }
+        as_finalize_rows_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(
+            n, d, dp, s, v, vn, c, cn, scal.p + 1, bidx.p, bkeys.p, old_labels, labels, cost, flagged.p, scal.p,
+            changes, d % 2 == 0 && ((reinterpret_cast<uintptr_t>(v) | reinterpret_cast<uintptr_t>(c)) & 15) == 0);
         SC_LAUNCHED(1);
         // uncertified rows: exact re-scan.  Few rows or few centroids: a warp
         // per row; otherwise the rows are gathered and run through the tiled
         // fp64 assignment kernel (the same arithmetic as the fp64 path)
-        const int64_t nf = flagged_count(st);
+        int64_t nf = flagged_count(st);
         if (nf == 0) return SC_OK;
-        if (nf * k < (int64_t)1 << 24) {
-            as_rescan_kernel<<<kNumSMs * 4, 256, 0, st>>>(d, k, v, vn, c, cn, flagged.p, scal.p, old_labels, labels,
+        evp.mark("resolve");
+        // at most three candidates within 2 delta of the best: exact keys of those
+        constexpr int res_smem = 8 * kPairStage * (int)sizeof(double);
+        SC_CUDA(cudaFuncSetAttribute(as_resolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, res_smem));
+        as_resolve_kernel<<<(unsigned)ceil_div(nf, 80), 256, res_smem, st>>>(
+            nf, d, dp, s, v, vn, c, cn, scal.p + 1, flagged.p, bkeys.p, akeys.p, bidx.p, aidx.p, old_labels, labels,
+            cost, changes, flagged2.p, scal.p + 3);
+        SC_LAUNCHED(1);
+        {
+            unsigned long long h = 0;
+            SC_CUDA(d2h_sync(&h, scal.p + 3, sizeof(h), st));
+            if (dbg) fprintf(stderr, "[assign_tc] uncertified %lld, after the three-candidate resolve %llu\n",
+                             (long long)nf, h);
+            nf = (int64_t)h;
+        }
+        if (nf == 0) return SC_OK;
+        evp.mark("rescan");
+        const int32_t* fl = flagged2.p;
+        DevBuf<double> ct, pval;
+        DevBuf<int32_t> pidx;
+        const int nchunks = (int)ceil_div(k, 256);
+        const int64_t batch = std::min<int64_t>(nf, std::max<int64_t>(RS_R, ((int64_t)1 << 24) / nchunks));
+        if ((rc = ct.alloc((size_t)k * d)) || (rc = pval.alloc((size_t)batch * nchunks)) ||
+            (rc = pidx.alloc((size_t)batch * nchunks)))
+            return rc;
+        as_transpose_kernel<<<(unsigned)ceil_div(k * d, 256), 256, 0, st>>>(k, d, c, ct.p);
+        SC_LAUNCHED(1);
+        const int rs_smem = (int)(RS_R * d * sizeof(double));
+        if (rs_smem > 200 * 1024) {  // very wide rows: warp per row
+            as_rescan_kernel<<<kNumSMs * 4, 256, 0, st>>>(d, k, v, vn, c, cn, fl, scal.p + 3, old_labels, labels,
                                                           cost, changes);
             SC_LAUNCHED(1);
             return SC_OK;
         }
-        DevBuf<double> vf, vnf, costf, partf;
-        DevBuf<int64_t> labf, oldf;
-        if ((rc = vf.alloc((size_t)nf * d)) || (rc = vnf.alloc(nf)) || (rc = costf.alloc(nf)) ||
-            (rc = partf.alloc(ceil_div(nf, TP))) || (rc = labf.alloc(nf)) || (rc = oldf.alloc(nf)))
-            return rc;
-        as_gather_kernel<<<(unsigned)ceil_div(nf * d, 256), 256, 0, st>>>(nf, d, flagged.p, v, vn, old_labels, vf.p,
-                                                                          vnf.p, oldf.p);
-        dist_tile_kernel<0><<<(unsigned)ceil_div(nf, TP), 256, 0, st>>>(nf, k, d, vf.p, vnf.p, c, cn, nullptr, labf.p,
-                                                                        old_labels ? oldf.p : nullptr, costf.p,
-                                                                        changes, partf.p);
-        as_scatter_kernel<<<(unsigned)ceil_div(nf, 256), 256, 0, st>>>(nf, flagged.p, labf.p, costf.p, labels, cost);
-        SC_LAUNCHED(3);
+        SC_CUDA(cudaFuncSetAttribute(as_rescan_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, rs_smem));
+        for (int64_t f0 = 0; f0 < nf; f0 += batch) {
+            const int64_t nb = std::min(batch, nf - f0);
+            as_rescan_tile_kernel<<<dim3((unsigned)ceil_div(nb, RS_R), (unsigned)nchunks), 256, rs_smem, st>>>(
+                nb, d, k, v, vn, ct.p, cn, fl + f0, nchunks, pval.p, pidx.p);
+            as_rescan_merge_kernel<<<(unsigned)ceil_div(nb, 256), 256, 0, st>>>(nb, nchunks, fl + f0, pval.p, pidx.p,
+                                                                              old_labels, labels, cost, changes);
+            SC_LAUNCHED(2);
+        }
         return SC_OK;
     }
     int64_t flagged_count(cudaStream_t st) {
         unsigned long long h = 0;
-        cudaMemcpyAsync(&h, scal.p, sizeof(h), cudaMemcpyDeviceToHost, st);
-        cudaStreamSynchronize(st);
+        d2h_sync(&h, scal.p, sizeof(h), st);
         return (int64_t)h;
     }
 };
@@ -1613,7 +1809,7 @@ int assign_nearest(int64_t n, int64_t d, const double* v, int64_t k, const doubl
     rownorm_kernel<<<(unsigned)ceil_div(k, 256), 256, 0, st>>>(k, d, c, cn.p);
     SC_LAUNCHED(2);
     AssignTc atc;
-    if ((rc = atc.init(n, d, k, v, st, false))) return rc;
+    if ((rc = atc.init(n, d, k, v, st))) return rc;
     if (atc.active) return atc.assign(k, v, vn.p, c, cn.p, nullptr, labels, cost.p, changes.p, st, false);
     dist_tile_kernel<0><<<(unsigned)nb, 256, 0, st>>>(n, k, d, v, vn.p, c, cn.p, nullptr, labels, nullptr, cost.p,
                                                       changes.p, part.p);
@@ -1658,8 +1854,7 @@ struct sc_kmeanspp {
     void screen_review() {
         if (!screen || ++screened_draws != 8) return;
         unsigned long long h[2] = {0, 0};
-        cudaMemcpyAsync(h, sstat.p, sizeof(h), cudaMemcpyDeviceToHost, st);
-        cudaStreamSynchronize(st);
+        d2h_sync(h, sstat.p, sizeof(h), st);
         if (h[0] > 0 && (double)h[1] < 0.25 * (double)h[0]) screen = false;
     }
 
@@ -1789,8 +1984,7 @@ int sc_lloyd(int64_t n, int64_t d, int64_t k, const double* v, const double* c_i
         if ((rc = bk.run(cur, st))) return rc;
         // cluster sizes (host): segment plan + empty clusters
         std::vector<int64_t> hstart(k + 1);
-        SC_CUDA(cudaMemcpyAsync(hstart.data(), bk.start.p, sizeof(int64_t) * (k + 1), cudaMemcpyDeviceToHost, st));
-        SC_CUDA(cudaStreamSynchronize(st));
+        SC_CUDA(d2h_sync(hstart.data(), bk.start.p, sizeof(int64_t) * (k + 1), st));
         for (int64_t c = 0; c < k; ++c) hseg[c + 1] = hseg[c] + ceil_div(hstart[c + 1] - hstart[c], CM_SEG);
         const int64_t nseg = hseg[k];
         {
@@ -1824,7 +2018,7 @@ int sc_lloyd(int64_t n, int64_t d, int64_t k, const double* v, const double* c_i
         if ((rc = assign_step(cur, nxt))) return rc;
         SC_LAUNCHED(1);
         unsigned long long hchg = 0;
-        SC_CUDA(cudaMemcpyAsync(&hchg, changes.p, sizeof(hchg), cudaMemcpyDeviceToHost, st));
+        SC_CUDA(d2h_sync(&hchg, changes.p, sizeof(hchg), st));
         if ((rc = npsum.sum(cost.p, n, &sse_history[iters + 1], st))) return rc;
         ++iters;
         std::swap(cur, nxt);
@@ -1875,8 +2069,7 @@ int sc_kmeanspp_create(int64_t n, int64_t d, const double* v, sc_stream_t stream
                 rownorm_sqrt_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s->st>>>(n, d, v, s->vnorm.p);
                 SC_LAUNCHED(2);
                 unsigned long long hb = 0;
-                SC_CUDA(cudaMemcpyAsync(&hb, amax.p, sizeof(hb), cudaMemcpyDeviceToHost, s->st));
-                SC_CUDA(cudaStreamSynchronize(s->st));
+                SC_CUDA(d2h_sync(&hb, amax.p, sizeof(hb), s->st));
                 double am;
                 std::memcpy(&am, &hb, sizeof(am));
                 // |s v| <= 2^14: far from the fp16 overflow at 65504
@@ -1906,8 +2099,7 @@ int sc_kmeanspp_take(sc_kmeanspp_t* s, int64_t index) {
 }
 
 int sc_kmeanspp_candidates(sc_kmeanspp_t* s, int64_t* count, int64_t* n_free) {
-    SC_CUDA(cudaMemcpyAsync(count, s->count.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s->st));
-    SC_CUDA(cudaStreamSynchronize(s->st));
+    SC_CUDA(d2h_sync(count, s->count.p, sizeof(int64_t), s->st));
     *n_free = s->n - s->taken_count;
     return SC_OK;
 }
@@ -1923,8 +2115,7 @@ int sc_kmeanspp_pick(sc_kmeanspp_t* s, int mode, double u, int64_t r, int64_t* i
         SC_LAUNCHED(1);
     }
     int64_t h = -1;
-    SC_CUDA(cudaMemcpyAsync(&h, s->pick.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s->st));
-    SC_CUDA(cudaStreamSynchronize(s->st));
+    SC_CUDA(d2h_sync(&h, s->pick.p, sizeof(int64_t), s->st));
     if (h < 0) return fail(SC_ERR_INTERNAL, "k-means++ draw found no row");
     *index = h;
     return sc_kmeanspp_take(s, h);
@@ -1942,9 +2133,8 @@ int sc_kmeanspp_take_row(sc_kmeanspp_t* s, const double* row, int64_t local_inde
 
 // local candidate weight sum (sum of d2 over untaken rows with d2 > 0), count, untaken rows
 int sc_kmeanspp_weight(sc_kmeanspp_t* s, double* wsum, int64_t* count, int64_t* n_free) {
-    SC_CUDA(cudaMemcpyAsync(wsum, s->total.p, sizeof(double), cudaMemcpyDeviceToHost, s->st));
-    SC_CUDA(cudaMemcpyAsync(count, s->count.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s->st));
-    SC_CUDA(cudaStreamSynchronize(s->st));
+    SC_CUDA(d2h_sync(wsum, s->total.p, sizeof(double), s->st));
+    SC_CUDA(d2h_sync(count, s->count.p, sizeof(int64_t), s->st));
     *n_free = s->n - s->taken_count;
     return SC_OK;
 }
@@ -1957,8 +2147,7 @@ int sc_kmeanspp_psum(sc_kmeanspp_t* s, double total_global, double* psum) {
     if (int rc = out.alloc(1)) return rc;
     sum_partials_kernel<<<1, 1024, 0, s->st>>>(s->nb_p, s->bsum.p, out.p);
     SC_LAUNCHED(2);
-    SC_CUDA(cudaMemcpyAsync(psum, out.p, sizeof(double), cudaMemcpyDeviceToHost, s->st));
-    SC_CUDA(cudaStreamSynchronize(s->st));
+    SC_CUDA(d2h_sync(psum, out.p, sizeof(double), s->st));
     return SC_OK;
 }
 
@@ -1968,16 +2157,14 @@ int sc_kmeanspp_search(sc_kmeanspp_t* s, double target, int64_t* index) {
     kpp_search_target_kernel<<<1, 32, 0, s->st>>>(s->n, s->nb_p, s->d2.p, s->taken.p, s->total.p, s->bsum.p, target,
                                                   s->pick.p);
     SC_LAUNCHED(1);
-    SC_CUDA(cudaMemcpyAsync(index, s->pick.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s->st));
-    SC_CUDA(cudaStreamSynchronize(s->st));
+    SC_CUDA(d2h_sync(index, s->pick.p, sizeof(int64_t), s->st));
     return SC_OK;
 }
 
 int sc_kmeanspp_nth_free(sc_kmeanspp_t* s, int64_t r, int64_t* index) {
     kpp_nth_free_kernel<<<1, 32, 0, s->st>>>(s->n, s->taken.p, r, s->pick.p);
     SC_LAUNCHED(1);
-    SC_CUDA(cudaMemcpyAsync(index, s->pick.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s->st));
-    SC_CUDA(cudaStreamSynchronize(s->st));
+    SC_CUDA(d2h_sync(index, s->pick.p, sizeof(int64_t), s->st));
     return SC_OK;
 }
 
@@ -2019,9 +2206,8 @@ int sc_kmeans_assign(int64_t n, int64_t d, int64_t k, const double* v, const dou
     sum_partials_kernel<<<1, 1024, 0, st>>>(nb, part.p, out.p);
     SC_LAUNCHED(2);
     unsigned long long hc = 0;
-    SC_CUDA(cudaMemcpyAsync(&hc, chg.p, sizeof(hc), cudaMemcpyDeviceToHost, st));
-    SC_CUDA(cudaMemcpyAsync(sse, out.p, sizeof(double), cudaMemcpyDeviceToHost, st));
-    SC_CUDA(cudaStreamSynchronize(st));
+    SC_CUDA(d2h_sync(&hc, chg.p, sizeof(hc), st));
+    SC_CUDA(d2h_sync(sse, out.p, sizeof(double), st));
     *changes = (int64_t)hc;
     return SC_OK;
 }
@@ -2046,8 +2232,7 @@ int sc_kmeans_local_sums(int64_t n, int64_t d, int64_t k, const double* v, const
         return rc;
     if ((rc = bk.run(labels, st))) return rc;
     std::vector<int64_t> hstart(k + 1), hseg(k + 1, 0);
-    SC_CUDA(cudaMemcpyAsync(hstart.data(), bk.start.p, sizeof(int64_t) * (k + 1), cudaMemcpyDeviceToHost, st));
-    SC_CUDA(cudaStreamSynchronize(st));
+    SC_CUDA(d2h_sync(hstart.data(), bk.start.p, sizeof(int64_t) * (k + 1), st));
     for (int64_t c = 0; c < k; ++c) hseg[c + 1] = hseg[c] + ceil_div(hstart[c + 1] - hstart[c], CM_SEG);
     const int64_t nseg = hseg[k];
     SC_CUDA(cudaMemcpyAsync(seg_off.p, hseg.data(), sizeof(int64_t) * (k + 1), cudaMemcpyHostToDevice, st));
@@ -2089,8 +2274,7 @@ int sc_farthest(int64_t n, const double* cost, int64_t e, int64_t* idx_out, sc_s
         argmax_finish_kernel<<<1, 32, 0, st>>>(256, pv.p, pi.p, used.p, pick.p + s);
         SC_LAUNCHED(2);
     }
-    SC_CUDA(cudaMemcpyAsync(idx_out, pick.p, sizeof(int64_t) * e, cudaMemcpyDeviceToHost, st));
-    SC_CUDA(cudaStreamSynchronize(st));
+    SC_CUDA(d2h_sync(idx_out, pick.p, sizeof(int64_t) * e, st));
     return SC_OK;
 }
 
@@ -2142,10 +2326,9 @@ int sc_ncut(int64_t n, const int64_t* row_ptr, const int32_t* col, const double*
     SC_LAUNCHED(2);
     std::vector<double> hb(k), hv(k);
     std::vector<int64_t> hs(k + 1);
-    SC_CUDA(cudaMemcpyAsync(hb.data(), bnd.p, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
-    SC_CUDA(cudaMemcpyAsync(hv.data(), vol.p, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
-    SC_CUDA(cudaMemcpyAsync(hs.data(), bk.start.p, sizeof(int64_t) * (k + 1), cudaMemcpyDeviceToHost, st));
-    SC_CUDA(cudaStreamSynchronize(st));
+    SC_CUDA(d2h_sync(hb.data(), bnd.p, sizeof(double) * k, st));
+    SC_CUDA(d2h_sync(hv.data(), vol.p, sizeof(double) * k, st));
+    SC_CUDA(d2h_sync(hs.data(), bk.start.p, sizeof(int64_t) * (k + 1), st));
     // parts in label order; empty parts are dropped when compacting (the
     // pipeline's np.unique relabelling, pipeline.py:256-257)
     std::vector<double> q;
@@ -2187,10 +2370,9 @@ int sc_partition_cuts(int64_t n, const int64_t* row_ptr, const int32_t* col, con
     std::vector<double> hb(k);
     std::vector<int64_t> hs(k + 1);
     double htot = 0.0;
-    SC_CUDA(cudaMemcpyAsync(hb.data(), bnd.p, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
-    SC_CUDA(cudaMemcpyAsync(hs.data(), bk.start.p, sizeof(int64_t) * (k + 1), cudaMemcpyDeviceToHost, st));
-    SC_CUDA(cudaMemcpyAsync(&htot, tot.p, sizeof(double), cudaMemcpyDeviceToHost, st));
-    SC_CUDA(cudaStreamSynchronize(st));
+    SC_CUDA(d2h_sync(hb.data(), bnd.p, sizeof(double) * k, st));
+    SC_CUDA(d2h_sync(hs.data(), bk.start.p, sizeof(int64_t) * (k + 1), st));
+    SC_CUDA(d2h_sync(&htot, tot.p, sizeof(double), st));
     *cut_out = 0.5 * htot;
     *empty_part = -1;
     std::vector<double> q(k);

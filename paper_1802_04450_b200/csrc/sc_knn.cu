@@ -1065,8 +1065,7 @@ static int launch_tc(const CUtensorMap& map, int64_t n, int64_t ntiles, int64_t 
     SC_LAUNCHED(1);
     if (want_dbg) {
         std::vector<long long> h((size_t)nq * 16);
-        SC_CUDA(cudaMemcpyAsync(h.data(), dbg.p, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, st));
-        SC_CUDA(cudaStreamSynchronize(st));
+        SC_CUDA(d2h_sync(h.data(), dbg.p, sizeof(long long) * h.size(), st));
         double acc[16] = {0};
         for (int64_t b = 0; b < nq; ++b)
             for (int q = 0; q < 16; ++q) acc[q] += (double)h[b * 16 + q];
@@ -1105,8 +1104,7 @@ static int launch_tc2_w(const CUtensorMap& map, int64_t n, int64_t ntiles, int64
     SC_LAUNCHED(1);
     if (WMODE & 64) {
         long long h[8];
-        SC_CUDA(cudaMemcpyAsync(h, dbg.p, sizeof(h), cudaMemcpyDeviceToHost, st));
-        SC_CUDA(cudaStreamSynchronize(st));
+        SC_CUDA(d2h_sync(h, dbg.p, sizeof(h), st));
         const double warps = (double)grid * 8;
         fprintf(stderr, "[knn_tc2 list path] per warp: cycles t<16 %.3g, 16<=t<128 %.3g, t>=128 %.3g; "
                         "fired halves %.0f / %.0f / %.0f\n",
@@ -1267,8 +1265,7 @@ int knn_select(int64_t n, int64_t d, const double* x, int64_t knn, double two_si
         knn_rownorm_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, st>>>(n, d, x, mean.p, rn.p, rmax.p);
         SC_LAUNCHED(1);
         unsigned long long rb = 0;
-        SC_CUDA(cudaMemcpyAsync(&rb, rmax.p, sizeof(rb), cudaMemcpyDeviceToHost, st));
-        SC_CUDA(cudaStreamSynchronize(st));
+        SC_CUDA(d2h_sync(&rb, rmax.p, sizeof(rb), st));
         double rm;
         std::memcpy(&rm, &rb, sizeof(rm));
         // power-of-two scale: every |element| <= 128, |row|^2 stays far from overflow
@@ -1317,8 +1314,7 @@ int knn_select(int64_t n, int64_t d, const double* x, int64_t knn, double two_si
                 pivot_dist_kernel<<<dim3((unsigned)ceil_div(C, 128), (unsigned)C), 128, 0, st>>>(C, d, piv.p, pd.p);
                 SC_LAUNCHED(1);
                 std::vector<float> hd((size_t)C * C);
-                SC_CUDA(cudaMemcpyAsync(hd.data(), pd.p, sizeof(float) * C * C, cudaMemcpyDeviceToHost, st));
-                SC_CUDA(cudaStreamSynchronize(st));
+                SC_CUDA(d2h_sync(hd.data(), pd.p, sizeof(float) * C * C, st));
                 std::vector<int32_t> order;
                 pivot_tour(C, hd, order);
                 SC_CUDA(cudaMemcpyAsync(ord.p, order.data(), sizeof(int32_t) * C, cudaMemcpyHostToDevice, st));
@@ -1336,9 +1332,11 @@ int knn_select(int64_t n, int64_t d, const double* x, int64_t knn, double two_si
         knn_prep_f16_kernel<<<(unsigned)ceil_div(n_pad, 8), 256, 0, st>>>(n, n_pad, d, dp64, x, mean.p, scale, perm,
                                                                           xh.p, cnf.p, qn.p);
         SC_LAUNCHED(1);
+        PhaseClock pct(st);
         if ((rc = knn_candidates_tc(n, n_pad, dp64, xh.p, cnf.p, (float)(-2.0 / (scale * scale)), qtile0, nq, cap, R,
                                     lists.p, counts.p, taus.p, st)))
             return rc;
+        pct.lap("candidate tiles");
         if (std::getenv("SPECLUST_KNN_TILE_ONLY"))  // profiling: stop after the candidate kernel
             return fail(SC_ERR_VALUE, "SPECLUST_KNN_TILE_ONLY set");
         // fp16 rounding of both operands (u = 2^-11) + fp32 accumulation of
@@ -1377,9 +1375,10 @@ int knn_select(int64_t n, int64_t d, const double* x, int64_t knn, double two_si
             rmax.p, cdelta, perm, sel, flagged.p, nflag.p, ms, xs.p, selv);
         SC_LAUNCHED(1);
     }
+    PhaseClock pcr(st);
     unsigned long long hflag = 0;
-    SC_CUDA(cudaMemcpyAsync(&hflag, nflag.p, sizeof(hflag), cudaMemcpyDeviceToHost, st));
-    SC_CUDA(cudaStreamSynchronize(st));
+    SC_CUDA(d2h_sync(&hflag, nflag.p, sizeof(hflag), st));
+    if (pcr.on) fprintf(stderr, "[knn_order] flagged rows %llu\n", hflag);
     lists.free();
     xf.free();
     xh.free();
@@ -1403,6 +1402,7 @@ int knn_select(int64_t n, int64_t d, const double* x, int64_t knn, double two_si
             iota_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, perm_out);
         SC_LAUNCHED((hflag > 0 ? 1 : 0) + (perm ? 0 : 1));
     }
+    pcr.lap("fallback + sort");
     // the pooled scratch above is released on st; callers see sel/perm ordered on st
     if (stats) {
         stats[0] = R;
@@ -1435,8 +1435,7 @@ int knn_union(int64_t n, int64_t d, const double* x, int64_t knn, double two_sig
     SC_LAUNCHED(2);
     if ((rc = exclusive_scan_i64(nl, rc_cnt.p, rev_ptr.p, tmp.p, st))) return rc;
     int64_t nrev = 0;
-    SC_CUDA(cudaMemcpyAsync(&nrev, rev_ptr.p + nl, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    SC_CUDA(cudaStreamSynchronize(st));
+    SC_CUDA(d2h_sync(&nrev, rev_ptr.p + nl, sizeof(int64_t), st));
     DevBuf<int64_t> rev_src;  // with selv: the selection slot of each reverse entry
     if ((rc = rev.alloc(std::max<int64_t>(nrev, 1))) || (rc = dup.alloc(std::max<int64_t>(nrev, 1)))) return rc;
     if (selv && (rc = rev_src.alloc(std::max<int64_t>(nrev, 1)))) return rc;
@@ -1447,8 +1446,7 @@ int knn_union(int64_t n, int64_t d, const double* x, int64_t knn, double two_sig
     SC_LAUNCHED(2);
     if ((rc = exclusive_scan_i64(nl, len.p, row_ptr, tmp.p, st))) return rc;
     int64_t nnz = 0;
-    SC_CUDA(cudaMemcpyAsync(&nnz, row_ptr + nl, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    SC_CUDA(cudaStreamSynchronize(st));
+    SC_CUDA(d2h_sync(&nnz, row_ptr + nl, sizeof(int64_t), st));
     *nnz_out = nnz;
     if (nnz > cap)
         return fail(SC_ERR_VALUE, "knn union: " + std::to_string(nnz) + " entries exceed the output capacity " +
@@ -1486,11 +1484,14 @@ int knn_graph_build(int64_t n, int64_t d, const double* x, int64_t knn, double t
     DevBuf<double> selv;  // exact d2 of every selection slot, reused by the CSR fill
     int rc;
     if ((rc = sel.alloc((size_t)n * knn)) || (rc = perm.alloc(n)) || (rc = selv.alloc((size_t)n * knn))) return rc;
+    PhaseClock pc(st);
     if ((rc = knn_select(n, d, x, knn, two_sigma_sq, 0, n, sel.p, perm.p, stats, st, KnnMeasure(), selv.p)))
         return rc;
+    pc.lap("select total");
     if ((rc = knn_union(n, d, x, knn, two_sigma_sq, sel.p, perm.p, 0, n, row_ptr, col, vals, 2 * n * knn, nnz_out,
                         st, KnnMeasure(), selv.p)))
         return rc;
+    pc.lap("union");
     if (stats) stats[3] = *nnz_out;
     return SC_OK;
 }
@@ -1634,8 +1635,7 @@ extern "C" int sc_knn_graph_measure_f64(int64_t n, int64_t d, const double* x, i
     corr_prep_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(n, d, x, kind == 2, xc.p, sq.p, xn.p, bad.p);
     SC_LAUNCHED(1);
     unsigned long long hb = 0;
-    SC_CUDA(cudaMemcpyAsync(&hb, bad.p, sizeof(hb), cudaMemcpyDeviceToHost, st));
-    SC_CUDA(cudaStreamSynchronize(st));
+    SC_CUDA(d2h_sync(&hb, bad.p, sizeof(hb), st));
     if (hb != ~0ull) {  // graph.py:158-163: every point is checked
         *degenerate = (int64_t)hb;
         return fail(SC_ERR_VALUE, "degenerate vector at point index " + std::to_string(hb));

@@ -930,8 +930,7 @@ struct sc_lanczos {
     }
     double read_scal(int idx) {
         double v = 0.0;
-        cudaMemcpyAsync(&v, scal.p + idx, sizeof(double), cudaMemcpyDeviceToHost, st);
-        cudaStreamSynchronize(st);
+        d2h_sync(&v, scal.p + idx, sizeof(double), st);
         return v;
     }
     // unit vector orthogonal to B[:, :count] into column `dst` (eigen.py:137-150)
@@ -1014,8 +1013,7 @@ struct sc_lanczos {
             sumsq_partial_kernel<<<(unsigned)nb_n, 256, 0, st>>>(n, w.p, sqp.p, nonfinite.p);
             SC_LAUNCHED(1);
             int bad = 0;
-            SC_CUDA(cudaMemcpyAsync(&bad, nonfinite.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-            SC_CUDA(cudaStreamSynchronize(st));
+            SC_CUDA(d2h_sync(&bad, nonfinite.p, sizeof(int), st));
             if (bad) return fail(SC_ERR_VALUE, "out_slot contains non-finite values");
         }
         // Orthogonalisation (reference: recurrence + CGS2 over the whole
@@ -1039,8 +1037,7 @@ struct sc_lanczos {
         if (windowed && !arrow_step && cnt <= WCG_MAX) {
             ProfScope prof("reorth", st, 3.0 * (double)n * cnt * 8.0);
             if ((rc = window_cgs2(lo, cnt))) return rc;
-            SC_CUDA(cudaMemcpyAsync(ab, scal.p, sizeof(double) * 4, cudaMemcpyDeviceToHost, st));
-            SC_CUDA(cudaStreamSynchronize(st));
+            SC_CUDA(d2h_sync(ab, scal.p, sizeof(double) * 4, st));
         } else {
             ProfScope prof("reorth", st, 2.0 * (double)n * cnt * 8.0);
             if ((rc = project(w.p, cnt, sq0.p, lo))) return rc;
@@ -1052,8 +1049,7 @@ struct sc_lanczos {
                 finish_norm_kernel<<<1, 1024, 0, st>>>(nb_n, sqp.p, scal.p, 0);
                 SC_LAUNCHED(1);
             }
-            SC_CUDA(cudaMemcpyAsync(ab, scal.p, sizeof(double) * 4, cudaMemcpyDeviceToHost, st));
-            SC_CUDA(cudaStreamSynchronize(st));
+            SC_CUDA(d2h_sync(ab, scal.p, sizeof(double) * 4, st));
         }
         // second pass over the WHOLE basis: always in full mode (the
         // reference's unconditional CGS2, eigen.py:131-135); in windowed mode
@@ -1069,8 +1065,7 @@ struct sc_lanczos {
             }
             finish_norm_kernel<<<1, 1024, 0, st>>>(nb_n, sqp.p, scal.p, 0);
             SC_LAUNCHED(1);
-            SC_CUDA(cudaMemcpyAsync(ab, scal.p, sizeof(double), cudaMemcpyDeviceToHost, st));
-            SC_CUDA(cudaStreamSynchronize(st));
+            SC_CUDA(d2h_sync(ab, scal.p, sizeof(double), st));
         }
         if (windowed && j + 1 == m) {
             // end of the sweep: the last window against the older basis, then
@@ -1086,8 +1081,7 @@ struct sc_lanczos {
             if ((rc = project(w.p, (int)m)) || (rc = subtract(w.p, (int)m, true))) return rc;
             finish_norm_kernel<<<1, 1024, 0, st>>>(nb_n, sqp.p, scal.p, 0);
             SC_LAUNCHED(1);
-            SC_CUDA(cudaMemcpyAsync(ab, scal.p, sizeof(double), cudaMemcpyDeviceToHost, st));
-            SC_CUDA(cudaStreamSynchronize(st));
+            SC_CUDA(d2h_sync(ab, scal.p, sizeof(double), st));
         }
         const double beta = ab[0], alpha = ab[2];
         scale = std::max(scale, std::max(std::fabs(alpha), beta));
@@ -1170,8 +1164,7 @@ struct sc_lanczos {
         if ((rc = block_tn(n, ld, (int)nb, B.p + ob * ld, B.p + c0 * ld, c, bH.p, bpart.p, bmax.p, st))) return rc;
         if ((rc = block_nn(n, ld, (int)nb, B.p + ob * ld, bH.p, c, B.p + c0 * ld, st))) return rc;
         unsigned long long bits = 0;
-        SC_CUDA(cudaMemcpyAsync(&bits, bmax.p, sizeof(bits), cudaMemcpyDeviceToHost, st));
-        SC_CUDA(cudaStreamSynchronize(st));
+        SC_CUDA(d2h_sync(&bits, bmax.p, sizeof(bits), st));
         double loss;
         memcpy(&loss, &bits, sizeof(loss));
         static const bool dbg = std::getenv("SPECLUST_FLUSH_DEBUG") != nullptr;
@@ -1255,10 +1248,9 @@ struct sc_lanczos {
         theta_k.assign(k, 0.0);
         std::vector<double> lr(k);
         int hinfo = 0;
-        SC_CUDA(cudaMemcpyAsync(theta_k.data(), wsort.p, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
-        SC_CUDA(cudaMemcpyAsync(lr.data(), lastrow.p, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
-        SC_CUDA(cudaMemcpyAsync(&hinfo, info.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-        SC_CUDA(cudaStreamSynchronize(st));
+        SC_CUDA(d2h_sync(theta_k.data(), wsort.p, sizeof(double) * k, st));
+        SC_CUDA(d2h_sync(lr.data(), lastrow.p, sizeof(double) * k, st));
+        SC_CUDA(d2h_sync(&hinfo, info.p, sizeof(int), st));
         if (hinfo) {
             state = 2;
             return fail(SC_ERR_INTERNAL, "projected eigenproblem: QL did not converge");
@@ -1362,8 +1354,7 @@ static int residuals_launch(int64_t n, int64_t k, const int64_t* row_ptr, const 
         residual_partial_kernel<<<(unsigned)nb, 256, 0, st>>>(n, k, row_ptr, col, vals, V, theta_dev, p.p);
     colnorm_finish_kernel<<<(unsigned)ceil_div(k, 128), 128, 0, st>>>(nb, k, p.p, nr.p);
     SC_LAUNCHED(2);
-    SC_CUDA(cudaMemcpyAsync(res_host, nr.p, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
-    SC_CUDA(cudaStreamSynchronize(st));
+    SC_CUDA(d2h_sync(res_host, nr.p, sizeof(double) * k, st));
     return SC_OK;
 }
 
@@ -1434,8 +1425,7 @@ int sc_eigensolve_csr(int64_t n, const int64_t* row_ptr, const int32_t* col, con
     if (rc) return rc;
     s.vec_out = vectors;  // the converged Ritz vectors go straight to the caller's buffer
     int64_t nnz = 0;
-    SC_CUDA(cudaMemcpyAsync(&nnz, row_ptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    SC_CUDA(cudaStreamSynchronize(st));
+    SC_CUDA(d2h_sync(&nnz, row_ptr + n, sizeof(int64_t), st));
     // large operators: SELL-32-sigma copy for the hundreds of matvecs
     SellMatrix sell;
     const char* fenv = std::getenv("SPECLUST_SPMV_FORMAT");
@@ -1475,8 +1465,7 @@ int sc_symmetry_probe(int64_t n, const int64_t* row_ptr, const int32_t* col, con
     *ratio_out = 0.0;
     if (n <= 0) return SC_OK;
     int64_t nnz = 0;
-    SC_CUDA(cudaMemcpyAsync(&nnz, row_ptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    SC_CUDA(cudaStreamSynchronize(st));
+    SC_CUDA(d2h_sync(&nnz, row_ptr + n, sizeof(int64_t), st));
     DevBuf<double> x, y, ax, ay, part, out;
     int64_t nb = ceil_div(n, 256);
     int rc;
@@ -1499,8 +1488,7 @@ int sc_symmetry_probe(int64_t n, const int64_t* row_ptr, const int32_t* col, con
         finish_norm_kernel<<<1, 1024, 0, st>>>(nb, part.p, out.p, 2);
         SC_LAUNCHED(6);
         double h[3];
-        SC_CUDA(cudaMemcpyAsync(h, out.p, sizeof(double) * 3, cudaMemcpyDeviceToHost, st));
-        SC_CUDA(cudaStreamSynchronize(st));
+        SC_CUDA(d2h_sync(h, out.p, sizeof(double) * 3, st));
         double denom = h[1] * h[2];
         double r = denom > 0 ? std::fabs(h[0]) / denom : 0.0;
         worst = std::max(worst, r);
@@ -1514,8 +1502,7 @@ int sc_symmetry_probe(int64_t n, const int64_t* row_ptr, const int32_t* col, con
         SC_LAUNCHED(1);
     }
     unsigned long long vb = 0;
-    SC_CUDA(cudaMemcpyAsync(&vb, vmax.p, sizeof(vb), cudaMemcpyDeviceToHost, st));
-    SC_CUDA(cudaStreamSynchronize(st));
+    SC_CUDA(d2h_sync(&vb, vmax.p, sizeof(vb), st));
     double vm;
     std::memcpy(&vm, &vb, sizeof(vm));
     *ratio_out = worst / std::max(1.0, vm);
@@ -1603,8 +1590,7 @@ int sc_symeig_f64(int64_t m, int64_t kout, const double* T, double* theta, doubl
     SC_CUDA(cudaMemcpyAsync(A.p, T, sizeof(double) * m * m, cudaMemcpyDeviceToDevice, st));
     if ((rc = symeig_launch((int)m, (int)kout, A.p, Z.p, wraw.p, theta, S, info.p, st))) return rc;
     int h = 0;
-    SC_CUDA(cudaMemcpyAsync(&h, info.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-    SC_CUDA(cudaStreamSynchronize(st));
+    SC_CUDA(d2h_sync(&h, info.p, sizeof(int), st));
     if (h) return fail(SC_ERR_INTERNAL, "projected eigenproblem: QL did not converge");
     return SC_OK;
 }

@@ -134,8 +134,7 @@ int sc_edge_similarity_f64(int64_t n, int64_t d, const double* x, int64_t m, con
     degenerate_kernel<<<(unsigned)ceil_div(2 * m, 256), 256, 0, st>>>(m, pairs, sq.p, first.p);
     SC_LAUNCHED(2);
     unsigned long long h = 0;
-    SC_CUDA(cudaMemcpyAsync(&h, first.p, sizeof(h), cudaMemcpyDeviceToHost, st));
-    SC_CUDA(cudaStreamSynchronize(st));
+    SC_CUDA(d2h_sync(&h, first.p, sizeof(h), st));
     if (h != ~0ull) {
         *degenerate = (int64_t)h;
         return fail(SC_ERR_VALUE, "degenerate vector at point index " + std::to_string(h));
@@ -178,8 +177,7 @@ int sc_pattern_edges_f64(int64_t n, int64_t d, const double* x, int mode, double
         SC_LAUNCHED(1);
         // the reference checks every point (graph.py:153: _check_nondegenerate(sq, kind))
         std::vector<double> hsq(n);
-        SC_CUDA(cudaMemcpyAsync(hsq.data(), sq.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
-        SC_CUDA(cudaStreamSynchronize(st));
+        SC_CUDA(d2h_sync(hsq.data(), sq.p, sizeof(double) * n, st));
         for (int64_t i = 0; i < n; ++i)
             if (hsq[i] == 0.0) {
                 *degenerate = i;
@@ -191,8 +189,7 @@ int sc_pattern_edges_f64(int64_t n, int64_t d, const double* x, int mode, double
     pattern_count_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, st>>>(n, d, xs, sq.p, kmode, pa, pb, counts.p);
     SC_LAUNCHED(1);
     if ((rc = exclusive_scan_i64(n, counts.p, offs.p, tmp.p, st))) return rc;
-    SC_CUDA(cudaMemcpyAsync(m_out, offs.p + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    SC_CUDA(cudaStreamSynchronize(st));
+    SC_CUDA(d2h_sync(m_out, offs.p + n, sizeof(int64_t), st));
     if (!pairs || *m_out == 0) return SC_OK;
     pattern_fill_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, st>>>(n, d, xs, sq.p, kmode, pa, pb, offs.p, pairs);
     SC_LAUNCHED(1);

@@ -243,8 +243,7 @@ int sc_sbm_csr(int64_t n, const int64_t* offsets, int64_t nblocks, double p_in, 
     SC_LAUNCHED(1);
     if ((rc = exclusive_scan_i64(n, up_cnt.p, up_ptr.p, tmp.p, st))) return rc;
     int64_t nup = 0;
-    SC_CUDA(cudaMemcpyAsync(&nup, up_ptr.p + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    SC_CUDA(cudaStreamSynchronize(st));
+    SC_CUDA(d2h_sync(&nup, up_ptr.p + n, sizeof(int64_t), st));
     *nnz_out = 2 * nup;
     if (!col) return SC_OK;
     DevBuf<int32_t> up_col;
@@ -262,8 +261,7 @@ int sc_sbm_csr(int64_t n, const int64_t* offsets, int64_t nblocks, double p_in, 
     sbm_row_len_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, up_ptr.p, low_cnt.p, len.p, maxlow.p);
     SC_LAUNCHED(2);
     unsigned int hmax = 0;
-    SC_CUDA(cudaMemcpyAsync(&hmax, maxlow.p, sizeof(hmax), cudaMemcpyDeviceToHost, st));
-    SC_CUDA(cudaStreamSynchronize(st));
+    SC_CUDA(d2h_sync(&hmax, maxlow.p, sizeof(hmax), st));
     if ((rc = exclusive_scan_i64(n, len.p, row_ptr, tmp.p, st))) return rc;
     sbm_scatter_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, up_ptr.p, up_col.p, low_cnt.p, row_ptr, cursor.p,
                                                                    col, vals);

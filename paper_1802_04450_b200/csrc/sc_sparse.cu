@@ -434,8 +434,7 @@ static int spmv_placed_launch(int64_t n, const int64_t* row_ptr, const int32_t* 
         SC_CUDA(cudaStreamSynchronize(st));
         smid_probe_kernel<<<nblk, 256, 0, st>>>(dsm);
         std::vector<int> sm(nblk);
-        SC_CUDA(cudaMemcpyAsync(sm.data(), dsm, sizeof(int) * nblk, cudaMemcpyDeviceToHost, st));
-        SC_CUDA(cudaStreamSynchronize(st));
+        SC_CUDA(d2h_sync(sm.data(), dsm, sizeof(int) * nblk, st));
         cudaFree(dsm);
         // ranges: the distinct SMs seen, in id order; blocks numbered within each
         std::vector<int> ids(sm), cnt;
@@ -660,8 +659,7 @@ int sc_spmv_f64(int64_t n_rows, int64_t n_cols, const int64_t* row_ptr, const in
     cudaStream_t st = as_stream(stream);
     StreamScope stream_scope(st);
     int64_t nnz = 0;
-    if (n_rows > 0) SC_CUDA(cudaMemcpyAsync(&nnz, row_ptr + n_rows, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    SC_CUDA(cudaStreamSynchronize(st));
+    if (n_rows > 0) SC_CUDA(d2h_sync(&nnz, row_ptr + n_rows, sizeof(int64_t), st));
     return spmv_launch(n_rows, nnz, row_ptr, col, vals, x, y, deterministic != 0, st);
 }
 
@@ -683,8 +681,7 @@ int sc_find_nonpositive(int64_t n, const double* d, int mode, int64_t* count_out
     count_nonpositive_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, d, mode, cnt.p);
     SC_LAUNCHED(1);
     unsigned long long h = 0;
-    SC_CUDA(cudaMemcpyAsync(&h, cnt.p, sizeof(h), cudaMemcpyDeviceToHost, st));
-    SC_CUDA(cudaStreamSynchronize(st));
+    SC_CUDA(d2h_sync(&h, cnt.p, sizeof(h), st));
     *count_out = (int64_t)h;
     if (h > 0 && idx_out && max_idx > 0) {
         list_nonpositive_kernel<<<1, 1024, 0, st>>>(n, d, mode, idx_out, max_idx);
@@ -759,9 +756,8 @@ int sc_csr_validate(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* 
     cudaStream_t st = as_stream(stream);
     StreamScope stream_scope(st);
     int64_t ends[2] = {0, 0};
-    SC_CUDA(cudaMemcpyAsync(&ends[0], row_ptr, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    SC_CUDA(cudaMemcpyAsync(&ends[1], row_ptr + n_rows, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    SC_CUDA(cudaStreamSynchronize(st));
+    SC_CUDA(d2h_sync(&ends[0], row_ptr, sizeof(int64_t), st));
+    SC_CUDA(d2h_sync(&ends[1], row_ptr + n_rows, sizeof(int64_t), st));
     if (ends[0] != 0 || ends[1] != nnz) return fail(SC_ERR_FORMAT, "row_ptr must start at 0 and end at nnz");
     if (n_rows == 0) return SC_OK;
     DevBuf<unsigned long long> flags;
@@ -771,8 +767,7 @@ int sc_csr_validate(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* 
                                                                        flags.p);
     SC_LAUNCHED(1);
     unsigned long long h[4];
-    SC_CUDA(cudaMemcpyAsync(h, flags.p, sizeof(h), cudaMemcpyDeviceToHost, st));
-    SC_CUDA(cudaStreamSynchronize(st));
+    SC_CUDA(d2h_sync(h, flags.p, sizeof(h), st));
     if (h[0]) return fail(SC_ERR_FORMAT, "row_ptr must be non-decreasing");
     if (h[1]) return fail(SC_ERR_FORMAT, "column index out of range");
     if (h[2]) return fail(SC_ERR_FORMAT, "column indices must strictly increase within rows");
@@ -797,9 +792,8 @@ int sc_csr_is_symmetric(int64_t n, int64_t nnz, const int64_t* row_ptr, const in
     SC_LAUNCHED(1);
     int h = 0;
     unsigned long long hul[2] = {0, 0};
-    SC_CUDA(cudaMemcpyAsync(&h, bad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-    SC_CUDA(cudaMemcpyAsync(hul, ul.p, sizeof(hul), cudaMemcpyDeviceToHost, st));
-    SC_CUDA(cudaStreamSynchronize(st));
+    SC_CUDA(d2h_sync(&h, bad.p, sizeof(int), st));
+    SC_CUDA(d2h_sync(hul, ul.p, sizeof(hul), st));
     *result = (h || hul[0] != hul[1]) ? 0 : 1;
     return SC_OK;
 }
@@ -1154,8 +1148,7 @@ int SellMatrix::build(int64_t n_, const int64_t* row_ptr_in, const int32_t* col_
     const int64_t nwin = ceil_div(n, SELL_SIGMA);
     nslices = nwin * (SELL_SIGMA / 32);
     int64_t nnz = 0;
-    SC_CUDA(cudaMemcpyAsync(&nnz, row_ptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    SC_CUDA(cudaStreamSynchronize(st));
+    SC_CUDA(d2h_sync(&nnz, row_ptr + n, sizeof(int64_t), st));
     // hub threshold: twice the mean row length (at least 64)
     lcap = std::max<int64_t>(64, 2 * ceil_div(nnz, std::max<int64_t>(n, 1)));
     DevBuf<int64_t> size, tmp;
@@ -1171,9 +1164,8 @@ int SellMatrix::build(int64_t n_, const int64_t* row_ptr_in, const int32_t* col_
     SC_LAUNCHED(2);
     if ((rc = exclusive_scan_i64(nslices, size.p, slice_ptr.p, tmp.p, st))) return rc;
     unsigned long long hl = 0;
-    SC_CUDA(cudaMemcpyAsync(&stored, slice_ptr.p + nslices, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    SC_CUDA(cudaMemcpyAsync(&hl, cnt.p, sizeof(hl), cudaMemcpyDeviceToHost, st));
-    SC_CUDA(cudaStreamSynchronize(st));
+    SC_CUDA(d2h_sync(&stored, slice_ptr.p + nslices, sizeof(int64_t), st));
+    SC_CUDA(d2h_sync(&hl, cnt.p, sizeof(hl), st));
     nlong = (int64_t)hl;
     if ((rc = col.alloc(std::max<int64_t>(stored, 1))) || (rc = vals.alloc(std::max<int64_t>(stored, 1)))) return rc;
     sell_fill_kernel<<<(unsigned)ceil_div(nslices, 8), 256, 0, st>>>(nslices, row_ptr_in, col_in, vals_in, slice_ptr.p,
@@ -1373,8 +1365,7 @@ int SpmvPlan::build(int64_t n_, const int64_t* row_ptr_, const int32_t* col_, co
     vals = vals_;
     nnz = 0;
     if (n > 0) {
-        SC_CUDA(cudaMemcpyAsync(&nnz, row_ptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-        SC_CUDA(cudaStreamSynchronize(st));
+        SC_CUDA(d2h_sync(&nnz, row_ptr + n, sizeof(int64_t), st));
     }
     nch = std::max<int64_t>(1, ceil_div(nnz, SPMV_CH));
     int rc;
@@ -1522,8 +1513,7 @@ extern "C" int sc_csr_remove_isolated(int64_t n, const int64_t* row_ptr, const i
     induced_fill_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, st>>>(n, row_ptr, col, vals, remap, out_row_ptr, out_col,
                                                                   out_vals);
     SC_LAUNCHED(1);
-    SC_CUDA(cudaMemcpyAsync(nnz_new, out_row_ptr + *n_new, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    SC_CUDA(cudaStreamSynchronize(st));
+    SC_CUDA(d2h_sync(nnz_new, out_row_ptr + *n_new, sizeof(int64_t), st));
     return SC_OK;
 }
 

@@ -551,10 +551,15 @@ def _lloyd_cases():
     for n, d, k, kind in [(20_000, 100, 100, "unit"), (9_000, 16, 10, "unit"), (12_000, 200, 300, "unit"),
                           (8_192, 64, 50, "raw"), (6_000, 33, 40, "dup"),
                           # dp > 256: the K-chunk-streaming kernel (odd tile count: a half-full last CTA)
-                          (4_200, 300, 130, "unit"), (5_000, 520, 64, "dup")]:
-        centers = rng.normal(0.0, 1.0, (k, d))
-        v = centers[rng.integers(0, k, n)] + 0.3 * rng.standard_normal((n, d))
-        if kind == "unit":
+                          (4_200, 300, 130, "unit"), (5_000, 520, 64, "dup"),
+                          # d = 256 (two resident point tiles per CTA); three centroids per planted
+                          # cluster: many rows sit between two or three centroids (near ties
+                          # settled by the kept three candidates, as_resolve_kernel)
+                          (10_000, 256, 600, "unit"), (9_000, 192, 240, "split"), (8_500, 256, 300, "split")]:
+        nc = k // 3 if kind == "split" else k
+        centers = rng.normal(0.0, 1.0, (nc, d))
+        v = centers[rng.integers(0, nc, n)] + 0.3 * rng.standard_normal((n, d))
+        if kind in ("unit", "split"):
             v /= np.linalg.norm(v, axis=1, keepdims=True)
         elif kind == "raw":
             v *= 1e3  # large magnitudes: exercises the operand scaling
