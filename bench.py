@@ -365,6 +365,49 @@ def c5_run(torch, n=10_000_000, iters=20):
     return out
 
 
+def c4_run(torch):
+    """C4 at full size (BASELINE.json configs[3]): a planted-partition graph
+    of 500 blocks x 32,000 nodes (p_in 1.6e-3, p_out 8e-7: ~512M undirected
+    unit-weight edges, SURVEY.md:594) drawn on this GPU by the device SBM
+    generator, then run() on it as MatrixInput with k = 500 (eigensolver +
+    k-means).  The 16M x 1001 Krylov basis (128 GB) does not fit beside a
+    separate 16M x 500 eigenvector array, so the pipeline keeps the result in
+    the basis (eigensolve_device_basis)."""
+    import paper_1802_04450_b200 as sc
+    from paper_1802_04450_b200 import pipeline as pl
+    from paper_1802_04450_b200.sbm import SbmConfig, sbm_generate_device
+
+    free, total = torch.cuda.mem_get_info()
+    if total < 170e9:
+        return {"skipped": f"needs ~165 GB of device memory, this GPU has {total / 1e9:.0f} GB"}
+    t0 = time.perf_counter()
+    w, truth = sbm_generate_device(SbmConfig(block_sizes=(32_000,) * 500, p_in=1.6e-3, p_out=8e-7, seed=0))
+    torch.cuda.synchronize()
+    gen_s = time.perf_counter() - t0
+    k = 500
+    cfg = sc.PipelineConfig(input=sc.MatrixInput(matrix=w), k_clusters=k, eigen=sc.LanczosConfig(k=k, seed=0),
+                            kmeans=sc.KmeansConfig(k=k, seed=0), normalize_rows=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    rep, _ = pl.run_device(cfg)
+    e1.record()
+    torch.cuda.synchronize()
+    out = {"workload": "c4: SBM 500 x 32000 nodes, p_in 1.6e-3, p_out 8e-7, k=500, unit weights "
+                       "(BASELINE.json configs[3]), graph resident",
+           "n": w.n_rows, "nnz": w.nnz, "generate_s": gen_s, "seconds": e0.elapsed_time(e1) / 1e3,
+           "stages_s": {a: round(b, 3) for a, b in rep.timings.items()},
+           "eigen": {a: b for a, b in pl.last_info.get("eigen", {}).items() if a != "history"},
+           "kmeans_iters": rep.labeling.iters_run, "max_eigen_residual": float(np.max(rep.eigen_residuals)),
+           "lambda_1": float(rep.eigenvalues[0]), "lambda_k": float(rep.eigenvalues[-1]),
+           "ari_vs_planted": float(sc.adjusted_rand_index(rep.labeling.labels, truth.cpu().numpy())),
+           "ncut": float(rep.ncut_value), "warnings": rep.warnings}
+    del w, truth, rep
+    from paper_1802_04450_b200 import _native as nat
+    nat.load().sc_trim_pool()
+    torch.cuda.empty_cache()
+    return out
+
+
 def _extra(fn):
     """An extra full-size run reported beside the C2 line: a failure is
     reported in its key instead of losing the line."""
@@ -389,6 +432,8 @@ def main():
                     help="skip the extra full-size C3 run (BASELINE.json configs[2] on this GPU) reported under 'c3'")
     ap.add_argument("--no-c5", action="store_true",
                     help="skip the extra full-size C5 k-means run (BASELINE.json configs[4]) reported under 'c5'")
+    ap.add_argument("--c4", action="store_true",
+                    help="also run full-size C4 (BASELINE.json configs[3], ~2-3 min) reported under 'c4'")
     ap.add_argument("--sharded", action="store_true",
                     help="use the sharded driver (distributed.run_sharded) even at N=1; it is always used for N>1")
     args = ap.parse_args()
@@ -573,6 +618,8 @@ def main():
         line["c3"] = _extra(lambda: c3_run(torch, sc, nat, run_device, lib))
     if rank == 0 and world == 1 and not args.no_c5:
         line["c5"] = _extra(lambda: c5_run(torch))
+    if rank == 0 and world == 1 and args.c4:
+        line["c4"] = _extra(lambda: c4_run(torch))
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         # measured CPU baseline: the oracle port on the full C1 workload
         # (BASELINE.json configs[0], the reference's own CPU-runnable case),

@@ -230,6 +230,18 @@ int sc_eigensolve_csr(int64_t n, const int64_t* row_ptr, const int32_t* col,
                       const double* vals, int64_t k, int64_t m, double tol,
                       int64_t max_restarts, uint64_t seed, double* values, double* vectors,
                       double* residuals, sc_lanczos_stats* stats, sc_stream_t stream);
+/* sc_eigensolve_csr with a caller-owned Krylov basis: `basis` holds
+ * (m + 1) * sc_lanczos_basis_ld(n) doubles (column-major, leading dimension
+ * ld = n rounded up to 32) and on return its columns 0..k-1 are the unit
+ * eigenvectors (eigen.py:291-302).  For operators whose basis and a separate
+ * n x k result do not fit the device together (C4: 16M x 1001 basis); the
+ * embedding is then built from the basis columns (sc_recover_embedding_cm)
+ * into its unused columns. */
+int sc_eigensolve_csr_basis(int64_t n, const int64_t* row_ptr, const int32_t* col,
+                            const double* vals, int64_t k, int64_t m, double tol,
+                            int64_t max_restarts, uint64_t seed, double* values, double* basis,
+                            double* residuals, sc_lanczos_stats* stats, sc_stream_t stream);
+int64_t sc_lanczos_basis_ld(int64_t n);
 /* max over the three probes of eigen.py:279-288 of |x'Ay - y'Ax| / (|x| |y|)
  * divided by max(1, max|a|) (host *ratio_out); probes are device Philox normals.
  * The caller raises NotSymmetric when ratio > 1e-10. */
@@ -242,6 +254,10 @@ int sc_symmetry_probe(int64_t n, const int64_t* row_ptr, const int32_t* col,
  * u, out: (dev) n x k row-major (may alias). */
 int sc_recover_embedding(int64_t n, int64_t k, const double* u, const double* d,
                          int normalize_rows, double* out, sc_stream_t stream);
+/* sc_recover_embedding from column-major eigenvectors (element (r, c) at
+ * u[c * ld + r]); out row-major n x k, not overlapping u; same values. */
+int sc_recover_embedding_cm(int64_t n, int64_t k, const double* u, int64_t ld, const double* d,
+                            int normalize_rows, double* out, sc_stream_t stream);
 int sc_normalize_rows(int64_t n, int64_t k, const double* v, double* out, sc_stream_t stream);
 
 /* ---- stage 3: k-means --------------------------------------------------------- */

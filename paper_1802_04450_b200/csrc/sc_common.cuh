@@ -79,8 +79,17 @@ struct DevBuf {
     T* p = nullptr;
     size_t n = 0;
     cudaStream_t s = nullptr;
+    bool owned = true;
+    // use caller memory (not freed here)
+    void borrow(T* ext, size_t count) {
+        free();
+        p = ext;
+        n = count;
+        owned = false;
+    }
     int alloc(size_t count) {
         free();
+        owned = true;
         n = count;
         if (count == 0) return SC_OK;
         ensure_pool();
@@ -101,9 +110,10 @@ struct DevBuf {
         return SC_OK;
     }
     void free() {
-        if (p) cudaFreeAsync(p, s);
+        if (p && owned) cudaFreeAsync(p, s);
         p = nullptr;
         n = 0;
+        owned = true;
     }
     ~DevBuf() { free(); }
     DevBuf() = default;

@@ -710,13 +710,41 @@ __global__ void copy_chunk_cols_kernel(int64_t rows, int64_t k, const double* __
 
 // per-block column sums of squares of a row-major n x k matrix
 constexpr int CN_ROWS = 256;
-__global__ void colsq_partial_kernel(int64_t n, int64_t k, const double* __restrict__ V, double* __restrict__ part) {
+// element (r, c) of V at V[r * rs + c * cs]: row-major (rs = k, cs = 1) or
+// column-major with leading dimension ld (rs = 1, cs = ld); same arithmetic
+__global__ void colsq_partial_kernel(int64_t n, int64_t k, const double* __restrict__ V, int64_t rs, int64_t cs,
+                                     double* __restrict__ part) {
     int64_t r0 = (int64_t)blockIdx.x * CN_ROWS, r1 = imin64(n, r0 + CN_ROWS);
     for (int64_t c = threadIdx.x; c < k; c += blockDim.x) {
         double a = 0.0;
-        for (int64_t r = r0; r < r1; ++r) a = fma(V[r * k + c], V[r * k + c], a);
+        for (int64_t r = r0; r < r1; ++r) a = fma(V[r * rs + c * cs], V[r * rs + c * cs], a);
         part[blockIdx.x * k + c] = a;
     }
+}
+__global__ void scale_cols_colmajor_kernel(int64_t n, int64_t k, int64_t ld, const double* __restrict__ norms,
+                                           double* __restrict__ V) {
+    const int64_t total = k * ld;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x)
+        if (i % ld < n) V[i] = V[i] / norms[i / ld];
+}
+// partial sums of (y_i - theta_c v_i)^2 for one column (residual of a
+// column-major eigenvector from its own SpMV)
+__global__ void resid_col_partial_kernel(int64_t n, const double* __restrict__ y, const double* __restrict__ v,
+                                         const double* __restrict__ theta, int64_t c, double* __restrict__ part) {
+    __shared__ double red[256];
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double a = 0.0;
+    if (i < n) {
+        const double r = y[i] - theta[c] * v[i];
+        a = r * r;
+    }
+    red[threadIdx.x] = a;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if ((int)threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = red[0];
 }
 __global__ void colnorm_finish_kernel(int64_t nb, int64_t k, const double* __restrict__ part,
                                       double* __restrict__ norms) {
@@ -893,6 +921,7 @@ struct sc_lanczos {
 
     DevBuf<double> B, T, w, part, h, sqp, sq0, scal, Y, A, Z, wraw, wsort, S, lastrow, vectors;
     double* vec_out = nullptr;  // converged Ritz vectors (row-major n x k): `vectors` or a caller buffer
+    bool in_basis = false;      // caller-owned basis; the result stays in its columns 0..k-1
     DevBuf<int> info, nonfinite;
     int64_t nb_t = 0, nb_n = 0;
     int rpb_t = GT_ROWS;  // rows per gemv_t block
@@ -955,7 +984,8 @@ struct sc_lanczos {
         return fail(SC_ERR_BREAKDOWN, "could not extend the basis past " + std::to_string(count) + " vectors");
     }
 
-    int init(int64_t n_, int64_t k_, int64_t m_, double tol_, int64_t maxr, uint64_t seed_, cudaStream_t st_) {
+    int init(int64_t n_, int64_t k_, int64_t m_, double tol_, int64_t maxr, uint64_t seed_, cudaStream_t st_,
+             double* basis = nullptr) {
         n = n_;
         k = k_;
         m = m_ > 0 ? m_ : imin64(n_, std::max<int64_t>(2 * k_, k_ + 8));  // eigen.py:53-55
@@ -974,7 +1004,11 @@ struct sc_lanczos {
         nb_t = ceil_div(n, rpb_t);
         nb_n = ceil_div(n, GN_THREADS);
         int rc;
-        if ((rc = B.alloc((size_t)ld * (m + 1))) || (rc = T.alloc((size_t)m * m)) || (rc = w.alloc(ld)) ||
+        if (basis) {
+            B.borrow(basis, (size_t)ld * (m + 1));
+            in_basis = true;
+        }
+        if ((!basis && (rc = B.alloc((size_t)ld * (m + 1)))) || (rc = T.alloc((size_t)m * m)) || (rc = w.alloc(ld)) ||
             (rc = part.alloc((size_t)std::max<int64_t>(nb_t, fz_blocks) * (m + 1))) || (rc = h.alloc(m + 1)) ||
             (rc = sqp.alloc(nb_n)) || (rc = sq0.alloc(nb_t)) ||
             (rc = scal.alloc(8)) || (rc = A.alloc((size_t)m * m)) || (rc = Z.alloc((size_t)m * m)) ||
@@ -1273,6 +1307,15 @@ struct sc_lanczos {
             }
         }
         if (converged && (m == n || verified)) {
+            if (in_basis) {
+                // result in the caller's basis memory: Ritz vectors into
+                // columns 0..k-1 in place (the restart's row-chunked product)
+                if ((rc = ritz_in_place())) return rc;
+                Y.free();
+                if ((rc = normalize_vectors())) return rc;
+                state = 1;
+                return SC_OK;
+            }
             Y.free();
             if (!vec_out) {
                 if ((rc = vectors.alloc((size_t)n * k))) return rc;
@@ -1291,17 +1334,7 @@ struct sc_lanczos {
             return fail(SC_ERR_MAX_RESTARTS, buf);
         }
         ++restarts;
-        // B[:, :k] = B[:, :m] S[:, :k] in place, one row chunk at a time
-        // through a chunk-sized temporary (rows of the product depend only on
-        // the same rows of B), so the restart needs no n x k copy
-        const int64_t chunk = std::min<int64_t>(n, std::max<int64_t>(GB_M, ((int64_t)1 << 28) / (8 * k) / GB_M * GB_M));
-        if (!Y.p && (rc = Y.alloc((size_t)chunk * k))) return rc;
-        for (int64_t r0 = 0; r0 < n; r0 += chunk) {
-            const int64_t rows = std::min<int64_t>(chunk, n - r0);
-            if ((rc = ritz(Y.p, chunk, 0, r0, rows))) return rc;
-            copy_chunk_cols_kernel<<<4 * kNumSMs, 256, 0, st>>>(rows, k, Y.p, chunk, B.p + r0, ld);
-            SC_LAUNCHED(1);
-        }
+        if ((rc = ritz_in_place())) return rc;
         const bool coupled = !converged && beta > kBreakdownRtol * std::max(1.0, scale);
         restart_T_kernel<<<1, 1024, 0, st>>>(m, k, wsort.p, S.p, scal.p, coupled ? 1 : 0, T.p);
         SC_LAUNCHED(1);
@@ -1324,14 +1357,36 @@ struct sc_lanczos {
         return SC_OK;
     }
 
+    // B[:, :k] = B[:, :m] S[:, :k] in place, one row chunk at a time
+    // through a chunk-sized temporary (rows of the product depend only on
+    // the same rows of B), so the restart needs no n x k copy
+    int ritz_in_place() {
+        int rc;
+        const int64_t chunk = std::min<int64_t>(n, std::max<int64_t>(GB_M, ((int64_t)1 << 28) / (8 * k) / GB_M * GB_M));
+        if (!Y.p && (rc = Y.alloc((size_t)chunk * k))) return rc;
+        for (int64_t r0 = 0; r0 < n; r0 += chunk) {
+            const int64_t rows = std::min<int64_t>(chunk, n - r0);
+            if ((rc = ritz(Y.p, chunk, 0, r0, rows))) return rc;
+            copy_chunk_cols_kernel<<<4 * kNumSMs, 256, 0, st>>>(rows, k, Y.p, chunk, B.p + r0, ld);
+            SC_LAUNCHED(1);
+        }
+        return SC_OK;
+    }
+
     int normalize_vectors() {
         int64_t nb = ceil_div(n, CN_ROWS);
         DevBuf<double> p, nr;
         int rc;
         if ((rc = p.alloc((size_t)nb * k)) || (rc = nr.alloc(k))) return rc;
-        colsq_partial_kernel<<<(unsigned)nb, 256, 0, st>>>(n, k, vec_out, p.p);
-        colnorm_finish_kernel<<<(unsigned)ceil_div(k, 128), 128, 0, st>>>(nb, k, p.p, nr.p);
-        scale_cols_rowmajor_kernel<<<4 * kNumSMs, 256, 0, st>>>(n, k, nr.p, vec_out);
+        if (vec_out) {
+            colsq_partial_kernel<<<(unsigned)nb, 256, 0, st>>>(n, k, vec_out, k, 1, p.p);
+            colnorm_finish_kernel<<<(unsigned)ceil_div(k, 128), 128, 0, st>>>(nb, k, p.p, nr.p);
+            scale_cols_rowmajor_kernel<<<4 * kNumSMs, 256, 0, st>>>(n, k, nr.p, vec_out);
+        } else {  // the vectors in the basis columns 0..k-1
+            colsq_partial_kernel<<<(unsigned)nb, 256, 0, st>>>(n, k, B.p, 1, ld, p.p);
+            colnorm_finish_kernel<<<(unsigned)ceil_div(k, 128), 128, 0, st>>>(nb, k, p.p, nr.p);
+            scale_cols_colmajor_kernel<<<4 * kNumSMs, 256, 0, st>>>(n, k, ld, nr.p, B.p);
+        }
         SC_LAUNCHED(3);
         SC_CUDA(cudaStreamSynchronize(st));
         return SC_OK;
@@ -1455,6 +1510,52 @@ int sc_eigensolve_csr(int64_t n, const int64_t* row_ptr, const int32_t* col, con
     if (stats) sc_lanczos_get_stats(&s, stats);
     return SC_OK;
 }
+
+int sc_eigensolve_csr_basis(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* vals, int64_t k,
+                            int64_t m, double tol, int64_t max_restarts, uint64_t seed, double* values, double* basis,
+                            double* residuals, sc_lanczos_stats* stats, sc_stream_t stream) {
+    cudaStream_t st = as_stream(stream);
+    StreamScope stream_scope(st);
+    if (!basis) return fail(SC_ERR_VALUE, "basis workspace required");
+    sc_lanczos s;
+    int rc = s.init(n, k, m, tol, max_restarts, seed, st, basis);
+    if (rc) return rc;
+    int64_t nnz = 0;
+    SC_CUDA(d2h_sync(&nnz, row_ptr + n, sizeof(int64_t), st));
+    while (s.state == 0) {
+        if ((rc = spmv_launch(n, nnz, row_ptr, col, vals, s.in_slot(), s.w.p, false, st))) return rc;
+        rc = s.advance(false);
+        if (rc) {
+            if (stats) sc_lanczos_get_stats(&s, stats);
+            if (rc == SC_ERR_MAX_RESTARTS) {
+                for (int64_t i = 0; i < k; ++i) {
+                    values[i] = s.theta_k[i];
+                    residuals[i] = s.est_k[i];
+                }
+            }
+            return rc;
+        }
+    }
+    for (int64_t i = 0; i < k; ++i) values[i] = s.theta_k[i];
+    // true residuals |A v - theta v| per column (eigen.py:241-248): one SpMV each
+    {
+        const int64_t nb = ceil_div(n, 256);
+        DevBuf<double> p, nr;
+        if ((rc = p.alloc(nb)) || (rc = nr.alloc(k))) return rc;
+        for (int64_t c = 0; c < k; ++c) {
+            const double* v = basis + c * s.ld;
+            if ((rc = spmv_launch(n, nnz, row_ptr, col, vals, v, s.w.p, false, st))) return rc;
+            resid_col_partial_kernel<<<(unsigned)nb, 256, 0, st>>>(n, s.w.p, v, s.wsort.p, c, p.p);
+            finish_norm_kernel<<<1, 1024, 0, st>>>(nb, p.p, nr.p, (int)c);
+            SC_LAUNCHED(2);
+        }
+        SC_CUDA(d2h_sync(residuals, nr.p, sizeof(double) * k, st));
+    }
+    if (stats) sc_lanczos_get_stats(&s, stats);
+    return SC_OK;
+}
+
+int64_t sc_lanczos_basis_ld(int64_t n) { return (n + 31) / 32 * 32; }
 
 int sc_symmetry_probe(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* vals,
                       uint64_t seed, double* ratio_out, sc_stream_t stream) {

@@ -246,6 +246,40 @@ def eigensolve_device(a: DeviceCsr, cfg: LanczosConfig, probe: bool = True):
     return vals, vecs, res, stats
 
 
+def eigensolve_device_basis(a: DeviceCsr, cfg: LanczosConfig, probe: bool = True):
+    """eigensolve_device with the Krylov basis as a caller-owned CUDA tensor
+    ((m + 1) x ld, column j = basis vector j); the eigenvectors come back in
+    its first k rows (column-major n x k with leading dimension ld) and no
+    separate n x k result is allocated -- for operators where the basis and
+    that result do not fit the device together (C4).  Returns (values,
+    basis, ld, residuals, stats)."""
+    torch = nat.torch_cuda()
+    if a.n_rows != a.n_cols:
+        raise NotSquare(f"eigensolve requires a square matrix, got {a.n_rows}x{a.n_cols}")
+    n = a.n_rows
+    m = _validate(n, cfg)
+    if probe:
+        check_symmetric_device(a, cfg.seed)
+    lib = nat.load()
+    ld = int(lib.sc_lanczos_basis_ld(n))
+    basis = nat.empty_device((m + 1, ld), torch.float64)
+    vals = np.zeros(cfg.k)
+    res = np.zeros(cfg.k)
+    st = nat.LanczosStats()
+    rc = lib.sc_eigensolve_csr_basis(n, nat.ptr(a.row_ptr), nat.ptr(a.col), nat.ptr(a.vals), cfg.k, m,
+                                     float(cfg.tol), cfg.max_restarts, int(cfg.seed) & (2**64 - 1),
+                                     vals.ctypes.data_as(nat.P_f64), nat.ptr(basis), res.ctypes.data_as(nat.P_f64),
+                                     nat.C.byref(st), nat.stream_handle())
+    if rc == -9:
+        nat.check(rc, values=vals.copy(), residuals=res.copy())
+    nat.check(rc)
+    stats = dict(restarts=int(st.restarts), breakdowns=int(st.breakdowns), matvecs=int(st.matvecs),
+                 second_passes=int(st.second_passes), flushes=int(st.flushes), max_loss=float(st.max_loss),
+                 mean_window=float(st.mean_window),
+                 history=[float(st.history[i]) for i in range(st.n_history)], m=m, in_basis=True)
+    return vals, basis, ld, res, stats
+
+
 def eigensolve(a, cfg: LanczosConfig) -> EigenBasis:
     """Top-k eigenpairs of a symmetric sparse matrix (eigen.py:291-302)."""
     if a.n_rows != a.n_cols:

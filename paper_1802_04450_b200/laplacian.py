@@ -138,6 +138,23 @@ def recover_embedding_device(u, d, normalize_rows: bool):
     return out
 
 
+def recover_embedding_from_basis(basis, ld: int, n: int, k: int, d, normalize_rows: bool):
+    """recover_embedding_device for eigenvectors left in the Lanczos basis
+    (eigen.eigensolve_device_basis: rows 0..k-1 of `basis`, each a vector of
+    length ld).  The row-major n x k embedding is written into the basis rows
+    k..2k-1 when the basis has them (a view: no new n x k allocation), else
+    into a new tensor."""
+    torch = nat.torch_cuda()
+    flat = basis.view(-1)
+    if basis.shape[0] >= 2 * k:
+        out = flat[k * ld: k * ld + n * k].view(n, k)
+    else:
+        out = nat.empty_device((n, k), torch.float64)
+    nat.check(nat.load().sc_recover_embedding_cm(n, k, nat.ptr(basis), ld, nat.ptr(d), 1 if normalize_rows else 0,
+                                                 nat.ptr(out), nat.stream_handle()))
+    return out
+
+
 def recover_row_eigvecs(u, d):
     """Eigenvectors of the symmetric form -> eigenvectors of D^-1 W with unit
     columns (reference laplacian.py:94-106)."""

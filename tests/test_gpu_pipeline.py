@@ -232,3 +232,48 @@ def test_pipeline_eps_and_threshold_patterns_vs_reference(golden):
     rep = sc.run(cfg)
     assert np.max(np.abs(rep.eigenvalues - f["pt_values"])) <= 1e-8
     assert orc.ari(rep.labeling.labels, f["pt_labels"]) >= 0.999
+
+
+def test_eigensolve_result_in_basis_matches(monkeypatch):
+    """The C4 memory mode (eigenvectors left in the caller-owned Krylov
+    basis, embedding built into its unused rows; sc_eigensolve_csr_basis +
+    sc_recover_embedding_cm) gives the same eigenpairs, embedding and labels
+    as the separate-result path, on an SBM graph (MatrixInput, no locality
+    order) and directly at the eigensolver."""
+    import torch
+
+    from paper_1802_04450_b200 import _native as nat
+    from paper_1802_04450_b200.eigen import eigensolve_device, eigensolve_device_basis
+    from paper_1802_04450_b200.laplacian import (degrees_device, recover_embedding_device,
+                                                 recover_embedding_from_basis, sym_scale)
+    from paper_1802_04450_b200.sbm import SbmConfig, sbm_generate_device
+
+    w, truth = sbm_generate_device(SbmConfig(block_sizes=(400,) * 50, p_in=0.1, p_out=0.002, seed=3))
+    k = 50
+    cfg = sc.PipelineConfig(input=sc.MatrixInput(matrix=w), k_clusters=k, eigen=sc.LanczosConfig(k=k, seed=0),
+                            kmeans=sc.KmeansConfig(k=k, seed=0), normalize_rows=True)
+    monkeypatch.setenv("SPECLUST_EIGEN_BASIS", "0")
+    ref, _ = run_device(cfg)
+    monkeypatch.setenv("SPECLUST_EIGEN_BASIS", "1")
+    got, _ = run_device(cfg)
+    assert np.array_equal(got.eigenvalues, ref.eigenvalues)
+    assert np.allclose(got.eigen_residuals, ref.eigen_residuals, rtol=1e-6, atol=1e-13)
+    assert np.array_equal(got.labeling.labels, ref.labeling.labels)
+    assert got.labeling.sse == ref.labeling.sse
+    # eigensolver level: vectors and the embedding built from the basis rows
+    deg = degrees_device(w)
+    a = sym_scale(w, deg)
+    ecfg = sc.LanczosConfig(k=k, seed=0)
+    vals, vecs, res, _ = eigensolve_device(a, ecfg)
+    vals_b, basis, ld, res_b, stats = eigensolve_device_basis(a, ecfg)
+    n = w.n_rows
+    vb = basis[:k, :n].T
+    assert np.array_equal(vals, vals_b)
+    assert torch.allclose(vb, vecs, rtol=0, atol=1e-12)
+    emb = recover_embedding_device(vecs.contiguous(), deg, True)
+    emb_b = recover_embedding_from_basis(basis, ld, n, k, deg, True)
+    assert emb_b.data_ptr() == basis.data_ptr() + 8 * k * ld  # written into the basis rows k..2k-1
+    emb_c = recover_embedding_device(vb.contiguous(), deg, True)
+    assert torch.equal(emb_b, emb_c)  # bit-identical to the row-major kernel on the same vectors
+    assert torch.allclose(emb_b, emb, rtol=0, atol=1e-11)
+    _ = nat
