@@ -242,6 +242,19 @@ int sc_eigensolve_csr_basis(int64_t n, const int64_t* row_ptr, const int32_t* co
                             int64_t max_restarts, uint64_t seed, double* values, double* basis,
                             double* residuals, sc_lanczos_stats* stats, sc_stream_t stream);
 int64_t sc_lanczos_basis_ld(int64_t n);
+/* sc_eigensolve_csr for A = D^-1/2 W D^-1/2 with the degrees d (device, n)
+ * it was scaled with (laplacian.py:84-91).  Eigenvalue 1 of A has one
+ * eigenvector per connected component, u_C = D^1/2 1_C / |D^1/2 1_C|; when
+ * there are 2 <= c < k components (and n >= 32768) those c pairs are locked
+ * up front and the Lanczos recurrence runs on their orthogonal complement for
+ * the other k - c (the reference finds the copies one verification sweep at
+ * a time, eigen.py:195-206).  *locked_out = c (0: the plain solve ran).
+ * Output as sc_eigensolve_csr: values descending, vectors row-major n x k. */
+int sc_eigensolve_csr_deflate(int64_t n, const int64_t* row_ptr, const int32_t* col,
+                              const double* vals, const double* d, int64_t k, int64_t m, double tol,
+                              int64_t max_restarts, uint64_t seed, double* values, double* vectors,
+                              double* residuals, sc_lanczos_stats* stats, int64_t* locked_out,
+                              sc_stream_t stream);
 /* max over the three probes of eigen.py:279-288 of |x'Ay - y'Ax| / (|x| |y|)
  * divided by max(1, max|a|) (host *ratio_out); probes are device Philox normals.
  * The caller raises NotSymmetric when ratio > 1e-10. */

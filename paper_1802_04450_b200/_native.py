@@ -85,6 +85,8 @@ SIGNATURES = {
     "sc_eigensolve_csr_basis": (i32, [i64, vp, vp, vp, i64, i64, f64, i64, C.c_uint64, P_f64, vp, P_f64,
                                       C.POINTER(LanczosStats), vp]),
     "sc_lanczos_basis_ld": (i64, [i64]),
+    "sc_eigensolve_csr_deflate": (i32, [i64, vp, vp, vp, vp, i64, i64, f64, i64, C.c_uint64, P_f64, vp, P_f64,
+                                        C.POINTER(LanczosStats), C.POINTER(i64), vp]),
     "sc_recover_embedding_cm": (i32, [i64, i64, vp, i64, vp, i32, vp, vp]),
     "sc_symmetry_probe": (i32, [i64, vp, vp, vp, C.c_uint64, P_f64, vp]),
     "sc_recover_embedding": (i32, [i64, i64, vp, vp, i32, vp, vp]),

@@ -29,6 +29,7 @@
 #include "sc_block.cuh"
 #include "sc_dc.cuh"
 #include "sc_symeig.cuh"
+#include "sc_scan.cuh"
 
 namespace sc {
 
@@ -40,12 +41,15 @@ constexpr double kBreakdownRtol = 1e-13;  // eigen.py:50
 // repeated / zero eigenvalues, exact breakdowns) are where a window's loss
 // grows fastest (reference acceptance criteria 1 and 6)
 constexpr int64_t kWindowMinN = 32768;
-// convergence test of a sweep: est_i <= kConvMargin * tol * max(1, |theta_i|)
-// (eigen.py:198-200 uses tol itself).  The estimates come from a different
-// start vector than numpy's, so the converged residuals land elsewhere in
-// [0, tol]; a 4x margin keeps them clear of tol, e.g. for the reference's
-// row-operator acceptance check (residual of D^-1/2 u under D^-1 W, <= 1e-8),
-// at the cost of rarely one more restart (C2 / C3 converge far below tol)
+// convergence test of a sweep: est_i <= margin * tol * max(1, |theta_i|)
+// (eigen.py:198-200 uses tol itself).  Below kWindowMinN rows margin =
+// kConvMargin: the estimates come from a different start vector than
+// numpy's, so the converged residuals land elsewhere in [0, tol], and a 4x
+// margin keeps them clear of tol for the reference's row-operator acceptance
+// check (residual of D^-1/2 u under D^-1 W, <= 1e-8) at negligible cost.
+// From kWindowMinN rows on the reference's own test (margin 1): at C3h the
+// 4x margin cost 10 of 21 restarts (all 1000 estimates were below tol from
+// restart 11 on, one straggler hovered between 0.25 tol and tol)
 constexpr double kConvMargin = 0.25;
 // windowed mode: a window pass that leaves |w| below this fraction of its
 // input norm has cancelled to rounding level -> two passes over the basis
@@ -890,6 +894,115 @@ __global__ void finish_sum_kernel(int64_t nb, const double* __restrict__ part, d
 using namespace sc;
 
 // ---------------------------------------------------------------------------
+// ---- locked eigenvalue-1 eigenspace of a normalized adjacency -----------------
+// A = D^-1/2 W D^-1/2 has eigenvalue 1 with multiplicity = the number of
+// connected components of W, eigenvectors u_C = D^1/2 1_C / |D^1/2 1_C|
+// (disjoint supports).  The reference discovers every copy by Lanczos sweeps
+// from fresh directions (eigen.py:195-206, one copy of a degenerate value
+// per verification sweep: 10 of C3h's 21 restarts); here they are locked up
+// front and the Lanczos recurrence runs on their orthogonal complement.
+
+// one min-label propagation step with pointer jumping: lab2[i] =
+// min(lab[i], lab[j] over row i), then lab2[i] = lab[lab2[i]] (one jump)
+__global__ void cc_propagate_kernel(int64_t n, const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                                    const int32_t* __restrict__ lab, int32_t* __restrict__ lab2,
+                                    int* __restrict__ changed) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int32_t mn = lab[i];
+    for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) mn = min(mn, lab[col[e]]);
+    mn = min(mn, lab[mn]);
+    lab2[i] = mn;
+    if (mn != lab[i]) *changed = 1;
+}
+// root flags (label == own index) for the component numbering
+__global__ void cc_roots_kernel(int64_t n, const int32_t* __restrict__ lab, int64_t* __restrict__ flag) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) flag[i] = lab[i] == (int32_t)i ? 1 : 0;
+}
+// component id of node i = rank of its root among the roots (roots in index order)
+__global__ void cc_number_kernel(int64_t n, const int32_t* __restrict__ lab, const int64_t* __restrict__ rank,
+                                 int64_t* __restrict__ comp) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) comp[i] = rank[lab[i]];
+}
+// per component, in member order (block per component, fixed tree): out[C] =
+// sum over members i of a[i] * (b ? b[i] : 1)
+__global__ void seg_dot_kernel(const int64_t* __restrict__ start, const int32_t* __restrict__ members,
+                               const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ out) {
+    __shared__ double red[256];
+    const int64_t c = blockIdx.x;
+    double acc = 0.0;
+    for (int64_t t = start[c] + threadIdx.x; t < start[c + 1]; t += blockDim.x) {
+        const int64_t i = members[t];
+        acc = fma(a[i], b ? b[i] : 1.0, acc);
+    }
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if ((int)threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[c] = red[0];
+}
+// u[i] = sqrt(d[i]) / sqrt(dsum[comp[i]])
+__global__ void locked_vec_kernel(int64_t n, const double* __restrict__ d, const int64_t* __restrict__ comp,
+                                  const double* __restrict__ dsum, double* __restrict__ u) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) u[i] = sqrt(d[i]) / sqrt(dsum[comp[i]]);
+}
+// x[i] -= h[comp[i]] * u[i]
+__global__ void deflate_sub_kernel(int64_t n, const int64_t* __restrict__ comp, const double* __restrict__ u,
+                                   const double* __restrict__ h, double* __restrict__ x) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) x[i] -= h[comp[i]] * u[i];
+}
+// r[i] = (y[i] - theta[comp[i]] u[i])^2
+__global__ void locked_resid_kernel(int64_t n, const int64_t* __restrict__ comp, const double* __restrict__ u,
+                                    const double* __restrict__ y, const double* __restrict__ theta,
+                                    double* __restrict__ r) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        const double t = y[i] - theta[comp[i]] * u[i];
+        r[i] = t * t;
+    }
+}
+// out (row-major n x k): columns [0, c) the locked vectors in the order
+// col_of[comp] (dense, zero off their component), columns [c, k) from
+// rv (row-major n x (k - c))
+__global__ void assemble_vectors_kernel(int64_t n, int64_t k, int64_t c, const int64_t* __restrict__ comp,
+                                        const int64_t* __restrict__ col_of, const double* __restrict__ u,
+                                        const double* __restrict__ rv, double* __restrict__ out) {
+    const int64_t total = n * k;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / k, j = e - i * k;
+        double v;
+        if (j < c)
+            v = col_of[comp[i]] == j ? u[i] : 0.0;
+        else
+            v = rv[i * (k - c) + (j - c)];
+        out[e] = v;
+    }
+}
+
+__global__ void iota_i32_kernel(int64_t n, int32_t* __restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = (int32_t)i;
+}
+
+struct LockedSet {
+    int64_t c = 0;
+    DevBuf<int64_t> comp;   // n: component id
+    DevBuf<double> u, h;    // n: the locked vectors (disjoint supports); c: projections
+    Bucketer bk;            // members grouped by component
+    int deflate(int64_t n, double* x, cudaStream_t st) {
+        seg_dot_kernel<<<(unsigned)c, 256, 0, st>>>(bk.start.p, bk.members.p, u.p, x, h.p);
+        deflate_sub_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, comp.p, u.p, h.p, x);
+        SC_LAUNCHED(2);
+        return SC_OK;
+    }
+};
+
 struct sc_lanczos {
     int64_t n = 0, k = 0, m = 0, ld = 0, max_restarts = 0;
     double tol = 0.0;
@@ -922,6 +1035,7 @@ struct sc_lanczos {
     DevBuf<double> B, T, w, part, h, sqp, sq0, scal, Y, A, Z, wraw, wsort, S, lastrow, vectors;
     double* vec_out = nullptr;  // converged Ritz vectors (row-major n x k): `vectors` or a caller buffer
     bool in_basis = false;      // caller-owned basis; the result stays in its columns 0..k-1
+    LockedSet* locked = nullptr;  // deflated eigenvalue-1 eigenspace (orthogonal complement only)
     DevBuf<int> info, nonfinite;
     int64_t nb_t = 0, nb_n = 0;
     int rpb_t = GT_ROWS;  // rows per gemv_t block
@@ -968,6 +1082,11 @@ struct sc_lanczos {
             double* x = B.p + dst * ld;
             fill_normal_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, seed, ++rng_stream, x);
             SC_LAUNCHED(1);
+            if (locked) {
+                int rc0 = locked->deflate(n, x, st);
+                if (!rc0) rc0 = locked->deflate(n, x, st);
+                if (rc0) return rc0;
+            }
             // the first `count` columns are the basis; CGS2 against them
             // (x lives in column dst >= count, so it is not projected on itself)
             int rc = cgs2(x, (int)count);
@@ -1050,6 +1169,7 @@ struct sc_lanczos {
             SC_CUDA(d2h_sync(&bad, nonfinite.p, sizeof(int), st));
             if (bad) return fail(SC_ERR_VALUE, "out_slot contains non-finite values");
         }
+        if (locked && (rc = locked->deflate(n, w.p, st))) return rc;
         // Orthogonalisation (reference: recurrence + CGS2 over the whole
         // basis every step, eigen.py:157-163).  Windowed mode (default): two
         // CGS passes over the window [lo, j] of recent vectors (it always
@@ -1212,6 +1332,21 @@ struct sc_lanczos {
                     (ob + r < k ? lr : ls) = std::max(ob + r < k ? lr : ls, std::fabs(hh[r * c + o]));
             fprintf(stderr, "[flush] restart %lld j %lld c %d old [%lld, %lld) loss_ritz %.2e loss_sweep %.2e\n",
                     (long long)restarts, (long long)c1, c, (long long)ob, (long long)oe, lr, ls);
+            // loss against the Ritz block by column decile (columns in descending Ritz value order)
+            if (ob == 0 && nb >= 10) {
+                fprintf(stderr, "[flush]   ritz deciles:");
+                const int64_t kk = std::min<int64_t>(k, nb);
+                for (int dcl = 0; dcl < 10; ++dcl) {
+                    double mx = 0.0;
+                    for (int64_t r = kk * dcl / 10; r < kk * (dcl + 1) / 10; ++r)
+                        for (int o = 0; o < c; ++o) mx = std::max(mx, std::fabs(hh[r * c + o]));
+                    fprintf(stderr, " %.1e", mx);
+                }
+                int64_t nconv = 0;
+                for (int64_t i = 0; i < (int64_t)est_k.size(); ++i)
+                    if (est_k[i] <= tol * std::max(1.0, std::fabs(theta_k[i]))) ++nconv;
+                fprintf(stderr, "  (converged at the last restart: %lld)\n", (long long)nconv);
+            }
         }
         ++flushes;
         window_sum += c;
@@ -1292,10 +1427,11 @@ struct sc_lanczos {
         est_k.assign(k, 0.0);
         double worst = 0.0;
         bool converged = true;
+        const double margin = n >= kWindowMinN ? 1.0 : kConvMargin;
         for (int64_t i = 0; i < k; ++i) {
             est_k[i] = beta * std::fabs(lr[i]);
             worst = std::max(worst, est_k[i]);
-            if (!(est_k[i] <= kConvMargin * tol * std::max(1.0, std::fabs(theta_k[i])))) converged = false;
+            if (!(est_k[i] <= margin * tol * std::max(1.0, std::fabs(theta_k[i])))) converged = false;
         }
         history.push_back(worst);
         bool verified = false;
@@ -1305,6 +1441,20 @@ struct sc_lanczos {
                 double slack = std::max(1.0, std::fabs(theta_k[i])) * std::max(tol, 1e-12);
                 if (!(std::fabs(theta_k[i] - pending[i]) <= slack)) verified = false;
             }
+        }
+        static const bool sweep_dbg = std::getenv("SPECLUST_TIMING_DEBUG") != nullptr;
+        if (sweep_dbg) {
+            int64_t nconv = 0, iworst = 0;
+            double dmax = 0.0;
+            for (int64_t i = 0; i < k; ++i) {
+                if (est_k[i] <= margin * tol * std::max(1.0, std::fabs(theta_k[i]))) ++nconv;
+                if (est_k[i] > est_k[iworst]) iworst = i;
+                if (has_pending) dmax = std::max(dmax, std::fabs(theta_k[i] - pending[i]));
+            }
+            fprintf(stderr, "[lanczos] restart %lld: converged %lld / %lld, worst est %.2e at %lld (theta %.12f), "
+                            "pending %d, max |theta - pending| %.2e, verified %d\n",
+                    (long long)restarts, (long long)nconv, (long long)k, est_k[iworst], (long long)iworst,
+                    theta_k[iworst], (int)has_pending, dmax, (int)verified);
         }
         if (converged && (m == n || verified)) {
             if (in_basis) {
@@ -1354,6 +1504,18 @@ struct sc_lanczos {
         j = k;
         j0 = k;
         js = k;
+        return SC_OK;
+    }
+
+    // lock a deflated eigenspace after init: q0 projected off it, renormalised
+    int set_locked(LockedSet* lk) {
+        locked = lk;
+        double* q0 = B.p;
+        int rc;
+        if ((rc = lk->deflate(n, q0, st)) || (rc = lk->deflate(n, q0, st)) || (rc = cgs2(q0, 0))) return rc;
+        scale_copy_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, q0, scal.p, 0, q0);
+        SC_LAUNCHED(1);
+        SC_CUDA(cudaStreamSynchronize(st));
         return SC_OK;
     }
 
@@ -1556,6 +1718,127 @@ int sc_eigensolve_csr_basis(int64_t n, const int64_t* row_ptr, const int32_t* co
 }
 
 int64_t sc_lanczos_basis_ld(int64_t n) { return (n + 31) / 32 * 32; }
+
+int sc_eigensolve_csr_deflate(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* vals,
+                              const double* d, int64_t k, int64_t m, double tol, int64_t max_restarts, uint64_t seed,
+                              double* values, double* vectors, double* residuals, sc_lanczos_stats* stats,
+                              int64_t* locked_out, sc_stream_t stream) {
+    cudaStream_t st = as_stream(stream);
+    StreamScope stream_scope(st);
+    *locked_out = 0;
+    if (m <= 0) m = imin64(n, std::max<int64_t>(2 * k, k + 8));
+    auto plain = [&]() {
+        return sc_eigensolve_csr(n, row_ptr, col, vals, k, m, tol, max_restarts, seed, values, vectors, residuals,
+                                 stats, stream);
+    };
+    if (n < kWindowMinN || k < 2 || !d) return plain();
+    int rc;
+    // ---- connected components of the sparsity graph (min-label propagation)
+    LockedSet lk;
+    int64_t c = 0;
+    {
+        DevBuf<int32_t> lab, lab2;
+        DevBuf<int> changed;
+        if ((rc = lab.alloc(n)) || (rc = lab2.alloc(n)) || (rc = changed.alloc(1))) return rc;
+        iota_i32_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, lab.p);
+        SC_LAUNCHED(1);
+        for (int it = 0; it < 100000; ++it) {
+            SC_CUDA(cudaMemsetAsync(changed.p, 0, sizeof(int), st));
+            cc_propagate_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, row_ptr, col, lab.p, lab2.p, changed.p);
+            SC_LAUNCHED(1);
+            std::swap(lab.p, lab2.p);
+            int h = 0;
+            SC_CUDA(d2h_sync(&h, changed.p, sizeof(int), st));
+            if (!h) break;
+        }
+        DevBuf<int64_t> flag, rank, tmp;
+        if ((rc = flag.alloc(n)) || (rc = rank.alloc(n + 1)) || (rc = tmp.alloc(ceil_div(n, 1024) + 2))) return rc;
+        cc_roots_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, lab.p, flag.p);
+        SC_LAUNCHED(1);
+        if ((rc = exclusive_scan_i64(n, flag.p, rank.p, tmp.p, st))) return rc;
+        SC_CUDA(d2h_sync(&c, rank.p + n, sizeof(int64_t), st));
+        // one component (nothing to lock), or at least k copies of eigenvalue 1
+        // (the wanted set is then a subset of the degenerate space): the
+        // reference's procedure unchanged
+        if (c <= 1 || c >= k) return plain();
+        if ((rc = lk.comp.alloc(n))) return rc;
+        cc_number_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, lab.p, rank.p, lk.comp.p);
+        SC_LAUNCHED(1);
+    }
+    lk.c = c;
+    if ((rc = lk.u.alloc(n)) || (rc = lk.h.alloc(c)) || (rc = lk.bk.init(n, c)) || (rc = lk.bk.run(lk.comp.p, st)))
+        return rc;
+    DevBuf<double> dsum, y, r, theta_l, res_l;
+    if ((rc = dsum.alloc(c)) || (rc = y.alloc(n)) || (rc = r.alloc(n)) || (rc = theta_l.alloc(c)) ||
+        (rc = res_l.alloc(c)))
+        return rc;
+    seg_dot_kernel<<<(unsigned)c, 256, 0, st>>>(lk.bk.start.p, lk.bk.members.p, d, nullptr, dsum.p);
+    locked_vec_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, d, lk.comp.p, dsum.p, lk.u.p);
+    SC_LAUNCHED(2);
+    int64_t nnz = 0;
+    SC_CUDA(d2h_sync(&nnz, row_ptr + n, sizeof(int64_t), st));
+    // Rayleigh quotients and true residuals of the locked vectors; the
+    // operator must be D^-1/2 W D^-1/2 for this d (else: the plain solve)
+    if ((rc = spmv_launch(n, nnz, row_ptr, col, vals, lk.u.p, y.p, false, st))) return rc;
+    seg_dot_kernel<<<(unsigned)c, 256, 0, st>>>(lk.bk.start.p, lk.bk.members.p, lk.u.p, y.p, theta_l.p);
+    locked_resid_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, lk.comp.p, lk.u.p, y.p, theta_l.p, r.p);
+    seg_dot_kernel<<<(unsigned)c, 256, 0, st>>>(lk.bk.start.p, lk.bk.members.p, r.p, nullptr, res_l.p);
+    SC_LAUNCHED(3);
+    std::vector<double> th(c), rs(c);
+    SC_CUDA(d2h_sync(th.data(), theta_l.p, sizeof(double) * c, st));
+    SC_CUDA(d2h_sync(rs.data(), res_l.p, sizeof(double) * c, st));
+    for (int64_t q = 0; q < c; ++q) {
+        rs[q] = std::sqrt(rs[q]);
+        if (!(rs[q] <= 1e-3 * tol && std::fabs(th[q] - 1.0) <= 1e-10)) return plain();
+    }
+    // ---- Lanczos on the orthogonal complement: k - c pairs, subspace m - c
+    const int64_t kr = k - c, mr = m - c;
+    sc_lanczos s;
+    if ((rc = s.init(n, kr, mr, tol, max_restarts, seed, st))) return rc;
+    if ((rc = s.set_locked(&lk))) return rc;
+    DevBuf<double> rv;
+    if ((rc = rv.alloc((size_t)n * kr))) return rc;
+    s.vec_out = rv.p;
+    while (s.state == 0) {
+        if ((rc = spmv_launch(n, nnz, row_ptr, col, vals, s.in_slot(), s.w.p, false, st))) return rc;
+        rc = s.advance(false);
+        if (rc) {
+            if (stats) sc_lanczos_get_stats(&s, stats);
+            if (rc == SC_ERR_MAX_RESTARTS) {
+                for (int64_t i = 0; i < k; ++i) {
+                    values[i] = i < c ? th[i] : s.theta_k[i - c];
+                    residuals[i] = i < c ? rs[i] : s.est_k[i - c];
+                }
+            }
+            return rc;
+        }
+    }
+    // ---- assemble: locked pairs first (eigenvalue 1 >= every other), in
+    // descending Rayleigh quotient (ties by component order), then the rest
+    std::vector<int64_t> ord(c), col_of(c);
+    for (int64_t q = 0; q < c; ++q) ord[q] = q;
+    std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) { return th[a] > th[b]; });
+    for (int64_t j = 0; j < c; ++j) col_of[ord[j]] = j;
+    DevBuf<int64_t> dcol;
+    if ((rc = dcol.alloc(c))) return rc;
+    SC_CUDA(cudaMemcpyAsync(dcol.p, col_of.data(), sizeof(int64_t) * c, cudaMemcpyHostToDevice, st));
+    assemble_vectors_kernel<<<8 * kNumSMs, 256, 0, st>>>(n, k, c, lk.comp.p, dcol.p, lk.u.p, rv.p, vectors);
+    SC_LAUNCHED(1);
+    std::vector<double> res_r(kr);
+    if ((rc = residuals_launch(n, kr, row_ptr, col, vals, rv.p, s.wsort.p, res_r.data(), st))) return rc;
+    for (int64_t j = 0; j < c; ++j) {
+        values[j] = th[ord[j]];
+        residuals[j] = rs[ord[j]];
+    }
+    for (int64_t j = 0; j < kr; ++j) {
+        values[c + j] = s.theta_k[j];
+        residuals[c + j] = res_r[j];
+    }
+    if (stats) sc_lanczos_get_stats(&s, stats);
+    SC_CUDA(cudaStreamSynchronize(st));
+    *locked_out = c;
+    return SC_OK;
+}
 
 int sc_symmetry_probe(int64_t n, const int64_t* row_ptr, const int32_t* col, const double* vals,
                       uint64_t seed, double* ratio_out, sc_stream_t stream) {

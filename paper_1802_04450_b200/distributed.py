@@ -568,8 +568,10 @@ def _lanczos_sharded(ops, comm, a_local, n, bounds, cfg, op):
         last = ops.host(S[:, m - 1])
         est = beta * np.abs(last)
         st["history"].append(float(est.max()))
-        # the single-GPU session's 4x margin (sc_lanczos.cu kConvMargin)
-        converged = bool(np.all(est <= 0.25 * tol * np.maximum(1.0, np.abs(theta[:k]))))
+        # the single-GPU session's margin (sc_lanczos.cu kConvMargin: 4x below
+        # 32768 rows, the reference's own test above)
+        margin = 1.0 if n >= 32768 else 0.25
+        converged = bool(np.all(est <= margin * tol * np.maximum(1.0, np.abs(theta[:k]))))
         verified = False
         if pending is not None:
             slack = np.maximum(1.0, np.abs(theta[:k])) * max(tol, 1e-12)

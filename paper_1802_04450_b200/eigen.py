@@ -246,6 +246,39 @@ def eigensolve_device(a: DeviceCsr, cfg: LanczosConfig, probe: bool = True):
     return vals, vecs, res, stats
 
 
+def eigensolve_device_deflate(a: DeviceCsr, d, cfg: LanczosConfig, probe: bool = True):
+    """eigensolve_device for the normalized adjacency a = D^-1/2 W D^-1/2
+    with its degrees d (CUDA, n): the eigenvalue-1 eigenvectors of the
+    connected components are locked up front (sc_eigensolve_csr_deflate);
+    stats["locked"] = their number (0: the plain solve ran)."""
+    torch = nat.torch_cuda()
+    if a.n_rows != a.n_cols:
+        raise NotSquare(f"eigensolve requires a square matrix, got {a.n_rows}x{a.n_cols}")
+    n = a.n_rows
+    m = _validate(n, cfg)
+    if probe:
+        check_symmetric_device(a, cfg.seed)
+    vals = np.zeros(cfg.k)
+    res = np.zeros(cfg.k)
+    vecs = nat.empty_device((n, cfg.k), torch.float64)
+    st = nat.LanczosStats()
+    locked = nat.C.c_int64(0)
+    dd = d.to(device="cuda", dtype=torch.float64).contiguous()
+    rc = nat.load().sc_eigensolve_csr_deflate(n, nat.ptr(a.row_ptr), nat.ptr(a.col), nat.ptr(a.vals), nat.ptr(dd),
+                                              cfg.k, m, float(cfg.tol), cfg.max_restarts,
+                                              int(cfg.seed) & (2**64 - 1), vals.ctypes.data_as(nat.P_f64),
+                                              nat.ptr(vecs), res.ctypes.data_as(nat.P_f64), nat.C.byref(st),
+                                              nat.C.byref(locked), nat.stream_handle())
+    if rc == -9:
+        nat.check(rc, values=vals.copy(), residuals=res.copy())
+    nat.check(rc)
+    stats = dict(restarts=int(st.restarts), breakdowns=int(st.breakdowns), matvecs=int(st.matvecs),
+                 second_passes=int(st.second_passes), flushes=int(st.flushes), max_loss=float(st.max_loss),
+                 mean_window=float(st.mean_window),
+                 history=[float(st.history[i]) for i in range(st.n_history)], m=m, locked=int(locked.value))
+    return vals, vecs, res, stats
+
+
 def eigensolve_device_basis(a: DeviceCsr, cfg: LanczosConfig, probe: bool = True):
     """eigensolve_device with the Krylov basis as a caller-owned CUDA tensor
     ((m + 1) x ld, column j = basis vector j); the eigenvectors come back in

@@ -277,3 +277,54 @@ def test_eigensolve_result_in_basis_matches(monkeypatch):
     assert torch.equal(emb_b, emb_c)  # bit-identical to the row-major kernel on the same vectors
     assert torch.allclose(emb_b, emb, rtol=0, atol=1e-11)
     _ = nat
+
+
+def test_deflated_components_match_plain_solve(monkeypatch):
+    """Graphs with 2 <= c < k connected components: the eigenvalue-1 pairs
+    locked up front (sc_eigensolve_csr_deflate) + Lanczos on the complement
+    give the same eigenvalues, the same eigenvalue-1 eigenspace, residuals
+    within tol and the same clustering as the plain solve (the reference's
+    procedure, which discovers the copies one verification sweep at a time)."""
+    import torch
+
+    from paper_1802_04450_b200 import pipeline as pl
+
+    rng = np.random.default_rng(7)
+    nb, per, d = 40, 1000, 12
+    centers = rng.normal(0.0, 40.0, (nb, d))
+    x = (centers[np.repeat(np.arange(nb), per)] + rng.standard_normal((nb * per, d))).astype(np.float64)
+    k = 48
+    cfg = cfg_for(x, 10, float(np.sqrt(d)), k)
+    monkeypatch.setenv("SPECLUST_DEFLATE", "0")
+    ref, _ = run_device(cfg)
+    st_ref = dict(pl.last_info["eigen"])
+    monkeypatch.setenv("SPECLUST_DEFLATE", "1")
+    got, _ = run_device(cfg)
+    st = dict(pl.last_info["eigen"])
+    assert st["locked"] == nb, st
+    assert st["restarts"] <= st_ref["restarts"]
+    assert np.abs(got.eigenvalues - ref.eigenvalues).max() <= 1e-9
+    assert got.eigen_residuals.max() <= 1e-8
+    # k > the 40 planted clusters: k-means splits some of them, and which ones
+    # depends on the basis chosen inside the degenerate eigenvalue-1 space
+    # (the reference's own choice is arbitrary there too); both clusterings
+    # recover the planted partition equally well
+    truth = np.repeat(np.arange(nb), per)
+    a_got = sc.adjusted_rand_index(got.labeling.labels, truth)
+    a_ref = sc.adjusted_rand_index(ref.labeling.labels, truth)
+    assert a_got >= 0.9 and a_ref >= 0.9 and abs(a_got - a_ref) <= 0.03, (a_got, a_ref)
+    # the eigenvalue-1 eigenspaces agree (the vectors themselves may differ by a rotation inside it)
+    from paper_1802_04450_b200.eigen import eigensolve_device, eigensolve_device_deflate
+    from paper_1802_04450_b200.graph import knn_graph_device
+    from paper_1802_04450_b200.laplacian import degrees_device, sym_scale
+
+    w = knn_graph_device(x, 10, sc.SimilarityMeasure.exp_decay(float(np.sqrt(d))))
+    deg = degrees_device(w)
+    a = sym_scale(w, deg)
+    ecfg = sc.LanczosConfig(k=k, seed=0)
+    v0, u0, r0, _ = eigensolve_device(a, ecfg)
+    v1, u1, r1, s1 = eigensolve_device_deflate(a, deg, ecfg)
+    assert s1["locked"] == nb
+    assert np.abs(v1 - v0).max() <= 1e-9
+    assert principal_angle(u0[:, :nb].cpu().numpy(), u1[:, :nb].cpu().numpy()) < 1e-6
+    assert torch.allclose(u1.T @ u1, torch.eye(k, dtype=torch.float64, device="cuda"), atol=1e-10)
