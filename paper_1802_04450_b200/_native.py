@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import sys
 from pathlib import Path
 
 import numpy as np
@@ -173,9 +174,42 @@ def load(path: str | os.PathLike | None = None):
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
+    slow_ms = os.environ.get("SPECLUST_SLOW_MS")
+    if slow_ms:  # diagnostics: report every library call slower than the threshold
+        lib = _SlowLib(lib, float(slow_ms))
     if path is None:
         _lib = lib
     return lib
+
+
+class _SlowLib:
+    """SPECLUST_SLOW_MS=t: wraps the library so that every call taking more
+    than t ms of host wall time is reported on stderr (with the time since
+    the previous call returned, to tell a blocked call from host-side gaps)."""
+
+    def __init__(self, lib, ms):
+        import time
+
+        self._lib, self._ms, self._time = lib, ms, time
+        self._last = time.perf_counter()
+
+    def __getattr__(self, name):
+        fn = getattr(self._lib, name)
+        if not callable(fn) or name.startswith("_"):
+            return fn
+        t = self._time
+
+        def wrapped(*a):
+            t0 = t.perf_counter()
+            gap = (t0 - self._last) * 1e3
+            r = fn(*a)
+            t1 = t.perf_counter()
+            self._last = t1
+            if (t1 - t0) * 1e3 > self._ms or gap > self._ms:
+                sys.stderr.write(f"[slow] {name} {(t1 - t0) * 1e3:.1f} ms (gap before {gap:.1f} ms)\n")
+            return r
+
+        return wrapped
 
 
 def last_error() -> str:

@@ -990,6 +990,25 @@ __global__ void iota_i32_kernel(int64_t n, int32_t* __restrict__ out) {
     if (i < n) out[i] = (int32_t)i;
 }
 
+// SPECLUST_SLOW_MS=t (diagnostics): Lanczos steps whose host wall time
+// exceeds t ms are reported with their step index and phase
+struct SlowWatch {
+    double ms = -1.0;
+    std::chrono::steady_clock::time_point t0;
+    SlowWatch() {
+        const char* e = std::getenv("SPECLUST_SLOW_MS");
+        if (e) ms = std::atof(e);
+        t0 = std::chrono::steady_clock::now();
+    }
+    void lap(const char* what, int64_t a, int64_t b) {
+        if (ms < 0) return;
+        const auto t1 = std::chrono::steady_clock::now();
+        const double dt = std::chrono::duration<double, std::milli>(t1 - t0).count();
+        if (dt > ms) fprintf(stderr, "[slow] lanczos %s %lld/%lld %.1f ms\n", what, (long long)a, (long long)b, dt);
+        t0 = t1;
+    }
+};
+
 struct LockedSet {
     int64_t c = 0;
     DevBuf<int64_t> comp;   // n: component id
@@ -1648,6 +1667,8 @@ int sc_eigensolve_csr(int64_t n, const int64_t* row_ptr, const int32_t* col, con
     const char* fenv = std::getenv("SPECLUST_SPMV_FORMAT");
     const bool use_sell = fenv ? std::strcmp(fenv, "sell") == 0 : n >= kSellMinRows;
     if (use_sell && (rc = sell.build(n, row_ptr, col, vals, st))) return rc;
+    SlowWatch sw;
+    sw.lap("init", 0, 0);
     while (s.state == 0) {
         if (use_sell)
             rc = sell.spmv(s.in_slot(), s.w.p, st);
@@ -1655,6 +1676,7 @@ int sc_eigensolve_csr(int64_t n, const int64_t* row_ptr, const int32_t* col, con
             rc = spmv_launch(n, nnz, row_ptr, col, vals, s.in_slot(), s.w.p, false, st);
         if (rc) return rc;
         rc = s.advance(false);
+        sw.lap("step", s.restarts, s.j);
         if (rc) {
             if (stats) sc_lanczos_get_stats(&s, stats);
             if (rc == SC_ERR_MAX_RESTARTS) {
@@ -1799,9 +1821,11 @@ int sc_eigensolve_csr_deflate(int64_t n, const int64_t* row_ptr, const int32_t* 
     DevBuf<double> rv;
     if ((rc = rv.alloc((size_t)n * kr))) return rc;
     s.vec_out = rv.p;
+    SlowWatch sw;
     while (s.state == 0) {
         if ((rc = spmv_launch(n, nnz, row_ptr, col, vals, s.in_slot(), s.w.p, false, st))) return rc;
         rc = s.advance(false);
+        sw.lap("step", s.restarts, s.j);
         if (rc) {
             if (stats) sc_lanczos_get_stats(&s, stats);
             if (rc == SC_ERR_MAX_RESTARTS) {
