@@ -31,6 +31,7 @@ object so the distributed logic runs on CPU under gloo.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -463,7 +464,60 @@ def knn_graph_sharded_full(ops, comm: Comm, x, knn: int, measure):
 
 # ---------------------------------------------------------------------------
 # row-sharded thick-restart Lanczos (eigen.py:86-302)
-def lanczos_sharded(ops, comm: Comm, a_local, n: int, bounds, cfg: LanczosConfig):
+def _deflate_min_n() -> int:
+    return int(os.environ.get("SPECLUST_DEFLATE_MIN_N", "32768"))
+
+
+class _LockedShards:
+    """The eigenvalue-1 eigenvectors of A = D^-1/2 W D^-1/2, one per
+    connected component (u_C = D^1/2 1_C / |D^1/2 1_C|, disjoint supports),
+    row-sharded like the operator: the sharded counterpart of
+    sc_eigensolve_csr_deflate.  Components by min-label propagation with
+    one pointer jump per pass over the local rows and an all-gather of the
+    labels; per-component sums by a stable sort of the local rows by
+    component (segment_reduce: fixed order) and one all-reduce of c values."""
+
+    def __init__(self, comm, a_local, bounds, d_local):
+        torch = comm.torch
+        self.comm, self.torch = comm, torch
+        r0, r1 = bounds[comm.rank], bounds[comm.rank + 1]
+        n = bounds[-1]
+        dev = d_local.device
+        rp = a_local.row_ptr.to(dev, torch.int64)
+        cols = a_local.col.to(dev, torch.int64)
+        rows = torch.repeat_interleave(torch.arange(r1 - r0, device=dev), torch.diff(rp))
+        lab = torch.arange(n, device=dev, dtype=torch.int64)
+        for _ in range(100000):
+            loc = lab[r0:r1].clone()
+            if cols.numel():
+                loc.scatter_reduce_(0, rows, lab[cols], reduce="amin")
+            new = comm.gather_rows(loc, bounds)
+            new = torch.minimum(new, new[new])  # one pointer jump
+            changed = torch.tensor([float((new != lab).any().item())], dtype=torch.float64, device=dev)
+            lab = new
+            if comm.sum_(changed)[0].item() == 0.0:
+                break
+        roots = lab == torch.arange(n, device=dev, dtype=torch.int64)
+        rank = torch.cumsum(roots.to(torch.int64), 0) - 1
+        self.c = int(roots.sum().item())
+        self.comp = rank[lab[r0:r1]]  # local rows -> component id (ordered by smallest node)
+        self.order = torch.sort(self.comp, stable=True).indices
+        self.lengths = torch.bincount(self.comp, minlength=self.c)
+        dsum = self.seg_sum(d_local)
+        self.u = torch.sqrt(d_local) / torch.sqrt(dsum[self.comp])
+
+    def seg_sum(self, v):
+        """sum of v over each component's rows on every rank (length c)"""
+        out = self.torch.segment_reduce(v[self.order], "sum", lengths=self.lengths)
+        return self.comm.sum_(out.contiguous())
+
+    def deflate(self, v):
+        h = self.seg_sum(self.u * v)
+        v -= h[self.comp] * self.u
+        return v
+
+
+def lanczos_sharded(ops, comm: Comm, a_local, n: int, bounds, cfg: LanczosConfig, d_local=None):
     """Top-k eigenpairs of the symmetric operator whose row block
     [bounds[rank], bounds[rank+1]) is ``a_local`` (global column indices).
 
@@ -471,15 +525,57 @@ def lanczos_sharded(ops, comm: Comm, a_local, n: int, bounds, cfg: LanczosConfig
     (k,), stats dict).  Raises MaxRestartsExceeded / Breakdown like eigen.py."""
     op = ops.operator(a_local) if hasattr(ops, "operator") else None
     try:
+        if d_local is not None and n >= _deflate_min_n() and cfg.k >= 2 and \
+                os.environ.get("SPECLUST_DEFLATE", "1") != "0":
+            return _lanczos_sharded_deflate(ops, comm, a_local, n, bounds, cfg, op, d_local)
         return _lanczos_sharded(ops, comm, a_local, n, bounds, cfg, op)
     finally:
         if op is not None:
             op.close()
 
 
-def _lanczos_sharded(ops, comm, a_local, n, bounds, cfg, op):
+def _lanczos_sharded_deflate(ops, comm, a_local, n, bounds, cfg, op, d_local):
+    """A = D^-1/2 W D^-1/2 with 2 <= c < k connected components: the c
+    eigenvalue-1 pairs locked (_LockedShards), the Lanczos recurrence for the
+    other k - c on their orthogonal complement (subspace m - c); else the
+    plain sharded solve.  stats["locked"] = c."""
+    torch = comm.torch
+    k = cfg.k
+    m = cfg.m if cfg.m is not None else default_subspace_dim(n, k)
+    lk = _LockedShards(comm, a_local, bounds, d_local)
+    c = lk.c
+    if not 2 <= c < k:
+        return _lanczos_sharded(ops, comm, a_local, n, bounds, cfg, op)
+
     def matvec(x_full):
         return op.apply(x_full) if op is not None else ops.spmv(a_local, x_full)
+
+    y = matvec(comm.gather_rows(lk.u.contiguous(), bounds))
+    theta_l = lk.seg_sum(lk.u * y)
+    res_l = torch.sqrt(lk.seg_sum((y - theta_l[lk.comp] * lk.u) ** 2))
+    th, rs = ops.host(theta_l), ops.host(res_l)
+    if not (np.all(np.abs(th - 1.0) <= 1e-10) and np.all(rs <= 1e-3 * float(cfg.tol))):
+        return _lanczos_sharded(ops, comm, a_local, n, bounds, cfg, op)
+    sub = LanczosConfig(k=k - c, m=m - c, tol=cfg.tol, max_restarts=cfg.max_restarts, seed=cfg.seed)
+    values, V, residuals, st = _lanczos_sharded(ops, comm, a_local, n, bounds, sub, op, deflate=lk.deflate)
+    ordr = np.argsort(-th, kind="stable")
+    col_of = np.empty(c, dtype=np.int64)
+    col_of[ordr] = np.arange(c)
+    nl = bounds[comm.rank + 1] - bounds[comm.rank]
+    out = ops.zeros((nl, k))
+    if nl:
+        cols = torch.as_tensor(col_of, device=lk.u.device)[lk.comp]
+        out[torch.arange(nl, device=lk.u.device), cols] = lk.u
+        out[:, c:] = V
+    st["locked"] = c
+    st["m"] = m
+    return (np.concatenate([th[ordr], values]), out, np.concatenate([rs[ordr], residuals]), st)
+
+
+def _lanczos_sharded(ops, comm, a_local, n, bounds, cfg, op, deflate=None):
+    def matvec(x_full):
+        w = op.apply(x_full) if op is not None else ops.spmv(a_local, x_full)
+        return deflate(w) if deflate is not None else w
 
     k = cfg.k
     m = cfg.m if cfg.m is not None else default_subspace_dim(n, k)
@@ -516,6 +612,8 @@ def _lanczos_sharded(ops, comm, a_local, n, bounds, cfg, op):
         for _ in range(3):
             rng_stream[0] += 1
             v = ops.normal(nl, r0, seed, rng_stream[0])
+            if deflate is not None:
+                deflate(deflate(v))
             nv = cgs2(v, count)
             if nv > 1e-6 * math.sqrt(n):
                 if is_breakdown:
@@ -525,6 +623,8 @@ def _lanczos_sharded(ops, comm, a_local, n, bounds, cfg, op):
         raise Breakdown(f"could not extend the basis past {count} vectors")
 
     v0 = ops.normal(nl, r0, seed, 0)
+    if deflate is not None:
+        deflate(deflate(v0))
     ops.div_into(B[0, :nl], v0, norm_of(v0))
     scale = 0.0
     pending = None
@@ -588,7 +688,8 @@ def _lanczos_sharded(ops, comm, a_local, n, bounds, cfg, op):
             one = ops.zeros((1,))
             for i in range(k):  # true residuals |A v - theta v| (eigen.py:241-248)
                 vi = V[:, i].contiguous()
-                yi = matvec(comm.gather_rows(vi, bounds))
+                xg = comm.gather_rows(vi, bounds)
+                yi = op.apply(xg) if op is not None else ops.spmv(a_local, xg)
                 one.fill_(values[i])
                 sq = ops.gemv_n(vi.reshape(1, -1), 1, one, yi, want_sq=True)
                 res[i] = float(comm.sum_(sq)[0].item())
@@ -817,8 +918,10 @@ def run_sharded(cfg, comm: Comm, ops=None):
         del a_p
     else:
         a_loc = ops.sym_scale_shard(w_loc, r0, d_full)
+    # degrees in the operator's row order (scan order on the locality path)
+    d_op = d_full[perm.to(d_full.device, torch.int64)][r0:r1] if locality else d_loc
     try:
-        values, U, residuals, est = lanczos_sharded(ops, comm, a_loc, n, bounds, ecfg)
+        values, U, residuals, est = lanczos_sharded(ops, comm, a_loc, n, bounds, ecfg, d_local=d_op.contiguous())
     except MaxRestartsExceeded as e:
         raise EigenNotConverged(e) from e
     if locality:

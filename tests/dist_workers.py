@@ -92,7 +92,51 @@ def matrix_gates_worker(rank, world):
     return dict(raised=np.array(raised))
 
 
-WORKERS = {"lanczos": lanczos_worker, "pipeline": pipeline_worker, "graph": graph_worker,
+def components_graph(nb=5, size=60, seed=9):
+    """Block-diagonal nonnegative symmetric W: nb connected components."""
+    rng = np.random.default_rng(seed)
+    n = nb * size
+    a = np.zeros((n, n))
+    for b in range(nb):
+        blk = rng.uniform(0.1, 1.0, (size, size)) * (rng.random((size, size)) < 0.3)
+        blk = np.triu(blk, 1)
+        blk = blk + blk.T
+        # a path keeps every block connected
+        for i in range(size - 1):
+            blk[i, i + 1] = blk[i + 1, i] = max(blk[i, i + 1], 0.5)
+        a[b * size:(b + 1) * size, b * size:(b + 1) * size] = blk
+    r, c = np.nonzero(a)
+    return a, sc.coo_to_csr(sc.coo_canonicalize(sc.CooMatrix(n, n, r, c, a[r, c])))
+
+
+def deflate_worker(rank, world):
+    """Row-sharded Lanczos on D^-1/2 W D^-1/2 of a 5-component graph with
+    the eigenvalue-1 eigenvectors locked (distributed._LockedShards) and
+    without (plain)."""
+    os.environ["SPECLUST_DEFLATE_MIN_N"] = "100"
+    _, m = components_graph()
+    ops = NumpyOps()
+    comm = Comm("cpu")
+    n = m.n_rows
+    bounds = row_bounds(n, comm.world)
+    r0, r1 = bounds[comm.rank], bounds[comm.rank + 1]
+    full = ops.from_host_csr(m)
+    w_loc = ops.slice_rows(full, r0, r1)
+    d_full = ops.degrees(full)
+    a_loc = ops.sym_scale_shard(w_loc, r0, d_full)
+    cfg = sc.LanczosConfig(k=8, seed=0)
+    out = {}
+    for tag, d in (("defl", d_full[r0:r1].contiguous()), ("plain", None)):
+        vals, V, res, st = lanczos_sharded(ops, comm, a_loc, n, bounds, cfg, d_local=d)
+        out[f"values_{tag}"] = vals
+        out[f"residuals_{tag}"] = res
+        out[f"vectors_{tag}"] = comm.gather_rows(V, bounds).numpy()
+        out[f"locked_{tag}"] = np.array(st.get("locked", 0))
+        out[f"restarts_{tag}"] = np.array(st["restarts"])
+    return out
+
+
+WORKERS = {"lanczos": lanczos_worker, "deflate": deflate_worker, "pipeline": pipeline_worker, "graph": graph_worker,
            "matrix_gates": matrix_gates_worker}
 
 
