@@ -17,6 +17,7 @@
 
 #include "sc_common.cuh"
 #include "sc_sparse.cuh"
+#include "sc_scan.cuh"
 
 namespace sc {
 
@@ -752,11 +753,16 @@ __global__ void __launch_bounds__(KPP_UPD_ROWS) kpp_update_panel_kernel(int64_t 
                                                                         int64_t* __restrict__ pc,
                                                                         const double* __restrict__ cc,
                                                                         int32_t* __restrict__ ctr, int t,
-                                                                        KppScreen scr) {
+                                                                        KppScreen scr,
+                                                                        const int32_t* __restrict__ reps,
+                                                                        int64_t nreps) {
     __shared__ double sw[KPP_UPD_ROWS / 32];
     __shared__ int64_t scn[KPP_UPD_ROWS / 32];
     extern __shared__ __align__(16) __half kpp_ch[];
-    const int64_t i = (int64_t)blockIdx.x * KPP_UPD_ROWS + threadIdx.x;
+    // reps: only the listed rows (one per group of identical rows), no
+    // partials (kpp_expand_kernel copies their d2 to the group and sums)
+    const int64_t ti = (int64_t)blockIdx.x * KPP_UPD_ROWS + threadIdx.x;
+    const int64_t i = reps ? (ti < nreps ? (int64_t)reps[ti] : n) : ti;
     const int64_t nch = (d + 7) / 8;
     if (scr.vh8) {
         for (int64_t l = threadIdx.x; l < nch * 8; l += blockDim.x) kpp_ch[l] = scr.ch[l];
@@ -842,7 +848,96 @@ __global__ void __launch_bounds__(KPP_UPD_ROWS) kpp_update_panel_kernel(int64_t 
             atomicAdd(&scr.stats[1], (unsigned long long)__popc(bp));
         }
     }
+    if (!reps) kpp_block_partials(w, cnt, sw, scn, pw, pc);
+}
+
+// rows with an identical earlier row (rep[i] < i): d2 and the nearest centre
+// are the representative's (identical arithmetic on identical bits); the
+// candidate partials over all rows in kpp_update_panel_kernel's block order
+__global__ void __launch_bounds__(KPP_UPD_ROWS) kpp_expand_kernel(int64_t n, const int32_t* __restrict__ rep,
+                                                                  int64_t pick, double* __restrict__ d2,
+                                                                  uint8_t* __restrict__ taken,
+                                                                  int32_t* __restrict__ ctr,
+                                                                  double* __restrict__ pw, int64_t* __restrict__ pc) {
+    __shared__ double sw[KPP_UPD_ROWS / 32];
+    __shared__ int64_t scn[KPP_UPD_ROWS / 32];
+    const int64_t i = (int64_t)blockIdx.x * KPP_UPD_ROWS + threadIdx.x;
+    double w = 0.0;
+    int64_t cnt = 0;
+    if (i < n) {
+        const int64_t r = rep[i];
+        double nv = d2[i];
+        if (r != i) {
+            nv = d2[r];
+            d2[i] = nv;
+            if (ctr) ctr[i] = ctr[r];
+        }
+        if (i == pick) taken[i] = 1;
+        const bool tk = (i == pick) || taken[i];
+        if (!tk && nv > 0.0) {
+            w = nv;
+            cnt = 1;
+        }
+    }
     kpp_block_partials(w, cnt, sw, scn, pw, pc);
+}
+
+// identical-row groups: 64-bit hash of each row's bit patterns
+__global__ void row_hash_kernel(int64_t n, int64_t d, const double* __restrict__ v, uint64_t* __restrict__ h) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint64_t x = 0x9E3779B97F4A7C15ull ^ (uint64_t)d;
+    for (int64_t l = 0; l < d; ++l) {
+        uint64_t b = (uint64_t)__double_as_longlong(v[i * d + l]);
+        b ^= b >> 33;
+        b *= 0xff51afd7ed558ccdull;
+        b ^= b >> 33;
+        x = (x ^ b) * 0x100000001b3ull + 0x632be59bd9b4e019ull;
+    }
+    x ^= x >> 31;
+    h[i] = x == ~0ull ? 0ull : x;  // ~0 marks an empty slot
+}
+// open addressing: slot key = hash, value = the smallest row index with it
+__global__ void hash_insert_kernel(int64_t n, const uint64_t* __restrict__ h, uint64_t mask,
+                                   unsigned long long* __restrict__ keys, unsigned long long* __restrict__ vals) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const unsigned long long key = h[i];
+    uint64_t s = key & mask;
+    while (true) {
+        const unsigned long long prev = atomicCAS(&keys[s], ~0ull, key);
+        if (prev == ~0ull || prev == key) {
+            atomicMin(&vals[s], (unsigned long long)i);
+            return;
+        }
+        s = (s + 1) & mask;
+    }
+}
+// rep[i] = the smallest index of a row with the same hash AND the same bits (else i)
+__global__ void hash_rep_kernel(int64_t n, int64_t d, const double* __restrict__ v, const uint64_t* __restrict__ h,
+                                uint64_t mask, const unsigned long long* __restrict__ keys,
+                                const unsigned long long* __restrict__ vals, int32_t* __restrict__ rep,
+                                int64_t* __restrict__ isrep) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const unsigned long long key = h[i];
+    uint64_t s = key & mask;
+    while (keys[s] != key) s = (s + 1) & mask;
+    int64_t r = (int64_t)vals[s];
+    if (r != i) {
+        for (int64_t l = 0; l < d; ++l)
+            if (__double_as_longlong(v[i * d + l]) != __double_as_longlong(v[r * d + l])) {
+                r = i;  // a hash collision: its own group
+                break;
+            }
+    }
+    rep[i] = (int32_t)r;
+    isrep[i] = r == i ? 1 : 0;
+}
+__global__ void compact_reps_kernel(int64_t n, const int64_t* __restrict__ isrep, const int64_t* __restrict__ pos,
+                                    int32_t* __restrict__ reps) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && isrep[i]) reps[pos[i]] = (int32_t)i;
 }
 
 
@@ -1840,6 +1935,10 @@ struct sc_kmeanspp {
     int ncent = 0;
     bool bound = false;
     // fp16 screen (KppScreen): points as fp16 panels, the centre in fp16
+    // groups of identical rows (rep[i]: smallest index with the same bits):
+    // the update computes one distance per group
+    DevBuf<int32_t> rep, reps;
+    int64_t nreps = 0;
     DevBuf<uint4> vh8;
     DevBuf<__half> ch;
     DevBuf<double> vnorm, cnorm;
@@ -1890,9 +1989,18 @@ struct sc_kmeanspp {
                 scr.stats = sstat.p;
                 smem = (size_t)ceil_div(d, 8) * 8 * sizeof(__half);
             }
-            kpp_update_panel_kernel<<<(unsigned)nb_upd, KPP_UPD_ROWS, smem, st>>>(
-                n, d, v8.p, row, pick_index, first ? 1 : 0, d2.p, taken.p, pw.p, pc.p, ccp, bound ? ctr.p : nullptr,
-                t, scr);
+            if (reps.p) {
+                kpp_update_panel_kernel<<<(unsigned)ceil_div(nreps, KPP_UPD_ROWS), KPP_UPD_ROWS, smem, st>>>(
+                    n, d, v8.p, row, -1, first ? 1 : 0, d2.p, taken.p, nullptr, nullptr, ccp,
+                    bound ? ctr.p : nullptr, t, scr, reps.p, nreps);
+                kpp_expand_kernel<<<(unsigned)nb_upd, KPP_UPD_ROWS, 0, st>>>(n, rep.p, pick_index, d2.p, taken.p,
+                                                                           bound ? ctr.p : nullptr, pw.p, pc.p);
+                SC_LAUNCHED(1);
+            } else {
+                kpp_update_panel_kernel<<<(unsigned)nb_upd, KPP_UPD_ROWS, smem, st>>>(
+                    n, d, v8.p, row, pick_index, first ? 1 : 0, d2.p, taken.p, pw.p, pc.p, ccp,
+                    bound ? ctr.p : nullptr, t, scr, nullptr, 0);
+            }
         } else {
             kpp_update_kernel<<<(unsigned)nb_upd, KPP_UPD_ROWS, 0, st>>>(n, d, v, row, pick_index, first ? 1 : 0, d2.p,
                                                                          taken.p, pw.p, pc.p);
@@ -2051,6 +2159,41 @@ int sc_kmeanspp_create(int64_t n, int64_t d, const double* v, sc_stream_t stream
     // 8-column panels of the points for the update (skipped when memory is short)
     const int64_t nch = ceil_div(d, 8);
     if (s->v8.alloc((size_t)nch * n * 8) == SC_OK) {
+        // identical rows (e.g. the constant rows of a graph component whose
+        // eigenvalue-1 eigenvector is locked): one distance per group;
+        // used when it saves at least a quarter of the rows
+        const char* denv = std::getenv("SPECLUST_KPP_DEDUP");
+        if (!(denv && denv[0] == '0') && n >= 4096 && d >= 8 && n < ((int64_t)1 << 31)) {
+            uint64_t tsz = 1;
+            while (tsz < (uint64_t)(2 * n)) tsz <<= 1;
+            DevBuf<uint64_t> hsh;
+            DevBuf<unsigned long long> keys, vals;
+            DevBuf<int64_t> isrep, pos, tmp;
+            if (hsh.alloc(n) == SC_OK && keys.alloc(tsz) == SC_OK && vals.alloc(tsz) == SC_OK &&
+                isrep.alloc(n) == SC_OK && pos.alloc(n + 1) == SC_OK && tmp.alloc(ceil_div(n, 1024) + 2) == SC_OK &&
+                s->rep.alloc(n) == SC_OK) {
+                cudaMemsetAsync(keys.p, 0xff, sizeof(unsigned long long) * tsz, s->st);
+                cudaMemsetAsync(vals.p, 0xff, sizeof(unsigned long long) * tsz, s->st);
+                const unsigned nbk = (unsigned)ceil_div(n, 256);
+                row_hash_kernel<<<nbk, 256, 0, s->st>>>(n, d, v, hsh.p);
+                hash_insert_kernel<<<nbk, 256, 0, s->st>>>(n, hsh.p, tsz - 1, keys.p, vals.p);
+                hash_rep_kernel<<<nbk, 256, 0, s->st>>>(n, d, v, hsh.p, tsz - 1, keys.p, vals.p, s->rep.p, isrep.p);
+                SC_LAUNCHED(3);
+                int64_t nr = n;
+                if (exclusive_scan_i64(n, isrep.p, pos.p, tmp.p, s->st) == SC_OK) {
+                    SC_CUDA(d2h_sync(&nr, pos.p + n, sizeof(int64_t), s->st));
+                    if (nr <= n - n / 4 && s->reps.alloc(std::max<int64_t>(nr, 1)) == SC_OK) {
+                        compact_reps_kernel<<<nbk, 256, 0, s->st>>>(n, isrep.p, pos.p, s->reps.p);
+                        SC_LAUNCHED(1);
+                        s->nreps = nr;
+                    }
+                }
+                if (std::getenv("SPECLUST_TIMING_DEBUG"))
+                    fprintf(stderr, "[kmeans++] identical-row groups: %lld of %lld rows (%s)\n", (long long)nr,
+                            (long long)n, s->reps.p ? "used" : "not used");
+            }
+            if (!s->reps.p) s->rep.free();
+        }
         to_panels_kernel<<<(unsigned)ceil_div(nch * n * 8, 256), 256, 0, s->st>>>(n, d, v, s->v8.p);
         SC_LAUNCHED(1);
         s->bound = s->cent.alloc((size_t)sc_kmeanspp::ccap * d) == SC_OK &&

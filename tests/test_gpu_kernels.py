@@ -743,27 +743,37 @@ def test_sbm_pipeline_and_binary_input(tmp_path):
 
 
 def test_kmeanspp_fp16_screen_exact(monkeypatch):
-    """k-means++ with the fp16 screen of the D^2 update (d >= 32) draws the
-    same rows as the CPU oracle's restatement of kmeans.py:107-136 (pinned to
-    the reference by tests/test_oracle_golden.py) and as the unscreened
-    update: the screen only skips rows whose certified lower bound exceeds
-    their current D^2.  Unit-norm embeddings, raw large-magnitude data and
-    exact duplicates (zero distances, ties)."""
+    """k-means++ with the fp16 screen of the D^2 update (d >= 32) and the
+    identical-row groups (one distance per group) draws the same rows as the
+    CPU oracle's restatement of kmeans.py:107-136 (pinned to the reference by
+    tests/test_oracle_golden.py) and as the unscreened update: the screen
+    only skips rows whose certified lower bound exceeds their current D^2.
+    Unit-norm embeddings, raw large-magnitude data, exact duplicates (zero
+    distances, ties) and mostly-one-hot rows (the embedding rows of locked
+    graph components)."""
     rng = np.random.default_rng(31)
-    for n, d, k, kind in [(20_000, 100, 100, "unit"), (6_000, 300, 40, "raw"), (5_000, 64, 30, "dup")]:
+    for n, d, k, kind in [(20_000, 100, 100, "unit"), (6_000, 300, 40, "raw"), (5_000, 64, 30, "dup"),
+                          (30_000, 64, 80, "onehot")]:
         centers = rng.normal(0.0, 1.0, (k, d))
         v = centers[rng.integers(0, k, n)] + 0.2 * rng.standard_normal((n, d))
         if kind == "unit":
             v /= np.linalg.norm(v, axis=1, keepdims=True)
         elif kind == "raw":
             v *= 3e4
-        else:
+        elif kind == "dup":
             v[n // 2:] = v[: n - n // 2]
+        else:  # rows of locked components: 60 distinct one-hot rows for 80 % of the points
+            hot = np.eye(d)[rng.integers(0, 60, n)]
+            v /= np.linalg.norm(v, axis=1, keepdims=True)
+            keep = rng.random(n) < 0.8
+            v[keep] = hot[keep]
         v = np.ascontiguousarray(v)
         want = orc.kmeanspp_indices(v, k, 7)
         init = sc.kmeanspp_init(v, k, 7)
         assert np.array_equal(init, v[want]), (n, d, kind)
         monkeypatch.setenv("SPECLUST_KPP_SCREEN", "0")
+        monkeypatch.setenv("SPECLUST_KPP_DEDUP", "0")
         plain = sc.kmeanspp_init(v, k, 7)
         monkeypatch.delenv("SPECLUST_KPP_SCREEN")
+        monkeypatch.delenv("SPECLUST_KPP_DEDUP")
         assert np.array_equal(plain, init)
