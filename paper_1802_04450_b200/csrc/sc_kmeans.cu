@@ -758,16 +758,19 @@ __global__ void __launch_bounds__(KPP_UPD_ROWS) kpp_update_panel_kernel(int64_t 
                                                                         int64_t nreps) {
     __shared__ double sw[KPP_UPD_ROWS / 32];
     __shared__ int64_t scn[KPP_UPD_ROWS / 32];
-    extern __shared__ __align__(16) __half kpp_ch[];
+    // dynamic shared memory: the new centre's row (nch * 8 doubles), then
+    // (screen) its fp16 copy
+    extern __shared__ __align__(16) double kpp_row[];
     // reps: only the listed rows (one per group of identical rows), no
     // partials (kpp_expand_kernel copies their d2 to the group and sums)
     const int64_t ti = (int64_t)blockIdx.x * KPP_UPD_ROWS + threadIdx.x;
     const int64_t i = reps ? (ti < nreps ? (int64_t)reps[ti] : n) : ti;
     const int64_t nch = (d + 7) / 8;
-    if (scr.vh8) {
+    __half* kpp_ch = reinterpret_cast<__half*>(kpp_row + nch * 8);
+    for (int64_t l = threadIdx.x; l < nch * 8; l += blockDim.x) kpp_row[l] = l < d ? prow[l] : 0.0;
+    if (scr.vh8)
         for (int64_t l = threadIdx.x; l < nch * 8; l += blockDim.x) kpp_ch[l] = scr.ch[l];
-        __syncthreads();
-    }
+    __syncthreads();
     NpDot acc;
     bool pruned = false, screened = false, screen_pruned = false;
     double old = 0.0;
@@ -802,18 +805,41 @@ __global__ void __launch_bounds__(KPP_UPD_ROWS) kpp_update_panel_kernel(int64_t 
             if (lb > 0.0 && lb * lb > old * scr.s * scr.s * (1.0 + 1e-9)) pruned = true;
             screen_pruned = pruned;
         }
-        for (int64_t c0 = 0; c0 < d && !pruned; c0 += 8) {
-            const double2* src = reinterpret_cast<const double2*>(v8 + ((c0 >> 3) * n + i) * 8);
-            const double2 a0 = __ldg(src), a1 = __ldg(src + 1), a2 = __ldg(src + 2), a3 = __ldg(src + 3);
-            const double x[8] = {a0.x, a0.y, a1.x, a1.y, a2.x, a2.y, a3.x, a3.y};
-            auto f = [&](int q) {
-                const double t = __dsub_rn(x[q], __ldg(prow + c0 + q));
+        // full panels two at a time (both panels' loads in flight before the
+        // arithmetic; the early exit is tested per pair), then the tail panel
+        const int64_t dfull = d / 8 * 8;
+        int64_t c0 = 0;
+        auto panel = [&](int64_t cc, const double2 a0, const double2 a1, const double2 a2, const double2 a3) {
+            const double2* cr = reinterpret_cast<const double2*>(kpp_row + cc);
+            const double2 b0 = cr[0], b1 = cr[1], b2 = cr[2], b3 = cr[3];
+            auto sq = [](double u, double w) {
+                const double t = __dsub_rn(u, w);
                 return __dmul_rn(t, t);
             };
+            acc.block(sq(a0.x, b0.x), sq(a0.y, b0.y), sq(a1.x, b1.x), sq(a1.y, b1.y), sq(a2.x, b2.x),
+                      sq(a2.y, b2.y), sq(a3.x, b3.x), sq(a3.y, b3.y));
+        };
+        for (; c0 + 16 <= dfull && !pruned; c0 += 16) {
+            const double2* s0 = reinterpret_cast<const double2*>(v8 + ((c0 >> 3) * n + i) * 8);
+            const double2* s1 = reinterpret_cast<const double2*>(v8 + (((c0 >> 3) + 1) * n + i) * 8);
+            const double2 a0 = __ldg(s0), a1 = __ldg(s0 + 1), a2 = __ldg(s0 + 2), a3 = __ldg(s0 + 3);
+            const double2 e0 = __ldg(s1), e1 = __ldg(s1 + 1), e2 = __ldg(s1 + 2), e3 = __ldg(s1 + 3);
+            panel(c0, a0, a1, a2, a3);
+            panel(c0 + 8, e0, e1, e2, e3);
+            if (!first && c0 + 16 < d && acc.result() >= old) pruned = true;
+        }
+        for (; c0 < d && !pruned; c0 += 8) {
+            const double2* src = reinterpret_cast<const double2*>(v8 + ((c0 >> 3) * n + i) * 8);
+            const double2 a0 = __ldg(src), a1 = __ldg(src + 1), a2 = __ldg(src + 2), a3 = __ldg(src + 3);
             const int rem = (int)(d - c0 < 8 ? d - c0 : 8);
             if (rem == 8) {
-                acc.block(f(0), f(1), f(2), f(3), f(4), f(5), f(6), f(7));
+                panel(c0, a0, a1, a2, a3);
             } else {  // the tail: pairs, then a single (np_dot_span)
+                const double x[8] = {a0.x, a0.y, a1.x, a1.y, a2.x, a2.y, a3.x, a3.y};
+                auto f = [&](int q) {
+                    const double t = __dsub_rn(x[q], kpp_row[c0 + q]);
+                    return __dmul_rn(t, t);
+                };
 #pragma unroll
                 for (int q = 0; q < 8; q += 2)
                     if (q + 2 <= rem) acc.pair(f(q), f(q + 1));
@@ -1977,7 +2003,8 @@ struct sc_kmeanspp {
                 bound = false;  // past ccap centres: plain updates from here on
             }
             KppScreen scr;
-            size_t smem = 0;
+            size_t smem = (size_t)ceil_div(d, 8) * 8 * sizeof(double);
+            static size_t smem_attr = 48 * 1024;
             if (screen && !first) {
                 kpp_centre_half_kernel<<<1, 256, 0, st>>>(d, row, hs, ch.p, cnorm.p);
                 SC_LAUNCHED(1);
@@ -1987,7 +2014,12 @@ struct sc_kmeanspp {
                 scr.cnorm = cnorm.p;
                 scr.s = hs;
                 scr.stats = sstat.p;
-                smem = (size_t)ceil_div(d, 8) * 8 * sizeof(__half);
+                smem += (size_t)ceil_div(d, 8) * 8 * sizeof(__half);
+            }
+            if (smem > smem_attr) {
+                SC_CUDA(cudaFuncSetAttribute(kpp_update_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem));
+                smem_attr = smem;
             }
             if (reps.p) {
                 kpp_update_panel_kernel<<<(unsigned)ceil_div(nreps, KPP_UPD_ROWS), KPP_UPD_ROWS, smem, st>>>(
@@ -2158,7 +2190,8 @@ int sc_kmeanspp_create(int64_t n, int64_t d, const double* v, sc_stream_t stream
     cudaMemsetAsync(s->taken.p, 0, n, s->st);
     // 8-column panels of the points for the update (skipped when memory is short)
     const int64_t nch = ceil_div(d, 8);
-    if (s->v8.alloc((size_t)nch * n * 8) == SC_OK) {
+    // (the panel update stages the centre row in shared memory: d <= 24576)
+    if (d <= 24576 && s->v8.alloc((size_t)nch * n * 8) == SC_OK) {
         // identical rows (e.g. the constant rows of a graph component whose
         // eigenvalue-1 eigenvector is locked): one distance per group;
         // used when it saves at least a quarter of the rows
