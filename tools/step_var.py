@@ -22,10 +22,11 @@ xd = torch.from_numpy(x).cuda()
 cfg = sc.PipelineConfig(
     input=sc.PointsInput(measure=sc.SimilarityMeasure.exp_decay(float(np.sqrt(d))), pattern="knn", points=xd, knn=knn),
     k_clusters=k, eigen=sc.LanczosConfig(k=k, seed=0), kmeans=sc.KmeansConfig(k=k, seed=0), normalize_rows=True)
-if os.environ.get("STEPVAR_MLOCK"):
-    import ctypes
-    rc = ctypes.CDLL("libc.so.6", use_errno=True).mlockall(3)  # MCL_CURRENT | MCL_FUTURE
-    print("mlockall", rc, ctypes.get_errno(), file=sys.stderr)
+if os.environ.get("STEPVAR_THREADS"):
+    from threadpoolctl import threadpool_limits
+    _tl = threadpool_limits(int(os.environ["STEPVAR_THREADS"]))
+    torch.set_num_threads(int(os.environ["STEPVAR_THREADS"]))
+    print("threads limited", file=sys.stderr)
 sched = os.environ.get("STEPVAR_SCHED")
 if sched:
     from cuda.bindings import runtime as rt
