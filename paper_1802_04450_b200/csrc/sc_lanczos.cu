@@ -926,14 +926,19 @@ __global__ void cc_number_kernel(int64_t n, const int32_t* __restrict__ lab, con
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) comp[i] = rank[lab[i]];
 }
-// per component, in member order (block per component, fixed tree): out[C] =
-// sum over members i of a[i] * (b ? b[i] : 1)
-__global__ void seg_dot_kernel(const int64_t* __restrict__ start, const int32_t* __restrict__ members,
-                               const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ out) {
+// per component C: sum over its members (member order) of a[i] * (b ? b[i] :
+// 1), in two fixed-order passes over chunks of at most SEG_CH members (one
+// block per component would leave C3's 164K-node component to one block's
+// serial loop every Lanczos step): chunk partials, then each component's
+// chunks in order
+constexpr int64_t SEG_CH = 4096;
+__global__ void seg_dot_chunks_kernel(const int64_t* __restrict__ cbeg, const int64_t* __restrict__ cend,
+                                      const int32_t* __restrict__ members, const double* __restrict__ a,
+                                      const double* __restrict__ b, double* __restrict__ part) {
     __shared__ double red[256];
-    const int64_t c = blockIdx.x;
+    const int64_t q = blockIdx.x;
     double acc = 0.0;
-    for (int64_t t = start[c] + threadIdx.x; t < start[c + 1]; t += blockDim.x) {
+    for (int64_t t = cbeg[q] + threadIdx.x; t < cend[q]; t += blockDim.x) {
         const int64_t i = members[t];
         acc = fma(a[i], b ? b[i] : 1.0, acc);
     }
@@ -943,8 +948,17 @@ __global__ void seg_dot_kernel(const int64_t* __restrict__ start, const int32_t*
         if ((int)threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
         __syncthreads();
     }
-    if (threadIdx.x == 0) out[c] = red[0];
+    if (threadIdx.x == 0) part[q] = red[0];
 }
+__global__ void seg_dot_combine_kernel(int64_t c, const int64_t* __restrict__ qoff, const double* __restrict__ part,
+                                       double* __restrict__ out) {
+    const int64_t C = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (C >= c) return;
+    double t = 0.0;
+    for (int64_t q = qoff[C]; q < qoff[C + 1]; ++q) t += part[q];
+    out[C] = t;
+}
+
 // u[i] = sqrt(d[i]) / sqrt(dsum[comp[i]])
 __global__ void locked_vec_kernel(int64_t n, const double* __restrict__ d, const int64_t* __restrict__ comp,
                                   const double* __restrict__ dsum, double* __restrict__ u) {
@@ -1010,14 +1024,49 @@ struct SlowWatch {
 };
 
 struct LockedSet {
-    int64_t c = 0;
+    int64_t c = 0, nq = 0;
     DevBuf<int64_t> comp;   // n: component id
     DevBuf<double> u, h;    // n: the locked vectors (disjoint supports); c: projections
     Bucketer bk;            // members grouped by component
-    int deflate(int64_t n, double* x, cudaStream_t st) {
-        seg_dot_kernel<<<(unsigned)c, 256, 0, st>>>(bk.start.p, bk.members.p, u.p, x, h.p);
-        deflate_sub_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, comp.p, u.p, h.p, x);
+    DevBuf<int64_t> cbeg, cend, qoff;  // member chunks (<= SEG_CH) and each component's first chunk
+    DevBuf<double> part;
+    // chunk table from the component sizes (bk.start, after bk.run)
+    int plan(cudaStream_t st) {
+        std::vector<int64_t> hs(c + 1);
+        SC_CUDA(d2h_sync(hs.data(), bk.start.p, sizeof(int64_t) * (c + 1), st));
+        std::vector<int64_t> hb, he, hq(c + 1, 0);
+        for (int64_t C = 0; C < c; ++C) {
+            for (int64_t t = hs[C]; t < hs[C + 1]; t += SEG_CH) {
+                hb.push_back(t);
+                he.push_back(std::min(hs[C + 1], t + SEG_CH));
+            }
+            if (hs[C + 1] == hs[C]) {  // (no empty component exists; keep the table total)
+                hb.push_back(hs[C]);
+                he.push_back(hs[C]);
+            }
+            hq[C + 1] = (int64_t)hb.size();
+        }
+        nq = (int64_t)hb.size();
+        int rc;
+        if ((rc = cbeg.alloc(nq)) || (rc = cend.alloc(nq)) || (rc = qoff.alloc(c + 1)) || (rc = part.alloc(nq)))
+            return rc;
+        SC_CUDA(cudaMemcpyAsync(cbeg.p, hb.data(), sizeof(int64_t) * nq, cudaMemcpyHostToDevice, st));
+        SC_CUDA(cudaMemcpyAsync(cend.p, he.data(), sizeof(int64_t) * nq, cudaMemcpyHostToDevice, st));
+        SC_CUDA(cudaMemcpyAsync(qoff.p, hq.data(), sizeof(int64_t) * (c + 1), cudaMemcpyHostToDevice, st));
+        SC_CUDA(cudaStreamSynchronize(st));
+        return SC_OK;
+    }
+    // out[C] = sum over component C's members of a[i] * (b ? b[i] : 1), fixed order
+    int seg_dot(const double* a, const double* b, double* out, cudaStream_t st) {
+        seg_dot_chunks_kernel<<<(unsigned)nq, 256, 0, st>>>(cbeg.p, cend.p, bk.members.p, a, b, part.p);
+        seg_dot_combine_kernel<<<(unsigned)ceil_div(c, 256), 256, 0, st>>>(c, qoff.p, part.p, out);
         SC_LAUNCHED(2);
+        return SC_OK;
+    }
+    int deflate(int64_t n, double* x, cudaStream_t st) {
+        if (int rc = seg_dot(u.p, x, h.p, st)) return rc;
+        deflate_sub_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, comp.p, u.p, h.p, x);
+        SC_LAUNCHED(1);
         return SC_OK;
     }
 };
@@ -1788,24 +1837,25 @@ int sc_eigensolve_csr_deflate(int64_t n, const int64_t* row_ptr, const int32_t* 
         SC_LAUNCHED(1);
     }
     lk.c = c;
-    if ((rc = lk.u.alloc(n)) || (rc = lk.h.alloc(c)) || (rc = lk.bk.init(n, c)) || (rc = lk.bk.run(lk.comp.p, st)))
+    if ((rc = lk.u.alloc(n)) || (rc = lk.h.alloc(c)) || (rc = lk.bk.init(n, c)) || (rc = lk.bk.run(lk.comp.p, st)) ||
+        (rc = lk.plan(st)))
         return rc;
     DevBuf<double> dsum, y, r, theta_l, res_l;
     if ((rc = dsum.alloc(c)) || (rc = y.alloc(n)) || (rc = r.alloc(n)) || (rc = theta_l.alloc(c)) ||
         (rc = res_l.alloc(c)))
         return rc;
-    seg_dot_kernel<<<(unsigned)c, 256, 0, st>>>(lk.bk.start.p, lk.bk.members.p, d, nullptr, dsum.p);
+    if ((rc = lk.seg_dot(d, nullptr, dsum.p, st))) return rc;
     locked_vec_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, d, lk.comp.p, dsum.p, lk.u.p);
-    SC_LAUNCHED(2);
+    SC_LAUNCHED(1);
     int64_t nnz = 0;
     SC_CUDA(d2h_sync(&nnz, row_ptr + n, sizeof(int64_t), st));
     // Rayleigh quotients and true residuals of the locked vectors; the
     // operator must be D^-1/2 W D^-1/2 for this d (else: the plain solve)
     if ((rc = spmv_launch(n, nnz, row_ptr, col, vals, lk.u.p, y.p, false, st))) return rc;
-    seg_dot_kernel<<<(unsigned)c, 256, 0, st>>>(lk.bk.start.p, lk.bk.members.p, lk.u.p, y.p, theta_l.p);
+    if ((rc = lk.seg_dot(lk.u.p, y.p, theta_l.p, st))) return rc;
     locked_resid_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, lk.comp.p, lk.u.p, y.p, theta_l.p, r.p);
-    seg_dot_kernel<<<(unsigned)c, 256, 0, st>>>(lk.bk.start.p, lk.bk.members.p, r.p, nullptr, res_l.p);
-    SC_LAUNCHED(3);
+    if ((rc = lk.seg_dot(r.p, nullptr, res_l.p, st))) return rc;
+    SC_LAUNCHED(1);
     std::vector<double> th(c), rs(c);
     SC_CUDA(d2h_sync(th.data(), theta_l.p, sizeof(double) * c, st));
     SC_CUDA(d2h_sync(rs.data(), res_l.p, sizeof(double) * c, st));
