@@ -1373,7 +1373,21 @@ struct sc_lanczos {
     int flush(int64_t c0, int64_t c1) { return flush_range(0, c0, c0, c1, win, kMaxWindow); }
     // columns [c0, c1] -= B[:, ob:oe] (B[:, ob:oe]^T B[:, c0..c1]); the
     // measured loss adapts `wv` (capped at wmax)
+    double flush_ms[2] = {0.0, 0.0};  // SPECLUST_TIMING_DEBUG: flushes against the Ritz block / the sweep
+    int64_t flush_n[2] = {0, 0};
     int flush_range(int64_t ob, int64_t oe, int64_t c0, int64_t c1, int64_t& wv, int64_t wmax) {
+        static const bool fdbg = std::getenv("SPECLUST_TIMING_DEBUG") != nullptr;
+        if (!fdbg) return flush_range_(ob, oe, c0, c1, wv, wmax);
+        cudaStreamSynchronize(st);
+        const auto t0 = std::chrono::steady_clock::now();
+        const int rc = flush_range_(ob, oe, c0, c1, wv, wmax);
+        cudaStreamSynchronize(st);
+        const int kind = ob == 0 ? 0 : 1;
+        flush_ms[kind] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        ++flush_n[kind];
+        return rc;
+    }
+    int flush_range_(int64_t ob, int64_t oe, int64_t c0, int64_t c1, int64_t& wv, int64_t wmax) {
         const int64_t nb = oe - ob;
         if (nb <= 0 || c1 < c0) return SC_OK;
         const int c = (int)(c1 - c0 + 1);
@@ -1461,9 +1475,12 @@ struct sc_lanczos {
         if (tdbg) {
             cudaStreamSynchronize(st);
             const auto t1 = std::chrono::steady_clock::now();
-            fprintf(stderr, "[lanczos] sweep %lld: %.3f ms, matvecs %lld, flushes %lld\n", (long long)restarts,
-                    std::chrono::duration<double, std::milli>(t1 - sweep_t0).count(), (long long)matvecs,
-                    (long long)flushes);
+            fprintf(stderr, "[lanczos] sweep %lld: %.3f ms, matvecs %lld, flushes %lld (from-0 %lld: %.1f ms, sweep %lld: %.1f ms)\n",
+                    (long long)restarts, std::chrono::duration<double, std::milli>(t1 - sweep_t0).count(),
+                    (long long)matvecs, (long long)flushes, (long long)flush_n[0], flush_ms[0],
+                    (long long)flush_n[1], flush_ms[1]);
+            flush_ms[0] = flush_ms[1] = 0.0;
+            flush_n[0] = flush_n[1] = 0;
             sweep_t0 = t1;
         }
         // T is diag(theta) + arrow at row k after a restart, tridiagonal
