@@ -125,19 +125,28 @@ __global__ void __launch_bounds__(256) block_tn_kernel(int64_t n, int64_t ld, in
 }
 
 // H[col][o] = sum_g part[g][col][o] (fixed order); *maxabs = max |H| (ordered bits)
+// H[col][o] = sum over the nsplit row groups of part[g][col][o]: one warp per
+// output element, lanes strided over the groups (4 loads in flight each),
+// then the warp's xor tree -- a fixed order.  (One thread per element looping
+// over all groups was a serial chain of L2 loads: 73 us per flush at C2.)
 __global__ void block_reduce_kernel(int nsplit, int nb, int c, int ldp, const double* __restrict__ part,
                                     double* __restrict__ H, unsigned long long* __restrict__ maxabs) {
-    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    double v = 0.0;
-    if (e < (int64_t)nb * c) {
-        const int col = (int)(e / c), o = (int)(e % c);
-        for (int g = 0; g < nsplit; ++g) v += part[((int64_t)g * nb + col) * ldp + o];
+    const int64_t e = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (e >= (int64_t)nb * c) return;
+    const int col = (int)(e / c), o = (int)(e % c);
+    const double* src = part + (int64_t)col * ldp + o;
+    const int64_t gstride = (int64_t)nb * ldp;
+    double t[4] = {0.0, 0.0, 0.0, 0.0};
+    int g = lane;
+    for (; g + 96 < nsplit; g += 128)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) t[u] += src[(int64_t)(g + 32 * u) * gstride];
+    for (; g < nsplit; g += 32) t[0] += src[(int64_t)g * gstride];
+    const double v = warp_sum((t[0] + t[1]) + (t[2] + t[3]));
+    if (lane == 0) {
         H[(int64_t)col * c + o] = v;
-    }
-    if (maxabs) {
-        double a = fabs(v);
-        for (int s = 16; s > 0; s >>= 1) a = fmax(a, __shfl_xor_sync(0xffffffffu, a, s));
-        if ((threadIdx.x & 31) == 0) atomicMax(maxabs, (unsigned long long)__double_as_longlong(a));
+        if (maxabs) atomicMax(maxabs, (unsigned long long)__double_as_longlong(fabs(v)));
     }
 }
 
@@ -296,7 +305,7 @@ int block_tn(int64_t n, int64_t ld, int nb, const double* B, const double* V, in
     int gs = 0;
     tn_dispatch(nt, n, ld, nb, B, V, c, &gs, part, st, false);
     const int64_t tot = (int64_t)nb * c;
-    block_reduce_kernel<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(gs, nb, c, nt * 8, part, H, maxabs);
+    block_reduce_kernel<<<(unsigned)ceil_div(tot, 8), 256, 0, st>>>(gs, nb, c, nt * 8, part, H, maxabs);
     SC_LAUNCHED(2);
     return SC_OK;
 }

@@ -244,16 +244,31 @@ __global__ void __launch_bounds__(256) window_cgs2_kernel(int64_t n, int64_t ld,
     cooperative_groups::grid_group grid = cooperative_groups::this_grid();
     constexpr int WCG_U = NC <= 8 ? 4 : (NC <= 16 ? 2 : 1);  // rows per thread per load group (registers)
     __shared__ double red[8][NC + 1];
-    __shared__ double hs[NC];
+    __shared__ double hs[NC + 1];
     const int nb = gridDim.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t per = ceil_div_dev(n, nb);
     const int64_t r0 = (int64_t)blockIdx.x * per, r1 = r0 + per < n ? r0 + per : n;
-    const int stride = WCG_MAX + 1;  // part[b * stride + c], c == cnt: |w|^2
-    auto gather_h = [&](int ncol) {
-        for (int c = threadIdx.x; c < ncol; c += blockDim.x) {
-            double t = 0.0;
-            for (int b = 0; b < nb; ++b) t += part[(int64_t)b * stride + c];
-            hs[c] = t;
+    const int stride = WCG_MAX + 1;  // part[b * stride + c], c == WCG_MAX: |w|^2
+    // sum of column `col` over the blocks' partials, fixed order: lane-strided
+    // partial sums (4 loads in flight per lane), then the warp's xor tree.
+    // (One thread per column looping over all blocks was a serial chain of
+    // ~300 L2 loads after every grid barrier: ~half of the kernel's time.)
+    auto col_sum = [&](int col) {
+        double t[4] = {0.0, 0.0, 0.0, 0.0};
+        int b = lane;
+        for (; b + 96 < nb; b += 128)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) t[u] += __ldcg(part + (int64_t)(b + 32 * u) * stride + col);
+        for (; b < nb; b += 32) t[0] += __ldcg(part + (int64_t)b * stride + col);
+        return warp_sum((t[0] + t[1]) + (t[2] + t[3]));
+    };
+    // hs[c] = column sums c < ncol (and hs[NC] = the |w|^2 column): warp q
+    // takes columns q, q + 8, ...
+    auto gather_h = [&](int ncol, bool with_w) {
+        const int tot = ncol + (with_w ? 1 : 0);
+        for (int q = warp; q < tot; q += 8) {
+            const double v = col_sum(q < ncol ? q : WCG_MAX);
+            if (lane == 0) hs[q < ncol ? q : NC] = v;
         }
         __syncthreads();
     };
@@ -297,9 +312,8 @@ __global__ void __launch_bounds__(256) window_cgs2_kernel(int64_t n, int64_t ld,
         part[(int64_t)blockIdx.x * stride + WCG_MAX] = t;
     }
     grid.sync();
-    gather_h(cnt);
-    double w0sq = 0.0;
-    for (int b = 0; b < nb; ++b) w0sq += part[(int64_t)b * stride + WCG_MAX];
+    gather_h(cnt, true);
+    const double w0sq = hs[NC];
     const double alpha = hs[cnt - 1];
     // update 1 fused with the projections of the updated w (pass 2)
 #pragma unroll
@@ -338,7 +352,7 @@ __global__ void __launch_bounds__(256) window_cgs2_kernel(int64_t n, int64_t ld,
     grid.sync();  // every block has read hs-dependent part[] before it is overwritten
     WCG_BLOCK_REDUCE_STORE(acc, cnt);
     grid.sync();
-    gather_h(cnt);
+    gather_h(cnt, false);
     // update 2 and |w|^2
     double sq = 0.0;
     r = r0 + threadIdx.x;
@@ -380,13 +394,14 @@ __global__ void __launch_bounds__(256) window_cgs2_kernel(int64_t n, int64_t ld,
         }
     }
     grid.sync();
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        double t = 0.0;
-        for (int b = 0; b < nb; ++b) t += part[(int64_t)b * stride + WCG_MAX];
-        scal[0] = sqrt(t);
-        scal[2] = alpha;
-        scal[3] = sqrt(w0sq);
-        T[j * m + j] = alpha;
+    if (blockIdx.x == 0 && warp == 0) {
+        const double t = col_sum(WCG_MAX);
+        if (lane == 0) {
+            scal[0] = sqrt(t);
+            scal[2] = alpha;
+            scal[3] = sqrt(w0sq);
+            T[j * m + j] = alpha;
+        }
     }
 }
 
