@@ -568,6 +568,38 @@ __global__ void to_panels_kernel(int64_t n, int64_t d, const double* __restrict_
     v8[e] = c < d ? v[i * d + c] : 0.0;
 }
 
+// nonzero-panel bitmap: bit p % 32 of word w = p / 32 of row i (at w * n + i)
+// is set when panel p of the row has a nonzero element; counts the zero
+// panels.  The k-means++ update skips loading zero panels (their elements
+// enter its numpy-order sums as exact zeros), which on an embedding with
+// locked component eigenvectors (C3: one nonzero among 850 columns) cuts the
+// bytes per row ~6x with bit-identical distances.
+__global__ void panel_nonzero_kernel(int64_t n, int64_t nch, const double* __restrict__ v8,
+                                     uint32_t* __restrict__ nzm, unsigned long long* __restrict__ nzero) {
+    const int64_t nw = (nch + 31) / 32;
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long zeros = 0;
+    if (e < nw * n) {
+        const int64_t w = e / n, i = e - w * n;
+        uint32_t bits = 0;
+        for (int b = 0; b < 32; ++b) {
+            const int64_t p = w * 32 + b;
+            if (p >= nch) break;
+            const double2* src = reinterpret_cast<const double2*>(v8 + (p * n + i) * 8);
+            bool nz = false;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const double2 a = src[q];
+                nz |= a.x != 0.0 || a.y != 0.0;
+            }
+            if (nz) bits |= 1u << b; else ++zeros;
+        }
+        nzm[e] = bits;
+    }
+    for (int o = 16; o > 0; o >>= 1) zeros += __shfl_xor_sync(0xffffffffu, zeros, o);
+    if ((threadIdx.x & 31) == 0 && zeros) atomicAdd(nzero, zeros);
+}
+
 // fp16 copy of s * v in 8-column panels (panel p of row i at p * n + i)
 __global__ void to_half_panels_kernel(int64_t n, int64_t d, const double* __restrict__ v, double s,
                                       uint4* __restrict__ vh8) {
@@ -755,7 +787,8 @@ __global__ void __launch_bounds__(KPP_UPD_ROWS) kpp_update_panel_kernel(int64_t 
                                                                         int32_t* __restrict__ ctr, int t,
                                                                         KppScreen scr,
                                                                         const int32_t* __restrict__ reps,
-                                                                        int64_t nreps) {
+                                                                        int64_t nreps,
+                                                                        const uint32_t* __restrict__ nzm) {
     __shared__ double sw[KPP_UPD_ROWS / 32];
     __shared__ int64_t scn[KPP_UPD_ROWS / 32];
     // dynamic shared memory: the new centre's row (nch * 8 doubles), then
@@ -819,18 +852,35 @@ __global__ void __launch_bounds__(KPP_UPD_ROWS) kpp_update_panel_kernel(int64_t 
             acc.block(sq(a0.x, b0.x), sq(a0.y, b0.y), sq(a1.x, b1.x), sq(a1.y, b1.y), sq(a2.x, b2.x),
                       sq(a2.y, b2.y), sq(a3.x, b3.x), sq(a3.y, b3.y));
         };
+        // zero panels (nzm) are not loaded: their elements are exact zeros
+        uint32_t nzw = 0xffffffffu;
+        int64_t nzw_at = -1;
+        auto panel_nz = [&](int64_t p) {
+            if (!nzm) return true;
+            if ((p >> 5) != nzw_at) {
+                nzw_at = p >> 5;
+                nzw = __ldg(nzm + nzw_at * n + i);
+            }
+            return ((nzw >> (p & 31)) & 1u) != 0;
+        };
+        const double2 z2 = make_double2(0.0, 0.0);
         for (; c0 + 16 <= dfull && !pruned; c0 += 16) {
             const double2* s0 = reinterpret_cast<const double2*>(v8 + ((c0 >> 3) * n + i) * 8);
             const double2* s1 = reinterpret_cast<const double2*>(v8 + (((c0 >> 3) + 1) * n + i) * 8);
-            const double2 a0 = __ldg(s0), a1 = __ldg(s0 + 1), a2 = __ldg(s0 + 2), a3 = __ldg(s0 + 3);
-            const double2 e0 = __ldg(s1), e1 = __ldg(s1 + 1), e2 = __ldg(s1 + 2), e3 = __ldg(s1 + 3);
+            const bool n0 = panel_nz(c0 >> 3), n1 = panel_nz((c0 >> 3) + 1);
+            const double2 a0 = n0 ? __ldg(s0) : z2, a1 = n0 ? __ldg(s0 + 1) : z2, a2 = n0 ? __ldg(s0 + 2) : z2,
+                          a3 = n0 ? __ldg(s0 + 3) : z2;
+            const double2 e0 = n1 ? __ldg(s1) : z2, e1 = n1 ? __ldg(s1 + 1) : z2, e2 = n1 ? __ldg(s1 + 2) : z2,
+                          e3 = n1 ? __ldg(s1 + 3) : z2;
             panel(c0, a0, a1, a2, a3);
             panel(c0 + 8, e0, e1, e2, e3);
             if (!first && c0 + 16 < d && acc.result() >= old) pruned = true;
         }
         for (; c0 < d && !pruned; c0 += 8) {
             const double2* src = reinterpret_cast<const double2*>(v8 + ((c0 >> 3) * n + i) * 8);
-            const double2 a0 = __ldg(src), a1 = __ldg(src + 1), a2 = __ldg(src + 2), a3 = __ldg(src + 3);
+            const bool n0 = panel_nz(c0 >> 3);
+            const double2 a0 = n0 ? __ldg(src) : z2, a1 = n0 ? __ldg(src + 1) : z2, a2 = n0 ? __ldg(src + 2) : z2,
+                          a3 = n0 ? __ldg(src + 3) : z2;
             const int rem = (int)(d - c0 < 8 ? d - c0 : 8);
             if (rem == 8) {
                 panel(c0, a0, a1, a2, a3);
@@ -1965,6 +2015,7 @@ struct sc_kmeanspp {
     // the update computes one distance per group
     DevBuf<int32_t> rep, reps;
     int64_t nreps = 0;
+    DevBuf<uint32_t> nzm;  // nonzero-panel bitmap (only when >= 1/4 of the panels are zero)
     DevBuf<uint4> vh8;
     DevBuf<__half> ch;
     DevBuf<double> vnorm, cnorm;
@@ -2024,14 +2075,14 @@ struct sc_kmeanspp {
             if (reps.p) {
                 kpp_update_panel_kernel<<<(unsigned)ceil_div(nreps, KPP_UPD_ROWS), KPP_UPD_ROWS, smem, st>>>(
                     n, d, v8.p, row, -1, first ? 1 : 0, d2.p, taken.p, nullptr, nullptr, ccp,
-                    bound ? ctr.p : nullptr, t, scr, reps.p, nreps);
+                    bound ? ctr.p : nullptr, t, scr, reps.p, nreps, nzm.p);
                 kpp_expand_kernel<<<(unsigned)nb_upd, KPP_UPD_ROWS, 0, st>>>(n, rep.p, pick_index, d2.p, taken.p,
                                                                            bound ? ctr.p : nullptr, pw.p, pc.p);
                 SC_LAUNCHED(1);
             } else {
                 kpp_update_panel_kernel<<<(unsigned)nb_upd, KPP_UPD_ROWS, smem, st>>>(
                     n, d, v8.p, row, pick_index, first ? 1 : 0, d2.p, taken.p, pw.p, pc.p, ccp,
-                    bound ? ctr.p : nullptr, t, scr, nullptr, 0);
+                    bound ? ctr.p : nullptr, t, scr, nullptr, 0, nzm.p);
             }
         } else {
             kpp_update_kernel<<<(unsigned)nb_upd, KPP_UPD_ROWS, 0, st>>>(n, d, v, row, pick_index, first ? 1 : 0, d2.p,
@@ -2229,6 +2280,25 @@ int sc_kmeanspp_create(int64_t n, int64_t d, const double* v, sc_stream_t stream
         }
         to_panels_kernel<<<(unsigned)ceil_div(nch * n * 8, 256), 256, 0, s->st>>>(n, d, v, s->v8.p);
         SC_LAUNCHED(1);
+        {
+            const char* zenv = std::getenv("SPECLUST_KPP_ZERO_PANELS");
+            const int64_t nw = ceil_div(nch, 32);
+            DevBuf<unsigned long long> nzero;
+            if (!(zenv && zenv[0] == '0') && nch >= 4 && s->nzm.alloc((size_t)nw * n) == SC_OK &&
+                nzero.alloc(1) == SC_OK) {
+                cudaMemsetAsync(nzero.p, 0, sizeof(unsigned long long), s->st);
+                panel_nonzero_kernel<<<(unsigned)ceil_div(nw * n, 256), 256, 0, s->st>>>(n, nch, s->v8.p, s->nzm.p,
+                                                                                        nzero.p);
+                SC_LAUNCHED(1);
+                unsigned long long hz = 0;
+                SC_CUDA(d2h_sync(&hz, nzero.p, sizeof(hz), s->st));
+                if (std::getenv("SPECLUST_TIMING_DEBUG"))
+                    fprintf(stderr, "[kmeans++] zero panels: %llu of %lld\n", hz, (long long)(nch * n));
+                if ((double)hz < 0.25 * (double)(nch * n)) s->nzm.free();
+            } else {
+                s->nzm.free();
+            }
+        }
         s->bound = s->cent.alloc((size_t)sc_kmeanspp::ccap * d) == SC_OK &&
                    s->cc.alloc(sc_kmeanspp::ccap) == SC_OK && s->ctr.alloc(n) == SC_OK;
         // the fp16 screen pays for itself once a row is wider than a few

@@ -777,3 +777,26 @@ def test_kmeanspp_fp16_screen_exact(monkeypatch):
         monkeypatch.delenv("SPECLUST_KPP_SCREEN")
         monkeypatch.delenv("SPECLUST_KPP_DEDUP")
         assert np.array_equal(plain, init)
+
+
+def test_kmeanspp_zero_panels_exact(monkeypatch):
+    """k-means++ on embeddings whose rows are mostly zero 8-column panels
+    (C3's embedding: each row has one nonzero among the locked component
+    columns plus a dense tail): the update skips loading zero panels and must
+    still draw the oracle's rows (kmeans.py:107-136), bit-identically to the
+    update with the skip switched off (SPECLUST_KPP_ZERO_PANELS=0)."""
+    rng = np.random.default_rng(43)
+    for n, d, k, ncomp, dense in [(30_000, 200, 60, 150, 24), (20_000, 77, 40, 60, 5), (12_000, 1000, 50, 850, 150)]:
+        comp = rng.integers(0, ncomp, n)
+        v = np.zeros((n, d))
+        v[np.arange(n), comp] = 1.0 + 0.01 * rng.standard_normal(n)
+        v[:, d - dense:] = 0.05 * rng.standard_normal((n, dense))
+        v[rng.random(n) < 0.1, d - dense:] = 0.0  # some rows without a dense tail
+        v /= np.linalg.norm(v, axis=1, keepdims=True)
+        v = np.ascontiguousarray(v)
+        want = orc.kmeanspp_indices(v, k, 5)
+        init = sc.kmeanspp_init(v, k, 5)
+        assert np.array_equal(init, v[want]), (n, d)
+        monkeypatch.setenv("SPECLUST_KPP_ZERO_PANELS", "0")
+        assert np.array_equal(sc.kmeanspp_init(v, k, 5), init), (n, d)
+        monkeypatch.delenv("SPECLUST_KPP_ZERO_PANELS")
