@@ -488,6 +488,31 @@ __global__ void scale_copy_couple_kernel(int64_t n, const double* __restrict__ s
     }
 }
 
+// The common step's couple, decided on the device (one-step lookahead,
+// sc_lanczos::spec_launch): with beta = scal[0], alpha = scal[2], |w0| =
+// scal[3] and the host's running scale, the host's tests -- no window
+// cancellation (beta >= wcancel |w0|) and no breakdown (beta > rtol *
+// max(1, max(scale, |alpha|, beta))) -- are evaluated on the same doubles; if
+// both pass, q_{j+1} = w / beta and the couplings are written exactly as
+// scale_copy_couple_kernel does, else nothing is written.  scal[6] = 0 / 1
+// tells the host which.
+__global__ void couple_guarded_kernel(int64_t n, const double* __restrict__ src, double* __restrict__ scal,
+                                      double* __restrict__ dst, int64_t m, int64_t j, double* __restrict__ T,
+                                      double scale, double wcancel, double rtol) {
+    const double beta = scal[0], alpha = scal[2], w0 = scal[3];
+    const double sc = fmax(scale, fmax(fabs(alpha), beta));
+    const bool ok = !(beta < wcancel * w0) && beta > rtol * fmax(1.0, sc);
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (ok && i < n) dst[i] = src[i] / beta;
+    if (i == 0) {
+        if (ok) {
+            T[j * m + j + 1] = beta;
+            T[(j + 1) * m + j] = beta;
+        }
+        scal[6] = ok ? 0.0 : 1.0;
+    }
+}
+
 // T[j,j] = alpha (= h[j] after the first projection), scal[2] = alpha
 __global__ void commit_alpha_kernel(int64_t m, int64_t j, const double* __restrict__ h,
                                     double* __restrict__ T, double* __restrict__ scal) {
@@ -1114,6 +1139,21 @@ struct sc_lanczos {
     double scale = 0.0;
     std::vector<double> history, pending, theta_k, est_k;
     bool has_pending = false;
+    // one-step lookahead (internal drivers only; SPECLUST_LOOKAHEAD=0 off): a
+    // common windowed step launches its couple guarded on the device
+    // (couple_guarded_kernel), swaps the work vector and returns, so the
+    // driver's next SpMV runs while the host reads this step's scalars; the
+    // next advance() settles them first and, if the device declined (window
+    // cancellation or breakdown), swaps back and takes this step's host path
+    bool spec_on = false, spec_pending = false;
+    DevBuf<double> w2;
+    double* spec_host = nullptr;  // pinned: scal[0..6] of the pending step
+    cudaEvent_t spec_ev = nullptr;
+    int64_t spec_hits = 0, spec_aborts = 0;
+    ~sc_lanczos() {
+        if (spec_host) cudaFreeHost(spec_host);
+        if (spec_ev) cudaEventDestroy(spec_ev);
+    }
 
     DevBuf<double> B, T, w, part, h, sqp, sq0, scal, Y, A, Z, wraw, wsort, S, lastrow, vectors;
     double* vec_out = nullptr;  // converged Ritz vectors (row-major n x k): `vectors` or a caller buffer
@@ -1239,9 +1279,73 @@ struct sc_lanczos {
 
     const double* in_slot() const { return B.p + j * ld; }
 
+    int enable_lookahead() {
+        const char* e = std::getenv("SPECLUST_LOOKAHEAD");
+        if (spec_on || (e && e[0] == '0')) return SC_OK;
+        int rc;
+        if ((rc = w2.alloc(ld))) return rc;
+        SC_CUDA(cudaMemsetAsync(w2.p, 0, sizeof(double) * ld, st));
+        if (cudaMallocHost(&spec_host, 8 * sizeof(double)) != cudaSuccess) {
+            spec_host = nullptr;
+            cudaGetLastError();
+            return SC_OK;  // no lookahead
+        }
+        if (cudaEventCreateWithFlags(&spec_ev, cudaEventDisableTiming) != cudaSuccess) {
+            spec_ev = nullptr;
+            cudaGetLastError();
+            return SC_OK;
+        }
+        spec_on = true;
+        return SC_OK;
+    }
+    // the step may be decided on the device: not the sweep's last, and no
+    // flush falls due after it (both need the host between the steps)
+    bool spec_can() const {
+        if (!spec_on || j + 1 >= m) return false;
+        const int64_t jn = j + 1;
+        if (windowed && tiered && restarts > 0) return !(jn - j0 >= win || jn + 1 - js >= win_s);
+        return !(windowed && jn - j0 >= win);
+    }
+    int spec_launch() {
+        double* next = B.p + (j + 1) * ld;
+        couple_guarded_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(n, w.p, scal.p, next, m, j, T.p, scale,
+                                                                          kWindowCancel, kBreakdownRtol);
+        SC_LAUNCHED(1);
+        SC_CUDA(cudaMemcpyAsync(spec_host, scal.p, 7 * sizeof(double), cudaMemcpyDeviceToHost, st));
+        SC_CUDA(cudaEventRecord(spec_ev, st));
+        std::swap(w.p, w2.p);
+        ++j;
+        spec_pending = true;
+        return SC_OK;
+    }
+    int spec_resolve(double* ab, bool* ok) {
+        spec_pending = false;
+        SC_CUDA(cudaEventSynchronize(spec_ev));
+        for (int i = 0; i < 4; ++i) ab[i] = spec_host[i];
+        *ok = spec_host[6] == 0.0;
+        if (*ok) {
+            ++spec_hits;
+            scale = std::max(scale, std::max(std::fabs(ab[2]), ab[0]));
+        } else {
+            ++spec_aborts;
+            std::swap(w.p, w2.p);
+            --j;
+        }
+        return SC_OK;
+    }
+
     // one Lanczos step on w = A q_j (eigen.py:152-179)
     int advance(bool check_finite) {
         if (state != 0) return fail(SC_ERR_STATE, "advance called in a finished session");
+        if (spec_pending) {
+            double ab[4];
+            bool ok = false;
+            int rc = spec_resolve(ab, &ok);
+            if (rc) return rc;
+            // declined: the pending step's host path; the driver's SpMV of
+            // the unwritten q_{j+1} (in the other work vector) is discarded
+            if (!ok) return tail(ab);
+        }
         ++matvecs;
         int rc;
         if (check_finite) {
@@ -1274,6 +1378,7 @@ struct sc_lanczos {
         if (windowed && !arrow_step && cnt <= WCG_MAX) {
             ProfScope prof("reorth", st, 3.0 * (double)n * cnt * 8.0);
             if ((rc = window_cgs2(lo, cnt))) return rc;
+            if (spec_can()) return spec_launch();
             SC_CUDA(d2h_sync(ab, scal.p, sizeof(double) * 4, st));
         } else {
             ProfScope prof("reorth", st, 2.0 * (double)n * cnt * 8.0);
@@ -1288,6 +1393,15 @@ struct sc_lanczos {
             }
             SC_CUDA(d2h_sync(ab, scal.p, sizeof(double) * 4, st));
         }
+        return tail(ab);
+    }
+
+    // the rest of a step once its scalars are on the host: cancellation
+    // passes, end of sweep, couple or breakdown, flushes
+    int tail(const double* ab_in) {
+        int rc;
+        double ab[4] = {ab_in[0], ab_in[1], ab_in[2], ab_in[3]};
+        const bool two = windowed && tiered && restarts > 0;
         // second pass over the WHOLE basis: always in full mode (the
         // reference's unconditional CGS2, eigen.py:131-135); in windowed mode
         // when the window pass cancelled w to rounding level (a breakdown or
@@ -1490,10 +1604,10 @@ struct sc_lanczos {
         if (tdbg) {
             cudaStreamSynchronize(st);
             const auto t1 = std::chrono::steady_clock::now();
-            fprintf(stderr, "[lanczos] sweep %lld: %.3f ms, matvecs %lld, flushes %lld (from-0 %lld: %.1f ms, sweep %lld: %.1f ms)\n",
+            fprintf(stderr, "[lanczos] sweep %lld: %.3f ms, matvecs %lld, flushes %lld (from-0 %lld: %.1f ms, sweep %lld: %.1f ms), lookahead %lld / declined %lld\n",
                     (long long)restarts, std::chrono::duration<double, std::milli>(t1 - sweep_t0).count(),
                     (long long)matvecs, (long long)flushes, (long long)flush_n[0], flush_ms[0],
-                    (long long)flush_n[1], flush_ms[1]);
+                    (long long)flush_n[1], flush_ms[1], (long long)spec_hits, (long long)spec_aborts);
             flush_ms[0] = flush_ms[1] = 0.0;
             flush_n[0] = flush_n[1] = 0;
             sweep_t0 = t1;
@@ -1740,6 +1854,7 @@ int sc_eigensolve_csr(int64_t n, const int64_t* row_ptr, const int32_t* col, con
     sc_lanczos s;
     int rc = s.init(n, k, m, tol, max_restarts, seed, st);
     if (rc) return rc;
+    if ((rc = s.enable_lookahead())) return rc;
     s.vec_out = vectors;  // the converged Ritz vectors go straight to the caller's buffer
     int64_t nnz = 0;
     SC_CUDA(d2h_sync(&nnz, row_ptr + n, sizeof(int64_t), st));
@@ -1785,6 +1900,7 @@ int sc_eigensolve_csr_basis(int64_t n, const int64_t* row_ptr, const int32_t* co
     sc_lanczos s;
     int rc = s.init(n, k, m, tol, max_restarts, seed, st, basis);
     if (rc) return rc;
+    if ((rc = s.enable_lookahead())) return rc;
     int64_t nnz = 0;
     SC_CUDA(d2h_sync(&nnz, row_ptr + n, sizeof(int64_t), st));
     while (s.state == 0) {
@@ -1899,6 +2015,7 @@ int sc_eigensolve_csr_deflate(int64_t n, const int64_t* row_ptr, const int32_t* 
     const int64_t kr = k - c, mr = m - c;
     sc_lanczos s;
     if ((rc = s.init(n, kr, mr, tol, max_restarts, seed, st))) return rc;
+    if ((rc = s.enable_lookahead())) return rc;
     if ((rc = s.set_locked(&lk))) return rc;
     DevBuf<double> rv;
     if ((rc = rv.alloc((size_t)n * kr))) return rc;
