@@ -29,12 +29,12 @@ def launches():
     total = sum(v[1] for v in per.values())
     # the capture covers several pipeline runs of identical work (warm-up,
     # timed, profiled): one knn_cand_tc2 launch per run
-    runs = max(1, sum(c for nm, (c, _) in per.items() if nm.startswith("knn_cand_tc2")))
+    runs = max(1, sum(c for nm, (c, _) in per.items() if "knn_cand_tc2" in nm))
     out = PROF / f"{tag}_launches_c2_by_kernel.csv"
     with out.open("w") as f:
         f.write("kernel,launches_per_step,ms_per_step,share\n")
         for name, (cnt, ms) in sorted(per.items(), key=lambda kv: -kv[1][1]):
-            f.write(f"{name},{cnt / runs:.0f},{ms / runs:.3f},{ms / total:.4f}\n")
+            f.write(f"\"{name}\",{cnt / runs:.0f},{ms / runs:.3f},{ms / total:.4f}\n")
     print(f"wrote {out}: {len(rows)} launches over {runs} runs, {total / runs:.1f} ms of kernels per run")
 
 
