@@ -1532,36 +1532,72 @@ __global__ void __launch_bounds__(256) as_finalize_rows_kernel(
     const int64_t* __restrict__ old_labels, int64_t* __restrict__ labels, double* __restrict__ cost,
     int32_t* __restrict__ flagged, unsigned long long* __restrict__ nflag, unsigned long long* __restrict__ changes,
     bool vec2) {
+    // vec2: the warp stages its rows' 8-element pieces of v and of their
+    // centroids in shared memory (lane quarter q of 8 rows per load: 8 lines
+    // per instruction instead of 32 -- one row per thread made every load an
+    // L1 wavefront per lane), and each thread sums its own row from there in
+    // the same NpDot order; row stride 10 doubles: conflict-free double2 reads
+    constexpr int FS = 10;
+    __shared__ __align__(16) double stv[8][32 * FS];
+    __shared__ __align__(16) double stc[8][32 * FS];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int chg = 0;
+    bool cert = false;
+    int32_t b = -1;
     if (i < n) {
         const double delta = as_delta(vn[i], __longlong_as_double((long long)*cnmax_bits), dp, s);
         const float2 bk = best_keys[i];
-        const int32_t b = best_idx[i];
-        if (b >= 0 && (double)bk.y - (double)bk.x > 2.0 * delta) {
-            const double* vi = v + i * d;
-            const double* cb = c + (int64_t)b * d;
-            NpDot acc;
-            int64_t l = 0;
-            if (vec2) {  // rows 16-byte aligned (d even, aligned bases): 16-byte loads
-                for (; l + 8 <= d; l += 8) {
-                    const double2* pv = reinterpret_cast<const double2*>(vi + l);
-                    const double2* pc = reinterpret_cast<const double2*>(cb + l);
-                    const double2 x0 = __ldg(pv), x1 = __ldg(pv + 1), x2 = __ldg(pv + 2), x3 = __ldg(pv + 3);
-                    const double2 y0 = __ldg(pc), y1 = __ldg(pc + 1), y2 = __ldg(pc + 2), y3 = __ldg(pc + 3);
-                    acc.block(__dmul_rn(x0.x, y0.x), __dmul_rn(x0.y, y0.y), __dmul_rn(x1.x, y1.x),
-                              __dmul_rn(x1.y, y1.y), __dmul_rn(x2.x, y2.x), __dmul_rn(x2.y, y2.y),
-                              __dmul_rn(x3.x, y3.x), __dmul_rn(x3.y, y3.y));
+        b = best_idx[i];
+        cert = b >= 0 && (double)bk.y - (double)bk.x > 2.0 * delta;
+        if (!cert) flagged[atomicAdd(nflag, 1ull)] = (int32_t)i;
+    }
+    NpDot acc;
+    int64_t l = 0;
+    if (vec2 && __any_sync(0xffffffffu, cert)) {
+        const int64_t d8 = d / 8 * 8;
+        const int64_t row0 = i - lane;
+        bool rc[4];
+        int32_t rb[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            rc[q] = __shfl_sync(0xffffffffu, cert, q * 8 + (lane >> 2));
+            rb[q] = __shfl_sync(0xffffffffu, b, q * 8 + (lane >> 2));
+        }
+        double* sv = stv[warp];
+        double* sc = stc[warp];
+        for (; l < d8; l += 8) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int rr = q * 8 + (lane >> 2);
+                if (rc[q]) {
+                    const double2 xv = __ldg(reinterpret_cast<const double2*>(v + (row0 + rr) * d + l) + (lane & 3));
+                    const double2 xc = __ldg(reinterpret_cast<const double2*>(c + (int64_t)rb[q] * d + l) + (lane & 3));
+                    reinterpret_cast<double2*>(sv + rr * FS)[lane & 3] = xv;
+                    reinterpret_cast<double2*>(sc + rr * FS)[lane & 3] = xc;
                 }
             }
-            np_dot_span(acc, l, d, [&](int64_t j) { return __dmul_rn(__ldg(vi + j), __ldg(cb + j)); });
-            labels[i] = b;
-            const double r = __dsub_rn(__dadd_rn(vn[i], cn[b]), __dmul_rn(2.0, acc.result()));
-            cost[i] = r > 0.0 ? r : 0.0;
-            if (old_labels) chg = old_labels[i] != b;
-        } else {
-            flagged[atomicAdd(nflag, 1ull)] = (int32_t)i;
+            __syncwarp();
+            if (cert) {
+                const double2* pv = reinterpret_cast<const double2*>(sv + lane * FS);
+                const double2* pc = reinterpret_cast<const double2*>(sc + lane * FS);
+                const double2 x0 = pv[0], x1 = pv[1], x2 = pv[2], x3 = pv[3];
+                const double2 y0 = pc[0], y1 = pc[1], y2 = pc[2], y3 = pc[3];
+                acc.block(__dmul_rn(x0.x, y0.x), __dmul_rn(x0.y, y0.y), __dmul_rn(x1.x, y1.x),
+                          __dmul_rn(x1.y, y1.y), __dmul_rn(x2.x, y2.x), __dmul_rn(x2.y, y2.y),
+                          __dmul_rn(x3.x, y3.x), __dmul_rn(x3.y, y3.y));
+            }
+            __syncwarp();
         }
+    }
+    if (cert) {
+        const double* vi = v + i * d;
+        const double* cb = c + (int64_t)b * d;
+        np_dot_span(acc, l, d, [&](int64_t j) { return __dmul_rn(__ldg(vi + j), __ldg(cb + j)); });
+        labels[i] = b;
+        const double r = __dsub_rn(__dadd_rn(vn[i], cn[b]), __dmul_rn(2.0, acc.result()));
+        cost[i] = r > 0.0 ? r : 0.0;
+        if (old_labels) chg = old_labels[i] != b;
     }
     const unsigned bal = __ballot_sync(0xffffffffu, chg);
     if ((threadIdx.x & 31) == 0 && bal) atomicAdd(changes, (unsigned long long)__popc(bal));
