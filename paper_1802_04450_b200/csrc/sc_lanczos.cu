@@ -1578,13 +1578,15 @@ struct sc_lanczos {
             }
         }
         // the loss grows geometrically with the window length: aim the next
-        // window at 1e-9 from the growth rate this one showed, growing by at
-        // most two vectors per flush
-        // (aim at 1e-11: the growth rate is not steady -- it rises as Ritz
-        // values converge inside a sweep -- so keep two decades of headroom
-        // below the 1e-9 the window must not exceed)
+        // window from the growth rate this one showed, growing by at most
+        // one vector per flush.  Aim at 1e-10, a decade and a half below
+        // semi-orthogonality (sqrt(eps) ~ 1.5e-8; windows above 1e-8 are
+        // re-orthonormalised): the growth rate is not steady -- it rises as
+        // Ritz values converge inside a sweep.  (Measured: aiming at 1e-11
+        // C3 eigen 7.92 s / 719 flushes / max loss 6e-10; at 1e-10 7.49 s /
+        // 571 / 5e-9; at 1e-9 7.56 s / 552 / 6e-6, tools/gpu_r2df.sh.)
         double target = (double)wmax;
-        if (loss > 1e-16) target = (double)c * 5.0 / std::log10(loss / 1e-16);
+        if (loss > 1e-16) target = (double)c * 6.0 / std::log10(loss / 1e-16);
         if (loss > 1e-9) target = std::min(target, (double)c / 2);
         wv = std::max<int64_t>(2, std::min<int64_t>({wmax, (int64_t)target, (int64_t)c + 1}));
         return SC_OK;
